@@ -1,0 +1,393 @@
+"""HyRes oracle: plain, slow, fp64 CPU implementation of the north_star hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import or call
+anything under ``oracle/``.  The product path (``paper_2204_06979_b200``) never
+imports it, and the two share no code: this file imports numpy/mpmath only.
+
+What it computes (BASELINE.json north_star stages (1)-(6); SURVEY.md §8(c)
+steps C1-C7; every reading of an ambiguous passage is listed in DESIGN.md §2):
+
+C1  G = Y Y^T (uncentered, B x B) over all N = R*C pixels; M = (G + delta I)^-1
+    with delta = 1e-6; sigma_b^2 = 1 / (N M_bb) -- the residual variance of the
+    least-squares regression of band b on all other bands (HySime's noise
+    estimator; "regress band i on all other
+    bands ... ridge damping delta=1e-6").
+C2  G_w = diag(sigma)^-1 G diag(sigma)^-1 / N; (lambda, V) = eigh(G_w) sorted
+    descending; each column of V sign-fixed so its largest-|.| entry is positive,
+    lowest index on ties (SPEC.md:181 D6, applied to V).
+C3  Daubechies filters by spectral factorisation (SPEC.md:179 D4: Haar, db4,
+    db8; default db8 = 16 taps); levels L = max(1, min(5, floor(log2(min(R,C) /
+    (taps-1))))).
+C4  Eigen-image e_k = (Y^T diag(sigma)^-1 v_k) as an R x C image; L-level
+    separable periodised orthonormal 2-D DWT, each level first padding an odd
+    extent by duplicating the last row/column (SPEC.md:182 D7); along an axis of
+    even length n: a_j = sum_m h_m x_{(2j+m) mod n}, d_j = sum_m g_m x_{(2j+m) mod n}
+    (SPEC.md:118-126).
+C5  Per subband (noise sigma = 1 in whitened units): SURE threshold
+    t* = a_(k*), k* = smallest argmin_k S_k, S_k = n - 2k + sum_{i<=k} a_(i)^2
+    + (n-k) a_(k)^2 over the sorted |x| with a_(0) = 0 (north_star stage (5):
+    "sort, prefix sums, argmin"); then soft threshold sign(x) max(|x|-t*, 0)
+    (SPEC.md:136-137).
+C6  Rank: E_post,k = sum of soft(x)^2 over all subbands of component k, N_c its
+    coefficient count; walking k = 1, 2, ...: the first k with E_post,k <= N_c
+    stops the walk and r* = max(1, k-1); r* = B if none fails (SPEC.md:380 step
+    (5) "retain components whose post-threshold energy exceeds a noise-floor
+    criterion").
+C7  e^_k = IDWT(soft coefficients) (the adjoint synthesis, cropping each level's
+    padding); X^ = sum_{k<=r*} (sigma (.) v_k) e^_k^T, returned as float32 BSQ
+    (SPEC.md:380 step (6) "inverse transforms and de-whitening").
+
+Parity pins for every function are in tests/test_oracle_*.py (SURVEY.md §8(c)
+P1-P8).  P9 (the paper's Houston anchor) is "parity unpinned":
+the data is not available.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+DEFAULT_RIDGE = 1e-6          # SPEC.md:364 "ridge damping delta=1e-6"
+DEFAULT_TAPS = 16             # SPEC.md:179 D4 "default Daubechies-8"
+SUPPORTED_TAPS = (2, 8, 16)   # Haar, db4, db8 (SPEC.md:179 D4)
+MAX_AUTO_LEVELS = 5
+
+
+# ----------------------------------------------------------------------------
+# C3: filters
+# ----------------------------------------------------------------------------
+def daubechies_lowpass(n_moments: int, dps: int = 50) -> np.ndarray:
+    """Daubechies minimum-phase scaling filter with `n_moments` vanishing moments
+    (2*n_moments taps), by spectral factorisation (Daubechies, Ten Lectures §6.1):
+    |H(w)|^2 = 2 cos^{2N}(w/2) P(sin^2(w/2)), P(y) = sum_{k<N} C(N-1+k, k) y^k.
+    Each root y_i of P gives z + 1/z = 2 - 4 y_i; the root z_i with |z_i| < 1 is
+    kept (minimum phase), H(z) ~ (1 + z)^N prod_i (z - z_i).  Normalised so
+    sum h = sqrt(2); ordered so h_0 is the coefficient of the highest power
+    (energy front-loaded; h_0 = 0.0544158... for N = 8)."""
+    import mpmath as mp
+    N = int(n_moments)
+    if N < 1:
+        raise ValueError("n_moments >= 1")
+    if N == 1:
+        return np.array([1.0, 1.0]) / math.sqrt(2.0)
+    with mp.workdps(dps):
+        # polyroots wants highest-degree coefficient first
+        coeffs = [mp.binomial(N - 1 + k, k) for k in range(N - 1, -1, -1)]
+        yroots = mp.polyroots(coeffs, maxsteps=200, extraprec=4 * dps)
+        zs = []
+        for y in yroots:
+            c = 1 - 2 * y                      # z^2 - 2c z + 1 = 0
+            s = mp.sqrt(c * c - 1)
+            z1, z2 = c + s, c - s
+            zs.append(z1 if abs(z1) < 1 else z2)
+        poly = [mp.mpc(1)]                     # coefficients, highest power first
+        for _ in range(N):
+            poly = _polymul(poly, [mp.mpc(1), mp.mpc(1)])
+        for z in zs:
+            poly = _polymul(poly, [mp.mpc(1), -z])
+        re = [mp.re(p) for p in poly]
+        tot = mp.fsum(re)
+        h = [p * mp.sqrt(2) / tot for p in re]
+        return np.array([float(v) for v in h])
+
+
+def _polymul(a, b):
+    out = [0] * (len(a) + len(b) - 1)
+    for i, x in enumerate(a):
+        for j, y in enumerate(b):
+            out[i + j] += x * y
+    return out
+
+
+def filters(taps: int = DEFAULT_TAPS):
+    """(h, g): analysis low/high-pass, g_k = (-1)^k h_{T-1-k} (quadrature mirror)."""
+    if taps not in SUPPORTED_TAPS:
+        raise ValueError(f"taps must be one of {SUPPORTED_TAPS}")
+    h = daubechies_lowpass(taps // 2)
+    T = len(h)
+    g = np.array([(-1.0) ** k * h[T - 1 - k] for k in range(T)])
+    return h, g
+
+
+def auto_levels(rows: int, cols: int, taps: int = DEFAULT_TAPS) -> int:
+    """L = max(1, min(5, floor(log2(min(R, C) / (taps - 1))))) -- DESIGN.md reading R6."""
+    m = min(rows, cols)
+    v = m / max(taps - 1, 1)
+    lv = int(math.floor(math.log2(v))) if v >= 1 else 0
+    return max(1, min(MAX_AUTO_LEVELS, lv))
+
+
+def level_shapes(rows: int, cols: int, levels: int):
+    """Subband shape per level 1..L: (ceil(h/2), ceil(w/2)) of the previous level's LL."""
+    shapes = []
+    h, w = rows, cols
+    for _ in range(levels):
+        h, w = (h + 1) // 2, (w + 1) // 2
+        shapes.append((h, w))
+    return shapes
+
+
+def check_levels(rows: int, cols: int, levels: int):
+    if levels < 1 or min(rows, cols) < 2 ** levels:
+        raise ValueError("levels impossible for this image size (SPEC.md:122)")
+
+
+def coeff_count(rows: int, cols: int, levels: int) -> int:
+    """N_c: coefficients of one eigen-image = 3 sum_l h_l w_l + h_L w_L."""
+    sh = level_shapes(rows, cols, levels)
+    return 3 * sum(h * w for h, w in sh) + sh[-1][0] * sh[-1][1]
+
+
+# ----------------------------------------------------------------------------
+# C4: DWT (periodised, per-level symmetric pad-to-even)
+# ----------------------------------------------------------------------------
+def _pad_even(x: np.ndarray, axis: int) -> np.ndarray:
+    if x.shape[axis] % 2 == 0:
+        return x
+    last = np.take(x, [x.shape[axis] - 1], axis=axis)
+    return np.concatenate([x, last], axis=axis)
+
+
+def analysis_1d(x: np.ndarray, h: np.ndarray, g: np.ndarray, axis: int):
+    """a_j = sum_m h_m x_{(2j+m) mod n}, d_j = sum_m g_m x_{(2j+m) mod n}; n even."""
+    x = np.moveaxis(np.asarray(x, dtype=np.float64), axis, -1)
+    n = x.shape[-1]
+    assert n % 2 == 0
+    j2 = 2 * np.arange(n // 2)
+    a = np.zeros(x.shape[:-1] + (n // 2,))
+    d = np.zeros_like(a)
+    for m in range(len(h)):
+        xm = x[..., (j2 + m) % n]
+        a += h[m] * xm
+        d += g[m] * xm
+    return np.moveaxis(a, -1, axis), np.moveaxis(d, -1, axis)
+
+
+def synthesis_1d(a: np.ndarray, d: np.ndarray, h: np.ndarray, g: np.ndarray, axis: int):
+    """Adjoint of analysis_1d: x_i = sum_{j,m: (2j+m) mod n = i} h_m a_j + g_m d_j."""
+    a = np.moveaxis(np.asarray(a, dtype=np.float64), axis, -1)
+    d = np.moveaxis(np.asarray(d, dtype=np.float64), axis, -1)
+    half = a.shape[-1]
+    n = 2 * half
+    x = np.zeros(a.shape[:-1] + (n,))
+    j2 = 2 * np.arange(half)
+    for m in range(len(h)):
+        idx = (j2 + m) % n
+        contrib = h[m] * a + g[m] * d
+        if len(np.unique(idx)) == len(idx):
+            x[..., idx] += contrib
+        else:  # filter longer than the signal: several taps wrap onto one sample
+            for jj in range(half):
+                x[..., idx[jj]] += contrib[..., jj]
+    return np.moveaxis(x, -1, axis)
+
+
+SUBBANDS = ("LH", "HL", "HH")   # (axis-0 filter, axis-1 filter): L=lowpass, H=highpass
+
+
+def dwt2(img: np.ndarray, levels: int, taps: int = DEFAULT_TAPS):
+    """Returns {'details': [(LH, HL, HH) for level 1..L], 'LL': LL_L, 'shapes': [...]}.
+    Level l: pad the current LL to even, filter along axis 1 (columns, contiguous),
+    then along axis 0."""
+    h, g = filters(taps)
+    x = np.asarray(img, dtype=np.float64)
+    check_levels(x.shape[0], x.shape[1], levels)
+    details, in_shapes = [], []
+    for _ in range(levels):
+        in_shapes.append(x.shape)
+        x = _pad_even(_pad_even(x, 0), 1)
+        lo1, hi1 = analysis_1d(x, h, g, axis=1)
+        ll, hl = analysis_1d(lo1, h, g, axis=0)      # axis0 L / H of the axis1-lowpass
+        lh, hh = analysis_1d(hi1, h, g, axis=0)      # axis0 L / H of the axis1-highpass
+        details.append((lh, hl, hh))
+        x = ll
+    return {"details": details, "LL": x, "in_shapes": in_shapes}
+
+
+def idwt2(coeffs, taps: int = DEFAULT_TAPS) -> np.ndarray:
+    """Inverse of dwt2: per level from coarsest, synthesise along axis 0 then axis 1,
+    then crop that level's padding."""
+    h, g = filters(taps)
+    x = coeffs["LL"]
+    for (lh, hl, hh), shp in zip(reversed(coeffs["details"]), reversed(coeffs["in_shapes"])):
+        lo1 = synthesis_1d(x, hl, h, g, axis=0)
+        hi1 = synthesis_1d(lh, hh, h, g, axis=0)
+        x = synthesis_1d(lo1, hi1, h, g, axis=1)
+        x = x[: shp[0], : shp[1]]
+    return x
+
+
+def flatten_coeffs(coeffs) -> List[np.ndarray]:
+    """Subbands in the storage order used at the C-ABI: level 1..L x (LH, HL, HH), then LL_L."""
+    out = []
+    for lh, hl, hh in coeffs["details"]:
+        out += [lh, hl, hh]
+    out.append(coeffs["LL"])
+    return out
+
+
+def unflatten_coeffs(subbands: List[np.ndarray], template):
+    lv = len(template["details"])
+    det = [tuple(subbands[3 * i: 3 * i + 3]) for i in range(lv)]
+    return {"details": det, "LL": subbands[-1], "in_shapes": template["in_shapes"]}
+
+
+# ----------------------------------------------------------------------------
+# C5: SURE
+# ----------------------------------------------------------------------------
+@dataclass
+class SureResult:
+    k: int              # index into {0} U sorted |x| (k = 0 means t = 0)
+    t: float            # threshold a_(k)
+    risk: float         # S_k
+    margin: float       # second-best S minus best S (tie diagnostics)
+
+
+def sure_threshold(x: np.ndarray) -> SureResult:
+    """k* = smallest argmin over k = 0..n of S_k = n - 2k + sum_{i<=k} a_(i)^2 + (n-k) a_(k)^2,
+    a = sorted |x|, a_(0) = 0 (noise sigma = 1)."""
+    a = np.sort(np.abs(np.asarray(x, dtype=np.float64).ravel()))
+    n = a.size
+    a0 = np.concatenate([[0.0], a])
+    k = np.arange(n + 1, dtype=np.float64)
+    csum = np.concatenate([[0.0], np.cumsum(a * a)])
+    s = n - 2.0 * k + csum + (n - k) * a0 * a0
+    kstar = int(np.argmin(s))
+    best = s[kstar]
+    rest = np.delete(s, kstar)
+    margin = float(np.min(rest) - best) if rest.size else float("inf")
+    return SureResult(kstar, float(a0[kstar]), float(best), margin)
+
+
+def sure_risk_direct(x: np.ndarray, t: float) -> float:
+    """S(t) = n - 2 #{|x_i| <= t} + sum_i min(x_i^2, t^2) (Stein's unbiased risk, sigma = 1)."""
+    ax = np.abs(np.asarray(x, dtype=np.float64).ravel())
+    return float(ax.size - 2.0 * np.count_nonzero(ax <= t) + np.sum(np.minimum(ax * ax, t * t)))
+
+
+def soft_threshold(x: np.ndarray, t: float) -> np.ndarray:
+    """sign(x) max(|x| - t, 0)."""
+    if t < 0:
+        raise ValueError("t >= 0")
+    x = np.asarray(x, dtype=np.float64)
+    return np.sign(x) * np.maximum(np.abs(x) - t, 0.0)
+
+
+# ----------------------------------------------------------------------------
+# C1: noise estimate
+# ----------------------------------------------------------------------------
+def _as_bands_by_pixels(cube: np.ndarray) -> np.ndarray:
+    cube = np.asarray(cube)
+    if cube.ndim != 3:
+        raise ValueError("cube must be (bands, rows, cols) BSQ")
+    if not np.all(np.isfinite(cube)):
+        raise FloatingPointError("non-finite input (SPEC.md:26)")
+    return cube.reshape(cube.shape[0], -1).astype(np.float64)
+
+
+def gram(cube: np.ndarray) -> np.ndarray:
+    """G = Y Y^T over all pixels (uncentered), fp64."""
+    y = _as_bands_by_pixels(cube)
+    return y @ y.T
+
+
+def estimate_noise(cube: np.ndarray, ridge: float = DEFAULT_RIDGE, want_residual: bool = False):
+    """sigma (B,), G (B,B) [, residual (B,R,C)] with sigma_b^2 = 1/(N M_bb), M = (G + ridge I)^-1.
+    residual_b = (M Y)_b / M_bb -- the regression residual of band b on the others."""
+    b, r, c = np.asarray(cube).shape
+    n = r * c
+    if b < 3 or n <= b:
+        raise ValueError("bands >= 3 and pixels > bands required (SPEC.md:363, :365)")
+    y = _as_bands_by_pixels(cube)
+    g = y @ y.T
+    m = np.linalg.inv(g + ridge * np.eye(b))
+    sigma = np.sqrt(1.0 / (n * np.diag(m)))
+    if want_residual:
+        res = (m @ y) / np.diag(m)[:, None]
+        return sigma, g, res.reshape(b, r, c)
+    return sigma, g
+
+
+# ----------------------------------------------------------------------------
+# C2: whitening + eigendecomposition
+# ----------------------------------------------------------------------------
+def sign_fix(v: np.ndarray) -> np.ndarray:
+    """Flip each column so its largest-|.| entry (lowest index on ties) is positive."""
+    v = v.copy()
+    for j in range(v.shape[1]):
+        i = int(np.argmax(np.abs(v[:, j])))
+        if v[i, j] < 0:
+            v[:, j] = -v[:, j]
+    return v
+
+
+def whiten_eig(g: np.ndarray, sigma: np.ndarray, n: int):
+    gw = g / np.outer(sigma, sigma) / n
+    lam, v = np.linalg.eigh(gw)
+    order = np.argsort(-lam, kind="stable")
+    return lam[order], sign_fix(v[:, order]), gw
+
+
+# ----------------------------------------------------------------------------
+# full path
+# ----------------------------------------------------------------------------
+@dataclass
+class HyresResult:
+    out: np.ndarray                 # float32 BSQ
+    rank: int
+    levels: int
+    sigma: np.ndarray
+    gram: np.ndarray
+    lam: np.ndarray
+    V: np.ndarray
+    n_coeffs: int
+    e_post: List[float] = field(default_factory=list)
+    sure: List[List[SureResult]] = field(default_factory=list)   # per visited component, per subband
+    eigen_images: List[np.ndarray] = field(default_factory=list) # e_k before the DWT (visited ones)
+    denoised_images: List[np.ndarray] = field(default_factory=list)  # e^_k for k <= r*
+
+
+def hyres(cube: np.ndarray, taps: int = DEFAULT_TAPS, levels: int = 0, ridge: float = DEFAULT_RIDGE,
+          keep_ll: bool = False, keep_images: bool = False) -> HyresResult:
+    cube = np.asarray(cube)
+    b, r, c = cube.shape
+    n = r * c
+    lv = levels if levels > 0 else auto_levels(r, c, taps)
+    check_levels(r, c, lv)
+    sigma, g = estimate_noise(cube, ridge)                                    # C1
+    lam, v, _ = whiten_eig(g, sigma, n)                                       # C2
+    y = _as_bands_by_pixels(cube)
+    nc = coeff_count(r, c, lv)
+    e_post, sure_all, eimgs, kept = [], [], [], []
+    for k in range(b):                                                        # C6 walk
+        w = v[:, k] / sigma
+        ek = (w @ y).reshape(r, c)                                            # C4 projection
+        co = dwt2(ek, lv, taps)
+        subs = flatten_coeffs(co)
+        res_k, soft = [], []
+        for si, sb in enumerate(subs):                                        # C5
+            if keep_ll and si == len(subs) - 1:
+                sr = SureResult(0, 0.0, float("nan"), float("inf"))
+            else:
+                sr = sure_threshold(sb)
+            res_k.append(sr)
+            soft.append(soft_threshold(sb, sr.t))
+        ep = float(sum(np.sum(s * s) for s in soft))
+        e_post.append(ep)
+        sure_all.append(res_k)
+        if keep_images:
+            eimgs.append(ek)
+        if ep <= nc and k > 0:
+            break
+        kept.append(idwt2(unflatten_coeffs(soft, co), taps))                  # C7 IDWT
+        if ep <= nc:       # k == 0 failed: r* = max(1, 0) keeps component 1
+            break
+    rank = len(kept)
+    u = v[:, :rank] * sigma[:, None]                                          # D^{1/2} V
+    ehat = np.stack([e.ravel() for e in kept])                                # (r*, N)
+    out = (u @ ehat).reshape(b, r, c).astype(np.float32)                      # C7
+    return HyresResult(out, rank, lv, sigma, g, lam, v, nc, e_post, sure_all,
+                       eimgs, kept if keep_images else [])
