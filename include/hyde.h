@@ -1,0 +1,171 @@
+/*
+ * hyde.h -- C-ABI of the B200-native HyRes hot path (libhyde.so).
+ *
+ * HyRes is HyDe's parameter-free, low-rank, wavelet-based Gaussian denoiser
+ * (Sec. 2.1 "High Level Conventional Methods"); its six
+ * stages are BASELINE.json north_star (1)-(6) and SURVEY.md §8(a) rows A1-A6.
+ * This header is the boundary of SURVEY.md §8(b): plain pointers and sizes,
+ * no torch types.  Every stage runs in this library's sm_100a kernels.
+ *
+ * Conventions (all entry points):
+ *  - Cube layout: band-sequential (BSQ) float32, C-contiguous
+ *    float[bands][rows][cols] (SPEC.md:22-27 HsiCube; BSQ order SPEC.md:23).
+ *    The BSQ cube is Y^T: a bands x N row-major matrix, N = rows*cols.
+ *  - Pointers are DEVICE pointers unless the name ends in _host.
+ *  - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream) and is asynchronous unless stated.  Exceptions: argument
+ *    validation is synchronous; hyde_hyres / _ex / _batched read the device
+ *    rank-decision flag once per 16-component chunk (one stream sync per
+ *    chunk) and therefore return after the GPU has finished
+ *    the rank decision (the output write may still be in flight).
+ *  - Ownership: the caller owns every buffer it passes; the library never
+ *    frees caller memory.  Workspace is owned by the handle (grown on demand
+ *    with cudaMallocAsync on `stream`, freed by hyde_destroy).
+ *  - In-place (out == cube) is allowed: every read of the cube (A1, A3)
+ *    precedes the only write (A6).  Partial overlap -> HYDE_EPARAM.
+ *  - Errors: no exceptions cross the ABI.  Status codes mirror the SPEC exit
+ *    codes: parameter errors -> HYDE_EPARAM (bands < 3 or
+ *    rows*cols <= bands: SPEC.md:363, :365, :381; taps not in {2,8,16} or
+ *    levels impossible: SPEC.md:122); non-finite input -> HYDE_EDATA
+ *    (SPEC.md:26), detected on the device during A1 and reported through
+ *    info->nonfinite_input and the return value of the call that synced.
+ *    CUDA failures -> HYDE_ECUDA (hyde_last_error() holds the message).
+ *  - A handle is not thread-safe; use one handle per host thread.
+ */
+#ifndef HYDE_H_
+#define HYDE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* hyde_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+  HYDE_OK = 0,
+  HYDE_EPARAM = 2,   /* SPEC.md:545 exit code 2: usage/parameter error  */
+  HYDE_EDATA = 3,    /* SPEC.md:545 exit code 3: data error (non-finite) */
+  HYDE_EMETHOD = 4,  /* SPEC.md:545 exit code 4: method failure          */
+  HYDE_ECUDA = 5,
+  HYDE_ENCCL = 6,
+  HYDE_ENOMEM = 7
+} hyde_status;
+
+typedef struct hyde_ctx* hyde_handle;
+
+/* Create a handle bound to CUDA device `device` (the caller's current device
+ * is restored on return).  Errors: HYDE_EPARAM (NULL out), HYDE_ECUDA. */
+hyde_status hyde_create(hyde_handle* out, int device);
+/* Synchronizes the handle's device, frees its workspace.  NULL is a no-op. */
+hyde_status hyde_destroy(hyde_handle h);
+const char* hyde_status_string(hyde_status s);
+/* Last error message recorded on this handle (never NULL). */
+const char* hyde_last_error(hyde_handle h);
+/* Library version string, and the sm architecture the kernels target (100 = sm_100a). */
+const char* hyde_version(void);
+int hyde_target_sm(void);
+
+/* HyRes parameters.  HyRes is parameter-free:
+ * zero-initialised params (or NULL) give the defaults of SURVEY.md §8(c). */
+typedef struct {
+  int wavelet_taps;  /* 2 (Haar) | 8 (db4) | 16 (db8, default)  -- SPEC.md:179 D4; 0 = 16 */
+  int levels;        /* 0 = auto: max(1, min(5, floor(log2(min(R,C)/(taps-1)))))         */
+  int chunk;         /* candidate components per projection chunk; 0 = 16; max 32      */
+  double ridge;      /* delta of (G + delta I)^-1; 0 = 1e-6                */
+  int flags;         /* bit0 HYDE_KEEP_LL: leave LL_L unthresholded (variant, Z7)       */
+} hyde_hyres_params;
+#define HYDE_KEEP_LL 1
+
+/* Diagnostics of one HyRes call (host memory). */
+typedef struct {
+  int rank;             /* r*: components kept          */
+  int levels;           /* DWT levels used                                   */
+  int chunks_run;       /* projection chunks processed                       */
+  int nonfinite_input;  /* 1 if a NaN/Inf was seen in the cube (A1)          */
+  int n_coeffs;         /* N_c: coefficients per eigen-image                  */
+  int reserved[3];
+} hyde_hyres_info;
+
+void hyde_hyres_params_default(hyde_hyres_params* p);
+
+/* --- A1: noise estimate (north_star stage (1); PAPER.md:105-106 HySime's
+ * regression estimator).  sigma_out[b] = sqrt(1/(N M_bb)),
+ * M = (G + ridge I)^-1, G = Y Y^T (bands x bands, uncentered, fp64) -- the
+ * residual standard deviation of the least-squares regression of band b on
+ * all other bands.  gram_out (bands*bands fp64, row-major) and noise_out
+ * (BSQ float32 like the cube: residual_b = (M Y)_b / M_bb) may be NULL.
+ * Asynchronous; non-finite input is reported by the return value of a later
+ * hyde_sync_status(h) (HYDE_EDATA). */
+hyde_status hyde_estimate_noise(hyde_handle h, const float* cube, int rows, int cols, int bands,
+                                double* sigma_out, double* gram_out, float* noise_out,
+                                hyde_stream_t stream);
+
+/* --- Full HyRes (stages (1)-(6)).  hyde_hyres == hyde_hyres_ex(.., NULL, NULL, ..). */
+hyde_status hyde_hyres(hyde_handle h, const float* cube, int rows, int cols, int bands,
+                       float* out, hyde_stream_t stream);
+hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, int bands,
+                          float* out, const hyde_hyres_params* params, hyde_hyres_info* info,
+                          hyde_stream_t stream);
+/* Same computation with HOST buffers (pageable or pinned): copies the cube
+ * in, runs hyde_hyres_ex, copies the result out; returns after the result is
+ * in out_host (synchronous). */
+hyde_status hyde_hyres_host(hyde_handle h, const float* cube_host, int rows, int cols, int bands,
+                            float* out_host, const hyde_hyres_params* params,
+                            hyde_hyres_info* info, hyde_stream_t stream);
+/* Bytes of device workspace hyde_hyres_ex / _batched will hold for this shape. */
+size_t hyde_hyres_workspace_size(int rows, int cols, int bands, int batch,
+                                 const hyde_hyres_params* params);
+/* `batch` independent same-shape cubes, cubes[batch][bands][rows][cols] ->
+ * outs (same layout); info may be NULL or point to `batch` records. */
+hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int rows, int cols,
+                               int bands, float* outs, const hyde_hyres_params* params,
+                               hyde_hyres_info* info, hyde_stream_t stream);
+/* Status of asynchronous device-side checks (non-finite input) of the work
+ * enqueued so far; synchronizes `stream`. */
+hyde_status hyde_sync_status(hyde_handle h, hyde_stream_t stream);
+
+/* --- Stage entry points (test/diagnostic; same conventions).  Each consumes
+ * and produces the oracle's intermediate layout (oracle/hyres_ref.py). ---- */
+
+/* A1: G = Y Y^T, fp64 row-major bands x bands. */
+hyde_status hyde_k_gram(hyde_handle h, const float* cube, int n_pixels, int bands, double* gram,
+                        hyde_stream_t stream);
+/* A1+A2: from G (fp64, bands x bands) and N: sigma[bands]; lam[bands] (all
+ * eigenvalues of G_w = diag(sigma)^-1 G diag(sigma)^-1 / N, descending);
+ * V[bands x ncomp] (row-major, eigenvectors of the ncomp largest, sign-fixed:
+ * largest-|.| entry positive, SPEC.md:181 D6). */
+hyde_status hyde_k_eig(hyde_handle h, const double* gram, int n_pixels, int bands, double ridge,
+                       int ncomp, double* sigma, double* lam, double* V, hyde_stream_t stream);
+/* A3: E[k][p] = sum_b W[b][k] Y[b][p], W = float32 row-major bands x ncomp. */
+hyde_status hyde_k_project(hyde_handle h, const float* cube, int n_pixels, int bands,
+                           const float* W, int ncomp, float* E, hyde_stream_t stream);
+/* A4: forward DWT of `count` images (each rows x cols, contiguous) into the
+ * subband layout: per image, level 1..L x (LH, HL, HH) then LL_L, each
+ * subband row-major; n_coeffs per image (see hyde_dwt_coeff_count). */
+hyde_status hyde_k_dwt_fwd(hyde_handle h, const float* images, int count, int rows, int cols,
+                           int levels, int taps, float* coeffs, hyde_stream_t stream);
+int hyde_dwt_coeff_count(int rows, int cols, int levels);
+int hyde_auto_levels(int rows, int cols, int taps);
+/* A5: per subband SURE (noise sigma = 1): kstar[count*(3L+1)] (index into
+ * {0} U sorted |x|), tstar[...] (threshold), in-place soft threshold of
+ * coeffs, e_post[count] (sum of squares of the thresholded coefficients). */
+hyde_status hyde_k_sure(hyde_handle h, float* coeffs, int count, int rows, int cols, int levels,
+                        int keep_ll, int* kstar, float* tstar, double* e_post,
+                        hyde_stream_t stream);
+/* A6a: inverse DWT of `count` coefficient sets -> images (rows x cols each). */
+hyde_status hyde_k_idwt(hyde_handle h, const float* coeffs, int count, int rows, int cols,
+                        int levels, int taps, float* images, hyde_stream_t stream);
+/* A6b: out[b][p] = sum_{k<rank} U[b][k] E[k][p], U float32 row-major bands x ldu. */
+hyde_status hyde_k_reconstruct(hyde_handle h, const float* E, int n_pixels, int bands,
+                               const float* U, int ldu, int rank, float* out,
+                               hyde_stream_t stream);
+/* Analysis low-pass filter the kernels use (host, fp64; taps values). */
+hyde_status hyde_filter(int taps, double* h_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYDE_H_ */

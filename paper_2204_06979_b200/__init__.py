@@ -1,0 +1,145 @@
+"""B200-native HyRes (HyDe, arXiv 2204.06979): Python binding of libhyde.so.
+
+PyTorch supplies device memory and the current CUDA stream; every stage of the
+method runs in libhyde's sm_100a kernels behind the C-ABI of include/hyde.h.
+Inputs must be CUDA float32 tensors in BSQ layout (bands, rows, cols); there
+is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional, Tuple
+
+from . import _lib
+from ._lib import HydeError, Info, Params, check, lib, make_params
+
+__all__ = ["hyres", "hyres_batched", "hyres_host", "estimate_noise", "workspace_size",
+           "HydeError", "stages", "version"]
+
+_handles: Dict[int, int] = {}
+
+
+def version() -> str:
+    return lib().hyde_version().decode()
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def handle(device: int) -> int:
+    h = _handles.get(device)
+    if h is None:
+        hv = ctypes.c_void_p()
+        check(lib().hyde_create(ctypes.byref(hv), int(device)))
+        h = hv.value
+        _handles[device] = h
+    return h
+
+
+def _stream(t) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _cube(t, name="cube", ndim=3):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise HydeError(2, f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != torch.float32:
+        raise HydeError(2, f"{name} must be float32")
+    if t.dim() != ndim:
+        raise HydeError(2, f"{name} must have {ndim} dims")
+    if not t.is_contiguous():
+        raise HydeError(2, f"{name} must be contiguous")
+    return t
+
+
+def hyres(cube, out=None, *, taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False,
+          return_info=False):
+    """HyRes denoising of one BSQ cube (bands, rows, cols) -> same shape."""
+    torch = _torch()
+    _cube(cube)
+    b, r, c = cube.shape
+    if out is None:
+        out = torch.empty_like(cube)
+    else:
+        _cube(out, "out")
+    p = make_params(taps, levels, chunk, ridge, keep_ll)
+    info = Info()
+    h = handle(cube.device.index)
+    check(lib().hyde_hyres_ex(h, cube.data_ptr(), r, c, b, out.data_ptr(), ctypes.byref(p),
+                              ctypes.byref(info), _stream(cube)), h)
+    return (out, info.as_dict()) if return_info else out
+
+
+def hyres_batched(cubes, out=None, *, taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False,
+                  return_info=False):
+    """`batch` independent cubes (batch, bands, rows, cols)."""
+    torch = _torch()
+    _cube(cubes, "cubes", 4)
+    n, b, r, c = cubes.shape
+    if out is None:
+        out = torch.empty_like(cubes)
+    p = make_params(taps, levels, chunk, ridge, keep_ll)
+    infos = (Info * max(n, 1))()
+    h = handle(cubes.device.index)
+    check(lib().hyde_hyres_batched(h, cubes.data_ptr(), n, r, c, b, out.data_ptr(), ctypes.byref(p),
+                                   infos, _stream(cubes)), h)
+    return (out, [infos[i].as_dict() for i in range(n)]) if return_info else out
+
+
+def hyres_host(cube_np, out_np=None, *, device=0, taps=16, levels=0, chunk=16, ridge=1e-6,
+               keep_ll=False, return_info=False):
+    """End-to-end call with HOST buffers (numpy float32, C-contiguous; pinned or pageable):
+    the library copies the cube in, denoises, copies the result out."""
+    import numpy as np
+    torch = _torch()
+    a = cube_np
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous():
+            raise HydeError(2, "host cube must be a contiguous float32 CPU tensor")
+        b, r, c = a.shape
+        out = torch.empty_like(a) if out_np is None else out_np
+        src, dst = a.data_ptr(), out.data_ptr()
+    else:
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        b, r, c = a.shape
+        out = np.empty_like(a) if out_np is None else out_np
+        src, dst = a.ctypes.data, out.ctypes.data
+    p = make_params(taps, levels, chunk, ridge, keep_ll)
+    info = Info()
+    h = handle(device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    check(lib().hyde_hyres_host(h, src, r, c, b, dst, ctypes.byref(p), ctypes.byref(info), stream), h)
+    return (out, info.as_dict()) if return_info else out
+
+
+def estimate_noise(cube, *, return_gram=False, return_residual=False):
+    """sigma (bands,) fp64 [, G (bands, bands) fp64] [, residual (bands, rows, cols) fp32]."""
+    torch = _torch()
+    _cube(cube)
+    b, r, c = cube.shape
+    sigma = torch.empty(b, dtype=torch.float64, device=cube.device)
+    gram = torch.empty((b, b), dtype=torch.float64, device=cube.device) if return_gram else None
+    res = torch.empty_like(cube) if return_residual else None
+    h = handle(cube.device.index)
+    check(lib().hyde_estimate_noise(h, cube.data_ptr(), r, c, b, sigma.data_ptr(),
+                                    gram.data_ptr() if gram is not None else None,
+                                    res.data_ptr() if res is not None else None, _stream(cube)), h)
+    check(lib().hyde_sync_status(h, _stream(cube)), h)
+    out = (sigma,)
+    if return_gram:
+        out += (gram,)
+    if return_residual:
+        out += (res,)
+    return out[0] if len(out) == 1 else out
+
+
+def workspace_size(rows, cols, bands, batch=1, chunk=16, taps=16, levels=0) -> int:
+    p = make_params(taps, levels, chunk)
+    return int(lib().hyde_hyres_workspace_size(rows, cols, bands, batch, ctypes.byref(p)))
+
+
+from . import stages  # noqa: E402

@@ -1,0 +1,106 @@
+"""ctypes binding of libhyde.so (include/hyde.h).  Argument marshalling only.
+
+There is no fallback: if libhyde.so is missing or a call fails, this raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_size_t, c_void_p
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libhyde.so")
+HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "hyde.h")
+
+HYDE_OK, HYDE_EPARAM, HYDE_EDATA, HYDE_EMETHOD, HYDE_ECUDA, HYDE_ENCCL, HYDE_ENOMEM = 0, 2, 3, 4, 5, 6, 7
+HYDE_KEEP_LL = 1
+
+
+class HydeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hyde status {status}: {msg}")
+        self.status = status
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("wavelet_taps", c_int), ("levels", c_int), ("chunk", c_int),
+                ("ridge", c_double), ("flags", c_int)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("rank", c_int), ("levels", c_int), ("chunks_run", c_int),
+                ("nonfinite_input", c_int), ("n_coeffs", c_int), ("reserved", c_int * 3)]
+
+    def as_dict(self):
+        return {"rank": self.rank, "levels": self.levels, "chunks_run": self.chunks_run,
+                "nonfinite_input": self.nonfinite_input, "n_coeffs": self.n_coeffs}
+
+
+_P = c_void_p  # device or host pointer
+_SIGS = {
+    "hyde_create": (c_int, [POINTER(c_void_p), c_int]),
+    "hyde_destroy": (c_int, [c_void_p]),
+    "hyde_status_string": (c_char_p, [c_int]),
+    "hyde_last_error": (c_char_p, [c_void_p]),
+    "hyde_version": (c_char_p, []),
+    "hyde_target_sm": (c_int, []),
+    "hyde_hyres_params_default": (None, [POINTER(Params)]),
+    "hyde_estimate_noise": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, _P, _P, c_void_p]),
+    "hyde_hyres": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, c_void_p]),
+    "hyde_hyres_ex": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
+    "hyde_hyres_host": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
+    "hyde_hyres_workspace_size": (c_size_t, [c_int, c_int, c_int, c_int, POINTER(Params)]),
+    "hyde_hyres_batched": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
+    "hyde_sync_status": (c_int, [c_void_p, c_void_p]),
+    "hyde_k_gram": (c_int, [c_void_p, _P, c_int, c_int, _P, c_void_p]),
+    "hyde_k_eig": (c_int, [c_void_p, _P, c_int, c_int, c_double, c_int, _P, _P, _P, c_void_p]),
+    "hyde_k_project": (c_int, [c_void_p, _P, c_int, c_int, _P, c_int, _P, c_void_p]),
+    "hyde_k_dwt_fwd": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, c_void_p]),
+    "hyde_dwt_coeff_count": (c_int, [c_int, c_int, c_int]),
+    "hyde_auto_levels": (c_int, [c_int, c_int, c_int]),
+    "hyde_k_sure": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, _P, _P, c_void_p]),
+    "hyde_k_idwt": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, c_void_p]),
+    "hyde_k_reconstruct": (c_int, [c_void_p, _P, c_int, c_int, _P, c_int, c_int, _P, c_void_p]),
+    "hyde_filter": (c_int, [c_int, POINTER(c_double)]),
+}
+
+_lib = None
+
+
+def header_functions(path: str = HEADER):
+    """Names of the functions include/hyde.h declares."""
+    txt = open(path).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(hyde_[a-z0-9_]+)\s*\(", txt)))
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise HydeError(-1, f"{LIB_PATH} is not built: run `python -m paper_2204_06979_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int, handle=None):
+    if status != HYDE_OK:
+        msg = lib().hyde_last_error(handle).decode(errors="replace")
+        raise HydeError(status, msg)
+
+
+def make_params(taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False) -> Params:
+    p = Params()
+    lib().hyde_hyres_params_default(ctypes.byref(p))
+    p.wavelet_taps = int(taps)
+    p.levels = int(levels)
+    p.chunk = int(chunk)
+    p.ridge = float(ridge)
+    p.flags = HYDE_KEEP_LL if keep_ll else 0
+    return p

@@ -1,0 +1,568 @@
+// libhyde C-ABI (include/hyde.h): validation, workspace planning, stream
+// ordering of the K1-K6 kernels, and the per-chunk rank decision.
+//
+// Orchestration of hyde_hyres_ex:
+//   K1 gram -> K2 noise+eig (first chunk of eigenvectors) ->
+//   for each chunk of r_c candidate components:
+//       [K2b more eigenvectors] -> K3 project -> K4 DWT levels -> K5 SURE ->
+//       rank decision (device) -> one D2H read of the 16-byte rank state ->
+//       K6a IDWT of the chunk's kept components
+//   -> K6b reconstruct (single write of the BSQ output).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace {
+thread_local std::string g_err;
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  int B, chunk, nsplit, nsub, ldwu, taps, levels;
+  long long n, ldE;
+  DwtPlan plan;
+  size_t G, partial, sigma, lam, tri, house, W, U, C, S1, S2, kstar, tstar, esub, epost, rs, total;
+  size_t s1_img, s2_img;  // per-image strides (floats) of the LL scratch
+};
+
+void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Layout* L) {
+  L->B = B;
+  L->chunk = chunk;
+  L->taps = taps;
+  L->levels = levels;
+  L->n = (long long)rows * cols;
+  L->ldE = (L->n + 63) / 64 * 64;
+  L->nsplit = gram_nsplit(L->n, B);
+  L->ldwu = B;
+  hyde_make_plan(rows, cols, levels, &L->plan);
+  L->nsub = 3 * levels + 1;
+  const size_t P = (size_t)B * (B + 1) / 2;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += al(bytes); return o; };
+  L->G = take((size_t)B * B * 8);
+  L->partial = take((size_t)L->nsplit * B * B * 8);
+  L->sigma = take((size_t)B * 8);
+  L->lam = take((size_t)B * 8);
+  L->tri = take((size_t)(3 * B + 8) * 8);
+  L->house = take(((size_t)B * B + 2 * (size_t)B + P + 64) * 8);
+  L->W = take((size_t)B * L->ldwu * 4);
+  L->U = take((size_t)B * L->ldwu * 4);
+  L->C = take((size_t)chunk * L->plan.n_coeffs * 4);
+  L->s1_img = (size_t)L->plan.lv[0].hs * L->plan.lv[0].ws;
+  L->s2_img = levels > 1 ? (size_t)L->plan.lv[1].hs * L->plan.lv[1].ws : 1;
+  L->S1 = take((size_t)chunk * L->s1_img * 4);
+  L->S2 = take((size_t)chunk * L->s2_img * 4);
+  L->kstar = take((size_t)chunk * L->nsub * 4);
+  L->tstar = take((size_t)chunk * L->nsub * 4);
+  L->esub = take((size_t)chunk * L->nsub * 8);
+  L->epost = take((size_t)B * 8);
+  L->rs = take(sizeof(RankState));
+  L->total = off;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+struct hyde_ctx {
+  int device = 0;
+  std::string err;
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  float* ebuf = nullptr;
+  size_t ebuf_cap = 0;   // bytes
+  RankState* rs_host = nullptr;
+  float* dev_in = nullptr;
+  float* dev_out = nullptr;
+  size_t dev_io_cap = 0;
+  RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
+};
+
+hyde_status hyde_cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+  g_err = buf;
+  return e == cudaErrorMemoryAllocation ? HYDE_ENOMEM : HYDE_ECUDA;
+}
+
+static hyde_status fail(hyde_handle h, hyde_status s, const std::string& msg) {
+  g_err = msg;
+  if (h) h->err = msg;
+  return s;
+}
+
+#define CK(expr)                                                              \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      hyde_status _s = hyde_cuda_fail(_e, #expr, __FILE__, __LINE__);         \
+      if (h) h->err = g_err;                                                  \
+      return _s;                                                              \
+    }                                                                         \
+  } while (0)
+
+static hyde_status ensure_ws(hyde_handle h, size_t bytes, cudaStream_t st) {
+  if (bytes <= h->ws_cap) return HYDE_OK;
+  if (h->ws) CK(cudaFreeAsync(h->ws, st));
+  h->ws = nullptr;
+  h->ws_cap = 0;
+  size_t cap = bytes + bytes / 8;
+  CK(cudaMallocAsync((void**)&h->ws, cap, st));
+  h->ws_cap = cap;
+  return HYDE_OK;
+}
+
+// grow the eigen-image buffer to `bytes`, preserving the first `keep` bytes
+static hyde_status ensure_ebuf(hyde_handle h, size_t bytes, size_t keep, cudaStream_t st) {
+  if (bytes <= h->ebuf_cap) return HYDE_OK;
+  float* nb = nullptr;
+  CK(cudaMallocAsync((void**)&nb, bytes, st));
+  if (h->ebuf && keep) CK(cudaMemcpyAsync(nb, h->ebuf, keep, cudaMemcpyDeviceToDevice, st));
+  if (h->ebuf) CK(cudaFreeAsync(h->ebuf, st));
+  h->ebuf = nb;
+  h->ebuf_cap = bytes;
+  return HYDE_OK;
+}
+
+static void defaults(const hyde_hyres_params* in, hyde_hyres_params* p) {
+  hyde_hyres_params_default(p);
+  if (!in) return;
+  if (in->wavelet_taps) p->wavelet_taps = in->wavelet_taps;
+  p->levels = in->levels;
+  if (in->chunk) p->chunk = in->chunk;
+  if (in->ridge != 0.0) p->ridge = in->ridge;
+  p->flags = in->flags;
+}
+
+static bool overlap(const void* a, size_t an, const void* b, size_t bn) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + bn && y < x + an;
+}
+
+static hyde_status validate_shape(hyde_handle h, int rows, int cols, int bands) {
+  if (!h) return HYDE_EPARAM;
+  if (rows < 1 || cols < 1) return fail(h, HYDE_EPARAM, "rows and cols must be >= 1");
+  if (bands < 3) return fail(h, HYDE_EPARAM, "bands must be >= 3 (SPEC.md:363)");
+  if (bands > 256) return fail(h, HYDE_EPARAM, "bands must be <= 256");
+  if ((long long)rows * cols <= bands) return fail(h, HYDE_EPARAM, "rows*cols must exceed bands (SPEC.md:365)");
+  if ((long long)rows * cols > (1LL << 31) / 4) return fail(h, HYDE_EPARAM, "cube too large for one call");
+  return HYDE_OK;
+}
+
+static hyde_status resolve_params(hyde_handle h, int rows, int cols, const hyde_hyres_params* in,
+                                  hyde_hyres_params* p, int* levels) {
+  defaults(in, p);
+  if (p->wavelet_taps != 2 && p->wavelet_taps != 8 && p->wavelet_taps != 16)
+    return fail(h, HYDE_EPARAM, "wavelet_taps must be 2, 8 or 16 (SPEC.md:179 D4)");
+  if (p->chunk < 1 || p->chunk > HYDE_MAX_CHUNK) return fail(h, HYDE_EPARAM, "chunk must be in [1, 32]");
+  if (p->ridge < 0.0) return fail(h, HYDE_EPARAM, "ridge must be >= 0");
+  int lv = p->levels > 0 ? p->levels : hyde_auto_levels(rows, cols, p->wavelet_taps);
+  if (lv > HYDE_MAX_LEVELS || (long long)(rows < cols ? rows : cols) < (1LL << lv))
+    return fail(h, HYDE_EPARAM, "levels impossible for this image size (SPEC.md:122)");
+  *levels = lv;
+  return HYDE_OK;
+}
+
+// forward DWT of `count` images at E (stride ldE) into C (stride N_c)
+static cudaError_t dwt_forward(const Layout& L, char* ws, const float* E, long long ldE, int count,
+                               const FilterBank& fb, cudaStream_t st) {
+  float* C = (float*)(ws + L.C);
+  float* S[2] = {(float*)(ws + L.S1), (float*)(ws + L.S2)};
+  long long sstr[2] = {(long long)L.s1_img, (long long)L.s2_img};
+  const long long nc = L.plan.n_coeffs;
+  for (int l = 0; l < L.levels; ++l) {
+    const float* in = l == 0 ? E : S[(l - 1) & 1];
+    long long in_str = l == 0 ? ldE : sstr[(l - 1) & 1];
+    float* llo = (l == L.levels - 1) ? C + L.plan.ll_off : S[l & 1];
+    long long ll_str = (l == L.levels - 1) ? nc : sstr[l & 1];
+    cudaError_t e = launch_dwt_level(in, in_str, L.plan.lv[l].h_in, L.plan.lv[l].w_in, llo, ll_str,
+                                     C + L.plan.sub_off[l], nc, count, fb, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+static cudaError_t dwt_inverse(const Layout& L, char* ws, const float* Cin, float* Eout, long long ldE,
+                               int count, const FilterBank& fb, cudaStream_t st) {
+  float* S[2] = {(float*)(ws + L.S1), (float*)(ws + L.S2)};
+  long long sstr[2] = {(long long)L.s1_img, (long long)L.s2_img};
+  const long long nc = L.plan.n_coeffs;
+  for (int l = L.levels - 1; l >= 0; --l) {
+    const float* llin = (l == L.levels - 1) ? Cin + L.plan.ll_off : S[l & 1];
+    long long ll_str = (l == L.levels - 1) ? nc : sstr[l & 1];
+    float* out = l == 0 ? Eout : S[(l - 1) & 1];
+    long long out_str = l == 0 ? ldE : sstr[(l - 1) & 1];
+    cudaError_t e = launch_idwt_level(llin, ll_str, Cin + L.plan.sub_off[l], nc, L.plan.lv[l].h_in,
+                                      L.plan.lv[l].w_in, out, out_str, count, fb, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+extern "C" {
+
+const char* hyde_version(void) { return "hyde-b200 0.1 (sm_100a)"; }
+int hyde_target_sm(void) { return 100; }
+
+const char* hyde_status_string(hyde_status s) {
+  switch (s) {
+    case HYDE_OK: return "ok";
+    case HYDE_EPARAM: return "parameter error";
+    case HYDE_EDATA: return "data error (non-finite input)";
+    case HYDE_EMETHOD: return "method failure";
+    case HYDE_ECUDA: return "CUDA error";
+    case HYDE_ENCCL: return "NCCL error";
+    case HYDE_ENOMEM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+const char* hyde_last_error(hyde_handle h) {
+  if (h && !h->err.empty()) return h->err.c_str();
+  return g_err.c_str();
+}
+
+void hyde_hyres_params_default(hyde_hyres_params* p) {
+  if (!p) return;
+  memset(p, 0, sizeof(*p));
+  p->wavelet_taps = 16;
+  p->levels = 0;
+  p->chunk = 16;
+  p->ridge = 1e-6;
+  p->flags = 0;
+}
+
+hyde_status hyde_create(hyde_handle* out, int device) {
+  if (!out) return HYDE_EPARAM;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return hyde_cuda_fail(e, "cudaGetDeviceCount", __FILE__, __LINE__);
+  if (device < 0 || device >= ndev) {
+    g_err = "no such CUDA device";
+    return HYDE_EPARAM;
+  }
+  hyde_ctx* h = new hyde_ctx();
+  h->device = device;
+  DeviceGuard g(device);
+  e = cudaMallocHost((void**)&h->rs_host, sizeof(RankState));
+  if (e != cudaSuccess) {
+    delete h;
+    return hyde_cuda_fail(e, "cudaMallocHost", __FILE__, __LINE__);
+  }
+  *out = h;
+  return HYDE_OK;
+}
+
+hyde_status hyde_destroy(hyde_handle h) {
+  if (!h) return HYDE_OK;
+  {
+    DeviceGuard g(h->device);
+    cudaDeviceSynchronize();
+    if (h->ws) cudaFree(h->ws);
+    if (h->ebuf) cudaFree(h->ebuf);
+    if (h->dev_in) cudaFree(h->dev_in);
+    if (h->dev_out) cudaFree(h->dev_out);
+    if (h->rs_host) cudaFreeHost(h->rs_host);
+  }
+  delete h;
+  return HYDE_OK;
+}
+
+size_t hyde_hyres_workspace_size(int rows, int cols, int bands, int batch, const hyde_hyres_params* params) {
+  hyde_hyres_params p;
+  int lv = 0;
+  if (rows < 1 || cols < 1 || bands < 3 || bands > 256) return 0;
+  defaults(params, &p);
+  if (p.wavelet_taps != 2 && p.wavelet_taps != 8 && p.wavelet_taps != 16) return 0;
+  lv = p.levels > 0 ? p.levels : hyde_auto_levels(rows, cols, p.wavelet_taps);
+  if (lv > HYDE_MAX_LEVELS) return 0;
+  (void)batch;
+  Layout L;
+  make_layout(rows, cols, bands, p.chunk, lv, p.wavelet_taps, &L);
+  return L.total + (size_t)p.chunk * L.ldE * 4;
+}
+
+hyde_status hyde_sync_status(hyde_handle h, hyde_stream_t stream) {
+  if (!h) return HYDE_EPARAM;
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaStreamSynchronize(st));
+  if (!h->last_rs) return HYDE_OK;
+  CK(cudaMemcpy(h->rs_host, h->last_rs, sizeof(RankState), cudaMemcpyDeviceToHost));
+  if (h->rs_host->nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
+  if (h->rs_host->sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
+  return HYDE_OK;
+}
+
+hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
+                          const hyde_hyres_params* params, hyde_hyres_info* info, hyde_stream_t stream) {
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  if (!cube || !out) return fail(h, HYDE_EPARAM, "NULL cube/out");
+  const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
+  if (cube != out && overlap(cube, bytes, out, bytes)) return fail(h, HYDE_EPARAM, "cube and out partially overlap");
+  hyde_hyres_params p;
+  int levels = 0;
+  s = resolve_params(h, rows, cols, params, &p, &levels);
+  if (s != HYDE_OK) return s;
+  FilterBank fb;
+  if (hyde_build_filters(p.wavelet_taps, &fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "filter derivation failed");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  const int B = bands;
+  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L);
+  s = ensure_ws(h, L.total, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  const long long n = L.n;
+  s = ensure_ebuf(h, (size_t)p.chunk * L.ldE * 4, 0, st);
+  if (s != HYDE_OK) return s;
+  RankState* rs = (RankState*)(ws + L.rs);
+  h->last_rs = rs;
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  double* G = (double*)(ws + L.G);
+  double* sigma = (double*)(ws + L.sigma);
+  double* house = (double*)(ws + L.house);
+  double* tri = (double*)(ws + L.tri);
+  float* W = (float*)(ws + L.W);
+  float* U = (float*)(ws + L.U);
+  float* C = (float*)(ws + L.C);
+  CK(launch_gram(cube, n, B, (double*)(ws + L.partial), L.nsplit, G, &rs->nonfinite, st));
+  const int first = p.chunk < B ? p.chunk : B;
+  CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
+  int rank = 0, chunks = 0;
+  for (int c = 0;; ++c) {
+    const int k0 = c * p.chunk;
+    const int cnt = (B - k0) < p.chunk ? (B - k0) : p.chunk;
+    if (c > 0) {
+      s = ensure_ebuf(h, (size_t)(k0 + cnt) * L.ldE * 4, (size_t)k0 * L.ldE * 4, st);
+      if (s != HYDE_OK) return s;
+      CK(launch_eigvec_more(tri, house, sigma, B, k0, cnt, nullptr, nullptr, W, U, L.ldwu, st));
+    }
+    float* E = h->ebuf + (size_t)k0 * L.ldE;
+    CK(launch_project(cube, n, B, W + k0, L.ldwu, cnt, E, L.ldE, st));
+    CK(dwt_forward(L, ws, E, L.ldE, cnt, fb, st));
+    CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
+                   (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, st));
+    CK(launch_rank_decide((double*)(ws + L.esub), L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs,
+                          (double*)(ws + L.epost), st));
+    CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ++chunks;
+    const RankState r = *h->rs_host;
+    if (r.nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
+    if (r.sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
+    const int kept = r.found ? (r.rank - k0) : cnt;
+    if (kept > 0) CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, st));
+    if (r.found) {
+      rank = r.rank;
+      break;
+    }
+  }
+  CK(launch_reconstruct(h->ebuf, L.ldE, n, B, U, L.ldwu, rank, out, st));
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->rank = rank;
+    info->levels = levels;
+    info->chunks_run = chunks;
+    info->nonfinite_input = 0;
+    info->n_coeffs = (int)L.plan.n_coeffs;
+  }
+  return HYDE_OK;
+}
+
+hyde_status hyde_hyres(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
+                       hyde_stream_t stream) {
+  return hyde_hyres_ex(h, cube, rows, cols, bands, out, nullptr, nullptr, stream);
+}
+
+hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int rows, int cols, int bands,
+                               float* outs, const hyde_hyres_params* params, hyde_hyres_info* info,
+                               hyde_stream_t stream) {
+  if (!h) return HYDE_EPARAM;
+  if (batch < 0 || (batch > 0 && (!cubes || !outs))) return fail(h, HYDE_EPARAM, "bad batch arguments");
+  const size_t per = (size_t)rows * cols * bands;
+  for (int i = 0; i < batch; ++i) {
+    hyde_status s = hyde_hyres_ex(h, cubes + per * i, rows, cols, bands, outs + per * i, params,
+                                  info ? info + i : nullptr, stream);
+    if (s != HYDE_OK) return s;
+  }
+  return HYDE_OK;
+}
+
+hyde_status hyde_hyres_host(hyde_handle h, const float* cube_host, int rows, int cols, int bands,
+                            float* out_host, const hyde_hyres_params* params, hyde_hyres_info* info,
+                            hyde_stream_t stream) {
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  if (!cube_host || !out_host) return fail(h, HYDE_EPARAM, "NULL host buffers");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
+  if (bytes > h->dev_io_cap) {
+    if (h->dev_in) CK(cudaFreeAsync(h->dev_in, st));
+    if (h->dev_out) CK(cudaFreeAsync(h->dev_out, st));
+    h->dev_in = h->dev_out = nullptr;
+    h->dev_io_cap = 0;
+    CK(cudaMallocAsync((void**)&h->dev_in, bytes, st));
+    CK(cudaMallocAsync((void**)&h->dev_out, bytes, st));
+    h->dev_io_cap = bytes;
+  }
+  CK(cudaMemcpyAsync(h->dev_in, cube_host, bytes, cudaMemcpyHostToDevice, st));
+  s = hyde_hyres_ex(h, h->dev_in, rows, cols, bands, h->dev_out, params, info, stream);
+  if (s != HYDE_OK) return s;
+  CK(cudaMemcpyAsync(out_host, h->dev_out, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_estimate_noise(hyde_handle h, const float* cube, int rows, int cols, int bands,
+                                double* sigma_out, double* gram_out, float* noise_out,
+                                hyde_stream_t stream) {
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  if (!cube || !sigma_out) return fail(h, HYDE_EPARAM, "NULL cube/sigma_out");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  make_layout(rows, cols, bands, 1, 1, 2, &L);
+  s = ensure_ws(h, L.total, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  RankState* rs = (RankState*)(ws + L.rs);
+  h->last_rs = rs;
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  double* G = gram_out ? gram_out : (double*)(ws + L.G);
+  CK(launch_gram(cube, L.n, bands, (double*)(ws + L.partial), L.nsplit, G, &rs->nonfinite, st));
+  CK(launch_noise_eig(G, L.n, bands, 1e-6, -1, 0, sigma_out, nullptr, nullptr, (double*)(ws + L.house),
+                      (double*)(ws + L.tri), (float*)(ws + L.W), (float*)(ws + L.U), L.ldwu, st));
+  if (noise_out)
+    CK(launch_noise_residual(cube, L.n, bands, G, 1e-6, (double*)(ws + L.house), noise_out, st));
+  return HYDE_OK;
+}
+
+// ---------------------------------------------------------------- stages
+hyde_status hyde_k_gram(hyde_handle h, const float* cube, int n_pixels, int bands, double* gram,
+                        hyde_stream_t stream) {
+  if (!h || !cube || !gram || n_pixels < 1 || bands < 1 || bands > 256) return fail(h, HYDE_EPARAM, "bad arguments");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  make_layout(n_pixels, 1, bands, 1, 1, 2, &L);
+  hyde_status s = ensure_ws(h, L.total, st);
+  if (s != HYDE_OK) return s;
+  RankState* rs = (RankState*)(h->ws + L.rs);
+  h->last_rs = rs;
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  CK(launch_gram(cube, L.n, bands, (double*)(h->ws + L.partial), L.nsplit, gram, &rs->nonfinite, st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_k_eig(hyde_handle h, const double* gram, int n_pixels, int bands, double ridge, int ncomp,
+                       double* sigma, double* lam, double* V, hyde_stream_t stream) {
+  if (!h || !gram || !sigma || n_pixels < 1 || bands < 3 || bands > 256 || ncomp < 0 || ncomp > bands ||
+      ncomp > HYDE_MAX_CHUNK)
+    return fail(h, HYDE_EPARAM, "bad arguments");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  make_layout(n_pixels, 1, bands, 1, 1, 2, &L);
+  hyde_status s = ensure_ws(h, L.total, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  CK(launch_noise_eig(gram, n_pixels, bands, ridge, ncomp, lam ? 1 : 0, sigma, lam, V,
+                      (double*)(ws + L.house), (double*)(ws + L.tri), (float*)(ws + L.W),
+                      (float*)(ws + L.U), L.ldwu, st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_k_project(hyde_handle h, const float* cube, int n_pixels, int bands, const float* W, int ncomp,
+                           float* E, hyde_stream_t stream) {
+  if (!h || !cube || !W || !E || n_pixels < 1 || bands < 1 || ncomp < 1 || ncomp > HYDE_MAX_CHUNK)
+    return fail(h, HYDE_EPARAM, "bad arguments");
+  DeviceGuard g(h->device);
+  CK(launch_project(cube, n_pixels, bands, W, ncomp, ncomp, E, n_pixels, (cudaStream_t)stream));
+  return HYDE_OK;
+}
+
+static hyde_status stage_layout(hyde_handle h, int count, int rows, int cols, int levels, int taps,
+                                Layout* L, FilterBank* fb, cudaStream_t st) {
+  if (!h || count < 1 || rows < 1 || cols < 1) return fail(h, HYDE_EPARAM, "bad arguments");
+  if (levels < 1 || levels > HYDE_MAX_LEVELS || (long long)(rows < cols ? rows : cols) < (1LL << levels))
+    return fail(h, HYDE_EPARAM, "levels impossible for this image size (SPEC.md:122)");
+  if (fb && hyde_build_filters(taps, fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "taps must be 2, 8 or 16");
+  make_layout(rows, cols, 3, count, levels, taps, L);
+  return ensure_ws(h, L->total, st);
+}
+
+hyde_status hyde_k_dwt_fwd(hyde_handle h, const float* images, int count, int rows, int cols, int levels,
+                           int taps, float* coeffs, hyde_stream_t stream) {
+  if (!images || !coeffs) return fail(h, HYDE_EPARAM, "NULL pointer");
+  DeviceGuard g(h ? h->device : 0);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  FilterBank fb;
+  hyde_status s = stage_layout(h, count, rows, cols, levels, taps, &L, &fb, st);
+  if (s != HYDE_OK) return s;
+  CK(dwt_forward(L, h->ws, images, (long long)rows * cols, count, fb, st));
+  CK(cudaMemcpyAsync(coeffs, h->ws + L.C, (size_t)count * L.plan.n_coeffs * 4, cudaMemcpyDeviceToDevice, st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_k_idwt(hyde_handle h, const float* coeffs, int count, int rows, int cols, int levels, int taps,
+                        float* images, hyde_stream_t stream) {
+  if (!images || !coeffs) return fail(h, HYDE_EPARAM, "NULL pointer");
+  DeviceGuard g(h ? h->device : 0);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  FilterBank fb;
+  hyde_status s = stage_layout(h, count, rows, cols, levels, taps, &L, &fb, st);
+  if (s != HYDE_OK) return s;
+  CK(dwt_inverse(L, h->ws, coeffs, images, (long long)rows * cols, count, fb, st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_k_sure(hyde_handle h, float* coeffs, int count, int rows, int cols, int levels, int keep_ll,
+                        int* kstar, float* tstar, double* e_post, hyde_stream_t stream) {
+  if (!coeffs || !kstar || !tstar || !e_post) return fail(h, HYDE_EPARAM, "NULL pointer");
+  DeviceGuard g(h ? h->device : 0);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  hyde_status s = stage_layout(h, count, rows, cols, levels, 2, &L, nullptr, st);
+  if (s != HYDE_OK) return s;
+  RankState* rs = (RankState*)(h->ws + L.rs);
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  CK(launch_sure(coeffs, L.plan.n_coeffs, L.plan, count, keep_ll, kstar, tstar, (double*)(h->ws + L.esub), rs, st));
+  CK(launch_rank_decide((double*)(h->ws + L.esub), L.nsub, count, 0, (double)L.plan.n_coeffs, 1 << 30, rs,
+                        e_post, st));
+  CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h->rs_host->sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
+  return HYDE_OK;
+}
+
+hyde_status hyde_k_reconstruct(hyde_handle h, const float* E, int n_pixels, int bands, const float* U, int ldu,
+                               int rank, float* out, hyde_stream_t stream) {
+  if (!h || !E || !U || !out || n_pixels < 1 || bands < 1 || rank < 1 || ldu < rank)
+    return fail(h, HYDE_EPARAM, "bad arguments");
+  DeviceGuard g(h->device);
+  CK(launch_reconstruct(E, n_pixels, n_pixels, bands, U, ldu, rank, out, (cudaStream_t)stream));
+  return HYDE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Shared definitions for libhyde's sm_100a kernels (not shared with oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hyde.h"
+
+#define HYDE_MAX_TAPS 16
+#define HYDE_MAX_LEVELS 12
+#define HYDE_MAX_CHUNK 32
+
+// Analysis filters (fp32) passed by value as a kernel argument (lives in the
+// constant bank).  g_k = (-1)^k h_{T-1-k}.
+struct FilterBank {
+  float h[HYDE_MAX_TAPS];
+  float g[HYDE_MAX_TAPS];
+  int taps;
+};
+
+// Geometry of one level of the 2-D DWT: input extent (h_in x w_in), padded
+// even extent (H x W), subband extent (H/2 x W/2).
+struct LevelGeom {
+  int h_in, w_in;   // input image of this level
+  int hs, ws;       // subband rows/cols = ceil(h_in/2), ceil(w_in/2)
+};
+
+struct DwtPlan {
+  int levels;
+  int rows, cols;
+  LevelGeom lv[HYDE_MAX_LEVELS];
+  long long sub_off[HYDE_MAX_LEVELS];  // offset of level l's LH within one coefficient set
+  long long ll_off;                    // offset of LL_L
+  long long n_coeffs;                  // N_c
+};
+
+// host helpers (filters.cpp / plan.cpp)
+int hyde_build_filters(int taps, FilterBank* fb, double* h64);
+void hyde_make_plan(int rows, int cols, int levels, DwtPlan* p);
+
+// device workspace pieces used by several kernels
+struct RankState {
+  int found;        // 1 once a failing component has been seen
+  int rank;         // r* once found (else running count of passing components)
+  int nonfinite;    // non-finite input flag (set by the Gram kernel)
+  int sure_overflow;// SURE survivor set exceeded its capacity (method failure)
+};
+
+#define HYDE_CUDA_OK(expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return ::hyde_cuda_fail(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+hyde_status hyde_cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+// kernel launchers (each returns cudaGetLastError() of its launch)
+cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int nsplit,
+                        double* G, int* nonfinite, cudaStream_t st);
+int gram_nsplit(long long n, int B);
+size_t eig_smem_bytes(int B, int ncomp);
+cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
+                             double* sigma, double* lam, double* V, double* house,
+                             double* tri, float* W, float* U, int ldwu, cudaStream_t st);
+cudaError_t launch_eigvec_more(const double* tri, const double* house, const double* sigma, int B,
+                               int k0, int ncomp, double* lam_top, double* V, float* W, float* U,
+                               int ldwu, cudaStream_t st);
+cudaError_t launch_noise_residual(const float* Y, long long n, int B, const double* G, double ridge,
+                                  double* work, float* out, cudaStream_t st);
+cudaError_t launch_project(const float* Y, long long n, int B, const float* W, int ldw, int ncomp,
+                           float* E, long long ldE, cudaStream_t st);
+cudaError_t launch_dwt_level(const float* in, long long in_stride, int h_in, int w_in,
+                             float* ll, long long ll_stride, float* sub, long long sub_stride,
+                             int count, const FilterBank& fb, cudaStream_t st);
+cudaError_t launch_idwt_level(const float* ll, long long ll_stride, const float* sub,
+                              long long sub_stride, int h_out, int w_out, float* out,
+                              long long out_stride, int count, const FilterBank& fb,
+                              cudaStream_t st);
+cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, int count,
+                        int keep_ll, int* kstar, float* tstar, double* e_sub,
+                        RankState* rs, cudaStream_t st);
+cudaError_t launch_rank_decide(const double* e_sub, int nsub, int count, int k0, double n_coeffs,
+                               int bands, RankState* rs, double* e_post, cudaStream_t st);
+cudaError_t launch_reconstruct(const float* E, long long ldE, long long n, int B, const float* U,
+                               int ldu, int rank, float* out, cudaStream_t st);

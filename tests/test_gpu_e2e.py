@@ -1,0 +1,154 @@
+"""End-to-end parity of the CUDA HyRes path (through the C-ABI) with the fp64 oracle
+(SURVEY.md §4 T2/T3): relative L2 <= 1e-4, |dMPSNR| <= 0.01 dB, identical rank r*
+(north_star acceptance), plus invariances, edge cases and error paths."""
+import numpy as np
+import pytest
+
+from oracle import hyres_ref as O
+from harness import synth, metrics
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+REL_L2 = 1e-4
+DMPSNR = 0.01
+
+
+@pytest.fixture(scope="module")
+def hy():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2204_06979_b200 as hy
+    return hy
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _compare(s, ref, out, info):
+    assert info["rank"] == ref.rank
+    assert info["levels"] == ref.levels
+    assert info["n_coeffs"] == ref.n_coeffs
+    assert metrics.rel_l2(ref.out, out) <= REL_L2
+    assert abs(metrics.mpsnr(s.clean, out) - metrics.mpsnr(s.clean, ref.out)) <= DMPSNR
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "medium", "wide"])
+def test_hyres_matches_oracle(hy, name):
+    s = synth.make_cube(name, 0)
+    ref = O.hyres(s.noisy)
+    out, info = hy.hyres(dev(s.noisy), return_info=True)
+    _compare(s, ref, out.cpu().numpy(), info)
+
+
+@pytest.mark.slow
+def test_hyres_large_matches_oracle(hy):
+    s = synth.make_cube("large", 0)
+    ref = O.hyres(s.noisy)
+    out, info = hy.hyres(dev(s.noisy), return_info=True)
+    _compare(s, ref, out.cpu().numpy(), info)
+
+
+def test_batched_matches_single_and_oracle(hy):
+    cfg = synth.CONFIGS["batched"]
+    seeds = [0, 1, 2]
+    samples = [synth.make_cube(cfg, sd) for sd in seeds]
+    cubes = dev(np.stack([x.noisy for x in samples]))
+    outs, infos = hy.hyres_batched(cubes, return_info=True)
+    for i, s in enumerate(samples):
+        single = hy.hyres(cubes[i].contiguous())
+        assert torch.equal(single, outs[i])
+        if i == 0:
+            ref = O.hyres(s.noisy)
+            _compare(s, ref, outs[i].cpu().numpy(), infos[i])
+
+
+def test_host_api_equals_device_api(hy):
+    s = synth.make_cube("small", 0)
+    d = hy.hyres(dev(s.noisy)).cpu().numpy()
+    h, info = hy.hyres_host(s.noisy, return_info=True)
+    assert np.array_equal(d, h)
+    pinned = torch.from_numpy(s.noisy).pin_memory()
+    h2 = hy.hyres_host(pinned)
+    assert np.array_equal(d, h2.numpy())
+
+
+def test_deterministic_and_in_place(hy):
+    s = synth.make_cube("tiny", 0)
+    a = hy.hyres(dev(s.noisy))
+    b = hy.hyres(dev(s.noisy))
+    assert torch.equal(a, b)
+    x = dev(s.noisy)
+    hy.hyres(x, out=x)
+    assert torch.equal(x, a)
+
+
+@pytest.mark.parametrize("taps,levels,keep_ll", [(2, 0, False), (8, 0, False), (16, 1, False), (16, 0, True)])
+def test_params_variants_match_oracle(hy, taps, levels, keep_ll):
+    s = synth.make_cube("tiny", 0)
+    ref = O.hyres(s.noisy, taps=taps, levels=levels, keep_ll=keep_ll)
+    out, info = hy.hyres(dev(s.noisy), taps=taps, levels=levels, keep_ll=keep_ll, return_info=True)
+    _compare(s, ref, out.cpu().numpy(), info)
+
+
+def test_chunk_boundary_rank(hy):
+    """Small chunks force several projection chunks (rank walk across chunk edges)."""
+    s = synth.make_cube("small", 0)
+    ref = O.hyres(s.noisy)
+    for chunk in (1, 2, 3):
+        out, info = hy.hyres(dev(s.noisy), chunk=chunk, return_info=True)
+        assert info["chunks_run"] >= (ref.rank + 1 + chunk - 1) // chunk
+        _compare(s, ref, out.cpu().numpy(), info)
+
+
+def test_noiseless_low_rank(hy):
+    s = synth.low_rank_cube(64, 64, 32, rank=4, seed=11)
+    ref = O.hyres(s.clean)
+    out, info = hy.hyres(dev(s.clean), return_info=True)
+    assert info["rank"] == 4 == ref.rank
+    assert metrics.rel_l2(s.clean, out.cpu().numpy()) < 1e-4
+
+
+def test_odd_ragged_shapes(hy):
+    for (b, r, c, seed) in [(3, 17, 33, 0), (9, 31, 29, 1), (40, 65, 127, 2), (256, 40, 40, 3)]:
+        s = synth.low_rank_cube(r, c, b, rank=min(3, b - 1), seed=seed, snr_db=20.0)
+        ref = O.hyres(s.noisy)
+        out, info = hy.hyres(dev(s.noisy), return_info=True)
+        assert info["rank"] == ref.rank, (b, r, c)
+        assert metrics.rel_l2(ref.out, out.cpu().numpy()) <= REL_L2, (b, r, c)
+
+
+def test_invariances_on_gpu(hy):
+    s = synth.make_cube("tiny", 0)
+    base = hy.hyres(dev(s.noisy)).cpu().numpy()
+    perm = np.random.default_rng(8).permutation(s.noisy.shape[0])
+    assert metrics.rel_l2(base[perm], hy.hyres(dev(s.noisy[perm])).cpu().numpy()) < 1e-5
+    tr = np.ascontiguousarray(s.noisy.transpose(0, 2, 1))
+    assert metrics.rel_l2(base.transpose(0, 2, 1), hy.hyres(dev(tr)).cpu().numpy()) < 1e-5
+    sh = np.roll(s.noisy, (12, -8), axis=(1, 2))
+    assert metrics.rel_l2(np.roll(base, (12, -8), axis=(1, 2)), hy.hyres(dev(sh)).cpu().numpy()) < 1e-5
+    sh1 = np.roll(s.noisy, 1, axis=2)
+    assert metrics.rel_l2(np.roll(base, 1, axis=2), hy.hyres(dev(sh1)).cpu().numpy()) > 1e-4
+
+
+def test_zero_cube_and_errors(hy):
+    z = torch.zeros((8, 16, 16), device="cuda")
+    out = hy.hyres(z)
+    assert torch.count_nonzero(out) == 0
+    bad = torch.ones((8, 16, 16), device="cuda")
+    bad[2, 3, 4] = float("nan")
+    with pytest.raises(hy.HydeError) as ei:
+        hy.hyres(bad)
+    assert ei.value.status == 3
+    with pytest.raises(hy.HydeError) as ei:
+        hy.hyres(torch.ones((2, 16, 16), device="cuda"))
+    assert ei.value.status == 2
+    with pytest.raises(hy.HydeError):
+        hy.hyres(torch.ones((8, 4, 2), device="cuda"))      # pixels <= bands
+    with pytest.raises(hy.HydeError):
+        hy.hyres(torch.ones((8, 16, 16), device="cuda"), taps=6)
+    with pytest.raises(hy.HydeError):
+        hy.hyres(torch.ones((8, 16, 16), device="cuda"), levels=7)
+    with pytest.raises(hy.HydeError):
+        hy.hyres(torch.ones((8, 16, 16)))                   # CPU tensor: no CPU path

@@ -1,0 +1,181 @@
+"""Stage-isolated parity: each CUDA stage, called through the C-ABI,
+against the oracle's same stage on identical inputs."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import hyres_ref as O
+from harness import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def hy():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2204_06979_b200 as hy
+    return hy
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "medium"])
+def test_gram_matches_oracle(hy, name):
+    s = synth.make_cube(name, 0)
+    g = hy.stages.gram(dev(s.noisy)).cpu().numpy()
+    ref = O.gram(s.noisy)
+    assert np.max(np.abs(g - ref)) / np.max(np.abs(ref)) < 1e-13
+    assert np.array_equal(g, g.T)
+
+
+def test_gram_ragged_and_tiny_shapes(hy):
+    rng = np.random.default_rng(0)
+    for b, n in [(3, 5), (7, 1000), (65, 333), (129, 4097), (256, 2049), (200, 31)]:
+        y = rng.standard_normal((b, n)).astype(np.float32)
+        g = hy.stages.gram(dev(y.reshape(b, n, 1))).cpu().numpy()
+        ref = y.astype(np.float64) @ y.astype(np.float64).T
+        assert np.max(np.abs(g - ref)) / np.max(np.abs(ref)) < 1e-13, (b, n)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "medium", "wide"])
+def test_noise_and_eig_match_oracle(hy, name):
+    s = synth.make_cube(name, 0)
+    b, r, c = s.noisy.shape
+    n = r * c
+    g = O.gram(s.noisy)
+    sig_ref, _ = O.estimate_noise(s.noisy)
+    lam_ref, v_ref, _ = O.whiten_eig(g, sig_ref, n)
+    k = min(16, b)
+    sig, lam, V = hy.stages.eig(dev(g), n, k)
+    sig, lam, V = sig.cpu().numpy(), lam.cpu().numpy(), V.cpu().numpy()
+    assert np.max(np.abs(sig / sig_ref - 1)) < 1e-9
+    assert np.max(np.abs(lam - lam_ref)) < 1e-11 * lam_ref[0]
+    # eigenvectors: compare where the eigenvalue is separated from its neighbours
+    for j in range(k):
+        gap = min([abs(lam_ref[j] - lam_ref[i]) for i in range(b) if i != j])
+        if gap > 1e-6 * lam_ref[0]:
+            err = np.max(np.abs(V[:, j] - v_ref[:, j]))
+            assert err < 1e-16 * lam_ref[0] / gap * 1e3 + 1e-10, (j, err, gap)
+    assert np.max(np.abs(V.T @ V - np.eye(k))) < 1e-8
+
+
+def test_estimate_noise_api(hy):
+    s = synth.make_cube("small", 0)
+    sig, g, res = hy.estimate_noise(dev(s.noisy), return_gram=True, return_residual=True)
+    sig_ref, g_ref, res_ref = O.estimate_noise(s.noisy, want_residual=True)
+    assert np.max(np.abs(sig.cpu().numpy() / sig_ref - 1)) < 1e-9
+    assert np.max(np.abs(g.cpu().numpy() - g_ref)) / np.max(np.abs(g_ref)) < 1e-13
+    rr = res.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(rr - res_ref) / np.linalg.norm(res_ref) < 1e-5
+
+
+def test_project_matches_fp64(hy):
+    rng = np.random.default_rng(1)
+    for b, n, k in [(32, 4096, 16), (200, 21025, 16), (7, 1001, 3), (103, 207400, 32), (50, 4099, 9)]:
+        y = rng.standard_normal((b, n)).astype(np.float32)
+        w = rng.standard_normal((b, k)).astype(np.float32)
+        e = hy.stages.project(dev(y.reshape(b, n, 1)), dev(w)).cpu().numpy()
+        ref = w.astype(np.float64).T @ y.astype(np.float64)
+        assert np.max(np.abs(e - ref)) / np.max(np.abs(ref)) < 2e-6, (b, n, k)
+
+
+DWT_SHAPES = [(64, 64, 2), (145, 145, 3), (610, 340, 4), (349, 1905, 4), (37, 50, 1), (17, 33, 2), (256, 256, 4)]
+
+
+@pytest.mark.parametrize("taps", [2, 8, 16])
+@pytest.mark.parametrize("shape", DWT_SHAPES)
+def test_dwt_forward_and_inverse_match_oracle(hy, taps, shape):
+    r, c, lv = shape
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((2, r, c)).astype(np.float32)
+    co = hy.stages.dwt_fwd(dev(x), lv, taps).cpu().numpy()
+    for i in range(2):
+        ref = np.concatenate([s.ravel() for s in O.flatten_coeffs(O.dwt2(x[i], lv, taps))])
+        assert co.shape[1] == ref.size
+        assert np.max(np.abs(co[i] - ref)) < 2e-5 * max(1.0, np.max(np.abs(ref)))
+    back = hy.stages.idwt(dev(co), r, c, lv, taps).cpu().numpy()
+    assert np.max(np.abs(back - x)) < 5e-5
+    # inverse of arbitrary coefficients vs the oracle's adjoint synthesis
+    cr = rng.standard_normal(co.shape).astype(np.float32)
+    img = hy.stages.idwt(dev(cr), r, c, lv, taps).cpu().numpy()
+    tmpl = O.dwt2(np.zeros((r, c)), lv, taps)
+    sizes = [s.size for s in O.flatten_coeffs(tmpl)]
+    offs = np.cumsum([0] + sizes)
+    for i in range(2):
+        subs = [cr[i, offs[j]:offs[j + 1]].reshape(O.flatten_coeffs(tmpl)[j].shape) for j in range(len(sizes))]
+        ref = O.idwt2(O.unflatten_coeffs([sb.astype(np.float64) for sb in subs], tmpl), taps)
+        assert np.max(np.abs(img[i] - ref)) < 5e-5 * max(1.0, np.max(np.abs(ref)))
+
+
+def _oracle_sure_on(co_row, r, c, lv):
+    tmpl = O.dwt2(np.zeros((r, c)), lv, 16)
+    subs = O.flatten_coeffs(tmpl)
+    offs = np.cumsum([0] + [s.size for s in subs])
+    out = []
+    for j in range(len(subs)):
+        out.append(O.sure_threshold(co_row[offs[j]:offs[j + 1]].astype(np.float64)))
+    return out, offs
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 2), (145, 145, 3), (1024, 1024, 5), (349, 1905, 4)])
+def test_sure_indices_bit_exact(hy, shape):
+    r, c, lv = shape
+    rng = np.random.default_rng(3)
+    nc = O.coeff_count(r, c, lv)
+    rows = []
+    # sparse signal + unit noise; pure noise; heavy signal
+    a = rng.standard_normal(nc); a[rng.random(nc) < 0.05] *= 20
+    rows.append(a)
+    rows.append(rng.standard_normal(nc))
+    b = rng.standard_normal(nc) * 0.3; b[rng.random(nc) < 0.3] += 50
+    rows.append(b)
+    co = np.stack(rows).astype(np.float32)
+    g = dev(co)
+    ks, ts, ep = hy.stages.sure(g, r, c, lv)
+    ks, ts, ep, soft = ks.cpu().numpy(), ts.cpu().numpy(), ep.cpu().numpy(), g.cpu().numpy()
+    for i in range(co.shape[0]):
+        res, offs = _oracle_sure_on(co[i], r, c, lv)
+        e_ref = 0.0
+        for j, sr in enumerate(res):
+            scale = offs[j + 1] - offs[j] + float(np.sum(co[i, offs[j]:offs[j + 1]].astype(np.float64) ** 2))
+            if sr.margin > 1e-9 * scale:
+                assert ks[i, j] == sr.k, (i, j, ks[i, j], sr.k, sr.margin)
+                assert ts[i, j] == np.float32(sr.t)
+            st = O.soft_threshold(co[i, offs[j]:offs[j + 1]].astype(np.float64), float(ts[i, j]))
+            assert np.max(np.abs(soft[i, offs[j]:offs[j + 1]] - st)) < 1e-5 * max(1.0, float(ts[i, j]))
+            e_ref += float(np.sum(st ** 2))
+        assert abs(ep[i] - e_ref) <= 1e-6 * max(1.0, e_ref)
+
+
+def test_sure_edge_cases(hy):
+    r, c, lv = 64, 64, 2
+    nc = O.coeff_count(r, c, lv)
+    rng = np.random.default_rng(4)
+    cases = [np.zeros(nc), np.full(nc, 0.5), np.full(nc, 7.0),
+             np.round(rng.standard_normal(nc) * 4) / 4,                  # many exact duplicates
+             np.where(rng.random(nc) < 0.5, 0.0, rng.standard_normal(nc))]
+    co = np.stack(cases).astype(np.float32)
+    ks, ts, ep = hy.stages.sure(dev(co), r, c, lv)
+    ks, ts = ks.cpu().numpy(), ts.cpu().numpy()
+    for i in range(co.shape[0]):
+        res, offs = _oracle_sure_on(co[i], r, c, lv)
+        for j, sr in enumerate(res):
+            scale = offs[j + 1] - offs[j] + float(np.sum(co[i, offs[j]:offs[j + 1]].astype(np.float64) ** 2))
+            if sr.margin > 1e-9 * scale:
+                assert ks[i, j] == sr.k and ts[i, j] == np.float32(sr.t), (i, j, ks[i, j], sr.k)
+
+
+def test_reconstruct_matches_fp64(hy):
+    rng = np.random.default_rng(5)
+    for b, n, r in [(224, 4096, 1), (32, 1001, 3), (200, 21025, 9), (17, 64, 17)]:
+        e = rng.standard_normal((r, n)).astype(np.float32)
+        u = rng.standard_normal((b, r)).astype(np.float32)
+        out = hy.stages.reconstruct(dev(e), dev(u)).cpu().numpy()
+        ref = u.astype(np.float64) @ e.astype(np.float64)
+        assert np.max(np.abs(out - ref)) / np.max(np.abs(ref)) < 1e-6
