@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""HyRes throughput benchmark (BASELINE.json metric: voxels/s and ms per cube).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config large]
+
+A step is one full HyRes pass (north_star stages (1)-(6)) over one synthetic
+cube resident in HBM.  Default workload: `large` (1024 x 1024 x 224 fp32, the
+north_star target; the cube is 940 MB, larger than the 126 MB L2, so no L2
+flush is needed between steps).  For N > 1 (torchrun, one rank per GPU) every
+rank denoises its own cube (seed = rank): independent problems, weak scaling,
+no data-path collective.
+
+Reports one JSON line (rank 0): value = whole-job voxels/s; e2e = the same
+metric through the C-ABI with HOST buffers (H2D + D2H inside the timed
+region); roofline = the dominant stage's algorithmic bytes / its CUDA-event
+duration vs MEASURED_PEAKS.json; cpu_baseline = the fp64 oracle on the host.
+`--impl reference` times the oracle itself (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from harness import synth  # noqa: E402
+
+METRIC = "HyRes voxels/sec and ms/cube"
+UNIT = "voxels/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), float(d.get("bf16_tflops", 1590.0)), "measured"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    """Polls SM clock and clock-event reasons every 20 ms in a thread."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, pci_bus_id: str | None):
+        self.samples = []
+        self.marks = []
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            if pci_bus_id:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(pci_bus_id.encode())
+            else:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(0)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                try:
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:  # noqa: BLE001
+                    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((time.perf_counter(), mhz, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def mark(self):
+        self.marks.append(time.perf_counter())
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "note": getattr(self, "err", "no samples")}
+        t0, t1 = (self.marks[0], self.marks[-1]) if len(self.marks) >= 2 else (0, float("inf"))
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        src = "timed region"
+        if len(inside) < 3:   # very short timed region: use warm-up + timed samples
+            inside = self.samples[-max(3, len(inside)):]
+            src = "warm-up + timed region (timed region shorter than 3 samples)"
+        mhz = [s[1] for s in inside]
+        reasons = set()
+        for s in inside:
+            for bit, name in self.REASONS.items():
+                if s[2] & bit:
+                    reasons.add(name)
+        return {"sm_mhz": float(statistics.median(mhz)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(reasons), "samples": len(inside), "window": src}
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+def stage_bytes(cfg, levels, rank, comps, chunks):
+    """Algorithmic HBM bytes per step for each stage: the minimum
+    each stage must move.  comps = candidate components projected/transformed."""
+    from oracle import hyres_ref as O  # geometry only (level shapes); not timed
+    n, b = cfg.rows * cfg.cols, cfg.bands
+    sh = O.level_shapes(cfg.rows, cfg.cols, levels)
+    nc = O.coeff_count(cfg.rows, cfg.cols, levels)
+    h, w = cfg.rows, cfg.cols
+    dwt_img = 0
+    for (hs, ws) in sh:
+        dwt_img += 4 * h * w + 4 * 4 * hs * ws     # read level input, write LL + 3 details
+        h, w = hs, ws
+    return {
+        "gram": 4 * n * b,
+        "project": chunks * 4 * n * b + 4 * n * comps,
+        "dwt": comps * dwt_img,
+        "sure": comps * 8 * nc,                     # read + in-place write of N_c coefficients
+        "idwt": rank * dwt_img,
+        "recon": 4 * n * rank + 4 * n * b,
+    }
+
+
+def cpu_baseline(cube, reps=2):
+    from oracle import hyres_ref as O
+    cores = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info
+        thr = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:  # noqa: BLE001
+        thr = cores
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.hyres(cube)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    return t, cores, thr
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return 0
+    s = synth.make_cube(cfg, 0)
+    cube = s.noisy
+    from oracle import hyres_ref as O
+    for _ in range(args.warmup):
+        O.hyres(cube)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.hyres(cube)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    v = cfg.voxels / t
+    cores = len(os.sched_getaffinity(0))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols, "bands": cfg.bands,
+                   "seed": 0},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"full {cfg.name} cube per step (oracle.hyres, numpy fp64, as it stands)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="large", choices=["tiny", "small", "medium", "wide", "large"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    cfg = synth.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2204_06979_b200 as hy
+
+    s = synth.make_cube(cfg, seed=rank)
+    cube_h = np.ascontiguousarray(s.noisy)
+    cube = torch.from_numpy(cube_h).cuda()
+    out = torch.empty_like(cube)
+    props = torch.cuda.get_device_properties(local)
+    bus = None
+    try:
+        bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+    except Exception:  # noqa: BLE001
+        pass
+    clk = ClockSampler(bus)
+    clk.start()
+
+    _, info = hy.hyres(cube, out, return_info=True)
+    for _ in range(args.warmup - 1):
+        hy.hyres(cube, out)
+    torch.cuda.synchronize()
+    hy.profile_enable(local, True)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = hy.launch_count(local)
+    clk.mark()
+    e0.record(st)
+    for _ in range(args.steps):
+        hy.hyres(cube, out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    clk.mark()
+    if world > 1:
+        dist.barrier()
+    launches = hy.launch_count(local) - launches0
+    stages = hy.profile_read(local)
+    hy.profile_enable(local, False)
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * cfg.voxels / (ms_max * 1e-3)
+
+    # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside ----
+    pin_in = torch.from_numpy(cube_h).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    hy.hyres_host(pin_in, pin_out, device=local)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        hy.hyres_host(pin_in, pin_out, device=local)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+    clk.stop()
+    csum = clk.summary()
+
+    # ---- roofline of the dominant stage ----
+    hbm, _, src = peaks()
+    rank_k = info["rank"]
+    chunks = info["chunks_run"]
+    comps = min(cfg.bands, chunks * 16) if chunks > 1 else min(16, cfg.bands)
+    sb = stage_bytes(cfg, info["levels"], rank_k, comps, chunks)
+    per = {}
+    for name, (tms, nl) in stages.items():
+        t = tms / args.steps
+        d = {"ms": round(t, 5), "launches_per_step": nl / args.steps}
+        if name in sb and t > 0:
+            gbs = sb[name] / (t * 1e-3) / 1e9
+            d.update({"bytes": sb[name], "GBps": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)})
+        per[name] = d
+    dws = sb["dwt"] + sb["sure"]
+    tds = (stages["dwt"][0] + stages["sure"][0]) / args.steps
+    per["dwt+sure"] = {"ms": round(tds, 5), "bytes": dws,
+                       "GBps": round(dws / (tds * 1e-3) / 1e9, 1) if tds > 0 else None,
+                       "frac_hbm": round(dws / (tds * 1e-3) / 1e9 / hbm, 4) if tds > 0 else None}
+    dom = max((k for k in stages), key=lambda k: stages[k][0])
+    if dom in sb:
+        t = stages[dom][0] / args.steps
+        ach = sb[dom] / (t * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                "peak_source": src, "share_of_step": round(t / ms_max, 4)}
+    else:   # eigensolver: fp64 ALU / latency bound, one CTA
+        t = stages[dom][0] / args.steps
+        B = cfg.bands
+        flops = (B ** 3) + (4.0 / 3.0) * B ** 3     # sweep (B^3/2 FMA) + tridiagonalisation (2/3 B^3 FMA)
+        peak_sm = 64 * 2 * 1.965e9 / 1e12            # one SM: 64 fp64 FMA/clk at 1965 MHz
+        ach = flops / (t * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 4), "peak": round(peak_sm, 4),
+                "unit": "TFLOP/s", "frac": round(ach / peak_sm, 4), "traffic": None,
+                "peak_source": "derived: one SM x 64 DFMA/clk x 1965 MHz (single-CTA kernel)",
+                "share_of_step": round(t / ms_max, 4)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "ms_per_cube": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols,
+                   "bands": cfg.bands, "seeds": f"rank r uses seed r (0..{world - 1})",
+                   "l2": (f"inputs larger than L2 (cube {cube_h.nbytes / 1e6:.0f} MB > 126 MB L2); no flush"
+                          if cube_h.nbytes > 126e6 else "cube fits in L2: steps run back to back (L2-warm)"),
+                   "rank": rank_k, "levels": info["levels"], "chunks": chunks},
+        "roofline": roof,
+        "stages": per,
+        "e2e": {"value": world * cfg.voxels / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(cube_h.nbytes), "d2h_bytes_per_step": int(cube_h.nbytes),
+                "ms_per_step": e2e_s * 1e3, "path": "hyde_hyres_host (pinned host buffers)"},
+        "gpu_launches": int(launches),
+        "clocks": csum,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        t, cores, thr = cpu_baseline(cube_h, reps=2)
+        line["cpu_baseline"] = {"value": cfg.voxels / t, "unit": UNIT, "cores": cores, "threads": thr,
+                                "kind": "oracle",
+                                "sample": f"2 full {cfg.name} cubes, oracle.hyres (numpy fp64), mean time"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -162,6 +162,27 @@ hyde_status hyde_k_idwt(hyde_handle h, const float* coeffs, int count, int rows,
 hyde_status hyde_k_reconstruct(hyde_handle h, const float* E, int n_pixels, int bands,
                                const float* U, int ldu, int rank, float* out,
                                hyde_stream_t stream);
+/* --- Stage timing (diagnostics; bench.py's roofline).  When enabled, the
+ * library records CUDA events on the call's stream around each stage of every
+ * subsequent call.  hyde_profile_read synchronizes the device, adds the
+ * elapsed time of every recorded stage to ms[stage] and the number of kernels
+ * launched in it to launches[stage] (arrays of HYDE_NSTAGES), and clears the
+ * records.  hyde_launch_count: kernels this handle launched since creation. */
+enum {
+  HYDE_STAGE_GRAM = 0,     /* K1: G = Y Y^T                       (A1)   */
+  HYDE_STAGE_EIG = 1,      /* K2: sigma, whitening, eigenpairs   (A1-A2) */
+  HYDE_STAGE_PROJECT = 2,  /* K3: eigen-images                   (A3)   */
+  HYDE_STAGE_DWT = 3,      /* K4: forward DWT levels             (A4)   */
+  HYDE_STAGE_SURE = 4,     /* K5: SURE + soft threshold          (A5)   */
+  HYDE_STAGE_RANK = 5,     /* rank decision + 16-byte D2H        (A5)   */
+  HYDE_STAGE_IDWT = 6,     /* K6a: inverse DWT                   (A6)   */
+  HYDE_STAGE_RECON = 7,    /* K6b: reconstruction to bands       (A6)   */
+  HYDE_NSTAGES = 8
+};
+hyde_status hyde_profile_enable(hyde_handle h, int on);
+hyde_status hyde_profile_read(hyde_handle h, double* ms, long long* launches);
+long long hyde_launch_count(hyde_handle h);
+
 /* Analysis low-pass filter the kernels use (host, fp64; taps values). */
 hyde_status hyde_filter(int taps, double* h_out);
 

@@ -143,3 +143,22 @@ def workspace_size(rows, cols, bands, batch=1, chunk=16, taps=16, levels=0) -> i
 
 
 from . import stages  # noqa: E402
+
+
+def profile_enable(device: int = 0, on: bool = True) -> None:
+    """Record per-stage CUDA events on subsequent calls (see include/hyde.h HYDE_STAGE_*)."""
+    h = handle(device)
+    check(lib().hyde_profile_enable(h, 1 if on else 0), h)
+
+
+def profile_read(device: int = 0):
+    """Synchronize and return {stage: (ms, kernel launches)} accumulated since the last read."""
+    h = handle(device)
+    ms = (ctypes.c_double * 8)()
+    nl = (ctypes.c_longlong * 8)()
+    check(lib().hyde_profile_read(h, ms, nl), h)
+    return {name: (ms[i], nl[i]) for i, name in enumerate(_lib.STAGES)}
+
+
+def launch_count(device: int = 0) -> int:
+    return int(lib().hyde_launch_count(handle(device)))

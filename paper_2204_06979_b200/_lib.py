@@ -15,6 +15,7 @@ HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "hyde.h")
 
 HYDE_OK, HYDE_EPARAM, HYDE_EDATA, HYDE_EMETHOD, HYDE_ECUDA, HYDE_ENCCL, HYDE_ENOMEM = 0, 2, 3, 4, 5, 6, 7
 HYDE_KEEP_LL = 1
+STAGES = ("gram", "eig", "project", "dwt", "sure", "rank", "idwt", "recon")
 
 
 class HydeError(RuntimeError):
@@ -63,6 +64,9 @@ _SIGS = {
     "hyde_k_idwt": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, c_void_p]),
     "hyde_k_reconstruct": (c_int, [c_void_p, _P, c_int, c_int, _P, c_int, c_int, _P, c_void_p]),
     "hyde_filter": (c_int, [c_int, POINTER(c_double)]),
+    "hyde_profile_enable": (c_int, [c_void_p, c_int]),
+    "hyde_profile_read": (c_int, [c_void_p, POINTER(c_double), POINTER(ctypes.c_longlong)]),
+    "hyde_launch_count": (ctypes.c_longlong, [c_void_p]),
 }
 
 _lib = None

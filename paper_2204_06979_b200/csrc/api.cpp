@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -88,7 +89,43 @@ struct hyde_ctx {
   float* dev_out = nullptr;
   size_t dev_io_cap = 0;
   RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
+  // stage profiling
+  int prof = 0;
+  struct Rec { int stage; int launches; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  long long launch_total = 0;
+  long long launch_by_stage[HYDE_NSTAGES] = {0};
+  cudaEvent_t ev() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
 };
+
+namespace {
+// Marks one stage on `st`: counts its kernel launches and, when profiling is
+// on, brackets it with CUDA events.
+struct Stage {
+  hyde_ctx* h;
+  int stage, launches;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  Stage(hyde_ctx* h_, int s, int nl, cudaStream_t st_) : h(h_), stage(s), launches(nl), st(st_) {
+    if (h->prof) { a = h->ev(); cudaEventRecord(a, st); }
+  }
+  void end() {
+    h->launch_total += launches;
+    h->launch_by_stage[stage] += launches;
+    if (h->prof) {
+      cudaEvent_t b = h->ev();
+      cudaEventRecord(b, st);
+      h->recs.push_back({stage, launches, a, b});
+    }
+  }
+};
+}  // namespace
 
 hyde_status hyde_cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   char buf[512];
@@ -277,6 +314,8 @@ hyde_status hyde_destroy(hyde_handle h) {
     if (h->dev_in) cudaFree(h->dev_in);
     if (h->dev_out) cudaFree(h->dev_out);
     if (h->rs_host) cudaFreeHost(h->rs_host);
+    for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : h->pool) cudaEventDestroy(e);
   }
   delete h;
   return HYDE_OK;
@@ -342,9 +381,17 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   float* W = (float*)(ws + L.W);
   float* U = (float*)(ws + L.U);
   float* C = (float*)(ws + L.C);
-  CK(launch_gram(cube, n, B, (double*)(ws + L.partial), L.nsplit, G, &rs->nonfinite, st));
+  {
+    Stage sg(h, HYDE_STAGE_GRAM, 2, st);
+    CK(launch_gram(cube, n, B, (double*)(ws + L.partial), L.nsplit, G, &rs->nonfinite, st));
+    sg.end();
+  }
   const int first = p.chunk < B ? p.chunk : B;
-  CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
+  {
+    Stage sg(h, HYDE_STAGE_EIG, 1, st);
+    CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
+    sg.end();
+  }
   int rank = 0, chunks = 0;
   for (int c = 0;; ++c) {
     const int k0 = c * p.chunk;
@@ -352,29 +399,55 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     if (c > 0) {
       s = ensure_ebuf(h, (size_t)(k0 + cnt) * L.ldE * 4, (size_t)k0 * L.ldE * 4, st);
       if (s != HYDE_OK) return s;
+      Stage sg(h, HYDE_STAGE_EIG, 1, st);
       CK(launch_eigvec_more(tri, house, sigma, B, k0, cnt, nullptr, nullptr, W, U, L.ldwu, st));
+      sg.end();
     }
     float* E = h->ebuf + (size_t)k0 * L.ldE;
-    CK(launch_project(cube, n, B, W + k0, L.ldwu, cnt, E, L.ldE, st));
-    CK(dwt_forward(L, ws, E, L.ldE, cnt, fb, st));
-    CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
-                   (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, st));
-    CK(launch_rank_decide((double*)(ws + L.esub), L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs,
-                          (double*)(ws + L.epost), st));
-    CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
+    {
+      Stage sg(h, HYDE_STAGE_PROJECT, 1, st);
+      CK(launch_project(cube, n, B, W + k0, L.ldwu, cnt, E, L.ldE, st));
+      sg.end();
+    }
+    {
+      Stage sg(h, HYDE_STAGE_DWT, levels, st);
+      CK(dwt_forward(L, ws, E, L.ldE, cnt, fb, st));
+      sg.end();
+    }
+    {
+      Stage sg(h, HYDE_STAGE_SURE, 1, st);
+      CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
+                     (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, st));
+      sg.end();
+    }
+    {
+      Stage sg(h, HYDE_STAGE_RANK, 1, st);
+      CK(launch_rank_decide((double*)(ws + L.esub), L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs,
+                            (double*)(ws + L.epost), st));
+      CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
+      sg.end();
+    }
     CK(cudaStreamSynchronize(st));
     ++chunks;
     const RankState r = *h->rs_host;
     if (r.nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
     if (r.sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
     const int kept = r.found ? (r.rank - k0) : cnt;
-    if (kept > 0) CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, st));
+    if (kept > 0) {
+      Stage sg(h, HYDE_STAGE_IDWT, levels, st);
+      CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, st));
+      sg.end();
+    }
     if (r.found) {
       rank = r.rank;
       break;
     }
   }
-  CK(launch_reconstruct(h->ebuf, L.ldE, n, B, U, L.ldwu, rank, out, st));
+  {
+    Stage sg(h, HYDE_STAGE_RECON, (rank + 7) / 8, st);
+    CK(launch_reconstruct(h->ebuf, L.ldE, n, B, U, L.ldwu, rank, out, st));
+    sg.end();
+  }
   if (info) {
     memset(info, 0, sizeof(*info));
     info->rank = rank;
@@ -385,6 +458,35 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   }
   return HYDE_OK;
 }
+
+hyde_status hyde_profile_enable(hyde_handle h, int on) {
+  if (!h) return HYDE_EPARAM;
+  DeviceGuard g(h->device);
+  CK(cudaDeviceSynchronize());
+  for (auto& r : h->recs) { h->pool.push_back(r.a); h->pool.push_back(r.b); }
+  h->recs.clear();
+  h->prof = on ? 1 : 0;
+  return HYDE_OK;
+}
+
+hyde_status hyde_profile_read(hyde_handle h, double* ms, long long* launches) {
+  if (!h || !ms) return HYDE_EPARAM;
+  DeviceGuard g(h->device);
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < HYDE_NSTAGES; ++i) { ms[i] = 0.0; if (launches) launches[i] = 0; }
+  for (auto& r : h->recs) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.stage] += t;
+    if (launches) launches[r.stage] += r.launches;
+    h->pool.push_back(r.a);
+    h->pool.push_back(r.b);
+  }
+  h->recs.clear();
+  return HYDE_OK;
+}
+
+long long hyde_launch_count(hyde_handle h) { return h ? h->launch_total : 0; }
 
 hyde_status hyde_hyres(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
                        hyde_stream_t stream) {

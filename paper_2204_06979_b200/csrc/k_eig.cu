@@ -137,7 +137,8 @@ __device__ void bisect_eigs(const double* d, const double* e2, int n, double glo
 __device__ void inv_iter(const double* d, const double* e, int n, double lam, double tnorm,
                          double* x, double* dd, double* u1, double* u2, double* ml,
                          unsigned char* piv, unsigned seed) {
-  const double tiny = 2.220446049250313e-16 * tnorm + 1e-300;
+  // pivot floor eps ||T|| (for T == 0 every vector is an eigenvector: floor 1)
+  const double tiny = tnorm > 0.0 ? 2.220446049250313e-16 * tnorm : 1.0;
   // factorise T - lam I = P L U (U has two super-diagonals)
   double a = d[0] - lam, b = (n > 1) ? e[0] : 0.0;
   for (int i = 0; i < n - 1; ++i) {
@@ -180,8 +181,11 @@ __device__ void inv_iter(const double* d, const double* e, int n, double lam, do
     x[n - 1] /= dd[n - 1];
     if (n > 1) x[n - 2] = (x[n - 2] - u1[n - 2] * x[n - 1]) / dd[n - 2];
     for (int i = n - 3; i >= 0; --i) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) / dd[i];
+    double mx = 0.0;
+    for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(x[i]));
+    mx = 1.0 / mx;                       // scale before squaring: no overflow
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += x[i] * x[i];
+    for (int i = 0; i < n; ++i) { x[i] *= mx; s += x[i] * x[i]; }
     s = 1.0 / sqrt(s);
     for (int i = 0; i < n; ++i) x[i] *= s;
   }
