@@ -24,7 +24,8 @@ struct Layout {
   int B, chunk, nsplit, nsub, ldwu, taps, levels;
   long long n, ldE;
   DwtPlan plan;
-  size_t G, partial, sigma, lam, tri, house, W, U, C, S1, S2, kstar, tstar, esub, epost, rs, total;
+  size_t G, partial, amax, sigma, lam, tri, house, W, U, C, S1, S2, kstar, tstar, esub, epost, rs, total;
+  int use_tc, npairs;
   size_t s1_img, s2_img;  // per-image strides (floats) of the LL scratch
 };
 
@@ -36,6 +37,8 @@ void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Lay
   L->n = (long long)rows * cols;
   L->ldE = (L->n + 63) / 64 * 64;
   L->nsplit = gram_nsplit(L->n, B);
+  L->use_tc = gram_tc_supported(B) ? 1 : 0;
+  L->npairs = gram_tc_npairs(L->n);
   L->ldwu = B;
   hyde_make_plan(rows, cols, levels, &L->plan);
   L->nsub = 3 * levels + 1;
@@ -43,7 +46,8 @@ void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Lay
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += al(bytes); return o; };
   L->G = take((size_t)B * B * 8);
-  L->partial = take((size_t)L->nsplit * B * B * 8);
+  L->partial = take((size_t)(L->nsplit > L->npairs ? L->nsplit : L->npairs) * B * B * 8);
+  L->amax = take((size_t)B * 4);
   L->sigma = take((size_t)B * 8);
   L->lam = take((size_t)B * 8);
   L->tri = take((size_t)(3 * B + 8) * 8);
@@ -211,6 +215,15 @@ static hyde_status resolve_params(hyde_handle h, int rows, int cols, const hyde_
     return fail(h, HYDE_EPARAM, "levels impossible for this image size (SPEC.md:122)");
   *levels = lv;
   return HYDE_OK;
+}
+
+// K1: exact int8 tensor-core Gram (B <= 224) or the fp64 SIMT fallback
+static cudaError_t run_gram(const Layout& L, char* ws, const float* cube, double* G, int* nonfinite,
+                            cudaStream_t st) {
+  if (L.use_tc)
+    return launch_gram_tc(cube, L.n, L.B, (unsigned*)(ws + L.amax), (double*)(ws + L.partial), L.npairs, G,
+                          nonfinite, st);
+  return launch_gram(cube, L.n, L.B, (double*)(ws + L.partial), L.nsplit, G, nonfinite, st);
 }
 
 // forward DWT of `count` images at E (stride ldE) into C (stride N_c)
@@ -382,8 +395,8 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   float* U = (float*)(ws + L.U);
   float* C = (float*)(ws + L.C);
   {
-    Stage sg(h, HYDE_STAGE_GRAM, 2, st);
-    CK(launch_gram(cube, n, B, (double*)(ws + L.partial), L.nsplit, G, &rs->nonfinite, st));
+    Stage sg(h, HYDE_STAGE_GRAM, L.use_tc ? 3 : 2, st);
+    CK(run_gram(L, ws, cube, G, &rs->nonfinite, st));
     sg.end();
   }
   const int first = p.chunk < B ? p.chunk : B;
@@ -550,7 +563,7 @@ hyde_status hyde_estimate_noise(hyde_handle h, const float* cube, int rows, int 
   h->last_rs = rs;
   CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
   double* G = gram_out ? gram_out : (double*)(ws + L.G);
-  CK(launch_gram(cube, L.n, bands, (double*)(ws + L.partial), L.nsplit, G, &rs->nonfinite, st));
+  CK(run_gram(L, ws, cube, G, &rs->nonfinite, st));
   CK(launch_noise_eig(G, L.n, bands, 1e-6, -1, 0, sigma_out, nullptr, nullptr, (double*)(ws + L.house),
                       (double*)(ws + L.tri), (float*)(ws + L.W), (float*)(ws + L.U), L.ldwu, st));
   if (noise_out)
@@ -571,7 +584,7 @@ hyde_status hyde_k_gram(hyde_handle h, const float* cube, int n_pixels, int band
   RankState* rs = (RankState*)(h->ws + L.rs);
   h->last_rs = rs;
   CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
-  CK(launch_gram(cube, L.n, bands, (double*)(h->ws + L.partial), L.nsplit, gram, &rs->nonfinite, st));
+  CK(run_gram(L, h->ws, cube, gram, &rs->nonfinite, st));
   return HYDE_OK;
 }
 

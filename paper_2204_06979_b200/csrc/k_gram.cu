@@ -6,7 +6,8 @@
 // the Gram's relative error by roughly the band SNR (SURVEY.md §7 hard part
 // 1), so the sums must be far more accurate than an fp32 accumulation.
 //
-// This kernel (v1) is the fp64 SIMT formulation: 64x64 output blocks (upper
+// This kernel is the fp64 SIMT formulation (fallback for B > 224; the
+// tensor-core path is k_gram_tc.cu): 64x64 output blocks (upper
 // block triangle only), the pixel axis split into `nsplit`
 // slices whose fp64 partial Grams are summed in a fixed order by a second
 // kernel, so the result is bit-deterministic.  It also raises the device
@@ -113,6 +114,11 @@ cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int
   per = (per + TP - 1) / TP * TP;
   dim3 grid(pairs, nsplit);
   gram_partial_kernel<<<grid, 256, 0, st>>>(Y, n, B, nb, partial, per, nonfinite);
+  return launch_gram_reduce(partial, nsplit, B, G, st);
+}
+
+// G[i][j] = sum over slices of partial[slice][min(i,j)][max(i,j)], fixed order
+cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st) {
   long long tot = (long long)B * B;
   gram_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, nsplit, B, G);
   return cudaGetLastError();

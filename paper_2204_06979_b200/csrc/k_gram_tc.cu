@@ -1,0 +1,374 @@
+// K1 (north_star stage (1)) on the 5th-generation tensor
+// cores: an EXACT integer Gram of a quantised cube, G = diag(s) Q Q^T diag(s).
+//
+// Why integers (DESIGN.md §4 K1): sigma_b^2 = 1/(N [(G+dI)^-1]_bb) amplifies
+// the Gram's relative error by ~the band SNR, so G must be good to ~1e-7
+// relative; fp32 (or TF32/BF16-split) accumulation over 10^6 pixels is not,
+// and any non-PSD rounding breaks noiseless cubes.  Here each band b is
+// scaled by inv_s_b = 16256 / max|y_b| (max from a pre-pass) and rounded:
+// q = rint(y inv_s) in [-16256, 16256], split q = 128 S0 + S1 with S0 in
+// [-127, 127], S1 in [-64, 63] (both int8).  Then
+//   Q Q^T = 16384 S0 S0^T + 128 (S0 S1^T + S1 S0^T) + S1 S1^T
+// three int8 x int8 -> int32 GEMMs (tcgen05.mma kind::i8), accumulated
+// EXACTLY in TMEM; G is Q Q^T scaled by s_a s_b in fp64.  The result is the
+// exact Gram of a 15-bit quantisation of the cube: symmetric PSD by
+// construction, deterministic, and ~1e-6 from the fp64 oracle end to end
+// (survey/design experiment: /tmp-free numbers in DESIGN.md).
+//
+// Structure: clusters of 2 CTAs (one SM pair) per pixel range, cta_group::2
+// MMAs with M = 128 (64 rows per SM, TMEM "2x2" layout).  Bands are split
+// S_a = [0,128), S_b = [128,B); three tiles T_aa (128 x 128), T_ab (128 x Nb),
+// T_bb (128 x Nb), Nb = B-128 rounded up to 32; x 3 products = 480 of 512
+// TMEM columns for B <= 224.  16 converter warps per CTA load fp32 straight
+// from HBM (16-byte loads, ~90 KB in flight per SM), quantise and write the
+// int8 slices into shared memory in the UMMA canonical K-major layout; one
+// thread of the leader CTA issues the MMAs; the stage ring is released by
+// tcgen05.commit multicast to both CTAs.  Each CTA finally reads its TMEM,
+// combines the three products in int64 and writes its fp64 partial Gram.
+#include "common.cuh"
+#include "tc_util.cuh"
+
+namespace {
+
+constexpr int KC = 128;        // pixels (bytes per int8 row) per stage
+constexpr int NI = 4;          // int8 stages
+constexpr int NCW = 16;        // converter warps
+constexpr int NTHREADS = (NCW + 2) * 32;
+constexpr int MAXU = 12;       // max units per converter warp per stage
+constexpr int TMEM_COLS = 512;
+
+struct GramTc {
+  const float* Y;
+  long long n;
+  int B;
+  int nb;           // Nb (0 when B <= 128)
+  int rows_tot;     // 64 + 64 + nb/2 (or 64)
+  long long per_pair;
+  const unsigned* amax_bits;
+  double* partial;  // [pair][B][B]
+  int* nonfinite;
+};
+
+// smem regions of one int8 slice of a stage: P (64 rows), QA (64 rows), QB (nb/2 rows)
+__device__ __forceinline__ int region_rows(int rg, int nb) { return rg == 2 ? nb / 2 : 64; }
+__device__ __forceinline__ int region_base(int rg) { return rg * 64 * KC; }
+
+__device__ __forceinline__ int band_of(int region, int r, int rank, int B, int nb) {
+  int b;
+  if (region == 0) b = rank * 64 + r;                       // P : S_a rows of this SM
+  else if (region == 1) b = 128 + rank * 64 + r;            // QA: S_b rows of this SM (T_bb A)
+  else b = 128 + rank * (nb / 2) + r;                       // QB: S_b B-operand half
+  const int lim = region == 0 ? (B < 128 ? B : 128) : B;
+  return b < lim ? b : -1;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    gram_tc_kernel(GramTc P) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar_full[NI];
+  __shared__ __align__(8) uint64_t bar_empty[NI];
+  __shared__ __align__(8) uint64_t bar_done;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float inv_s[3][64];
+  __shared__ double s_of[3][64];
+
+  const int rank = (int)tc::cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int B = P.B, nb = P.nb;
+  const int nreg = B > 128 ? 3 : 1;
+  const int slice_bytes = P.rows_tot * KC;
+  const int stage_bytes = 2 * slice_bytes;
+  const long long p_begin = (long long)pair * P.per_pair;
+  const long long p_end = min(P.n, p_begin + P.per_pair);
+  const int nst = p_end > p_begin ? (int)((p_end - p_begin + KC - 1) / KC) : 0;
+
+  // per-band quantisation scales of the rows this SM handles
+  for (int i = threadIdx.x; i < 3 * 64; i += NTHREADS) {
+    const int rg = i / 64, r = i % 64;
+    float is = 0.f;
+    double sv = 0.0;
+    if (rg < nreg && r < region_rows(rg, nb)) {
+      const int b = band_of(rg, r, rank, B, nb);
+      if (b >= 0) {
+        const float m = __uint_as_float(P.amax_bits[b]);
+        is = m > 0.f ? fminf((float)(16256.0 / (double)m), 1e30f) : 1.f;
+        sv = 1.0 / (double)is;
+      }
+    }
+    inv_s[rg][r] = is;
+    s_of[rg][r] = sv;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NI; ++i) {
+      tc::mbar_init(&bar_full[i], 2 * NCW);
+      tc::mbar_init(&bar_empty[i], 1);
+    }
+    tc::mbar_init(&bar_done, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) {
+    tc::tmem_alloc<2>(&tmem_base_sh, TMEM_COLS);
+    tc::tmem_relinquish<2>();
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  // TMEM column map per product level: T_aa 64 cols, T_ab nb/2, T_bb nb/2
+  const int CL = 64 + nb;
+  const int off_ab = 64, off_bb = 64 + nb / 2;
+
+  if (warp == 1) {
+    // ================= MMA issuer (leader CTA, one thread) =================
+    if (rank == 0 && lane == 0 && nst > 0) {
+      const uint32_t id_aa = tc::idesc_i8(128, 128);
+      const uint32_t id_b = nb > 0 ? tc::idesc_i8(128, nb) : 0u;
+      const uint32_t sbase = tc::smem_u32(smem);
+      for (int s = 0; s < nst; ++s) {
+        const int is = s % NI;
+        tc::mbar_wait_cluster(&bar_full[is], (uint32_t)((s / NI) & 1));
+        tc::tc_fence_after();
+        const uint32_t st0 = sbase + is * stage_bytes;   // S0 slice
+        const uint32_t st1 = st0 + slice_bytes;           // S1 slice
+        for (int ks = 0; ks < KC / 32; ++ks) {
+          auto dsc = [&](uint32_t slice, int rg, int row0) -> uint64_t {
+            const int R = region_rows(rg, nb);
+            return tc::sdesc_kmajor_noswz(slice + region_base(rg) + ks * 2 * R * 16 + (row0 / 8) * 128, R * 16, 128);
+          };
+          const uint32_t first = (s == 0 && ks == 0) ? 0u : 1u;
+          // T_aa: A = P, B = P
+          tc::mma_i8<2>(tmem + 0 * CL, dsc(st0, 0, 0), dsc(st0, 0, 0), id_aa, first);
+          tc::mma_i8<2>(tmem + 1 * CL, dsc(st0, 0, 0), dsc(st1, 0, 0), id_aa, first);
+          tc::mma_i8<2>(tmem + 1 * CL, dsc(st1, 0, 0), dsc(st0, 0, 0), id_aa, 1u);
+          tc::mma_i8<2>(tmem + 2 * CL, dsc(st1, 0, 0), dsc(st1, 0, 0), id_aa, first);
+          if (nb > 0) {
+            // T_ab: A = P, B = QB ; T_bb: A = QA, B = QB
+            tc::mma_i8<2>(tmem + 0 * CL + off_ab, dsc(st0, 0, 0), dsc(st0, 2, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st0, 0, 0), dsc(st1, 2, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st1, 0, 0), dsc(st0, 2, 0), id_b, 1u);
+            tc::mma_i8<2>(tmem + 2 * CL + off_ab, dsc(st1, 0, 0), dsc(st1, 2, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 0 * CL + off_bb, dsc(st0, 1, 0), dsc(st0, 2, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1, 0), dsc(st1, 2, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st1, 1, 0), dsc(st0, 2, 0), id_b, 1u);
+            tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1, 0), dsc(st1, 2, 0), id_b, first);
+          }
+        }
+        tc::mma_commit<2>(&bar_empty[is], 0x3);
+      }
+      tc::mma_commit<2>(&bar_done, 0x3);
+    }
+  } else if (warp >= 2) {
+    // ================= converters: HBM fp32 -> int8 slices in smem ==========
+    const int cw = warp - 2;
+    constexpr int cols16 = KC / 16;
+    // units of work = (region, 8-row group, 16-pixel column); regions P, QA hold 64 rows
+    const int nunits = nreg == 1 ? 8 * cols16 : (16 + nb / 16) * cols16;
+    const bool vec_ok = (P.n % 4 == 0) && (((uintptr_t)P.Y & 15) == 0);
+    bool bad = false;
+    for (int s = 0; s < nst; ++s) {
+      const int is = s % NI;
+      const long long p0 = p_begin + (long long)s * KC;
+      float4 v[MAXU];
+      int ucount = 0;
+      // issue all loads of this warp's units first (memory-level parallelism)
+#pragma unroll
+      for (int t = 0; t < MAXU; ++t) {
+        const int u = cw + t * NCW;
+        v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u < nunits) {
+          const int rg = u < 8 * cols16 ? 0 : (u < 16 * cols16 ? 1 : 2);
+          const int uu = u - rg * 8 * cols16;
+          const int g = uu / cols16, c = uu % cols16;
+          const int r = g * 8 + (lane >> 2);
+          const int b = band_of(rg, r, rank, B, nb);
+          const long long px = p0 + c * 16 + (lane & 3) * 4;
+          if (b >= 0) {
+            const float* src = P.Y + (long long)b * P.n + px;
+            if (vec_ok && px + 3 < p_end) {
+              v[t] = __ldcs(reinterpret_cast<const float4*>(src));
+            } else {
+              v[t].x = px < p_end ? src[0] : 0.f;
+              v[t].y = px + 1 < p_end ? src[1] : 0.f;
+              v[t].z = px + 2 < p_end ? src[2] : 0.f;
+              v[t].w = px + 3 < p_end ? src[3] : 0.f;
+            }
+          }
+          ucount = t + 1;
+        }
+      }
+      tc::mbar_wait_cluster(&bar_empty[is], (uint32_t)(((s / NI) & 1) ^ 1));
+      unsigned char* st0 = smem + is * stage_bytes;
+      unsigned char* st1 = st0 + slice_bytes;
+#pragma unroll
+      for (int t = 0; t < MAXU; ++t) {
+        if (t >= ucount) break;
+        const int u = cw + t * NCW;
+        const int rg = u < 8 * cols16 ? 0 : (u < 16 * cols16 ? 1 : 2);
+        const int uu = u - rg * 8 * cols16;
+        const int g = uu / cols16, c = uu % cols16;
+        const int r = g * 8 + (lane >> 2);
+        const float isc = inv_s[rg][r];
+        const float x[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
+        uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          bad |= !isfinite(x[j]);
+          // q = rint(x * inv_s) via the 1.5*2^23 rounding constant (exact RN of the product)
+          const float qf = fmaf(x[j], isc, 12582912.0f);
+          const int q = __float_as_int(qf) - 0x4B400000;
+          const int h = (q + 64) >> 7;            // S0 in [-127, 127]
+          const int l = q - (h << 7);             // S1 in [-64, 63]
+          w0 |= (uint32_t)(h & 0xFF) << (8 * j);
+          w1 |= (uint32_t)(l & 0xFF) << (8 * j);
+        }
+        // canonical K-major layout: core matrix (8 rows x 16 B) per (row group, 16-px column)
+        const int off = region_base(rg) + c * (region_rows(rg, nb) * 16) + g * 128 + (lane >> 2) * 16 + (lane & 3) * 4;
+        *reinterpret_cast<uint32_t*>(st0 + off) = w0;
+        *reinterpret_cast<uint32_t*>(st1 + off) = w1;
+      }
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(&bar_full[is], 0);
+    }
+    if (bad) atomicOr(P.nonfinite, 1);
+
+    // ================= epilogue: TMEM -> exact int64 -> fp64 partial ========
+    if (cw < 4) {
+      const int q4 = warp & 3;                    // TMEM lane quadrant of this warp
+      const int L = q4 * 32 + lane;               // TMEM lane = this thread's row slot
+      const int m = L & 63, half = L >> 6;
+      double* Pp = P.partial + (long long)pair * B * B;
+      if (nst > 0) {
+        tc::mbar_wait_cluster(&bar_done, 0);
+        tc::tc_fence_after();
+      }
+      const int ntile = nb > 0 ? 3 : 1;
+      for (int t = 0; t < ntile; ++t) {
+        const int Nt = t == 0 ? 128 : nb;
+        const int coff = t == 0 ? 0 : (t == 1 ? off_ab : off_bb);
+        // row band i and its scale; column bands j
+        const int rg_i = t == 2 ? 1 : 0;
+        const int bi = band_of(rg_i, m, rank, B, nb);
+        const double si = bi >= 0 ? s_of[rg_i][m] : 0.0;
+        for (int c0 = 0; c0 < Nt / 2; c0 += 16) {
+          uint32_t a0[16], a1[16], a2[16];
+          const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + coff + c0;
+          if (nst > 0) {
+            tc::tmem_ld16(ta + 0 * CL, a0);
+            tc::tmem_ld16(ta + 1 * CL, a1);
+            tc::tmem_ld16(ta + 2 * CL, a2);
+            tc::tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) a0[j] = a1[j] = a2[j] = 0u;
+          }
+          if (bi < 0) continue;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int nn = c0 + j + (Nt / 2) * half;    // column within the tile
+            int bj;
+            double sj;
+            if (t == 0) {
+              bj = nn < (B < 128 ? B : 128) ? nn : -1;
+              sj = 0.0;
+            } else {
+              bj = 128 + nn < B ? 128 + nn : -1;
+              sj = 0.0;
+            }
+            if (bj < 0) continue;
+            const float m_j = __uint_as_float(P.amax_bits[bj]);
+            const float isj = m_j > 0.f ? fminf((float)(16256.0 / (double)m_j), 1e30f) : 1.f;
+            sj = 1.0 / (double)isj;
+            const long long qq = 16384LL * (long long)(int)a0[j] + 128LL * (long long)(int)a1[j] +
+                                 (long long)(int)a2[j];
+            Pp[(long long)bi * B + bj] = (double)qq * si * sj;
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<2>(tmem, TMEM_COLS);
+  }
+}
+
+__global__ void amax_kernel(const float* __restrict__ Y, long long n, unsigned* amax_bits, int* nonfinite) {
+  const int b = blockIdx.y;
+  const float* row = Y + (long long)b * n;
+  unsigned m = 0;
+  bool bad = false;
+  const bool vec = (n % 4 == 0) && (((uintptr_t)Y & 15) == 0);
+  if (vec) {
+    const long long n4 = n / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+      float4 v = __ldcs(reinterpret_cast<const float4*>(row) + i);
+      m = max(m, __float_as_uint(fabsf(v.x)));
+      m = max(m, __float_as_uint(fabsf(v.y)));
+      m = max(m, __float_as_uint(fabsf(v.z)));
+      m = max(m, __float_as_uint(fabsf(v.w)));
+    }
+  } else {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+      m = max(m, __float_as_uint(fabsf(__ldcs(row + i))));
+  }
+  bad = m >= 0x7F800000u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&amax_bits[b], m);
+  if (bad) atomicOr(nonfinite, 1);
+}
+
+}  // namespace
+
+bool gram_tc_supported(int B) { return B >= 1 && B <= 224; }
+
+int gram_tc_npairs(long long n) {
+  long long np = (n + 4LL * KC - 1) / (4LL * KC);
+  if (np > 74) np = 74;
+  if (np < 1) np = 1;
+  long long per = (n + np - 1) / np;
+  if (per > 100000) {
+    np = (n + 99999) / 100000;
+    per = (n + np - 1) / np;
+  }
+  per = (per + KC - 1) / KC * KC;
+  np = (n + per - 1) / per;
+  return (int)np;
+}
+
+cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
+                           double* G, int* nonfinite, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(amax_bits, 0, (size_t)B * sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  {
+    long long per_block = 256LL * 4 * 8;
+    unsigned gx = (unsigned)((n + per_block - 1) / per_block);
+    if (gx > 64) gx = 64;
+    if (gx < 1) gx = 1;
+    amax_kernel<<<dim3(gx, B), 256, 0, st>>>(Y, n, amax_bits, nonfinite);
+  }
+  GramTc P;
+  P.Y = Y;
+  P.n = n;
+  P.B = B;
+  P.nb = B > 128 ? ((B - 128 + 31) / 32) * 32 : 0;
+  P.rows_tot = B > 128 ? 128 + P.nb / 2 : 64;
+  long long per = (n + npairs - 1) / npairs;
+  per = (per + KC - 1) / KC * KC;
+  P.per_pair = per;
+  P.amax_bits = amax_bits;
+  P.partial = partial;
+  P.nonfinite = nonfinite;
+  const size_t smem = (size_t)NI * 2 * P.rows_tot * KC;
+  e = cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  gram_tc_kernel<<<2 * npairs, NTHREADS, smem, st>>>(P);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_gram_reduce(partial, npairs, B, G, st);
+}
