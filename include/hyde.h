@@ -183,6 +183,11 @@ hyde_status hyde_profile_enable(hyde_handle h, int on);
 hyde_status hyde_profile_read(hyde_handle h, double* ms, long long* launches);
 long long hyde_launch_count(hyde_handle h);
 
+/* clock64() stamps (SM cycles) of the phases of the last K2 kernel run:
+ * [0] start [1] sweep [2] tridiagonalisation [3] eigenvalues [4] inverse
+ * iteration [5] back-transform; synchronizes the device. */
+hyde_status hyde_debug_eig_clocks(long long* out8);
+
 /* Analysis low-pass filter the kernels use (host, fp64; taps values). */
 hyde_status hyde_filter(int taps, double* h_out);
 

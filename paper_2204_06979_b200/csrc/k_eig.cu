@@ -26,6 +26,14 @@ namespace {
 constexpr int NT = 1024;
 constexpr int NW = NT / 32;
 
+// clock64() stamps of the last noise_eig_kernel run (diagnostics, hyde_debug_eig_clocks):
+// [0] start [1] sweep done [2] tridiagonal done [3] eigenvalues [4] inverse iteration
+// [5] back-transform done
+__device__ long long g_eig_clk[8];
+__device__ __forceinline__ void stamp(int i) {
+  if (threadIdx.x == 0) g_eig_clk[i] = clock64();
+}
+
 __device__ __forceinline__ long long pk(int i, int j) {  // packed lower, i >= j
   return (long long)i * (i + 1) / 2 + j;
 }
@@ -203,6 +211,7 @@ __device__ void vectors_phase(const double* d, const double* e, const double* e2
                               int ldwu, double* red) {
   bisect_eigs(d, e2, B, glo, ghi, pivmin, k0, K, lamk);
   __syncthreads();
+  stamp(3);
   const double tnorm = fmax(fabs(glo), fabs(ghi));
   // per-vector scratch: x, dd, u1, u2, ml (5B doubles) + piv (B bytes)
   double* xs = scratch;
@@ -238,6 +247,7 @@ __device__ void vectors_phase(const double* d, const double* e, const double* e2
     }
   }
   __syncthreads();
+  stamp(4);
   // back-transform: one warp per vector, reflectors k = B-3 .. 0
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (int k = w; k < K; k += NW) {
@@ -276,6 +286,7 @@ __device__ void vectors_phase(const double* d, const double* e, const double* e2
     if (l == 0 && lam_top_out) lam_top_out[kk] = lamk[k];
   }
   __syncthreads();
+  stamp(5);
 }
 
 // tri layout (global): d[B], e[B], e2[B], misc[4] = {glo, ghi, pivmin, 0}
@@ -296,6 +307,7 @@ __global__ void __launch_bounds__(NT, 1) noise_eig_kernel(
   double* e2 = e + B;           // B
   double* red = e2 + B;         // NW + 2
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  stamp(0);
 
   // ---- (1) sweep operator on G + ridge I (packed lower) ----
   for (int i = w; i < B; i += NW)
@@ -326,6 +338,7 @@ __global__ void __launch_bounds__(NT, 1) noise_eig_kernel(
     sigma_out[i] = s;
   }
   __syncthreads();
+  stamp(1);
   if (ncomp < 0) return;   // noise estimate only (hyde_estimate_noise)
 
   // ---- (2) G_w = S G S / N, Householder tridiagonalisation (lower) ----
@@ -406,6 +419,7 @@ __global__ void __launch_bounds__(NT, 1) noise_eig_kernel(
   for (int i = tid; i < B; i += NT) { tri[i] = d[i]; tri[B + i] = e[i]; tri[2 * B + i] = e2[i]; }
   if (tid == 0) { tri[3 * B] = glo; tri[3 * B + 1] = ghi; tri[3 * B + 2] = pivmin; }
   __syncthreads();
+  stamp(2);
 
   // ---- (3) eigenvalues (all if requested), vectors for the top ncomp ----
   double* lamk = red + NW + 2;                 // B doubles
@@ -484,6 +498,11 @@ __global__ void residual_kernel(const float* __restrict__ Y, long long n, int B,
 }
 
 }  // namespace
+
+extern "C" hyde_status hyde_debug_eig_clocks(long long* out) {
+  if (!out) return HYDE_EPARAM;
+  return cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(long long) * 8) == cudaSuccess ? HYDE_OK : HYDE_ECUDA;
+}
 
 static size_t eig_ext_bytes(int B) { return (size_t)(8 * B + NW + 2) * sizeof(double); }
 static size_t eig_scr_bytes(int B, int ncomp) {
