@@ -183,10 +183,18 @@ hyde_status hyde_profile_enable(hyde_handle h, int on);
 hyde_status hyde_profile_read(hyde_handle h, double* ms, long long* launches);
 long long hyde_launch_count(hyde_handle h);
 
-/* clock64() stamps (SM cycles) of the phases of the last K2 kernel run:
- * [0] start [1] sweep [2] tridiagonalisation [3] eigenvalues [4] inverse
- * iteration [5] back-transform; synchronizes the device. */
-hyde_status hyde_debug_eig_clocks(long long* out8);
+/* clock64() stamps / accumulators (SM cycles) of the last K2 kernels:
+ * [0,1] Cholesky start/end, [2,3] tridiagonalisation start/end, [4..7]
+ * eigenpair CTA 0 start / bisection / inverse iteration / back-transform,
+ * [8..10] Cholesky panel-block / panel-rows / trailing-update totals,
+ * [11..13] tridiagonalisation column / SYMV / rank-2-update totals.
+ * Copies 16 values; synchronizes the device. */
+hyde_status hyde_debug_eig_clocks(long long* out16);
+
+/* Copies the tridiagonal T (d[B], e[B], e^2[B], glo, ghi) and the reflector
+ * buffer (B*B Householder columns, B*B eigenvectors, B betas) of the handle's
+ * last hyde_k_eig call (same n_pixels and bands) into device buffers. */
+hyde_status hyde_debug_eig_state(hyde_handle h, int n_pixels, int bands, double* tri_out, double* house_out);
 
 /* Analysis low-pass filter the kernels use (host, fp64; taps values). */
 hyde_status hyde_filter(int taps, double* h_out);

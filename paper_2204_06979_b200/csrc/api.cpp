@@ -51,7 +51,7 @@ void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Lay
   L->sigma = take((size_t)B * 8);
   L->lam = take((size_t)B * 8);
   L->tri = take((size_t)(3 * B + 8) * 8);
-  L->house = take(((size_t)B * B + 2 * (size_t)B + P + 64) * 8);
+  L->house = take(eig_workspace_doubles(B) * 8);
   L->W = take((size_t)B * L->ldwu * 4);
   L->U = take((size_t)B * L->ldwu * 4);
   L->C = take((size_t)chunk * L->plan.n_coeffs * 4);
@@ -603,6 +603,16 @@ hyde_status hyde_k_eig(hyde_handle h, const double* gram, int n_pixels, int band
   CK(launch_noise_eig(gram, n_pixels, bands, ridge, ncomp, lam ? 1 : 0, sigma, lam, V,
                       (double*)(ws + L.house), (double*)(ws + L.tri), (float*)(ws + L.W),
                       (float*)(ws + L.U), L.ldwu, st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_debug_eig_state(hyde_handle h, int n_pixels, int bands, double* tri_out, double* house_out) {
+  if (!h || !h->ws || !tri_out || !house_out || bands < 3) return HYDE_EPARAM;
+  DeviceGuard g(h->device);
+  Layout L;
+  make_layout(n_pixels, 1, bands, 1, 1, 2, &L);   // the layout hyde_k_eig used
+  CK(cudaMemcpy(tri_out, h->ws + L.tri, (size_t)(3 * bands + 2) * 8, cudaMemcpyDeviceToDevice));
+  CK(cudaMemcpy(house_out, h->ws + L.house, ((size_t)bands * bands * 2 + bands) * 8, cudaMemcpyDeviceToDevice));
   return HYDE_OK;
 }
 

@@ -98,6 +98,28 @@ def test_noise_and_eig_match_oracle(hy, name):
     assert np.max(np.abs(V.T @ V - np.eye(k))) < 1e-8
 
 
+@pytest.mark.parametrize("b,r,c", [(3, 17, 33), (4, 20, 20), (6, 20, 20), (9, 31, 29), (33, 40, 40), (224, 40, 40)])
+def test_eigenpairs_are_eigenpairs(hy, b, r, c):
+    """Every returned pair satisfies G_w v = lam v and V is orthonormal (small and odd band counts,
+    the tridiagonal edge cases), independent of how close the eigenvalues are."""
+    s = synth.low_rank_cube(r, c, b, rank=min(3, b - 1), seed=b, snr_db=20.0)
+    n = r * c
+    g = O.gram(s.noisy)
+    sig_ref, _ = O.estimate_noise(s.noisy)
+    k = min(16, b)
+    sig, lam, V = hy.stages.eig(dev(g), n, k)
+    sig, lam, V = sig.cpu().numpy(), lam.cpu().numpy(), V.cpu().numpy()
+    assert np.max(np.abs(sig / sig_ref - 1)) < 1e-9
+    gw = g / np.outer(sig, sig) / n
+    lam_ref = np.sort(np.linalg.eigvalsh(gw))[::-1]
+    assert np.max(np.abs(lam - lam_ref)) < 1e-11 * lam_ref[0]
+    assert np.max(np.abs(gw @ V - V * lam[None, :k])) < 1e-9 * lam_ref[0]
+    assert np.max(np.abs(V.T @ V - np.eye(k))) < 1e-8
+    for j in range(k):                      # sign convention (S:181 D6)
+        i = int(np.argmax(np.abs(V[:, j])))
+        assert V[i, j] > 0
+
+
 def test_estimate_noise_api(hy):
     s = synth.make_cube("small", 0)
     sig, g, res = hy.estimate_noise(dev(s.noisy), return_gram=True, return_residual=True)
