@@ -24,7 +24,7 @@ struct Layout {
   int B, chunk, nsplit, nsub, ldwu, taps, levels;
   long long n, ldE;
   DwtPlan plan;
-  size_t G, partial, amax, sigma, lam, tri, house, W, U, C, S1, S2, kstar, tstar, esub, epost, rs, total;
+  size_t G, partial, amax, sigma, lam, tri, house, W, U, C, surv, S1, S2, kstar, tstar, esub, epost, rs, total;
   int use_tc, npairs;
   size_t s1_img, s2_img;  // per-image strides (floats) of the LL scratch
 };
@@ -55,6 +55,7 @@ void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Lay
   L->W = take((size_t)B * L->ldwu * 4);
   L->U = take((size_t)B * L->ldwu * 4);
   L->C = take((size_t)chunk * L->plan.n_coeffs * 4);
+  L->surv = take((size_t)chunk * L->plan.n_coeffs * 4);
   L->s1_img = (size_t)L->plan.lv[0].hs * L->plan.lv[0].ws;
   L->s2_img = levels > 1 ? (size_t)L->plan.lv[1].hs * L->plan.lv[1].ws : 1;
   L->S1 = take((size_t)chunk * L->s1_img * 4);
@@ -245,8 +246,10 @@ static cudaError_t dwt_forward(const Layout& L, char* ws, const float* E, long l
   return cudaSuccess;
 }
 
+// inverse DWT of `count` coefficient sets; when tstar != NULL each subband is
+// soft-thresholded with its t* as it is loaded (K5 -> K6a fusion)
 static cudaError_t dwt_inverse(const Layout& L, char* ws, const float* Cin, float* Eout, long long ldE,
-                               int count, const FilterBank& fb, cudaStream_t st) {
+                               int count, const FilterBank& fb, const float* tstar, cudaStream_t st) {
   float* S[2] = {(float*)(ws + L.S1), (float*)(ws + L.S2)};
   long long sstr[2] = {(long long)L.s1_img, (long long)L.s2_img};
   const long long nc = L.plan.n_coeffs;
@@ -255,8 +258,9 @@ static cudaError_t dwt_inverse(const Layout& L, char* ws, const float* Cin, floa
     long long ll_str = (l == L.levels - 1) ? nc : sstr[l & 1];
     float* out = l == 0 ? Eout : S[(l - 1) & 1];
     long long out_str = l == 0 ? ldE : sstr[(l - 1) & 1];
+    const int s_ll = (l == L.levels - 1) ? 3 * L.levels : -1;   // only LL_L comes from K5
     cudaError_t e = launch_idwt_level(llin, ll_str, Cin + L.plan.sub_off[l], nc, L.plan.lv[l].h_in,
-                                      L.plan.lv[l].w_in, out, out_str, count, fb, st);
+                                      L.plan.lv[l].w_in, out, out_str, count, fb, tstar, L.nsub, 3 * l, s_ll, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -430,7 +434,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     {
       Stage sg(h, HYDE_STAGE_SURE, 1, st);
       CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
-                     (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, st));
+                     (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, (unsigned*)(ws + L.surv), st));
       sg.end();
     }
     {
@@ -448,7 +452,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     const int kept = r.found ? (r.rank - k0) : cnt;
     if (kept > 0) {
       Stage sg(h, HYDE_STAGE_IDWT, levels, st);
-      CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, st));
+      CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, (const float*)(ws + L.tstar), st));
       sg.end();
     }
     if (r.found) {
@@ -658,7 +662,7 @@ hyde_status hyde_k_idwt(hyde_handle h, const float* coeffs, int count, int rows,
   FilterBank fb;
   hyde_status s = stage_layout(h, count, rows, cols, levels, taps, &L, &fb, st);
   if (s != HYDE_OK) return s;
-  CK(dwt_inverse(L, h->ws, coeffs, images, (long long)rows * cols, count, fb, st));
+  CK(dwt_inverse(L, h->ws, coeffs, images, (long long)rows * cols, count, fb, nullptr, st));
   return HYDE_OK;
 }
 
@@ -672,7 +676,9 @@ hyde_status hyde_k_sure(hyde_handle h, float* coeffs, int count, int rows, int c
   if (s != HYDE_OK) return s;
   RankState* rs = (RankState*)(h->ws + L.rs);
   CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
-  CK(launch_sure(coeffs, L.plan.n_coeffs, L.plan, count, keep_ll, kstar, tstar, (double*)(h->ws + L.esub), rs, st));
+  CK(launch_sure(coeffs, L.plan.n_coeffs, L.plan, count, keep_ll, kstar, tstar, (double*)(h->ws + L.esub), rs,
+                 (unsigned*)(h->ws + L.surv), st));
+  CK(launch_soft_threshold(coeffs, L.plan.n_coeffs, L.plan, count, tstar, st));
   CK(launch_rank_decide((double*)(h->ws + L.esub), L.nsub, count, 0, (double)L.plan.n_coeffs, 1 << 30, rs,
                         e_post, st));
   CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));

@@ -79,10 +79,13 @@ cudaError_t launch_dwt_level(const float* in, long long in_stride, int h_in, int
 cudaError_t launch_idwt_level(const float* ll, long long ll_stride, const float* sub,
                               long long sub_stride, int h_out, int w_out, float* out,
                               long long out_stride, int count, const FilterBank& fb,
-                              cudaStream_t st);
+                              const float* tstar, int nsub, int s_lh, int s_ll, cudaStream_t st);
+cudaError_t launch_soft_threshold(float* coeffs, long long cstride, const DwtPlan& plan, int count, const float* tstar,
+                                  cudaStream_t st);
+// surv: scratch of count * cstride keys (the survivor lists of the clustered subbands)
 cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, int count,
                         int keep_ll, int* kstar, float* tstar, double* e_sub,
-                        RankState* rs, cudaStream_t st);
+                        RankState* rs, unsigned* surv, cudaStream_t st);
 cudaError_t launch_rank_decide(const double* e_sub, int nsub, int count, int k0, double n_coeffs,
                                int bands, RankState* rs, double* e_post, cudaStream_t st);
 cudaError_t launch_reconstruct(const float* E, long long ldE, long long n, int B, const float* U,

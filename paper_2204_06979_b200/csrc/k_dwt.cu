@@ -85,11 +85,23 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
   }
 }
 
+__device__ __forceinline__ float soft(float v, float t) {
+  const float a = fabsf(v) - t;
+  return a > 0.f ? copysignf(a, v) : 0.f;
+}
+
+// thresholds applied on load (K5's t* per subband): tstar
+// [image][nsub], this level's LH/HL/HH at s_lh .. s_lh+2, LL at s_ll (-1 = none)
+struct SoftSpec {
+  const float* tstar;
+  int nsub, s_lh, s_ll;
+};
+
 template <int T>
 __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ llp, long long ll_stride,
                                                       const float* __restrict__ sub, long long sub_stride,
                                                       int h_out, int w_out, float* __restrict__ out,
-                                                      long long out_stride, FilterBank fb) {
+                                                      long long out_stride, FilterBank fb, SoftSpec sp) {
   constexpr int CR = IR / 2 + T / 2 - 1;
   constexpr int CC = IC / 2 + T / 2 - 1;
   __shared__ float t_ll[CR][CC + 1], t_hl[CR][CC + 1], t_lh[CR][CC + 1], t_hh[CR][CC + 1];
@@ -104,15 +116,23 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
   const float* a_lh = sub + (long long)blockIdx.z * sub_stride;
   const float* a_hl = a_lh + nsb;
   const float* a_hh = a_hl + nsb;
+  float th_ll = 0.f, th_lh = 0.f, th_hl = 0.f, th_hh = 0.f;
+  if (sp.tstar) {
+    const float* tz = sp.tstar + (long long)blockIdx.z * sp.nsub;
+    th_lh = tz[sp.s_lh];
+    th_hl = tz[sp.s_lh + 1];
+    th_hh = tz[sp.s_lh + 2];
+    if (sp.s_ll >= 0) th_ll = tz[sp.s_ll];
+  }
   for (int idx = threadIdx.x; idx < CR * CC; idx += 256) {
     int r = idx / CC, c = idx % CC;
     int gi = ((ilo + r) % hs + hs) % hs;
     int gj = ((jlo + c) % ws + ws) % ws;
     long long o = (long long)gi * ws + gj;
-    t_ll[r][c] = a_ll[o];
-    t_lh[r][c] = a_lh[o];
-    t_hl[r][c] = a_hl[o];
-    t_hh[r][c] = a_hh[o];
+    t_ll[r][c] = soft(a_ll[o], th_ll);
+    t_lh[r][c] = soft(a_lh[o], th_lh);
+    t_hl[r][c] = soft(a_hl[o], th_hl);
+    t_hh[r][c] = soft(a_hh[o], th_hh);
   }
   __syncthreads();
   // synthesis along axis 0: lo1 <- (LL, HL), hi1 <- (LH, HH)
@@ -175,13 +195,14 @@ cudaError_t launch_dwt_level(const float* in, long long in_stride, int h_in, int
 cudaError_t launch_idwt_level(const float* ll, long long ll_stride, const float* sub,
                               long long sub_stride, int h_out, int w_out, float* out,
                               long long out_stride, int count, const FilterBank& fb,
-                              cudaStream_t st) {
+                              const float* tstar, int nsub, int s_lh, int s_ll, cudaStream_t st) {
   const int H = h_out + (h_out & 1), Wd = w_out + (w_out & 1);
   dim3 grid((Wd + IC - 1) / IC, (H + IR - 1) / IR, count);
+  const SoftSpec sp{tstar, nsub, s_lh, s_ll};
   switch (fb.taps) {
-    case 2: dwt_inv_kernel<2><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb); break;
-    case 8: dwt_inv_kernel<8><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb); break;
-    case 16: dwt_inv_kernel<16><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb); break;
+    case 2: dwt_inv_kernel<2><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;
+    case 8: dwt_inv_kernel<8><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;
+    case 16: dwt_inv_kernel<16><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -30,25 +30,46 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
 #pragma unroll
     for (int q = 0; q < PIX; ++q) acc[k][q] = 0.f;
   const bool full = p0 + PIX <= n;
-#pragma unroll 4
-  for (int b = 0; b < B; ++b) {
-    float y[PIX];
-    const float* row = Y + (size_t)b * n + p0;
-    if (VEC && full) {
-      if constexpr (PIX == 4) {
-        float4 v = __ldcs(reinterpret_cast<const float4*>(row));
-        y[0] = v.x; y[1] = v.y; y[2] = v.z; y[3] = v.w;
-      } else if constexpr (PIX == 2) {
-        float2 v = __ldcs(reinterpret_cast<const float2*>(row));
-        y[0] = v.x; y[1] = v.y;
+  // 8 bands per step: 8 independent 16-byte loads in flight per thread
+  constexpr int UB = 8;
+  int b = 0;
+  for (; b + UB <= B; b += UB) {
+    float y[UB][PIX];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const float* row = Y + (size_t)(b + u) * n + p0;
+      if (VEC && full) {
+        if constexpr (PIX == 4) {
+          const float4 v = __ldcs(reinterpret_cast<const float4*>(row));
+          y[u][0] = v.x; y[u][1] = v.y; y[u][2] = v.z; y[u][3] = v.w;
+        } else if constexpr (PIX == 2) {
+          const float2 v = __ldcs(reinterpret_cast<const float2*>(row));
+          y[u][0] = v.x; y[u][1] = v.y;
+        } else {
+#pragma unroll
+          for (int q = 0; q < PIX; ++q) y[u][q] = row[q];
+        }
       } else {
 #pragma unroll
-        for (int q = 0; q < PIX; ++q) y[q] = row[q];
+        for (int q = 0; q < PIX; ++q) y[u][q] = (p0 + q < n) ? row[q] : 0.f;
       }
-    } else {
-#pragma unroll
-      for (int q = 0; q < PIX; ++q) y[q] = (p0 + q < n) ? row[q] : 0.f;
     }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const float* wb = Ws + (b + u) * NC;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const float wk = wb[k];
+#pragma unroll
+        for (int q = 0; q < PIX; ++q) acc[k][q] = fmaf(wk, y[u][q], acc[k][q]);
+      }
+    }
+  }
+  for (; b < B; ++b) {
+    float y[PIX];
+    const float* row = Y + (size_t)b * n + p0;
+#pragma unroll
+    for (int q = 0; q < PIX; ++q) y[q] = (p0 + q < n) ? row[q] : 0.f;
     const float* wb = Ws + b * NC;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
