@@ -15,7 +15,7 @@
  *  - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
  *    stream) and is asynchronous unless stated.  Exceptions: argument
  *    validation is synchronous; hyde_hyres / _ex / _batched read the device
- *    rank-decision flag once per 16-component chunk (one stream sync per
+ *    rank-decision flag once per component chunk (one stream sync per
  *    chunk) and therefore return after the GPU has finished
  *    the rank decision (the output write may still be in flight).
  *  - Ownership: the caller owns every buffer it passes; the library never
@@ -73,7 +73,8 @@ int hyde_target_sm(void);
 typedef struct {
   int wavelet_taps;  /* 2 (Haar) | 8 (db4) | 16 (db8, default)  -- SPEC.md:179 D4; 0 = 16 */
   int levels;        /* 0 = auto: max(1, min(5, floor(log2(min(R,C)/(taps-1)))))         */
-  int chunk;         /* candidate components per projection chunk; 0 = 16; max 32      */
+  int chunk;         /* max candidate components per chunk; 0 = 16; max 32. Chunks   */
+                     /* grow 4, 8, 16, ... up to this cap (results are independent)  */
   double ridge;      /* delta of (G + delta I)^-1; 0 = 1e-6                */
   int flags;         /* bit0 HYDE_KEEP_LL: leave LL_L unthresholded (variant, Z7)       */
 } hyde_hyres_params;

@@ -20,6 +20,8 @@ thread_local std::string g_err;
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+constexpr int kFirstChunk = 4;   // components in the first chunk of the rank loop
+
 struct Layout {
   int B, chunk, nsplit, nsub, ldwu, taps, levels;
   long long n, ldE;
@@ -403,16 +405,25 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     CK(run_gram(L, ws, cube, G, &rs->nonfinite, st));
     sg.end();
   }
-  const int first = p.chunk < B ? p.chunk : B;
+  // Geometric chunk schedule: 4, 8, 16, ... components (capped at p.chunk).
+  // The rank rule stops at the first failing component, so small ranks never
+  // pay for a full chunk; results do not depend on the schedule.
+  auto chunk_len = [&](int c) {
+    long long want = (long long)kFirstChunk << (c < 20 ? c : 20);
+    if (want > p.chunk) want = p.chunk;
+    return (int)want;
+  };
+  const int first = chunk_len(0) < B ? chunk_len(0) : B;
   {
     Stage sg(h, HYDE_STAGE_EIG, 1, st);
     CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
     sg.end();
   }
   int rank = 0, chunks = 0;
+  int k0 = 0;
   for (int c = 0;; ++c) {
-    const int k0 = c * p.chunk;
-    const int cnt = (B - k0) < p.chunk ? (B - k0) : p.chunk;
+    const int cl = chunk_len(c);
+    const int cnt = (B - k0) < cl ? (B - k0) : cl;
     if (c > 0) {
       s = ensure_ebuf(h, (size_t)(k0 + cnt) * L.ldE * 4, (size_t)k0 * L.ldE * 4, st);
       if (s != HYDE_OK) return s;
@@ -459,6 +470,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
       rank = r.rank;
       break;
     }
+    k0 += cnt;
   }
   {
     Stage sg(h, HYDE_STAGE_RECON, (rank + 7) / 8, st);
