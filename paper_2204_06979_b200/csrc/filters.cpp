@@ -9,6 +9,7 @@
 // g_k = (-1)^k h_{T-1-k}.
 #include <cmath>
 #include <complex>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -79,10 +80,23 @@ static int daubechies(int nmom, std::vector<ld>& h) {
   return 0;
 }
 
+// The derivation (Durand-Kerner in long double) costs ~1 ms of host time, so
+// each filter is derived once per process and cached; every hyres call used to
+// pay it on the critical path before its first launch.
+static const std::vector<ld>* cached_filter(int taps) {
+  static std::once_flag once[3];
+  static std::vector<ld> h[3];
+  static int ok[3];
+  const int i = taps == 2 ? 0 : taps == 8 ? 1 : 2;
+  std::call_once(once[i], [&] { ok[i] = daubechies(taps / 2, h[i]) == 0 && (int)h[i].size() == taps; });
+  return ok[i] ? &h[i] : nullptr;
+}
+
 int hyde_build_filters(int taps, FilterBank* fb, double* h64) {
   if (taps != 2 && taps != 8 && taps != 16) return -1;
-  std::vector<ld> h;
-  if (daubechies(taps / 2, h) != 0 || (int)h.size() != taps) return -1;
+  const std::vector<ld>* hp = cached_filter(taps);
+  if (!hp) return -1;
+  const std::vector<ld>& h = *hp;
   if (fb) {
     fb->taps = taps;
     for (int k = 0; k < HYDE_MAX_TAPS; ++k) {
