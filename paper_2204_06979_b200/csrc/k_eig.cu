@@ -1,60 +1,145 @@
 // K2 (SURVEY.md §8(a) A1 tail + A2; north_star stages (1)-(2)): per-band
-// noise and the eigendecomposition of the whitened Gram, as a short chain of
-// kernels that each map to what B200 is good at:
+// noise sigma_b^2 = 1 / (N [(G + delta I)^-1]_bb) (HySime's
+// regression estimator) and the leading eigenpairs of the whitened
+// Gram G_w = S G S / N, S = diag(sigma)^-1 (S:380 steps (1)-(2)), fp64.
 //
-//  K2a chol_kernel     (1 CTA)   G + delta I = L L^T, blocked right-looking
-//                                Cholesky on the packed triangle in shared
-//                                memory (panel 16, 4x4 register tiles).
-//  K2b invdiag_kernel  (B/8 CTAs) one warp per band: forward substitution
-//                                L x = e_b, M_bb = |x|^2 = [(G+dI)^-1]_bb,
-//                                sigma_b = sqrt(1 / (N M_bb))  (
-//                                HySime's regression estimator).
-//  K2c tridiag_kernel  (1 CTA)   G_w = S G S / N (S = diag(sigma)^-1) in
-//                                shared memory, Householder reduction to
-//                                tridiagonal T; reflectors to an L2-resident
-//                                column-major buffer.
-//  K2d eigpair_kernel  (1 CTA per eigenpair) multisection bisection of T
-//                                (division-free Sturm counts, 512 points per
-//                                step), inverse iteration, back-transform,
-//                                sign fix (largest-|.| entry positive, lowest
-//                                index on ties: S:181 D6 applied to V), and
-//                                W = S v, U = S^-1 v in fp32 for K3 / K6b.
-//  K2e reorth_kernel   (1 CTA)   Gram-Schmidt inside clusters of numerically
-//                                coincident eigenvalues (|dl| <= 1e-9 ||T||).
+// B200 design: the whole B x B problem (B <= 256) lives in the REGISTERS of
+// one thread-block cluster of CL = 16 CTAs (8 when the GPU cannot co-schedule
+// 16).  Row i of the matrix is owned by CTA i % CL, warp (i / CL) % 8, row
+// slot i / (8 CL); column j by lane j % 32, column slot j / 32 -- cyclic, so
+// the shrinking trailing matrix of the reduction stays balanced.  Rows are
+// exchanged through distributed shared memory (st.shared::cluster) and ordered
+// by the hardware cluster barrier; there is no global-memory round trip and
+// no shared-memory-bandwidth bound on the O(B^3) work.
+//
+//  phase 1  blocked sweep (Gauss-Jordan) of G + delta I, 8 pivots per cluster
+//           exchange: A -> -(G + delta I)^-1, whose diagonal gives sigma.  The
+//           pivot block is Cholesky-factored (P = L L^T) and the trailing
+//           update is A_RR -= W^T W with W = L^-1 A_KR -- the form whose error
+//           stays O(eps ||A||) even when P is nearly singular (a noiseless
+//           low-rank cube), unlike an explicit P^-1.
+//  phase 2  whitening and Householder tridiagonalisation G_w = Q T Q^T with
+//           ONE cluster exchange per column: the all-gather of p = beta A v
+//           carries, one column ahead, the owners' entries of column k+2, so
+//           every CTA updates a replica of the next column itself and forms
+//           the next reflector without a second exchange.  Q = H_0 H_1 ... is
+//           accumulated in registers while the barrier is in flight; rows and
+//           column slots that are already reduced are skipped.
+//  phase 3  eigenpair k on CTA k % CL: 128-section bisection on the Sturm
+//           count of T, inverse iteration, z all-gathered, Gram-Schmidt inside
+//           numerically coincident eigenvalue groups, V = Q Z on the row
+//           owners, sign fix (largest-|.| entry positive, lowest index on ties:
+//           S:181 D6 applied to V) by a cluster-wide argmax, and W = S v,
+//           U = S^-1 v in fp32 for K3 / K6b.
+//
+// Later chunks of the rank loop (launch_eigvec_more) reuse T and Q from
+// global memory: one CTA per eigenpair, a re-orthogonalisation warp and one
+// CTA per vector for V = Q z.
 //
 // Why not the north_star's single-CTA Jacobi (DESIGN.md §4 K2): a dense fp64
 // B x B matrix is 401 KB at B = 224 -- more than one SM's 227 KB of shared
-// memory -- so rotating A *and* V cannot stay on chip in one CTA, and Jacobi's
-// ~8 sweeps x 5 B^3/2 flops would be ~20x the Householder path's work.  The
-// packed triangle (201 KB) fits, and only the chunk's eigenpairs are formed,
-// each on its own SM.  Everything is fp64.
+// memory -- and Jacobi's ~8 sweeps x 5 B^3/2 flops with O(B) barriers per
+// sweep is both more work and a longer dependency chain than Householder.
 #include <math.h>
 
 #include "common.cuh"
 
 namespace {
 
-constexpr int NT = 1024;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NT = 256;    // threads per CTA
 constexpr int NW = NT / 32;
-constexpr int CNB = 16;        // Cholesky panel width
-constexpr int CT = 512;        // Cholesky threads (4x4 fp64 register tiles need > 64 registers)
-constexpr int CW = CT / 32;
+constexpr int CS = 8;      // column slots per lane: 32 * CS = 256 columns
+constexpr int BM = 256;    // max bands
+constexpr int NB = 8;      // sweep block (pivots per cluster exchange)
+constexpr int KM = HYDE_MAX_CHUNK;
+constexpr int BT = 128;    // bisection threads (points per round)
+constexpr int CLMAX = 16;
 
-// clock64() stamps (diagnostics, hyde_debug_eig_clocks): [0] chol start [1] chol end
-// [2] tridiag start [3] tridiag end [4] eigpair start (CTA 0) [5] bisection done
-// [6] inverse iteration done [7] back-transform done
-__device__ long long g_eig_clk[16];
+// clock64() stamps (diagnostics, hyde_debug_eig_clocks; CTA 0 of the cluster):
+// [0] start [1] sweep done [2] tridiagonalisation done [3] eigenpairs done
+// [4] vectors written; [5..] per-segment accumulators
+__device__ long long g_eig_clk[32];
 __device__ __forceinline__ void stamp(int i) {
   if (threadIdx.x == 0) g_eig_clk[i] = clock64();
 }
-// accumulate (clock64() - t0) into slot i (thread 0); returns the new t0
-__device__ __forceinline__ long long acc_clk(int i, long long t0) {
-  const long long t = clock64();
-  if (threadIdx.x == 0) g_eig_clk[i] += t - t0;
-  return t;
-}
+// Segment clocks accumulate in registers and are flushed once at the end;
+// compiled in only with -DHYDE_EIG_PROF (a global read-modify-write per
+// segment would itself dominate the latency-bound loops).
+#ifdef HYDE_EIG_PROF
+#define CLK_DECL long long clk_acc[20] = {0};
+#define ACC(i)                            \
+  do {                                    \
+    const long long t_ = clock64();       \
+    clk_acc[i] += t_ - tc;                \
+    tc = t_;                              \
+  } while (0)
+#define CLK_FLUSH                                                        \
+  if (prof && threadIdx.x == 0)                                          \
+    for (int i_ = 5; i_ < 20; ++i_) g_eig_clk[i_] = clk_acc[i_];
+#else
+#define CLK_DECL
+#define ACC(i) \
+  do {         \
+  } while (0)
+#define CLK_FLUSH
+#endif
 
-__device__ __forceinline__ int off(int i) { return (i * (i + 1)) >> 1; }   // packed lower row start
+// ------------------------------------------------------------ primitives
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_sync() {
+  cl_arrive();
+  cl_wait();
+}
+__device__ __forceinline__ unsigned saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa(unsigned a, unsigned cta) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void st_cl(unsigned a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl_i(unsigned a, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// remote store that completes 8 bytes of the destination CTA's mbarrier
+// transaction count (no release fence on the sender)
+__device__ __forceinline__ void st_async(unsigned a, double v, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(a), "d"(v),
+               "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned mbar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W%=;\n"
+      "}\n" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+// store v at the same shared offset in every CTA of the cluster
+template <int CL>
+__device__ __forceinline__ void st_all(const void* local, double v) {
+  const unsigned a = saddr(local);
+#pragma unroll
+  for (int r = 0; r < CL; ++r) st_cl(mapa(a, r), v);
+}
 
 // 1/a to full fp64 accuracy without the division's long dependent sequence:
 // MUFU reciprocal seed + two Newton steps (a finite, |a| >= 1e-300)
@@ -69,486 +154,109 @@ __device__ __forceinline__ double rcp64(double a) {
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
 
-// block-wide sum (NT threads), broadcast; `red` holds NW + 1 doubles
-__device__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double t = l < NW ? red[l] : 0.0;
-  t = warp_sum(t);
-  __syncthreads();          // everyone has read red before it is reused
-  return t;
+// r[idx] for a runtime, warp-uniform idx without dynamic register indexing
+template <int N>
+__device__ __forceinline__ double sel(const double (&r)[N], int idx) {
+  double v = 0.0;
+#pragma unroll
+  for (int t = 0; t < N; ++t) v = (t == idx) ? r[t] : v;
+  return v;
 }
 
-// Workspace carve-up of the K2 buffer `house` (doubles):
-struct EigWs {
-  double* house_col;   // B*B  column k = Householder vector k (zeros at i <= k)
-  double* vtop;        // B*B  fp64 eigenvectors, column k (row-major B x B)
-  double* house_beta;  // B
-  double* lam_top;     // B    eigenvalues by descending index
-  double* rdiag;       // B    1 / L_ii
-  double* flags;       // 8    [0] Cholesky failure
-  double* Lp;          // P    packed Cholesky factor (also global fallback storage)
-  double* Aw;          // B*B  global fallback storage for the tridiagonalisation / M
-};
-__host__ __device__ inline EigWs carve(double* house, int B) {
-  EigWs w;
-  const long long P = (long long)B * (B + 1) / 2;
-  w.house_col = house;
-  w.vtop = house + (long long)B * B;
-  w.house_beta = w.vtop + (long long)B * B;
-  w.lam_top = w.house_beta + B;
-  w.rdiag = w.lam_top + B;
-  w.flags = w.rdiag + B;
-  w.Lp = w.flags + 8;
-  w.Aw = w.Lp + P;
-  return w;
+// Transposed warp reduction of N per-lane partials (N | 32): lane L returns
+// the warp-wide sum of x[L / (32 / N)] (5 shuffle levels, the first log2 N of
+// them halving the live values).
+template <int N>
+__device__ __forceinline__ double reduceT(const double (&x)[N], int lane) {
+  double cur[N];
+#pragma unroll
+  for (int m = 0; m < N; ++m) cur[m] = x[m];
+  int off = 16;
+#pragma unroll
+  for (int n = N; n > 1; n >>= 1, off >>= 1) {
+    const bool hi = lane & off;
+#pragma unroll
+    for (int m = 0; m < n / 2; ++m) {
+      const double keep = hi ? cur[m + n / 2] : cur[m];
+      const double send = hi ? cur[m] : cur[m + n / 2];
+      cur[m] = keep + __shfl_xor_sync(FULL, send, off);
+    }
+  }
+  double v = cur[0];
+#pragma unroll
+  for (; off > 0; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
+  return v;
 }
 
-// =====================================================================
-// K2a: blocked right-looking Cholesky of G + ridge I (packed lower)
-// =====================================================================
-template <bool SMEM>
-__global__ void __launch_bounds__(CT, 1) chol_kernel(const double* __restrict__ G, int B, double ridge, EigWs ws) {
-  extern __shared__ double sm[];
-  double* A = SMEM ? sm : ws.Lp;
-  __shared__ double dinv_sh;
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  stamp(0);
-  for (int i = w; i < B; i += CW)
-    for (int j = l; j <= i; j += 32) A[off(i) + j] = G[(size_t)i * B + j] + (i == j ? ridge : 0.0);
-  __syncthreads();
-  if (threadIdx.x == 0) { g_eig_clk[8] = 0; g_eig_clk[9] = 0; g_eig_clk[10] = 0; }
-  long long tc0 = clock64();
-  for (int k0 = 0; k0 < B; k0 += CNB) {
-    const int kb = min(CNB, B - k0);
-    // ---- panel: (a) kb x kb diagonal block by warp 0, rows in registers ----
-    if (w == 0) {
-      double a[CNB];
-      const int r = l;
-#pragma unroll
-      for (int c = 0; c < CNB; ++c) a[c] = (r < kb && c <= r) ? A[off(k0 + r) + k0 + c] : 0.0;
-#pragma unroll
-      for (int c = 0; c < CNB; ++c) {
-        if (c < kb) {
-          double dc = __shfl_sync(0xffffffffu, a[c], c);
-          if (!(dc > 0.0)) {   // not positive definite (cannot happen for G + dI, d > 0, G PSD)
-            if (l == 0) ws.flags[0] = 1.0;
-            dc = 1e-300;
-          }
-          const double piv = sqrt(dc);
-          const double rinv = 1.0 / piv;
-          if (r == c) a[c] = piv;
-          else if (r > c) a[c] *= rinv;
-          if (l == 0) ws.rdiag[k0 + c] = rinv;
-#pragma unroll
-          for (int j = c + 1; j < CNB; ++j) {
-            const double ljc = __shfl_sync(0xffffffffu, a[c], j);
-            if (j < kb && r >= j && r < kb) a[j] = fma(-a[c], ljc, a[j]);
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < CNB; ++c)
-        if (r < kb && c <= r) A[off(k0 + r) + k0 + c] = a[c];
-    }
-    __syncthreads();
-    tc0 = acc_clk(8, tc0);
-    // ---- panel: (b) rows below the block, one thread per row (triangular solve) ----
-    for (int i = k0 + kb + tid; i < B; i += CT) {
-      double li[CNB];
-      const int oi = off(i);
-#pragma unroll
-      for (int c = 0; c < CNB; ++c) {
-        if (c < kb) {
-          double x = A[oi + k0 + c];
-          const int oc = off(k0 + c);
-#pragma unroll
-          for (int q = 0; q < CNB; ++q)
-            if (q < c) x = fma(-li[q], A[oc + k0 + q], x);
-          li[c] = x * ws.rdiag[k0 + c];
-          A[oi + k0 + c] = li[c];
-        }
-      }
-    }
-    __syncthreads();
-    tc0 = acc_clk(9, tc0);
-    // ---- trailing update A22 -= P P^T with 4x4 register tiles ----
-    const int k1 = k0 + kb;
-    const int m = B - k1;
-    if (m <= 0) break;
-    const int nt = (m + 3) >> 2;
-    const int ntiles = nt * (nt + 1) / 2;
-    for (int t = tid; t < ntiles; t += CT) {
-      int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-      while (off(ti + 1) <= t) ++ti;
-      while (off(ti) > t) --ti;
-      const int tj = t - off(ti);
-      const int i0 = k1 + 4 * ti, j0 = k1 + 4 * tj;
-      double acc[4][4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int s = 0; s < 4; ++s) acc[r][s] = 0.0;
-      int oi[4], oj[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        oi[r] = (i0 + r < B) ? off(i0 + r) + k0 : -1;
-        oj[r] = (j0 + r < B) ? off(j0 + r) + k0 : -1;
-      }
-      for (int c = 0; c < kb; ++c) {
-        double li[4], lj[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          li[r] = oi[r] >= 0 ? A[oi[r] + c] : 0.0;
-          lj[r] = oj[r] >= 0 ? A[oj[r] + c] : 0.0;
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = fma(li[r], lj[s], acc[r][s]);
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int i = i0 + r, j = j0 + s;
-          if (i < B && j <= i) A[off(i) + j] -= acc[r][s];
-        }
-    }
-    __syncthreads();
-    tc0 = acc_clk(10, tc0);
-  }
-  if (SMEM) {
-    const int P = off(B);
-    for (int t = tid; t < P; t += CT) ws.Lp[t] = A[t];
-  }
-  stamp(1);
-}
-
-// =====================================================================
-// K2b: M_bb = |L^-1 e_b|^2 by forward substitution, one warp per band
-// =====================================================================
-__global__ void __launch_bounds__(256) invdiag_kernel(EigWs ws, int B, long long n, double* sigma_out) {
-  __shared__ double xs[8][256];
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + w;
-  if (b >= B) return;
-  double* x = xs[w];
-  const double* L = ws.Lp;
-  const double* rd = ws.rdiag;
-  const double xb = rd[b];
-  if (l == 0) x[b] = xb;
-  double ss = xb * xb;
-  __syncwarp();
-  // prefetch row b+1's entries (j in [b, i)) held strided by lane
-  double cur[8];
-  int i = b + 1;
-  auto load_row = [&](int row, double (&dst)[8]) {
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int j = b + l + 32 * t;
-      dst[t] = (row < B && j < row) ? L[off(row) + j] : 0.0;
-    }
-  };
-  if (i < B) load_row(i, cur);
-  for (; i < B; ++i) {
-    double nxt[8];
-    load_row(i + 1, nxt);
-    double s = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int j = b + l + 32 * t;
-      if (j < i) s = fma(cur[t], x[j], s);
-    }
-    s = warp_sum(s);
-    const double xi = -s * rd[i];
-    if (l == 0) x[i] = xi;
-    ss = fma(xi, xi, ss);
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < 8; ++t) cur[t] = nxt[t];
-  }
-  if (l == 0) sigma_out[b] = sqrt(1.0 / ((double)n * ss));
-}
-
-// =====================================================================
-// K2c: whitening + Householder tridiagonalisation (one CTA)
-// =====================================================================
-constexpr int TT = 1024;        // tridiagonalisation threads
-constexpr int TW = TT / 32;
-
-// Warp 0 only: from the (final) column c below its diagonal, x = A[c+1.., c],
-// form the Householder reflector H = I - beta v v^T with H x = alpha e_1;
-// writes v (entries > c) into vout, d[c] / e[c] / beta to tri / ws, the
-// reflector to ws.house_col and beta to *beta_sh.
-__device__ void make_reflector(const double* A, int B, int c, double dcc, double* vout, double* tri, EigWs& ws,
-                               double* beta_sh) {
-  const int l = threadIdx.x & 31;
-  double part = 0.0, x0 = 0.0;
-  for (int i = c + 1 + l; i < B; i += 32) {
-    const double x = A[off(i) + c];
-    vout[i] = x;
-    if (i == c + 1) x0 = x;
-    else part = fma(x, x, part);             // |x[1:]|^2 directly: exactly 0 when x has one entry
-  }
-  const double tail = warp_sum(part);
-  x0 = warp_sum(x0);                         // only the lane holding i = c+1 contributed
-  double beta = 0.0, alpha = x0;
-  // the last column (c = B-2) is already tridiagonal: no reflector (only 0..B-3 are applied)
-  if (tail > 0.0 && c < B - 2) {
-    const double sumsq = fma(x0, x0, tail);
-    alpha = -copysign(sqrt(sumsq), x0);
-    const double v0 = x0 - alpha;
-    beta = 2.0 / (tail + v0 * v0);
-    __syncwarp();
-    if (l == 0) vout[c + 1] = v0;
-  }
-  __syncwarp();
-  for (int i = l; i < B; i += 32) ws.house_col[(size_t)c * B + i] = (i > c) ? vout[i] : 0.0;
-  if (l == 0) {
-    tri[c] = dcc;
-    tri[B + c] = alpha;
-    ws.house_beta[c] = beta;
-    *beta_sh = beta;
-  }
-  __syncwarp();
-}
-
-// Householder tridiagonalisation of G_w (one CTA, TT threads), look-ahead form:
-// per column k two barriers -- (1) p = beta A22 v on blocks of 4 rows (four
-// independent dot products per lane) plus the p.v partials; (2) the rank-2
-// update A22 -= v w^T + w v^T by warps 1.. while warp 0 updates column k+1
-// itself and immediately forms reflector k+1 into the other v buffer.
-template <bool SMEM>
-__global__ void __launch_bounds__(TT, 1) tridiag_kernel(const double* __restrict__ G, const double* __restrict__ sigma,
-                                                        long long n, int B, EigWs ws, double* tri) {
-  extern __shared__ double sm[];
-  // shared layout: vbuf[2][B] pp[B] sig[B] red[TW+8] | A (packed) if SMEM
-  double* vbuf0 = sm;
-  double* vbuf1 = sm + B;
-  double* pp = sm + 2 * B;
-  double* sig = pp + B;
-  double* red = sig + B;
-  double* A = SMEM ? (red + TW + 8) : ws.Aw;
-  __shared__ double beta_sh;
-  __shared__ double hi_red[TW], lo_red[TW];
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  stamp(2);
-  for (int i = tid; i < B; i += TT) sig[i] = sigma[i];
-  __syncthreads();
-  const double invn = 1.0 / (double)n;
-  for (int i = w; i < B; i += TW)
-    for (int j = l; j <= i; j += 32) A[off(i) + j] = G[(size_t)i * B + j] / (sig[i] * sig[j]) * invn;
-  __syncthreads();
-  if (threadIdx.x == 0) { g_eig_clk[11] = 0; g_eig_clk[12] = 0; g_eig_clk[13] = 0; }
-  long long tt0 = clock64();
-  if (w == 0) make_reflector(A, B, 0, A[0], vbuf0, tri, ws, &beta_sh);
-  __syncthreads();
-  for (int k = 0; k < B - 2; ++k) {
-    double* vv = (k & 1) ? vbuf1 : vbuf0;
-    double* vn = (k & 1) ? vbuf0 : vbuf1;
-    const double beta = beta_sh;
-    // ---- (1) p = beta A22 v, rows k+1 .. B-1, and p.v partials ----
-    const int nblk = (B - k - 1 + 3) >> 2;
-    double pvp = 0.0;
-    for (int blk = w; blk < nblk; blk += TW) {
-      const int i0 = k + 1 + 4 * blk;
-      const int nr = min(4, B - i0);
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      const int o0 = off(i0), o1 = off(i0 + 1), o2 = off(i0 + 2), o3 = off(i0 + 3);
-      for (int j = k + 1 + l; j < i0; j += 32) {
-        const double vj = vv[j];
-        s0 = fma(A[o0 + j], vj, s0);
-        if (nr > 1) s1 = fma(A[o1 + j], vj, s1);
-        if (nr > 2) s2 = fma(A[o2 + j], vj, s2);
-        if (nr > 3) s3 = fma(A[o3 + j], vj, s3);
-      }
-      for (int j = i0 + 4 + l; j < B; j += 32) {
-        const double vj = vv[j];
-        const int bj = off(j) + i0;
-        s0 = fma(A[bj], vj, s0);
-        s1 = fma(A[bj + 1], vj, s1);
-        s2 = fma(A[bj + 2], vj, s2);
-        s3 = fma(A[bj + 3], vj, s3);
-      }
-      if (l < nr) {   // diagonal 4x4 block: lane r adds row r's part
-        double add = 0.0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (c < nr) {
-            const double a = (c <= l) ? A[off(i0 + l) + i0 + c] : A[off(i0 + c) + i0 + l];
-            add = fma(a, vv[i0 + c], add);
-          }
-        if (l == 0) s0 += add;
-        else if (l == 1) s1 += add;
-        else if (l == 2) s2 += add;
-        else s3 += add;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        s3 += __shfl_xor_sync(0xffffffffu, s3, o);
-      }
-      if (l < nr) {
-        const double sr = l == 0 ? s0 : (l == 1 ? s1 : (l == 2 ? s2 : s3));
-        const double pr = beta * sr;
-        pp[i0 + l] = pr;
-        pvp = fma(pr, vv[i0 + l], pvp);
-      }
-    }
-    pvp = warp_sum(pvp);
-    if (l == 0) red[w] = pvp;
-    __syncthreads();
-    tt0 = acc_clk(12, tt0);
-    const double Kc = 0.5 * beta * warp_sum(l < TW ? red[l] : 0.0);
-    // ---- (2) rank-2 update; warp 0 owns column k+1 and the next reflector ----
-    if (w == 0) {
-      const double vk1 = vv[k + 1], wk1 = pp[k + 1] - Kc * vk1;
-      double dnext = 0.0;
-      for (int i = k + 1 + l; i < B; i += 32) {
-        const double vi = vv[i], wi = pp[i] - Kc * vi;
-        const double a = A[off(i) + k + 1] - fma(vi, wk1, wi * vk1);
-        A[off(i) + k + 1] = a;
-        if (i == k + 1) dnext = a;
-      }
-      dnext = warp_sum(dnext);
-      __syncwarp();
-      make_reflector(A, B, k + 1, dnext, vn, tri, ws, &beta_sh);
-    } else {
-      for (int blk = w - 1; blk < nblk; blk += TW - 1) {
-        const int i0 = k + 1 + 4 * blk;
-        const int nr = min(4, B - i0);
-        double vi[4], wi[4];
-        int oi[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          vi[r] = r < nr ? vv[i0 + r] : 0.0;
-          wi[r] = r < nr ? pp[i0 + r] - Kc * vi[r] : 0.0;
-          oi[r] = off(i0 + r);
-        }
-        for (int j = k + 2 + l; j < i0 + nr; j += 32) {
-          const double vj = vv[j], wj = pp[j] - Kc * vj;
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (r < nr && j <= i0 + r) A[oi[r] + j] -= fma(vi[r], wj, wi[r] * vj);
-        }
-      }
-    }
-    __syncthreads();
-    tt0 = acc_clk(13, tt0);
-  }
-  if (tid == 0) {
-    tri[B - 1] = A[off(B - 1) + B - 1];
-    tri[B + B - 1] = 0.0;
-    ws.house_beta[B - 1] = 0.0;
-  }
-  for (int i = tid; i < B; i += TT) ws.house_col[(size_t)(B - 1) * B + i] = 0.0;
-  __syncthreads();
-  double lo = INFINITY, hi = -INFINITY;
-  for (int i = tid; i < B; i += TT) {
-    const double ei = tri[B + i];
-    tri[2 * B + i] = ei * ei;
-    const double r = (i > 0 ? fabs(tri[B + i - 1]) : 0.0) + (i < B - 1 ? fabs(ei) : 0.0);
-    lo = fmin(lo, tri[i] - r);
-    hi = fmax(hi, tri[i] + r);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  if (l == 0) { lo_red[w] = lo; hi_red[w] = hi; }
-  __syncthreads();
-  if (tid == 0) {
-    double a = INFINITY, b2 = -INFINITY;
-    for (int q = 0; q < TW; ++q) { a = fmin(a, lo_red[q]); b2 = fmax(b2, hi_red[q]); }
-    tri[3 * B] = a;
-    tri[3 * B + 1] = b2;
-  }
-  stamp(3);
-}
-
-// =====================================================================
-// K2d: one eigenpair per CTA
-// =====================================================================
-constexpr int EP_T = 256;           // threads per eigenpair CTA
-constexpr int EP_W = EP_T / 32;
-constexpr int RB = 16;              // reflectors per staged block (back-transform)
-
+// ------------------------------------------------------------ tridiagonal eigen helpers
 // Sign changes of the Sturm sequence p_0 = 1, p_i = det(T_i - x I) =
-// (d_i - x) p_{i-1} - e2_{i-1} p_{i-2} at two points (= eigenvalues below x).
+// (d_i - x) p_{i-1} - e2_{i-1} p_{i-2} (= eigenvalues of T below x).
 // Division-free (one dependent FMA per step), power-of-two rescaling every 4
 // steps, exact zeros take the sign opposite to their predecessor (LAPACK's
 // -pivmin convention for q_i = p_i / p_{i-1}).
-__device__ __forceinline__ void sturm2(const double* d, const double* e2, int n, double x0, double x1, int& c0,
-                                       int& c1) {
-  double a0 = 1.0, b0 = d[0] - x0;
-  double a1 = 1.0, b1 = d[0] - x1;
-  if (b0 == 0.0) b0 = -1e-300;
-  if (b1 == 0.0) b1 = -1e-300;
-  int n0 = b0 < 0.0, n1 = b1 < 0.0;
-#pragma unroll 4
-  for (int i = 1; i < n; ++i) {
-    const double di = d[i], ei = e2[i - 1];
-    const double u0 = ei * a0, u1 = ei * a1;
-    double t0 = fma(di - x0, b0, -u0);
-    double t1 = fma(di - x1, b1, -u1);
-    if (t0 == 0.0) t0 = b0 < 0.0 ? 1e-300 * fabs(b0) : -1e-300 * fabs(b0);
-    if (t1 == 0.0) t1 = b1 < 0.0 ? 1e-300 * fabs(b1) : -1e-300 * fabs(b1);
-    n0 += (t0 < 0.0) != (b0 < 0.0);
-    n1 += (t1 < 0.0) != (b1 < 0.0);
-    a0 = b0; b0 = t0;
-    a1 = b1; b1 = t1;
-    if ((i & 3) == 3) {
-      const double m0 = fmax(fabs(a0), fabs(b0)), m1 = fmax(fabs(a1), fabs(b1));
-      if (m0 > 0x1p+500) { a0 *= 0x1p-500; b0 *= 0x1p-500; }
-      else if (m0 < 0x1p-500) { a0 *= 0x1p+500; b0 *= 0x1p+500; }
-      if (m1 > 0x1p+500) { a1 *= 0x1p-500; b1 *= 0x1p-500; }
-      else if (m1 < 0x1p-500) { a1 *= 0x1p+500; b1 *= 0x1p+500; }
+__device__ __forceinline__ int sturm1(const double* d, const double* e2, int n, double x) {
+  double a = 1.0, b = d[0] - x;
+  if (b == 0.0) b = -1e-300;
+  int cnt = b < 0.0;
+  int i = 1;
+  for (; i + 3 < n; i += 4) {
+    double dv[4], ev[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { dv[u] = d[i + u] - x; ev[u] = e2[i + u - 1]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double t = fma(dv[u], b, -ev[u] * a);
+      t = (t == 0.0) ? -1e-300 * b : t;    // zero: sign opposite to its predecessor
+      cnt += (int)((unsigned)(__double2hiint(t) ^ __double2hiint(b)) >> 31);
+      a = b;
+      b = t;
     }
+    const double m = fmax(fabs(a), fabs(b));
+    const double sc = m > 0x1p+300 ? 0x1p-300 : (m < 0x1p-300 ? 0x1p+300 : 1.0);
+    a *= sc;
+    b *= sc;
   }
-  c0 = n0;
-  c1 = n1;
+  for (; i < n; ++i) {
+    double t = fma(d[i] - x, b, -e2[i - 1] * a);
+    t = (t == 0.0) ? -1e-300 * b : t;
+    cnt += (int)((unsigned)(__double2hiint(t) ^ __double2hiint(b)) >> 31);
+    a = b;
+    b = t;
+  }
+  return cnt;
 }
 
-// Eigenvalue with ascending index `asc` of T by (2*EP_T)-section; all threads
-// of the CTA cooperate and end with the same (lo, hi).
+// Eigenvalue with ascending index `asc` of T by BT-section (BT threads count,
+// all NT threads pass the barriers and end with the same (lo, hi)).
 __device__ double bisect_one(const double* d, const double* e2, int n, double glo, double ghi, int asc, int* qsh) {
-  constexpr int NP = 2 * EP_T;
   const double range = fmax(ghi - glo, 1e-300);
   const double tol = 4.0 * 2.220446049250313e-16 * fmax(fabs(glo), fabs(ghi)) + 1e-300;
-  int iters = (int)ceil(log2(range / tol) / log2((double)NP + 1.0)) + 1;
+  int iters = (int)ceil(log2(range / tol) / log2((double)BT + 1.0)) + 1;
   if (iters > 64) iters = 64;
   double lo = glo, hi = ghi;
   const int t = threadIdx.x;
   for (int it = 0; it < iters; ++it) {
-    const double h = (hi - lo) / (double)(NP + 1);
-    const double x0 = lo + h * (double)(2 * t + 1);
-    const double x1 = lo + h * (double)(2 * t + 2);
-    int ca, cb;
-    sturm2(d, e2, n, x0, x1, ca, cb);
-    int q = NP;
-    if (cb > asc) q = 2 * t + 1;
-    if (ca > asc) q = 2 * t;
+    const double h = (hi - lo) / (double)(BT + 1);
+    int q = BT;
+    if (t < BT) {
+      const double x = lo + h * (double)(t + 1);
+      if (sturm1(d, e2, n, x) > asc) q = t;
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) q = min(q, __shfl_xor_sync(0xffffffffu, q, o));
+    for (int o = 16; o > 0; o >>= 1) q = min(q, __shfl_xor_sync(FULL, q, o));
     if ((t & 31) == 0) qsh[t >> 5] = q;
     __syncthreads();
     int qq = qsh[0];
 #pragma unroll
-    for (int wv = 1; wv < EP_W; ++wv) qq = min(qq, qsh[wv]);
+    for (int wv = 1; wv < NW; ++wv) qq = min(qq, qsh[wv]);
     __syncthreads();
     // point p sits at lo + h (p + 1): the target lies in (x_{q-1}, x_q]
     const double nlo = qq > 0 ? lo + h * (double)qq : lo;
-    const double nhi = qq < NP ? lo + h * (double)(qq + 1) : hi;
+    const double nhi = qq < BT ? lo + h * (double)(qq + 1) : hi;
     lo = nlo;
     hi = nhi;
   }
@@ -556,7 +264,9 @@ __device__ double bisect_one(const double* d, const double* e2, int n, double gl
 }
 
 // Inverse iteration for eigenvalue lam of T (one thread): partial-pivot LU of
-// T - lam I (two super-diagonals), two solves from a fixed start vector.
+// T - lam I (two super-diagonals), two solves from a fixed start vector.  The
+// running values are carried in registers; shared memory only holds the
+// factors and x.
 __device__ void inv_iter(const double* d, const double* e, int n, double lam, double tnorm, double* x,
                          double* dd, double* u1, double* u2, double* ml, unsigned char* piv, unsigned seed) {
   const double tiny = tnorm > 0.0 ? 2.220446049250313e-16 * tnorm : 1.0;
@@ -570,13 +280,13 @@ __device__ void inv_iter(const double* d, const double* e, int n, double lam, do
       const double ra = rcp64(a);
       const double m = c * ra;
       dd[i] = ra; u1[i] = b; u2[i] = 0.0; ml[i] = m; piv[i] = 0;
-      a = a1 - m * b;
+      a = fma(-m, b, a1);
       b = b1;
     } else {
       const double rc = rcp64(c);
       const double m = a * rc;
       dd[i] = rc; u1[i] = a1; u2[i] = b1; ml[i] = m; piv[i] = 1;
-      a = b - m * a1;
+      a = fma(-m, a1, b);
       b = -m * b1;
     }
   }
@@ -588,231 +298,736 @@ __device__ void inv_iter(const double* d, const double* e, int n, double lam, do
     x[i] = 0.5 + (double)(h & 0xFFFF) / 65536.0;
   }
   for (int it = 0; it < 2; ++it) {
-    for (int i = 0; i < n - 1; ++i) {
+    double cur = x[0];
+    for (int i = 0; i < n - 1; ++i) {   // forward: L^-1 with the row interchanges
+      double nx = x[i + 1];
+      const double m = ml[i];
       if (piv[i]) {
-        const double t = x[i];
-        x[i] = x[i + 1];
-        x[i + 1] = t - ml[i] * x[i + 1];
+        x[i] = nx;
+        nx = fma(-m, nx, cur);
       } else {
-        x[i + 1] -= ml[i] * x[i];
+        x[i] = cur;
+        nx = fma(-m, cur, nx);
       }
+      cur = nx;
     }
-    x[n - 1] *= dd[n - 1];
-    if (n > 1) x[n - 2] = (x[n - 2] - u1[n - 2] * x[n - 1]) * dd[n - 2];
-    for (int i = n - 3; i >= 0; --i) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) * dd[i];
-    double mx = 0.0;
-    for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(x[i]));
+    double c1 = cur * dd[n - 1];     // backward: U^-1, two super-diagonals
+    x[n - 1] = c1;
+    double mx = fabs(c1);
+    double c0 = c1;
+    if (n > 1) {
+      c0 = (x[n - 2] - u1[n - 2] * c1) * dd[n - 2];
+      x[n - 2] = c0;
+      mx = fmax(mx, fabs(c0));
+    }
+    for (int i = n - 3; i >= 0; --i) {
+      const double xi = (x[i] - u1[i] * c0 - u2[i] * c1) * dd[i];
+      x[i] = xi;
+      mx = fmax(mx, fabs(xi));
+      c1 = c0;
+      c0 = xi;
+    }
     mx = 1.0 / mx;
     double s = 0.0;
-    for (int i = 0; i < n; ++i) { x[i] *= mx; s = fma(x[i], x[i], s); }
+    for (int i = 0; i < n; ++i) {
+      const double v = x[i] * mx;
+      x[i] = v;
+      s = fma(v, v, s);
+    }
     s = 1.0 / sqrt(s);
     for (int i = 0; i < n; ++i) x[i] *= s;
   }
 }
 
-// one CTA = eigenpair k0 + blockIdx.x (descending order); vectors_only = 0
-// also computes the vector, 1 = eigenvalue only (all-eigenvalue diagnostics)
-__global__ void __launch_bounds__(EP_T) eigpair_kernel(const double* __restrict__ tri, EigWs ws,
-                                                       const double* __restrict__ sigma, int B, int k0,
-                                                       int values_only, double* lam_out, double* V, int ldv,
-                                                       float* W, float* U, int ldwu) {
-  extern __shared__ double sm[];
-  double* d = sm;
-  double* e = d + B;
-  double* e2 = e + B;
-  double* y = e2 + B;
-  double* dd = y + B;
-  double* u1 = dd + B;
-  double* u2 = u1 + B;
-  double* ml = u2 + B;
-  unsigned char* piv = reinterpret_cast<unsigned char*>(ml + B);
-  __shared__ int qsh[EP_W];
-  const int kdesc = k0 + blockIdx.x;
-  const int tid = threadIdx.x;
-  if (blockIdx.x == 0) stamp(4);
-  for (int i = tid; i < B; i += EP_T) { d[i] = tri[i]; e[i] = tri[B + i]; e2[i] = tri[2 * B + i]; }
-  __syncthreads();
-  const double glo = tri[3 * B], ghi = tri[3 * B + 1];
-  const double lam = bisect_one(d, e2, B, glo, ghi, B - 1 - kdesc, qsh);
-  if (blockIdx.x == 0) stamp(5);
-  if (values_only) {
-    if (tid == 0) lam_out[kdesc] = lam;
-    return;
+// Gershgorin interval of T and e2 = e^2 (NT threads; d, e, e2 in shared memory)
+__device__ void tri_bounds(const double* d, const double* e, double* e2, int B, double* red, double& glo,
+                           double& ghi) {
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  double lo = INFINITY, hi = -INFINITY;
+  for (int i = tid; i < B; i += NT) {
+    e2[i] = e[i] * e[i];
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < B - 1 ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
   }
-  const double tnorm = fmax(fabs(glo), fabs(ghi));
-  if (tid == 0) inv_iter(d, e, B, lam, tnorm, y, dd, u1, u2, ml, piv, (unsigned)kdesc);
-  __syncthreads();
-  if (blockIdx.x == 0) stamp(6);
-  // back-transform y <- H_0 ... H_{B-3} y: reflectors staged through shared
-  // memory in blocks of RB (double-buffered: warps 1.. load the next block
-  // while warp 0 applies the current one)
-  double* rbuf = reinterpret_cast<double*>(piv + ((B + 15) & ~15));   // 2 x RB x B
-  const int l = tid & 31;
-  double yl[8];
-  if (tid < 32) {
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int i = l + 32 * t;
-      yl[t] = i < B ? y[i] : 0.0;
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(FULL, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(FULL, hi, o));
   }
-  const int nref = B - 2;                       // reflectors 0 .. B-3
-  const int nblkr = (nref + RB - 1) / RB;       // blocks from the top (r = B-3 downwards)
-  auto load_block = [&](int bb, int buf, int t0, int tstep) {
-    const int rhi = nref - 1 - bb * RB;         // first reflector of the block
-    for (int t = t0; t < RB * B; t += tstep) {
-      const int q = t / B, i = t % B;
-      const int r = rhi - q;
-      rbuf[(size_t)buf * RB * B + t] = (r >= 0) ? ws.house_col[(size_t)r * B + i] : 0.0;
-    }
-  };
-  load_block(0, 0, tid, EP_T);
+  if (l == 0) { red[w] = lo; red[NW + w] = hi; }
   __syncthreads();
-  for (int bb = 0; bb < nblkr; ++bb) {
-    if (tid >= 32) {
-      if (bb + 1 < nblkr) load_block(bb + 1, (bb + 1) & 1, tid - 32, EP_T - 32);
-    } else {
-      const double* rb = rbuf + (size_t)(bb & 1) * RB * B;
-      const int rhi = nref - 1 - bb * RB;
-      for (int q = 0; q < RB; ++q) {
-        const int r = rhi - q;
-        if (r < 0) break;
-        const double beta = ws.house_beta[r];
-        double s = 0.0;
+  lo = red[0];
+  hi = red[NW];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int i = l + 32 * t;
-          if (i < B) s = fma(rb[q * B + i], yl[t], s);
-        }
-        s = warp_sum(s) * beta;
+  for (int q = 1; q < NW; ++q) { lo = fmin(lo, red[q]); hi = fmax(hi, red[NW + q]); }
+  __syncthreads();
+  glo = lo;
+  ghi = hi;
+}
+
+// Global workspace carve-up of the K2 buffer `house` (doubles)
+struct EigWs {
+  double* Q;        // B*B row-major: Q = H_0 H_1 ... H_{B-3}, G_w = Q T Q^T
+  double* vtop;     // B*B row-major, column k = eigenvector k of G_w (sign-fixed)
+  double* ztop;     // B*B, row k = eigenvector k of T
+  double* M;        // B*B  (G + ridge I)^-1 (only when requested)
+  double* lam_top;  // B    eigenvalues by descending index
+  double* flags;    // 8    [0] non-positive pivot in the sweep
+};
+__host__ __device__ inline EigWs carve(double* house, int B) {
+  EigWs w;
+  const long long BB = (long long)B * B;
+  w.Q = house;
+  w.vtop = house + BB;
+  w.ztop = house + 2 * BB;
+  w.M = house + 3 * BB;
+  w.lam_top = house + 4 * BB;
+  w.flags = w.lam_top + B;
+  return w;
+}
+
+struct K2Args {
+  const double* G;
+  long long n;
+  int B;
+  double ridge;
+  int K;           // eigenpairs of the first chunk
+  int tridiag;     // 0: sigma only
+  int want_M;      // write (G + ridge I)^-1 to ws.M
+  double* sigma;
+  double* tri;     // d[B] e[B] e2[B] glo ghi
+  EigWs ws;
+  double* lam_out; // nullable, eigenvalue k at [k]
+  double* V;       // nullable, column k at [i * ldv + k]
+  int ldv;
+  float* W;
+  float* U;
+  int ldwu;
+};
+
+struct K2Smem {
+  unsigned long long mbar[2];   // tridiagonalisation exchange, one per column parity
+  double pbuf[2][BM];      // p = beta A v, all-gathered (double-buffered by column parity)
+  double xbuf[2][BM];      // column k+2 entries, all-gathered one column ahead
+  double colK[2][BM * NB]; // sweep: pivot-block columns of every row (double-buffered by block)
+  double Wb[NB][BM];       // sweep: L^-1 A_K,:
+  double Zb[NB][BM];       // sweep: P^-1 A_K,:
+  double Lb[NB * NB];      // sweep: Cholesky factor of the pivot block
+  double Lr[NB];           //        1 / L_qq
+  double Pinv[NB * NB];
+  double sig[BM];
+  double vw[NW][BM];       // per-warp copy of the current reflector vector
+  double cw[NW][BM];       // per-warp copy of the column being reduced
+  double d[BM], e[BM], e2[BM];
+  double zb[KM][BM];       // eigenvectors of T (all-gathered)
+  double lamk[KM];
+  double vrow[KM][32];     // V rows owned by this CTA (local row index w*RS+s)
+  double am[CLMAX][KM];    // sign reduction: max |V_ik| per CTA
+  double av[CLMAX][KM];    //                 the entry itself
+  int ai[CLMAX][KM];       //                 its lowest row index
+  double dd[BM], u1[BM], u2[BM], ml[BM], y[BM];
+  unsigned char piv[BM];
+  double red[4 * NW];
+  int qsh[NW];
+};
+
+// Householder reflector from column kk (lane-distributed in col[], rows j >
+// kk used): H = I - beta v v^T with H x = alpha e_1 on rows kk+1.. (LAPACK
+// dlarfg convention, unnormalised v with v_{kk+1} = x_{kk+1} - alpha).
+// Every warp computes it redundantly and keeps a copy of v in S.vw[w];
+// thread 0 records d_kk, e_kk.
+template <int RS>
+__device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, int B, int lane, int w,
+                                               const int (&rowi)[RS], double (&vreg)[CS], double (&vrow)[RS],
+                                               double& beta, K2Smem& S) {
+  double* cw = S.cw[w];
+  double* vw = S.vw[w];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int i = l + 32 * t;
-          if (i < B) yl[t] = fma(-s, rb[q * B + i], yl[t]);
+  for (int t = 0; t < CS; ++t) cw[lane + 32 * t] = col[t];
+  double part = 0.0;
+#pragma unroll
+  for (int t = 0; t < CS; ++t) {
+    const int j = lane + 32 * t;
+    if (j > kk + 1 && j < B) part = fma(col[t], col[t], part);
+  }
+  const double tail = warp_sum(part);
+  __syncwarp();
+  const double dkk = cw[kk];
+  const double x0 = cw[kk + 1];
+  double alpha = x0, v0 = 0.0;
+  beta = 0.0;
+  if (tail > 0.0 && kk < B - 2) {
+    const double sumsq = fma(x0, x0, tail);
+    alpha = -copysign(sqrt(sumsq), x0);
+    v0 = x0 - alpha;
+    beta = 2.0 * rcp64(fma(v0, v0, tail));
+  }
+#pragma unroll
+  for (int t = 0; t < CS; ++t) {
+    const int j = lane + 32 * t;
+    vreg[t] = beta == 0.0 ? 0.0 : (j > kk + 1 && j < B) ? col[t] : (j == kk + 1 ? v0 : 0.0);
+    vw[j] = vreg[t];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < RS; ++s) vrow[s] = vw[rowi[s]];
+  if (threadIdx.x == 0) {
+    S.d[kk] = dkk;
+    S.e[kk] = alpha;
+  }
+}
+
+template <int CL>
+__global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
+  constexpr int RS = 32 / CL;          // row slots per warp (CL * NW * RS = 256 rows)
+  constexpr int LPR = 16 / RS;         // lanes holding one reduced row value
+  constexpr int LR = NW * RS;          // rows per CTA
+  extern __shared__ __align__(16) unsigned char smraw[];
+  K2Smem& S = *reinterpret_cast<K2Smem*>(smraw);
+  const int c = (int)cl_rank();
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int B = A.B;
+  const double* __restrict__ G = A.G;
+  int rowi[RS];
+#pragma unroll
+  for (int s = 0; s < RS; ++s) rowi[s] = c + CL * w + CL * NW * s;
+  if (tid == 0) {
+    mbar_init(saddr(&S.mbar[0]), 1);
+    mbar_init(saddr(&S.mbar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const bool prof = (c == 0);
+  if (prof) stamp(0);
+  long long tc = clock64();
+  CLK_DECL
+
+  double a[RS][CS];
+  // ================= phase 1: blocked sweep of G + ridge I =================
+#pragma unroll
+  for (int s = 0; s < RS; ++s)
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int i = rowi[s], j = lane + 32 * t;
+      a[s][t] = (i < B && j < B) ? G[(size_t)i * B + j] + (i == j ? A.ridge : 0.0) : 0.0;
+    }
+  for (int k0 = 0, blk = 0; k0 < B; k0 += NB, ++blk) {
+    const int kb = min(NB, B - k0), t0 = k0 >> 5, L0 = k0 & 31;
+    double* colK = S.colK[blk & 1];
+    {   // all-gather the pivot-block columns of every row: lane L owns the pair
+        // (row slot, column) = (L % 8RS) / 8, L % 8 and 8 of the CL destinations
+      const int pr = lane % (8 * RS), sp = pr >> 3, q = pr & 7;
+      double val = 0.0;
+#pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        const double tmp = __shfl_sync(FULL, sel(a[s], t0), L0 + q);
+        if (s == sp) val = tmp;
+      }
+      const int i = rowi[0] + CL * NW * sp;
+      if (i < B && q < kb) {
+        const unsigned la = saddr(&colK[i * NB + q]);
+        const int d0 = lane / (8 * RS);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) st_cl(mapa(la, d0 + u * (CL / 8)), val);
+      }
+    }
+    ACC(5);
+    cl_sync();
+    ACC(6);
+    // Cholesky of the kb x kb pivot block by warp 0 (lane L holds entries
+    // (L>>2, 2(L&3)) and (L>>2, 2(L&3)+1); padding = identity)
+    if (w == 0) {
+      const int r = lane >> 2, q0 = 2 * (lane & 3);
+      double e0 = (r < kb && q0 < kb) ? colK[(k0 + r) * NB + q0] : (r == q0 ? 1.0 : 0.0);
+      double e1 = (r < kb && q0 + 1 < kb) ? colK[(k0 + r) * NB + q0 + 1] : (r == q0 + 1 ? 1.0 : 0.0);
+      for (int p = 0; p < kb; ++p) {
+        const double mine = (p & 1) ? e1 : e0;
+        double pp = __shfl_sync(FULL, mine, (p << 2) + (p >> 1));
+        const double rp = __shfl_sync(FULL, mine, (r << 2) + (p >> 1));
+        const double tq0 = __shfl_sync(FULL, mine, (q0 << 2) + (p >> 1));
+        const double tq1 = __shfl_sync(FULL, mine, ((q0 + 1) << 2) + (p >> 1));
+        if (!(pp > 0.0)) {   // not SPD (cannot happen for ridge > 0 in exact arithmetic)
+          if (lane == 0) A.ws.flags[0] = 1.0;
+          pp = 1e-300;
         }
+        const double lpp = sqrt(pp);
+        const double il = rcp64(lpp);
+        const double lrp = (r == p) ? lpp : (r > p ? rp * il : 0.0);
+        const double lq0 = q0 > p ? tq0 * il : 0.0, lq1 = q0 + 1 > p ? tq1 * il : 0.0;
+        e0 = (q0 == p) ? lrp : (q0 > p ? fma(-lrp, lq0, e0) : e0);
+        e1 = (q0 + 1 == p) ? lrp : (q0 + 1 > p ? fma(-lrp, lq1, e1) : e1);
+        if (lane == 0) S.Lr[p] = il;
+      }
+      S.Lb[r * NB + q0] = (q0 <= r) ? e0 : 0.0;
+      S.Lb[r * NB + q0 + 1] = (q0 + 1 <= r) ? e1 : 0.0;
+    }
+    __syncthreads();
+    ACC(7);
+    // W = L^-1 A_K,j and Z = L^-T W = P^-1 A_K,j for every column j (A_K,j = colK[j]);
+    // the last kb tasks form column j of P^-1 from the unit vector e_j
+    for (int task = tid; task < B + kb; task += NT) {
+      const bool unit = task >= B;
+      const int j = unit ? task - B : task;
+      double x[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) x[r] = unit ? (r == j ? 1.0 : 0.0) : (r < kb ? colK[j * NB + r] : 0.0);
+#pragma unroll
+      for (int qq = 0; qq < NB; ++qq) {
+        double v = x[qq];
+#pragma unroll
+        for (int r = 0; r < qq; ++r) v = fma(-S.Lb[qq * NB + r], x[r], v);
+        x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
+      }
+      if (!unit) {
+#pragma unroll
+        for (int qq = 0; qq < NB; ++qq) S.Wb[qq][j] = x[qq];
+      }
+#pragma unroll
+      for (int qq = NB - 1; qq >= 0; --qq) {
+        double v = x[qq];
+#pragma unroll
+        for (int r = qq + 1; r < NB; ++r) v = fma(-S.Lb[r * NB + qq], x[r], v);
+        x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
+      }
+      if (unit) {
+#pragma unroll
+        for (int qq = 0; qq < NB; ++qq) S.Pinv[qq * NB + j] = x[qq];
+      } else {
+#pragma unroll
+        for (int qq = 0; qq < NB; ++qq) S.Zb[qq][j] = x[qq];
       }
     }
     __syncthreads();
-  }
-  if (tid < 32) {
-    // sign convention: largest |y_i| positive, lowest index on ties
-    double best = -1.0;
-    int bi = 0x7fffffff;
+    ACC(8);
+    double wi[RS][NB];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int i = l + 32 * t;
-      if (i < B && fabs(yl[t]) > best) { best = fabs(yl[t]); bi = i; }
-    }
+    for (int s = 0; s < RS; ++s)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    double ysel = 0.0;
+      for (int r = 0; r < NB; ++r) wi[s][r] = rowi[s] < B ? S.Wb[r][rowi[s]] : 0.0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t)
-      if (l + 32 * t == bi) ysel = yl[t];
-    ysel = warp_sum(ysel);   // exactly one lane holds it
-    const double sgn = ysel < 0.0 ? -1.0 : 1.0;
+    for (int t = 0; t < CS; ++t) {
+      const int j = lane + 32 * t;
+      if (j >= B) continue;
+      double wj[NB];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int i = l + 32 * t;
-      if (i < B) {
-        const double vi = sgn * yl[t];
-        ws.vtop[(size_t)i * B + kdesc] = vi;
-        if (V) V[(size_t)i * ldv + (kdesc - k0)] = vi;
-        const double si = sigma[i];
-        W[(size_t)i * ldwu + kdesc] = (float)(vi / si);
-        U[(size_t)i * ldwu + kdesc] = (float)(vi * si);
+      for (int r = 0; r < NB; ++r) wj[r] = S.Wb[r][j];
+      const int jk = j - k0;
+      const bool inj = (unsigned)jk < (unsigned)kb;
+#pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        const int i = rowi[s];
+        if (i >= B) continue;
+        const int ik = i - k0;
+        const bool ini = (unsigned)ik < (unsigned)kb;
+        if (!ini && !inj) {
+          double u = a[s][t];
+#pragma unroll
+          for (int r = 0; r < NB; ++r) u = fma(-wi[s][r], wj[r], u);
+          a[s][t] = u;
+        } else if (ini && !inj) {
+          a[s][t] = S.Zb[ik][j];
+        } else if (!ini) {
+          a[s][t] = S.Zb[jk][i];
+        } else {
+          a[s][t] = -S.Pinv[ik * NB + jk];
+        }
       }
     }
-    if (l == 0) {
-      ws.lam_top[kdesc] = lam;
-      if (lam_out) lam_out[kdesc] = lam;
+    ACC(9);
+  }
+  // a = -(G + ridge I)^-1: sigma_i = sqrt(1 / (N M_ii)), all-gathered
+#pragma unroll
+  for (int s = 0; s < RS; ++s) {
+    const int i = rowi[s];
+    if (i < B && lane == (i & 31)) {
+      const double mii = -sel(a[s], i >> 5);
+      if (!(mii > 0.0)) A.ws.flags[0] = 1.0;
+      const double sg = sqrt(1.0 / ((double)A.n * mii));
+      st_all<CL>(&S.sig[i], sg);
+      A.sigma[i] = sg;
     }
   }
-  if (blockIdx.x == 0) stamp(7);
+  if (A.want_M) {
+#pragma unroll
+    for (int s = 0; s < RS; ++s)
+#pragma unroll
+      for (int t = 0; t < CS; ++t) {
+        const int i = rowi[s], j = lane + 32 * t;
+        if (i < B && j < B) A.ws.M[(size_t)i * B + j] = -a[s][t];
+      }
+  }
+  cl_sync();
+  if (prof) stamp(1);
+  if (!A.tridiag) return;
+
+  // ================= phase 2: whitening + tridiagonalisation =================
+  const double invn = 1.0 / (double)A.n;
+  double q[RS][CS];
+#pragma unroll
+  for (int s = 0; s < RS; ++s)
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int i = rowi[s], j = lane + 32 * t;
+      a[s][t] = (i < B && j < B) ? G[(size_t)i * B + j] / (S.sig[i] * S.sig[j]) * invn : 0.0;
+      q[s][t] = (i == j && i < B) ? 1.0 : 0.0;
+    }
+  double vreg[CS], vrow[RS], beta, rrep[CS];
+  {
+    double col[CS];
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int j = lane + 32 * t;
+      col[t] = j < B ? G[(size_t)j * B] / (S.sig[j] * S.sig[0]) * invn : 0.0;
+      rrep[t] = j < B ? G[(size_t)j * B + 1] / (S.sig[j] * S.sig[1]) * invn : 0.0;
+    }
+    form_reflector<RS>(col, 0, B, lane, w, rowi, vreg, vrow, beta, S);
+  }
+  // lanes [0,16) carry p rows, lanes [16,32) carry Q v rows / column k+2 entries
+  const int sp = (lane & 15) / LPR;
+  const int ip = rowi[0] + CL * NW * sp;
+  const int dA = lane % LPR;
+  const unsigned xbytes = 16u * (unsigned)B;   // p and column k+2 entry of every row
+  if (tid == 0) {
+    mbar_expect(saddr(&S.mbar[0]), xbytes);
+    if (B - 3 >= 1) mbar_expect(saddr(&S.mbar[1]), xbytes);
+  }
+  tc = clock64();
+  for (int k = 0; k <= B - 3; ++k) {
+    const int par = k & 1;
+    const int tmin = (k + 1) >> 5;   // first column slot holding any j > k
+    // (a) p = beta A v on the live rows and Q v on all rows, one fused reduction
+    double x2[2 * RS];
+#pragma unroll
+    for (int s = 0; s < RS; ++s) {
+      double pa = 0.0, pq = 0.0;
+#pragma unroll
+      for (int t = 0; t < CS; ++t)
+        if (t >= tmin) {
+          pa = fma(a[s][t], vreg[t], pa);
+          pq = fma(q[s][t], vreg[t], pq);
+        }
+      x2[s] = (rowi[s] > k) ? pa : 0.0;
+      x2[RS + s] = pq;
+    }
+    const double red = reduceT<2 * RS>(x2, lane);
+    double xv = 0.0;
+    {
+      const int t2 = (k + 2) >> 5, l2 = (k + 2) & 31;
+#pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        const double tmp = __shfl_sync(FULL, sel(a[s], t2), l2);
+        if (s == sp) xv = tmp;
+      }
+    }
+    if (ip < B) {
+      const bool isp = lane < 16;
+      const double val = isp ? ((ip > k) ? beta * red : 0.0) : xv;
+      const unsigned la = saddr(isp ? &S.pbuf[par][ip] : &S.xbuf[par][ip]);
+      const unsigned mb = saddr(&S.mbar[par]);
+#pragma unroll
+      for (int u = 0; u < CL / LPR; ++u) st_async(mapa(la, dA + u * LPR), val, mapa(mb, dA + u * LPR));
+    }
+    ACC(10);
+    // Q <- Q H_k while the exchange is in flight
+    if (beta != 0.0) {
+#pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        const double qv = beta * __shfl_sync(FULL, red, 16 + LPR * s);
+#pragma unroll
+        for (int t = 0; t < CS; ++t)
+          if (t >= tmin) q[s][t] = fma(-qv, vreg[t], q[s][t]);
+      }
+    }
+    ACC(11);
+    mbar_wait(saddr(&S.mbar[par]), (unsigned)(k >> 1) & 1u);
+    if (tid == 0 && k + 2 <= B - 3) mbar_expect(saddr(&S.mbar[par]), xbytes);
+    ACC(12);
+    // (b) w = p - (beta/2)(p.v) v; A <- A - v w^T - w v^T on the live block
+    const double* pb = S.pbuf[par];
+    double wreg[CS], wrow[RS];
+    double Kc;
+    {
+      double pv = 0.0;
+#pragma unroll
+      for (int t = 0; t < CS; ++t) {
+        wreg[t] = lane + 32 * t < B ? pb[lane + 32 * t] : 0.0;
+        pv = fma(wreg[t], vreg[t], pv);
+      }
+      Kc = 0.5 * beta * warp_sum(pv);
+#pragma unroll
+      for (int t = 0; t < CS; ++t) wreg[t] = fma(-Kc, vreg[t], wreg[t]);
+#pragma unroll
+      for (int s = 0; s < RS; ++s) wrow[s] = rowi[s] < B ? fma(-Kc, vrow[s], pb[rowi[s]]) : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < RS; ++s)
+      if (rowi[s] > k) {
+#pragma unroll
+        for (int t = 0; t < CS; ++t)
+          if (t >= tmin) a[s][t] = fma(-wrow[s], vreg[t], fma(-vrow[s], wreg[t], a[s][t]));
+      }
+    // replica of column k+1 (-> through update k) and the arrived column k+2 (-> through update k)
+    const double* vw = S.vw[w];
+    const double v1 = vw[k + 1], v2 = vw[k + 2];
+    const double w1 = fma(-Kc, v1, pb[k + 1]), w2 = fma(-Kc, v2, pb[k + 2]);
+    double xn[CS];
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int j = lane + 32 * t;
+      rrep[t] = fma(-wreg[t], v1, fma(-vreg[t], w1, rrep[t]));
+      xn[t] = j < B ? fma(-wreg[t], v2, fma(-vreg[t], w2, S.xbuf[par][j])) : 0.0;
+    }
+    ACC(13);
+    // (c) reflector k+1
+    form_reflector<RS>(rrep, k + 1, B, lane, w, rowi, vreg, vrow, beta, S);
+#pragma unroll
+    for (int t = 0; t < CS; ++t) rrep[t] = xn[t];
+    ACC(14);
+  }
+  // rrep = column B-1 after the last update: d_{B-1}
+  {
+    const double dl = __shfl_sync(FULL, sel(rrep, (B - 1) >> 5), (B - 1) & 31);
+    if (tid == 0) { S.d[B - 1] = dl; S.e[B - 1] = 0.0; }
+  }
+  __syncthreads();
+  double glo, ghi;
+  tri_bounds(S.d, S.e, S.e2, B, S.red, glo, ghi);
+  if (c == 0) {
+    for (int i = tid; i < B; i += NT) { A.tri[i] = S.d[i]; A.tri[B + i] = S.e[i]; A.tri[2 * B + i] = S.e2[i]; }
+    if (tid == 0) { A.tri[3 * B] = glo; A.tri[3 * B + 1] = ghi; }
+  }
+#pragma unroll
+  for (int s = 0; s < RS; ++s)
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int i = rowi[s], j = lane + 32 * t;
+      if (i < B && j < B) A.ws.Q[(size_t)i * B + j] = q[s][t];
+    }
+  if (prof) stamp(2);
+  const int K = A.K;
+  if (K <= 0) {
+    CLK_FLUSH
+    return;
+  }
+
+  // ================= phase 3: eigenpairs of the first chunk =================
+  const double tnorm = fmax(fabs(glo), fabs(ghi));
+  for (int kd = c; kd < K; kd += CL) {
+    tc = clock64();
+    const double lam = bisect_one(S.d, S.e2, B, glo, ghi, B - 1 - kd, S.qsh);
+    ACC(16);
+    if (tid == 0) inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
+    __syncthreads();
+    ACC(17);
+    for (int j = tid; j < B; j += NT) st_all<CL>(&S.zb[kd][j], S.y[j]);
+    if (tid == 0) {
+      st_all<CL>(&S.lamk[kd], lam);
+      A.ws.lam_top[kd] = lam;
+      if (A.lam_out) A.lam_out[kd] = lam;
+    }
+    __syncthreads();
+  }
+  cl_sync();
+  if (prof) stamp(3);
+  // Gram-Schmidt inside groups of numerically coincident eigenvalues (usually
+  // a no-op); every CTA does the same arithmetic on its copy of Z
+  if (w == 0) {
+    for (int j = 1; j < K; ++j) {
+      bool touched = false;
+      for (int i = 0; i < j; ++i) {
+        if (fabs(S.lamk[i] - S.lamk[j]) > 1e-9 * tnorm) continue;
+        double dot = 0.0;
+        for (int t = lane; t < B; t += 32) dot = fma(S.zb[i][t], S.zb[j][t], dot);
+        dot = warp_sum(dot);
+        for (int t = lane; t < B; t += 32) S.zb[j][t] = fma(-dot, S.zb[i][t], S.zb[j][t]);
+        __syncwarp();
+        touched = true;
+      }
+      if (!touched) continue;
+      double ss = 0.0;
+      for (int t = lane; t < B; t += 32) ss = fma(S.zb[j][t], S.zb[j][t], ss);
+      ss = 1.0 / sqrt(warp_sum(ss));
+      for (int t = lane; t < B; t += 32) S.zb[j][t] *= ss;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (c == 0)
+    for (int x = tid; x < K * B; x += NT) A.ws.ztop[(size_t)(x / B) * B + x % B] = S.zb[x / B][x % B];
+  // V = Q Z on the owned rows
+  for (int kk = 0; kk < K; ++kk) {
+    double vs[RS];
+#pragma unroll
+    for (int s = 0; s < RS; ++s) vs[s] = 0.0;
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int j = lane + 32 * t;
+      const double zj = j < B ? S.zb[kk][j] : 0.0;
+#pragma unroll
+      for (int s = 0; s < RS; ++s) vs[s] = fma(q[s][t], zj, vs[s]);
+    }
+    const double vsum = reduceT<RS>(vs, lane);
+    const int sv = lane / (32 / RS);
+    if (lane % (32 / RS) == 0) S.vrow[kk][w * RS + sv] = (rowi[0] + CL * NW * sv < B) ? vsum : 0.0;
+  }
+  __syncthreads();
+  // sign: cluster-wide argmax |V_ik| (lowest index on ties) per eigenvector
+  for (int kk = w; kk < K; kk += NW) {
+    const int lr = lane;   // local row index = warp * RS + slot
+    const int i = c + CL * (lr / RS) + CL * NW * (lr % RS);
+    const bool ok = lr < LR && i < B;
+    const double v = ok ? S.vrow[kk][lr] : 0.0;
+    double best = ok ? fabs(v) : -1.0;
+    int bi = ok ? i : 0x7fffffff;
+    double bv = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(FULL, best, o);
+      const int oi = __shfl_xor_sync(FULL, bi, o);
+      const double ov = __shfl_xor_sync(FULL, bv, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; bv = ov; }
+    }
+    if (lane == 0) {
+      st_all<CL>(&S.am[c][kk], best);
+      st_all<CL>(&S.av[c][kk], bv);
+      const unsigned a0 = saddr(&S.ai[c][kk]);
+#pragma unroll
+      for (int r = 0; r < CL; ++r) st_cl_i(mapa(a0, r), bi);
+    }
+  }
+  cl_sync();
+  // write the owned rows: vtop (fp64), W = S v, U = S^-1 v (fp32), V
+  for (int x = tid; x < K * LR; x += NT) {
+    const int kk = x / LR, lr = x % LR;
+    const int i = c + CL * (lr / RS) + CL * NW * (lr % RS);
+    if (i >= B) continue;
+    double best = -1.0, bv = 0.0;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      const double ob = S.am[r][kk];
+      const int oi = S.ai[r][kk];
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; bv = S.av[r][kk]; }
+    }
+    const double vi = (bv < 0.0 ? -1.0 : 1.0) * S.vrow[kk][lr];
+    const double si = S.sig[i];
+    A.ws.vtop[(size_t)i * B + kk] = vi;
+    if (A.V) A.V[(size_t)i * A.ldv + kk] = vi;
+    A.W[(size_t)i * A.ldwu + kk] = (float)(vi / si);
+    A.U[(size_t)i * A.ldwu + kk] = (float)(vi * si);
+  }
+  if (prof) stamp(4);
+  CLK_FLUSH
+  (void)tc;
 }
 
 // =====================================================================
-// K2e: re-orthogonalise numerically coincident eigenvalues (usually no-op)
+// later chunks: eigenpairs k0 .. k0+K-1 from T and Q in global memory
 // =====================================================================
-__global__ void __launch_bounds__(256) reorth_kernel(const double* __restrict__ tri, EigWs ws,
-                                                     const double* __restrict__ sigma, int B, int k0, int K,
-                                                     double* V, int ldv, float* W, float* U, int ldwu) {
+struct MoreSmem {
+  double d[BM], e[BM], e2[BM];
+  double dd[BM], u1[BM], u2[BM], ml[BM], y[BM];
+  unsigned char piv[BM];
+  double red[4 * NW];
+  int qsh[NW];
+};
+
+// one CTA per eigenpair (values_only: eigenvalues of every requested index)
+__global__ void __launch_bounds__(NT) more_pairs_kernel(const double* __restrict__ tri, EigWs ws, int B, int k0,
+                                                        int values_only, double* lam_out) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  MoreSmem& S = *reinterpret_cast<MoreSmem*>(smraw);
+  const int kd = k0 + blockIdx.x, tid = threadIdx.x;
+  for (int i = tid; i < B; i += NT) { S.d[i] = tri[i]; S.e[i] = tri[B + i]; S.e2[i] = tri[2 * B + i]; }
+  __syncthreads();
+  const double glo = tri[3 * B], ghi = tri[3 * B + 1];
+  const double lam = bisect_one(S.d, S.e2, B, glo, ghi, B - 1 - kd, S.qsh);
+  if (values_only) {
+    if (tid == 0) lam_out[kd] = lam;
+    return;
+  }
+  const double tnorm = fmax(fabs(glo), fabs(ghi));
+  if (tid == 0) {
+    inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
+    ws.lam_top[kd] = lam;
+    if (lam_out) lam_out[kd] = lam;
+  }
+  __syncthreads();
+  for (int i = tid; i < B; i += NT) ws.ztop[(size_t)kd * B + i] = S.y[i];
+}
+
+// Gram-Schmidt of z_j (j in [k0, k0+K)) against every earlier z_i with a
+// numerically coincident eigenvalue (one warp, sequential like the first chunk)
+__global__ void __launch_bounds__(32) more_reorth_kernel(const double* __restrict__ tri, EigWs ws, int B, int k0,
+                                                         int K) {
   const double tnorm = fmax(fabs(tri[3 * B]), fabs(tri[3 * B + 1]));
-  const int l = threadIdx.x & 31;
-  if (threadIdx.x >= 32) return;
+  const int l = threadIdx.x;
   for (int j = max(k0, 1); j < k0 + K; ++j) {
     bool touched = false;
+    double* zj = ws.ztop + (size_t)j * B;
     for (int i = 0; i < j; ++i) {
       if (fabs(ws.lam_top[i] - ws.lam_top[j]) > 1e-9 * tnorm) continue;
+      const double* zi = ws.ztop + (size_t)i * B;
       double dot = 0.0;
-      for (int t = l; t < B; t += 32) dot = fma(ws.vtop[(size_t)t * B + i], ws.vtop[(size_t)t * B + j], dot);
+      for (int t = l; t < B; t += 32) dot = fma(zi[t], zj[t], dot);
       dot = warp_sum(dot);
-      for (int t = l; t < B; t += 32) ws.vtop[(size_t)t * B + j] -= dot * ws.vtop[(size_t)t * B + i];
+      for (int t = l; t < B; t += 32) zj[t] = fma(-dot, zi[t], zj[t]);
       __syncwarp();
       touched = true;
     }
     if (!touched) continue;
     double s = 0.0;
-    for (int t = l; t < B; t += 32) s = fma(ws.vtop[(size_t)t * B + j], ws.vtop[(size_t)t * B + j], s);
+    for (int t = l; t < B; t += 32) s = fma(zj[t], zj[t], s);
     s = 1.0 / sqrt(warp_sum(s));
-    double best = -1.0;
-    int bi = 0x7fffffff;
-    for (int t = l; t < B; t += 32) {
-      const double a = fabs(ws.vtop[(size_t)t * B + j]);
-      if (a > best) { best = a; bi = t; }
-    }
+    for (int t = l; t < B; t += 32) zj[t] *= s;
+    __syncwarp();
+  }
+}
+
+// v_k = Q z_k, sign fix, W/U/vtop (one CTA per vector)
+__global__ void __launch_bounds__(NT) more_vec_kernel(EigWs ws, const double* __restrict__ sigma, int B, int k0,
+                                                      double* V, int ldv, float* W, float* U, int ldwu) {
+  __shared__ double z[BM], v[BM];
+  __shared__ double bbest[NW];
+  __shared__ int bidx[NW];
+  const int kd = k0 + blockIdx.x, tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  for (int i = tid; i < B; i += NT) z[i] = ws.ztop[(size_t)kd * B + i];
+  __syncthreads();
+  for (int i = w; i < B; i += NW) {
+    const double* qi = ws.Q + (size_t)i * B;
+    double acc = 0.0;
+    for (int j = l; j < B; j += 32) acc = fma(qi[j], z[j], acc);
+    acc = warp_sum(acc);
+    if (l == 0) v[i] = acc;
+  }
+  __syncthreads();
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int i = tid; i < B; i += NT)
+    if (fabs(v[i]) > best) { best = fabs(v[i]); bi = i; }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    const double sg = ws.vtop[(size_t)bi * B + j] < 0.0 ? -s : s;
-    __syncwarp();
-    for (int t = l; t < B; t += 32) {
-      const double vi = ws.vtop[(size_t)t * B + j] * sg;
-      ws.vtop[(size_t)t * B + j] = vi;
-      if (V && j >= k0) V[(size_t)t * ldv + (j - k0)] = vi;
-      W[(size_t)t * ldwu + j] = (float)(vi / sigma[t]);
-      U[(size_t)t * ldwu + j] = (float)(vi * sigma[t]);
-    }
-    __syncwarp();
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(FULL, best, o);
+    const int oi = __shfl_xor_sync(FULL, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if (l == 0) { bbest[w] = best; bidx[w] = bi; }
+  __syncthreads();
+  best = bbest[0];
+  bi = bidx[0];
+  for (int q = 1; q < NW; ++q)
+    if (bbest[q] > best || (bbest[q] == best && bidx[q] < bi)) { best = bbest[q]; bi = bidx[q]; }
+  const double sg = v[bi] < 0.0 ? -1.0 : 1.0;
+  for (int i = tid; i < B; i += NT) {
+    const double vi = sg * v[i];
+    ws.vtop[(size_t)i * B + kd] = vi;
+    if (V) V[(size_t)i * ldv + (kd - k0)] = vi;
+    W[(size_t)i * ldwu + kd] = (float)(vi / sigma[i]);
+    U[(size_t)i * ldwu + kd] = (float)(vi * sigma[i]);
   }
 }
 
 // residual_b = (M Y)_b / M_bb with M = (G + ridge I)^-1 (noise estimate output)
-__global__ void __launch_bounds__(256) inverse_cols_kernel(EigWs ws, int B, double* Minv) {
-  // column b of M = L^-T L^-1 e_b: one warp per column: x = L^-1 e_b, then M e_b = L^-T x
-  __shared__ double xs[8][256];
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + w;
-  if (b >= B) return;
-  double* x = xs[w];
-  for (int i = l; i < B; i += 32) x[i] = 0.0;
-  __syncwarp();
-  const double* L = ws.Lp;
-  for (int i = b; i < B; ++i) {
-    double s = 0.0;
-    for (int j = b + l; j < i; j += 32) s = fma(L[off(i) + j], x[j], s);
-    s = warp_sum(s);
-    if (l == 0) x[i] = ((i == b ? 1.0 : 0.0) - s) * ws.rdiag[i];
-    __syncwarp();
-  }
-  // back substitution with L^T: z_i = (x_i - sum_{j>i} L_ji z_j) / L_ii
-  for (int i = B - 1; i >= 0; --i) {
-    double s = 0.0;
-    for (int j = i + 1 + l; j < B; j += 32) s = fma(L[off(j) + i], x[j], s);
-    s = warp_sum(s);
-    if (l == 0) x[i] = (x[i] - s) * ws.rdiag[i];
-    __syncwarp();
-  }
-  for (int i = l; i < B; i += 32) Minv[(size_t)i * B + b] = x[i];
-}
-
 __global__ void residual_kernel(const float* __restrict__ Y, long long n, int B, const double* __restrict__ M,
                                 float* __restrict__ out) {
   long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -823,45 +1038,80 @@ __global__ void residual_kernel(const float* __restrict__ Y, long long n, int B,
   out[(size_t)b * n + p] = (float)(s / M[(size_t)b * B + b]);
 }
 
+int g_cluster = 0;   // cluster size chosen at the first launch (16, else 8)
+
+template <int CL>
+cudaLaunchConfig_t k2_config(cudaLaunchAttribute* attr, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = sizeof(K2Smem);
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+template <int CL>
+cudaError_t prepare_k2() {
+  cudaError_t e = cudaFuncSetAttribute(k2_cluster_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(K2Smem));
+  if (e == cudaSuccess && CL > 8)
+    e = cudaFuncSetAttribute(k2_cluster_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
+
+template <int CL>
+bool cluster_fits() {
+  if (prepare_k2<CL>() != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = k2_config<CL>(attr, 0);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k2_cluster_kernel<CL>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return n >= 1;
+}
+
+template <int CL>
+cudaError_t launch_k2(const K2Args& a, cudaStream_t st) {
+  cudaError_t e = prepare_k2<CL>();
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = k2_config<CL>(attr, st);
+  return cudaLaunchKernelEx(&cfg, k2_cluster_kernel<CL>, a);
+}
+
 }  // namespace
 
 extern "C" hyde_status hyde_debug_eig_clocks(long long* out) {
   if (!out) return HYDE_EPARAM;
-  return cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(long long) * 16) == cudaSuccess ? HYDE_OK : HYDE_ECUDA;
+  return cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(long long) * 32) == cudaSuccess ? HYDE_OK : HYDE_ECUDA;
 }
 
-static const size_t kMaxSmem = 227 * 1024 - 1024;   // dynamic budget (static smem is separate)
+size_t eig_workspace_doubles(int B) { return 4 * (size_t)B * B + (size_t)B + 8 + 64; }
 
-size_t eig_workspace_doubles(int B) {
-  const size_t P = (size_t)B * (B + 1) / 2;
-  return 3 * (size_t)B * B + 3 * (size_t)B + 8 + P + 64;
+static cudaError_t run_k2(const K2Args& a, cudaStream_t st) {
+  if (g_cluster == 0) g_cluster = cluster_fits<16>() ? 16 : 8;
+  return g_cluster == 16 ? launch_k2<16>(a, st) : launch_k2<8>(a, st);
 }
 
-static cudaError_t run_chol(const double* G, int B, double ridge, const EigWs& ws, cudaStream_t st) {
-  const size_t P = (size_t)B * (B + 1) / 2;
-  const size_t smem = P * sizeof(double);
-  cudaError_t e;
-  if (smem <= kMaxSmem) {
-    e = cudaFuncSetAttribute(chol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    chol_kernel<true><<<1, CT, smem, st>>>(G, B, ridge, ws);
-  } else {
-    chol_kernel<false><<<1, CT, 0, st>>>(G, B, ridge, ws);
-  }
-  return cudaGetLastError();
-}
-
-static size_t eigpair_smem(int B) {
-  return (size_t)B * 8 * sizeof(double) + (size_t)((B + 15) & ~15) + 2 * (size_t)RB * B * sizeof(double) + 64;
-}
-
-static cudaError_t run_eigpairs(const double* tri, const EigWs& ws, const double* sigma, int B, int k0, int K,
-                                double* lam, double* V, int ldv, float* W, float* U, int ldwu, cudaStream_t st) {
-  const size_t smem = eigpair_smem(B);
-  cudaError_t e = cudaFuncSetAttribute(eigpair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static cudaError_t run_more(const double* tri, const EigWs& ws, const double* sigma, int B, int k0, int K,
+                            double* lam, double* V, int ldv, float* W, float* U, int ldwu, cudaStream_t st) {
+  const size_t smem = sizeof(MoreSmem);
+  cudaError_t e = cudaFuncSetAttribute(more_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  eigpair_kernel<<<K, EP_T, smem, st>>>(tri, ws, sigma, B, k0, 0, lam, V, ldv, W, U, ldwu);
-  reorth_kernel<<<1, 256, 0, st>>>(tri, ws, sigma, B, k0, K, V, ldv, W, U, ldwu);
+  more_pairs_kernel<<<K, NT, smem, st>>>(tri, ws, B, k0, 0, lam);
+  more_reorth_kernel<<<1, 32, 0, st>>>(tri, ws, B, k0, K);
+  more_vec_kernel<<<K, NT, 0, st>>>(ws, sigma, B, k0, V, ldv, W, U, ldwu);
   return cudaGetLastError();
 }
 
@@ -869,36 +1119,37 @@ static cudaError_t run_eigpairs(const double* tri, const EigWs& ws, const double
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house, double* tri, float* W, float* U,
                              int ldwu, cudaStream_t st) {
+  if (B > BM || B < 3) return cudaErrorInvalidValue;
   const EigWs ws = carve(house, B);
   cudaError_t e = cudaMemsetAsync(ws.flags, 0, 8 * sizeof(double), st);
   if (e != cudaSuccess) return e;
-  e = run_chol(G, B, ridge, ws, st);
-  if (e != cudaSuccess) return e;
-  invdiag_kernel<<<(B + 7) / 8, 256, 0, st>>>(ws, B, n, sigma);
-  e = cudaGetLastError();
-  if (e != cudaSuccess || ncomp < 0) return e;
-  const size_t P = (size_t)B * (B + 1) / 2;
-  const size_t ext = (size_t)(4 * B + TW + 8) * sizeof(double);
-  if (ext + P * sizeof(double) <= kMaxSmem) {
-    e = cudaFuncSetAttribute(tridiag_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(ext + P * sizeof(double)));
-    if (e != cudaSuccess) return e;
-    tridiag_kernel<true><<<1, TT, ext + P * sizeof(double), st>>>(G, sigma, n, B, ws, tri);
-  } else {
-    tridiag_kernel<false><<<1, TT, ext, st>>>(G, sigma, n, B, ws, tri);
-  }
-  e = cudaGetLastError();
+  K2Args a;
+  a.G = G;
+  a.n = n;
+  a.B = B;
+  a.ridge = ridge;
+  a.K = ncomp > 0 ? (ncomp < KM ? ncomp : KM) : 0;
+  a.tridiag = (ncomp >= 0) ? 1 : 0;
+  a.want_M = (ncomp < 0) ? 1 : 0;   // estimate_noise: M feeds the residual
+  a.sigma = sigma;
+  a.tri = tri;
+  a.ws = ws;
+  a.lam_out = all_lam ? nullptr : lam;
+  a.V = V;
+  a.ldv = ncomp > 0 ? ncomp : 1;
+  a.W = W;
+  a.U = U;
+  a.ldwu = ldwu;
+  e = run_k2(a, st);
   if (e != cudaSuccess) return e;
   if (all_lam && lam) {
-    const size_t smem = eigpair_smem(B);
-    e = cudaFuncSetAttribute(eigpair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = sizeof(MoreSmem);
+    e = cudaFuncSetAttribute(more_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    eigpair_kernel<<<B, EP_T, smem, st>>>(tri, ws, sigma, B, 0, 1, lam, nullptr, 0, W, U, ldwu);
+    more_pairs_kernel<<<B, NT, smem, st>>>(tri, ws, B, 0, 1, lam);
     e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
   }
-  if (ncomp > 0) return run_eigpairs(tri, ws, sigma, B, 0, ncomp, nullptr, V, ncomp, W, U, ldwu, st);
-  return cudaSuccess;
+  return e;
 }
 
 cudaError_t launch_eigvec_more(const double* tri, const double* house, const double* sigma, int B, int k0,
@@ -906,18 +1157,16 @@ cudaError_t launch_eigvec_more(const double* tri, const double* house, const dou
                                cudaStream_t st) {
   (void)lam_top_unused;
   const EigWs ws = carve(const_cast<double*>(house), B);
-  return run_eigpairs(tri, ws, sigma, B, k0, ncomp, nullptr, V, ncomp, W, U, ldwu, st);
+  return run_more(tri, ws, sigma, B, k0, ncomp, nullptr, V, ncomp, W, U, ldwu, st);
 }
 
 cudaError_t launch_noise_residual(const float* Y, long long n, int B, const double* G, double ridge, double* work,
                                   float* out, cudaStream_t st) {
-  // work: the K2 buffer (Cholesky factor already computed by launch_noise_eig) + B*B for M
+  // work: the K2 buffer; launch_noise_eig(ncomp < 0) already wrote M = (G + ridge I)^-1
   (void)G;
   (void)ridge;
   const EigWs ws = carve(work, B);
-  double* M = ws.Aw;   // P >= ... use the trailing region (B*B doubles needed)
-  inverse_cols_kernel<<<(B + 7) / 8, 256, 0, st>>>(ws, B, M);
   dim3 grid((unsigned)((n + 255) / 256), B);
-  residual_kernel<<<grid, 256, 0, st>>>(Y, n, B, M, out);
+  residual_kernel<<<grid, 256, 0, st>>>(Y, n, B, ws.M, out);
   return cudaGetLastError();
 }
