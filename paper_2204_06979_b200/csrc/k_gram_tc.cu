@@ -32,9 +32,9 @@ namespace {
 
 constexpr int KC = 128;        // pixels (bytes per int8 row) per stage
 constexpr int NI = 4;          // int8 stages
-constexpr int NCW = 16;        // converter warps
+constexpr int NCW = 14;        // converter warps
 constexpr int NTHREADS = (NCW + 2) * 32;
-constexpr int MAXU = 12;       // max units per converter warp per stage
+constexpr int MAXU = 8;        // max units per converter warp per stage: (8 + 96/16) x 8 / 14
 constexpr int TMEM_COLS = 512;
 
 struct GramTc {
@@ -49,17 +49,22 @@ struct GramTc {
   int* nonfinite;
 };
 
-// smem regions of one int8 slice of a stage: P (64 rows), QA (64 rows), QB (nb/2 rows)
-__device__ __forceinline__ int region_rows(int rg, int nb) { return rg == 2 ? nb / 2 : 64; }
+// smem regions of one int8 slice of a stage: P (64 rows: S_a bands of this SM)
+// and QS (64 rows: this SM's half of S_b, nb/2 live rows then zeros).  QS is
+// both the A operand of T_bb and -- its first nb/2 rows -- this SM's half of
+// the B operand of T_ab and T_bb, so every band is read from HBM once.
+__device__ __forceinline__ int region_rows(int rg, int nb) { return 64; }
 __device__ __forceinline__ int region_base(int rg) { return rg * 64 * KC; }
 
 __device__ __forceinline__ int band_of(int region, int r, int rank, int B, int nb) {
   int b;
-  if (region == 0) b = rank * 64 + r;                       // P : S_a rows of this SM
-  else if (region == 1) b = 128 + rank * 64 + r;            // QA: S_b rows of this SM (T_bb A)
-  else b = 128 + rank * (nb / 2) + r;                       // QB: S_b B-operand half
-  const int lim = region == 0 ? (B < 128 ? B : 128) : B;
-  return b < lim ? b : -1;
+  if (region == 0) {
+    b = rank * 64 + r;                                      // P : S_a rows of this SM
+    return b < (B < 128 ? B : 128) ? b : -1;
+  }
+  if (r >= nb / 2) return -1;                               // QS padding rows
+  b = 128 + rank * (nb / 2) + r;                            // QS: S_b rows of this SM
+  return b < B ? b : -1;
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
@@ -69,14 +74,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   __shared__ __align__(8) uint64_t bar_empty[NI];
   __shared__ __align__(8) uint64_t bar_done;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float inv_s[3][64];
-  __shared__ double s_of[3][64];
+  __shared__ float inv_s[2][64];
+  __shared__ double s_of[2][64];
 
   const int rank = (int)tc::cluster_ctarank();
   const int pair = blockIdx.x >> 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int B = P.B, nb = P.nb;
-  const int nreg = B > 128 ? 3 : 1;
+  const int nreg = B > 128 ? 2 : 1;
   const int slice_bytes = P.rows_tot * KC;
   const int stage_bytes = 2 * slice_bytes;
   const long long p_begin = (long long)pair * P.per_pair;
@@ -84,7 +89,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const int nst = p_end > p_begin ? (int)((p_end - p_begin + KC - 1) / KC) : 0;
 
   // per-band quantisation scales of the rows this SM handles
-  for (int i = threadIdx.x; i < 3 * 64; i += NTHREADS) {
+  for (int i = threadIdx.x; i < 2 * 64; i += NTHREADS) {
     const int rg = i / 64, r = i % 64;
     float is = 0.f;
     double sv = 0.0;
@@ -98,6 +103,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     inv_s[rg][r] = is;
     s_of[rg][r] = sv;
+  }
+  if (nreg == 2) {   // QS rows [nb/2, 64) stay zero in every stage and slice
+    const int g0 = (nb / 2) / 8;
+    for (int i = threadIdx.x; i < NI * 2 * (8 - g0) * (KC / 16) * 32; i += NTHREADS) {
+      const int w4 = i & 31, rest = i >> 5;
+      const int c = rest % (KC / 16), rest2 = rest / (KC / 16);
+      const int g = g0 + rest2 % (8 - g0), sl = rest2 / (8 - g0);   // sl = stage*2 + slice
+      const int off = sl * slice_bytes + region_base(1) + c * (64 * 16) + g * 128 + w4 * 4;
+      *reinterpret_cast<uint32_t*>(smem + off) = 0u;
+    }
+    tc::fence_proxy_async_smem();
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NI; ++i) {
@@ -145,14 +161,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           tc::mma_i8<2>(tmem + 2 * CL, dsc(st1, 0, 0), dsc(st1, 0, 0), id_aa, first);
           if (nb > 0) {
             // T_ab: A = P, B = QB ; T_bb: A = QA, B = QB
-            tc::mma_i8<2>(tmem + 0 * CL + off_ab, dsc(st0, 0, 0), dsc(st0, 2, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st0, 0, 0), dsc(st1, 2, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st1, 0, 0), dsc(st0, 2, 0), id_b, 1u);
-            tc::mma_i8<2>(tmem + 2 * CL + off_ab, dsc(st1, 0, 0), dsc(st1, 2, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 0 * CL + off_bb, dsc(st0, 1, 0), dsc(st0, 2, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1, 0), dsc(st1, 2, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st1, 1, 0), dsc(st0, 2, 0), id_b, 1u);
-            tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1, 0), dsc(st1, 2, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 0 * CL + off_ab, dsc(st0, 0, 0), dsc(st0, 1, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st0, 0, 0), dsc(st1, 1, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st1, 0, 0), dsc(st0, 1, 0), id_b, 1u);
+            tc::mma_i8<2>(tmem + 2 * CL + off_ab, dsc(st1, 0, 0), dsc(st1, 1, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 0 * CL + off_bb, dsc(st0, 1, 0), dsc(st0, 1, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1, 0), dsc(st1, 1, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st1, 1, 0), dsc(st0, 1, 0), id_b, 1u);
+            tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1, 0), dsc(st1, 1, 0), id_b, first);
           }
         }
         tc::mma_commit<2>(&bar_empty[is], 0x3);
@@ -163,22 +179,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     // ================= converters: HBM fp32 -> int8 slices in smem ==========
     const int cw = warp - 2;
     constexpr int cols16 = KC / 16;
-    // units of work = (region, 8-row group, 16-pixel column); regions P, QA hold 64 rows
-    const int nunits = nreg == 1 ? 8 * cols16 : (16 + nb / 16) * cols16;
+    // units of work = (region, 8-row group, 16-pixel column); P has 8 groups,
+    // QS nb/16 live groups (its zero groups were written once above)
+    const int nunits = nreg == 1 ? 8 * cols16 : (8 + nb / 16) * cols16;
     const bool vec_ok = (P.n % 4 == 0) && (((uintptr_t)P.Y & 15) == 0);
     bool bad = false;
-    for (int s = 0; s < nst; ++s) {
-      const int is = s % NI;
+    float4 va[MAXU], vb[MAXU];
+    // issue every load of stage s for this warp (memory-level parallelism)
+    auto load_stage = [&](int s, float4 (&v)[MAXU]) {
       const long long p0 = p_begin + (long long)s * KC;
-      float4 v[MAXU];
-      int ucount = 0;
-      // issue all loads of this warp's units first (memory-level parallelism)
 #pragma unroll
       for (int t = 0; t < MAXU; ++t) {
         const int u = cw + t * NCW;
         v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (u < nunits) {
-          const int rg = u < 8 * cols16 ? 0 : (u < 16 * cols16 ? 1 : 2);
+        if (u < nunits && s < nst) {
+          const int rg = u < 8 * cols16 ? 0 : 1;
           const int uu = u - rg * 8 * cols16;
           const int g = uu / cols16, c = uu % cols16;
           const int r = g * 8 + (lane >> 2);
@@ -195,17 +210,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               v[t].w = px + 3 < p_end ? src[3] : 0.f;
             }
           }
-          ucount = t + 1;
         }
       }
+    };
+    // quantise the registers of stage s into its smem slot
+    auto store_stage = [&](int s, const float4 (&v)[MAXU]) {
+      const int is = s % NI;
       tc::mbar_wait_cluster(&bar_empty[is], (uint32_t)(((s / NI) & 1) ^ 1));
       unsigned char* st0 = smem + is * stage_bytes;
       unsigned char* st1 = st0 + slice_bytes;
 #pragma unroll
       for (int t = 0; t < MAXU; ++t) {
-        if (t >= ucount) break;
         const int u = cw + t * NCW;
-        const int rg = u < 8 * cols16 ? 0 : (u < 16 * cols16 ? 1 : 2);
+        if (u >= nunits) break;
+        const int rg = u < 8 * cols16 ? 0 : 1;
         const int uu = u - rg * 8 * cols16;
         const int g = uu / cols16, c = uu % cols16;
         const int r = g * 8 + (lane >> 2);
@@ -224,13 +242,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           w1 |= (uint32_t)(l & 0xFF) << (8 * j);
         }
         // canonical K-major layout: core matrix (8 rows x 16 B) per (row group, 16-px column)
-        const int off = region_base(rg) + c * (region_rows(rg, nb) * 16) + g * 128 + (lane >> 2) * 16 + (lane & 3) * 4;
+        const int off = region_base(rg) + c * (64 * 16) + g * 128 + (lane >> 2) * 16 + (lane & 3) * 4;
         *reinterpret_cast<uint32_t*>(st0 + off) = w0;
         *reinterpret_cast<uint32_t*>(st1 + off) = w1;
       }
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_cluster(&bar_full[is], 0);
+    };
+    load_stage(0, va);
+    for (int s = 0; s < nst; s += 2) {
+      load_stage(s + 1, vb);          // next stage's loads fly while this one converts
+      store_stage(s, va);
+      if (s + 1 >= nst) break;
+      load_stage(s + 2, va);
+      store_stage(s + 1, vb);
     }
     if (bad) atomicOr(P.nonfinite, 1);
 
@@ -357,7 +383,7 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bi
   P.n = n;
   P.B = B;
   P.nb = B > 128 ? ((B - 128 + 31) / 32) * 32 : 0;
-  P.rows_tot = B > 128 ? 128 + P.nb / 2 : 64;
+  P.rows_tot = B > 128 ? 128 : 64;
   long long per = (n + npairs - 1) / npairs;
   per = (per + KC - 1) / KC * KC;
   P.per_pair = per;
