@@ -135,7 +135,7 @@ def stage_bytes(cfg, levels, rank, comps, chunks):
         "gram": 4 * n * b,
         "project": chunks * 4 * n * b + 4 * n * comps,
         "dwt": comps * dwt_img,
-        "sure": comps * 8 * nc,                     # read + in-place write of N_c coefficients
+        "sure": comps * 4 * nc,                     # one read of N_c coefficients (soft threshold is applied by the IDWT)
         "idwt": rank * dwt_img,
         "recon": 4 * n * rank + 4 * n * b,
     }
@@ -282,7 +282,7 @@ def main():
     hbm, _, src = peaks()
     rank_k = info["rank"]
     chunks = info["chunks_run"]
-    comps = min(cfg.bands, chunks * 16) if chunks > 1 else min(16, cfg.bands)
+    comps = info["comps"]   # candidate components actually projected / transformed
     sb = stage_bytes(cfg, info["levels"], rank_k, comps, chunks)
     per = {}
     for name, (tms, nl) in stages.items():
@@ -328,7 +328,7 @@ def main():
                    "bands": cfg.bands, "seeds": f"rank r uses seed r (0..{world - 1})",
                    "l2": (f"inputs larger than L2 (cube {cube_h.nbytes / 1e6:.0f} MB > 126 MB L2); no flush"
                           if cube_h.nbytes > 126e6 else "cube fits in L2: steps run back to back (L2-warm)"),
-                   "rank": rank_k, "levels": info["levels"], "chunks": chunks},
+                   "rank": rank_k, "levels": info["levels"], "chunks": chunks, "components": comps},
         "roofline": roof,
         "stages": per,
         "e2e": {"value": world * cfg.voxels / e2e_s, "unit": UNIT,

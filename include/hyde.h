@@ -87,7 +87,8 @@ typedef struct {
   int chunks_run;       /* projection chunks processed                       */
   int nonfinite_input;  /* 1 if a NaN/Inf was seen in the cube (A1)          */
   int n_coeffs;         /* N_c: coefficients per eigen-image                  */
-  int reserved[3];
+  int comps;            /* candidate components projected / transformed       */
+  int reserved[2];
 } hyde_hyres_info;
 
 void hyde_hyres_params_default(hyde_hyres_params* p);

@@ -31,11 +31,13 @@ class Params(ctypes.Structure):
 
 class Info(ctypes.Structure):
     _fields_ = [("rank", c_int), ("levels", c_int), ("chunks_run", c_int),
-                ("nonfinite_input", c_int), ("n_coeffs", c_int), ("reserved", c_int * 3)]
+                ("nonfinite_input", c_int), ("n_coeffs", c_int), ("comps", c_int),
+                ("reserved", c_int * 2)]
 
     def as_dict(self):
         return {"rank": self.rank, "levels": self.levels, "chunks_run": self.chunks_run,
-                "nonfinite_input": self.nonfinite_input, "n_coeffs": self.n_coeffs}
+                "nonfinite_input": self.nonfinite_input, "n_coeffs": self.n_coeffs,
+                "comps": self.comps}
 
 
 _P = c_void_p  # device or host pointer

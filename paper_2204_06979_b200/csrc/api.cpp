@@ -420,7 +420,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     sg.end();
   }
   int rank = 0, chunks = 0;
-  int k0 = 0;
+  int k0 = 0, comps = 0;
   for (int c = 0;; ++c) {
     const int cl = chunk_len(c);
     const int cnt = (B - k0) < cl ? (B - k0) : cl;
@@ -457,6 +457,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     }
     CK(cudaStreamSynchronize(st));
     ++chunks;
+    comps += cnt;
     const RankState r = *h->rs_host;
     if (r.nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
     if (r.sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
@@ -484,6 +485,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     info->chunks_run = chunks;
     info->nonfinite_input = 0;
     info->n_coeffs = (int)L.plan.n_coeffs;
+    info->comps = comps;
   }
   return HYDE_OK;
 }
