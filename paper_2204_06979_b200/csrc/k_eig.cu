@@ -42,6 +42,8 @@
 // sweep is both more work and a longer dependency chain than Householder.
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace {
@@ -436,20 +438,26 @@ struct K2Smem {
 // kk used): H = I - beta v v^T with H x = alpha e_1 on rows kk+1.. (LAPACK
 // dlarfg convention, unnormalised v with v_{kk+1} = x_{kk+1} - alpha).
 // Every warp computes it redundantly and keeps a copy of v in S.vw[w];
-// thread 0 records d_kk, e_kk.
-template <int RS>
+// thread 0 records d_kk, e_kk.  TM = kk >> 5 (compile time): column slots
+// below TM hold only rows <= kk; entries j >= B of col are zero.
+template <int TM, int RS>
 __device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, int B, int lane, int w,
                                                const int (&rowi)[RS], double (&vreg)[CS], double (&vrow)[RS],
                                                double& beta, K2Smem& S) {
+  constexpr int T1 = TM + 1 < CS ? TM + 1 : CS - 1;
   double* cw = S.cw[w];
   double* vw = S.vw[w];
-#pragma unroll
-  for (int t = 0; t < CS; ++t) cw[lane + 32 * t] = col[t];
+  cw[lane + 32 * TM] = col[TM];
+  cw[lane + 32 * T1] = col[T1];
   double part = 0.0;
 #pragma unroll
-  for (int t = 0; t < CS; ++t) {
-    const int j = lane + 32 * t;
-    if (j > kk + 1 && j < B) part = fma(col[t], col[t], part);
+  for (int t = TM; t < CS; ++t) {
+    if (t <= TM + 1) {
+      const int j = lane + 32 * t;
+      if (j > kk + 1) part = fma(col[t], col[t], part);
+    } else {
+      part = fma(col[t], col[t], part);
+    }
   }
   const double tail = warp_sum(part);
   __syncwarp();
@@ -465,13 +473,24 @@ __device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, 
   }
 #pragma unroll
   for (int t = 0; t < CS; ++t) {
-    const int j = lane + 32 * t;
-    vreg[t] = beta == 0.0 ? 0.0 : (j > kk + 1 && j < B) ? col[t] : (j == kk + 1 ? v0 : 0.0);
-    vw[j] = vreg[t];
+    if (t < TM) {
+      vreg[t] = 0.0;
+    } else if (t <= TM + 1) {
+      const int j = lane + 32 * t;
+      vreg[t] = (j > kk + 1) ? col[t] : (j == kk + 1 ? v0 : 0.0);
+    } else {
+      vreg[t] = col[t];
+    }
   }
+  if (beta == 0.0) {
+#pragma unroll
+    for (int t = 0; t < CS; ++t) vreg[t] = 0.0;
+  }
+#pragma unroll
+  for (int t = TM; t < CS; ++t) vw[lane + 32 * t] = vreg[t];
   __syncwarp();
 #pragma unroll
-  for (int s = 0; s < RS; ++s) vrow[s] = vw[rowi[s]];
+  for (int s = 0; s < RS; ++s) vrow[s] = rowi[s] > kk ? vw[rowi[s]] : 0.0;
   if (threadIdx.x == 0) {
     S.d[kk] = dkk;
     S.e[kk] = alpha;
@@ -680,7 +699,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
       col[t] = j < B ? G[(size_t)j * B] / (S.sig[j] * S.sig[0]) * invn : 0.0;
       rrep[t] = j < B ? G[(size_t)j * B + 1] / (S.sig[j] * S.sig[1]) * invn : 0.0;
     }
-    form_reflector<RS>(col, 0, B, lane, w, rowi, vreg, vrow, beta, S);
+    form_reflector<0, RS>(col, 0, B, lane, w, rowi, vreg, vrow, beta, S);
   }
   // lanes [0,16) carry p rows, lanes [16,32) carry Q v rows / column k+2 entries
   const int sp = (lane & 15) / LPR;
@@ -692,30 +711,34 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
     if (B - 3 >= 1) mbar_expect(saddr(&S.mbar[1]), xbytes);
   }
   tc = clock64();
-  for (int k = 0; k <= B - 3; ++k) {
+  // One column of the reduction.  TM = (k+1) >> 5 is a compile-time constant
+  // for each segment of k: column slots below TM are already reduced and are
+  // skipped statically (no predication or selects).
+  auto step = [&](auto TMc, int k) {
+    constexpr int TM = decltype(TMc)::value;
+    constexpr int T1 = TM + 1 < CS ? TM + 1 : CS - 1;
     const int par = k & 1;
-    const int tmin = (k + 1) >> 5;   // first column slot holding any j > k
     // (a) p = beta A v on the live rows and Q v on all rows, one fused reduction
     double x2[2 * RS];
 #pragma unroll
     for (int s = 0; s < RS; ++s) {
       double pa = 0.0, pq = 0.0;
 #pragma unroll
-      for (int t = 0; t < CS; ++t)
-        if (t >= tmin) {
-          pa = fma(a[s][t], vreg[t], pa);
-          pq = fma(q[s][t], vreg[t], pq);
-        }
+      for (int t = TM; t < CS; ++t) {
+        pa = fma(a[s][t], vreg[t], pa);
+        pq = fma(q[s][t], vreg[t], pq);
+      }
       x2[s] = (rowi[s] > k) ? pa : 0.0;
       x2[RS + s] = pq;
     }
     const double red = reduceT<2 * RS>(x2, lane);
     double xv = 0.0;
     {
-      const int t2 = (k + 2) >> 5, l2 = (k + 2) & 31;
+      const bool lo = ((k + 2) >> 5) == TM;
+      const int l2 = (k + 2) & 31;
 #pragma unroll
       for (int s = 0; s < RS; ++s) {
-        const double tmp = __shfl_sync(FULL, sel(a[s], t2), l2);
+        const double tmp = __shfl_sync(FULL, lo ? a[s][TM] : a[s][T1], l2);
         if (s == sp) xv = tmp;
       }
     }
@@ -734,8 +757,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
       for (int s = 0; s < RS; ++s) {
         const double qv = beta * __shfl_sync(FULL, red, 16 + LPR * s);
 #pragma unroll
-        for (int t = 0; t < CS; ++t)
-          if (t >= tmin) q[s][t] = fma(-qv, vreg[t], q[s][t]);
+        for (int t = TM; t < CS; ++t) q[s][t] = fma(-qv, vreg[t], q[s][t]);
       }
     }
     ACC(11);
@@ -750,12 +772,16 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
       double pv = 0.0;
 #pragma unroll
       for (int t = 0; t < CS; ++t) {
-        wreg[t] = lane + 32 * t < B ? pb[lane + 32 * t] : 0.0;
-        pv = fma(wreg[t], vreg[t], pv);
+        if (t < TM) {
+          wreg[t] = 0.0;
+        } else {
+          wreg[t] = lane + 32 * t < B ? pb[lane + 32 * t] : 0.0;
+          pv = fma(wreg[t], vreg[t], pv);
+        }
       }
       Kc = 0.5 * beta * warp_sum(pv);
 #pragma unroll
-      for (int t = 0; t < CS; ++t) wreg[t] = fma(-Kc, vreg[t], wreg[t]);
+      for (int t = TM; t < CS; ++t) wreg[t] = fma(-Kc, vreg[t], wreg[t]);
 #pragma unroll
       for (int s = 0; s < RS; ++s) wrow[s] = rowi[s] < B ? fma(-Kc, vrow[s], pb[rowi[s]]) : 0.0;
     }
@@ -763,8 +789,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
     for (int s = 0; s < RS; ++s)
       if (rowi[s] > k) {
 #pragma unroll
-        for (int t = 0; t < CS; ++t)
-          if (t >= tmin) a[s][t] = fma(-wrow[s], vreg[t], fma(-vrow[s], wreg[t], a[s][t]));
+        for (int t = TM; t < CS; ++t) a[s][t] = fma(-wrow[s], vreg[t], fma(-vrow[s], wreg[t], a[s][t]));
       }
     // replica of column k+1 (-> through update k) and the arrived column k+2 (-> through update k)
     const double* vw = S.vw[w];
@@ -772,18 +797,31 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
     const double w1 = fma(-Kc, v1, pb[k + 1]), w2 = fma(-Kc, v2, pb[k + 2]);
     double xn[CS];
 #pragma unroll
-    for (int t = 0; t < CS; ++t) {
+    for (int t = TM; t < CS; ++t) {
       const int j = lane + 32 * t;
       rrep[t] = fma(-wreg[t], v1, fma(-vreg[t], w1, rrep[t]));
       xn[t] = j < B ? fma(-wreg[t], v2, fma(-vreg[t], w2, S.xbuf[par][j])) : 0.0;
     }
     ACC(13);
     // (c) reflector k+1
-    form_reflector<RS>(rrep, k + 1, B, lane, w, rowi, vreg, vrow, beta, S);
+    form_reflector<TM, RS>(rrep, k + 1, B, lane, w, rowi, vreg, vrow, beta, S);
 #pragma unroll
-    for (int t = 0; t < CS; ++t) rrep[t] = xn[t];
+    for (int t = TM; t < CS; ++t) rrep[t] = xn[t];
     ACC(14);
-  }
+  };
+  int k = 0;
+  auto segment = [&](auto TMc) {
+    constexpr int TM = decltype(TMc)::value;
+    for (; k <= B - 3 && ((k + 1) >> 5) == TM; ++k) step(TMc, k);
+  };
+  segment(std::integral_constant<int, 0>{});
+  segment(std::integral_constant<int, 1>{});
+  segment(std::integral_constant<int, 2>{});
+  segment(std::integral_constant<int, 3>{});
+  segment(std::integral_constant<int, 4>{});
+  segment(std::integral_constant<int, 5>{});
+  segment(std::integral_constant<int, 6>{});
+  segment(std::integral_constant<int, 7>{});
   // rrep = column B-1 after the last update: d_{B-1}
   {
     const double dl = __shfl_sync(FULL, sel(rrep, (B - 1) >> 5), (B - 1) & 31);
