@@ -25,7 +25,7 @@
 //           the next reflector without a second exchange.  Q = H_0 H_1 ... is
 //           accumulated in registers while the barrier is in flight; rows and
 //           column slots that are already reduced are skipped.
-//  phase 3  eigenpair k on CTA k % CL: 128-section bisection on the Sturm
+//  phase 3  eigenpair k on CTA k % CL: 256-section bisection on the Sturm
 //           count of T, inverse iteration, z all-gathered, Gram-Schmidt inside
 //           numerically coincident eigenvalue groups, V = Q Z on the row
 //           owners, sign fix (largest-|.| entry positive, lowest index on ties:
@@ -55,7 +55,6 @@ constexpr int CS = 8;      // column slots per lane: 32 * CS = 256 columns
 constexpr int BM = 256;    // max bands
 constexpr int NB = 8;      // sweep block (pivots per cluster exchange)
 constexpr int KM = HYDE_MAX_CHUNK;
-constexpr int BT = 128;    // bisection threads (points per round)
 constexpr int CLMAX = 16;
 
 // clock64() stamps (diagnostics, hyde_debug_eig_clocks; CTA 0 of the cluster):
@@ -81,9 +80,7 @@ __device__ __forceinline__ void stamp(int i) {
     for (int i_ = 5; i_ < 20; ++i_) g_eig_clk[i_] = clk_acc[i_];
 #else
 #define CLK_DECL
-#define ACC(i) \
-  do {         \
-  } while (0)
+#define ACC(i) asm volatile("" ::: "memory")   /* keeps the segment order of the profiled build */
 #define CLK_FLUSH
 #endif
 
@@ -195,36 +192,37 @@ __device__ __forceinline__ double reduceT(const double (&x)[N], int lane) {
 }
 
 // ------------------------------------------------------------ tridiagonal eigen helpers
-// Sign changes of the Sturm sequence p_0 = 1, p_i = det(T_i - x I) =
-// (d_i - x) p_{i-1} - e2_{i-1} p_{i-2} (= eigenvalues of T below x).
-// Division-free (one dependent FMA per step), power-of-two rescaling every 4
-// steps, exact zeros take the sign opposite to their predecessor (LAPACK's
-// -pivmin convention for q_i = p_i / p_{i-1}).
-__device__ __forceinline__ int sturm1(const double* d, const double* e2, int n, double x) {
+// Number of eigenvalues of T below x by the sign changes of the Sturm
+// sequence p_0 = 1, p_i = det(T_i - x I) = (d_i - x) p_{i-1} - e2_{i-1} p_{i-2},
+// one dependent FMA per step.  T is pre-scaled by a power of two to ||T|| <= 1
+// (d, e2, x all scaled: |p_i| grows by at most 3x per step, so a power-of-two
+// rescale every 8 steps keeps it in range) and e2 is floored at 1e-60 (a
+// 1e-30 relative perturbation of e).  With every e2 > 0 an exact zero p_i is
+// followed by p_{i+1} = -e2 p_{i-1}, of the sign opposite to p_{i-1}, so the
+// zero contributes exactly one sign change whichever sign its bit pattern
+// carries -- LAPACK's -pivmin convention without a select on the chain.
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x) {
   double a = 1.0, b = d[0] - x;
-  if (b == 0.0) b = -1e-300;
-  int cnt = b < 0.0;
+  int cnt = (int)((unsigned)__double2hiint(b) >> 31);
   int i = 1;
-  for (; i + 3 < n; i += 4) {
-    double dv[4], ev[4];
+  for (; i + 7 < n; i += 8) {
+    double dv[8], ev[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { dv[u] = d[i + u] - x; ev[u] = e2[i + u - 1]; }
+    for (int u = 0; u < 8; ++u) { dv[u] = d[i + u] - x; ev[u] = e2[i + u - 1]; }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double t = fma(dv[u], b, -ev[u] * a);
-      t = (t == 0.0) ? -1e-300 * b : t;    // zero: sign opposite to its predecessor
+    for (int u = 0; u < 8; ++u) {
+      const double t = fma(dv[u], b, -ev[u] * a);
       cnt += (int)((unsigned)(__double2hiint(t) ^ __double2hiint(b)) >> 31);
       a = b;
       b = t;
     }
     const double m = fmax(fabs(a), fabs(b));
-    const double sc = m > 0x1p+300 ? 0x1p-300 : (m < 0x1p-300 ? 0x1p+300 : 1.0);
+    const double sc = m > 0x1p+500 ? 0x1p-500 : (m < 0x1p-500 ? 0x1p+500 : 1.0);
     a *= sc;
     b *= sc;
   }
   for (; i < n; ++i) {
-    double t = fma(d[i] - x, b, -e2[i - 1] * a);
-    t = (t == 0.0) ? -1e-300 * b : t;
+    const double t = fma(d[i] - x, b, -e2[i - 1] * a);
     cnt += (int)((unsigned)(__double2hiint(t) ^ __double2hiint(b)) >> 31);
     a = b;
     b = t;
@@ -232,22 +230,19 @@ __device__ __forceinline__ int sturm1(const double* d, const double* e2, int n, 
   return cnt;
 }
 
-// Eigenvalue with ascending index `asc` of T by BT-section (BT threads count,
-// all NT threads pass the barriers and end with the same (lo, hi)).
+// Eigenvalue with ascending index `asc` of the pre-scaled T (interval [glo,
+// ghi] in scaled units) by NT-section; all threads end with the same (lo, hi).
 __device__ double bisect_one(const double* d, const double* e2, int n, double glo, double ghi, int asc, int* qsh) {
+  constexpr int NP = NT;
   const double range = fmax(ghi - glo, 1e-300);
   const double tol = 4.0 * 2.220446049250313e-16 * fmax(fabs(glo), fabs(ghi)) + 1e-300;
-  int iters = (int)ceil(log2(range / tol) / log2((double)BT + 1.0)) + 1;
+  int iters = (int)ceil(log2(range / tol) / log2((double)NP + 1.0)) + 1;
   if (iters > 64) iters = 64;
   double lo = glo, hi = ghi;
   const int t = threadIdx.x;
   for (int it = 0; it < iters; ++it) {
-    const double h = (hi - lo) / (double)(BT + 1);
-    int q = BT;
-    if (t < BT) {
-      const double x = lo + h * (double)(t + 1);
-      if (sturm1(d, e2, n, x) > asc) q = t;
-    }
+    const double h = (hi - lo) / (double)(NP + 1);
+    int q = sturm_count(d, e2, n, lo + h * (double)(t + 1)) > asc ? t : NP;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) q = min(q, __shfl_xor_sync(FULL, q, o));
     if ((t & 31) == 0) qsh[t >> 5] = q;
@@ -258,86 +253,114 @@ __device__ double bisect_one(const double* d, const double* e2, int n, double gl
     __syncthreads();
     // point p sits at lo + h (p + 1): the target lies in (x_{q-1}, x_q]
     const double nlo = qq > 0 ? lo + h * (double)qq : lo;
-    const double nhi = qq < BT ? lo + h * (double)(qq + 1) : hi;
+    const double nhi = qq < NP ? lo + h * (double)(qq + 1) : hi;
     lo = nlo;
     hi = nhi;
   }
   return 0.5 * (lo + hi);
 }
 
-// Inverse iteration for eigenvalue lam of T (one thread): partial-pivot LU of
-// T - lam I (two super-diagonals), two solves from a fixed start vector.  The
-// running values are carried in registers; shared memory only holds the
-// factors and x.
+// power-of-two scale 2^-ceil(log2 tnorm) that brings ||T|| to <= 1
+__device__ __forceinline__ double tri_scale(double tnorm) {
+  if (!(tnorm > 0.0) || !isfinite(tnorm)) return 1.0;
+  int ex;
+  frexp(tnorm, &ex);   // tnorm = f 2^ex, f in [0.5, 1)
+  return ldexp(1.0, -ex);
+}
+
+// scaled copies for the Sturm counts: ds = sc d, e2s = max(sc^2 e^2, 1e-60)
+__device__ void tri_scaled(const double* d, const double* e2, int B, double sc, double* ds, double* e2s) {
+  for (int i = threadIdx.x; i < B; i += NT) {
+    ds[i] = d[i] * sc;
+    e2s[i] = fmax(e2[i] * (sc * sc), 1e-60);
+  }
+  __syncthreads();
+}
+
+// Inverse iteration for eigenvalue lam of T, called by one full warp: lane 0
+// runs the serial partial-pivot LU of T - lam I (two super-diagonals) and the
+// two triangular solves per iteration with running values in registers and
+// select-based pivoting; the start vector and the normalisations are
+// lane-parallel.  Two iterations from a fixed pseudo-random start vector.
 __device__ void inv_iter(const double* d, const double* e, int n, double lam, double tnorm, double* x,
                          double* dd, double* u1, double* u2, double* ml, unsigned char* piv, unsigned seed) {
+  const int lane = threadIdx.x & 31;
   const double tiny = tnorm > 0.0 ? 2.220446049250313e-16 * tnorm : 1.0;
-  double a = d[0] - lam, b = (n > 1) ? e[0] : 0.0;
-  for (int i = 0; i < n - 1; ++i) {
-    const double c = e[i];
-    const double a1 = d[i + 1] - lam;
-    const double b1 = (i + 1 < n - 1) ? e[i + 1] : 0.0;
-    if (fabs(a) >= fabs(c)) {
-      if (fabs(a) < tiny) a = (a < 0 ? -tiny : tiny);
-      const double ra = rcp64(a);
-      const double m = c * ra;
-      dd[i] = ra; u1[i] = b; u2[i] = 0.0; ml[i] = m; piv[i] = 0;
-      a = fma(-m, b, a1);
-      b = b1;
-    } else {
-      const double rc = rcp64(c);
-      const double m = a * rc;
-      dd[i] = rc; u1[i] = a1; u2[i] = b1; ml[i] = m; piv[i] = 1;
-      a = fma(-m, a1, b);
-      b = -m * b1;
+  if (lane == 0) {
+    double a = d[0] - lam, b = (n > 1) ? e[0] : 0.0;
+#pragma unroll 4
+    for (int i = 0; i < n - 1; ++i) {
+      const double c = e[i];
+      const double a1 = d[i + 1] - lam;
+      const double b1 = (i + 1 < n - 1) ? e[i + 1] : 0.0;
+      const bool sw = fabs(a) < fabs(c);
+      double pv = sw ? c : a;
+      if (fabs(pv) < tiny) pv = pv < 0.0 ? -tiny : tiny;
+      // reciprocal: MUFU seed + one Newton step (~1e-13 relative; the LU only
+      // steers the inverse-iteration direction)
+      double r;
+      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(pv));
+      r = fma(r, fma(-pv, r, 1.0), r);
+      const double m = (sw ? a : c) * r;
+      dd[i] = r;
+      u1[i] = sw ? a1 : b;
+      u2[i] = sw ? b1 : 0.0;
+      ml[i] = m;
+      piv[i] = sw;
+      const double an = fma(-m, sw ? a1 : b, sw ? b : a1);
+      b = sw ? -m * b1 : b1;
+      a = an;
     }
+    if (fabs(a) < tiny) a = (a < 0 ? -tiny : tiny);
+    dd[n - 1] = rcp64(a);
   }
-  if (fabs(a) < tiny) a = (a < 0 ? -tiny : tiny);
-  dd[n - 1] = rcp64(a);
-  for (int i = 0; i < n; ++i) {
+  for (int i = lane; i < n; i += 32) {
     unsigned h = (unsigned)(i * 2654435761u) ^ (seed * 40503u + 0x9E3779B9u);
     h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
     x[i] = 0.5 + (double)(h & 0xFFFF) / 65536.0;
   }
+  __syncwarp();
   for (int it = 0; it < 2; ++it) {
-    double cur = x[0];
-    for (int i = 0; i < n - 1; ++i) {   // forward: L^-1 with the row interchanges
-      double nx = x[i + 1];
-      const double m = ml[i];
-      if (piv[i]) {
-        x[i] = nx;
-        nx = fma(-m, nx, cur);
-      } else {
-        x[i] = cur;
-        nx = fma(-m, cur, nx);
+    if (lane == 0) {
+      double cur = x[0];
+#pragma unroll 4
+      for (int i = 0; i < n - 1; ++i) {   // forward: L^-1 with the row interchanges
+        const double nx = x[i + 1];
+        const double m = ml[i];
+        const bool sw = piv[i];
+        x[i] = sw ? nx : cur;
+        cur = sw ? fma(-m, nx, cur) : fma(-m, cur, nx);
       }
-      cur = nx;
+      double c1 = cur * dd[n - 1];     // backward: U^-1, two super-diagonals
+      x[n - 1] = c1;
+      double c0 = c1;
+      if (n > 1) {
+        c0 = (x[n - 2] - u1[n - 2] * c1) * dd[n - 2];
+        x[n - 2] = c0;
+      }
+#pragma unroll 4
+      for (int i = n - 3; i >= 0; --i) {
+        const double xi = fma(-u2[i], c1, fma(-u1[i], c0, x[i])) * dd[i];
+        x[i] = xi;
+        c1 = c0;
+        c0 = xi;
+      }
     }
-    double c1 = cur * dd[n - 1];     // backward: U^-1, two super-diagonals
-    x[n - 1] = c1;
-    double mx = fabs(c1);
-    double c0 = c1;
-    if (n > 1) {
-      c0 = (x[n - 2] - u1[n - 2] * c1) * dd[n - 2];
-      x[n - 2] = c0;
-      mx = fmax(mx, fabs(c0));
-    }
-    for (int i = n - 3; i >= 0; --i) {
-      const double xi = (x[i] - u1[i] * c0 - u2[i] * c1) * dd[i];
-      x[i] = xi;
-      mx = fmax(mx, fabs(xi));
-      c1 = c0;
-      c0 = xi;
-    }
+    __syncwarp();
+    double mx = 0.0;
+    for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(x[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
     mx = 1.0 / mx;
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) {
+    double ss = 0.0;
+    for (int i = lane; i < n; i += 32) {
       const double v = x[i] * mx;
-      x[i] = v;
-      s = fma(v, v, s);
+      ss = fma(v, v, ss);
     }
-    s = 1.0 / sqrt(s);
-    for (int i = 0; i < n; ++i) x[i] *= s;
+    ss = 1.0 / sqrt(warp_sum(ss));
+    const double f = mx * ss;
+    for (int i = lane; i < n; i += 32) x[i] *= f;
+    __syncwarp();
   }
 }
 
@@ -410,6 +433,7 @@ struct K2Args {
 
 struct K2Smem {
   unsigned long long mbar[2];   // tridiagonalisation exchange, one per column parity
+  unsigned long long smb[2];    // sweep exchange, one per block parity
   double pbuf[2][BM];      // p = beta A v, all-gathered (double-buffered by column parity)
   double xbuf[2][BM];      // column k+2 entries, all-gathered one column ahead
   double colK[2][BM * NB]; // sweep: pivot-block columns of every row (double-buffered by block)
@@ -422,6 +446,7 @@ struct K2Smem {
   double vw[NW][BM];       // per-warp copy of the current reflector vector
   double cw[NW][BM];       // per-warp copy of the column being reduced
   double d[BM], e[BM], e2[BM];
+  double ds[BM], e2s[BM];  // scaled copies for the Sturm counts
   double zb[KM][BM];       // eigenvectors of T (all-gathered)
   double lamk[KM];
   double vrow[KM][32];     // V rows owned by this CTA (local row index w*RS+s)
@@ -514,8 +539,14 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
   if (tid == 0) {
     mbar_init(saddr(&S.mbar[0]), 1);
     mbar_init(saddr(&S.mbar[1]), 1);
+    mbar_init(saddr(&S.smb[0]), 1);
+    mbar_init(saddr(&S.smb[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int nblk = (A.B + NB - 1) / NB;
+    mbar_expect(saddr(&S.smb[0]), (unsigned)(A.B * min(NB, A.B) * 8));
+    if (nblk > 1) mbar_expect(saddr(&S.smb[1]), (unsigned)(A.B * min(NB, A.B - NB) * 8));
   }
+  cl_sync();   // barrier initialisation visible cluster-wide before any remote st.async
   const bool prof = (c == 0);
   if (prof) stamp(0);
   long long tc = clock64();
@@ -545,13 +576,18 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
       const int i = rowi[0] + CL * NW * sp;
       if (i < B && q < kb) {
         const unsigned la = saddr(&colK[i * NB + q]);
+        const unsigned mb = saddr(&S.smb[blk & 1]);
         const int d0 = lane / (8 * RS);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) st_cl(mapa(la, d0 + u * (CL / 8)), val);
+        for (int u = 0; u < 8; ++u) {
+          const unsigned dst = d0 + u * (CL / 8);
+          st_async(mapa(la, dst), val, mapa(mb, dst));
+        }
       }
     }
     ACC(5);
-    cl_sync();
+    mbar_wait(saddr(&S.smb[blk & 1]), (unsigned)(blk >> 1) & 1u);
+    if (tid == 0 && k0 + 2 * NB < B) mbar_expect(saddr(&S.smb[blk & 1]), (unsigned)(B * min(NB, B - k0 - 2 * NB) * 8));
     ACC(6);
     // Cholesky of the kb x kb pivot block by warp 0 (lane L holds entries
     // (L>>2, 2(L&3)) and (L>>2, 2(L&3)+1); padding = identity)
@@ -850,11 +886,13 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
 
   // ================= phase 3: eigenpairs of the first chunk =================
   const double tnorm = fmax(fabs(glo), fabs(ghi));
+  const double tsc = tri_scale(tnorm);
+  tri_scaled(S.d, S.e2, B, tsc, S.ds, S.e2s);
   for (int kd = c; kd < K; kd += CL) {
     tc = clock64();
-    const double lam = bisect_one(S.d, S.e2, B, glo, ghi, B - 1 - kd, S.qsh);
+    const double lam = bisect_one(S.ds, S.e2s, B, glo * tsc, ghi * tsc, B - 1 - kd, S.qsh) / tsc;
     ACC(16);
-    if (tid == 0) inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
+    if (w == 0) inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
     __syncthreads();
     ACC(17);
     for (int j = tid; j < B; j += NT) st_all<CL>(&S.zb[kd][j], S.y[j]);
@@ -964,6 +1002,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
 // =====================================================================
 struct MoreSmem {
   double d[BM], e[BM], e2[BM];
+  double ds[BM], e2s[BM];
   double dd[BM], u1[BM], u2[BM], ml[BM], y[BM];
   unsigned char piv[BM];
   double red[4 * NW];
@@ -979,14 +1018,16 @@ __global__ void __launch_bounds__(NT) more_pairs_kernel(const double* __restrict
   for (int i = tid; i < B; i += NT) { S.d[i] = tri[i]; S.e[i] = tri[B + i]; S.e2[i] = tri[2 * B + i]; }
   __syncthreads();
   const double glo = tri[3 * B], ghi = tri[3 * B + 1];
-  const double lam = bisect_one(S.d, S.e2, B, glo, ghi, B - 1 - kd, S.qsh);
+  const double tsc = tri_scale(fmax(fabs(glo), fabs(ghi)));
+  tri_scaled(S.d, S.e2, B, tsc, S.ds, S.e2s);
+  const double lam = bisect_one(S.ds, S.e2s, B, glo * tsc, ghi * tsc, B - 1 - kd, S.qsh) / tsc;
   if (values_only) {
     if (tid == 0) lam_out[kd] = lam;
     return;
   }
   const double tnorm = fmax(fabs(glo), fabs(ghi));
+  if (tid < 32) inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
   if (tid == 0) {
-    inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
     ws.lam_top[kd] = lam;
     if (lam_out) lam_out[kd] = lam;
   }
