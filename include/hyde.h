@@ -117,6 +117,16 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
 hyde_status hyde_hyres_host(hyde_handle h, const float* cube_host, int rows, int cols, int bands,
                             float* out_host, const hyde_hyres_params* params,
                             hyde_hyres_info* info, hyde_stream_t stream);
+/* Streaming end-to-end path for a sequence of same-shape HOST cubes:
+ * cubes_host[i] -> outs_host[i] for i < n.  The host->device copy of cube
+ * i+1 and the device->host copy of cube i-1 run on the library's own copy
+ * streams while cube i is denoised on `stream` (full-duplex PCIe / C2C), with
+ * two device-resident cube slots double-buffered.  Host buffers should be
+ * pinned for the copies to overlap; info may be NULL or hold n records.
+ * Returns after every result is in its host buffer. */
+hyde_status hyde_hyres_host_stream(hyde_handle h, const float* const* cubes_host, float* const* outs_host, int n,
+                                   int rows, int cols, int bands, const hyde_hyres_params* params,
+                                   hyde_hyres_info* info, hyde_stream_t stream);
 /* Bytes of device workspace hyde_hyres_ex / _batched will hold for this shape. */
 size_t hyde_hyres_workspace_size(int rows, int cols, int bands, int batch,
                                  const hyde_hyres_params* params);

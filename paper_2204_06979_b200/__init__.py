@@ -13,7 +13,7 @@ from typing import Dict, Optional, Tuple
 from . import _lib
 from ._lib import HydeError, Info, Params, check, lib, make_params
 
-__all__ = ["hyres", "hyres_batched", "hyres_host", "estimate_noise", "workspace_size",
+__all__ = ["hyres", "hyres_batched", "hyres_host", "hyres_host_stream", "estimate_noise", "workspace_size",
            "HydeError", "stages", "version"]
 
 _handles: Dict[int, int] = {}
@@ -114,6 +114,32 @@ def hyres_host(cube_np, out_np=None, *, device=0, taps=16, levels=0, chunk=16, r
     stream = torch.cuda.current_stream(device).cuda_stream
     check(lib().hyde_hyres_host(h, src, r, c, b, dst, ctypes.byref(p), ctypes.byref(info), stream), h)
     return (out, info.as_dict()) if return_info else out
+
+
+def hyres_host_stream(cubes, outs=None, *, device=0, taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False,
+                      return_info=False):
+    """Streaming end-to-end path over a list of HOST cubes (contiguous float32
+    CPU tensors, ideally pinned): the H2D copy of cube i+1 and the D2H copy of
+    cube i-1 overlap the denoising of cube i (include/hyde.h
+    hyde_hyres_host_stream).  Returns the list of output host tensors."""
+    torch = _torch()
+    n = len(cubes)
+    if n == 0:
+        return ([], []) if return_info else []
+    if outs is None:
+        outs = [torch.empty_like(c) for c in cubes]
+    for c in list(cubes) + list(outs):
+        if not isinstance(c, torch.Tensor) or c.is_cuda or c.dtype != torch.float32 or not c.is_contiguous():
+            raise HydeError(2, "host cubes must be contiguous float32 CPU tensors")
+    b, r, c = cubes[0].shape
+    src = (ctypes.c_void_p * max(n, 1))(*[x.data_ptr() for x in cubes])
+    dst = (ctypes.c_void_p * max(n, 1))(*[x.data_ptr() for x in outs])
+    p = make_params(taps, levels, chunk, ridge, keep_ll)
+    infos = (Info * max(n, 1))()
+    h = handle(device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    check(lib().hyde_hyres_host_stream(h, src, dst, n, r, c, b, ctypes.byref(p), infos, stream), h)
+    return (outs, [infos[i].as_dict() for i in range(n)]) if return_info else outs
 
 
 def estimate_noise(cube, *, return_gram=False, return_residual=False):

@@ -53,6 +53,8 @@ _SIGS = {
     "hyde_hyres": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, c_void_p]),
     "hyde_hyres_ex": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_hyres_host": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
+    "hyde_hyres_host_stream": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p), c_int, c_int, c_int, c_int,
+                                       POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_hyres_workspace_size": (c_size_t, [c_int, c_int, c_int, c_int, POINTER(Params)]),
     "hyde_hyres_batched": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_sync_status": (c_int, [c_void_p, c_void_p]),

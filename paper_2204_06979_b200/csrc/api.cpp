@@ -95,6 +95,11 @@ struct hyde_ctx {
   float* dev_in = nullptr;
   float* dev_out = nullptr;
   size_t dev_io_cap = 0;
+  // streaming host path: two cube slots (in, out) and its copy streams / events
+  float* pipe_buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t pipe_cap = 0;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
   // stage profiling
   int prof = 0;
@@ -332,6 +337,15 @@ hyde_status hyde_destroy(hyde_handle h) {
     if (h->ebuf) cudaFree(h->ebuf);
     if (h->dev_in) cudaFree(h->dev_in);
     if (h->dev_out) cudaFree(h->dev_out);
+    for (auto b : h->pipe_buf)
+      if (b) cudaFree(b);
+    if (h->s_in) cudaStreamDestroy(h->s_in);
+    if (h->s_out) cudaStreamDestroy(h->s_out);
+    for (int i = 0; i < 2; ++i) {
+      if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
+      if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
+      if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
+    }
     if (h->rs_host) cudaFreeHost(h->rs_host);
     for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
@@ -560,6 +574,71 @@ hyde_status hyde_hyres_host(hyde_handle h, const float* cube_host, int rows, int
   s = hyde_hyres_ex(h, h->dev_in, rows, cols, bands, h->dev_out, params, info, stream);
   if (s != HYDE_OK) return s;
   CK(cudaMemcpyAsync(out_host, h->dev_out, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_hyres_host_stream(hyde_handle h, const float* const* cubes_host, float* const* outs_host, int n,
+                                   int rows, int cols, int bands, const hyde_hyres_params* params,
+                                   hyde_hyres_info* info, hyde_stream_t stream) {
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  if (n < 0 || (n > 0 && (!cubes_host || !outs_host))) return fail(h, HYDE_EPARAM, "bad stream arguments");
+  for (int i = 0; i < n; ++i)
+    if (!cubes_host[i] || !outs_host[i]) return fail(h, HYDE_EPARAM, "NULL host buffer");
+  if (n == 0) return HYDE_OK;
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
+  if (!h->s_in) {
+    CK(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming));
+    }
+  }
+  if (bytes > h->pipe_cap) {
+    CK(cudaDeviceSynchronize());
+    for (auto& b : h->pipe_buf) {
+      if (b) CK(cudaFree(b));
+      b = nullptr;
+    }
+    h->pipe_cap = 0;
+    for (auto& b : h->pipe_buf) CK(cudaMalloc((void**)&b, bytes));
+    h->pipe_cap = bytes;
+  }
+  // slot j: input pipe_buf[j], output pipe_buf[2 + j].  Order per cube i (slot j = i & 1):
+  //   s_in : wait ev_done[j] (cube i-2 consumed slot j's input) -> H2D -> ev_in[j]
+  //   st   : wait ev_in[j], wait ev_out[j] (cube i-2's result copied out) -> hyres -> ev_done[j]
+  //   s_out: wait ev_done[j] -> D2H -> ev_out[j]
+  auto h2d = [&](int i) -> hyde_status {
+    const int j = i & 1;
+    if (i >= 2) CK(cudaStreamWaitEvent(h->s_in, h->ev_done[j], 0));
+    CK(cudaMemcpyAsync(h->pipe_buf[j], cubes_host[i], bytes, cudaMemcpyHostToDevice, h->s_in));
+    CK(cudaEventRecord(h->ev_in[j], h->s_in));
+    return HYDE_OK;
+  };
+  s = h2d(0);
+  if (s != HYDE_OK) return s;
+  for (int i = 0; i < n; ++i) {
+    const int j = i & 1;
+    if (i + 1 < n) {
+      s = h2d(i + 1);   // next cube's copy overlaps this cube's compute
+      if (s != HYDE_OK) return s;
+    }
+    CK(cudaStreamWaitEvent(st, h->ev_in[j], 0));
+    if (i >= 2) CK(cudaStreamWaitEvent(st, h->ev_out[j], 0));
+    s = hyde_hyres_ex(h, h->pipe_buf[j], rows, cols, bands, h->pipe_buf[2 + j], params, info ? info + i : nullptr,
+                      stream);
+    if (s != HYDE_OK) return s;
+    CK(cudaEventRecord(h->ev_done[j], st));
+    CK(cudaStreamWaitEvent(h->s_out, h->ev_done[j], 0));
+    CK(cudaMemcpyAsync(outs_host[i], h->pipe_buf[2 + j], bytes, cudaMemcpyDeviceToHost, h->s_out));
+    CK(cudaEventRecord(h->ev_out[j], h->s_out));
+  }
+  CK(cudaStreamSynchronize(h->s_out));
   CK(cudaStreamSynchronize(st));
   return HYDE_OK;
 }

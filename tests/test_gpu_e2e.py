@@ -74,6 +74,20 @@ def test_host_api_equals_device_api(hy):
     assert np.array_equal(d, h2.numpy())
 
 
+def test_host_stream_equals_device_api(hy):
+    """Streaming host path (overlapped H2D / compute / D2H, two device slots):
+    every output equals the device-API result of its own cube, including when
+    consecutive cubes differ and n exceeds the two slots."""
+    cubes = [synth.make_cube("tiny", seed).noisy for seed in range(5)]
+    ref = [hy.hyres(dev(c)).cpu().numpy() for c in cubes]
+    pins = [torch.from_numpy(c).pin_memory() for c in cubes]
+    outs, infos = hy.hyres_host_stream(pins, return_info=True)
+    for r, o, info in zip(ref, outs, infos):
+        assert np.array_equal(r, o.numpy())
+        assert info["rank"] >= 1
+    assert hy.hyres_host_stream([]) == []
+
+
 def test_deterministic_and_in_place(hy):
     s = synth.make_cube("tiny", 0)
     a = hy.hyres(dev(s.noisy))
