@@ -18,11 +18,17 @@
 
 namespace {
 
-constexpr int FR = 16;   // forward: subband rows per tile
+constexpr int FR = 32;   // forward: subband rows per tile
 constexpr int FC = 32;   // forward: subband cols per tile
+constexpr int FJ = 8;    // forward row pass: outputs per thread (register window 2FJ+T-2)
+constexpr int FI = 4;    // forward column pass: output rows per thread
 constexpr int IR = 32;   // inverse: output rows per tile
 constexpr int IC = 64;   // inverse: output cols per tile
 
+// Forward level.  Each thread of the row pass slides a register window of
+// 2 FJ + T - 2 inputs along one staged row and produces FJ (lo, hi) pairs; each
+// thread of the column pass does the same down one column for FI output rows
+// of all four subbands -- ~1 shared-memory load per 8 FMAs instead of 1:1.
 template <int T>
 __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ in, long long in_stride,
                                                       int h_in, int w_in, float* __restrict__ ll,
@@ -30,6 +36,8 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
                                                       long long sub_stride, FilterBank fb) {
   constexpr int NR = 2 * FR + T - 2;
   constexpr int NC = 2 * FC + T - 2;
+  constexpr int WR = 2 * FJ + T - 2;   // row-pass window
+  constexpr int WC = 2 * FI + T - 2;   // column-pass window
   __shared__ float xin[NR][NC + 1];
   __shared__ float lo[NR][FC + 1];
   __shared__ float hi[NR][FC + 1];
@@ -38,25 +46,31 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
   const int i0 = blockIdx.y * FR, j0 = blockIdx.x * FC;
   const float* x = in + (long long)blockIdx.z * in_stride;
   for (int idx = threadIdx.x; idx < NR * NC; idx += 256) {
-    int r = idx / NC, c = idx % NC;
-    int gr = (2 * i0 + r) % H;
-    int gc = (2 * j0 + c) % Wd;
-    gr = min(gr, h_in - 1);
+    const int r = idx / NC, c = idx - r * NC;
+    int gr = 2 * i0 + r, gc = 2 * j0 + c;
+    gr = gr >= H ? gr - H * (gr / H) : gr;
+    gc = gc >= Wd ? gc - Wd * (gc / Wd) : gc;
+    gr = min(gr, h_in - 1);   // odd extent: the padding row/column duplicates the last one
     gc = min(gc, w_in - 1);
     xin[r][c] = x[(long long)gr * w_in + gc];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < NR * FC; idx += 256) {
-    int r = idx / FC, j = idx % FC;
-    float a = 0.f, d = 0.f;
+  for (int it = threadIdx.x; it < NR * (FC / FJ); it += 256) {
+    const int r = it / (FC / FJ), q = it - r * (FC / FJ);
+    float v[WR];
 #pragma unroll
-    for (int m = 0; m < T; ++m) {
-      float v = xin[r][2 * j + m];
-      a = fmaf(fb.h[m], v, a);
-      d = fmaf(fb.g[m], v, d);
+    for (int t = 0; t < WR; ++t) v[t] = xin[r][2 * FJ * q + t];
+#pragma unroll
+    for (int jj = 0; jj < FJ; ++jj) {
+      float a = 0.f, d = 0.f;
+#pragma unroll
+      for (int m = 0; m < T; ++m) {
+        a = fmaf(fb.h[m], v[2 * jj + m], a);
+        d = fmaf(fb.g[m], v[2 * jj + m], d);
+      }
+      lo[r][FJ * q + jj] = a;
+      hi[r][FJ * q + jj] = d;
     }
-    lo[r][j] = a;
-    hi[r][j] = d;
   }
   __syncthreads();
   const long long nsb = (long long)hs * ws;
@@ -64,24 +78,34 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
   float* hl = lh + nsb;
   float* hh = hl + nsb;
   float* llo = ll + (long long)blockIdx.z * ll_stride;
-  for (int idx = threadIdx.x; idx < FR * FC; idx += 256) {
-    int i = idx / FC, j = idx % FC;
-    int gi = i0 + i, gj = j0 + j;
-    if (gi >= hs || gj >= ws) continue;
-    float s_ll = 0.f, s_hl = 0.f, s_lh = 0.f, s_hh = 0.f;
+  for (int it = threadIdx.x; it < FC * (FR / FI); it += 256) {
+    const int j = it % FC, p = it / FC;   // lanes run along j: coalesced stores
+    float L[WC], Hh[WC];
 #pragma unroll
-    for (int m = 0; m < T; ++m) {
-      float a = lo[2 * i + m][j], d = hi[2 * i + m][j];
-      s_ll = fmaf(fb.h[m], a, s_ll);
-      s_hl = fmaf(fb.g[m], a, s_hl);
-      s_lh = fmaf(fb.h[m], d, s_lh);
-      s_hh = fmaf(fb.g[m], d, s_hh);
+    for (int t = 0; t < WC; ++t) {
+      L[t] = lo[2 * FI * p + t][j];
+      Hh[t] = hi[2 * FI * p + t][j];
     }
-    long long o = (long long)gi * ws + gj;
-    llo[o] = s_ll;
-    lh[o] = s_lh;
-    hl[o] = s_hl;
-    hh[o] = s_hh;
+    const int gj = j0 + j;
+#pragma unroll
+    for (int ii = 0; ii < FI; ++ii) {
+      float s_ll = 0.f, s_hl = 0.f, s_lh = 0.f, s_hh = 0.f;
+#pragma unroll
+      for (int m = 0; m < T; ++m) {
+        s_ll = fmaf(fb.h[m], L[2 * ii + m], s_ll);
+        s_hl = fmaf(fb.g[m], L[2 * ii + m], s_hl);
+        s_lh = fmaf(fb.h[m], Hh[2 * ii + m], s_lh);
+        s_hh = fmaf(fb.g[m], Hh[2 * ii + m], s_hh);
+      }
+      const int gi = i0 + FI * p + ii;
+      if (gi < hs && gj < ws) {
+        const long long o = (long long)gi * ws + gj;
+        llo[o] = s_ll;
+        lh[o] = s_lh;
+        hl[o] = s_hl;
+        hh[o] = s_hh;
+      }
+    }
   }
 }
 
@@ -97,20 +121,29 @@ struct SoftSpec {
   int nsub, s_lh, s_ll;
 };
 
+constexpr int II = 4;    // inverse axis-0 pass: output rows per thread (even)
+constexpr int IJ = 8;    // inverse axis-1 pass: output cols per thread (even)
+
+// Inverse level, register-tiled like the forward: output rows r = 2u + par
+// take taps m = 2q + par, coefficient index u - q, so II consecutive rows of
+// one column read a window of II/2 + T/2 - 1 coefficients per subband.
 template <int T>
 __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ llp, long long ll_stride,
                                                       const float* __restrict__ sub, long long sub_stride,
                                                       int h_out, int w_out, float* __restrict__ out,
                                                       long long out_stride, FilterBank fb, SoftSpec sp) {
-  constexpr int CR = IR / 2 + T / 2 - 1;
-  constexpr int CC = IC / 2 + T / 2 - 1;
+  constexpr int HT = T / 2;
+  constexpr int CR = IR / 2 + HT - 1;
+  constexpr int CC = IC / 2 + HT - 1;
+  constexpr int W0 = II / 2 + HT - 1;   // axis-0 window
+  constexpr int W1 = IJ / 2 + HT - 1;   // axis-1 window
   __shared__ float t_ll[CR][CC + 1], t_hl[CR][CC + 1], t_lh[CR][CC + 1], t_hh[CR][CC + 1];
   __shared__ float lo1[IR][CC + 1], hi1[IR][CC + 1];
   const int H = h_out + (h_out & 1), Wd = w_out + (w_out & 1);
   const int hs = H >> 1, ws = Wd >> 1;
   const int r0 = blockIdx.y * IR, c0 = blockIdx.x * IC;
-  const int ilo = (r0 >> 1) - (T / 2 - 1);
-  const int jlo = (c0 >> 1) - (T / 2 - 1);
+  const int ilo = (r0 >> 1) - (HT - 1);
+  const int jlo = (c0 >> 1) - (HT - 1);
   const long long nsb = (long long)hs * ws;
   const float* a_ll = llp + (long long)blockIdx.z * ll_stride;
   const float* a_lh = sub + (long long)blockIdx.z * sub_stride;
@@ -125,54 +158,74 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
     if (sp.s_ll >= 0) th_ll = tz[sp.s_ll];
   }
   for (int idx = threadIdx.x; idx < CR * CC; idx += 256) {
-    int r = idx / CC, c = idx % CC;
-    int gi = ((ilo + r) % hs + hs) % hs;
-    int gj = ((jlo + c) % ws + ws) % ws;
-    long long o = (long long)gi * ws + gj;
+    const int r = idx / CC, c = idx - r * CC;
+    int gi = (ilo + r) % hs;
+    gi += gi < 0 ? hs : 0;
+    int gj = (jlo + c) % ws;
+    gj += gj < 0 ? ws : 0;
+    const long long o = (long long)gi * ws + gj;
     t_ll[r][c] = soft(a_ll[o], th_ll);
     t_lh[r][c] = soft(a_lh[o], th_lh);
     t_hl[r][c] = soft(a_hl[o], th_hl);
     t_hh[r][c] = soft(a_hh[o], th_hh);
   }
   __syncthreads();
-  // synthesis along axis 0: lo1 <- (LL, HL), hi1 <- (LH, HH)
-  for (int idx = threadIdx.x; idx < IR * CC; idx += 256) {
-    int rr = idx / CC, c = idx % CC;
-    int r = r0 + rr;
-    float s_lo = 0.f, s_hi = 0.f;
-    const int par = r & 1;   // taps m with m = r (mod 2) contribute
+  // synthesis along axis 0: lo1 <- (LL, HL), hi1 <- (LH, HH); II rows per thread
+  for (int it = threadIdx.x; it < CC * (IR / II); it += 256) {
+    const int c = it % CC, p = it / CC;
+    const int ub = (II / 2) * p;   // first coefficient row of the window (tile-relative, + HT - 1 offset)
+    float wl[W0], wh[W0], wlh[W0], whh[W0];
 #pragma unroll
-    for (int q = 0; q < T / 2; ++q) {
-      const int m = 2 * q + par;
-      const float hm = par ? fb.h[2 * q + 1] : fb.h[2 * q];
-      const float gm = par ? fb.g[2 * q + 1] : fb.g[2 * q];
-      const int ti = ((r - m) >> 1) - ilo;
-      s_lo = fmaf(hm, t_ll[ti][c], s_lo);
-      s_lo = fmaf(gm, t_hl[ti][c], s_lo);
-      s_hi = fmaf(hm, t_lh[ti][c], s_hi);
-      s_hi = fmaf(gm, t_hh[ti][c], s_hi);
+    for (int t = 0; t < W0; ++t) {
+      wl[t] = t_ll[ub + t][c];
+      wh[t] = t_hl[ub + t][c];
+      wlh[t] = t_lh[ub + t][c];
+      whh[t] = t_hh[ub + t][c];
     }
-    lo1[rr][c] = s_lo;
-    hi1[rr][c] = s_hi;
+#pragma unroll
+    for (int k = 0; k < II; ++k) {
+      const int par = k & 1, u = k >> 1;   // output row rr = II p + k = 2 (ub + u) + par (r0 even)
+      float s_lo = 0.f, s_hi = 0.f;
+#pragma unroll
+      for (int q = 0; q < HT; ++q) {
+        const int m = 2 * q + par;
+        const int ti = u - q + HT - 1;   // window index of coefficient row (ub + u) - q
+        s_lo = fmaf(fb.h[m], wl[ti], s_lo);
+        s_lo = fmaf(fb.g[m], wh[ti], s_lo);
+        s_hi = fmaf(fb.h[m], wlh[ti], s_hi);
+        s_hi = fmaf(fb.g[m], whh[ti], s_hi);
+      }
+      lo1[II * p + k][c] = s_lo;
+      hi1[II * p + k][c] = s_hi;
+    }
   }
   __syncthreads();
   float* o = out + (long long)blockIdx.z * out_stride;
-  for (int idx = threadIdx.x; idx < IR * IC; idx += 256) {
-    int rr = idx / IC, cc = idx % IC;
-    int r = r0 + rr, c = c0 + cc;
-    if (r >= h_out || c >= w_out) continue;
-    float s = 0.f;
-    const int par = c & 1;
+  for (int it = threadIdx.x; it < IR * (IC / IJ); it += 256) {
+    const int q8 = it % (IC / IJ), rr = it / (IC / IJ);
+    const int vb = (IJ / 2) * q8;
+    float wl[W1], wh[W1];
 #pragma unroll
-    for (int q = 0; q < T / 2; ++q) {
-      const int m = 2 * q + par;
-      const float hm = par ? fb.h[2 * q + 1] : fb.h[2 * q];
-      const float gm = par ? fb.g[2 * q + 1] : fb.g[2 * q];
-      const int tj = ((c - m) >> 1) - jlo;
-      s = fmaf(hm, lo1[rr][tj], s);
-      s = fmaf(gm, hi1[rr][tj], s);
+    for (int t = 0; t < W1; ++t) {
+      wl[t] = lo1[rr][vb + t];
+      wh[t] = hi1[rr][vb + t];
     }
-    o[(long long)r * w_out + c] = s;
+    const int r = r0 + rr;
+    if (r >= h_out) continue;
+#pragma unroll
+    for (int k = 0; k < IJ; ++k) {
+      const int par = k & 1, u = k >> 1;
+      float sacc = 0.f;
+#pragma unroll
+      for (int q = 0; q < HT; ++q) {
+        const int m = 2 * q + par;
+        const int tj = u - q + HT - 1;
+        sacc = fmaf(fb.h[m], wl[tj], sacc);
+        sacc = fmaf(fb.g[m], wh[tj], sacc);
+      }
+      const int cc = c0 + IJ * q8 + k;
+      if (cc < w_out) o[(long long)r * w_out + cc] = sacc;
+    }
   }
 }
 
