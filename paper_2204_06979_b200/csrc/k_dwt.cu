@@ -45,14 +45,33 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
   const int hs = H >> 1, ws = Wd >> 1;
   const int i0 = blockIdx.y * FR, j0 = blockIdx.x * FC;
   const float* x = in + (long long)blockIdx.z * in_stride;
-  for (int idx = threadIdx.x; idx < NR * NC; idx += 256) {
-    const int r = idx / NC, c = idx - r * NC;
-    int gr = 2 * i0 + r, gc = 2 * j0 + c;
-    gr = gr >= H ? gr - H * (gr / H) : gr;
-    gc = gc >= Wd ? gc - Wd * (gc / Wd) : gc;
-    gr = min(gr, h_in - 1);   // odd extent: the padding row/column duplicates the last one
-    gc = min(gc, w_in - 1);
-    xin[r][c] = x[(long long)gr * w_in + gc];
+  {
+    // stage the tile: every load of this thread is issued before the first
+    // shared store, so the L2/HBM round trips overlap instead of serialising
+    constexpr int NL = (NR * NC + 255) / 256;
+    float v[NL];
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int idx = threadIdx.x + 256 * u;
+      v[u] = 0.f;
+      if (idx < NR * NC) {
+        const int r = idx / NC, c = idx - r * NC;
+        int gr = 2 * i0 + r, gc = 2 * j0 + c;
+        gr = gr >= H ? gr - H * (gr / H) : gr;
+        gc = gc >= Wd ? gc - Wd * (gc / Wd) : gc;
+        gr = min(gr, h_in - 1);   // odd extent: the padding row/column duplicates the last one
+        gc = min(gc, w_in - 1);
+        v[u] = __ldg(x + (long long)gr * w_in + gc);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int idx = threadIdx.x + 256 * u;
+      if (idx < NR * NC) {
+        const int r = idx / NC, c = idx - r * NC;
+        xin[r][c] = v[u];
+      }
+    }
   }
   __syncthreads();
   for (int it = threadIdx.x; it < NR * (FC / FJ); it += 256) {
@@ -157,17 +176,38 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
     th_hh = tz[sp.s_lh + 2];
     if (sp.s_ll >= 0) th_ll = tz[sp.s_ll];
   }
-  for (int idx = threadIdx.x; idx < CR * CC; idx += 256) {
-    const int r = idx / CC, c = idx - r * CC;
-    int gi = (ilo + r) % hs;
-    gi += gi < 0 ? hs : 0;
-    int gj = (jlo + c) % ws;
-    gj += gj < 0 ? ws : 0;
-    const long long o = (long long)gi * ws + gj;
-    t_ll[r][c] = soft(a_ll[o], th_ll);
-    t_lh[r][c] = soft(a_lh[o], th_lh);
-    t_hl[r][c] = soft(a_hl[o], th_hl);
-    t_hh[r][c] = soft(a_hh[o], th_hh);
+  {
+    // stage the four coefficient tiles, all loads in flight before the stores
+    constexpr int NL = (CR * CC + 255) / 256;
+    float v0[NL], v1[NL], v2[NL], v3[NL];
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int idx = threadIdx.x + 256 * u;
+      v0[u] = v1[u] = v2[u] = v3[u] = 0.f;
+      if (idx < CR * CC) {
+        const int r = idx / CC, c = idx - r * CC;
+        int gi = (ilo + r) % hs;
+        gi += gi < 0 ? hs : 0;
+        int gj = (jlo + c) % ws;
+        gj += gj < 0 ? ws : 0;
+        const long long o = (long long)gi * ws + gj;
+        v0[u] = a_ll[o];
+        v1[u] = a_lh[o];
+        v2[u] = a_hl[o];
+        v3[u] = a_hh[o];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int idx = threadIdx.x + 256 * u;
+      if (idx < CR * CC) {
+        const int r = idx / CC, c = idx - r * CC;
+        t_ll[r][c] = soft(v0[u], th_ll);
+        t_lh[r][c] = soft(v1[u], th_lh);
+        t_hl[r][c] = soft(v2[u], th_hl);
+        t_hh[r][c] = soft(v3[u], th_hh);
+      }
+    }
   }
   __syncthreads();
   // synthesis along axis 0: lo1 <- (LL, HL), hi1 <- (LH, HH); II rows per thread

@@ -81,17 +81,40 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const float* __restri
     }
 }
 
-__global__ void gram_reduce_kernel(const double* __restrict__ partial, int nsplit, int B,
-                                   double* __restrict__ G) {
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long tot = (long long)B * B;
-  if (idx >= tot) return;
-  int i = (int)(idx / B), j = (int)(idx % B);
-  // sum in a fixed order; read the (min,max) element so G is exactly symmetric
-  long long src = (long long)min(i, j) * B + max(i, j);
+// G = sum of the per-split partial Grams.  One block = 32 consecutive
+// elements (coalesced lanes) x 8 warps; warp w sums splits k = w, w + 8, ...
+// with its loads in flight together, then the 8 warp sums are added in a
+// fixed order -- deterministic, and not one 74-deep chain of L2 round trips
+// per element.  The (min, max) element is read so G is exactly symmetric.
+__global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restrict__ partial, int nsplit, int B,
+                                                          double* __restrict__ G) {
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long tot = (long long)B * B;
+  const long long idx = blockIdx.x * 32LL + lane;
   double s = 0.0;
-  for (int k = 0; k < nsplit; ++k) s += partial[(long long)k * tot + src];
-  G[idx] = s;
+  if (idx < tot) {
+    const int i = (int)(idx / B), j = (int)(idx % B);
+    const long long src = (long long)min(i, j) * B + max(i, j);
+    double v[16];
+    for (int k0 = w; k0 < nsplit; k0 += 8 * 16) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = k0 + 8 * u;
+        v[u] = k < nsplit ? __ldcs(partial + (long long)k * tot + src) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+  }
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && idx < tot) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += part[q][lane];
+    G[idx] = t;
+  }
 }
 
 }  // namespace
@@ -120,6 +143,6 @@ cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int
 // G[i][j] = sum over slices of partial[slice][min(i,j)][max(i,j)], fixed order
 cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st) {
   long long tot = (long long)B * B;
-  gram_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, nsplit, B, G);
+  gram_reduce_kernel<<<(unsigned)((tot + 31) / 32), 256, 0, st>>>(partial, nsplit, B, G);
   return cudaGetLastError();
 }
