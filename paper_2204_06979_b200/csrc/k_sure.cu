@@ -49,6 +49,7 @@ constexpr int G = 8;              // cluster size (CTAs per big subband)
 constexpr int CAPL = NT * 32;     // keys one CTA sorts at a time (8192)
 constexpr int BIG_MIN = 32768;    // subbands at least this long use a cluster
 constexpr int MAXPASS = 12;
+constexpr int SURV_GOAL = 2048;   // prune until at most this many keys survive (or no progress)
 constexpr int PF = 16;            // loads in flight per thread in the streaming passes
 constexpr int PFC = 8;            // ... in the compaction streams (more live state per value)
 constexpr size_t SMEM_DYN = (size_t)NBIN * NT * sizeof(unsigned long long);   // == 2 x CAPL keys
@@ -538,7 +539,10 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         nlo = edge[first];
         nhi = edge[last + 1] - 1u;
         const bool progress = !(nlo == klo && nhi == khi);
-        go = (progress && msum > (unsigned)(nr * CAPL)) ? 1u : 0u;
+        // keep pruning while it makes progress and the survivors exceed a
+        // small exact-evaluation set: a streaming pass over the slice is far
+        // cheaper than sorting tens of thousands of survivors
+        go = (progress && msum > (unsigned)SURV_GOAL) ? 1u : 0u;
       }
       if (l == 0) {
         s_ub = ub;
