@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+from harness import dist as hd  # noqa: E402
 from harness import synth  # noqa: E402
 
 METRIC = "HyRes voxels/sec and ms/cube"
@@ -190,21 +191,26 @@ def run_reference(args, cfg, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def k2_flops(B):
+    """Algorithmic fp64 flops of K2: Gauss-Jordan inverse of
+    G + dI (2 B^3), Householder tridiagonalisation (4/3 B^3) and the
+    accumulation of Q (4/3 B^3); the tridiagonal eigenpairs are O(B^2)."""
+    return (2.0 + 4.0 / 3.0 + 4.0 / 3.0) * B ** 3
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="large", choices=["tiny", "small", "medium", "wide", "large"])
+    ap.add_argument("--config", default="large", choices=["tiny", "small", "medium", "wide", "large", "batched"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = synth.CONFIGS[args.config]
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = hd.env_rank()
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
@@ -216,10 +222,21 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2204_06979_b200 as hy
 
-    s = synth.make_cube(cfg, seed=rank)
-    cube_h = np.ascontiguousarray(s.noisy)
-    cube = torch.from_numpy(cube_h).cuda()
-    out = torch.empty_like(cube)
+    # Work of this rank: one cube (seed = rank; weak scaling) or, for the batched
+    # workload, its round-robin shard of the fixed batch of independent cubes
+    # (strong scaling).  No data-path collective either way.
+    batched = cfg.batch > 1
+    seeds = hd.shard(cfg.batch, rank, world) if batched else [rank]
+    cubes_h = [np.ascontiguousarray(synth.make_cube(cfg, seed=sd).noisy) for sd in seeds]
+    ncube = len(cubes_h)
+    if batched:
+        cube = torch.from_numpy(np.stack(cubes_h)).cuda()
+        out = torch.empty_like(cube)
+        run = lambda: hy.hyres_batched(cube, out, return_info=True)   # noqa: E731
+    else:
+        cube = torch.from_numpy(cubes_h[0]).cuda()
+        out = torch.empty_like(cube)
+        run = lambda: hy.hyres(cube, out, return_info=True)   # noqa: E731
     props = torch.cuda.get_device_properties(local)
     bus = None
     try:
@@ -229,9 +246,11 @@ def main():
     clk = ClockSampler(bus)
     clk.start()
 
-    _, info = hy.hyres(cube, out, return_info=True)
+    _, info = run()
+    if batched:
+        info = info[0]
     for _ in range(args.warmup - 1):
-        hy.hyres(cube, out)
+        run()
     torch.cuda.synchronize()
     hy.profile_enable(local, True)
     st = torch.cuda.current_stream()
@@ -243,7 +262,7 @@ def main():
     clk.mark()
     e0.record(st)
     for _ in range(args.steps):
-        hy.hyres(cube, out)
+        run()
     e1.record(st)
     torch.cuda.synchronize()
     clk.mark()
@@ -253,30 +272,26 @@ def main():
     stages = hy.profile_read(local)
     hy.profile_enable(local, False)
     ms = e0.elapsed_time(e1) / args.steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = world * cfg.voxels / (ms_max * 1e-3)
+    ms_max = hd.max_over_ranks(ms, device="cuda")
+    cubes_total = hd.sum_over_ranks(ncube, device="cuda")
+    value = hd.whole_job_rate(cubes_total * cfg.voxels, ms_max * 1e-3)
 
     # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside ----
-    # hyde_hyres_host_stream: every step copies its cube in and its result out;
-    # the copies of neighbouring steps overlap this step's compute (full-duplex link)
-    pin_in = torch.from_numpy(cube_h).pin_memory()
-    pin_out = torch.empty_like(pin_in).pin_memory()
-    hy.hyres_host_stream([pin_in], [pin_out], device=local)
+    # hyde_hyres_host_stream: every step copies its cubes in and its results out;
+    # the copies of neighbouring cubes overlap the current cube's compute
+    pins = [torch.from_numpy(c).pin_memory() for c in cubes_h]
+    pouts = [torch.empty_like(p).pin_memory() for p in pins]
+    hy.hyres_host_stream(pins[:1], pouts[:1], device=local)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ne = max(args.e2e_steps, 1)
+    seq_in = [pins[i % ncube] for i in range(ne * ncube)]
+    seq_out = [pouts[i % ncube] for i in range(ne * ncube)]
     t0 = time.perf_counter()
-    hy.hyres_host_stream([pin_in] * ne, [pin_out] * ne, device=local)
+    hy.hyres_host_stream(seq_in, seq_out, device=local)
     torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / ne
-    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_s = float(e2e_t.item())
+    e2e_s = hd.max_over_ranks((time.perf_counter() - t0) / ne, device="cuda")
     clk.stop()
     csum = clk.summary()
 
@@ -285,7 +300,7 @@ def main():
     rank_k = info["rank"]
     chunks = info["chunks_run"]
     comps = info["comps"]   # candidate components actually projected / transformed
-    sb = stage_bytes(cfg, info["levels"], rank_k, comps, chunks)
+    sb = {k: v * ncube for k, v in stage_bytes(cfg, info["levels"], rank_k, comps, chunks).items()}
     per = {}
     for name, (tms, nl) in stages.items():
         t = tms / args.steps
@@ -300,48 +315,52 @@ def main():
                        "GBps": round(dws / (tds * 1e-3) / 1e9, 1) if tds > 0 else None,
                        "frac_hbm": round(dws / (tds * 1e-3) / 1e9 / hbm, 4) if tds > 0 else None}
     dom = max((k for k in stages), key=lambda k: stages[k][0])
+    t = stages[dom][0] / args.steps
     if dom in sb:
-        t = stages[dom][0] / args.steps
         ach = sb[dom] / (t * 1e-3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
                 "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
                 "peak_source": src, "share_of_step": round(t / ms_max, 4)}
-    else:   # eigensolver: fp64 ALU / latency bound, one CTA
-        t = stages[dom][0] / args.steps
-        B = cfg.bands
-        flops = (B ** 3) + (4.0 / 3.0) * B ** 3     # sweep (B^3/2 FMA) + tridiagonalisation (2/3 B^3 FMA)
-        peak_sm = 64 * 2 * 1.965e9 / 1e12            # one SM: 64 fp64 FMA/clk at 1965 MHz
+    else:   # K2: one 16-CTA cluster, fp64, a B-step dependency chain
+        ncta = hy.eig_cluster_size() or 16
+        flops = ncube * k2_flops(cfg.bands)
+        peak = ncta * 64 * 2 * 1.965e9 / 1e12          # DFMA/clk/SM x 2 flops x max SM clock
         ach = flops / (t * 1e-3) / 1e12
-        roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 4), "peak": round(peak_sm, 4),
-                "unit": "TFLOP/s", "frac": round(ach / peak_sm, 4), "traffic": None,
-                "peak_source": "derived: one SM x 64 DFMA/clk x 1965 MHz (single-CTA kernel)",
+        roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4),
+                "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": None,
+                "peak_source": f"derived: {ncta} SMs (one cluster) x 64 DFMA/clk x 2 x 1965 MHz; "
+                               "latency-bound (B sequential Householder steps)",
                 "share_of_step": round(t / ms_max, 4)}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
+    nbytes = int(sum(c.nbytes for c in cubes_h))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "ms_per_cube": ms_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": ms_max, "ms_per_cube": ms_max / ncube,
+        "higher_is_better": True, "scaling": "strong" if batched else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols,
-                   "bands": cfg.bands, "seeds": f"rank r uses seed r (0..{world - 1})",
-                   "l2": (f"inputs larger than L2 (cube {cube_h.nbytes / 1e6:.0f} MB > 126 MB L2); no flush"
-                          if cube_h.nbytes > 126e6 else "cube fits in L2: steps run back to back (L2-warm)"),
+                   "bands": cfg.bands, "cubes_per_rank": ncube,
+                   "seeds": (f"batch of {cfg.batch} (seeds 0..{cfg.batch - 1}) round-robin over ranks"
+                             if batched else f"rank r uses seed r (0..{world - 1})"),
+                   "l2": (f"inputs larger than L2 ({nbytes / 1e6:.0f} MB per rank > 126 MB L2); no flush"
+                          if nbytes > 126e6 else "cube fits in L2: steps run back to back (L2-warm)"),
                    "rank": rank_k, "levels": info["levels"], "chunks": chunks, "components": comps},
         "roofline": roof,
         "stages": per,
-        "e2e": {"value": world * cfg.voxels / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": int(cube_h.nbytes), "d2h_bytes_per_step": int(cube_h.nbytes),
-                "ms_per_step": e2e_s * 1e3, "steps": max(args.e2e_steps, 1),
-                "path": "hyde_hyres_host_stream (pinned host buffers; H2D of step i+1 and D2H of step i-1 overlap step i)"},
+        "e2e": {"value": world * ncube * cfg.voxels / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "ms_per_step": e2e_s * 1e3, "steps": ne,
+                "path": "hyde_hyres_host_stream (pinned host buffers; H2D of the next cube and D2H of "
+                        "the previous one overlap the current cube)"},
         "gpu_launches": int(launches),
         "clocks": csum,
     }
     if world == 1 and not args.no_cpu_baseline:
-        t, cores, thr = cpu_baseline(cube_h, reps=2)
+        t, cores, thr = cpu_baseline(cubes_h[0], reps=2)
         line["cpu_baseline"] = {"value": cfg.voxels / t, "unit": UNIT, "cores": cores, "threads": thr,
                                 "kind": "oracle",
                                 "sample": f"2 full {cfg.name} cubes, oracle.hyres (numpy fp64), mean time"}

@@ -195,17 +195,22 @@ hyde_status hyde_profile_enable(hyde_handle h, int on);
 hyde_status hyde_profile_read(hyde_handle h, double* ms, long long* launches);
 long long hyde_launch_count(hyde_handle h);
 
-/* clock64() stamps / accumulators (SM cycles) of the last K2 kernels:
- * [0,1] Cholesky start/end, [2,3] tridiagonalisation start/end, [4..7]
- * eigenpair CTA 0 start / bisection / inverse iteration / back-transform,
- * [8..10] Cholesky panel-block / panel-rows / trailing-update totals,
- * [11..13] tridiagonalisation column / SYMV / rank-2-update totals.
- * Copies 16 values; synchronizes the device. */
-hyde_status hyde_debug_eig_clocks(long long* out16);
+/* clock64() stamps (SM cycles, CTA 0 of the K2 cluster) of the last K2
+ * launch: [0] start, [1] sweep (sigma) done, [2] tridiagonalisation done,
+ * [3] eigenpairs done, [4] vectors written.  With -DHYDE_EIG_PROF builds,
+ * [5..17] hold per-segment accumulators (sweep gather / exchange / pivot
+ * Cholesky / solves / update; column symv+send / Q update / wait / update /
+ * reflector; bisection; inverse iteration).  Copies 32 values; synchronizes. */
+hyde_status hyde_debug_eig_clocks(long long* out32);
 
-/* Copies the tridiagonal T (d[B], e[B], e^2[B], glo, ghi) and the reflector
- * buffer (B*B Householder columns, B*B eigenvectors, B betas) of the handle's
- * last hyde_k_eig call (same n_pixels and bands) into device buffers. */
+/* CTAs per K2 eigensolver cluster on the current device: 16 (non-portable
+ * cluster size) when the GPU can co-schedule it, else 8. */
+int hyde_eig_cluster_size(void);
+
+/* Copies the tridiagonal T (d[B], e[B], e^2[B], glo, ghi) and the first
+ * 2 B^2 + B doubles of the K2 workspace (Q = H_0 H_1 ... row-major, the
+ * sign-fixed eigenvectors, eigenvalues) of the handle's last hyde_k_eig call
+ * (same n_pixels and bands) into device buffers. */
 hyde_status hyde_debug_eig_state(hyde_handle h, int n_pixels, int bands, double* tri_out, double* house_out);
 
 /* Analysis low-pass filter the kernels use (host, fp64; taps values). */

@@ -188,3 +188,8 @@ def profile_read(device: int = 0):
 
 def launch_count(device: int = 0) -> int:
     return int(lib().hyde_launch_count(handle(device)))
+
+
+def eig_cluster_size() -> int:
+    """CTAs in the K2 eigensolver cluster on this device (16, or 8 when 16 cannot co-schedule)."""
+    return int(lib().hyde_eig_cluster_size())

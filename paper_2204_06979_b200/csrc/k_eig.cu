@@ -1176,6 +1176,11 @@ extern "C" hyde_status hyde_debug_eig_clocks(long long* out) {
   return cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(long long) * 32) == cudaSuccess ? HYDE_OK : HYDE_ECUDA;
 }
 
+extern "C" int hyde_eig_cluster_size(void) {
+  if (g_cluster == 0) g_cluster = cluster_fits<16>() ? 16 : 8;
+  return g_cluster;
+}
+
 size_t eig_workspace_doubles(int B) { return 4 * (size_t)B * B + (size_t)B + 8 + 64; }
 
 static cudaError_t run_k2(const K2Args& a, cudaStream_t st) {
