@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -100,6 +101,12 @@ struct hyde_ctx {
   size_t pipe_cap = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  // batched path: lanes (own workspace, stream and host thread) so that
+  // independent cubes overlap on the GPU
+  std::vector<hyde_ctx*> lanes;
+  std::vector<cudaStream_t> lane_st;
+  std::vector<cudaEvent_t> lane_ev;
+  cudaEvent_t ev_batch = nullptr;
   RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
   // stage profiling
   int prof = 0;
@@ -346,6 +353,10 @@ hyde_status hyde_destroy(hyde_handle h) {
       if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
       if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
     }
+    for (auto l : h->lanes) hyde_destroy(l);
+    for (auto st : h->lane_st) cudaStreamDestroy(st);
+    for (auto e : h->lane_ev) cudaEventDestroy(e);
+    if (h->ev_batch) cudaEventDestroy(h->ev_batch);
     if (h->rs_host) cudaFreeHost(h->rs_host);
     for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
@@ -538,16 +549,80 @@ hyde_status hyde_hyres(hyde_handle h, const float* cube, int rows, int cols, int
   return hyde_hyres_ex(h, cube, rows, cols, bands, out, nullptr, nullptr, stream);
 }
 
+constexpr int kLanes = 8;   // concurrent cubes in hyde_hyres_batched
+
 hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int rows, int cols, int bands,
                                float* outs, const hyde_hyres_params* params, hyde_hyres_info* info,
                                hyde_stream_t stream) {
   if (!h) return HYDE_EPARAM;
   if (batch < 0 || (batch > 0 && (!cubes || !outs))) return fail(h, HYDE_EPARAM, "bad batch arguments");
   const size_t per = (size_t)rows * cols * bands;
-  for (int i = 0; i < batch; ++i) {
-    hyde_status s = hyde_hyres_ex(h, cubes + per * i, rows, cols, bands, outs + per * i, params,
-                                  info ? info + i : nullptr, stream);
+  if (batch <= 1) {
+    for (int i = 0; i < batch; ++i) {
+      hyde_status s = hyde_hyres_ex(h, cubes + per * i, rows, cols, bands, outs + per * i, params,
+                                    info ? info + i : nullptr, stream);
+      if (s != HYDE_OK) return s;
+    }
+    return HYDE_OK;
+  }
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  // Independent cubes run on kLanes lanes -- each its own workspace, stream and
+  // host thread (hyres_ex synchronises its stream once per rank-loop chunk) --
+  // so that, e.g., one cube's K2 cluster (16 SMs) overlaps another cube's
+  // HBM-bound stages.  Cube i runs on lane i % kLanes; every output is the one
+  // hyde_hyres_ex gives for that cube alone.
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int L = batch < kLanes ? batch : kLanes;
+  while ((int)h->lanes.size() < L) {
+    hyde_handle l = nullptr;
+    s = hyde_create(&l, h->device);
     if (s != HYDE_OK) return s;
+    h->lanes.push_back(l);
+    cudaStream_t ls = nullptr;
+    CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
+    h->lane_st.push_back(ls);
+    cudaEvent_t le = nullptr;
+    CK(cudaEventCreateWithFlags(&le, cudaEventDisableTiming));
+    h->lane_ev.push_back(le);
+  }
+  if (!h->ev_batch) CK(cudaEventCreateWithFlags(&h->ev_batch, cudaEventDisableTiming));
+  CK(cudaEventRecord(h->ev_batch, st));   // the cubes are ready on the caller's stream
+  std::vector<hyde_status> res(L, HYDE_OK);
+  std::vector<std::thread> th;
+  for (int j = 0; j < L; ++j) {
+    hyde_ctx* lh = h->lanes[j];
+    lh->prof = h->prof;
+    th.emplace_back([&, j, lh]() {
+      cudaSetDevice(h->device);
+      cudaStream_t ls = h->lane_st[j];
+      if (cudaStreamWaitEvent(ls, h->ev_batch, 0) != cudaSuccess) {
+        res[j] = HYDE_ECUDA;
+        return;
+      }
+      for (int i = j; i < batch; i += L) {
+        const hyde_status r = hyde_hyres_ex(lh, cubes + per * i, rows, cols, bands, outs + per * i, params,
+                                            info ? info + i : nullptr, (hyde_stream_t)ls);
+        if (r != HYDE_OK) {
+          res[j] = r;
+          return;
+        }
+      }
+      if (cudaEventRecord(h->lane_ev[j], ls) != cudaSuccess) res[j] = HYDE_ECUDA;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int j = 0; j < L; ++j) {
+    hyde_ctx* lh = h->lanes[j];
+    h->launch_total += lh->launch_total;
+    for (int k = 0; k < HYDE_NSTAGES; ++k) h->launch_by_stage[k] += lh->launch_by_stage[k];
+    lh->launch_total = 0;
+    for (int k = 0; k < HYDE_NSTAGES; ++k) lh->launch_by_stage[k] = 0;
+    for (auto& r : lh->recs) h->recs.push_back(r);   // stage time summed over lanes (busy time)
+    lh->recs.clear();
+    if (res[j] != HYDE_OK) return fail(h, res[j], lh->err.empty() ? "batched lane failed" : lh->err);
+    CK(cudaStreamWaitEvent(st, h->lane_ev[j], 0));
   }
   return HYDE_OK;
 }
