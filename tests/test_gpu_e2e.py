@@ -50,6 +50,19 @@ def test_hyres_large_matches_oracle(hy):
     _compare(s, ref, out.cpu().numpy(), info)
 
 
+def test_batched_lanes_reuse_and_mixed_cubes(hy):
+    """More cubes than the batched path's 8 lanes (lanes reused, cube i on lane
+    i % 8), mixed contents: each output equals the single-cube result, bit for bit."""
+    cubes = [synth.make_cube("tiny", sd).noisy for sd in range(11)]
+    cubes[5] = synth.low_rank_cube(64, 64, 32, rank=4, seed=5).clean     # a noiseless one in the middle
+    x = dev(np.stack(cubes))
+    outs, infos = hy.hyres_batched(x, return_info=True)
+    for i in range(len(cubes)):
+        single, info = hy.hyres(x[i].contiguous(), return_info=True)
+        assert torch.equal(single, outs[i]), i
+        assert infos[i]["rank"] == info["rank"]
+
+
 def test_batched_matches_single_and_oracle(hy):
     cfg = synth.CONFIGS["batched"]
     seeds = [0, 1, 2]

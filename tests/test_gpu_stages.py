@@ -98,15 +98,17 @@ def test_noise_and_eig_match_oracle(hy, name):
     assert np.max(np.abs(V.T @ V - np.eye(k))) < 1e-8
 
 
-@pytest.mark.parametrize("b,r,c", [(3, 17, 33), (4, 20, 20), (6, 20, 20), (9, 31, 29), (33, 40, 40), (224, 40, 40)])
-def test_eigenpairs_are_eigenpairs(hy, b, r, c):
+@pytest.mark.parametrize("b,r,c,kmax", [(3, 17, 33, 16), (4, 20, 20, 16), (6, 20, 20, 16), (9, 31, 29, 16),
+                                        (33, 40, 40, 16), (224, 40, 40, 16), (129, 30, 30, 32), (256, 50, 50, 32)])
+def test_eigenpairs_are_eigenpairs(hy, b, r, c, kmax):
     """Every returned pair satisfies G_w v = lam v and V is orthonormal (small and odd band counts,
-    the tridiagonal edge cases), independent of how close the eigenvalues are."""
+    the tridiagonal edge cases, B = 256 -- every row slot of the 16-CTA cluster -- and 32
+    eigenpairs, two per CTA), independent of how close the eigenvalues are."""
     s = synth.low_rank_cube(r, c, b, rank=min(3, b - 1), seed=b, snr_db=20.0)
     n = r * c
     g = O.gram(s.noisy)
     sig_ref, _ = O.estimate_noise(s.noisy)
-    k = min(16, b)
+    k = min(kmax, b)
     sig, lam, V = hy.stages.eig(dev(g), n, k)
     sig, lam, V = sig.cpu().numpy(), lam.cpu().numpy(), V.cpu().numpy()
     assert np.max(np.abs(sig / sig_ref - 1)) < 1e-9
