@@ -345,8 +345,23 @@ __global__ void amax_kernel(const float* __restrict__ Y, long long n, unsigned* 
   bool bad = false;
   const bool vec = (n % 4 == 0) && (((uintptr_t)Y & 15) == 0);
   if (vec) {
+    // four independent 16-byte loads in flight per thread per step
     const long long n4 = n / 4;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n4; i += 4 * stride) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(row) + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        m = max(m, __float_as_uint(fabsf(v[u].x)));
+        m = max(m, __float_as_uint(fabsf(v[u].y)));
+        m = max(m, __float_as_uint(fabsf(v[u].z)));
+        m = max(m, __float_as_uint(fabsf(v[u].w)));
+      }
+    }
+    for (; i < n4; i += stride) {
       float4 v = __ldcs(reinterpret_cast<const float4*>(row) + i);
       m = max(m, __float_as_uint(fabsf(v.x)));
       m = max(m, __float_as_uint(fabsf(v.y)));

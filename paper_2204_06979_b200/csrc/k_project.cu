@@ -12,7 +12,7 @@
 
 namespace {
 
-template <int NC, int PIX, bool VEC>
+template <int NC, int PIX, bool VEC, int UB>
 __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ Y, long long n, int B,
                                                       const float* __restrict__ W, int ldw, int ncomp,
                                                       float* __restrict__ E, long long ldE) {
@@ -30,8 +30,7 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
 #pragma unroll
     for (int q = 0; q < PIX; ++q) acc[k][q] = 0.f;
   const bool full = p0 + PIX <= n;
-  // 8 bands per step: 8 independent 16-byte loads in flight per thread
-  constexpr int UB = 8;
+  // UB bands per step: UB independent 16-byte loads in flight per thread
   int b = 0;
   for (; b + UB <= B; b += UB) {
     float y[UB][PIX];
@@ -92,7 +91,7 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
   }
 }
 
-template <int NC, int PIX>
+template <int NC, int PIX, int UB = 8>
 cudaError_t launch_nc(const float* Y, long long n, int B, const float* W, int ldw, int ncomp,
                       float* E, long long ldE, cudaStream_t st) {
   const long long threads = (n + PIX - 1) / PIX;
@@ -100,11 +99,11 @@ cudaError_t launch_nc(const float* Y, long long n, int B, const float* W, int ld
   const size_t smem = (size_t)B * NC * sizeof(float);
   const bool vec = (n % 4 == 0) && (ldE % 4 == 0) && ((uintptr_t)Y % 16 == 0) && ((uintptr_t)E % 16 == 0);
   if (vec) {
-    cudaFuncSetAttribute(project_kernel<NC, PIX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    project_kernel<NC, PIX, true><<<blocks, 256, smem, st>>>(Y, n, B, W, ldw, ncomp, E, ldE);
+    cudaFuncSetAttribute(project_kernel<NC, PIX, true, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    project_kernel<NC, PIX, true, UB><<<blocks, 256, smem, st>>>(Y, n, B, W, ldw, ncomp, E, ldE);
   } else {
-    cudaFuncSetAttribute(project_kernel<NC, PIX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    project_kernel<NC, PIX, false><<<blocks, 256, smem, st>>>(Y, n, B, W, ldw, ncomp, E, ldE);
+    cudaFuncSetAttribute(project_kernel<NC, PIX, false, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    project_kernel<NC, PIX, false, UB><<<blocks, 256, smem, st>>>(Y, n, B, W, ldw, ncomp, E, ldE);
   }
   return cudaGetLastError();
 }
@@ -113,6 +112,8 @@ cudaError_t launch_nc(const float* Y, long long n, int B, const float* W, int ld
 
 cudaError_t launch_project(const float* Y, long long n, int B, const float* W, int ldw, int ncomp,
                            float* E, long long ldE, cudaStream_t st) {
+  // the rank loop's first chunk is 4 components: fewer accumulators, more loads in flight
+  if (ncomp <= 4) return launch_nc<4, 4, 16>(Y, n, B, W, ldw, ncomp, E, ldE, st);
   if (ncomp <= 8) return launch_nc<8, 4>(Y, n, B, W, ldw, ncomp, E, ldE, st);
   if (ncomp <= 16) return launch_nc<16, 4>(Y, n, B, W, ldw, ncomp, E, ldE, st);
   return launch_nc<32, 2>(Y, n, B, W, ldw, ncomp, E, ldE, st);
