@@ -34,7 +34,7 @@ constexpr int KC = 128;        // pixels (bytes per int8 row) per stage
 constexpr int NI = 4;          // int8 stages
 constexpr int NCW = 14;        // converter warps
 constexpr int NTHREADS = (NCW + 2) * 32;
-constexpr int MAXU = 8;        // max units per converter warp per stage: (8 + 96/16) x 8 / 14
+constexpr int MAXU = 8;        // max band rows per converter warp per stage: (64 + 48) / 14
 constexpr int TMEM_COLS = 512;
 
 struct GramTc {
@@ -104,17 +104,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     inv_s[rg][r] = is;
     s_of[rg][r] = sv;
   }
-  if (nreg == 2) {   // QS rows [nb/2, 64) stay zero in every stage and slice
-    const int g0 = (nb / 2) / 8;
-    for (int i = threadIdx.x; i < NI * 2 * (8 - g0) * (KC / 16) * 32; i += NTHREADS) {
-      const int w4 = i & 31, rest = i >> 5;
-      const int c = rest % (KC / 16), rest2 = rest / (KC / 16);
-      const int g = g0 + rest2 % (8 - g0), sl = rest2 / (8 - g0);   // sl = stage*2 + slice
-      const int off = sl * slice_bytes + region_base(1) + c * (64 * 16) + g * 128 + w4 * 4;
-      *reinterpret_cast<uint32_t*>(smem + off) = 0u;
-    }
-    tc::fence_proxy_async_smem();
-  }
+  // dead rows (QS padding, bands >= B) are never written: zero the ring once
+  for (int i = threadIdx.x; i < NI * stage_bytes / 16; i += NTHREADS)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+  tc::fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     for (int i = 0; i < NI; ++i) {
       tc::mbar_init(&bar_full[i], 2);   // one forwarded arrival per CTA
@@ -157,8 +150,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const uint32_t st1 = st0 + slice_bytes;           // S1 slice
         for (int ks = 0; ks < KC / 32; ++ks) {
           auto dsc = [&](uint32_t slice, int rg, int row0) -> uint64_t {
-            const int R = region_rows(rg, nb);
-            return tc::sdesc_kmajor_noswz(slice + region_base(rg) + ks * 2 * R * 16 + (row0 / 8) * 128, R * 16, 128);
+            (void)row0;
+            return tc::sdesc_kmajor_sw128(slice + region_base(rg) + ks * 32);
           };
           const uint32_t first = (s == 0 && ks == 0) ? 0u : 1u;
           // T_aa: A = P, B = P
@@ -185,12 +178,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   } else if (warp >= 2) {
     // ================= converters: HBM fp32 -> int8 slices in smem ==========
     // (non-finite input is detected by the amax pre-pass)
+    // One unit = one live band row of the stage: the warp's 32 lanes load its
+    // 128 pixels as 32 contiguous 16-byte pieces (512 B per load instruction)
+    // and write the 128 int8 bytes of each slice as one swizzled 128-B line
+    // (conflict-free).  The per-unit offsets and scale are stage-invariant.
     const int cw = warp - 2;
-    constexpr int cols16 = KC / 16;
-    // units of work = (region, 8-row group, 16-pixel column); P has 8 groups,
-    // QS nb/16 live groups (its zero groups were written once above).  The
-    // per-unit source offset, smem offset and scale are stage-invariant.
-    const int nunits = nreg == 1 ? 8 * cols16 : (8 + nb / 16) * cols16;
+    const int hb = nb / 2;
+    const int nrow_p = max(0, min(64, (B < 128 ? B : 128) - rank * 64));
+    const int nrow_q = nreg == 2 ? max(0, min(hb, B - 128 - rank * hb)) : 0;
+    const int nunits = nrow_p + nrow_q;
     const bool vec_ok = (P.n % 4 == 0) && (((uintptr_t)P.Y & 15) == 0);
     long long src0[MAXU];
     int soff[MAXU];
@@ -202,13 +198,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       soff[t] = 0;
       isc[t] = 0.f;
       if (u < nunits) {
-        const int rg = u < 8 * cols16 ? 0 : 1;
-        const int uu = u - rg * 8 * cols16;
-        const int g = uu / cols16, c = uu % cols16;
-        const int r = g * 8 + (lane >> 2);
-        const int b = band_of(rg, r, rank, B, nb);
-        if (b >= 0) src0[t] = (long long)b * P.n + p_begin + c * 16 + (lane & 3) * 4;
-        soff[t] = region_base(rg) + c * (64 * 16) + g * 128 + (lane >> 2) * 16 + (lane & 3) * 4;
+        const int rg = u < nrow_p ? 0 : 1;
+        const int r = rg ? u - nrow_p : u;
+        const int b = rg ? 128 + rank * hb + r : rank * 64 + r;
+        src0[t] = (long long)b * P.n + p_begin + 4 * lane;
+        soff[t] = region_base(rg) + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + 4 * (lane & 3);
         isc[t] = inv_s[rg][r];
       }
     }
@@ -226,8 +220,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           if (full) {
             v[t] = __ldcs(reinterpret_cast<const float4*>(src));
           } else {
-            // pixel index within the pair: stage offset + 16-px column (from soff) + lane quad
-            const long long pix = sh + ((soff[t] & 8191) >> 10) * 16 + (lane & 3) * 4;
+            const long long pix = sh + 4 * lane;   // pixel index within the pair
             v[t].x = pix < n_end ? src[0] : 0.f;
             v[t].y = pix + 1 < n_end ? src[1] : 0.f;
             v[t].z = pix + 2 < n_end ? src[2] : 0.f;

@@ -103,6 +103,18 @@ __device__ __forceinline__ uint64_t sdesc_kmajor_noswz(uint32_t saddr, uint32_t 
   // base offset 0, lbo mode 0, layout type 0 = SWIZZLE_NONE
   return d;
 }
+// K-major, 128-byte swizzle: each row's 128 bytes of K are one 128-B line,
+// 8-row atoms of 1024 B (1024-B aligned) with the 16-B chunk index XORed by
+// the row index within the atom; SBO = 1024 between 8-row groups, LBO unused.
+__device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                 // layout type SWIZZLE_128B
+  return d;
+}
 // instruction descriptor: kind::i8, s32 accumulate, signed A and B, K-major both
 __device__ __forceinline__ uint32_t idesc_i8(int M, int N) {
   uint32_t d = 0;
