@@ -207,6 +207,8 @@ def main():
     ap.add_argument("--config", default="large", choices=["tiny", "small", "medium", "wide", "large", "batched"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="one cube split into pixel-row slabs across the ranks (hyde_hyres_sharded; strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = synth.CONFIGS[args.config]
@@ -226,10 +228,24 @@ def main():
     # workload, its round-robin shard of the fixed batch of independent cubes
     # (strong scaling).  No data-path collective either way.
     batched = cfg.batch > 1
-    seeds = hd.shard(cfg.batch, rank, world) if batched else [rank]
+    sharded = args.shard and not batched
+    seeds = hd.shard(cfg.batch, rank, world) if batched else ([0] if sharded else [rank])
     cubes_h = [np.ascontiguousarray(synth.make_cube(cfg, seed=sd).noisy) for sd in seeds]
     ncube = len(cubes_h)
-    if batched:
+    if sharded:
+        # this rank's pixel-row slab of cube 0; Gram all-reduce + eigen-image
+        # all-gather through NCCL (torch.distributed) on the library's stream
+        r0, r1 = hy.slab_rows(cfg.rows, rank, world)
+        cubes_h = [np.ascontiguousarray(cubes_h[0][:, r0:r1, :])]
+        if world > 1:
+            comm = hy.torch_dist_comm()
+        else:
+            comm = hy.make_comm(0, 1, lambda t, st: None, lambda t, st: None,
+                                lambda snd, rcv, st: rcv.copy_(snd))
+        cube = torch.from_numpy(cubes_h[0]).cuda()
+        out = torch.empty_like(cube)
+        run = lambda: hy.hyres_sharded(cube, cfg.rows, comm, out, return_info=True)   # noqa: E731
+    elif batched:
         cube = torch.from_numpy(np.stack(cubes_h)).cuda()
         out = torch.empty_like(cube)
         run = lambda: hy.hyres_batched(cube, out, return_info=True)   # noqa: E731
@@ -273,7 +289,7 @@ def main():
     hy.profile_enable(local, False)
     ms = e0.elapsed_time(e1) / args.steps
     ms_max = hd.max_over_ranks(ms, device="cuda")
-    cubes_total = hd.sum_over_ranks(ncube, device="cuda")
+    cubes_total = 1.0 if sharded else hd.sum_over_ranks(ncube, device="cuda")
     value = hd.whole_job_rate(cubes_total * cfg.voxels, ms_max * 1e-3)
 
     # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside ----
@@ -281,16 +297,31 @@ def main():
     # the copies of neighbouring cubes overlap the current cube's compute
     pins = [torch.from_numpy(c).pin_memory() for c in cubes_h]
     pouts = [torch.empty_like(p).pin_memory() for p in pins]
-    hy.hyres_host_stream(pins[:1], pouts[:1], device=local)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     ne = max(args.e2e_steps, 1)
-    seq_in = [pins[i % ncube] for i in range(ne * ncube)]
-    seq_out = [pouts[i % ncube] for i in range(ne * ncube)]
-    t0 = time.perf_counter()
-    hy.hyres_host_stream(seq_in, seq_out, device=local)
-    torch.cuda.synchronize()
+    if sharded:
+        # each rank: its slab H2D, hyde_hyres_sharded, its slab D2H -- every step
+        def e2e_step():
+            x = pins[0].to("cuda", non_blocking=True)
+            y = hy.hyres_sharded(x, cfg.rows, comm)
+            pouts[0].copy_(y, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            e2e_step()
+        torch.cuda.synchronize()
+    else:
+        hy.hyres_host_stream(pins[:1], pouts[:1], device=local)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        seq_in = [pins[i % ncube] for i in range(ne * ncube)]
+        seq_out = [pouts[i % ncube] for i in range(ne * ncube)]
+        t0 = time.perf_counter()
+        hy.hyres_host_stream(seq_in, seq_out, device=local)
+        torch.cuda.synchronize()
     e2e_s = hd.max_over_ranks((time.perf_counter() - t0) / ne, device="cuda")
     clk.stop()
     csum = clk.summary()
@@ -340,22 +371,24 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "ms_per_cube": ms_max / ncube,
-        "higher_is_better": True, "scaling": "strong" if batched else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if (batched or sharded) else "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols,
                    "bands": cfg.bands, "cubes_per_rank": ncube,
                    "seeds": (f"batch of {cfg.batch} (seeds 0..{cfg.batch - 1}) round-robin over ranks"
-                             if batched else f"rank r uses seed r (0..{world - 1})"),
+                             if batched else ("one cube (seed 0), pixel-row slabs per rank (hyde_hyres_sharded)"
+                                              if sharded else f"rank r uses seed r (0..{world - 1})")),
                    "l2": (f"inputs larger than L2 ({nbytes / 1e6:.0f} MB per rank > 126 MB L2); no flush"
                           if nbytes > 126e6 else "cube fits in L2: steps run back to back (L2-warm)"),
                    "rank": rank_k, "levels": info["levels"], "chunks": chunks, "components": comps},
         "roofline": roof,
         "stages": per,
-        "e2e": {"value": world * ncube * cfg.voxels / e2e_s, "unit": UNIT,
+        "e2e": {"value": (1 if sharded else world * ncube) * cfg.voxels / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "ms_per_step": e2e_s * 1e3, "steps": ne,
-                "path": "hyde_hyres_host_stream (pinned host buffers; H2D of the next cube and D2H of "
-                        "the previous one overlap the current cube)"},
+                "path": ("slab H2D + hyde_hyres_sharded + slab D2H per rank (pinned)" if sharded else
+                         "hyde_hyres_host_stream (pinned host buffers; H2D of the next cube and D2H of "
+                         "the previous one overlap the current cube)")},
         "gpu_launches": int(launches),
         "clocks": csum,
     }

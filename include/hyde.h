@@ -127,6 +127,41 @@ hyde_status hyde_hyres_host(hyde_handle h, const float* cube_host, int rows, int
 hyde_status hyde_hyres_host_stream(hyde_handle h, const float* const* cubes_host, float* const* outs_host, int n,
                                    int rows, int cols, int bands, const hyde_hyres_params* params,
                                    hyde_hyres_info* info, hyde_stream_t stream);
+/* --- E1: pixel-sharded single cube (BASELINE.json
+ * north_star: "the pixel-sharded Gram matrix is all-reduced (B x B); eigen-
+ * images ... are distributed for the wavelet stage").  Rank g of G holds pixel
+ * rows [g*rows/G, (g+1)*rows/G) of every band (a BSQ slab, floor division).
+ * The library calls back for the three collectives; each callback receives
+ * DEVICE pointers whose contents were produced by work enqueued on `stream`,
+ * must run the collective after that work and make its result visible to work
+ * enqueued on `stream` afterwards (NCCL on `stream` does both), and returns 0
+ * on success.
+ *   allreduce_max_u32: element-wise max over ranks (per-band max |y| bit
+ *                      patterns: one global quantisation scale per band);
+ *   allreduce_sum_f64: element-wise sum (the B x B partial Grams);
+ *   allgather:         recv[g * bytes + i] = send_i of rank g (the ranks'
+ *                      eigen-image slabs, padded to ceil(rows/G) rows). */
+typedef struct {
+  int rank, world;
+  void* user;
+  int (*allreduce_max_u32)(void* user, unsigned* buf, size_t count, hyde_stream_t stream);
+  int (*allreduce_sum_f64)(void* user, double* buf, size_t count, hyde_stream_t stream);
+  int (*allgather)(void* user, const void* send, void* recv, size_t bytes_per_rank, hyde_stream_t stream);
+} hyde_comm;
+
+/* Denoise the rank's slab local[bands][local_rows][cols] of a rows x cols x
+ * bands cube into local_out (same layout).  Requires row0 == rank*rows/world
+ * and local_rows == (rank+1)*rows/world - row0.  The Gram, the noise estimate
+ * and the eigendecomposition are global (identical on every rank); the DWT /
+ * SURE / rank stages run on the gathered eigen-images (replicated); the
+ * reconstruction writes only the local rows.  The result equals
+ * hyde_hyres_ex on the whole cube up to the summation order of the Gram
+ * partials.  Errors: HYDE_EPARAM (shape, split or NULL callbacks), HYDE_ENCCL
+ * (a callback failed), and those of hyde_hyres_ex. */
+hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows, int row0, int rows, int cols,
+                               int bands, float* local_out, const hyde_hyres_params* params,
+                               hyde_hyres_info* info, const hyde_comm* comm, hyde_stream_t stream);
+
 /* Bytes of device workspace hyde_hyres_ex / _batched will hold for this shape. */
 size_t hyde_hyres_workspace_size(int rows, int cols, int bands, int batch,
                                  const hyde_hyres_params* params);

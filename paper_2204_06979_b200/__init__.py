@@ -13,7 +13,8 @@ from typing import Dict, Optional, Tuple
 from . import _lib
 from ._lib import HydeError, Info, Params, check, lib, make_params
 
-__all__ = ["hyres", "hyres_batched", "hyres_host", "hyres_host_stream", "estimate_noise", "workspace_size",
+__all__ = ["hyres", "hyres_batched", "hyres_host", "hyres_host_stream", "hyres_sharded", "torch_dist_comm",
+           "make_comm", "estimate_noise", "workspace_size",
            "HydeError", "stages", "version"]
 
 _handles: Dict[int, int] = {}
@@ -140,6 +141,97 @@ def hyres_host_stream(cubes, outs=None, *, device=0, taps=16, levels=0, chunk=16
     stream = torch.cuda.current_stream(device).cuda_stream
     check(lib().hyde_hyres_host_stream(h, src, dst, n, r, c, b, ctypes.byref(p), infos, stream), h)
     return (outs, [infos[i].as_dict() for i in range(n)]) if return_info else outs
+
+
+class _DevBuf:
+    """Zero-copy view of a raw device buffer for torch.as_tensor (CUDA array interface)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def dev_view(ptr, count, typestr):
+    return _torch().as_tensor(_DevBuf(ptr, count, typestr), device="cuda")
+
+
+def slab_rows(rows, rank, world):
+    """Pixel rows [r0, r1) of rank `rank` in the sharded path (include/hyde.h hyde_hyres_sharded)."""
+    return rank * rows // world, (rank + 1) * rows // world
+
+
+def make_comm(rank, world, allreduce_max_u32, allreduce_sum_f64, allgather):
+    """Wrap three Python collectives (each taking torch views of the device
+    buffers and the raw stream handle) into a hyde_comm; keep the returned
+    object alive for the duration of the call."""
+    def amax(user, buf, count, stream):
+        try:
+            allreduce_max_u32(dev_view(buf, count, "<i4"), stream)   # bit patterns of |y| >= 0: int32 max == uint32 max
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def asum(user, buf, count, stream):
+        try:
+            allreduce_sum_f64(dev_view(buf, count, "<f8"), stream)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def agather(user, send, recv, nbytes, stream):
+        try:
+            allgather(dev_view(send, nbytes, "|u1"), dev_view(recv, nbytes * world, "|u1"), stream)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    fns = (_lib.ALLREDUCE_FN(amax), _lib.ALLREDUCE_FN(asum), _lib.ALLGATHER_FN(agather))
+    c = _lib.Comm(rank, world, None, *fns)
+    c._keep = fns
+    return c
+
+
+def torch_dist_comm(group=None):
+    """hyde_comm backed by torch.distributed (NCCL over NVLink on B200 boxes);
+    the collectives run ordered on the library's stream."""
+    import torch.distributed as dist
+    torch = _torch()
+
+    def on(stream):
+        return torch.cuda.stream(torch.cuda.ExternalStream(stream))
+
+    def amax(t, stream):
+        with on(stream):
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+
+    def asum(t, stream):
+        with on(stream):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    def agather(send, recv, stream):
+        with on(stream):
+            dist.all_gather_into_tensor(recv, send, group=group)
+
+    return make_comm(dist.get_rank(group), dist.get_world_size(group), amax, asum, agather)
+
+
+def hyres_sharded(local, rows, comm, out=None, *, handle_id=None, taps=16, levels=0, chunk=16, ridge=1e-6,
+                  keep_ll=False, return_info=False):
+    """Pixel-sharded HyRes of one cube (include/hyde.h hyde_hyres_sharded):
+    `local` is this rank's BSQ slab (bands, r1 - r0, cols) with
+    (r0, r1) = slab_rows(rows, rank, world); returns the denoised slab."""
+    torch = _torch()
+    _cube(local, "local")
+    b, lr, c = local.shape
+    if out is None:
+        out = torch.empty_like(local)
+    r0, r1 = slab_rows(rows, comm.rank, comm.world)
+    p = make_params(taps, levels, chunk, ridge, keep_ll)
+    info = Info()
+    h = handle_id if handle_id is not None else handle(local.device.index)
+    check(lib().hyde_hyres_sharded(h, local.data_ptr(), lr, r0, rows, c, b, out.data_ptr(), ctypes.byref(p),
+                                   ctypes.byref(info), ctypes.byref(comm), _stream(local)), h)
+    return (out, info.as_dict()) if return_info else out
 
 
 def estimate_noise(cube, *, return_gram=False, return_residual=False):

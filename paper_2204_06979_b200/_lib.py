@@ -41,6 +41,16 @@ class Info(ctypes.Structure):
 
 
 _P = c_void_p  # device or host pointer
+
+# hyde_comm callbacks (include/hyde.h): device pointers, the caller's stream
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_void_p, c_size_t, c_void_p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p)
+
+
+class Comm(ctypes.Structure):
+    _fields_ = [("rank", c_int), ("world", c_int), ("user", c_void_p),
+                ("allreduce_max_u32", ALLREDUCE_FN), ("allreduce_sum_f64", ALLREDUCE_FN),
+                ("allgather", ALLGATHER_FN)]
 _SIGS = {
     "hyde_create": (c_int, [POINTER(c_void_p), c_int]),
     "hyde_destroy": (c_int, [c_void_p]),
@@ -55,6 +65,8 @@ _SIGS = {
     "hyde_hyres_host": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_hyres_host_stream": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p), c_int, c_int, c_int, c_int,
                                        POINTER(Params), POINTER(Info), c_void_p]),
+    "hyde_hyres_sharded": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, POINTER(Params),
+                                   POINTER(Info), POINTER(Comm), c_void_p]),
     "hyde_hyres_workspace_size": (c_size_t, [c_int, c_int, c_int, c_int, POINTER(Params)]),
     "hyde_hyres_batched": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_sync_status": (c_int, [c_void_p, c_void_p]),

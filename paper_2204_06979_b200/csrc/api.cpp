@@ -515,6 +515,175 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   return HYDE_OK;
 }
 
+hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows, int row0, int rows, int cols,
+                               int bands, float* local_out, const hyde_hyres_params* params,
+                               hyde_hyres_info* info, const hyde_comm* comm, hyde_stream_t stream) {
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  if (!local || !local_out || !comm || !comm->allreduce_max_u32 || !comm->allreduce_sum_f64 || !comm->allgather)
+    return fail(h, HYDE_EPARAM, "NULL slab / output / collective callbacks");
+  const int G = comm->world, gr = comm->rank;
+  if (G < 1 || gr < 0 || gr >= G || rows < G) return fail(h, HYDE_EPARAM, "bad rank / world");
+  auto rbeg = [&](int g) { return (int)((long long)g * rows / G); };
+  if (row0 != rbeg(gr) || local_rows != rbeg(gr + 1) - row0)
+    return fail(h, HYDE_EPARAM, "slab must be rows [rank*rows/world, (rank+1)*rows/world)");
+  hyde_hyres_params p;
+  int levels = 0;
+  s = resolve_params(h, rows, cols, params, &p, &levels);
+  if (s != HYDE_OK) return s;
+  FilterBank fb;
+  if (hyde_build_filters(p.wavelet_taps, &fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "filter derivation failed");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = bands;
+  Layout L;                        // full-image geometry (DWT plan, eigen-images)
+  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L);
+  const long long n_loc = (long long)local_rows * cols;
+  Layout Ll;                       // slab geometry (Gram partials, projection)
+  make_layout(local_rows, cols, B, p.chunk, levels < 1 ? 1 : 1, 2, &Ll);
+  s = ensure_ws(h, L.total + Ll.total, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  char* wl = h->ws + L.total;      // slab-sized pieces (Gram partials, amax)
+  const long long n = L.n;
+  s = ensure_ebuf(h, (size_t)p.chunk * L.ldE * 4, 0, st);
+  if (s != HYDE_OK) return s;
+  RankState* rs = (RankState*)(ws + L.rs);
+  h->last_rs = rs;
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  double* Gm = (double*)(ws + L.G);
+  double* sigma = (double*)(ws + L.sigma);
+  double* house = (double*)(ws + L.house);
+  double* tri = (double*)(ws + L.tri);
+  float* W = (float*)(ws + L.W);
+  float* U = (float*)(ws + L.U);
+  float* C = (float*)(ws + L.C);
+  auto coll = [&](int rc) -> hyde_status {
+    return rc == 0 ? HYDE_OK : fail(h, HYDE_ENCCL, "collective callback failed");
+  };
+  // ---- A1: global per-band scales, local exact Gram, all-reduced ----
+  {
+    Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? 3 : 2, st);
+    if (Ll.use_tc) {
+      unsigned* amax = (unsigned*)(wl + Ll.amax);
+      CK(launch_gram_amax(local, n_loc, B, amax, &rs->nonfinite, st));
+      s = coll(comm->allreduce_max_u32(comm->user, amax, (size_t)B, stream));
+      if (s != HYDE_OK) return s;
+      CK(launch_gram_tc_scaled(local, n_loc, B, amax, (double*)(wl + Ll.partial), Ll.npairs, Gm, &rs->nonfinite,
+                               st));
+    } else {
+      CK(launch_gram(local, n_loc, B, (double*)(wl + Ll.partial), Ll.nsplit, Gm, &rs->nonfinite, st));
+    }
+    s = coll(comm->allreduce_sum_f64(comm->user, Gm, (size_t)B * B, stream));
+    if (s != HYDE_OK) return s;
+    sg.end();
+  }
+  auto chunk_len = [&](int c) {
+    long long want = (long long)kFirstChunk << (c < 20 ? c : 20);
+    if (want > p.chunk) want = p.chunk;
+    return (int)want;
+  };
+  const int first = chunk_len(0) < B ? chunk_len(0) : B;
+  {
+    Stage sg(h, HYDE_STAGE_EIG, 1, st);
+    CK(launch_noise_eig(Gm, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
+    sg.end();
+  }
+  // all-gather buffers: every rank's slab of every chunk component, padded to ceil(rows/G) rows
+  const long long lr_max = (rows + G - 1) / G;
+  const size_t slab_f = (size_t)lr_max * cols;
+  float* sendb = nullptr;
+  float* recvb = nullptr;
+  CK(cudaMallocAsync((void**)&sendb, (size_t)p.chunk * slab_f * 4, st));
+  CK(cudaMallocAsync((void**)&recvb, (size_t)G * p.chunk * slab_f * 4, st));
+  struct Free {
+    float *a, *b;
+    cudaStream_t st;
+    ~Free() {
+      cudaFreeAsync(a, st);
+      cudaFreeAsync(b, st);
+    }
+  } fr{sendb, recvb, st};
+  int rank = 0, chunks = 0;
+  int k0 = 0, comps = 0;
+  for (int c = 0;; ++c) {
+    const int cl = chunk_len(c);
+    const int cnt = (B - k0) < cl ? (B - k0) : cl;
+    if (c > 0) {
+      s = ensure_ebuf(h, (size_t)(k0 + cnt) * L.ldE * 4, (size_t)k0 * L.ldE * 4, st);
+      if (s != HYDE_OK) return s;
+      Stage sg(h, HYDE_STAGE_EIG, 1, st);
+      CK(launch_eigvec_more(tri, house, sigma, B, k0, cnt, nullptr, nullptr, W, U, L.ldwu, st));
+      sg.end();
+    }
+    float* E = h->ebuf + (size_t)k0 * L.ldE;
+    {
+      // A3 on the local slab, then slab -> whole eigen-images on every rank
+      Stage sg(h, HYDE_STAGE_PROJECT, 1 + G * cnt, st);
+      CK(launch_project(local, n_loc, B, W + k0, L.ldwu, cnt, sendb, (long long)slab_f, st));
+      s = coll(comm->allgather(comm->user, sendb, recvb, (size_t)cnt * slab_f * 4, stream));
+      if (s != HYDE_OK) return s;
+      for (int g = 0; g < G; ++g) {
+        const long long rb = rbeg(g), lr = rbeg(g + 1) - rb;
+        for (int k = 0; k < cnt; ++k)
+          CK(cudaMemcpyAsync(E + (size_t)k * L.ldE + rb * cols, recvb + ((size_t)g * cnt + k) * slab_f,
+                             (size_t)lr * cols * 4, cudaMemcpyDeviceToDevice, st));
+      }
+      sg.end();
+    }
+    {
+      Stage sg(h, HYDE_STAGE_DWT, levels, st);
+      CK(dwt_forward(L, ws, E, L.ldE, cnt, fb, st));
+      sg.end();
+    }
+    {
+      Stage sg(h, HYDE_STAGE_SURE, 1, st);
+      CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
+                     (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, (unsigned*)(ws + L.surv), st));
+      sg.end();
+    }
+    {
+      Stage sg(h, HYDE_STAGE_RANK, 1, st);
+      CK(launch_rank_decide((double*)(ws + L.esub), L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs,
+                            (double*)(ws + L.epost), st));
+      CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
+      sg.end();
+    }
+    CK(cudaStreamSynchronize(st));
+    ++chunks;
+    comps += cnt;
+    const RankState r = *h->rs_host;
+    if (r.nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
+    if (r.sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
+    const int kept = r.found ? (r.rank - k0) : cnt;
+    if (kept > 0) {
+      Stage sg(h, HYDE_STAGE_IDWT, levels, st);
+      CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, (const float*)(ws + L.tstar), st));
+      sg.end();
+    }
+    if (r.found) {
+      rank = r.rank;
+      break;
+    }
+    k0 += cnt;
+  }
+  {
+    // A6 on the local rows only
+    Stage sg(h, HYDE_STAGE_RECON, (rank + 7) / 8, st);
+    CK(launch_reconstruct(h->ebuf + (size_t)row0 * cols, L.ldE, n_loc, B, U, L.ldwu, rank, local_out, st));
+    sg.end();
+  }
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->rank = rank;
+    info->levels = levels;
+    info->chunks_run = chunks;
+    info->n_coeffs = (int)L.plan.n_coeffs;
+    info->comps = comps;
+  }
+  return HYDE_OK;
+}
+
 hyde_status hyde_profile_enable(hyde_handle h, int on) {
   if (!h) return HYDE_EPARAM;
   DeviceGuard g(h->device);

@@ -62,6 +62,9 @@ bool gram_tc_supported(int B);
 int gram_tc_npairs(long long n);
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
                            double* G, int* nonfinite, cudaStream_t st);
+cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st);
+cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsigned* amax_bits, double* partial,
+                                  int npairs, double* G, int* nonfinite, cudaStream_t st);
 size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,

@@ -390,17 +390,22 @@ int gram_tc_npairs(long long n) {
   return (int)np;
 }
 
-cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
-                           double* G, int* nonfinite, cudaStream_t st) {
+// per-band max |y| bit patterns (the quantisation scales of K1) + non-finite flag
+cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(amax_bits, 0, (size_t)B * sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
-  {
-    long long per_block = 256LL * 4 * 8;
-    unsigned gx = (unsigned)((n + per_block - 1) / per_block);
-    if (gx > 64) gx = 64;
-    if (gx < 1) gx = 1;
-    amax_kernel<<<dim3(gx, B), 256, 0, st>>>(Y, n, amax_bits, nonfinite);
-  }
+  long long per_block = 256LL * 4 * 8;
+  unsigned gx = (unsigned)((n + per_block - 1) / per_block);
+  if (gx > 64) gx = 64;
+  if (gx < 1) gx = 1;
+  amax_kernel<<<dim3(gx, B), 256, 0, st>>>(Y, n, amax_bits, nonfinite);
+  return cudaGetLastError();
+}
+
+// exact integer Gram of Y with the given per-band scales (amax_bits)
+cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsigned* amax_bits, double* partial,
+                                  int npairs, double* G, int* nonfinite, cudaStream_t st) {
+  cudaError_t e;
   GramTc P;
   P.Y = Y;
   P.n = n;
@@ -420,4 +425,11 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bi
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_gram_reduce(partial, npairs, B, G, st);
+}
+
+cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
+                           double* G, int* nonfinite, cudaStream_t st) {
+  cudaError_t e = launch_gram_amax(Y, n, B, amax_bits, nonfinite, st);
+  if (e != cudaSuccess) return e;
+  return launch_gram_tc_scaled(Y, n, B, amax_bits, partial, npairs, G, nonfinite, st);
 }
