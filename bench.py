@@ -120,18 +120,35 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ algorithmic bytes
+def level_shapes(rows, cols, levels):
+    """Subband shape per level: (ceil(h/2), ceil(w/2)) of the previous LL (R5)."""
+    out, h, w = [], rows, cols
+    for _ in range(levels):
+        h, w = (h + 1) // 2, (w + 1) // 2
+        out.append((h, w))
+    return out
+
+
+def dwt_image_bytes(rows, cols, levels):
+    """Per image and level: read the level input, write LL + 3 detail subbands."""
+    h, w, b = rows, cols, 0
+    for (hs, ws) in level_shapes(rows, cols, levels):
+        b += 4 * h * w + 4 * 4 * hs * ws
+        h, w = hs, ws
+    return b
+
+
+def coeff_count(rows, cols, levels):
+    sh = level_shapes(rows, cols, levels)
+    return 3 * sum(h * w for h, w in sh) + sh[-1][0] * sh[-1][1]
+
+
 def stage_bytes(cfg, levels, rank, comps, chunks):
     """Algorithmic HBM bytes per step for each stage: the minimum
     each stage must move.  comps = candidate components projected/transformed."""
-    from oracle import hyres_ref as O  # geometry only (level shapes); not timed
     n, b = cfg.rows * cfg.cols, cfg.bands
-    sh = O.level_shapes(cfg.rows, cfg.cols, levels)
-    nc = O.coeff_count(cfg.rows, cfg.cols, levels)
-    h, w = cfg.rows, cfg.cols
-    dwt_img = 0
-    for (hs, ws) in sh:
-        dwt_img += 4 * h * w + 4 * 4 * hs * ws     # read level input, write LL + 3 details
-        h, w = hs, ws
+    nc = coeff_count(cfg.rows, cfg.cols, levels)
+    dwt_img = dwt_image_bytes(cfg.rows, cfg.cols, levels)
     return {
         "gram": 4 * n * b,
         "project": chunks * 4 * n * b + 4 * n * comps,
@@ -140,6 +157,65 @@ def stage_bytes(cfg, levels, rank, comps, chunks):
         "idwt": rank * dwt_img,
         "recon": 4 * n * rank + 4 * n * b,
     }
+
+
+def wavelet_isolated(hy, torch, cube, cfg, levels, steps, hbm):
+    """Stage-isolated A4 -> A5 -> A6a on ALL B eigen-images of the cube (SURVEY.md
+    §8(d): the end-to-end path transforms only a few components, too short for a
+    stable HBM fraction).  Setup (not timed): G by the library's Gram, sigma by
+    K2, the whitened eigenvectors by torch.linalg.eigh and E = W^T Y by a torch
+    matmul.  Timed: hyde_wavelet_shrink (DWT levels + one SURE launch + IDWT
+    levels with the fused soft threshold), `steps` calls, CUDA events per stage."""
+    b, n = cfg.bands, cfg.rows * cfg.cols
+    y = cube.view(b, n)
+    G = hy.stages.gram(cube)
+    sigma, _, _ = hy.stages.eig(G, n, 1, all_lam=False)
+    gw = G / (sigma[:, None] * sigma[None, :]) / n
+    _, V = torch.linalg.eigh(gw)
+    W = (V.flip(1) / sigma[:, None]).to(torch.float32)
+    E = (W.t() @ y).view(b, cfg.rows, cfg.cols).contiguous()
+    del G, gw, V, W
+    out = torch.empty_like(E)
+    hy.stages.wavelet_shrink(E, levels, out=out, stats=False)
+    hy.stages.wavelet_shrink(E, levels, out=out, stats=False)
+    torch.cuda.synchronize()
+    dev = cube.device.index
+    hy.profile_enable(dev, True)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        hy.stages.wavelet_shrink(E, levels, out=out, stats=False)
+    e1.record(st)
+    torch.cuda.synchronize()
+    stg = hy.profile_read(dev)
+    hy.profile_enable(dev, False)
+    ms = e0.elapsed_time(e1) / steps
+    nc = coeff_count(cfg.rows, cfg.cols, levels)
+    lvl = b * dwt_image_bytes(cfg.rows, cfg.cols, levels)
+    byt = {"dwt": lvl, "sure": b * 4 * nc, "idwt": lvl}
+    res = {"images": b, "rows": cfg.rows, "cols": cfg.cols, "levels": levels, "ms": round(ms, 4)}
+    tot_b, tot_t = 0, 0.0
+    for k in ("dwt", "sure", "idwt"):
+        t = stg[k][0] / steps
+        gbs = byt[k] / (t * 1e-3) / 1e9
+        res[k] = {"ms": round(t, 4), "bytes": byt[k], "GBps": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
+        tot_b += byt[k]
+        tot_t += t
+    ds_b = byt["dwt"] + byt["sure"]
+    ds_t = res["dwt"]["ms"] + res["sure"]["ms"]
+    res["dwt+sure"] = {"ms": round(ds_t, 4), "bytes": ds_b, "GBps": round(ds_b / (ds_t * 1e-3) / 1e9, 1),
+                       "frac_hbm": round(ds_b / (ds_t * 1e-3) / 1e9 / hbm, 4)}
+    res["dwt+sure+idwt"] = {"ms": round(tot_t, 4), "bytes": tot_b,
+                            "GBps": round(tot_b / (tot_t * 1e-3) / 1e9, 1),
+                            "frac_hbm": round(tot_b / (tot_t * 1e-3) / 1e9 / hbm, 4)}
+    # the method's minimum (SURVEY.md §8(d)): DWT one read of N + one write of N_c
+    # per image (a fused multi-level transform), SURE one read of N_c
+    mb = b * (4 * n + 4 * nc + 4 * nc)
+    res["dwt+sure_min_bytes"] = {"bytes": mb, "frac_hbm": round(mb / (ds_t * 1e-3) / 1e9 / hbm, 4)}
+    del E, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def cpu_baseline(cube, reps=2):
@@ -207,6 +283,8 @@ def main():
     ap.add_argument("--config", default="large", choices=["tiny", "small", "medium", "wide", "large", "batched"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--iso-steps", type=int, default=5,
+                    help="steps of the stage-isolated DWT/SURE/IDWT leg on all B eigen-images (0: skip)")
     ap.add_argument("--shard", action="store_true",
                     help="one cube split into pixel-row slabs across the ranks (hyde_hyres_sharded; strong scaling)")
     args = ap.parse_args()
@@ -291,6 +369,11 @@ def main():
     ms_max = hd.max_over_ranks(ms, device="cuda")
     cubes_total = 1.0 if sharded else hd.sum_over_ranks(ncube, device="cuda")
     value = hd.whole_job_rate(cubes_total * cfg.voxels, ms_max * 1e-3)
+
+    iso = None
+    if args.iso_steps > 0 and not batched and not sharded and rank == 0:
+        hbm_, _, _ = peaks()
+        iso = wavelet_isolated(hy, torch, cube, cfg, info["levels"], args.iso_steps, hbm_)
 
     # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside ----
     # hyde_hyres_host_stream: every step copies its cubes in and its results out;
@@ -392,6 +475,8 @@ def main():
         "gpu_launches": int(launches),
         "clocks": csum,
     }
+    if iso is not None:
+        line["wavelet_isolated"] = iso
     if world == 1 and not args.no_cpu_baseline:
         t, cores, thr = cpu_baseline(cubes_h[0], reps=2)
         line["cpu_baseline"] = {"value": cfg.voxels / t, "unit": UNIT, "cores": cores, "threads": thr,

@@ -205,6 +205,24 @@ hyde_status hyde_k_sure(hyde_handle h, float* coeffs, int count, int rows, int c
 /* A6a: inverse DWT of `count` coefficient sets -> images (rows x cols each). */
 hyde_status hyde_k_idwt(hyde_handle h, const float* coeffs, int count, int rows, int cols,
                         int levels, int taps, float* images, hyde_stream_t stream);
+/* A4 -> A5 -> A6a on `count` images exactly as the hot path runs them
+ * (BASELINE.json north_star stages (4)-(6): "a batched multi-level orthogonal
+ * 2D discrete wavelet transform of every eigen-image; per-subband SURE
+ * threshold selection ... with soft-thresholding; inverse DWT"):
+ * forward DWT (L launches), one SURE launch over every (image, subband), and
+ * the inverse DWT with each subband soft-thresholded by its t* as it is
+ * loaded (no rank rule: every image is reconstructed).  images / out: DEVICE,
+ * count x rows x cols fp32 (out == images allowed; partial overlap ->
+ * HYDE_EPARAM).  kstar / tstar [count*(3L+1)] (DEVICE, subband order of
+ * hyde_k_dwt_fwd) and e_post [count] (DEVICE, sum of the thresholded
+ * coefficients squared) may each be NULL.  Workspace (about 2.3 x the image
+ * bytes) is held by the handle.  Asynchronous; a SURE capacity failure is
+ * reported by hyde_sync_status (HYDE_EMETHOD).  This is the stage-isolated
+ * measurement of SURVEY.md §8(d) ("a stage-isolated run on all B eigen-images
+ * of large") and a standalone wavelet-shrinkage denoiser. */
+hyde_status hyde_wavelet_shrink(hyde_handle h, const float* images, int count, int rows, int cols,
+                                int levels, int taps, int keep_ll, float* out, int* kstar,
+                                float* tstar, double* e_post, hyde_stream_t stream);
 /* A6b: out[b][p] = sum_{k<rank} U[b][k] E[k][p], U float32 row-major bands x ldu. */
 hyde_status hyde_k_reconstruct(hyde_handle h, const float* E, int n_pixels, int bands,
                                const float* U, int ldu, int rank, float* out,

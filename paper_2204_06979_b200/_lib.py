@@ -78,6 +78,8 @@ _SIGS = {
     "hyde_auto_levels": (c_int, [c_int, c_int, c_int]),
     "hyde_k_sure": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, _P, _P, c_void_p]),
     "hyde_k_idwt": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, c_void_p]),
+    "hyde_wavelet_shrink": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, c_int, _P, _P, _P, _P,
+                                    c_void_p]),
     "hyde_k_reconstruct": (c_int, [c_void_p, _P, c_int, c_int, _P, c_int, c_int, _P, c_void_p]),
     "hyde_filter": (c_int, [c_int, POINTER(c_double)]),
     "hyde_profile_enable": (c_int, [c_void_p, c_int]),

@@ -1024,6 +1024,53 @@ hyde_status hyde_k_sure(hyde_handle h, float* coeffs, int count, int rows, int c
   return HYDE_OK;
 }
 
+hyde_status hyde_wavelet_shrink(hyde_handle h, const float* images, int count, int rows, int cols, int levels,
+                                int taps, int keep_ll, float* out, int* kstar, float* tstar, double* e_post,
+                                hyde_stream_t stream) {
+  if (!images || !out) return fail(h, HYDE_EPARAM, "NULL pointer");
+  const size_t ib = (size_t)count * rows * cols * sizeof(float);
+  if (images != out && overlap(images, ib, out, ib)) return fail(h, HYDE_EPARAM, "images and out partially overlap");
+  DeviceGuard g(h ? h->device : 0);
+  cudaStream_t st = (cudaStream_t)stream;
+  Layout L;
+  FilterBank fb;
+  hyde_status s = stage_layout(h, count, rows, cols, levels, taps, &L, &fb, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  RankState* rs = (RankState*)(ws + L.rs);
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  float* C = (float*)(ws + L.C);
+  int* ks = (int*)(ws + L.kstar);
+  float* ts = (float*)(ws + L.tstar);
+  double* es = (double*)(ws + L.esub);
+  const long long ld = (long long)rows * cols;
+  {
+    Stage sg(h, HYDE_STAGE_DWT, levels, st);
+    CK(dwt_forward(L, ws, images, ld, count, fb, st));
+    sg.end();
+  }
+  {
+    Stage sg(h, HYDE_STAGE_SURE, 1, st);
+    CK(launch_sure(C, L.plan.n_coeffs, L.plan, count, keep_ll, ks, ts, es, rs, (unsigned*)(ws + L.surv), st));
+    sg.end();
+  }
+  {
+    Stage sg(h, HYDE_STAGE_IDWT, levels, st);
+    CK(dwt_inverse(L, ws, C, out, ld, count, fb, ts, st));
+    sg.end();
+  }
+  if (e_post) {
+    Stage sg(h, HYDE_STAGE_RANK, 1, st);
+    CK(launch_rank_decide(es, L.nsub, count, 0, (double)L.plan.n_coeffs, 1 << 30, rs, e_post, st));
+    sg.end();
+  }
+  const size_t nk = (size_t)count * L.nsub;
+  if (kstar) CK(cudaMemcpyAsync(kstar, ks, nk * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  if (tstar) CK(cudaMemcpyAsync(tstar, ts, nk * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  h->last_rs = rs;
+  return HYDE_OK;
+}
+
 hyde_status hyde_k_reconstruct(hyde_handle h, const float* E, int n_pixels, int bands, const float* U, int ldu,
                                int rank, float* out, hyde_stream_t stream) {
   if (!h || !E || !U || !out || n_pixels < 1 || bands < 1 || rank < 1 || ldu < rank)

@@ -7,6 +7,7 @@ Each consumes / produces the oracle's intermediate layout (oracle/hyres_ref.py):
   dwt_fwd    images (count, R, C)     -> coeffs (count, N_c): level 1..L x (LH, HL, HH), LL_L
   sure       coeffs (in place)        -> kstar, tstar (count, 3L+1), e_post (count,)
   idwt       coeffs                   -> images
+  wavelet_shrink images (count, R, C)  -> denoised images, kstar, tstar, e_post (A4 -> A5 -> A6a)
   reconstruct E (r, N), U (B, r)      -> out (B, N)
 """
 from __future__ import annotations
@@ -105,6 +106,25 @@ def idwt(coeffs, rows, cols, levels, taps=16):
     check(lib().hyde_k_idwt(h, coeffs.contiguous().data_ptr(), cnt, rows, cols, levels, taps, out.data_ptr(),
                             _stream(coeffs)), h)
     return out
+
+
+def wavelet_shrink(images, levels, taps=16, keep_ll=False, out=None, stats=True):
+    """A4 -> A5 -> A6a on a batch of images, as the hot path runs them (hyde_wavelet_shrink).
+    Returns out (count, R, C) and, with stats, kstar / tstar (count, 3L+1) and e_post (count,)."""
+    torch = _torch()
+    _cube(images, "images")
+    cnt, r, c = images.shape
+    nsub = 3 * levels + 1
+    if out is None:
+        out = torch.empty_like(images)
+    ks = torch.empty((cnt, nsub), dtype=torch.int32, device=images.device) if stats else None
+    ts = torch.empty((cnt, nsub), dtype=torch.float32, device=images.device) if stats else None
+    ep = torch.empty(cnt, dtype=torch.float64, device=images.device) if stats else None
+    h = _h(images)
+    p = lambda t: t.data_ptr() if t is not None else None
+    check(lib().hyde_wavelet_shrink(h, images.data_ptr(), cnt, r, c, levels, taps, 1 if keep_ll else 0, out.data_ptr(),
+                                    p(ks), p(ts), p(ep), _stream(images)), h)
+    return (out, ks, ts, ep) if stats else out
 
 
 def reconstruct(E, U, bands_shape=None):

@@ -237,3 +237,37 @@ def test_reconstruct_matches_fp64(hy):
         out = hy.stages.reconstruct(dev(e), dev(u)).cpu().numpy()
         ref = u.astype(np.float64) @ e.astype(np.float64)
         assert np.max(np.abs(out - ref)) / np.max(np.abs(ref)) < 1e-6
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 2), (145, 145, 3), (256, 256, 4), (37, 50, 1)])
+def test_wavelet_shrink_matches_oracle(hy, shape):
+    """hyde_wavelet_shrink (A4 -> A5 -> A6a as the hot path runs them) vs the oracle's
+    dwt2 -> per-subband SURE -> soft threshold -> idwt2 on the same images."""
+    r, c, lv = shape
+    rng = np.random.default_rng(6)
+    yy, xx = np.mgrid[0:r, 0:c]
+    imgs = []
+    for k in range(3):
+        clean = (8.0 / (k + 1)) * np.sin(xx / (5.0 + 3 * k)) * np.cos(yy / (7.0 + k))
+        imgs.append(clean + rng.standard_normal((r, c)))
+    x = np.stack(imgs).astype(np.float32)
+    out, ks, ts, ep = hy.stages.wavelet_shrink(dev(x), lv)
+    out, ks, ts, ep = out.cpu().numpy(), ks.cpu().numpy(), ts.cpu().numpy(), ep.cpu().numpy()
+    co = hy.stages.dwt_fwd(dev(x), lv).cpu().numpy()          # the coefficients SURE saw
+    for i in range(x.shape[0]):
+        res, offs = _oracle_sure_on(co[i], r, c, lv)
+        for j, sr in enumerate(res):
+            scale = offs[j + 1] - offs[j] + float(np.sum(co[i, offs[j]:offs[j + 1]].astype(np.float64) ** 2))
+            if sr.margin > 1e-9 * scale:
+                assert ks[i, j] == sr.k and ts[i, j] == np.float32(sr.t), (i, j, ks[i, j], sr.k)
+        subs = O.flatten_coeffs(O.dwt2(x[i].astype(np.float64), lv, 16))
+        soft = [O.soft_threshold(sb, float(ts[i, j])) for j, sb in enumerate(subs)]
+        tmpl = O.dwt2(np.zeros((r, c)), lv, 16)
+        ref = O.idwt2(O.unflatten_coeffs(soft, tmpl), 16)
+        assert np.linalg.norm(out[i] - ref) <= 1e-4 * np.linalg.norm(ref)
+        e_ref = sum(float(np.sum(sb ** 2)) for sb in soft)
+        assert abs(ep[i] - e_ref) <= 1e-5 * e_ref
+    # in place (out == images) gives the same result
+    g = dev(x)
+    same = hy.stages.wavelet_shrink(g, lv, out=g, stats=False)
+    assert np.array_equal(same.cpu().numpy(), out)
