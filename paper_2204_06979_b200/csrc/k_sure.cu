@@ -10,49 +10,63 @@
 // The soft threshold itself is applied by the inverse DWT when it loads the
 // coefficients (K6a), so this kernel only reads the subband.
 //
-// Exact argmin without sorting n elements.  One launch covers every
-// (component, subband); a subband with n >= BIG_MIN is split over a cluster
-// of G CTAs (slices of n/G), smaller ones take one CTA each (G per cluster).
-//  * the fp32 bit pattern of |x| is an order-preserving uint32 key; the key
-//    window starts as the exact [min, max] of the subband;
-//  * pruning passes: every thread keeps PRIVATE (count, fp64 sum of squares)
-//    accumulators for 32 bins -- 30 equal key-bins over the window (equal key
-//    width = log-spaced magnitudes) plus two catch-alls -- in shared memory
-//    (no atomics: shared-memory float/int64 atomics are CAS loops on sm_100),
-//    reduced in a fixed order; each rank pushes its bins to the cluster
-//    leader over DSMEM.  Exact counts and sums at the bin edges give, per bin j,
-//      S_k >= LB_j = n - 2(c_j+m_j) + q_j + (n - c_j) lo_j^2,
-//      min S <= UB_j = n - 2(c_j+m_j) + q_j + sq_j + (n-c_j-m_j) hi_j^2.
-//    Bins whose LB exceeds the best UB cannot hold the argmin; the window
-//    shrinks to the hull of the surviving bins (everything outside it was
-//    pruned earlier: the best UB only decreases);
-//  * the survivors are written to a scratch list, the window is cut at bin
-//    edges into one key sub-range per rank, and each rank evaluates S_k
-//    exactly over its sub-range in ascending chunks of <= CAPL keys (gathered,
-//    sorted in shared memory by a register bitonic + merge-path sort, fp64
-//    prefix sums in sorted order; products of fp32 values are exact in fp64),
-//    starting from the exact count / sum below the sub-range.  A chunk that
-//    is one repeated key is evaluated in closed form (S falls by 2 per step
-//    along a run of equal magnitudes: its best is the run end).
-// Every sum is taken in a fixed order, so the result is deterministic.
+// Exact argmin with two streaming reads of the subband instead of a sort of n
+// keys.  One launch covers every (component, subband); a subband with
+// n >= BIG_MIN is split over the CTAs of a cluster (slices of n/G; G = 8 when
+// few subbands are in flight, 1 when there are enough to fill the GPU),
+// shorter ones take one CTA each.
+//  * the fp32 bit pattern of |x| is an order-preserving uint32 key;
+//  * histogram pass: HB = 4096 bins of 2^17 keys (64 bins per octave) over
+//    |x| in [2^-40, 2^24) with exact counts and exact integer sums of the
+//    fixed-point squares (fxsq: x^2 known to 2^-14 relative, bounded both
+//    ways), shared-memory u32 atomics; keys outside the range are summed
+//    exactly in fp64.  Cluster slices are merged by a reduce-scatter over
+//    DSMEM (each rank owns HB/G bins, summed in rank order).  Exact counts and
+//    bounded sums at the bin edges give, per bin j (c keys below, m in it,
+//    values in [lo, hi]):
+//      S_k >= LB_j = n - 2(c+m) + P_lo(c) + (n-c) lo^2   for every k in bin j,
+//      min S <= UB_j = n - 2(c+m) + P_hi(c) + Q_hi,j + (n-c-m) hi^2;
+//    bins whose LB exceeds the least UB cannot hold the argmin.  The window
+//    [klo, khi] = hull of the surviving bins holds a few hundred keys on
+//    real subbands (at most CAP = 8192 allowed; otherwise the window is
+//    re-binned with finer bins and the pass repeats);
+//  * compaction pass: window keys go to the leader's shared memory; the exact
+//    fp64 sum of x^2 below the window and the sums of x and x^2 above it are
+//    accumulated in a fixed order;
+//  * the leader sorts the window keys (register bitonic + merge path) and
+//    evaluates S_k exactly with fp64 prefix sums (fp32 products are exact in
+//    fp64) from the exact prefix below the window; a window that is one
+//    repeated key is evaluated in closed form (S falls by 2 per step along a
+//    run of equal magnitudes: its best is the run end);
+//  * E_post = sum over the window of (a - t)_+^2 + (Q2 - 2 t Q1 + c t^2) above
+//    the window (+ the sum below it when t = 0).
+// Every sum is taken in a fixed order, so the result is deterministic for a
+// given launch configuration.
 #include "common.cuh"
 #include "tc_util.cuh"
+#include <climits>
 #include <cstdio>
 
 namespace {
 
 constexpr int NT = 256;
 constexpr int NWS = NT / 32;
-constexpr int NBIN = 32;          // 0 = below, 1..30 inner, 31 = above
-constexpr int NIN = NBIN - 2;
-constexpr int G = 8;              // cluster size (CTAs per big subband)
-constexpr int CAPL = NT * 32;     // keys one CTA sorts at a time (8192)
-constexpr int BIG_MIN = 32768;    // subbands at least this long use a cluster
-constexpr int MAXPASS = 12;
-constexpr int SURV_GOAL = 2048;   // prune until at most this many keys survive (or no progress)
-constexpr int PF = 16;            // loads in flight per thread in the streaming passes
-constexpr int PFC = 8;            // ... in the compaction streams (more live state per value)
-constexpr size_t SMEM_DYN = (size_t)NBIN * NT * sizeof(unsigned long long);   // == 2 x CAPL keys
+constexpr int GMAX = 8;                   // largest cluster per subband
+constexpr int HB = 4096;                  // histogram bins per pass
+constexpr int HS0 = 17;                   // pass-1 bin width: 2^17 keys = 64 bins per octave
+constexpr unsigned KB0 = 87u << 23;       // pass-1 bins cover |x| in [2^-40, 2^24)
+constexpr unsigned KE0 = KB0 + ((unsigned)HB << HS0) - 1u;
+constexpr int CAP = NT * 32;              // window keys sorted at once (8192)
+constexpr int BIG_MIN = 32768;            // subbands at least this long may use a cluster
+constexpr int MAXPASS = 8;
+constexpr size_t SMEM_DYN = (size_t)2 * CAP * sizeof(unsigned);   // histogram (2 HB u32) | sort buffers (2 CAP u32)
+static_assert(2 * HB <= 2 * CAP, "histogram must fit the sort buffers");
+
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
 
 struct SubTable {
   long long off[3 * HYDE_MAX_LEVELS + 1];
@@ -127,8 +141,6 @@ __device__ double block_excl_scan(double v, double* scan, double* total) {
   return r;
 }
 
-__device__ __forceinline__ unsigned keyof(float x) { return __float_as_uint(fabsf(x)); }
-__device__ __forceinline__ double kval(unsigned k) { return (double)__uint_as_float(k); }
 
 // Sort buffers are addressed through sw(): the low 5 index bits are XORed with
 // the row (index / 32), so per-thread contiguous runs of 32 keys -- the
@@ -202,568 +214,532 @@ __device__ unsigned* block_sort(unsigned* keys, unsigned* buf, int P) {
   return keys + so;
 }
 
-// bin(k) = min(NIN-1, int(float(k-klo) * inv)) is monotone in k and THE bin
-// definition; edge[] inverts it exactly (inner bin j holds keys
-// [edge[j], edge[j+1]-1]), so bounds built on the edges hold whatever the
-// rounding of inv.
-__device__ __forceinline__ float bin_inv(unsigned klo, unsigned khi) {
-  return (float)NIN * __frcp_rn((float)(khi - klo) + 1.0f);
-}
-__device__ __forceinline__ int bin_of(unsigned k, unsigned klo, unsigned khi, float inv) {
-  if (k < klo) return 0;
-  if (k > khi) return NBIN - 1;
-  return 1 + min(NIN - 1, (int)((float)(k - klo) * inv));
-}
-// lane j of the calling warp computes edge[j]
-__device__ __forceinline__ void bin_edges(unsigned klo, unsigned khi, unsigned* edge) {
-  const int l = threadIdx.x & 31;
-  const float inv = bin_inv(klo, khi);
-  if (l == 0) { edge[0] = klo; edge[NIN] = khi + 1u; }
-  if (l >= 1 && l < NIN) {
-    unsigned lo = klo, hi = khi + 1u;
-    while (lo < hi) {
-      const unsigned mid = lo + ((hi - lo) >> 1);
-      const int bm = min(NIN - 1, (int)((float)(mid - klo) * inv));
-      if (bm >= l) hi = mid; else lo = mid + 1u;
-    }
-    edge[l] = lo;
-  }
+__device__ __forceinline__ unsigned keyof(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
+__device__ __forceinline__ double kval(unsigned k) { return (double)__uint_as_float(k); }
+
+// Fixed-point square of |x| relative to its binade: with |x| = M 2^(e-150),
+// M = 2^23 | mantissa (24 bits), v = floor(M^2 / 2^32) in [2^14, 2^16) and
+// x^2 in [v, v + 1) * 2^(2e - 268).  Integer, so per-bin sums are exact and
+// independent of the summation order.
+__device__ __forceinline__ unsigned fxsq(unsigned key) {
+  const unsigned M = (key & 0x7FFFFFu) | 0x800000u;
+  return __umulhi(M, M);
 }
 
-// Streams src[0..n) with PF loads in flight per thread, double-buffered so the
-// next batch is in flight while f(i, value, valid) consumes the current one.
-// Iteration is block-uniform (f may use warp collectives); a thread visits its
-// elements in a fixed order.  CG: read through L2 only (data written earlier
-// in this kernel by other CTAs), else the read-only path.
-template <bool CG, typename F>
-__device__ __forceinline__ void stream_u32(const unsigned* __restrict__ src, int n, F&& f) {
+// Streams x[0..n) (any alignment) with 16-byte loads, U float4 per thread in
+// flight, and calls f(key) for every element.
+template <typename F>
+__device__ __forceinline__ void stream_keys(const float* __restrict__ x, int n, F&& f) {
+  constexpr int U = 4;
   const int tid = threadIdx.x;
-  unsigned cur[PF], nxt[PF];
+  int head = (int)(((16u - ((unsigned)(uintptr_t)x & 15u)) & 15u) >> 2);
+  head = min(head, n);
+  if (tid < head) f(keyof(__ldg(x + tid)));
+  const float4* v = reinterpret_cast<const float4*>(x + head);
+  const int nv = (n - head) >> 2;
+  int i = tid;
+  for (; i + (U - 1) * NT < nv; i += U * NT) {
+    float4 r[U];
 #pragma unroll
-  for (int u = 0; u < PF; ++u) {
-    const int i = u * NT + tid;
-    cur[u] = i < n ? (CG ? __ldcg(src + i) : __ldg(src + i)) : 0u;
+    for (int u = 0; u < U; ++u) r[u] = __ldg(v + i + u * NT);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      f(keyof(r[u].x));
+      f(keyof(r[u].y));
+      f(keyof(r[u].z));
+      f(keyof(r[u].w));
+    }
   }
-  for (int b0 = 0; b0 < n; b0 += NT * PF) {
-    const int b1 = b0 + NT * PF;
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int i = b1 + u * NT + tid;
-      nxt[u] = i < n ? (CG ? __ldcg(src + i) : __ldg(src + i)) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int i = b0 + u * NT + tid;
-      f(i, cur[u], i < n);
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
+  for (; i < nv; i += NT) {
+    const float4 r = __ldg(v + i);
+    f(keyof(r.x));
+    f(keyof(r.y));
+    f(keyof(r.z));
+    f(keyof(r.w));
   }
-}
-
-// Order-preserving single-stream compaction of the streamed values v with
-// pred(v): per batch of NT*PFC values, per-warp counts (ballots) are published,
-// every warp takes its exclusive offset, then writes -- no atomics, two block
-// barriers per batch, deterministic output order (batch, warp, slot, lane).
-// store(pos, v) receives the output position; acc(v) sees every valid value.
-// Returns the total (all threads).
-template <bool CG, typename P, typename S, typename A>
-__device__ __forceinline__ int compact_stream(const unsigned* __restrict__ src, int n, P&& pred, S&& store, A&& acc,
-                                              int* wcnt) {
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const unsigned lt = (1u << l) - 1u;
-  unsigned cur[PFC], nxt[PFC];
-#pragma unroll
-  for (int u = 0; u < PFC; ++u) {
-    const int i = u * NT + tid;
-    cur[u] = i < n ? (CG ? __ldcg(src + i) : __ldg(src + i)) : 0u;
-  }
-  int total = 0;
-  for (int b0 = 0; b0 < n; b0 += NT * PFC) {
-    const int b1 = b0 + NT * PFC;
-#pragma unroll
-    for (int u = 0; u < PFC; ++u) {
-      const int i = b1 + u * NT + tid;
-      nxt[u] = i < n ? (CG ? __ldcg(src + i) : __ldg(src + i)) : 0u;
-    }
-    unsigned bal[PFC];
-    int wc = 0;
-#pragma unroll
-    for (int u = 0; u < PFC; ++u) {
-      const bool valid = b0 + u * NT + tid < n;
-      bal[u] = __ballot_sync(0xffffffffu, valid && pred(cur[u]));
-      wc += __popc(bal[u]);
-      if (valid) acc(cur[u]);
-    }
-    if (l == 0) wcnt[w] = wc;
-    __syncthreads();
-    int off = total;
-#pragma unroll
-    for (int q = 0; q < NWS; ++q) {
-      const int c = wcnt[q];
-      off += q < w ? c : 0;
-      total += c;
-    }
-#pragma unroll
-    for (int u = 0; u < PFC; ++u) {
-      if ((bal[u] >> l) & 1u) store(off + __popc(bal[u] & lt), cur[u]);
-      off += __popc(bal[u]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < PFC; ++u) cur[u] = nxt[u];
-  }
-  return total;
-}
-
-// Exact binning of n values over [klo, khi]: exact counts and sums of squares
-// per bin into bcnt / bsq, edges into edge.  Each thread's private bin is one
-// 64-bit word (u32 count | fp32 partial sum of squares), so an update is one
-// LDS.64 + one STS.64; the fp32 partials (at most ept = ceil(n/NT) terms, so
-// relative error <= ept * 2^-24) are reduced in fp64 in a fixed order -- the
-// pruning bounds carry that error as slack.  KEYS: the source holds keys (a
-// survivor list, read through L2), else fp32 coefficients.
-template <bool KEYS>
-__device__ __forceinline__ void bin_pass(const void* __restrict__ src, int n, unsigned klo, unsigned khi,
-                                         unsigned long long* pb, unsigned* bcnt, double* bsq, unsigned* edge) {
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const float inv = bin_inv(klo, khi);
-  for (int b = 0; b < NBIN; ++b) pb[b * NT + tid] = 0ull;
-  stream_u32<KEYS>(static_cast<const unsigned*>(src), n, [&](int, unsigned v, bool valid) {
-    if (valid) {
-      const unsigned k = KEYS ? v : (v & 0x7FFFFFFFu);
-      const int b = bin_of(k, klo, khi, inv);
-      const unsigned long long e = pb[b * NT + tid];
-      const float a = __uint_as_float(k);
-      const float q = fmaf(a, a, __uint_as_float((unsigned)(e >> 32)));
-      pb[b * NT + tid] = ((unsigned long long)__float_as_uint(q) << 32) | (unsigned)(e + 1ull);
-    }
-  });
-  __syncthreads();
-  for (int b = w; b < NBIN; b += NWS) {      // fixed-order reduction
-    unsigned c = 0;
-    double q = 0.0;
-    for (int t = l; t < NT; t += 32) {
-      const unsigned long long e = pb[b * NT + t];
-      c += (unsigned)e;
-      q += (double)__uint_as_float((unsigned)(e >> 32));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    q = warp_sum_d(q);
-    if (l == 0) { bcnt[b] = c; bsq[b] = q; }
-  }
-  if (w == NWS - 1) bin_edges(klo, khi, edge);
-  __syncthreads();
+  const int t0 = head + (nv << 2);
+  if (t0 + tid < n) f(keyof(__ldg(x + t0 + tid)));
 }
 
 __device__ __forceinline__ bool better(double s1, long long k1, double s2, long long k2) {
   return s1 < s2 || (s1 == s2 && k1 < k2);
 }
 
+// block-wide exclusive scan of three fp64 values per thread (fixed order);
+// returns this thread's offsets in o[], block totals in tot[]
+__device__ void block_excl_scan3(const double (&v)[3], double (&o)[3], double (&tot)[3], double* sc) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  double inc[3] = {v[0], v[1], v[2]};
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double t = __shfl_up_sync(0xffffffffu, inc[q], off);
+      if (l >= off) inc[q] += t;
+    }
+  }
+  if (l == 31) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) sc[q * NWS + w] = inc[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    double base = 0.0, all = 0.0;
+    for (int u = 0; u < NWS; ++u) {
+      const double t = sc[q * NWS + u];
+      base += u < w ? t : 0.0;
+      all += t;
+    }
+    o[q] = base + inc[q] - v[q];
+    tot[q] = all;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double block_min_d(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int u = 1; u < NWS; ++u) r = fmin(r, red[u]);
+  return r;
+}
+__device__ __forceinline__ int block_min_i(int v, int* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  int r = red[0];
+  for (int u = 1; u < NWS; ++u) r = min(r, red[u]);
+  return r;
+}
+__device__ __forceinline__ unsigned block_max_u(unsigned v, unsigned* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  unsigned r = red[0];
+  for (int u = 1; u < NWS; ++u) r = max(r, red[u]);
+  return r;
+}
+
+// Per-item cluster context: `nr` CTAs (cluster ranks 0..nr-1, or this CTA
+// alone) work on one subband; xput() writes a value into slot `slot` of the
+// same __shared__ array in every participating CTA.
+struct Ctx {
+  int nr, rank, myrank;
+  __device__ void sync() const {
+    if (nr > 1) tc::cluster_sync(); else __syncthreads();
+  }
+  __device__ uint32_t at(const void* p, int r) const { return tc::mapa(tc::smem_u32(p), nr == 1 ? myrank : r); }
+  __device__ void xput_d(double* arr, int slot, double v) const {
+    for (int r = 0; r < nr; ++r) st_dsm_f64(at(arr + slot, r), v);
+  }
+  __device__ void xput_u(unsigned* arr, int slot, unsigned v) const {
+    for (int r = 0; r < nr; ++r) st_dsm_u32(at(arr + slot, r), v);
+  }
+};
+
+__device__ __forceinline__ unsigned ld_dsm_u32(uint32_t a) {
+  unsigned v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_dsm_add_u32(uint32_t a, unsigned v) {
+  unsigned r;
+  asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+  return r;
+}
+
+constexpr int BPT = HB / NT;   // bins per thread when one CTA owns the whole histogram
+
+// Exact per-subband SURE (see the file comment).  One item = (component,
+// subband); a subband with n >= BIG_MIN is split over the nr = cluster-size
+// CTAs of a cluster (slices of n/nr), smaller ones take one CTA each.
 __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ coeffs, long long cstride, SubTable tab,
                                                      int count, int keep_ll, int* kstar, float* tstar, double* e_sub,
-                                                     RankState* rs, unsigned* surv) {
+                                                     RankState* rs) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  // union: pass accumulators (NBIN x NT packed u64) | sort buffers (2 x CAPL u32)
-  unsigned long long* pb = reinterpret_cast<unsigned long long*>(smraw);
+  // union: histogram (HB counts | HB fixed-point sums) | window keys + sort buffer
+  unsigned* hcnt = reinterpret_cast<unsigned*>(smraw);
+  unsigned* hsum = hcnt + HB;
   unsigned* skeys = reinterpret_cast<unsigned*>(smraw);
-  unsigned* sbuf = skeys + CAPL;
-  __shared__ double red[NWS + 2];
-  __shared__ double scan[2 * NWS + 1];
-  __shared__ unsigned bcnt[NBIN];
-  __shared__ double bsq[NBIN];
-  __shared__ unsigned edge[NIN + 1];
-  // leader-side gather areas (written by the ranks over DSMEM)
-  __shared__ unsigned g_cnt[G][NBIN];
-  __shared__ double g_sq[G][NBIN];
-  __shared__ double g_S[G];
-  __shared__ long long g_k[G];
-  __shared__ unsigned g_key[G];
-  __shared__ double g_e[G];
-  // state broadcast by the leader
-  __shared__ unsigned s_klo, s_khi, s_m;
-  __shared__ unsigned s_go;                  // 1: run another pruning pass
-  __shared__ unsigned s_u, s_v, s_mg;        // this rank's sub-range and its key count
-  __shared__ long long s_cbw;                // count of keys below the window (cluster)
-  __shared__ unsigned s_reg;                 // this rank's slot in the survivor list
-  __shared__ unsigned s_t;                   // t* bits
-  // leader-only state
-  __shared__ double s_ub;
-  __shared__ int s_first, s_last, s_pass;
-  __shared__ int s_J;
-  __shared__ unsigned pt_u[G], pt_v[G], pt_m[G], pt_reg[G];
-  __shared__ int s_wc[NWS];
-  __shared__ double bestS[NWS];
-  __shared__ long long bestK[NWS];
-  __shared__ unsigned bestT[NWS];
+  unsigned* sbuf = skeys + CAP;
+  __shared__ double red[3 * NWS + 2];
+  __shared__ int redi[NWS];
+  __shared__ unsigned redu[NWS];
+  // exchange slots (one per participating rank)
+  __shared__ double x_seg[GMAX][3];          // segment totals: count, sum lower, sum upper
+  __shared__ double x_ub[GMAX];
+  __shared__ int x_first[GMAX], x_last[GMAX];
+  __shared__ double x_win[GMAX][4];          // window count in segment; prefix (count, pl, ph) at `first`
+  __shared__ double x_v[GMAX][5];            // pass-1 out-of-range stats: cb, qb, ca, qa, maxkey
+  __shared__ double x_fin[GMAX][5];          // compaction: sum below (x^2), above (x, x^2), counts below / above
+  __shared__ unsigned s_wpos;                // leader: next free slot of the window-key buffer
 
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int tid = threadIdx.x;
+  const int G = (int)cluster_nctarank();
   const int cid = blockIdx.x / G;
-  const int myrank = (int)tc::cluster_ctarank();
+  const int myrank = G > 1 ? (int)tc::cluster_ctarank() : 0;
   const int nbig_items = count * tab.nbig;
-  int comp, s, nr, rank;
+  int comp, s;
+  Ctx cx;
+  cx.myrank = myrank;
   if (cid < nbig_items) {
     comp = cid / tab.nbig;
     s = tab.big[cid % tab.nbig];
-    nr = G;
-    rank = myrank;
+    cx.nr = G;
+    cx.rank = myrank;
   } else {
     const int it = (cid - nbig_items) * G + myrank;
     if (it >= count * tab.nsmall) return;    // idle CTA of the last small cluster
     comp = it / tab.nsmall;
     s = tab.small[it % tab.nsmall];
-    nr = 1;
-    rank = 0;
+    cx.nr = 1;
+    cx.rank = 0;
   }
-  const int leader = nr == 1 ? myrank : 0;   // cluster rank of the leader
-  const bool is_leader = rank == 0;
-  auto rk = [&](int r) { return nr == 1 ? myrank : r; };   // item rank -> cluster rank
-  auto gsync = [&]() {
-    if (nr > 1) tc::cluster_sync(); else __syncthreads();
-  };
-  auto put_u32 = [&](unsigned& var, int r, unsigned v) { st_dsm_u32(tc::mapa(tc::smem_u32(&var), rk(r)), v); };
+  const int nr = cx.nr, rank = cx.rank;
+  const bool leader = rank == 0;
   const int n = tab.n[s];
+  const double dn = (double)n;
   const float* xs = coeffs + (long long)comp * cstride + tab.off[s];
   const int lo_i = (int)((long long)n * rank / nr), hi_i = (int)((long long)n * (rank + 1) / nr);
   const float* x = xs + lo_i;                // this rank's slice
-  const unsigned* xu = reinterpret_cast<const unsigned*>(x);
   const int ns = hi_i - lo_i;
-  unsigned* sl = surv + (long long)comp * cstride + tab.off[s];
   const int ks = comp * tab.nsub + s;
-  const double dn = (double)n;
   const bool skip = keep_ll && s == tab.nsub - 1;   // LL kept: t = 0
-#ifdef HYDE_SURE_DEBUG
-  const long long dbg_t0 = clock64();
-  long long dbg_t1 = 0, dbg_t2 = 0, dbg_t3 = 0;
-  int dbg_chunks = 0, dbg_pass = 0;
-  long long dbg_g = 0, dbg_s = 0, dbg_e = 0, dbg_p = 0, dbg_sc = 0;
-#endif
 
-  // ---------------- starting window: exact min / max key ----------------
-  {
-    unsigned kmn = 0xFFFFFFFFu, kmx = 0u;
-    stream_u32<false>(xu, ns, [&](int, unsigned v, bool valid) {
-      if (valid) { const unsigned k = v & 0x7FFFFFFFu; kmn = min(kmn, k); kmx = max(kmx, k); }
-    });
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
-      kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
-    }
-    if (l == 0) { bcnt[w] = kmn; bcnt[NWS + w] = kmx; }
-    __syncthreads();
-    if (tid == 0) {
-      unsigned a0 = 0xFFFFFFFFu, a1 = 0u;
-      for (int q = 0; q < NWS; ++q) { a0 = min(a0, bcnt[q]); a1 = max(a1, bcnt[NWS + q]); }
-      st_dsm_u32(tc::mapa(tc::smem_u32(&g_cnt[rank][0]), leader), a0);
-      st_dsm_u32(tc::mapa(tc::smem_u32(&g_cnt[rank][1]), leader), a1);
-    }
-    gsync();
-    if (is_leader && tid == 0) {
-      unsigned a0 = 0xFFFFFFFFu, a1 = 0u;
-      for (int r = 0; r < nr; ++r) { a0 = min(a0, g_cnt[r][0]); a1 = max(a1, g_cnt[r][1]); }
-      a1 = min(a1, 0x7F800000u);
-      s_m = skip ? 0u : (unsigned)n;
-      s_ub = dn;
-      s_first = -1;
-      s_pass = 0;
-      const unsigned go = (!skip && n > CAPL) ? 1u : 0u;   // clusters always prune once (partition)
-      for (int r = 0; r < nr; ++r) {
-        put_u32(s_klo, r, a0);
-        put_u32(s_khi, r, a1);
-        put_u32(s_go, r, go);
-      }
-    }
-    gsync();
-  }
-#ifdef HYDE_SURE_DEBUG
-  dbg_t1 = clock64();
-#endif
-
-  // ---------------- pruning passes ----------------
-  for (int pass = 0; pass < MAXPASS && s_go; ++pass) {
-#ifdef HYDE_SURE_DEBUG
-    ++dbg_pass;
-#endif
-    const unsigned klo = s_klo, khi = s_khi;
-    bin_pass<false>(x, ns, klo, khi, pb, bcnt, bsq, edge);
-    if (w == 0) {                            // push this rank's bins to the leader
-      st_dsm_u32(tc::mapa(tc::smem_u32(&g_cnt[rank][l]), leader), bcnt[l]);
-      st_dsm_f64(tc::mapa(tc::smem_u32(&g_sq[rank][l]), leader), bsq[l]);
-    }
-    gsync();
-    if (is_leader && w == 0) {
-      // lane b: cluster totals of bin b (fixed rank order), then exclusive
-      // prefix counts / sums over the bins, one inner bin per lane
-      unsigned cb = 0;
-      double qb = 0.0;
-      for (int r = 0; r < nr; ++r) { cb += g_cnt[r][l]; qb += g_sq[r][l]; }
-      bcnt[l] = cb;                          // the leader's bcnt / bsq now hold totals
-      bsq[l] = qb;
-      long long cincl = cb;
-      double qincl = qb;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long tc_ = __shfl_up_sync(0xffffffffu, cincl, o);
-        const double tq = __shfl_up_sync(0xffffffffu, qincl, o);
-        if (l >= o) { cincl += tc_; qincl += tq; }
-      }
-      const double tot_q = __shfl_sync(0xffffffffu, qincl, 31);
-      const long long c = cincl - cb;        // keys below bin l
-      const double q = qincl - qb;
-      const bool inner = l >= 1 && l <= NIN && cb > 0u;
-      double lbv = INFINITY, ubv = INFINITY;
-      if (inner) {
-        const double m = (double)cb;
-        const double lo = kval(edge[l - 1]), hi = kval(edge[l] - 1u);
-        lbv = dn - 2.0 * ((double)c + m) + q + (dn - (double)c) * lo * lo;
-        ubv = dn - 2.0 * ((double)c + m) + q + qb + (dn - (double)c - m) * hi * hi;
-      }
-      double ub = ubv;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ub = fmin(ub, __shfl_xor_sync(0xffffffffu, ub, o));
-      ub = fmin(ub, s_ub);
-      const double ept = (double)((n / nr + NT) / NT);   // fp32 terms per thread partial
-      const double tol = 1e-9 * dn + 1e-12 * (dn + tot_q) + 4.0 * ept * 5.9604644775390625e-8 * tot_q;
-      const unsigned surv_mask = __ballot_sync(0xffffffffu, inner && lbv <= ub + tol);
-      unsigned go = 0, nlo = 1u, nhi = 0u, msum = 0;
-      int first = -1, last = -1;
-      if (surv_mask) {
-        first = __ffs(surv_mask) - 2;        // inner bin index = lane - 1
-        last = 30 - __clz(surv_mask);
-        unsigned part = (l >= first + 1 && l <= last + 1) ? cb : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        msum = part;
-        nlo = edge[first];
-        nhi = edge[last + 1] - 1u;
-        const bool progress = !(nlo == klo && nhi == khi);
-        // keep pruning while it makes progress and the survivors exceed a
-        // small exact-evaluation set: a streaming pass over the slice is far
-        // cheaper than sorting tens of thousands of survivors
-        go = (progress && msum > (unsigned)SURV_GOAL) ? 1u : 0u;
-      }
-      if (l == 0) {
-        s_ub = ub;
-        s_pass = 1;
-        s_first = first;
-        s_last = last;
-        s_m = msum;                          // 0: only t = 0 (k = 0) can win
-      }
-      if (l < nr) {
-        put_u32(s_klo, l, nlo);
-        put_u32(s_khi, l, nhi);
-        put_u32(s_go, l, go);
-      }
-    }
-    gsync();
-  }
-#ifdef HYDE_SURE_DEBUG
-  dbg_t2 = clock64();
-#endif
-
-  // ---------------- partition the window into one sub-range per rank ----------------
-  // (leader) the last pass's bin counts split the window at bin edges into nr
-  // owners of ~M/nr keys and give each rank its slot in the survivor list and
-  // the exact count below the window; without a pass (single CTA) the window is
-  // the whole subband.
-  if (is_leader && w == 0) {
-    const unsigned klo = s_klo, khi = s_khi;
-    const unsigned M = s_m;
-    long long cbw = 0;
-    if (l == 0) {                            // greedy split (serial, on local smem)
-      for (int g = 0; g < nr; ++g) { pt_u[g] = 1u; pt_v[g] = 0u; pt_m[g] = 0u; pt_reg[g] = 0u; }
-      if (M == 0u || klo > khi) {
-      } else if (!s_pass) {                  // single CTA, whole subband
-        pt_u[0] = klo;
-        pt_v[0] = khi;
-        pt_m[0] = (unsigned)n;
+  // ---------------- window search ----------------
+  // window [klo, khi] of keys that can hold the argmin; (cb, pl, ph): exact
+  // count and bounds of sum x^2 of the keys below it.
+  unsigned klo = 0u, khi = 0x7FFFFFFFu;
+  double cb = 0.0, pl = 0.0, ph = 0.0, M = dn;
+  bool empty = false;                        // only k = 0 can win
+  if (skip) {
+    empty = true;
+  } else if (n > CAP) {
+    const int seg = HB / nr;                 // bins owned by this rank in the bound computation
+    const int bpt = seg / NT;                // ... per thread (1..16)
+    for (int pass = 0; pass < MAXPASS; ++pass) {
+      const bool p1 = pass == 0;
+      // binned key range [bl, bh] with bins of 2^sh keys from kb
+      int sh;
+      unsigned kb, bl, bh;
+      if (p1) {
+        sh = HS0; kb = KB0; bl = KB0; bh = KE0;
       } else {
-        const int first = s_first, last = s_last;
-        unsigned woff = 0;
-        for (int r = 0; r < nr; ++r) {       // each rank's slot in the survivor list
-          pt_reg[r] = woff;
-          for (int jj = first; jj <= last; ++jj) woff += g_cnt[r][1 + jj];
+        sh = 0;
+        while ((((khi - (klo & ~((1u << sh) - 1u))) >> sh) + 1u) > (unsigned)HB) ++sh;
+        kb = klo & ~((1u << sh) - 1u);
+        bl = klo;
+        bh = khi;
+      }
+      for (int b = tid; b < 2 * HB; b += NT) hcnt[b] = 0u;
+      __syncthreads();
+      double cbv = 0.0, qbv = 0.0, cav = 0.0, qav = 0.0;
+      unsigned kmax = 0u;
+      stream_keys(x, ns, [&](unsigned k) {
+        if (k >= bl && k <= bh) {
+          const unsigned b = (k - kb) >> sh;
+          atomicAdd(hcnt + b, 1u);
+          atomicAdd(hsum + b, fxsq(k));
+        } else if (p1) {                     // pass 1: keys outside [2^-40, 2^24), exact fp64
+          const double a = kval(k);
+          if (k < bl) { cbv += 1.0; qbv = fma(a, a, qbv); }
+          else { cav += 1.0; qav = fma(a, a, qav); kmax = max(kmax, k); }
         }
-        cbw = bcnt[0];
-        for (int j = 0; j < first; ++j) cbw += bcnt[1 + j];
-        const long long target = ((long long)M + nr - 1) / nr;
-        int j = first;
-        for (int g = 0; g < nr; ++g) {       // bins first..last -> nr owners of ~M/nr keys
-          const int j0 = j;
-          long long mg = 0;
-          while (j <= last && (mg < target || g == nr - 1)) { mg += bcnt[1 + j]; ++j; }
-          if (j > j0) { pt_u[g] = edge[j0]; pt_v[g] = edge[j] - 1u; }
-          pt_m[g] = (unsigned)mg;
+      });
+      if (p1) {
+        cbv = block_sum_d(cbv, red);
+        qbv = block_sum_d(qbv, red);
+        cav = block_sum_d(cav, red);
+        qav = block_sum_d(qav, red);
+        kmax = block_max_u(kmax, redu);
+        if (tid == 0) {
+          cx.xput_d(&x_v[0][0], rank * 5 + 0, cbv);
+          cx.xput_d(&x_v[0][0], rank * 5 + 1, qbv);
+          cx.xput_d(&x_v[0][0], rank * 5 + 2, cav);
+          cx.xput_d(&x_v[0][0], rank * 5 + 3, qav);
+          cx.xput_d(&x_v[0][0], rank * 5 + 4, (double)kmax);
         }
       }
+      cx.sync();                             // histograms complete everywhere
+      // merge: this rank's segment of bins, summed over ranks in rank order
+      unsigned mc[BPT];
+      unsigned long long msum[BPT];
+      unsigned ovf = 0u;                     // bit i: a rank's fixed-point sum of bin i may have wrapped
+      const int b0 = rank * seg + tid * bpt;
+#pragma unroll
+      for (int i = 0; i < BPT; ++i) {
+        mc[i] = 0u;
+        msum[i] = 0ull;
+        if (i < bpt) {
+          for (int r = 0; r < nr; ++r) {
+            unsigned c, q;
+            if (nr == 1) { c = hcnt[b0 + i]; q = hsum[b0 + i]; }
+            else { c = ld_dsm_u32(cx.at(hcnt + b0 + i, r)); q = ld_dsm_u32(cx.at(hsum + b0 + i, r)); }
+            mc[i] += c;
+            msum[i] += q;
+            if (c >= 65536u) ovf |= 1u << i;
+          }
+        }
+      }
+      // out-of-range (pass 1) stats, identical on every rank
+      double vcb = 0.0, vqb = 0.0, vca = 0.0, vqa = 0.0, vmax = 0.0;
+      if (p1) {
+        for (int r = 0; r < nr; ++r) {
+          vcb += x_v[r][0]; vqb += x_v[r][1]; vca += x_v[r][2]; vqa += x_v[r][3];
+          vmax = fmax(vmax, x_v[r][4]);
+        }
+      }
+      // base prefix: keys below the binned range
+      const double c0 = p1 ? vcb : cb, p0l = p1 ? vqb : pl, p0h = p1 ? vqb : ph;
+      // per-bin value bounds and sum bounds (recomputed where needed: registers)
+      auto binfo = [&](int i, double& lo2, double& hi2, double& q_l, double& q_h) {
+        const unsigned kb0 = kb + ((unsigned)(b0 + i) << sh);
+        const unsigned kb1 = kb0 + ((1u << sh) - 1u);
+        const unsigned lok = max(kb0, bl), hik = min(kb1, bh);
+        const double lo = kval(lok), hi = kval(hik);
+        lo2 = lo * lo;
+        hi2 = hi * hi;
+        const unsigned e = lok >> 23;
+        const double m = (double)mc[i];
+        if ((hik >> 23) == e && e > 0u && !((ovf >> i) & 1u)) {
+          const double sc = ldexp(1.0, 2 * (int)e - 268);
+          q_l = (double)msum[i] * sc;
+          q_h = ((double)msum[i] + m) * sc;
+        } else {
+          q_l = m * lo2;
+          q_h = m * hi2;
+        }
+      };
+      double tv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < BPT; ++i) {
+        if (i < bpt && mc[i] > 0u) {
+          double lo2, hi2, q_l, q_h;
+          binfo(i, lo2, hi2, q_l, q_h);
+          tv[0] += (double)mc[i]; tv[1] += q_l; tv[2] += q_h;
+        }
+      }
+      double off[3], segtot[3];
+      block_excl_scan3(tv, off, segtot, red);
+      if (tid == 0) {
+        cx.xput_d(&x_seg[0][0], rank * 3 + 0, segtot[0]);
+        cx.xput_d(&x_seg[0][0], rank * 3 + 1, segtot[1]);
+        cx.xput_d(&x_seg[0][0], rank * 3 + 2, segtot[2]);
+      }
+      cx.sync();
+      double sc0 = c0, sl0 = p0l, sh0 = p0h, allc = c0, allh = p0h, alll = p0l;
+      for (int r = 0; r < nr; ++r) {
+        if (r < rank) { sc0 += x_seg[r][0]; sl0 += x_seg[r][1]; sh0 += x_seg[r][2]; }
+        allc += x_seg[r][0]; alll += x_seg[r][1]; allh += x_seg[r][2];
+      }
+      // bounds.  Bin j, c keys below it, m in it, values in [lo, hi]:
+      //   S_k >= LB = n - 2(c+m) + P_lo(c) + (n-c) lo^2 for every k in the bin,
+      //   min S <= UB = n - 2(c+m) + P_hi(c) + Q_hi + (n-c-m) hi^2  (S at k = c+m).
+      const double tol = 1e-9 * dn + 1e-12 * (dn + allh);
+      double lbs[BPT];
+      double ubt = INFINITY;
+      {
+        double c = sc0 + off[0], p_l = sl0 + off[1], p_h = sh0 + off[2];
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+          lbs[i] = INFINITY;
+          if (i < bpt && mc[i] > 0u) {
+            double lo2, hi2, q_l, q_h;
+            binfo(i, lo2, hi2, q_l, q_h);
+            const double m = (double)mc[i];
+            lbs[i] = dn - 2.0 * (c + m) + p_l + (dn - c) * lo2;
+            const double ub = dn - 2.0 * (c + m) + p_h + q_h + (dn - c - m) * hi2;
+            ubt = fmin(ubt, ub);
+            c += m; p_l += q_l; p_h += q_h;
+          }
+        }
+      }
+      // virtual bins of pass 1: below 2^-40 (index -1) and from 2^24 (index HB)
+      double lb_lo = INFINITY, lb_hi = INFINITY;
+      if (p1) {
+        const double hi_lo = kval(KB0 - 1u);
+        if (vcb > 0.0) {
+          lb_lo = dn - 2.0 * vcb;
+          ubt = fmin(ubt, dn - 2.0 * vcb + vqb + (dn - vcb) * hi_lo * hi_lo);
+        }
+        if (vca > 0.0) {
+          const double lo = kval(KE0 + 1u), hi = kval((unsigned)vmax);
+          lb_hi = dn - 2.0 * dn + alll + vca * lo * lo;
+          ubt = fmin(ubt, -dn + allh + vqa);
+          (void)hi;
+        }
+      }
+      ubt = block_min_d(ubt, red);
+      if (tid == 0) cx.xput_d(x_ub, rank, ubt);
+      cx.sync();
+      double ub = dn;                        // k = 0: S_0 = n
+      for (int r = 0; r < nr; ++r) ub = fmin(ub, x_ub[r]);
+      const double thr = ub + tol;
+      int fst = INT_MAX, lst = -2;
+#pragma unroll
+      for (int i = 0; i < BPT; ++i)
+        if (i < bpt && lbs[i] <= thr) { fst = min(fst, b0 + i); lst = max(lst, b0 + i); }
+      fst = block_min_i(fst, redi);
+      lst = -block_min_i(-lst, redi);
+      if (tid == 0) { cx.xput_u((unsigned*)x_first, rank, (unsigned)fst); cx.xput_u((unsigned*)x_last, rank, (unsigned)lst); }
+      cx.sync();
+      int gf = INT_MAX, gl = -2;
+      for (int r = 0; r < nr; ++r) { gf = min(gf, x_first[r]); gl = max(gl, x_last[r]); }
+      if (p1 && lb_lo <= thr) gf = -1;
+      if (p1 && lb_hi <= thr) { gl = HB; if (gf == INT_MAX) gf = HB; }
+      if (p1 && gf == -1 && gl == -2) gl = -1;
+      // window count in this segment and, for the owner of `gf`, the prefix there
+      double mwin = 0.0;
+      {
+        double c = sc0 + off[0], p_l = sl0 + off[1], p_h = sh0 + off[2];
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+          if (i < bpt) {
+            const int b = b0 + i;
+            if (b == gf) {
+              x_win[rank][1] = c; x_win[rank][2] = p_l; x_win[rank][3] = p_h;   // local slot, pushed below
+            }
+            if (b >= gf && b <= gl) mwin += (double)mc[i];
+            if (mc[i] > 0u) {
+              double lo2, hi2, q_l, q_h;
+              binfo(i, lo2, hi2, q_l, q_h);
+              c += (double)mc[i]; p_l += q_l; p_h += q_h;
+            }
+          }
+        }
+      }
+      mwin = block_sum_d(mwin, red);         // contains barriers: x_win[rank][1..3] visible
+      const bool own_first = gf >= rank * seg && gf < (rank + 1) * seg;
+      if (tid == 0) {
+        cx.xput_d(&x_win[0][0], rank * 4 + 0, mwin);
+        if (own_first) {
+          const double a1 = x_win[rank][1], a2 = x_win[rank][2], a3 = x_win[rank][3];
+          cx.xput_d(&x_win[0][0], rank * 4 + 1, a1);
+          cx.xput_d(&x_win[0][0], rank * 4 + 2, a2);
+          cx.xput_d(&x_win[0][0], rank * 4 + 3, a3);
+        }
+      }
+      cx.sync();
+      double Mw = 0.0;
+      for (int r = 0; r < nr; ++r) Mw += x_win[r][0];
+      const unsigned oklo = klo, okhi = khi;
+      if (gf == INT_MAX) {                   // nothing survives: t = 0
+        empty = true;
+        break;
+      }
+      // window keys and the prefix at its start
+      if (gf == -1) { klo = 0u; cb = 0.0; pl = ph = 0.0; Mw += vcb; }
+      else if (gf == HB) { klo = KE0 + 1u; cb = allc; pl = alll; ph = allh; }
+      else {
+        const int ow = gf / seg;
+        klo = max(kb + ((unsigned)gf << sh), bl);
+        cb = x_win[ow][1]; pl = x_win[ow][2]; ph = x_win[ow][3];
+      }
+      if (gl == HB) { khi = (unsigned)vmax; Mw += vca; }
+      else if (gl == -1) { khi = KB0 - 1u; }
+      else khi = min(kb + ((unsigned)(gl + 1) << sh) - 1u, bh);
+      M = Mw;
+      if (M <= (double)CAP || klo == khi) break;
+      if (!p1 && klo == oklo && khi == okhi) {   // no progress: cannot narrow to CAP keys
+        if (tid == 0 && leader) atomicOr(&rs->sure_overflow, 1);
+        break;
+      }
+      cx.sync();                             // everyone done with x_* and the histograms
     }
-    cbw = __shfl_sync(0xffffffffu, cbw, 0);
-    __syncwarp();
-    if (l < nr) {                            // lane g -> rank g
-      put_u32(s_m, l, M);
-      put_u32(s_u, l, pt_u[l]);
-      put_u32(s_v, l, pt_v[l]);
-      put_u32(s_mg, l, pt_m[l]);
-      put_u32(s_reg, l, pt_reg[l]);
-      st_dsm_s64(tc::mapa(tc::smem_u32(&s_cbw), rk(l)), cbw);
-    }
+  } else {
+    M = dn;                                  // short subband: the whole of it is the window
   }
-  gsync();
+  const bool closed = !empty && klo == khi && M > (double)CAP;   // one repeated key: closed form
+  const bool overflow = !empty && !closed && M > (double)CAP;
+  if (overflow) empty = true;                // flagged above; keep going to write something
+  if (empty) { klo = 0xFFFFFFFFu; khi = 0u; }  // every key is "below"
 
-#ifdef HYDE_SURE_DEBUG
-  dbg_p = clock64() - dbg_t2;
-#endif
-  // ---------------- survivors -> this rank's slot of the scratch list (clusters) ----------------
-  // The same stream sums x^2 below the window exactly (fp64, fixed order).
-  const unsigned klo = s_klo, khi = s_khi;
-  const unsigned M = s_m;
-  const bool clustered = nr > 1 && M > 0u && klo <= khi;
-  if (clustered) {
-    const unsigned woff = s_reg;
-    double qb = 0.0;
-    compact_stream<false>(
-        xu, ns, [&](unsigned v) { const unsigned k = v & 0x7FFFFFFFu; return k >= klo && k <= khi; },
-        [&](int pos, unsigned v) { sl[woff + pos] = v & 0x7FFFFFFFu; },
-        [&](unsigned v) {
-          const unsigned k = v & 0x7FFFFFFFu;
-          if (k < klo) { const double a = kval(k); qb = fma(a, a, qb); }
-        },
-        s_wc);
-    qb = block_sum_d(qb, red);
-    if (tid == 0) st_dsm_f64(tc::mapa(tc::smem_u32(&g_e[rank]), leader), qb);
+  // ---------------- compaction: window keys -> the leader's buffer ----------------
+  if (leader && tid == 0) s_wpos = 0u;
+  cx.sync();
+  double qb = 0.0, q1 = 0.0, q2 = 0.0, cbl = 0.0, cab = 0.0;
+  {
+    const bool wr = !closed;
+    const uint32_t wpos = cx.at(&s_wpos, 0);
+    const uint32_t kbase = cx.at(skeys, 0);
+    stream_keys(x, ns, [&](unsigned k) {
+      const double a = kval(k);
+      if (k < klo) { qb = fma(a, a, qb); cbl += 1.0; }
+      else if (k > khi) { q1 += a; q2 = fma(a, a, q2); cab += 1.0; }
+      else if (wr) {
+        unsigned p;
+        if (nr == 1) p = atomicAdd(&s_wpos, 1u);
+        else p = atom_dsm_add_u32(wpos, 1u);
+        if (p < (unsigned)CAP) {
+          if (nr == 1) skeys[sw((int)p)] = k; else st_dsm_u32(kbase + 4u * (unsigned)sw((int)p), k);
+        }
+      }
+    });
   }
-  gsync();
-  double qbw = 0.0;                          // exact sum of x^2 below the window (cluster)
-  long long cbw = 0;
-  if (clustered) {
-    double t = 0.0;
-    if (l < nr) t = ld_dsm_f64(tc::mapa(tc::smem_u32(&g_e[l]), leader));
-    qbw = warp_sum_d(t);
-    cbw = s_cbw;
+  qb = block_sum_d(qb, red);
+  q1 = block_sum_d(q1, red);
+  q2 = block_sum_d(q2, red);
+  cbl = block_sum_d(cbl, red);
+  cab = block_sum_d(cab, red);
+  if (tid == 0) {
+    const uint32_t a = cx.at(&x_fin[rank][0], 0);
+    st_dsm_f64(a, qb);
+    st_dsm_f64(a + 8, q1);
+    st_dsm_f64(a + 16, q2);
+    st_dsm_f64(a + 24, cbl);
+    st_dsm_f64(a + 32, cab);
   }
+  cx.sync();
+  if (!leader) return;
 
-#ifdef HYDE_SURE_DEBUG
-  dbg_sc = clock64() - dbg_t2 - dbg_p;
-#endif
-  // ---------------- exact evaluation of this rank's sub-range ----------------
-  // Chunk [u, v] of <= CAPL keys: one compaction stream over the source gathers
-  // its keys and sums (count, x^2) of the source keys below u, so the prefix at
-  // u is exact: (cbw, qbw) + those.
-  double sbest = dn;          // k = 0 (t = 0): S_0 = n
+  // ---------------- exact evaluation on the leader ----------------
+  double P0 = 0.0, Q1 = 0.0, Q2 = 0.0, CB = 0.0, cabove = 0.0;
+  for (int r = 0; r < nr; ++r) {
+    P0 += x_fin[r][0]; Q1 += x_fin[r][1]; Q2 += x_fin[r][2]; CB += x_fin[r][3]; cabove += x_fin[r][4];
+  }
+  if (!closed && !empty && s_wpos > (unsigned)CAP && tid == 0) atomicOr(&rs->sure_overflow, 1);
+  double sbest = dn;                         // k = 0
   long long kbest = 0;
   unsigned tkey = 0u;
-  {
-    const unsigned v_g = s_v;
-    unsigned u = s_u;
-    unsigned m_rem = s_mg;
-    unsigned whi = v_g;
-    // source of this sub-range's keys: the survivor list (cluster) or the
-    // subband itself (single CTA)
-    const bool from_list = nr > 1;
-    const unsigned* srcp = from_list ? sl : reinterpret_cast<const unsigned*>(xs);
-    const int nsrc = from_list ? (int)M : n;
-    for (int it = 0; it < 4096 && u <= v_g && m_rem > 0u; ++it) {
-      unsigned v;
-      bool run = false;
-      if (m_rem <= (unsigned)CAPL && whi == v_g) {
-        v = v_g;
-      } else {
-        if (from_list) bin_pass<true>(srcp, nsrc, u, whi, pb, bcnt, bsq, edge);
-        else bin_pass<false>(srcp, nsrc, u, whi, pb, bcnt, bsq, edge);
-        if (tid == 0) {
-          long long acc = 0;
-          int J = 0;
-          while (J < NIN && acc + (long long)bcnt[1 + J] <= (long long)CAPL) { acc += bcnt[1 + J]; ++J; }
-          s_J = J;
-        }
-        __syncthreads();
-        const int J = s_J;
-        const unsigned e1 = edge[1], eJ = edge[J < NIN ? J : NIN];
-        __syncthreads();
-        if (J == NIN) {
-          v = whi;
-        } else if (J > 0) {
-          v = eJ - 1u;
-        } else if (e1 - 1u == u) {
-          v = u;
-          run = true;
-        } else {              // first bin alone exceeds CAPL: narrow and re-bin
-          whi = e1 - 1u;
-          continue;
-        }
-      }
-#ifdef HYDE_SURE_DEBUG
-      ++dbg_chunks;
-      long long dq0 = clock64();
-#endif
-      double sql = 0.0, cl = 0.0;
-      auto inr = [&](unsigned val) { const unsigned k = from_list ? val : (val & 0x7FFFFFFFu); return k >= u && k <= v; };
-      auto put = [&](int pos, unsigned val) { if (pos < CAPL) skeys[sw(pos)] = from_list ? val : (val & 0x7FFFFFFFu); };
-      auto below = [&](unsigned val) {
-        const unsigned k = from_list ? val : (val & 0x7FFFFFFFu);
-        if (k < u) { const double a = kval(k); sql = fma(a, a, sql); cl += 1.0; }
-      };
-      const int mc = from_list ? compact_stream<true>(srcp, nsrc, inr, put, below, s_wc)
-                               : compact_stream<false>(srcp, nsrc, inr, put, below, s_wc);
-      const long long c_run = cbw + (long long)block_sum_d(cl, red);
-      const double q_run = qbw + block_sum_d(sql, red);
-#ifdef HYDE_SURE_DEBUG
-      dbg_g += clock64() - dq0;
-#endif
-      if (run) {              // one repeated key: best at the run end
-        const double a = kval(u);
-        const long long k = c_run + mc;
-        const double S = dn - 2.0 * (double)k + q_run + (double)mc * a * a + (dn - (double)k) * a * a;
-        if (tid == 0 && better(S, k, sbest, kbest)) { sbest = S; kbest = k; tkey = u; }
-        m_rem -= (unsigned)mc;
-      } else if (mc > CAPL) {
-        if (tid == 0) atomicOr(&rs->sure_overflow, 1);   // unreachable by construction
-        break;
-      } else if (mc > 0) {
-        int P2 = 32;
-        while (P2 < mc) P2 <<= 1;
-        for (int i = mc + tid; i < P2; i += NT) skeys[sw(i)] = 0xFFFFFFFFu;
-        __syncthreads();
-#ifdef HYDE_SURE_DEBUG
-        long long dq1 = clock64();
-#endif
-        const unsigned* sk = P2 <= NT * 16 ? block_sort<16>(skeys, sbuf, P2) : block_sort<32>(skeys, sbuf, P2);
-#ifdef HYDE_SURE_DEBUG
-        dbg_s += clock64() - dq1;
-        dq1 = clock64();
-#endif
-        const int seg = (mc + NT - 1) / NT;
-        const int b0 = min(mc, tid * seg), b1 = min(mc, b0 + seg);
-        double tsum = 0.0;
-        for (int i = b0; i < b1; ++i) { const double aa = kval(sk[sw(i)]); tsum = fma(aa, aa, tsum); }
-        double tot;
-        double Q = q_run + block_excl_scan(tsum, scan, &tot);
-        for (int i = b0; i < b1; ++i) {
-          const unsigned kk = sk[sw(i)];
-          const double aa = kval(kk);
-          Q = fma(aa, aa, Q);
-          const long long k = c_run + i + 1;
-          const double S = dn - 2.0 * (double)k + Q + (dn - (double)k) * aa * aa;
-          if (better(S, k, sbest, kbest)) { sbest = S; kbest = k; tkey = kk; }
-        }
-#ifdef HYDE_SURE_DEBUG
-        __syncthreads();
-        dbg_e += clock64() - dq1;
-#endif
-        m_rem -= (unsigned)mc;
-      }
-      __syncthreads();
-      if (v >= v_g) break;
-      u = v + 1u;
-      whi = v_g;
+  const int mc = closed || empty ? 0 : min((int)s_wpos, CAP);
+  const unsigned* sk = skeys;
+  if (closed) {
+    const double a = kval(klo);
+    const long long k = (long long)CB + (long long)M;
+    const double S = dn - 2.0 * (double)k + P0 + M * a * a + (dn - (double)k) * a * a;
+    if (better(S, k, sbest, kbest)) { sbest = S; kbest = k; tkey = klo; }
+  } else if (mc > 0) {
+    int P2 = 32;
+    while (P2 < mc) P2 <<= 1;
+    for (int i = mc + tid; i < P2; i += NT) skeys[sw(i)] = 0xFFFFFFFFu;
+    __syncthreads();
+    sk = P2 <= NT * 16 ? block_sort<16>(skeys, sbuf, P2) : block_sort<32>(skeys, sbuf, P2);
+    const int seg = (mc + NT - 1) / NT;
+    const int e0 = min(mc, tid * seg), e1 = min(mc, e0 + seg);
+    double tsum = 0.0;
+    for (int i = e0; i < e1; ++i) { const double aa = kval(sk[sw(i)]); tsum = fma(aa, aa, tsum); }
+    double tot;
+    double Q = P0 + block_excl_scan(tsum, red, &tot);
+    for (int i = e0; i < e1; ++i) {
+      const unsigned kk = sk[sw(i)];
+      const double aa = kval(kk);
+      Q = fma(aa, aa, Q);
+      const long long k = (long long)CB + i + 1;
+      const double S = dn - 2.0 * (double)k + Q + (dn - (double)k) * aa * aa;
+      if (better(S, k, sbest, kbest)) { sbest = S; kbest = k; tkey = kk; }
     }
   }
-#ifdef HYDE_SURE_DEBUG
-  dbg_t3 = clock64();
-#endif
-  // block argmin (min S, then min k) -> leader
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double os = __shfl_xor_sync(0xffffffffu, sbest, o);
@@ -771,54 +747,41 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
     const unsigned ot = __shfl_xor_sync(0xffffffffu, tkey, o);
     if (better(os, ok, sbest, kbest)) { sbest = os; kbest = ok; tkey = ot; }
   }
-  if (l == 0) { bestS[w] = sbest; bestK[w] = kbest; bestT[w] = tkey; }
-  __syncthreads();
-  if (tid == 0) {
-    double sv = bestS[0];
-    long long kv = bestK[0];
-    unsigned tv = bestT[0];
-    for (int q = 1; q < NWS; ++q)
-      if (better(bestS[q], bestK[q], sv, kv)) { sv = bestS[q]; kv = bestK[q]; tv = bestT[q]; }
-    st_dsm_f64(tc::mapa(tc::smem_u32(&g_S[rank]), leader), sv);
-    st_dsm_s64(tc::mapa(tc::smem_u32(&g_k[rank]), leader), kv);
-    st_dsm_u32(tc::mapa(tc::smem_u32(&g_key[rank]), leader), tv);
-  }
-  gsync();
-  if (is_leader && tid == 0) {
-    double sv = g_S[0];
-    long long kv = g_k[0];
-    unsigned tv = g_key[0];
-    for (int r = 1; r < nr; ++r)
-      if (better(g_S[r], g_k[r], sv, kv)) { sv = g_S[r]; kv = g_k[r]; tv = g_key[r]; }
-    g_k[0] = kv;
-    for (int r = 0; r < nr; ++r) put_u32(s_t, r, kv > 0 ? tv : 0u);
-  }
-  gsync();
-  // ---------------- E_post = sum (|x| - t)_+^2 over this slice -> leader ----------------
-  double e_in = 0.0;
   {
-    const double td = kval(s_t);
-    stream_u32<false>(xu, ns, [&](int, unsigned v, bool valid) {
-      const double aa = kval(v & 0x7FFFFFFFu) - td;
-      if (valid && aa > 0.0) e_in = fma(aa, aa, e_in);
-    });
+    __shared__ double bS[NWS];
+    __shared__ long long bK[NWS];
+    __shared__ unsigned bT[NWS];
+    const int w = tid >> 5, l = tid & 31;
+    if (l == 0) { bS[w] = sbest; bK[w] = kbest; bT[w] = tkey; }
+    __syncthreads();
+    sbest = bS[0]; kbest = bK[0]; tkey = bT[0];
+    for (int q = 1; q < NWS; ++q)
+      if (better(bS[q], bK[q], sbest, kbest)) { sbest = bS[q]; kbest = bK[q]; tkey = bT[q]; }
   }
-  const double e = block_sum_d(e_in, red);
-  if (tid == 0) st_dsm_f64(tc::mapa(tc::smem_u32(&g_e[rank]), leader), e);
-  gsync();
-  if (is_leader && tid == 0) {
-    double et = 0.0;
-    for (int r = 0; r < nr; ++r) et += g_e[r];
-    kstar[ks] = (int)g_k[0];
-    tstar[ks] = __uint_as_float(s_t);
-    e_sub[ks] = et;
-#ifdef HYDE_SURE_DEBUG
-    if (n > 40000)
-      printf("SUREDBG comp %d sub %d n %d minmax %lld prune %lld (passes %d) eval %lld (chunks %d, M %u: part %lld "
-             "scatter %lld gather %lld sort %lld S %lld) epost %lld total %lld\n",
-             comp, s, n, dbg_t1 - dbg_t0, dbg_t2 - dbg_t1, dbg_pass, dbg_t3 - dbg_t2, dbg_chunks, M, dbg_p, dbg_sc,
-             dbg_g, dbg_s, dbg_e, clock64() - dbg_t3, clock64() - dbg_t0);
-#endif
+  if (kbest == 0) tkey = 0u;
+  const double t = kval(tkey);
+  // E_post = sum over the subband of (|x| - t)_+^2: window keys + keys above
+  // the window (from their sums; every one of them exceeds t) + the keys below
+  // it when t = 0
+  double ew = 0.0;
+  if (closed) {
+    const double d = kval(klo) - t;
+    ew = d > 0.0 ? M * d * d : 0.0;
+  } else if (mc > 0) {
+    const int seg = (mc + NT - 1) / NT;
+    const int e0 = min(mc, tid * seg), e1 = min(mc, e0 + seg);
+    for (int i = e0; i < e1; ++i) {
+      const double d = kval(sk[sw(i)]) - t;
+      if (d > 0.0) ew = fma(d, d, ew);
+    }
+  }
+  ew = block_sum_d(ew, red);
+  if (tid == 0) {
+    double e = ew + (Q2 - 2.0 * t * Q1 + cabove * t * t);
+    if (kbest == 0) e += P0;
+    kstar[ks] = (int)kbest;
+    tstar[ks] = __uint_as_float(tkey);
+    e_sub[ks] = e;
   }
 }
 
@@ -885,9 +848,16 @@ SubTable make_table(const DwtPlan& plan) {
 
 cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, int count, int keep_ll, int* kstar,
                         float* tstar, double* e_sub, RankState* rs, unsigned* surv, cudaStream_t st) {
+  (void)surv;
   const SubTable tab = make_table(plan);
   cudaError_t e = cudaFuncSetAttribute(sure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_DYN);
   if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // CTAs per big subband: as many as keep about two waves of CTAs busy
+  int G = GMAX;
+  while (G > 1 && (long long)count * tab.nbig * G > 2LL * sms) G >>= 1;
   const int nclusters = count * tab.nbig + (count * tab.nsmall + G - 1) / G;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nclusters * G);
@@ -902,7 +872,7 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, sure_kernel, (const float*)coeffs, cstride, tab, count, keep_ll, kstar, tstar, e_sub,
-                            rs, surv);
+                            rs);
 }
 
 cudaError_t launch_soft_threshold(float* coeffs, long long cstride, const DwtPlan& plan, int count, const float* tstar,

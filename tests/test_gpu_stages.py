@@ -211,6 +211,33 @@ def test_sure_indices_bit_exact(hy, shape):
         assert abs(ep[i] - e_ref) <= 1e-6 * max(1.0, e_ref)
 
 
+def test_sure_many_subbands_single_cta_path(hy):
+    """Enough big subbands in one launch that each takes ONE CTA (no cluster split):
+    same exact indices as the oracle."""
+    r, c, lv = 1024, 1024, 5
+    nc = O.coeff_count(r, c, lv)
+    rng = np.random.default_rng(7)
+    rows = []
+    for i in range(20):
+        a = rng.standard_normal(nc) * (1.0 + 0.1 * i)
+        a[rng.random(nc) < 0.02 * (i % 5)] *= 15
+        rows.append(a)
+    co = np.stack(rows).astype(np.float32)
+    g = dev(co)
+    ks, ts, ep = hy.stages.sure(g, r, c, lv)
+    ks, ts, ep = ks.cpu().numpy(), ts.cpu().numpy(), ep.cpu().numpy()
+    for i in range(co.shape[0]):
+        res, offs = _oracle_sure_on(co[i], r, c, lv)
+        e_ref = 0.0
+        for j, sr in enumerate(res):
+            x = co[i, offs[j]:offs[j + 1]].astype(np.float64)
+            scale = x.size + float(np.sum(x ** 2))
+            if sr.margin > 1e-9 * scale:
+                assert ks[i, j] == sr.k and ts[i, j] == np.float32(sr.t), (i, j, ks[i, j], sr.k)
+            e_ref += float(np.sum(O.soft_threshold(x, float(ts[i, j])) ** 2))
+        assert abs(ep[i] - e_ref) <= 1e-6 * max(1.0, e_ref)
+
+
 def test_sure_edge_cases(hy):
     r, c, lv = 64, 64, 2
     nc = O.coeff_count(r, c, lv)
