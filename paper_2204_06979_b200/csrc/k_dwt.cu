@@ -25,6 +25,13 @@ constexpr int FI = 4;    // forward column pass: output rows per thread
 constexpr int IR = 32;   // inverse: output rows per tile
 constexpr int IC = 64;   // inverse: output cols per tile
 
+// g mod n for g >= -n (the common case g in [0, n) costs one compare)
+__device__ __forceinline__ int wrap(int g, int n) {
+  if (g >= n) return g < 2 * n ? g - n : g % n;
+  if (g < 0) { g += n; return g >= 0 ? g : (g % n + n) % n; }
+  return g;
+}
+
 // Forward level.  Each thread of the row pass slides a register window of
 // 2 FJ + T - 2 inputs along one staged row and produces FJ (lo, hi) pairs; each
 // thread of the column pass does the same down one column for FI output rows
@@ -46,31 +53,32 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
   const int i0 = blockIdx.y * FR, j0 = blockIdx.x * FC;
   const float* x = in + (long long)blockIdx.z * in_stride;
   {
-    // stage the tile: every load of this thread is issued before the first
-    // shared store, so the L2/HBM round trips overlap instead of serialising
-    constexpr int NL = (NR * NC + 255) / 256;
-    float v[NL];
+    // stage the tile: warp w takes rows w, w + 8, ...; lane l columns l + 32u
+    // (coalesced rows; the periodic indices are computed once per row and
+    // once per column -- the per-element index math of a linear mapping cost
+    // more than the loads); every load of this thread is issued before the
+    // first shared store, so the L2/HBM round trips overlap
+    constexpr int NCI = (NC + 31) / 32;
+    constexpr int NRI = (NR + 7) / 8;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    int gcol[NCI];
 #pragma unroll
-    for (int u = 0; u < NL; ++u) {
-      const int idx = threadIdx.x + 256 * u;
-      v[u] = 0.f;
-      if (idx < NR * NC) {
-        const int r = idx / NC, c = idx - r * NC;
-        int gr = 2 * i0 + r, gc = 2 * j0 + c;
-        gr = gr >= H ? gr - H * (gr / H) : gr;
-        gc = gc >= Wd ? gc - Wd * (gc / Wd) : gc;
-        gr = min(gr, h_in - 1);   // odd extent: the padding row/column duplicates the last one
-        gc = min(gc, w_in - 1);
-        v[u] = __ldg(x + (long long)gr * w_in + gc);
-      }
+    for (int u = 0; u < NCI; ++u) gcol[u] = min(wrap(2 * j0 + l + 32 * u, Wd), w_in - 1);   // odd extent: duplicate the last column
+    float v[NRI][NCI];
+#pragma unroll
+    for (int ri = 0; ri < NRI; ++ri) {
+      const int r = w + 8 * ri;
+      const float* rowp = x + (long long)min(wrap(2 * i0 + r, H), h_in - 1) * w_in;
+#pragma unroll
+      for (int u = 0; u < NCI; ++u)
+        v[ri][u] = (r < NR && l + 32 * u < NC) ? __ldg(rowp + gcol[u]) : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < NL; ++u) {
-      const int idx = threadIdx.x + 256 * u;
-      if (idx < NR * NC) {
-        const int r = idx / NC, c = idx - r * NC;
-        xin[r][c] = v[u];
-      }
+    for (int ri = 0; ri < NRI; ++ri) {
+      const int r = w + 8 * ri;
+#pragma unroll
+      for (int u = 0; u < NCI; ++u)
+        if (r < NR && l + 32 * u < NC) xin[r][l + 32 * u] = v[ri][u];
     }
   }
   __syncthreads();
@@ -177,7 +185,9 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
     if (sp.s_ll >= 0) th_ll = tz[sp.s_ll];
   }
   {
-    // stage the four coefficient tiles, all loads in flight before the stores
+    // stage the four coefficient tiles (linear index, constant divide, cheap
+    // periodic wrap), all loads in flight before the stores, soft-thresholded
+    // as they land
     constexpr int NL = (CR * CC + 255) / 256;
     float v0[NL], v1[NL], v2[NL], v3[NL];
 #pragma unroll
@@ -186,11 +196,7 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
       v0[u] = v1[u] = v2[u] = v3[u] = 0.f;
       if (idx < CR * CC) {
         const int r = idx / CC, c = idx - r * CC;
-        int gi = (ilo + r) % hs;
-        gi += gi < 0 ? hs : 0;
-        int gj = (jlo + c) % ws;
-        gj += gj < 0 ? ws : 0;
-        const long long o = (long long)gi * ws + gj;
+        const long long o = (long long)wrap(ilo + r, hs) * ws + wrap(jlo + c, ws);
         v0[u] = a_ll[o];
         v1[u] = a_lh[o];
         v2[u] = a_hl[o];

@@ -59,8 +59,10 @@ constexpr unsigned KE0 = KB0 + ((unsigned)HB << HS0) - 1u;
 constexpr int CAP = NT * 32;              // window keys sorted at once (8192)
 constexpr int BIG_MIN = 32768;            // subbands at least this long may use a cluster
 constexpr int MAXPASS = 8;
-constexpr size_t SMEM_DYN = (size_t)2 * CAP * sizeof(unsigned);   // histogram (2 HB u32) | sort buffers (2 CAP u32)
-static_assert(2 * HB <= 2 * CAP, "histogram must fit the sort buffers");
+constexpr size_t SMEM_DYN = (size_t)2 * CAP * sizeof(unsigned);   // histogram (2 (HB+2) u32) | sort buffers (2 CAP u32)
+static_assert(HB + 2 <= CAP && 2 * (HB + 2) <= 2 * CAP, "histogram must fit the sort buffers");
+static_assert(2 * (HB + 2) + 8 + HB / 2 * 3 <= 2 * CAP && (2 * (HB + 2) + 8 + HB / 2) % 2 == 0,
+              "merged segment (nr >= 2) must fit past the histogram");
 
 __device__ __forceinline__ uint32_t cluster_nctarank() {
   uint32_t r;
@@ -227,14 +229,15 @@ __device__ __forceinline__ unsigned fxsq(unsigned key) {
 }
 
 // Streams x[0..n) (any alignment) with 16-byte loads, U float4 per thread in
-// flight, and calls f(key) for every element.
+// flight, and calls f(key, j) for every element (j in 0..3: a compile-time
+// slot, so callers can keep independent accumulators per slot).
 template <typename F>
 __device__ __forceinline__ void stream_keys(const float* __restrict__ x, int n, F&& f) {
   constexpr int U = 4;
   const int tid = threadIdx.x;
   int head = (int)(((16u - ((unsigned)(uintptr_t)x & 15u)) & 15u) >> 2);
   head = min(head, n);
-  if (tid < head) f(keyof(__ldg(x + tid)));
+  if (tid < head) f(keyof(__ldg(x + tid)), 0);
   const float4* v = reinterpret_cast<const float4*>(x + head);
   const int nv = (n - head) >> 2;
   int i = tid;
@@ -244,21 +247,21 @@ __device__ __forceinline__ void stream_keys(const float* __restrict__ x, int n, 
     for (int u = 0; u < U; ++u) r[u] = __ldg(v + i + u * NT);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      f(keyof(r[u].x));
-      f(keyof(r[u].y));
-      f(keyof(r[u].z));
-      f(keyof(r[u].w));
+      f(keyof(r[u].x), 0);
+      f(keyof(r[u].y), 1);
+      f(keyof(r[u].z), 2);
+      f(keyof(r[u].w), 3);
     }
   }
   for (; i < nv; i += NT) {
     const float4 r = __ldg(v + i);
-    f(keyof(r.x));
-    f(keyof(r.y));
-    f(keyof(r.z));
-    f(keyof(r.w));
+    f(keyof(r.x), 0);
+    f(keyof(r.y), 1);
+    f(keyof(r.z), 2);
+    f(keyof(r.w), 3);
   }
   const int t0 = head + (nv << 2);
-  if (t0 + tid < n) f(keyof(__ldg(x + t0 + tid)));
+  if (t0 + tid < n) f(keyof(__ldg(x + t0 + tid)), 0);
 }
 
 __device__ __forceinline__ bool better(double s1, long long k1, double s2, long long k2) {
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   extern __shared__ __align__(16) unsigned char smraw[];
   // union: histogram (HB counts | HB fixed-point sums) | window keys + sort buffer
   unsigned* hcnt = reinterpret_cast<unsigned*>(smraw);
-  unsigned* hsum = hcnt + HB;
+  unsigned* hsum = hcnt + HB + 2;
   unsigned* skeys = reinterpret_cast<unsigned*>(smraw);
   unsigned* sbuf = skeys + CAP;
   __shared__ double red[3 * NWS + 2];
@@ -382,8 +385,9 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   __shared__ int x_first[GMAX], x_last[GMAX];
   __shared__ double x_win[GMAX][4];          // window count in segment; prefix (count, pl, ph) at `first`
   __shared__ double x_v[GMAX][5];            // pass-1 out-of-range stats: cb, qb, ca, qa, maxkey
-  __shared__ double x_fin[GMAX][5];          // compaction: sum below (x^2), above (x, x^2), counts below / above
+  __shared__ double x_fin[GMAX][4];          // compaction: sum below (x^2), above (x, x^2), count above
   __shared__ unsigned s_wpos;                // leader: next free slot of the window-key buffer
+  __shared__ unsigned s_kmax;                // pass 1: largest key from 2^24 up
 
   const int tid = threadIdx.x;
   const int G = (int)cluster_nctarank();
@@ -427,10 +431,14 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
     empty = true;
   } else if (n > CAP) {
     const int seg = HB / nr;                 // bins owned by this rank in the bound computation
-    const int bpt = seg / NT;                // ... per thread (1..16)
+    // merged bins of this rank's segment: the local histogram itself (nr = 1)
+    // or counts | 64-bit sums in the upper half of the dynamic buffer
+    unsigned* gcnt = skeys + 2 * (HB + 2) + 8;          // past the histogram (still read remotely)
+    unsigned long long* gsum = reinterpret_cast<unsigned long long*>(gcnt + HB / 2);
     for (int pass = 0; pass < MAXPASS; ++pass) {
       const bool p1 = pass == 0;
-      // binned key range [bl, bh] with bins of 2^sh keys from kb
+      // binned key range [bl, bh] with bins of 2^sh keys from kb; pass 1 adds
+      // two catch-all bins: HB (keys below 2^-40) and HB + 1 (from 2^24)
       int sh;
       unsigned kb, bl, bh;
       if (p1) {
@@ -442,93 +450,84 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         bl = klo;
         bh = khi;
       }
-      for (int b = tid; b < 2 * HB; b += NT) hcnt[b] = 0u;
+      for (int b = tid; b < HB + 2; b += NT) { hcnt[b] = 0u; hsum[b] = 0u; }
+      if (tid == 0) s_kmax = 0u;
       __syncthreads();
-      double cbv = 0.0, qbv = 0.0, cav = 0.0, qav = 0.0;
-      unsigned kmax = 0u;
-      stream_keys(x, ns, [&](unsigned k) {
-        if (k >= bl && k <= bh) {
-          const unsigned b = (k - kb) >> sh;
+      if (p1) {
+        stream_keys(x, ns, [&](unsigned k, int) {
+          int b = (int)(k >> HS0) - (int)(KB0 >> HS0);
+          b = b < 0 ? HB : b;
+          if (b >= HB + 1) { b = HB + 1; atomicMax(&s_kmax, k); }
           atomicAdd(hcnt + b, 1u);
           atomicAdd(hsum + b, fxsq(k));
-        } else if (p1) {                     // pass 1: keys outside [2^-40, 2^24), exact fp64
-          const double a = kval(k);
-          if (k < bl) { cbv += 1.0; qbv = fma(a, a, qbv); }
-          else { cav += 1.0; qav = fma(a, a, qav); kmax = max(kmax, k); }
-        }
-      });
-      if (p1) {
-        cbv = block_sum_d(cbv, red);
-        qbv = block_sum_d(qbv, red);
-        cav = block_sum_d(cav, red);
-        qav = block_sum_d(qav, red);
-        kmax = block_max_u(kmax, redu);
-        if (tid == 0) {
-          cx.xput_d(&x_v[0][0], rank * 5 + 0, cbv);
-          cx.xput_d(&x_v[0][0], rank * 5 + 1, qbv);
-          cx.xput_d(&x_v[0][0], rank * 5 + 2, cav);
-          cx.xput_d(&x_v[0][0], rank * 5 + 3, qav);
-          cx.xput_d(&x_v[0][0], rank * 5 + 4, (double)kmax);
-        }
+        });
+      } else {
+        stream_keys(x, ns, [&](unsigned k, int) {
+          if (k >= bl && k <= bh) {
+            const unsigned b = (k - kb) >> sh;
+            atomicAdd(hcnt + b, 1u);
+            atomicAdd(hsum + b, fxsq(k));
+          }
+        });
       }
       cx.sync();                             // histograms complete everywhere
-      // merge: this rank's segment of bins, summed over ranks in rank order
-      unsigned mc[BPT];
-      unsigned long long msum[BPT];
-      unsigned ovf = 0u;                     // bit i: a rank's fixed-point sum of bin i may have wrapped
-      const int b0 = rank * seg + tid * bpt;
-#pragma unroll
-      for (int i = 0; i < BPT; ++i) {
-        mc[i] = 0u;
-        msum[i] = 0ull;
-        if (i < bpt) {
+      // merge this rank's segment over the ranks (rank order) + the catch-alls
+      if (nr > 1) {
+        for (int b = tid; b < seg; b += NT) {
+          const int gb = rank * seg + b;
+          unsigned c = 0u;
+          unsigned long long q = 0ull;
+          bool ov = false;
           for (int r = 0; r < nr; ++r) {
-            unsigned c, q;
-            if (nr == 1) { c = hcnt[b0 + i]; q = hsum[b0 + i]; }
-            else { c = ld_dsm_u32(cx.at(hcnt + b0 + i, r)); q = ld_dsm_u32(cx.at(hsum + b0 + i, r)); }
-            mc[i] += c;
-            msum[i] += q;
-            if (c >= 65536u) ovf |= 1u << i;
+            const unsigned cr = ld_dsm_u32(cx.at(hcnt + gb, r));
+            c += cr;
+            q += ld_dsm_u32(cx.at(hsum + gb, r));
+            ov |= cr >= 65536u;
           }
+          gcnt[b] = c;
+          gsum[b] = ov ? ~0ull : q;
         }
       }
-      // out-of-range (pass 1) stats, identical on every rank
-      double vcb = 0.0, vqb = 0.0, vca = 0.0, vqa = 0.0, vmax = 0.0;
+      double vcb = 0.0, vca = 0.0;
+      unsigned vmax = 0u;
       if (p1) {
         for (int r = 0; r < nr; ++r) {
-          vcb += x_v[r][0]; vqb += x_v[r][1]; vca += x_v[r][2]; vqa += x_v[r][3];
-          vmax = fmax(vmax, x_v[r][4]);
+          vcb += (double)(nr > 1 ? ld_dsm_u32(cx.at(hcnt + HB, r)) : hcnt[HB]);
+          vca += (double)(nr > 1 ? ld_dsm_u32(cx.at(hcnt + HB + 1, r)) : hcnt[HB + 1]);
+          vmax = max(vmax, nr > 1 ? ld_dsm_u32(cx.at(&s_kmax, r)) : s_kmax);
         }
       }
-      // base prefix: keys below the binned range
-      const double c0 = p1 ? vcb : cb, p0l = p1 ? vqb : pl, p0h = p1 ? vqb : ph;
-      // per-bin value bounds and sum bounds (recomputed where needed: registers)
-      auto binfo = [&](int i, double& lo2, double& hi2, double& q_l, double& q_h) {
-        const unsigned kb0 = kb + ((unsigned)(b0 + i) << sh);
+      __syncthreads();
+      // bin i of the segment: count, value bounds, sum bounds
+      auto binfo = [&](int i, double& m, double& lo2, double& hi2, double& q_l, double& q_h) {
+        const unsigned c = nr > 1 ? gcnt[i] : hcnt[i];
+        m = (double)c;
+        if (c == 0u) { lo2 = hi2 = q_l = q_h = 0.0; return; }
+        const unsigned kb0 = kb + ((unsigned)(rank * seg + i) << sh);
         const unsigned kb1 = kb0 + ((1u << sh) - 1u);
         const unsigned lok = max(kb0, bl), hik = min(kb1, bh);
         const double lo = kval(lok), hi = kval(hik);
         lo2 = lo * lo;
         hi2 = hi * hi;
         const unsigned e = lok >> 23;
-        const double m = (double)mc[i];
-        if ((hik >> 23) == e && e > 0u && !((ovf >> i) & 1u)) {
+        const unsigned long long q = nr > 1 ? gsum[i] : (c >= 65536u ? ~0ull : (unsigned long long)hsum[i]);
+        if ((hik >> 23) == e && e > 0u && q != ~0ull) {
           const double sc = ldexp(1.0, 2 * (int)e - 268);
-          q_l = (double)msum[i] * sc;
-          q_h = ((double)msum[i] + m) * sc;
+          q_l = (double)q * sc;
+          q_h = ((double)q + m) * sc;
         } else {
           q_l = m * lo2;
           q_h = m * hi2;
         }
       };
+      const int bpt = seg / NT;              // bins per thread (1..16), contiguous
+      const int i0 = tid * bpt;
       double tv[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int i = 0; i < BPT; ++i) {
-        if (i < bpt && mc[i] > 0u) {
-          double lo2, hi2, q_l, q_h;
-          binfo(i, lo2, hi2, q_l, q_h);
-          tv[0] += (double)mc[i]; tv[1] += q_l; tv[2] += q_h;
-        }
+#pragma unroll 1
+      for (int i = i0; i < i0 + bpt; ++i) {
+        double m, lo2, hi2, q_l, q_h;
+        binfo(i, m, lo2, hi2, q_l, q_h);
+        tv[0] += m; tv[1] += q_l; tv[2] += q_h;
       }
       double off[3], segtot[3];
       block_excl_scan3(tv, off, segtot, red);
@@ -538,6 +537,10 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         cx.xput_d(&x_seg[0][0], rank * 3 + 2, segtot[2]);
       }
       cx.sync();
+      // base prefix: keys below the binned range (pass 1: the low catch-all,
+      // count-only bounds; its values are below 2^-40)
+      const double lo_cut = kval(KB0 - 1u);
+      const double c0 = p1 ? vcb : cb, p0l = p1 ? 0.0 : pl, p0h = p1 ? vcb * lo_cut * lo_cut : ph;
       double sc0 = c0, sl0 = p0l, sh0 = p0h, allc = c0, allh = p0h, alll = p0l;
       for (int r = 0; r < nr; ++r) {
         if (r < rank) { sc0 += x_seg[r][0]; sl0 += x_seg[r][1]; sh0 += x_seg[r][2]; }
@@ -546,38 +549,30 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       // bounds.  Bin j, c keys below it, m in it, values in [lo, hi]:
       //   S_k >= LB = n - 2(c+m) + P_lo(c) + (n-c) lo^2 for every k in the bin,
       //   min S <= UB = n - 2(c+m) + P_hi(c) + Q_hi + (n-c-m) hi^2  (S at k = c+m).
-      const double tol = 1e-9 * dn + 1e-12 * (dn + allh);
-      double lbs[BPT];
+      const double hi_top = kval(vmax);
+      const double tol = 1e-9 * dn + 1e-12 * (dn + allh + vca * hi_top * hi_top);
       double ubt = INFINITY;
       {
         double c = sc0 + off[0], p_l = sl0 + off[1], p_h = sh0 + off[2];
-#pragma unroll
-        for (int i = 0; i < BPT; ++i) {
-          lbs[i] = INFINITY;
-          if (i < bpt && mc[i] > 0u) {
-            double lo2, hi2, q_l, q_h;
-            binfo(i, lo2, hi2, q_l, q_h);
-            const double m = (double)mc[i];
-            lbs[i] = dn - 2.0 * (c + m) + p_l + (dn - c) * lo2;
-            const double ub = dn - 2.0 * (c + m) + p_h + q_h + (dn - c - m) * hi2;
-            ubt = fmin(ubt, ub);
-            c += m; p_l += q_l; p_h += q_h;
-          }
+#pragma unroll 1
+        for (int i = i0; i < i0 + bpt; ++i) {
+          double m, lo2, hi2, q_l, q_h;
+          binfo(i, m, lo2, hi2, q_l, q_h);
+          if (m > 0.0) ubt = fmin(ubt, dn - 2.0 * (c + m) + p_h + q_h + (dn - c - m) * hi2);
+          c += m; p_l += q_l; p_h += q_h;
         }
       }
-      // virtual bins of pass 1: below 2^-40 (index -1) and from 2^24 (index HB)
+      // catch-all bins of pass 1: below 2^-40 (index -1) and from 2^24 (index HB)
       double lb_lo = INFINITY, lb_hi = INFINITY;
       if (p1) {
-        const double hi_lo = kval(KB0 - 1u);
         if (vcb > 0.0) {
           lb_lo = dn - 2.0 * vcb;
-          ubt = fmin(ubt, dn - 2.0 * vcb + vqb + (dn - vcb) * hi_lo * hi_lo);
+          ubt = fmin(ubt, dn - 2.0 * vcb + p0h + (dn - vcb) * lo_cut * lo_cut);
         }
         if (vca > 0.0) {
-          const double lo = kval(KE0 + 1u), hi = kval((unsigned)vmax);
-          lb_hi = dn - 2.0 * dn + alll + vca * lo * lo;
-          ubt = fmin(ubt, -dn + allh + vqa);
-          (void)hi;
+          const double lo = kval(KE0 + 1u);
+          lb_hi = -dn + alll + vca * lo * lo;
+          ubt = fmin(ubt, -dn + allh + vca * hi_top * hi_top);
         }
       }
       ubt = block_min_d(ubt, red);
@@ -587,9 +582,20 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       for (int r = 0; r < nr; ++r) ub = fmin(ub, x_ub[r]);
       const double thr = ub + tol;
       int fst = INT_MAX, lst = -2;
-#pragma unroll
-      for (int i = 0; i < BPT; ++i)
-        if (i < bpt && lbs[i] <= thr) { fst = min(fst, b0 + i); lst = max(lst, b0 + i); }
+      double mwin_t = 0.0;
+      {
+        double c = sc0 + off[0], p_l = sl0 + off[1];
+#pragma unroll 1
+        for (int i = i0; i < i0 + bpt; ++i) {
+          double m, lo2, hi2, q_l, q_h;
+          binfo(i, m, lo2, hi2, q_l, q_h);
+          if (m > 0.0 && dn - 2.0 * (c + m) + p_l + (dn - c) * lo2 <= thr) {
+            fst = min(fst, rank * seg + i);
+            lst = max(lst, rank * seg + i);
+          }
+          c += m; p_l += q_l;
+        }
+      }
       fst = block_min_i(fst, redi);
       lst = -block_min_i(-lst, redi);
       if (tid == 0) { cx.xput_u((unsigned*)x_first, rank, (unsigned)fst); cx.xput_u((unsigned*)x_last, rank, (unsigned)lst); }
@@ -600,26 +606,19 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       if (p1 && lb_hi <= thr) { gl = HB; if (gf == INT_MAX) gf = HB; }
       if (p1 && gf == -1 && gl == -2) gl = -1;
       // window count in this segment and, for the owner of `gf`, the prefix there
-      double mwin = 0.0;
       {
         double c = sc0 + off[0], p_l = sl0 + off[1], p_h = sh0 + off[2];
-#pragma unroll
-        for (int i = 0; i < BPT; ++i) {
-          if (i < bpt) {
-            const int b = b0 + i;
-            if (b == gf) {
-              x_win[rank][1] = c; x_win[rank][2] = p_l; x_win[rank][3] = p_h;   // local slot, pushed below
-            }
-            if (b >= gf && b <= gl) mwin += (double)mc[i];
-            if (mc[i] > 0u) {
-              double lo2, hi2, q_l, q_h;
-              binfo(i, lo2, hi2, q_l, q_h);
-              c += (double)mc[i]; p_l += q_l; p_h += q_h;
-            }
-          }
+#pragma unroll 1
+        for (int i = i0; i < i0 + bpt; ++i) {
+          double m, lo2, hi2, q_l, q_h;
+          binfo(i, m, lo2, hi2, q_l, q_h);
+          const int b = rank * seg + i;
+          if (b == gf) { x_win[rank][1] = c; x_win[rank][2] = p_l; x_win[rank][3] = p_h; }
+          if (b >= gf && b <= gl) mwin_t += m;
+          c += m; p_l += q_l; p_h += q_h;
         }
       }
-      mwin = block_sum_d(mwin, red);         // contains barriers: x_win[rank][1..3] visible
+      const double mwin = block_sum_d(mwin_t, red);   // contains barriers: x_win[rank][1..3] visible
       const bool own_first = gf >= rank * seg && gf < (rank + 1) * seg;
       if (tid == 0) {
         cx.xput_d(&x_win[0][0], rank * 4 + 0, mwin);
@@ -646,7 +645,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         klo = max(kb + ((unsigned)gf << sh), bl);
         cb = x_win[ow][1]; pl = x_win[ow][2]; ph = x_win[ow][3];
       }
-      if (gl == HB) { khi = (unsigned)vmax; Mw += vca; }
+      if (gl == HB) { khi = vmax; Mw += vca; }
       else if (gl == -1) { khi = KB0 - 1u; }
       else khi = min(kb + ((unsigned)(gl + 1) << sh) - 1u, bh);
       M = Mw;
@@ -668,16 +667,25 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   // ---------------- compaction: window keys -> the leader's buffer ----------------
   if (leader && tid == 0) s_wpos = 0u;
   cx.sync();
-  double qb = 0.0, q1 = 0.0, q2 = 0.0, cbl = 0.0, cab = 0.0;
+  // below the window (the bulk): exact fp64 squares, the fp64 value built from
+  // the fp32 bits (rebias: no conversion instruction; subnormals count as 0),
+  // two independent chains; window and above-window keys take the rare branch
+  double qb0 = 0.0, qb1 = 0.0, q1 = 0.0, q2 = 0.0;
+  int cai = 0;
   {
     const bool wr = !closed;
     const uint32_t wpos = cx.at(&s_wpos, 0);
     const uint32_t kbase = cx.at(skeys, 0);
-    stream_keys(x, ns, [&](unsigned k) {
-      const double a = kval(k);
-      if (k < klo) { qb = fma(a, a, qb); cbl += 1.0; }
-      else if (k > khi) { q1 += a; q2 = fma(a, a, q2); cab += 1.0; }
-      else if (wr) {
+    stream_keys(x, ns, [&](unsigned k, int j) {
+      if (__builtin_expect(k < klo, 1)) {
+        const double a = k < 0x800000u ? 0.0 : __longlong_as_double(((long long)k << 29) + (896LL << 52));
+        if (j & 1) qb1 = fma(a, a, qb1); else qb0 = fma(a, a, qb0);
+      } else if (k > khi) {
+        const double a = kval(k);
+        q1 += a;
+        q2 = fma(a, a, q2);
+        ++cai;
+      } else if (wr) {
         unsigned p;
         if (nr == 1) p = atomicAdd(&s_wpos, 1u);
         else p = atom_dsm_add_u32(wpos, 1u);
@@ -687,27 +695,26 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       }
     });
   }
-  qb = block_sum_d(qb, red);
+  const double qb = block_sum_d(qb0 + qb1, red);
+  const double cab = block_sum_d((double)cai, red);
   q1 = block_sum_d(q1, red);
   q2 = block_sum_d(q2, red);
-  cbl = block_sum_d(cbl, red);
-  cab = block_sum_d(cab, red);
   if (tid == 0) {
     const uint32_t a = cx.at(&x_fin[rank][0], 0);
     st_dsm_f64(a, qb);
     st_dsm_f64(a + 8, q1);
     st_dsm_f64(a + 16, q2);
-    st_dsm_f64(a + 24, cbl);
-    st_dsm_f64(a + 32, cab);
+    st_dsm_f64(a + 24, cab);
   }
   cx.sync();
   if (!leader) return;
 
   // ---------------- exact evaluation on the leader ----------------
-  double P0 = 0.0, Q1 = 0.0, Q2 = 0.0, CB = 0.0, cabove = 0.0;
-  for (int r = 0; r < nr; ++r) {
-    P0 += x_fin[r][0]; Q1 += x_fin[r][1]; Q2 += x_fin[r][2]; CB += x_fin[r][3]; cabove += x_fin[r][4];
-  }
+  double P0 = 0.0, Q1 = 0.0, Q2 = 0.0, cabove = 0.0;
+  for (int r = 0; r < nr; ++r) { P0 += x_fin[r][0]; Q1 += x_fin[r][1]; Q2 += x_fin[r][2]; cabove += x_fin[r][3]; }
+  // keys below the window: the rest (window count exact: written keys, or M
+  // of a closed-form run)
+  const double CB = dn - cabove - (empty ? 0.0 : (closed ? M : (double)s_wpos));
   if (!closed && !empty && s_wpos > (unsigned)CAP && tid == 0) atomicOr(&rs->sure_overflow, 1);
   double sbest = dn;                         // k = 0
   long long kbest = 0;
