@@ -256,6 +256,13 @@ long long hyde_launch_count(hyde_handle h);
  * reflector; bisection; inverse iteration).  Copies 32 values; synchronizes. */
 hyde_status hyde_debug_eig_clocks(long long* out32);
 
+/* K5 phase profile of the SURE launches since the last call (builds with
+ * HYDE_SURE_PROF=1 only; returns 0 and zeros otherwise, 1 when filled):
+ * out16[c*8 + p] = SM cycles summed over CTAs, class c (0: subbands longer than
+ * the 8192-key window capacity, 1: shorter), phase p (0 window search,
+ * 1 compaction, 2 sort + exact evaluation, 3 = number of CTAs).  Synchronizes. */
+int hyde_debug_sure_prof(unsigned long long* out16);
+
 /* CTAs per K2 eigensolver cluster on the current device: 16 (non-portable
  * cluster size) when the GPU can co-schedule it, else 8. */
 int hyde_eig_cluster_size(void);

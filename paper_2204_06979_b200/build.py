@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhyde.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3"] + (["-DHYDE_SURE_DEBUG"] if os.environ.get("HYDE_SURE_DEBUG") else []) + \
+FLAGS = ["-O3"] + (["-DHYDE_SURE_PROF"] if os.environ.get("HYDE_SURE_PROF") else []) + \
     (["-DHYDE_EIG_PROF"] if os.environ.get("HYDE_EIG_PROF") else []) + ["-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
 

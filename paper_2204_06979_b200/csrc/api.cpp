@@ -947,6 +947,8 @@ hyde_status hyde_k_eig(hyde_handle h, const double* gram, int n_pixels, int band
   return HYDE_OK;
 }
 
+int hyde_debug_sure_prof(unsigned long long* out16) { return out16 ? sure_prof_read(out16) : -1; }
+
 hyde_status hyde_debug_eig_state(hyde_handle h, int n_pixels, int bands, double* tri_out, double* house_out) {
   if (!h || !h->ws || !tri_out || !house_out || bands < 3) return HYDE_EPARAM;
   DeviceGuard g(h->device);

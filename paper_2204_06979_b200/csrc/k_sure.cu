@@ -59,7 +59,10 @@ constexpr unsigned KE0 = KB0 + ((unsigned)HB << HS0) - 1u;
 constexpr int CAP = NT * 32;              // window keys sorted at once (8192)
 constexpr int BIG_MIN = 32768;            // subbands at least this long may use a cluster
 constexpr int MAXPASS = 8;
-constexpr size_t SMEM_DYN = (size_t)2 * CAP * sizeof(unsigned);   // histogram (2 (HB+2) u32) | sort buffers (2 CAP u32)
+constexpr int RING_OFF = 2 * (HB + 2);   // u32 offset of the streaming ring (16-byte aligned)
+// dynamic buffer: histogram (2 (HB+2) u32) + streaming ring | window keys + sort buffer (2 CAP u32)
+constexpr size_t SMEM_DYN = (size_t)(RING_OFF + 8 * NT * 4) * sizeof(unsigned);
+static_assert(RING_OFF % 4 == 0 && (size_t)2 * CAP * sizeof(unsigned) <= SMEM_DYN, "buffer layout");
 static_assert(HB + 2 <= CAP && 2 * (HB + 2) <= 2 * CAP, "histogram must fit the sort buffers");
 static_assert(2 * (HB + 2) + 8 + HB / 2 * 3 <= 2 * CAP && (2 * (HB + 2) + 8 + HB / 2) % 2 == 0,
               "merged segment (nr >= 2) must fit past the histogram");
@@ -228,39 +231,54 @@ __device__ __forceinline__ unsigned fxsq(unsigned key) {
   return __umulhi(M, M);
 }
 
-// Streams x[0..n) (any alignment) with 16-byte loads, U float4 per thread in
-// flight, and calls f(key, j) for every element (j in 0..3: a compile-time
-// slot, so callers can keep independent accumulators per slot).
+// Streams x[0..n) (any alignment) through a ring of NSTG shared-memory
+// stages of NT float4 filled by 1-D bulk copies (TMA engine, completion on one
+// mbarrier per stage): NSTG x 4 KB in flight per CTA without holding registers.
+// Calls f(key, j) for every element (j in 0..3: a compile-time slot, so callers
+// can keep independent accumulators per slot).  `ru` counts the chunks this
+// CTA has consumed so far (stage = ru % NSTG, parity = (ru / NSTG) & 1); every
+// thread calls with the same arguments.
+constexpr int NSTG = 8;
+constexpr int CHB = NT * 16;   // bytes per stage
 template <typename F>
-__device__ __forceinline__ void stream_keys(const float* __restrict__ x, int n, F&& f) {
-  constexpr int U = 4;
+__device__ __forceinline__ void stream_keys(const float* __restrict__ x, int n, float4* ring, uint64_t* full,
+                                            unsigned& ru, F&& f) {
   const int tid = threadIdx.x;
-  int head = (int)(((16u - ((unsigned)(uintptr_t)x & 15u)) & 15u) >> 2);
-  head = min(head, n);
+  const int head = min(n, (int)(((16u - ((unsigned)(uintptr_t)x & 15u)) & 15u) >> 2));
+  const char* base = reinterpret_cast<const char*>(x + head);
+  const long long nbytes = ((long long)(n - head) * 4) & ~15LL;
+  const int nch = (int)((nbytes + CHB - 1) / CHB);
+  auto issue = [&](int c) {
+    const unsigned s = (ru + (unsigned)c) % NSTG;
+    const unsigned bytes = (unsigned)min((long long)CHB, nbytes - (long long)c * CHB);
+    tc::mbar_expect_tx(&full[s], bytes);
+    tc::bulk_g2s(ring + s * NT, base + (long long)c * CHB, bytes, &full[s]);
+  };
+  if (tid == 0) {
+    tc::fence_proxy_async_smem();
+    for (int c = 0; c < min(nch, NSTG); ++c) issue(c);
+  }
   if (tid < head) f(keyof(__ldg(x + tid)), 0);
-  const float4* v = reinterpret_cast<const float4*>(x + head);
-  const int nv = (n - head) >> 2;
-  int i = tid;
-  for (; i + (U - 1) * NT < nv; i += U * NT) {
-    float4 r[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = __ldg(v + i + u * NT);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      f(keyof(r[u].x), 0);
-      f(keyof(r[u].y), 1);
-      f(keyof(r[u].z), 2);
-      f(keyof(r[u].w), 3);
+  for (int c = 0; c < nch; ++c) {
+    const unsigned u = ru + (unsigned)c, s = u % NSTG;
+    tc::mbar_wait(&full[s], (u / NSTG) & 1u);
+    const bool ok = (long long)c * CHB + tid * 16 < nbytes;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) v = ring[s * NT + tid];
+    __syncthreads();                         // stage s consumed by every thread
+    if (tid == 0 && c + NSTG < nch) {
+      tc::fence_proxy_async_smem();
+      issue(c + NSTG);
+    }
+    if (ok) {
+      f(keyof(v.x), 0);
+      f(keyof(v.y), 1);
+      f(keyof(v.z), 2);
+      f(keyof(v.w), 3);
     }
   }
-  for (; i < nv; i += NT) {
-    const float4 r = __ldg(v + i);
-    f(keyof(r.x), 0);
-    f(keyof(r.y), 1);
-    f(keyof(r.z), 2);
-    f(keyof(r.w), 3);
-  }
-  const int t0 = head + (nv << 2);
+  ru += (unsigned)nch;
+  const int t0 = head + (int)(nbytes >> 2);
   if (t0 + tid < n) f(keyof(__ldg(x + t0 + tid)), 0);
 }
 
@@ -362,6 +380,14 @@ __device__ __forceinline__ unsigned atom_dsm_add_u32(uint32_t a, unsigned v) {
   return r;
 }
 
+#ifdef HYDE_SURE_PROF
+// [class*8 + phase] cycles summed over CTAs (class 0: n > CAP, 1: n <= CAP;
+// phase 0 window search, 1 compaction, 2 sort + evaluation, 3 CTAs)
+__device__ unsigned long long g_sure_prof[16];
+#define SPROF(cls, ph, t0) do { if (threadIdx.x == 0) atomicAdd(&g_sure_prof[(cls) * 8 + (ph)], (unsigned long long)(clock64() - (t0))); } while (0)
+#else
+#define SPROF(cls, ph, t0) do { } while (0)
+#endif
 constexpr int BPT = HB / NT;   // bins per thread when one CTA owns the whole histogram
 
 // Exact per-subband SURE (see the file comment).  One item = (component,
@@ -388,6 +414,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   __shared__ double x_fin[GMAX][4];          // compaction: sum below (x^2), above (x, x^2), count above
   __shared__ unsigned s_wpos;                // leader: next free slot of the window-key buffer
   __shared__ unsigned s_kmax;                // pass 1: largest key from 2^24 up
+  __shared__ __align__(8) uint64_t s_full[NSTG];   // streaming ring: one mbarrier per stage
 
   const int tid = threadIdx.x;
   const int G = (int)cluster_nctarank();
@@ -420,8 +447,22 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   const int ns = hi_i - lo_i;
   const int ks = comp * tab.nsub + s;
   const bool skip = keep_ll && s == tab.nsub - 1;   // LL kept: t = 0
+  // streaming ring past the histogram (overlaps the sort buffer and the merged
+  // bins, idle while streaming; the compaction's window keys land below it)
+  float4* ring = reinterpret_cast<float4*>(skeys + RING_OFF);
+  unsigned ru = 0u;
+  if (tid == 0) {
+    for (int i = 0; i < NSTG; ++i) tc::mbar_init(&s_full[i], 1u);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
 
   // ---------------- window search ----------------
+  const int pcls = n > CAP ? 0 : 1;
+  long long pt0 = clock64();
+#ifdef HYDE_SURE_PROF
+  if (tid == 0) atomicAdd(&g_sure_prof[pcls * 8 + 3], 1ull);
+#endif
   // window [klo, khi] of keys that can hold the argmin; (cb, pl, ph): exact
   // count and bounds of sum x^2 of the keys below it.
   unsigned klo = 0u, khi = 0x7FFFFFFFu;
@@ -454,7 +495,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       if (tid == 0) s_kmax = 0u;
       __syncthreads();
       if (p1) {
-        stream_keys(x, ns, [&](unsigned k, int) {
+        stream_keys(x, ns, ring, s_full, ru, [&](unsigned k, int) {
           int b = (int)(k >> HS0) - (int)(KB0 >> HS0);
           b = b < 0 ? HB : b;
           if (b >= HB + 1) { b = HB + 1; atomicMax(&s_kmax, k); }
@@ -462,7 +503,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
           atomicAdd(hsum + b, fxsq(k));
         });
       } else {
-        stream_keys(x, ns, [&](unsigned k, int) {
+        stream_keys(x, ns, ring, s_full, ru, [&](unsigned k, int) {
           if (k >= bl && k <= bh) {
             const unsigned b = (k - kb) >> sh;
             atomicAdd(hcnt + b, 1u);
@@ -664,6 +705,8 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   if (overflow) empty = true;                // flagged above; keep going to write something
   if (empty) { klo = 0xFFFFFFFFu; khi = 0u; }  // every key is "below"
 
+  SPROF(pcls, 0, pt0);
+  pt0 = clock64();
   // ---------------- compaction: window keys -> the leader's buffer ----------------
   if (leader && tid == 0) s_wpos = 0u;
   cx.sync();
@@ -676,7 +719,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
     const bool wr = !closed;
     const uint32_t wpos = cx.at(&s_wpos, 0);
     const uint32_t kbase = cx.at(skeys, 0);
-    stream_keys(x, ns, [&](unsigned k, int j) {
+    stream_keys(x, ns, ring, s_full, ru, [&](unsigned k, int j) {
       if (__builtin_expect(k < klo, 1)) {
         const double a = k < 0x800000u ? 0.0 : __longlong_as_double(((long long)k << 29) + (896LL << 52));
         if (j & 1) qb1 = fma(a, a, qb1); else qb0 = fma(a, a, qb0);
@@ -709,6 +752,8 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   cx.sync();
   if (!leader) return;
 
+  SPROF(pcls, 1, pt0);
+  pt0 = clock64();
   // ---------------- exact evaluation on the leader ----------------
   double P0 = 0.0, Q1 = 0.0, Q2 = 0.0, cabove = 0.0;
   for (int r = 0; r < nr; ++r) { P0 += x_fin[r][0]; Q1 += x_fin[r][1]; Q2 += x_fin[r][2]; cabove += x_fin[r][3]; }
@@ -786,6 +831,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   if (tid == 0) {
     double e = ew + (Q2 - 2.0 * t * Q1 + cabove * t * t);
     if (kbest == 0) e += P0;
+    SPROF(pcls, 2, pt0);
     kstar[ks] = (int)kbest;
     tstar[ks] = __uint_as_float(tkey);
     e_sub[ks] = e;
@@ -880,6 +926,19 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, sure_kernel, (const float*)coeffs, cstride, tab, count, keep_ll, kstar, tstar, e_sub,
                             rs);
+}
+
+int sure_prof_read(unsigned long long* out16) {
+#ifdef HYDE_SURE_PROF
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out16, g_sure_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_sure_prof, z, sizeof(z));
+  return 1;
+#else
+  for (int i = 0; i < 16; ++i) out16[i] = 0ull;
+  return 0;
+#endif
 }
 
 cudaError_t launch_soft_threshold(float* coeffs, long long cstride, const DwtPlan& plan, int count, const float* tstar,
