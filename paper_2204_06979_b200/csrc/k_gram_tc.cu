@@ -338,16 +338,16 @@ __global__ void amax_kernel(const float* __restrict__ Y, long long n, unsigned* 
   bool bad = false;
   const bool vec = (n % 4 == 0) && (((uintptr_t)Y & 15) == 0);
   if (vec) {
-    // four independent 16-byte loads in flight per thread per step
+    // eight independent 16-byte loads in flight per thread per step
     const long long n4 = n / 4;
     const long long stride = (long long)gridDim.x * blockDim.x;
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    for (; i + 3 * stride < n4; i += 4 * stride) {
-      float4 v[4];
+    for (; i + 7 * stride < n4; i += 8 * stride) {
+      float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(row) + i + u * stride);
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(row) + i + u * stride);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         m = max(m, __float_as_uint(fabsf(v[u].x)));
         m = max(m, __float_as_uint(fabsf(v[u].y)));
         m = max(m, __float_as_uint(fabsf(v[u].z)));
@@ -396,7 +396,7 @@ cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_
   if (e != cudaSuccess) return e;
   long long per_block = 256LL * 4 * 8;
   unsigned gx = (unsigned)((n + per_block - 1) / per_block);
-  if (gx > 64) gx = 64;
+  if (gx > 16) gx = 16;   // 16 x B blocks: 64K-element band segments at B = 224, N = 2^20
   if (gx < 1) gx = 1;
   amax_kernel<<<dim3(gx, B), 256, 0, st>>>(Y, n, amax_bits, nonfinite);
   return cudaGetLastError();

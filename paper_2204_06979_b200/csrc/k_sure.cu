@@ -46,6 +46,7 @@
 #include "tc_util.cuh"
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 namespace {
 
@@ -59,10 +60,8 @@ constexpr unsigned KE0 = KB0 + ((unsigned)HB << HS0) - 1u;
 constexpr int CAP = NT * 32;              // window keys sorted at once (8192)
 constexpr int BIG_MIN = 32768;            // subbands at least this long may use a cluster
 constexpr int MAXPASS = 8;
-constexpr int RING_OFF = 2 * (HB + 2);   // u32 offset of the streaming ring (16-byte aligned)
-// dynamic buffer: histogram (2 (HB+2) u32) + streaming ring | window keys + sort buffer (2 CAP u32)
-constexpr size_t SMEM_DYN = (size_t)(RING_OFF + 8 * NT * 4) * sizeof(unsigned);
-static_assert(RING_OFF % 4 == 0 && (size_t)2 * CAP * sizeof(unsigned) <= SMEM_DYN, "buffer layout");
+// dynamic buffer: histogram (2 (HB+2) u32) + merged bins | window keys + sort buffer (2 CAP u32)
+constexpr size_t SMEM_DYN = (size_t)2 * CAP * sizeof(unsigned);
 static_assert(HB + 2 <= CAP && 2 * (HB + 2) <= 2 * CAP, "histogram must fit the sort buffers");
 static_assert(2 * (HB + 2) + 8 + HB / 2 * 3 <= 2 * CAP && (2 * (HB + 2) + 8 + HB / 2) % 2 == 0,
               "merged segment (nr >= 2) must fit past the histogram");
@@ -89,15 +88,7 @@ __device__ __forceinline__ void st_dsm_u32(uint32_t a, unsigned v) {
 __device__ __forceinline__ void st_dsm_f64(uint32_t a, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
-__device__ __forceinline__ void st_dsm_s64(uint32_t a, long long v) {
-  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
-}
 
-__device__ __forceinline__ double ld_dsm_f64(uint32_t a) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
-  return v;
-}
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -231,54 +222,40 @@ __device__ __forceinline__ unsigned fxsq(unsigned key) {
   return __umulhi(M, M);
 }
 
-// Streams x[0..n) (any alignment) through a ring of NSTG shared-memory
-// stages of NT float4 filled by 1-D bulk copies (TMA engine, completion on one
-// mbarrier per stage): NSTG x 4 KB in flight per CTA without holding registers.
-// Calls f(key, j) for every element (j in 0..3: a compile-time slot, so callers
-// can keep independent accumulators per slot).  `ru` counts the chunks this
-// CTA has consumed so far (stage = ru % NSTG, parity = (ru / NSTG) & 1); every
-// thread calls with the same arguments.
-constexpr int NSTG = 8;
-constexpr int CHB = NT * 16;   // bytes per stage
-template <typename F>
-__device__ __forceinline__ void stream_keys(const float* __restrict__ x, int n, float4* ring, uint64_t* full,
-                                            unsigned& ru, F&& f) {
+// Streams x[0..n) (any alignment) with 16-byte loads, U float4 per thread in
+// flight, and calls f(key, j) for every element (j in 0..3: a compile-time
+// slot, so callers can keep independent accumulators per slot).  (A TMA
+// bulk-copy ring of 8 x 4 KB stages per CTA measured slower: the per-stage
+// block barrier put the consumers in lockstep.)
+template <int U = 4, typename F>
+__device__ __forceinline__ void stream_keys(const float* __restrict__ x, int n, F&& f) {
   const int tid = threadIdx.x;
-  const int head = min(n, (int)(((16u - ((unsigned)(uintptr_t)x & 15u)) & 15u) >> 2));
-  const char* base = reinterpret_cast<const char*>(x + head);
-  const long long nbytes = ((long long)(n - head) * 4) & ~15LL;
-  const int nch = (int)((nbytes + CHB - 1) / CHB);
-  auto issue = [&](int c) {
-    const unsigned s = (ru + (unsigned)c) % NSTG;
-    const unsigned bytes = (unsigned)min((long long)CHB, nbytes - (long long)c * CHB);
-    tc::mbar_expect_tx(&full[s], bytes);
-    tc::bulk_g2s(ring + s * NT, base + (long long)c * CHB, bytes, &full[s]);
-  };
-  if (tid == 0) {
-    tc::fence_proxy_async_smem();
-    for (int c = 0; c < min(nch, NSTG); ++c) issue(c);
-  }
+  int head = (int)(((16u - ((unsigned)(uintptr_t)x & 15u)) & 15u) >> 2);
+  head = min(head, n);
   if (tid < head) f(keyof(__ldg(x + tid)), 0);
-  for (int c = 0; c < nch; ++c) {
-    const unsigned u = ru + (unsigned)c, s = u % NSTG;
-    tc::mbar_wait(&full[s], (u / NSTG) & 1u);
-    const bool ok = (long long)c * CHB + tid * 16 < nbytes;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (ok) v = ring[s * NT + tid];
-    __syncthreads();                         // stage s consumed by every thread
-    if (tid == 0 && c + NSTG < nch) {
-      tc::fence_proxy_async_smem();
-      issue(c + NSTG);
-    }
-    if (ok) {
-      f(keyof(v.x), 0);
-      f(keyof(v.y), 1);
-      f(keyof(v.z), 2);
-      f(keyof(v.w), 3);
+  const float4* v = reinterpret_cast<const float4*>(x + head);
+  const int nv = (n - head) >> 2;
+  int i = tid;
+  for (; i + (U - 1) * NT < nv; i += U * NT) {
+    float4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = __ldg(v + i + u * NT);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      f(keyof(r[u].x), 0);
+      f(keyof(r[u].y), 1);
+      f(keyof(r[u].z), 2);
+      f(keyof(r[u].w), 3);
     }
   }
-  ru += (unsigned)nch;
-  const int t0 = head + (int)(nbytes >> 2);
+  for (; i < nv; i += NT) {
+    const float4 r = __ldg(v + i);
+    f(keyof(r.x), 0);
+    f(keyof(r.y), 1);
+    f(keyof(r.z), 2);
+    f(keyof(r.w), 3);
+  }
+  const int t0 = head + (nv << 2);
   if (t0 + tid < n) f(keyof(__ldg(x + t0 + tid)), 0);
 }
 
@@ -340,17 +317,6 @@ __device__ __forceinline__ int block_min_i(int v, int* red) {
   for (int u = 1; u < NWS; ++u) r = min(r, red[u]);
   return r;
 }
-__device__ __forceinline__ unsigned block_max_u(unsigned v, unsigned* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  unsigned r = red[0];
-  for (int u = 1; u < NWS; ++u) r = max(r, red[u]);
-  return r;
-}
 
 // Per-item cluster context: `nr` CTAs (cluster ranks 0..nr-1, or this CTA
 // alone) work on one subband; xput() writes a value into slot `slot` of the
@@ -369,9 +335,11 @@ struct Ctx {
   }
 };
 
+// plain (non-volatile) DSMEM load: ordering comes from the cluster barriers,
+// and independent loads may be in flight together
 __device__ __forceinline__ unsigned ld_dsm_u32(uint32_t a) {
   unsigned v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ unsigned atom_dsm_add_u32(uint32_t a, unsigned v) {
@@ -388,7 +356,6 @@ __device__ unsigned long long g_sure_prof[16];
 #else
 #define SPROF(cls, ph, t0) do { } while (0)
 #endif
-constexpr int BPT = HB / NT;   // bins per thread when one CTA owns the whole histogram
 
 // Exact per-subband SURE (see the file comment).  One item = (component,
 // subband); a subband with n >= BIG_MIN is split over the nr = cluster-size
@@ -404,7 +371,6 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   unsigned* sbuf = skeys + CAP;
   __shared__ double red[3 * NWS + 2];
   __shared__ int redi[NWS];
-  __shared__ unsigned redu[NWS];
   // exchange slots (one per participating rank)
   __shared__ double x_seg[GMAX][3];          // segment totals: count, sum lower, sum upper
   __shared__ double x_ub[GMAX];
@@ -414,7 +380,6 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   __shared__ double x_fin[GMAX][4];          // compaction: sum below (x^2), above (x, x^2), count above
   __shared__ unsigned s_wpos;                // leader: next free slot of the window-key buffer
   __shared__ unsigned s_kmax;                // pass 1: largest key from 2^24 up
-  __shared__ __align__(8) uint64_t s_full[NSTG];   // streaming ring: one mbarrier per stage
 
   const int tid = threadIdx.x;
   const int G = (int)cluster_nctarank();
@@ -447,18 +412,9 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   const int ns = hi_i - lo_i;
   const int ks = comp * tab.nsub + s;
   const bool skip = keep_ll && s == tab.nsub - 1;   // LL kept: t = 0
-  // streaming ring past the histogram (overlaps the sort buffer and the merged
-  // bins, idle while streaming; the compaction's window keys land below it)
-  float4* ring = reinterpret_cast<float4*>(skeys + RING_OFF);
-  unsigned ru = 0u;
-  if (tid == 0) {
-    for (int i = 0; i < NSTG; ++i) tc::mbar_init(&s_full[i], 1u);
-    tc::fence_mbar_init();
-  }
-  __syncthreads();
 
   // ---------------- window search ----------------
-  const int pcls = n > CAP ? 0 : 1;
+  [[maybe_unused]] const int pcls = n > CAP ? 0 : 1;
   long long pt0 = clock64();
 #ifdef HYDE_SURE_PROF
   if (tid == 0) atomicAdd(&g_sure_prof[pcls * 8 + 3], 1ull);
@@ -491,11 +447,15 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         bl = klo;
         bh = khi;
       }
+#ifdef HYDE_SURE_PROF
+      const long long ph0 = clock64();
+      if (tid == 0) atomicAdd(&g_sure_prof[pcls * 8 + 5], 1ull);
+#endif
       for (int b = tid; b < HB + 2; b += NT) { hcnt[b] = 0u; hsum[b] = 0u; }
       if (tid == 0) s_kmax = 0u;
       __syncthreads();
       if (p1) {
-        stream_keys(x, ns, ring, s_full, ru, [&](unsigned k, int) {
+        stream_keys(x, ns, [&](unsigned k, int) {
           int b = (int)(k >> HS0) - (int)(KB0 >> HS0);
           b = b < 0 ? HB : b;
           if (b >= HB + 1) { b = HB + 1; atomicMax(&s_kmax, k); }
@@ -503,7 +463,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
           atomicAdd(hsum + b, fxsq(k));
         });
       } else {
-        stream_keys(x, ns, ring, s_full, ru, [&](unsigned k, int) {
+        stream_keys(x, ns, [&](unsigned k, int) {
           if (k >= bl && k <= bh) {
             const unsigned b = (k - kb) >> sh;
             atomicAdd(hcnt + b, 1u);
@@ -511,33 +471,47 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
           }
         });
       }
+#ifdef HYDE_SURE_PROF
+      __syncthreads();
+      if (tid == 0) atomicAdd(&g_sure_prof[pcls * 8 + 4], (unsigned long long)(clock64() - ph0));
+#endif
+      if (p1) {                              // catch-all counts and the largest key -> every rank
+        __syncthreads();
+        if (tid == 0) {
+          cx.xput_d(&x_v[0][0], rank * 5 + 0, (double)hcnt[HB]);
+          cx.xput_d(&x_v[0][0], rank * 5 + 1, (double)hcnt[HB + 1]);
+          cx.xput_d(&x_v[0][0], rank * 5 + 2, (double)s_kmax);
+        }
+      }
+#ifdef HYDE_SURE_PROF
+      const long long pb0 = clock64();
+#endif
       cx.sync();                             // histograms complete everywhere
-      // merge this rank's segment over the ranks (rank order) + the catch-alls
+#ifdef HYDE_SURE_PROF
+      if (tid == 0) atomicAdd(&g_sure_prof[pcls * 8 + 6], (unsigned long long)(clock64() - pb0));
+#endif
+      // merge this rank's segment over the ranks (rank order)
       if (nr > 1) {
         for (int b = tid; b < seg; b += NT) {
           const int gb = rank * seg + b;
+          unsigned cr[GMAX], qr[GMAX];
+#pragma unroll
+          for (int r = 0; r < GMAX; ++r)
+            if (r < nr) { cr[r] = ld_dsm_u32(cx.at(hcnt + gb, r)); qr[r] = ld_dsm_u32(cx.at(hsum + gb, r)); }
           unsigned c = 0u;
           unsigned long long q = 0ull;
           bool ov = false;
-          for (int r = 0; r < nr; ++r) {
-            const unsigned cr = ld_dsm_u32(cx.at(hcnt + gb, r));
-            c += cr;
-            q += ld_dsm_u32(cx.at(hsum + gb, r));
-            ov |= cr >= 65536u;
-          }
+#pragma unroll
+          for (int r = 0; r < GMAX; ++r)
+            if (r < nr) { c += cr[r]; q += qr[r]; ov |= cr[r] >= 65536u; }
           gcnt[b] = c;
           gsum[b] = ov ? ~0ull : q;
         }
       }
       double vcb = 0.0, vca = 0.0;
       unsigned vmax = 0u;
-      if (p1) {
-        for (int r = 0; r < nr; ++r) {
-          vcb += (double)(nr > 1 ? ld_dsm_u32(cx.at(hcnt + HB, r)) : hcnt[HB]);
-          vca += (double)(nr > 1 ? ld_dsm_u32(cx.at(hcnt + HB + 1, r)) : hcnt[HB + 1]);
-          vmax = max(vmax, nr > 1 ? ld_dsm_u32(cx.at(&s_kmax, r)) : s_kmax);
-        }
-      }
+      if (p1)
+        for (int r = 0; r < nr; ++r) { vcb += x_v[r][0]; vca += x_v[r][1]; vmax = max(vmax, (unsigned)x_v[r][2]); }
       __syncthreads();
       // bin i of the segment: count, value bounds, sum bounds
       auto binfo = [&](int i, double& m, double& lo2, double& hi2, double& q_l, double& q_h) {
@@ -553,7 +527,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         const unsigned e = lok >> 23;
         const unsigned long long q = nr > 1 ? gsum[i] : (c >= 65536u ? ~0ull : (unsigned long long)hsum[i]);
         if ((hik >> 23) == e && e > 0u && q != ~0ull) {
-          const double sc = ldexp(1.0, 2 * (int)e - 268);
+          const double sc = __longlong_as_double((long long)(2 * (int)e - 268 + 1023) << 52);   // 2^(2e-268)
           q_l = (double)q * sc;
           q_h = ((double)q + m) * sc;
         } else {
@@ -618,61 +592,73 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       }
       ubt = block_min_d(ubt, red);
       if (tid == 0) cx.xput_d(x_ub, rank, ubt);
+#ifdef HYDE_SURE_PROF
+      const long long pb1 = clock64();
+#endif
       cx.sync();
+#ifdef HYDE_SURE_PROF
+      if (tid == 0) atomicAdd(&g_sure_prof[pcls * 8 + 7], (unsigned long long)(clock64() - pb1));
+#endif
       double ub = dn;                        // k = 0: S_0 = n
       for (int r = 0; r < nr; ++r) ub = fmin(ub, x_ub[r]);
       const double thr = ub + tol;
+      // this rank's first / last surviving bin with the prefix (count, sums) at
+      // the first and the count past the last: one exchange gives the window
+      // and its key count
       int fst = INT_MAX, lst = -2;
-      double mwin_t = 0.0;
-      {
-        double c = sc0 + off[0], p_l = sl0 + off[1];
-#pragma unroll 1
-        for (int i = i0; i < i0 + bpt; ++i) {
-          double m, lo2, hi2, q_l, q_h;
-          binfo(i, m, lo2, hi2, q_l, q_h);
-          if (m > 0.0 && dn - 2.0 * (c + m) + p_l + (dn - c) * lo2 <= thr) {
-            fst = min(fst, rank * seg + i);
-            lst = max(lst, rank * seg + i);
-          }
-          c += m; p_l += q_l;
-        }
-      }
-      fst = block_min_i(fst, redi);
-      lst = -block_min_i(-lst, redi);
-      if (tid == 0) { cx.xput_u((unsigned*)x_first, rank, (unsigned)fst); cx.xput_u((unsigned*)x_last, rank, (unsigned)lst); }
-      cx.sync();
-      int gf = INT_MAX, gl = -2;
-      for (int r = 0; r < nr; ++r) { gf = min(gf, x_first[r]); gl = max(gl, x_last[r]); }
-      if (p1 && lb_lo <= thr) gf = -1;
-      if (p1 && lb_hi <= thr) { gl = HB; if (gf == INT_MAX) gf = HB; }
-      if (p1 && gf == -1 && gl == -2) gl = -1;
-      // window count in this segment and, for the owner of `gf`, the prefix there
+      double f_c = 0.0, f_l = 0.0, f_h = 0.0, l_c = 0.0;
       {
         double c = sc0 + off[0], p_l = sl0 + off[1], p_h = sh0 + off[2];
 #pragma unroll 1
         for (int i = i0; i < i0 + bpt; ++i) {
           double m, lo2, hi2, q_l, q_h;
           binfo(i, m, lo2, hi2, q_l, q_h);
-          const int b = rank * seg + i;
-          if (b == gf) { x_win[rank][1] = c; x_win[rank][2] = p_l; x_win[rank][3] = p_h; }
-          if (b >= gf && b <= gl) mwin_t += m;
+          if (m > 0.0 && dn - 2.0 * (c + m) + p_l + (dn - c) * lo2 <= thr) {
+            if (fst == INT_MAX) { fst = rank * seg + i; f_c = c; f_l = p_l; f_h = p_h; }
+            lst = rank * seg + i;
+            l_c = c + m;
+          }
           c += m; p_l += q_l; p_h += q_h;
         }
       }
-      const double mwin = block_sum_d(mwin_t, red);   // contains barriers: x_win[rank][1..3] visible
-      const bool own_first = gf >= rank * seg && gf < (rank + 1) * seg;
-      if (tid == 0) {
-        cx.xput_d(&x_win[0][0], rank * 4 + 0, mwin);
-        if (own_first) {
-          const double a1 = x_win[rank][1], a2 = x_win[rank][2], a3 = x_win[rank][3];
-          cx.xput_d(&x_win[0][0], rank * 4 + 1, a1);
-          cx.xput_d(&x_win[0][0], rank * 4 + 2, a2);
-          cx.xput_d(&x_win[0][0], rank * 4 + 3, a3);
+      {
+        const int bf = block_min_i(fst, redi);
+        const int bl_ = -block_min_i(-lst, redi);
+        if (fst == bf && fst != INT_MAX) { x_win[rank][1] = f_c; x_win[rank][2] = f_l; x_win[rank][3] = f_h; }
+        if (lst == bl_ && lst != -2) x_win[rank][0] = l_c;
+        __syncthreads();
+        if (tid == 0) {
+          cx.xput_u((unsigned*)x_first, rank, (unsigned)bf);
+          cx.xput_u((unsigned*)x_last, rank, (unsigned)bl_);
+          if (bf != INT_MAX) {
+            const double a0 = x_win[rank][0], a1 = x_win[rank][1], a2 = x_win[rank][2], a3 = x_win[rank][3];
+            cx.xput_d(&x_win[0][0], rank * 4 + 0, a0);
+            cx.xput_d(&x_win[0][0], rank * 4 + 1, a1);
+            cx.xput_d(&x_win[0][0], rank * 4 + 2, a2);
+            cx.xput_d(&x_win[0][0], rank * 4 + 3, a3);
+          }
         }
       }
       cx.sync();
-      double Mw = 0.0;
-      for (int r = 0; r < nr; ++r) Mw += x_win[r][0];
+      int gf = INT_MAX, gl = -2, of = -1, ol = -1;
+      for (int r = 0; r < nr; ++r) {
+        if (x_first[r] < gf) { gf = x_first[r]; of = r; }
+        if (x_last[r] > gl) { gl = x_last[r]; ol = r; }
+      }
+      // window count over the binned range: count past the last minus count at the first
+      double Mw = (of >= 0) ? x_win[ol][0] - x_win[of][1] : 0.0;
+      double fcb = of >= 0 ? x_win[of][1] : 0.0, fpl = of >= 0 ? x_win[of][2] : 0.0, fph = of >= 0 ? x_win[of][3] : 0.0;
+      if (p1 && lb_lo <= thr) {              // the low catch-all joins the window
+        if (gf == INT_MAX) { gl = -1; Mw = 0.0; }
+        else Mw += fcb - vcb;               // binned keys below the first surviving bin
+        gf = -1;
+      }
+      if (p1 && lb_hi <= thr) {              // the high catch-all joins the window
+        if (gf == INT_MAX) { gf = HB; Mw = 0.0; fcb = allc; fpl = alll; fph = allh; }
+        else if (gl >= 0) Mw += allc - x_win[ol][0];   // binned keys past the last surviving bin
+        else Mw += allc - vcb;
+        gl = HB;
+      }
       const unsigned oklo = klo, okhi = khi;
       if (gf == INT_MAX) {                   // nothing survives: t = 0
         empty = true;
@@ -680,11 +666,10 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       }
       // window keys and the prefix at its start
       if (gf == -1) { klo = 0u; cb = 0.0; pl = ph = 0.0; Mw += vcb; }
-      else if (gf == HB) { klo = KE0 + 1u; cb = allc; pl = alll; ph = allh; }
+      else if (gf == HB) { klo = KE0 + 1u; cb = fcb; pl = fpl; ph = fph; }
       else {
-        const int ow = gf / seg;
         klo = max(kb + ((unsigned)gf << sh), bl);
-        cb = x_win[ow][1]; pl = x_win[ow][2]; ph = x_win[ow][3];
+        cb = fcb; pl = fpl; ph = fph;
       }
       if (gl == HB) { khi = vmax; Mw += vca; }
       else if (gl == -1) { khi = KB0 - 1u; }
@@ -719,7 +704,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
     const bool wr = !closed;
     const uint32_t wpos = cx.at(&s_wpos, 0);
     const uint32_t kbase = cx.at(skeys, 0);
-    stream_keys(x, ns, ring, s_full, ru, [&](unsigned k, int j) {
+    stream_keys(x, ns, [&](unsigned k, int j) {
       if (__builtin_expect(k < klo, 1)) {
         const double a = k < 0x800000u ? 0.0 : __longlong_as_double(((long long)k << 29) + (896LL << 52));
         if (j & 1) qb1 = fma(a, a, qb1); else qb0 = fma(a, a, qb0);
@@ -908,9 +893,16 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // CTAs per big subband: as many as keep about two waves of CTAs busy
+  // CTAs per big subband: GMAX-CTA clusters while the launch has few big
+  // subbands (latency: the hot path's 4-16 components), fewer when there are
+  // enough subbands to fill the GPU (throughput; each extra CTA per subband
+  // repeats the per-pass analysis).  HYDE_SURE_G overrides (experiments).
   int G = GMAX;
-  while (G > 1 && (long long)count * tab.nbig * G > 2LL * sms) G >>= 1;
+  while (G > 1 && (long long)count * tab.nbig * G > 4LL * sms) G >>= 1;
+  if (const char* ev = getenv("HYDE_SURE_G")) {
+    const int g = atoi(ev);
+    if (g == 1 || g == 2 || g == 4 || g == 8) G = g;
+  }
   const int nclusters = count * tab.nbig + (count * tab.nsmall + G - 1) / G;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nclusters * G);

@@ -41,4 +41,4 @@ for c, name in ((0, "n > 8192"), (1, "n <= 8192")):
     ctas = max(v[c * 8 + 3], 1)
     tot = sum(v[c * 8 + p] for p in range(3))
     print(f"{name:10s} CTAs {v[c*8+3]:6d}  window {v[c*8]/ctas:10.0f}  compaction {v[c*8+1]/ctas:10.0f}  "
-          f"sort+eval {v[c*8+2]/ctas:10.0f} cycles/CTA   (share of all CTA-cycles {tot / max(1, sum(v[0:3]) + sum(v[8:11])):.2f})")
+          f"sort+eval {v[c*8+2]/ctas:10.0f} cycles/CTA; hist streaming {v[c*8+4]/ctas:10.0f}, passes {v[c*8+5]/ctas:.2f}, wait after hist {v[c*8+6]/ctas:.0f}, wait at ub exchange {v[c*8+7]/ctas:.0f}   (share of all CTA-cycles {tot / max(1, sum(v[0:3]) + sum(v[8:11])):.2f})")
