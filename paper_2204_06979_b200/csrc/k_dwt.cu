@@ -65,13 +65,27 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
 #pragma unroll
     for (int u = 0; u < NCI; ++u) gcol[u] = min(wrap(2 * j0 + l + 32 * u, Wd), w_in - 1);   // odd extent: duplicate the last column
     float v[NRI][NCI];
+    // interior tile (no periodic wrap, no odd-extent padding): plain strided
+    // addressing; boundary tiles take the general path
+    const bool interior = 2 * i0 + NR <= h_in && 2 * j0 + NC <= w_in;
+    if (interior) {
+      const float* base = x + (long long)(2 * i0 + w) * w_in + 2 * j0 + l;
 #pragma unroll
-    for (int ri = 0; ri < NRI; ++ri) {
-      const int r = w + 8 * ri;
-      const float* rowp = x + (long long)min(wrap(2 * i0 + r, H), h_in - 1) * w_in;
+      for (int ri = 0; ri < NRI; ++ri) {
+        const int r = w + 8 * ri;
 #pragma unroll
-      for (int u = 0; u < NCI; ++u)
-        v[ri][u] = (r < NR && l + 32 * u < NC) ? __ldg(rowp + gcol[u]) : 0.f;
+        for (int u = 0; u < NCI; ++u)
+          v[ri][u] = (r < NR && l + 32 * u < NC) ? __ldg(base + (long long)(8 * ri) * w_in + 32 * u) : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int ri = 0; ri < NRI; ++ri) {
+        const int r = w + 8 * ri;
+        const float* rowp = x + (long long)min(wrap(2 * i0 + r, H), h_in - 1) * w_in;
+#pragma unroll
+        for (int u = 0; u < NCI; ++u)
+          v[ri][u] = (r < NR && l + 32 * u < NC) ? __ldg(rowp + gcol[u]) : 0.f;
+      }
     }
 #pragma unroll
     for (int ri = 0; ri < NRI; ++ri) {
