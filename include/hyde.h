@@ -260,7 +260,11 @@ hyde_status hyde_debug_eig_clocks(long long* out32);
  * HYDE_SURE_PROF=1 only; returns 0 and zeros otherwise, 1 when filled):
  * out16[c*8 + p] = SM cycles summed over CTAs, class c (0: subbands longer than
  * the 8192-key window capacity, 1: shorter), phase p (0 window search,
- * 1 compaction, 2 sort + exact evaluation, 3 = number of CTAs).  Synchronizes. */
+ * 1 compaction, 2 sort + exact evaluation, 3 = number of CTAs, 4 histogram
+ * streaming, 5 passes, 6-7 cluster-barrier waits); out16[16..20]: largest /
+ * summed window size and item count of the long subbands, longest sort +
+ * evaluation (long, short subbands); out16[32 + c*8 + p]: the longest CTA of
+ * class c in phase p.  Copies 48 values.  Synchronizes. */
 int hyde_debug_sure_prof(unsigned long long* out16);
 
 /* CTAs per K2 eigensolver cluster on the current device: 16 (non-portable

@@ -351,8 +351,9 @@ __device__ __forceinline__ unsigned atom_dsm_add_u32(uint32_t a, unsigned v) {
 #ifdef HYDE_SURE_PROF
 // [class*8 + phase] cycles summed over CTAs (class 0: n > CAP, 1: n <= CAP;
 // phase 0 window search, 1 compaction, 2 sort + evaluation, 3 CTAs)
-__device__ unsigned long long g_sure_prof[16];
-#define SPROF(cls, ph, t0) do { if (threadIdx.x == 0) atomicAdd(&g_sure_prof[(cls) * 8 + (ph)], (unsigned long long)(clock64() - (t0))); } while (0)
+__device__ unsigned long long g_sure_prof[48];
+#define SPROF(cls, ph, t0) do { if (threadIdx.x == 0) { const unsigned long long d_ = (unsigned long long)(clock64() - (t0)); \
+    atomicAdd(&g_sure_prof[(cls) * 8 + (ph)], d_); atomicMax(&g_sure_prof[32 + (cls) * 8 + (ph)], d_); } } while (0)
 #else
 #define SPROF(cls, ph, t0) do { } while (0)
 #endif
@@ -382,6 +383,12 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
   __shared__ unsigned s_kmax;                // pass 1: largest key from 2^24 up
 
   const int tid = threadIdx.x;
+#ifdef HYDE_SURE_PROF
+  unsigned long long gt0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+  const long long life0 = clock64();
+  if (tid == 0) { atomicMin(&g_sure_prof[21], gt0); atomicMax(&g_sure_prof[22], gt0); }
+#endif
   const int G = (int)cluster_nctarank();
   const int cid = blockIdx.x / G;
   const int myrank = G > 1 ? (int)tc::cluster_ctarank() : 0;
@@ -714,9 +721,15 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         q2 = fma(a, a, q2);
         ++cai;
       } else if (wr) {
-        unsigned p;
-        if (nr == 1) p = atomicAdd(&s_wpos, 1u);
-        else p = atom_dsm_add_u32(wpos, 1u);
+        // one slot allocation per warp-instruction: the lanes holding a
+        // window key in this step share one (remote) atomic
+        const unsigned am = __activemask();
+        const int lane = tid & 31;
+        const int lead = __ffs(am) - 1;
+        unsigned base = 0u;
+        if (lane == lead) base = nr == 1 ? atomicAdd(&s_wpos, (unsigned)__popc(am)) : atom_dsm_add_u32(wpos, (unsigned)__popc(am));
+        base = __shfl_sync(am, base, lead);
+        const unsigned p = base + (unsigned)__popc(am & ((1u << lane) - 1u));
         if (p < (unsigned)CAP) {
           if (nr == 1) skeys[sw((int)p)] = k; else st_dsm_u32(kbase + 4u * (unsigned)sw((int)p), k);
         }
@@ -817,6 +830,22 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
     double e = ew + (Q2 - 2.0 * t * Q1 + cabove * t * t);
     if (kbest == 0) e += P0;
     SPROF(pcls, 2, pt0);
+#ifdef HYDE_SURE_PROF
+    {
+      unsigned long long gt1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+      atomicMax(&g_sure_prof[23], gt1);
+      atomicMax(&g_sure_prof[24], (unsigned long long)(clock64() - life0));
+    }
+    if (pcls == 0) {
+      atomicMax(&g_sure_prof[16], (unsigned long long)mc);
+      atomicAdd(&g_sure_prof[17], (unsigned long long)mc);
+      atomicAdd(&g_sure_prof[18], 1ull);
+      atomicMax(&g_sure_prof[19], (unsigned long long)(clock64() - pt0));
+    } else {
+      atomicMax(&g_sure_prof[20], (unsigned long long)(clock64() - pt0));
+    }
+#endif
     kstar[ks] = (int)kbest;
     tstar[ks] = __uint_as_float(tkey);
     e_sub[ks] = e;
@@ -923,12 +952,13 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
 int sure_prof_read(unsigned long long* out16) {
 #ifdef HYDE_SURE_PROF
   cudaDeviceSynchronize();
-  if (cudaMemcpyFromSymbol(out16, g_sure_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) return -1;
-  unsigned long long z[16] = {0};
+  if (cudaMemcpyFromSymbol(out16, g_sure_prof, 48 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  unsigned long long z[48] = {0};
+  z[21] = ~0ull;
   cudaMemcpyToSymbol(g_sure_prof, z, sizeof(z));
   return 1;
 #else
-  for (int i = 0; i < 16; ++i) out16[i] = 0ull;
+  for (int i = 0; i < 48; ++i) out16[i] = 0ull;
   return 0;
 #endif
 }
