@@ -721,15 +721,9 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         q2 = fma(a, a, q2);
         ++cai;
       } else if (wr) {
-        // one slot allocation per warp-instruction: the lanes holding a
-        // window key in this step share one (remote) atomic
-        const unsigned am = __activemask();
-        const int lane = tid & 31;
-        const int lead = __ffs(am) - 1;
-        unsigned base = 0u;
-        if (lane == lead) base = nr == 1 ? atomicAdd(&s_wpos, (unsigned)__popc(am)) : atom_dsm_add_u32(wpos, (unsigned)__popc(am));
-        base = __shfl_sync(am, base, lead);
-        const unsigned p = base + (unsigned)__popc(am & ((1u << lane) - 1u));
+        unsigned p;
+        if (nr == 1) p = atomicAdd(&s_wpos, 1u);
+        else p = atom_dsm_add_u32(wpos, 1u);
         if (p < (unsigned)CAP) {
           if (nr == 1) skeys[sw((int)p)] = k; else st_dsm_u32(kbase + 4u * (unsigned)sw((int)p), k);
         }
