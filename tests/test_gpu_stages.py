@@ -298,3 +298,35 @@ def test_wavelet_shrink_matches_oracle(hy, shape):
     g = dev(x)
     same = hy.stages.wavelet_shrink(g, lv, out=g, stats=False)
     assert np.array_equal(same.cpu().numpy(), out)
+
+
+def test_sure_dense_window_refinement(hy):
+    """Subbands whose first-pass window exceeds the 8192-key capacity (a dense cluster
+    of magnitudes where SURE is flat) go through the finer re-binning passes and still
+    give the oracle's exact index; a subband with only a few distinct values (runs)
+    takes the closed form."""
+    r, c, lv = 1024, 1024, 5
+    nc = O.coeff_count(r, c, lv)
+    rng = np.random.default_rng(8)
+    rows = []
+    a = rng.standard_normal(nc)
+    a[:nc // 3] = rng.uniform(3.4, 3.7, nc // 3) * np.sign(rng.standard_normal(nc // 3))
+    rows.append(a)
+    b = rng.standard_normal(nc)
+    idx = rng.random(nc) < 0.15
+    b[idx] = 2.5 + 1e-3 * rng.standard_normal(int(idx.sum()))
+    rows.append(b)
+    d = np.round(rng.standard_normal(nc) * 2) / 2          # runs of equal magnitudes
+    rows.append(d)
+    co = np.stack(rows).astype(np.float32)
+    ks, ts, ep = hy.stages.sure(dev(co), r, c, lv)
+    ks, ts, ep = ks.cpu().numpy(), ts.cpu().numpy(), ep.cpu().numpy()
+    for i in range(co.shape[0]):
+        res, offs = _oracle_sure_on(co[i], r, c, lv)
+        e_ref = 0.0
+        for j, sr in enumerate(res):
+            x = co[i, offs[j]:offs[j + 1]].astype(np.float64)
+            if sr.margin > 1e-9 * (x.size + float(np.sum(x ** 2))):
+                assert ks[i, j] == sr.k and ts[i, j] == np.float32(sr.t), (i, j, ks[i, j], sr.k)
+            e_ref += float(np.sum(O.soft_threshold(x, float(ts[i, j])) ** 2))
+        assert abs(ep[i] - e_ref) <= 1e-6 * max(1.0, e_ref)
