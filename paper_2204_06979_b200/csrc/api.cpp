@@ -108,6 +108,7 @@ struct hyde_ctx {
   std::vector<cudaEvent_t> lane_ev;
   cudaEvent_t ev_batch = nullptr;
   RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
+  cudaEvent_t ev_rank = nullptr; // recorded after the per-chunk D2H copy of the rank state
   // stage profiling
   int prof = 0;
   struct Rec { int stage; int launches; cudaEvent_t a, b; };
@@ -263,7 +264,8 @@ static cudaError_t dwt_forward(const Layout& L, char* ws, const float* E, long l
 // inverse DWT of `count` coefficient sets; when tstar != NULL each subband is
 // soft-thresholded with its t* as it is loaded (K5 -> K6a fusion)
 static cudaError_t dwt_inverse(const Layout& L, char* ws, const float* Cin, float* Eout, long long ldE,
-                               int count, const FilterBank& fb, const float* tstar, cudaStream_t st) {
+                               int count, const FilterBank& fb, const float* tstar, cudaStream_t st,
+                               const RankState* rs = nullptr, int k0 = 0) {
   float* S[2] = {(float*)(ws + L.S1), (float*)(ws + L.S2)};
   long long sstr[2] = {(long long)L.s1_img, (long long)L.s2_img};
   const long long nc = L.plan.n_coeffs;
@@ -274,7 +276,7 @@ static cudaError_t dwt_inverse(const Layout& L, char* ws, const float* Cin, floa
     long long out_str = l == 0 ? ldE : sstr[(l - 1) & 1];
     const int s_ll = (l == L.levels - 1) ? 3 * L.levels : -1;   // only LL_L comes from K5
     cudaError_t e = launch_idwt_level(llin, ll_str, Cin + L.plan.sub_off[l], nc, L.plan.lv[l].h_in,
-                                      L.plan.lv[l].w_in, out, out_str, count, fb, tstar, L.nsub, 3 * l, s_ll, st);
+                                      L.plan.lv[l].w_in, out, out_str, count, fb, tstar, L.nsub, 3 * l, s_ll, rs, k0, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -357,6 +359,7 @@ hyde_status hyde_destroy(hyde_handle h) {
     for (auto st : h->lane_st) cudaStreamDestroy(st);
     for (auto e : h->lane_ev) cudaEventDestroy(e);
     if (h->ev_batch) cudaEventDestroy(h->ev_batch);
+    if (h->ev_rank) cudaEventDestroy(h->ev_rank);
     if (h->rs_host) cudaFreeHost(h->rs_host);
     for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
@@ -478,30 +481,35 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
       CK(launch_rank_decide((double*)(ws + L.esub), L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs,
                             (double*)(ws + L.epost), st));
       CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
+      if (!h->ev_rank) CK(cudaEventCreateWithFlags(&h->ev_rank, cudaEventDisableTiming));
+      CK(cudaEventRecord(h->ev_rank, st));
       sg.end();
     }
-    CK(cudaStreamSynchronize(st));
+    // The inverse DWT of the kept components and the reconstruction are
+    // enqueued BEFORE the host reads the rank: both read r* from the device
+    // rank state (no-ops while no failing component has been seen), so the GPU
+    // never idles while the host round-trips the 16-byte decision.
+    {
+      Stage sg(h, HYDE_STAGE_IDWT, levels, st);
+      CK(dwt_inverse(L, ws, C, E, L.ldE, cnt, fb, (const float*)(ws + L.tstar), st, rs, k0));
+      sg.end();
+    }
+    {
+      Stage sg(h, HYDE_STAGE_RECON, (k0 + cnt + 7) / 8, st);
+      CK(launch_reconstruct(h->ebuf, L.ldE, n, B, U, L.ldwu, k0 + cnt, out, st, rs));
+      sg.end();
+    }
+    CK(cudaEventSynchronize(h->ev_rank));
     ++chunks;
     comps += cnt;
     const RankState r = *h->rs_host;
     if (r.nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
     if (r.sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
-    const int kept = r.found ? (r.rank - k0) : cnt;
-    if (kept > 0) {
-      Stage sg(h, HYDE_STAGE_IDWT, levels, st);
-      CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, (const float*)(ws + L.tstar), st));
-      sg.end();
-    }
     if (r.found) {
       rank = r.rank;
       break;
     }
     k0 += cnt;
-  }
-  {
-    Stage sg(h, HYDE_STAGE_RECON, (rank + 7) / 8, st);
-    CK(launch_reconstruct(h->ebuf, L.ldE, n, B, U, L.ldwu, rank, out, st));
-    sg.end();
   }
   if (info) {
     memset(info, 0, sizeof(*info));

@@ -82,7 +82,7 @@ cudaError_t launch_dwt_level(const float* in, long long in_stride, int h_in, int
 cudaError_t launch_idwt_level(const float* ll, long long ll_stride, const float* sub,
                               long long sub_stride, int h_out, int w_out, float* out,
                               long long out_stride, int count, const FilterBank& fb,
-                              const float* tstar, int nsub, int s_lh, int s_ll, cudaStream_t st);
+                              const float* tstar, int nsub, int s_lh, int s_ll, const RankState* rs, int k0, cudaStream_t st);
 cudaError_t launch_soft_threshold(float* coeffs, long long cstride, const DwtPlan& plan, int count, const float* tstar,
                                   cudaStream_t st);
 // surv: scratch of count * cstride keys (the survivor lists of the clustered subbands)
@@ -93,4 +93,4 @@ int sure_prof_read(unsigned long long* out16);   // K5 phase cycles (HYDE_SURE_P
 cudaError_t launch_rank_decide(const double* e_sub, int nsub, int count, int k0, double n_coeffs,
                                int bands, RankState* rs, double* e_post, cudaStream_t st);
 cudaError_t launch_reconstruct(const float* E, long long ldE, long long n, int B, const float* U,
-                               int ldu, int rank, float* out, cudaStream_t st);
+                               int ldu, int rank, float* out, cudaStream_t st, const RankState* rs = nullptr);

@@ -160,6 +160,8 @@ __device__ __forceinline__ float soft(float v, float t) {
 struct SoftSpec {
   const float* tstar;
   int nsub, s_lh, s_ll;
+  const RankState* rs;   // non-NULL: images z >= kept (rank rule, decided on the device) are skipped
+  int k0, cnt;           // first component of the chunk, components in it
 };
 
 constexpr int II = 4;    // inverse axis-0 pass: output rows per thread (even)
@@ -180,6 +182,10 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
   constexpr int W1 = IJ / 2 + HT - 1;   // axis-1 window
   __shared__ float t_ll[CR][CC + 1], t_hl[CR][CC + 1], t_lh[CR][CC + 1], t_hh[CR][CC + 1];
   __shared__ float lo1[IR][CC + 1], hi1[IR][CC + 1];
+  if (sp.rs) {
+    const int kept = sp.rs->found ? sp.rs->rank - sp.k0 : sp.cnt;
+    if ((int)blockIdx.z >= kept) return;
+  }
   const int H = h_out + (h_out & 1), Wd = w_out + (w_out & 1);
   const int hs = H >> 1, ws = Wd >> 1;
   const int r0 = blockIdx.y * IR, c0 = blockIdx.x * IC;
@@ -308,10 +314,11 @@ cudaError_t launch_dwt_level(const float* in, long long in_stride, int h_in, int
 cudaError_t launch_idwt_level(const float* ll, long long ll_stride, const float* sub,
                               long long sub_stride, int h_out, int w_out, float* out,
                               long long out_stride, int count, const FilterBank& fb,
-                              const float* tstar, int nsub, int s_lh, int s_ll, cudaStream_t st) {
+                              const float* tstar, int nsub, int s_lh, int s_ll, const RankState* rs, int k0,
+                              cudaStream_t st) {
   const int H = h_out + (h_out & 1), Wd = w_out + (w_out & 1);
   dim3 grid((Wd + IC - 1) / IC, (H + IR - 1) / IR, count);
-  const SoftSpec sp{tstar, nsub, s_lh, s_ll};
+  const SoftSpec sp{tstar, nsub, s_lh, s_ll, rs, k0, count};
   switch (fb.taps) {
     case 2: dwt_inv_kernel<2><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;
     case 8: dwt_inv_kernel<8><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;

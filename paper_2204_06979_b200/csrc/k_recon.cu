@@ -14,7 +14,13 @@ constexpr int RK = 8;  // components held in registers per pass
 template <int PIX, bool VEC>
 __global__ void __launch_bounds__(256) recon_kernel(const float* __restrict__ E, long long ldE, long long n,
                                                     int B, const float* __restrict__ U, int ldu, int k0,
-                                                    int kcount, int accumulate, float* __restrict__ out) {
+                                                    int kcount, int accumulate, float* __restrict__ out,
+                                                    const RankState* __restrict__ rs) {
+  if (rs) {   // rank decided on the device: nothing until it is found, then r* - k0 components
+    if (!rs->found) return;
+    kcount = min(kcount, rs->rank - k0);
+    if (kcount <= 0) return;
+  }
   extern __shared__ float Us[];  // B x RK
   for (int i = threadIdx.x; i < B * RK; i += blockDim.x) {
     int b = i / RK, k = i % RK;
@@ -69,8 +75,10 @@ __global__ void __launch_bounds__(256) recon_kernel(const float* __restrict__ E,
 
 }  // namespace
 
+// rs == NULL: rank is the component count.  rs != NULL: rank is an upper bound
+// and the kernels read r* from the device rank state (no-ops until it is found).
 cudaError_t launch_reconstruct(const float* E, long long ldE, long long n, int B, const float* U,
-                               int ldu, int rank, float* out, cudaStream_t st) {
+                               int ldu, int rank, float* out, cudaStream_t st, const RankState* rs) {
   constexpr int PIX = 4;
   const long long threads = (n + PIX - 1) / PIX;
   const unsigned blocks = (unsigned)((threads + 255) / 256);
@@ -80,9 +88,9 @@ cudaError_t launch_reconstruct(const float* E, long long ldE, long long n, int B
     const int kc = rank - k0 < RK ? rank - k0 : RK;
     const int acc = k0 > 0;
     if (vec)
-      recon_kernel<PIX, true><<<blocks, 256, smem, st>>>(E, ldE, n, B, U, ldu, k0, kc, acc, out);
+      recon_kernel<PIX, true><<<blocks, 256, smem, st>>>(E, ldE, n, B, U, ldu, k0, kc, acc, out, rs);
     else
-      recon_kernel<PIX, false><<<blocks, 256, smem, st>>>(E, ldE, n, B, U, ldu, k0, kc, acc, out);
+      recon_kernel<PIX, false><<<blocks, 256, smem, st>>>(E, ldE, n, B, U, ldu, k0, kc, acc, out, rs);
   }
   return cudaGetLastError();
 }
