@@ -472,14 +472,14 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
     }
     {
       Stage sg(h, HYDE_STAGE_SURE, 1, st);
+      // the rank decision of the chunk is made by the last SURE subband to finish
       CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
-                     (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, (unsigned*)(ws + L.surv), st));
+                     (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, (unsigned*)(ws + L.surv), st, k0,
+                     (double)L.plan.n_coeffs, B, (double*)(ws + L.epost)));
       sg.end();
     }
     {
-      Stage sg(h, HYDE_STAGE_RANK, 1, st);
-      CK(launch_rank_decide((double*)(ws + L.esub), L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs,
-                            (double*)(ws + L.epost), st));
+      Stage sg(h, HYDE_STAGE_RANK, 0, st);
       CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
       if (!h->ev_rank) CK(cudaEventCreateWithFlags(&h->ev_rank, cudaEventDisableTiming));
       CK(cudaEventRecord(h->ev_rank, st));

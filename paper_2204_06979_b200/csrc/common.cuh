@@ -43,6 +43,7 @@ struct RankState {
   int rank;         // r* once found (else running count of passing components)
   int nonfinite;    // non-finite input flag (set by the Gram kernel)
   int sure_overflow;// SURE survivor set exceeded its capacity (method failure)
+  unsigned sure_done; // subbands finished in the current K5 launch (the last one decides the rank)
 };
 
 #define HYDE_CUDA_OK(expr)                                   \
@@ -88,7 +89,8 @@ cudaError_t launch_soft_threshold(float* coeffs, long long cstride, const DwtPla
 // surv: scratch of count * cstride keys (the survivor lists of the clustered subbands)
 cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, int count,
                         int keep_ll, int* kstar, float* tstar, double* e_sub,
-                        RankState* rs, unsigned* surv, cudaStream_t st);
+                        RankState* rs, unsigned* surv, cudaStream_t st,
+                        int k0 = 0, double n_coeffs = 0.0, int bands = 0, double* e_post = nullptr);
 int sure_prof_read(unsigned long long* out16);   // K5 phase cycles (HYDE_SURE_PROF builds), 0 otherwise
 cudaError_t launch_rank_decide(const double* e_sub, int nsub, int count, int k0, double n_coeffs,
                                int bands, RankState* rs, double* e_post, cudaStream_t st);

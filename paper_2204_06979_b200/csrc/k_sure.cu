@@ -318,6 +318,30 @@ __device__ __forceinline__ int block_min_i(int v, int* red) {
   return r;
 }
 
+// E_post per component (sum over its subbands, fixed order) and the
+// first-failure rank rule: walk k = k0, k0+1, ...; the first component with
+// E_post <= N_c stops, r* = max(1, k); r* = bands if none fails.
+__device__ void rank_decide_one(const double* e_sub, int nsub, int count, int k0, double n_coeffs, int bands,
+                                RankState* rs, double* e_post) {
+  for (int k = 0; k < count; ++k) {
+    double e = 0.0;
+    for (int s = 0; s < nsub; ++s) e += __ldcg(e_sub + k * nsub + s);
+    e_post[k0 + k] = e;
+    if (!rs->found) {
+      if (e <= n_coeffs) {
+        rs->found = 1;
+        rs->rank = max(1, k0 + k);
+      } else {
+        rs->rank = k0 + k + 1;
+      }
+    }
+  }
+  if (!rs->found && k0 + count >= bands) {
+    rs->found = 1;
+    rs->rank = bands;
+  }
+}
+
 // Per-item cluster context: `nr` CTAs (cluster ranks 0..nr-1, or this CTA
 // alone) work on one subband; xput() writes a value into slot `slot` of the
 // same __shared__ array in every participating CTA.
@@ -363,7 +387,8 @@ __device__ unsigned long long g_sure_prof[48];
 // CTAs of a cluster (slices of n/nr), smaller ones take one CTA each.
 __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ coeffs, long long cstride, SubTable tab,
                                                      int count, int keep_ll, int* kstar, float* tstar, double* e_sub,
-                                                     RankState* rs) {
+                                                     RankState* rs, int k0, double n_coeffs, int bands,
+                                                     double* e_post) {
   extern __shared__ __align__(16) unsigned char smraw[];
   // union: histogram (HB counts | HB fixed-point sums) | window keys + sort buffer
   unsigned* hcnt = reinterpret_cast<unsigned*>(smraw);
@@ -843,6 +868,17 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
     kstar[ks] = (int)kbest;
     tstar[ks] = __uint_as_float(tkey);
     e_sub[ks] = e;
+    if (e_post) {
+      // the last subband to finish makes the rank decision of the chunk (the
+      // first-failure rule): no separate launch
+      __threadfence();
+      const unsigned prev = atomicAdd(&rs->sure_done, 1u);
+      if (prev == (unsigned)(count * tab.nsub) - 1u) {
+        __threadfence();
+        rank_decide_one(e_sub, tab.nsub, count, k0, n_coeffs, bands, rs, e_post);
+        rs->sure_done = 0u;
+      }
+    }
   }
 }
 
@@ -863,23 +899,7 @@ __global__ void soft_kernel(float* coeffs, long long cstride, SubTable tab, cons
 __global__ void rank_decide_kernel(const double* __restrict__ e_sub, int nsub, int count, int k0, double n_coeffs,
                                    int bands, RankState* rs, double* e_post) {
   if (threadIdx.x != 0) return;
-  for (int k = 0; k < count; ++k) {
-    double e = 0.0;
-    for (int s = 0; s < nsub; ++s) e += e_sub[k * nsub + s];
-    e_post[k0 + k] = e;
-    if (!rs->found) {
-      if (e <= n_coeffs) {
-        rs->found = 1;
-        rs->rank = max(1, k0 + k);
-      } else {
-        rs->rank = k0 + k + 1;
-      }
-    }
-  }
-  if (!rs->found && k0 + count >= bands) {
-    rs->found = 1;
-    rs->rank = bands;
-  }
+  rank_decide_one(e_sub, nsub, count, k0, n_coeffs, bands, rs, e_post);
 }
 
 SubTable make_table(const DwtPlan& plan) {
@@ -908,7 +928,8 @@ SubTable make_table(const DwtPlan& plan) {
 }  // namespace
 
 cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, int count, int keep_ll, int* kstar,
-                        float* tstar, double* e_sub, RankState* rs, unsigned* surv, cudaStream_t st) {
+                        float* tstar, double* e_sub, RankState* rs, unsigned* surv, cudaStream_t st, int k0,
+                        double n_coeffs, int bands, double* e_post) {
   (void)surv;
   const SubTable tab = make_table(plan);
   cudaError_t e = cudaFuncSetAttribute(sure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_DYN);
@@ -940,7 +961,7 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, sure_kernel, (const float*)coeffs, cstride, tab, count, keep_ll, kstar, tstar, e_sub,
-                            rs);
+                            rs, k0, n_coeffs, bands, e_post);
 }
 
 int sure_prof_read(unsigned long long* out16) {
