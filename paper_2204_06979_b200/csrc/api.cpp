@@ -92,7 +92,8 @@ struct hyde_ctx {
   size_t ws_cap = 0;
   float* ebuf = nullptr;
   size_t ebuf_cap = 0;   // bytes
-  RankState* rs_host = nullptr;
+  RankState* rs_host = nullptr;      // pinned, mapped host mirror of the rank state
+  RankState* rs_host_dev = nullptr;  // its device address
   float* dev_in = nullptr;
   float* dev_out = nullptr;
   size_t dev_io_cap = 0;
@@ -328,10 +329,12 @@ hyde_status hyde_create(hyde_handle* out, int device) {
   hyde_ctx* h = new hyde_ctx();
   h->device = device;
   DeviceGuard g(device);
-  e = cudaMallocHost((void**)&h->rs_host, sizeof(RankState));
+  // pinned + mapped: the SURE kernel writes each chunk's rank decision here
+  e = cudaHostAlloc((void**)&h->rs_host, sizeof(RankState), cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&h->rs_host_dev, h->rs_host, 0);
   if (e != cudaSuccess) {
     delete h;
-    return hyde_cuda_fail(e, "cudaMallocHost", __FILE__, __LINE__);
+    return hyde_cuda_fail(e, "cudaHostAlloc", __FILE__, __LINE__);
   }
   *out = h;
   return HYDE_OK;
@@ -475,12 +478,13 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
       // the rank decision of the chunk is made by the last SURE subband to finish
       CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
                      (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, (unsigned*)(ws + L.surv), st, k0,
-                     (double)L.plan.n_coeffs, B, (double*)(ws + L.epost)));
+                     (double)L.plan.n_coeffs, B, (double*)(ws + L.epost), h->rs_host_dev));
       sg.end();
     }
     {
+      // the deciding SURE thread also wrote the decision into the pinned host
+      // mirror (mapped memory): an event after the kernel is all the host needs
       Stage sg(h, HYDE_STAGE_RANK, 0, st);
-      CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
       if (!h->ev_rank) CK(cudaEventCreateWithFlags(&h->ev_rank, cudaEventDisableTiming));
       CK(cudaEventRecord(h->ev_rank, st));
       sg.end();

@@ -90,7 +90,8 @@ cudaError_t launch_soft_threshold(float* coeffs, long long cstride, const DwtPla
 cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, int count,
                         int keep_ll, int* kstar, float* tstar, double* e_sub,
                         RankState* rs, unsigned* surv, cudaStream_t st,
-                        int k0 = 0, double n_coeffs = 0.0, int bands = 0, double* e_post = nullptr);
+                        int k0 = 0, double n_coeffs = 0.0, int bands = 0, double* e_post = nullptr,
+                        RankState* rs_mirror = nullptr);
 int sure_prof_read(unsigned long long* out16);   // K5 phase cycles (HYDE_SURE_PROF builds), 0 otherwise
 cudaError_t launch_rank_decide(const double* e_sub, int nsub, int count, int k0, double n_coeffs,
                                int bands, RankState* rs, double* e_post, cudaStream_t st);

@@ -388,7 +388,7 @@ __device__ unsigned long long g_sure_prof[48];
 __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ coeffs, long long cstride, SubTable tab,
                                                      int count, int keep_ll, int* kstar, float* tstar, double* e_sub,
                                                      RankState* rs, int k0, double n_coeffs, int bands,
-                                                     double* e_post) {
+                                                     double* e_post, RankState* rs_mirror) {
   extern __shared__ __align__(16) unsigned char smraw[];
   // union: histogram (HB counts | HB fixed-point sums) | window keys + sort buffer
   unsigned* hcnt = reinterpret_cast<unsigned*>(smraw);
@@ -877,6 +877,15 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
         __threadfence();
         rank_decide_one(e_sub, tab.nsub, count, k0, n_coeffs, bands, rs, e_post);
         rs->sure_done = 0u;
+        if (rs_mirror) {   // pinned host copy of the decision (no copy-engine op on the stream)
+          __threadfence();
+          rs_mirror->found = rs->found;
+          rs_mirror->rank = rs->rank;
+          rs_mirror->nonfinite = *(volatile int*)&rs->nonfinite;
+          rs_mirror->sure_overflow = *(volatile int*)&rs->sure_overflow;
+          rs_mirror->sure_done = 0u;
+          __threadfence_system();
+        }
       }
     }
   }
@@ -929,7 +938,7 @@ SubTable make_table(const DwtPlan& plan) {
 
 cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, int count, int keep_ll, int* kstar,
                         float* tstar, double* e_sub, RankState* rs, unsigned* surv, cudaStream_t st, int k0,
-                        double n_coeffs, int bands, double* e_post) {
+                        double n_coeffs, int bands, double* e_post, RankState* rs_mirror) {
   (void)surv;
   const SubTable tab = make_table(plan);
   cudaError_t e = cudaFuncSetAttribute(sure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_DYN);
@@ -961,7 +970,7 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, sure_kernel, (const float*)coeffs, cstride, tab, count, keep_ll, kstar, tstar, e_sub,
-                            rs, k0, n_coeffs, bands, e_post);
+                            rs, k0, n_coeffs, bands, e_post, rs_mirror);
 }
 
 int sure_prof_read(unsigned long long* out16) {
