@@ -49,7 +49,7 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks (NVML)
 class ClockSampler:
-    """Polls SM clock and clock-event reasons every 20 ms in a thread."""
+    """Polls SM clock and clock-event reasons every ~5 ms in a thread."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
@@ -84,7 +84,7 @@ class ClockSampler:
                 self.samples.append((time.perf_counter(), mhz, rs))
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def start(self):
         if self.ok:
@@ -406,6 +406,25 @@ def main():
         hy.hyres_host_stream(seq_in, seq_out, device=local)
         torch.cuda.synchronize()
     e2e_s = hd.max_over_ranks((time.perf_counter() - t0) / ne, device="cuda")
+    # the link's own floor for the same bytes: H2D of the inputs and D2H of the
+    # outputs on two streams at once (full-duplex PCIe), device buffers only
+    link_s = None
+    if not sharded and args.e2e_steps > 0:
+        din = torch.empty_like(pins[0], device="cuda")
+        dout = torch.empty_like(pins[0], device="cuda")
+        s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
+        reps = 3
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(reps):
+            for i in range(ncube):
+                with torch.cuda.stream(s_a):
+                    din.copy_(pins[i], non_blocking=True)
+                with torch.cuda.stream(s_b):
+                    pouts[i].copy_(dout, non_blocking=True)
+        torch.cuda.synchronize()
+        link_s = (time.perf_counter() - t1) / reps
+        del din, dout
     clk.stop()
     csum = clk.summary()
 
@@ -469,6 +488,8 @@ def main():
         "e2e": {"value": (1 if sharded else world * ncube) * cfg.voxels / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "ms_per_step": e2e_s * 1e3, "steps": ne,
+                "link_floor_ms": (link_s * 1e3) if link_s else None,
+                "frac_of_link": (link_s / e2e_s) if link_s else None,
                 "path": ("slab H2D + hyde_hyres_sharded + slab D2H per rank (pinned)" if sharded else
                          "hyde_hyres_host_stream (pinned host buffers; H2D of the next cube and D2H of "
                          "the previous one overlap the current cube)")},

@@ -41,6 +41,7 @@
 // memory -- and Jacobi's ~8 sweeps x 5 B^3/2 flops with O(B) barriers per
 // sweep is both more work and a longer dependency chain than Householder.
 #include <math.h>
+#include <cstdlib>
 
 #include <type_traits>
 
@@ -1177,14 +1178,18 @@ extern "C" hyde_status hyde_debug_eig_clocks(long long* out) {
 }
 
 extern "C" int hyde_eig_cluster_size(void) {
-  if (g_cluster == 0) g_cluster = cluster_fits<16>() ? 16 : 8;
+  if (g_cluster == 0) {
+    g_cluster = cluster_fits<16>() ? 16 : 8;
+    if (const char* ev = getenv("HYDE_EIG_CL"))   // experiments: force 8
+      if (atoi(ev) == 8) g_cluster = 8;
+  }
   return g_cluster;
 }
 
 size_t eig_workspace_doubles(int B) { return 4 * (size_t)B * B + (size_t)B + 8 + 64; }
 
 static cudaError_t run_k2(const K2Args& a, cudaStream_t st) {
-  if (g_cluster == 0) g_cluster = cluster_fits<16>() ? 16 : 8;
+  hyde_eig_cluster_size();
   return g_cluster == 16 ? launch_k2<16>(a, st) : launch_k2<8>(a, st);
 }
 
