@@ -58,7 +58,7 @@ hyde_status hyde_cuda_fail(cudaError_t e, const char* what, const char* file, in
 cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int nsplit,
                         double* G, int* nonfinite, cudaStream_t st);
 int gram_nsplit(long long n, int B);
-cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st);
+cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st, int sym = 0);
 bool gram_tc_supported(int B);
 int gram_tc_npairs(long long n);
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,

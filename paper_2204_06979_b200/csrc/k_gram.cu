@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const float* __restri
 // fixed order -- deterministic, and not one 74-deep chain of L2 round trips
 // per element.  The (min, max) element is read so G is exactly symmetric.
 __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restrict__ partial, int nsplit, int B,
-                                                          double* __restrict__ G) {
+                                                          double* __restrict__ G, int sym) {
   __shared__ double part[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long tot = (long long)B * B;
@@ -96,16 +96,22 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restri
   if (idx < tot) {
     const int i = (int)(idx / B), j = (int)(idx % B);
     const long long src = (long long)min(i, j) * B + max(i, j);
+    // sym > 0: partials of the diagonal blocks ([0, sym) and [sym, B)) are not
+    // symmetric -- G = (sum P + sum P^T) / 2 there (tensor-core Gram, K1)
+    const bool both = sym > 0 && ((i < sym) == (j < sym));
+    const long long srt = (long long)max(i, j) * B + min(i, j);
     double v[16];
     for (int k0 = w; k0 < nsplit; k0 += 8 * 16) {
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int k = k0 + 8 * u;
         v[u] = k < nsplit ? __ldcs(partial + (long long)k * tot + src) : 0.0;
+        if (both && k < nsplit) v[u] += __ldcs(partial + (long long)k * tot + srt);
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) s += v[u];
     }
+    if (both) s *= 0.5;
   }
   part[w][lane] = s;
   __syncthreads();
@@ -141,8 +147,8 @@ cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int
 }
 
 // G[i][j] = sum over slices of partial[slice][min(i,j)][max(i,j)], fixed order
-cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st) {
+cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st, int sym) {
   long long tot = (long long)B * B;
-  gram_reduce_kernel<<<(unsigned)((tot + 31) / 32), 256, 0, st>>>(partial, nsplit, B, G);
+  gram_reduce_kernel<<<(unsigned)((tot + 31) / 32), 256, 0, st>>>(partial, nsplit, B, G, sym);
   return cudaGetLastError();
 }

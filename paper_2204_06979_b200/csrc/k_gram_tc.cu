@@ -156,8 +156,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint32_t first = (s == 0 && ks == 0) ? 0u : 1u;
           // T_aa: A = P, B = P
           tc::mma_i8<2>(tmem + 0 * CL, dsc(st0, 0, 0), dsc(st0, 0, 0), id_aa, first);
+          // diagonal tiles: only X = S0 S1^T (the cross term is X + X^T,
+          // symmetrised in the reduction) -- one MMA of four saved
           tc::mma_i8<2>(tmem + 1 * CL, dsc(st0, 0, 0), dsc(st1, 0, 0), id_aa, first);
-          tc::mma_i8<2>(tmem + 1 * CL, dsc(st1, 0, 0), dsc(st0, 0, 0), id_aa, 1u);
           tc::mma_i8<2>(tmem + 2 * CL, dsc(st1, 0, 0), dsc(st1, 0, 0), id_aa, first);
           if (nb > 0) {
             // T_ab: A = P, B = QB ; T_bb: A = QA, B = QB
@@ -167,7 +168,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             tc::mma_i8<2>(tmem + 2 * CL + off_ab, dsc(st1, 0, 0), dsc(st1, 1, 0), id_b, first);
             tc::mma_i8<2>(tmem + 0 * CL + off_bb, dsc(st0, 1, 0), dsc(st0, 1, 0), id_b, first);
             tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1, 0), dsc(st1, 1, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st1, 1, 0), dsc(st0, 1, 0), id_b, 1u);
             tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1, 0), dsc(st1, 1, 0), id_b, first);
           }
         }
@@ -315,7 +315,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const float m_j = __uint_as_float(P.amax_bits[bj]);
             const float isj = m_j > 0.f ? fminf((float)(16256.0 / (double)m_j), 1e30f) : 1.f;
             sj = 1.0 / (double)isj;
-            const long long qq = 16384LL * (long long)(int)a0[j] + 128LL * (long long)(int)a1[j] +
+            // T_ab holds S0 S1^T + S1 S0^T; the diagonal tiles hold X = S0 S1^T only:
+            // 256 X here, (P + P^T) / 2 in the reduction gives 128 (X + X^T)
+            const long long qq = 16384LL * (long long)(int)a0[j] + (t == 1 ? 128LL : 256LL) * (long long)(int)a1[j] +
                                  (long long)(int)a2[j];
             Pp[(long long)bi * B + bj] = (double)qq * si * sj;
           }
@@ -424,7 +426,7 @@ cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsi
   gram_tc_kernel<<<2 * npairs, NTHREADS, smem, st>>>(P);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_gram_reduce(partial, npairs, B, G, st);
+  return launch_gram_reduce(partial, npairs, B, G, st, 128);
 }
 
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
