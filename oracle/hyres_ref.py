@@ -38,6 +38,11 @@ C7  e^_k = IDWT(soft coefficients) (the adjoint synthesis, cropping each level's
     padding); X^ = sum_{k<=r*} (sigma (.) v_k) e^_k^T, returned as float32 BSQ
     (SPEC.md:380 step (6) "inverse transforms and de-whitening").
 
+F1  (NEXT row of SURVEY.md §8(f)) HySime subspace identification: R_y = Y Y^T/N,
+    R_n = N~ N~^T/N from the band-by-band regression residual N~, R_x = R_y - R_n
+    = E diag(mu) E^T, delta_i = -e_i^T R_y e_i + 2 e_i^T R_n e_i, k = #{delta_i < 0}
+    (SPEC.md:370-377), pinned by tests/test_oracle_pins.py::test_f1_*.
+
 Parity pins for every function are in tests/test_oracle_*.py (SURVEY.md §8(c)
 P1-P8).  P9 (the paper's Houston anchor) is "parity unpinned":
 the data is not available.
@@ -54,6 +59,7 @@ DEFAULT_RIDGE = 1e-6          # SPEC.md:364 "ridge damping delta=1e-6"
 DEFAULT_TAPS = 16             # SPEC.md:179 D4 "default Daubechies-8"
 SUPPORTED_TAPS = (2, 8, 16)   # Haar, db4, db8 (SPEC.md:179 D4)
 MAX_AUTO_LEVELS = 5
+HYSIME_TOL = 1e-9             # DESIGN.md R13: |delta_i| below this x max p_j counts as zero
 
 
 # ----------------------------------------------------------------------------
@@ -391,3 +397,72 @@ def hyres(cube: np.ndarray, taps: int = DEFAULT_TAPS, levels: int = 0, ridge: fl
     out = (u @ ehat).reshape(b, r, c).astype(np.float32)                      # C7
     return HyresResult(out, rank, lv, sigma, g, lam, v, nc, e_post, sure_all,
                        eimgs, kept if keep_images else [])
+
+
+# ----------------------------------------------------------------------------
+# F1: HySime subspace identification
+# ----------------------------------------------------------------------------
+@dataclass
+class HysimeResult:
+    k: int                  # signal subspace dimension: #{i : delta_i < 0}
+    basis: np.ndarray       # B x k, eigenvectors of R_x in ascending-delta order (D6 signs)
+    delta: np.ndarray       # (B,) delta_i = -p_i + 2 sigma_i^2, in the order of mu (descending)
+    mu: np.ndarray          # (B,) eigenvalues of R_x, descending
+    E: np.ndarray           # B x B eigenvectors of R_x (columns, descending mu, D6 signs)
+    noise_cov: np.ndarray   # R_n = N~^T N~ / N (B x B)
+    r_y: np.ndarray         # R_y = Y Y^T / N
+
+
+def noise_residual(cube: np.ndarray, ridge: float = DEFAULT_RIDGE) -> np.ndarray:
+    """N~ (B x N): residual of the least-squares regression of every band on all
+    the other bands, N~_b = y_b - Y_{-b} beta_b, written out
+    band by band from the normal equations with the ridge of S:364 on the
+    other-band block.  Slow (B solves); small cubes only."""
+    y = _as_bands_by_pixels(cube)
+    b = y.shape[0]
+    g = y @ y.T
+    res = np.empty_like(y)
+    for i in range(b):
+        o = [j for j in range(b) if j != i]
+        a = g[np.ix_(o, o)] + ridge * np.eye(b - 1)
+        beta = np.linalg.solve(a, g[o, i])
+        res[i] = y[i] - beta @ y[o]
+    return res
+
+
+def hysime(cube: np.ndarray, ridge: float = DEFAULT_RIDGE) -> HysimeResult:
+    """HySime ("eigendecompose the signal correlation estimate
+    (R_y - R_n), select dimension k minimizing the sum of projection-error and
+    noise-power terms"; the criterion of Bioucas-Dias & Nascimento, HySime, which
+    HyDe implements):
+      R_y = Y Y^T / N;  R_n = N~ N~^T / N with N~ the regression residual
+      (noise_residual, SPEC.md:364 post: noise_cov = (1/N) N~^T N~);
+      R_x = R_y - R_n = E diag(mu) E^T (mu descending, D6 signs);
+      p_i = e_i^T R_y e_i, sigma_i^2 = e_i^T R_n e_i, delta_i = -p_i + 2 sigma_i^2
+      (the mean-square-error change of adding e_i to the subspace: minus the
+      projected signal power plus twice the projected noise power);
+      the error sum over a subspace is minimised by taking exactly the
+      eigenvectors with delta_i < 0: k = #{delta_i < 0}, basis = those
+      eigenvectors in ascending-delta order (stable on ties).
+    Reading (R13): a delta_i within 1e-9 max_j p_j of zero counts as
+    non-negative -- on a noiseless cube the null-space eigenvectors carry
+    p_i ~ sigma_i^2 ~ rounding and their sign is noise (SPEC.md:375 expects
+    k == 1 for a noiseless rank-1 cube)."""
+    y = _as_bands_by_pixels(cube)
+    b, n = y.shape
+    if b < 3 or n <= b:
+        raise ValueError("bands >= 3 and pixels > bands required (SPEC.md:363, :365)")
+    r_y = (y @ y.T) / n
+    res = noise_residual(cube, ridge)
+    r_n = (res @ res.T) / n
+    r_x = r_y - r_n
+    mu, e = np.linalg.eigh(0.5 * (r_x + r_x.T))
+    order = np.argsort(-mu, kind="stable")
+    mu, e = mu[order], sign_fix(e[:, order])
+    p = np.einsum("ij,ik,kj->j", e, r_y, e)
+    s2 = np.einsum("ij,ik,kj->j", e, r_n, e)
+    delta = -p + 2.0 * s2
+    asc = np.argsort(delta, kind="stable")
+    tol = HYSIME_TOL * float(np.max(np.abs(p)))
+    k = int(np.count_nonzero(delta < -tol))
+    return HysimeResult(k, e[:, asc[:k]], delta, mu, e, r_n, r_y)

@@ -377,3 +377,87 @@ def test_olympic_mean_spec(golden_dir):
         assert abs(metrics.olympic_mean(v) - np.mean(np.sort(v)[1:-1])) < 1e-12
     with pytest.raises(ValueError):
         metrics.olympic_mean([1.0, 2.0])
+
+
+# ---------------------------------------------------------------- F1: HySime
+def _low_rank_cube(rng, r, c, b, rank, snr_db=None):
+    a = rng.random((rank, r * c))
+    s = rng.random((b, rank))
+    x = s @ a
+    if snr_db is not None:
+        sig = np.sqrt(np.mean(x ** 2) / 10 ** (snr_db / 10))
+        x = x + sig * rng.standard_normal(x.shape)
+    return x.reshape(b, r, c)
+
+
+def test_f1_noise_residual_is_the_regression_residual():
+    """N~_b is orthogonal to every other band (normal equations) and equals the
+    closed form (M Y)_b / M_bb of the full inverse (ridge 0) -- a different route."""
+    rng = np.random.default_rng(11)
+    y = rng.standard_normal((6, 200))
+    res = O.noise_residual(y.reshape(6, 10, 20), ridge=0.0)
+    g = y @ y.T
+    for i in range(6):
+        o = [j for j in range(6) if j != i]
+        assert np.max(np.abs(y[o] @ res[i])) < 1e-9 * np.max(np.abs(g))
+    m = np.linalg.inv(g)
+    closed = (m @ y) / np.diag(m)[:, None]
+    assert np.max(np.abs(closed - res)) < 1e-9
+
+
+def test_f1_spec_rank5_30db():
+    """SPEC.md:374 example: synthetic rank-5 cube (64x64x50) at 30 dB -> k == 5 (+-1);
+    basis orthonormal."""
+    rng = np.random.default_rng(12)
+    cube = _low_rank_cube(rng, 64, 64, 50, 5, snr_db=30)
+    h = O.hysime(cube)
+    assert abs(h.k - 5) <= 1, h.k
+    assert np.max(np.abs(h.basis.T @ h.basis - np.eye(h.k))) < 1e-10
+
+
+def test_f1_noiseless_rank1():
+    """noiseless rank-1 cube -> k == 1 (the ridge leaves a residual
+    of order delta; its projected power is far below the signal's)."""
+    rng = np.random.default_rng(13)
+    cube = _low_rank_cube(rng, 32, 32, 12, 1)
+    assert O.hysime(cube).k == 1
+
+
+def test_f1_pure_noise_has_no_signal_subspace():
+    """White noise: R_x ~ 0, every delta_i ~ sigma_i^2 > 0 -> k == 0."""
+    rng = np.random.default_rng(14)
+    cube = rng.standard_normal((16, 64, 64))
+    assert O.hysime(cube).k == 0
+
+
+def test_f1_criterion_is_the_brute_force_minimum():
+    """k and the basis minimise the HySime error sum over subspaces spanned by
+    eigenvectors of R_x: brute force over every subset of a small problem."""
+    import itertools
+    rng = np.random.default_rng(15)
+    cube = _low_rank_cube(rng, 16, 16, 7, 3, snr_db=15)
+    h = O.hysime(cube)
+    b = 7
+    best, best_set = None, None
+    for r in range(b + 1):
+        for sub in itertools.combinations(range(b), r):
+            v = float(sum(h.delta[i] for i in sub))   # error(S) - const = sum_{i in S} delta_i
+            if best is None or v < best - 1e-15:
+                best, best_set = v, sub
+    assert len(best_set) == h.k
+    assert set(best_set) == set(int(i) for i in np.nonzero(h.delta < 0)[0])
+    assert np.min(np.abs(h.delta)) > O.HYSIME_TOL * np.max(np.abs(h.delta))   # no near-zero delta here
+
+
+def test_f1_eigen_identities():
+    """R_x = E diag(mu) E^T, E orthonormal, R_n symmetric PSD, p_i - sigma_i^2 = mu_i."""
+    rng = np.random.default_rng(16)
+    cube = _low_rank_cube(rng, 32, 32, 20, 4, snr_db=20)
+    h = O.hysime(cube)
+    rx = h.r_y - h.noise_cov
+    assert np.max(np.abs(h.E @ np.diag(h.mu) @ h.E.T - rx)) < 1e-12 * np.max(np.abs(rx))
+    assert np.max(np.abs(h.E.T @ h.E - np.eye(20))) < 1e-12
+    assert np.min(np.linalg.eigvalsh(h.noise_cov)) > -1e-14
+    p = np.einsum("ij,ik,kj->j", h.E, h.r_y, h.E)
+    s2 = np.einsum("ij,ik,kj->j", h.E, h.noise_cov, h.E)
+    assert np.max(np.abs((p - s2) - h.mu)) < 1e-12 * np.max(np.abs(h.mu))
