@@ -370,6 +370,19 @@ def main():
     cubes_total = 1.0 if sharded else hd.sum_over_ranks(ncube, device="cuda")
     value = hd.whole_job_rate(cubes_total * cfg.voxels, ms_max * 1e-3)
 
+    hys = None
+    if args.iso_steps > 0 and not batched and not sharded and rank == 0:
+        # F1: HySime on the same cube -- Gram + sweep + raw
+        # eigendecomposition of R_x (all B eigenpairs) + criterion
+        hy.hysime(cube)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            hres = hy.hysime(cube)
+            ts.append(time.perf_counter() - t0)
+        hys = {"ms": round(1e3 * statistics.median(ts), 4), "k": hres["k"], "bands": cfg.bands,
+               "timing": "host wall clock of the synchronous call (returns k), median of 3"}
     iso = None
     if args.iso_steps > 0 and not batched and not sharded and rank == 0:
         hbm_, _, _ = peaks()
@@ -498,6 +511,8 @@ def main():
     }
     if iso is not None:
         line["wavelet_isolated"] = iso
+    if hys is not None:
+        line["hysime"] = hys
     if world == 1 and not args.no_cpu_baseline:
         t, cores, thr = cpu_baseline(cubes_h[0], reps=2)
         line["cpu_baseline"] = {"value": cfg.voxels / t, "unit": UNIT, "cores": cores, "threads": thr,

@@ -162,6 +162,20 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
                                int bands, float* local_out, const hyde_hyres_params* params,
                                hyde_hyres_info* info, const hyde_comm* comm, hyde_stream_t stream);
 
+/* --- F1: HySime signal-subspace identification
+ * ("HySime ... implemented in HyDe") on the
+ * same A1/A2 data: R_y = Y Y^T / N, R_n = N~ N~^T / N with N~ the regression
+ * residual of every band on all others (ridge 1e-6, as A1), computed without a
+ * second pass as D^-1 (M - delta M^2) D^-1 / N, M = (G + delta I)^-1,
+ * D = diag(M); R_x = R_y - R_n = E diag(mu) E^T; delta_i = -e_i^T R_y e_i +
+ * 2 e_i^T R_n e_i; *k_out (HOST) = #{delta_i < -1e-9 max_j |p_j|} (DESIGN.md
+ * R13).  Optional DEVICE outputs (NULL = skip): basis (bands x bands row-major;
+ * columns 0..k-1 = the selected eigenvectors in ascending-delta order, D6 signs),
+ * delta and mu ([bands], in descending-mu order), noise_cov (R_n, bands x
+ * bands).  Synchronous (returns after k is known).  Errors: as hyde_hyres. */
+hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, int bands, int* k_out,
+                        double* basis, double* delta, double* mu, double* noise_cov, hyde_stream_t stream);
+
 /* Bytes of device workspace hyde_hyres_ex / _batched will hold for this shape. */
 size_t hyde_hyres_workspace_size(int rows, int cols, int bands, int batch,
                                  const hyde_hyres_params* params);

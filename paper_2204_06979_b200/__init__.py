@@ -255,6 +255,24 @@ def estimate_noise(cube, *, return_gram=False, return_residual=False):
     return out[0] if len(out) == 1 else out
 
 
+def hysime(cube):
+    """HySime signal-subspace identification (F1; include/hyde.h hyde_hysime):
+    returns dict(k, basis (bands, k) fp64, delta (bands,), mu (bands,), noise_cov (bands, bands))."""
+    torch = _torch()
+    _cube(cube)
+    b, r, c = cube.shape
+    dev = cube.device
+    basis = torch.zeros((b, b), dtype=torch.float64, device=dev)
+    delta = torch.empty(b, dtype=torch.float64, device=dev)
+    mu = torch.empty(b, dtype=torch.float64, device=dev)
+    ncov = torch.empty((b, b), dtype=torch.float64, device=dev)
+    k = ctypes.c_int(0)
+    h = handle(dev.index)
+    check(lib().hyde_hysime(h, cube.data_ptr(), r, c, b, ctypes.byref(k), basis.data_ptr(), delta.data_ptr(),
+                            mu.data_ptr(), ncov.data_ptr(), _stream(cube)), h)
+    return {"k": int(k.value), "basis": basis[:, :k.value], "delta": delta, "mu": mu, "noise_cov": ncov}
+
+
 def workspace_size(rows, cols, bands, batch=1, chunk=16, taps=16, levels=0) -> int:
     p = make_params(taps, levels, chunk)
     return int(lib().hyde_hyres_workspace_size(rows, cols, bands, batch, ctypes.byref(p)))

@@ -925,6 +925,72 @@ hyde_status hyde_estimate_noise(hyde_handle h, const float* cube, int rows, int 
 }
 
 // ---------------------------------------------------------------- stages
+hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, int bands, int* k_out, double* basis,
+                        double* delta, double* mu, double* noise_cov, hyde_stream_t stream) {
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  if (!cube || !k_out) return fail(h, HYDE_EPARAM, "NULL cube/k_out");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = bands;
+  Layout L;
+  make_layout(rows, cols, B, 1, 1, 2, &L);
+  // HySime buffers past the HyRes layout
+  const size_t BB = (size_t)B * B;
+  size_t off = L.total;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+  const size_t oRy = take(BB * 8), oRn = take(BB * 8), oRx = take(BB * 8), oV = take(BB * 8), oB = take(BB * 8);
+  const size_t oLam = take((size_t)B * 8), oP = take((size_t)B * 8), oS2 = take((size_t)B * 8),
+               oD = take((size_t)B * 8), oOnes = take((size_t)B * 8), oK = take(sizeof(int)), oW = take(BB * 4),
+               oU = take(BB * 4);
+  s = ensure_ws(h, off, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  RankState* rs = (RankState*)(ws + L.rs);
+  h->last_rs = rs;
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  double* G = (double*)(ws + L.G);
+  double* house = (double*)(ws + L.house);
+  double* tri = (double*)(ws + L.tri);
+  double* Ry = (double*)(ws + oRy);
+  double* Rn = (double*)(ws + oRn);
+  double* Rx = (double*)(ws + oRx);
+  double* V = (double*)(ws + oV);
+  double* lam = (double*)(ws + oLam);
+  double* dl = (double*)(ws + oD);
+  double* ones = (double*)(ws + oOnes);
+  float* W = (float*)(ws + oW);
+  float* U = (float*)(ws + oU);
+  CK(run_gram(L, ws, cube, G, &rs->nonfinite, st));
+  // M = (G + delta I)^-1 (K2 sweep only): R_n without another pass over the cube
+  CK(launch_noise_eig(G, L.n, B, 1e-6, -1, 0, (double*)(ws + L.sigma), nullptr, nullptr, house, tri, nullptr,
+                      nullptr, B, st));
+  const double* M = house + 3 * BB;   // EigWs::M of the K2 workspace
+  CK(launch_hysime_prep(G, M, B, L.n, 1e-6, Ry, Rn, Rx, st));
+  // every eigenpair of R_x: the first chunk in the cluster kernel, the rest from its T and Q
+  const int k1 = B < HYDE_MAX_CHUNK ? B : HYDE_MAX_CHUNK;
+  CK(launch_eig_raw(Rx, B, k1, ones, lam, V, B, house, tri, W, U, B, st));
+  for (int k0 = k1; k0 < B; k0 += HYDE_MAX_CHUNK) {
+    const int kc = (B - k0) < HYDE_MAX_CHUNK ? (B - k0) : HYDE_MAX_CHUNK;
+    CK(launch_eig_more_raw(tri, house, ones, B, k0, kc, lam, V, B, W, U, B, st));
+  }
+  CK(launch_hysime_delta(V, B, Ry, Rn, B, (double*)(ws + oP), (double*)(ws + oS2), dl, st));
+  CK(launch_hysime_select(dl, (double*)(ws + oP), B, 1e-9, V, B, basis ? (double*)(ws + oB) : nullptr,
+                          (int*)(ws + oK), st));
+  if (basis) CK(cudaMemcpyAsync(basis, ws + oB, BB * 8, cudaMemcpyDeviceToDevice, st));
+  if (delta) CK(cudaMemcpyAsync(delta, dl, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
+  if (mu) CK(cudaMemcpyAsync(mu, lam, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
+  if (noise_cov) CK(cudaMemcpyAsync(noise_cov, Rn, BB * 8, cudaMemcpyDeviceToDevice, st));
+  int k = 0;
+  CK(cudaMemcpyAsync(&h->rs_host->sure_done, ws + oK, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h->rs_host->nonfinite, &rs->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  k = (int)h->rs_host->sure_done;
+  if (h->rs_host->nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
+  *k_out = k;
+  return HYDE_OK;
+}
+
 hyde_status hyde_k_gram(hyde_handle h, const float* cube, int n_pixels, int bands, double* gram,
                         hyde_stream_t stream) {
   if (!h || !cube || !gram || n_pixels < 1 || bands < 1 || bands > 256) return fail(h, HYDE_EPARAM, "bad arguments");

@@ -70,6 +70,17 @@ size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,
                              double* tri, float* W, float* U, int ldwu, cudaStream_t st);
+// F1: HySime (k_hysime.cu)
+cudaError_t launch_hysime_prep(const double* G, const double* M, int B, long long n, double ridge, double* Ry,
+                               double* Rn, double* Rx, cudaStream_t st);
+cudaError_t launch_hysime_delta(const double* V, int ldv, const double* Ry, const double* Rn, int B, double* p,
+                                double* s2, double* delta, cudaStream_t st);
+cudaError_t launch_hysime_select(const double* delta, const double* p, int B, double tol_rel, const double* V,
+                                 int ldv, double* basis, int* k_out, cudaStream_t st);
+cudaError_t launch_eig_more_raw(const double* tri, const double* house, const double* ones, int B, int k0, int K,
+                                double* lam, double* V, int ldv, float* W, float* U, int ldwu, cudaStream_t st);
+cudaError_t launch_eig_raw(const double* Amat, int B, int ncomp, double* ones, double* lam, double* V, int ldv,
+                           double* house, double* tri, float* W, float* U, int ldwu, cudaStream_t st);
 cudaError_t launch_eigvec_more(const double* tri, const double* house, const double* sigma, int B,
                                int k0, int ncomp, double* lam_top, double* V, float* W, float* U,
                                int ldwu, cudaStream_t st);

@@ -417,6 +417,7 @@ struct K2Args {
   const double* G;
   long long n;
   int B;
+  int raw;         // 1: eigendecompose G itself (no sweep, sigma = 1, n = 1) -- HySime's R_x (F1)
   double ridge;
   int K;           // eigenpairs of the first chunk
   int tridiag;     // 0: sigma only
@@ -554,163 +555,175 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
   CLK_DECL
 
   double a[RS][CS];
-  // ================= phase 1: blocked sweep of G + ridge I =================
+  if (A.raw) {
+    // F1 (HySime): the input is the matrix to decompose; no noise whitening
 #pragma unroll
-  for (int s = 0; s < RS; ++s)
-#pragma unroll
-    for (int t = 0; t < CS; ++t) {
-      const int i = rowi[s], j = lane + 32 * t;
-      a[s][t] = (i < B && j < B) ? G[(size_t)i * B + j] + (i == j ? A.ridge : 0.0) : 0.0;
-    }
-  for (int k0 = 0, blk = 0; k0 < B; k0 += NB, ++blk) {
-    const int kb = min(NB, B - k0), t0 = k0 >> 5, L0 = k0 & 31;
-    double* colK = S.colK[blk & 1];
-    {   // all-gather the pivot-block columns of every row: lane L owns the pair
-        // (row slot, column) = (L % 8RS) / 8, L % 8 and 8 of the CL destinations
-      const int pr = lane % (8 * RS), sp = pr >> 3, q = pr & 7;
-      double val = 0.0;
-#pragma unroll
-      for (int s = 0; s < RS; ++s) {
-        const double tmp = __shfl_sync(FULL, sel(a[s], t0), L0 + q);
-        if (s == sp) val = tmp;
-      }
-      const int i = rowi[0] + CL * NW * sp;
-      if (i < B && q < kb) {
-        const unsigned la = saddr(&colK[i * NB + q]);
-        const unsigned mb = saddr(&S.smb[blk & 1]);
-        const int d0 = lane / (8 * RS);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const unsigned dst = d0 + u * (CL / 8);
-          st_async(mapa(la, dst), val, mapa(mb, dst));
-        }
+    for (int s = 0; s < RS; ++s) {
+      const int i = rowi[s];
+      if (i < B && lane == (i & 31)) {
+        st_all<CL>(&S.sig[i], 1.0);
+        A.sigma[i] = 1.0;
       }
     }
-    ACC(5);
-    mbar_wait(saddr(&S.smb[blk & 1]), (unsigned)(blk >> 1) & 1u);
-    if (tid == 0 && k0 + 2 * NB < B) mbar_expect(saddr(&S.smb[blk & 1]), (unsigned)(B * min(NB, B - k0 - 2 * NB) * 8));
-    ACC(6);
-    // Cholesky of the kb x kb pivot block by warp 0 (lane L holds entries
-    // (L>>2, 2(L&3)) and (L>>2, 2(L&3)+1); padding = identity)
-    if (w == 0) {
-      const int r = lane >> 2, q0 = 2 * (lane & 3);
-      double e0 = (r < kb && q0 < kb) ? colK[(k0 + r) * NB + q0] : (r == q0 ? 1.0 : 0.0);
-      double e1 = (r < kb && q0 + 1 < kb) ? colK[(k0 + r) * NB + q0 + 1] : (r == q0 + 1 ? 1.0 : 0.0);
-      for (int p = 0; p < kb; ++p) {
-        const double mine = (p & 1) ? e1 : e0;
-        double pp = __shfl_sync(FULL, mine, (p << 2) + (p >> 1));
-        const double rp = __shfl_sync(FULL, mine, (r << 2) + (p >> 1));
-        const double tq0 = __shfl_sync(FULL, mine, (q0 << 2) + (p >> 1));
-        const double tq1 = __shfl_sync(FULL, mine, ((q0 + 1) << 2) + (p >> 1));
-        if (!(pp > 0.0)) {   // not SPD (cannot happen for ridge > 0 in exact arithmetic)
-          if (lane == 0) A.ws.flags[0] = 1.0;
-          pp = 1e-300;
-        }
-        const double lpp = sqrt(pp);
-        const double il = rcp64(lpp);
-        const double lrp = (r == p) ? lpp : (r > p ? rp * il : 0.0);
-        const double lq0 = q0 > p ? tq0 * il : 0.0, lq1 = q0 + 1 > p ? tq1 * il : 0.0;
-        e0 = (q0 == p) ? lrp : (q0 > p ? fma(-lrp, lq0, e0) : e0);
-        e1 = (q0 + 1 == p) ? lrp : (q0 + 1 > p ? fma(-lrp, lq1, e1) : e1);
-        if (lane == 0) S.Lr[p] = il;
-      }
-      S.Lb[r * NB + q0] = (q0 <= r) ? e0 : 0.0;
-      S.Lb[r * NB + q0 + 1] = (q0 + 1 <= r) ? e1 : 0.0;
-    }
-    __syncthreads();
-    ACC(7);
-    // W = L^-1 A_K,j and Z = L^-T W = P^-1 A_K,j for every column j (A_K,j = colK[j]);
-    // the last kb tasks form column j of P^-1 from the unit vector e_j
-    for (int task = tid; task < B + kb; task += NT) {
-      const bool unit = task >= B;
-      const int j = unit ? task - B : task;
-      double x[NB];
-#pragma unroll
-      for (int r = 0; r < NB; ++r) x[r] = unit ? (r == j ? 1.0 : 0.0) : (r < kb ? colK[j * NB + r] : 0.0);
-#pragma unroll
-      for (int qq = 0; qq < NB; ++qq) {
-        double v = x[qq];
-#pragma unroll
-        for (int r = 0; r < qq; ++r) v = fma(-S.Lb[qq * NB + r], x[r], v);
-        x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
-      }
-      if (!unit) {
-#pragma unroll
-        for (int qq = 0; qq < NB; ++qq) S.Wb[qq][j] = x[qq];
-      }
-#pragma unroll
-      for (int qq = NB - 1; qq >= 0; --qq) {
-        double v = x[qq];
-#pragma unroll
-        for (int r = qq + 1; r < NB; ++r) v = fma(-S.Lb[r * NB + qq], x[r], v);
-        x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
-      }
-      if (unit) {
-#pragma unroll
-        for (int qq = 0; qq < NB; ++qq) S.Pinv[qq * NB + j] = x[qq];
-      } else {
-#pragma unroll
-        for (int qq = 0; qq < NB; ++qq) S.Zb[qq][j] = x[qq];
-      }
-    }
-    __syncthreads();
-    ACC(8);
-    double wi[RS][NB];
-#pragma unroll
+  } else {
+    // ================= phase 1: blocked sweep of G + ridge I =================
+  #pragma unroll
     for (int s = 0; s < RS; ++s)
-#pragma unroll
-      for (int r = 0; r < NB; ++r) wi[s][r] = rowi[s] < B ? S.Wb[r][rowi[s]] : 0.0;
-#pragma unroll
-    for (int t = 0; t < CS; ++t) {
-      const int j = lane + 32 * t;
-      if (j >= B) continue;
-      double wj[NB];
-#pragma unroll
-      for (int r = 0; r < NB; ++r) wj[r] = S.Wb[r][j];
-      const int jk = j - k0;
-      const bool inj = (unsigned)jk < (unsigned)kb;
-#pragma unroll
-      for (int s = 0; s < RS; ++s) {
-        const int i = rowi[s];
-        if (i >= B) continue;
-        const int ik = i - k0;
-        const bool ini = (unsigned)ik < (unsigned)kb;
-        if (!ini && !inj) {
-          double u = a[s][t];
-#pragma unroll
-          for (int r = 0; r < NB; ++r) u = fma(-wi[s][r], wj[r], u);
-          a[s][t] = u;
-        } else if (ini && !inj) {
-          a[s][t] = S.Zb[ik][j];
-        } else if (!ini) {
-          a[s][t] = S.Zb[jk][i];
-        } else {
-          a[s][t] = -S.Pinv[ik * NB + jk];
-        }
-      }
-    }
-    ACC(9);
-  }
-  // a = -(G + ridge I)^-1: sigma_i = sqrt(1 / (N M_ii)), all-gathered
-#pragma unroll
-  for (int s = 0; s < RS; ++s) {
-    const int i = rowi[s];
-    if (i < B && lane == (i & 31)) {
-      const double mii = -sel(a[s], i >> 5);
-      if (!(mii > 0.0)) A.ws.flags[0] = 1.0;
-      const double sg = sqrt(1.0 / ((double)A.n * mii));
-      st_all<CL>(&S.sig[i], sg);
-      A.sigma[i] = sg;
-    }
-  }
-  if (A.want_M) {
-#pragma unroll
-    for (int s = 0; s < RS; ++s)
-#pragma unroll
+  #pragma unroll
       for (int t = 0; t < CS; ++t) {
         const int i = rowi[s], j = lane + 32 * t;
-        if (i < B && j < B) A.ws.M[(size_t)i * B + j] = -a[s][t];
+        a[s][t] = (i < B && j < B) ? G[(size_t)i * B + j] + (i == j ? A.ridge : 0.0) : 0.0;
       }
+    for (int k0 = 0, blk = 0; k0 < B; k0 += NB, ++blk) {
+      const int kb = min(NB, B - k0), t0 = k0 >> 5, L0 = k0 & 31;
+      double* colK = S.colK[blk & 1];
+      {   // all-gather the pivot-block columns of every row: lane L owns the pair
+          // (row slot, column) = (L % 8RS) / 8, L % 8 and 8 of the CL destinations
+        const int pr = lane % (8 * RS), sp = pr >> 3, q = pr & 7;
+        double val = 0.0;
+  #pragma unroll
+        for (int s = 0; s < RS; ++s) {
+          const double tmp = __shfl_sync(FULL, sel(a[s], t0), L0 + q);
+          if (s == sp) val = tmp;
+        }
+        const int i = rowi[0] + CL * NW * sp;
+        if (i < B && q < kb) {
+          const unsigned la = saddr(&colK[i * NB + q]);
+          const unsigned mb = saddr(&S.smb[blk & 1]);
+          const int d0 = lane / (8 * RS);
+  #pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const unsigned dst = d0 + u * (CL / 8);
+            st_async(mapa(la, dst), val, mapa(mb, dst));
+          }
+        }
+      }
+      ACC(5);
+      mbar_wait(saddr(&S.smb[blk & 1]), (unsigned)(blk >> 1) & 1u);
+      if (tid == 0 && k0 + 2 * NB < B) mbar_expect(saddr(&S.smb[blk & 1]), (unsigned)(B * min(NB, B - k0 - 2 * NB) * 8));
+      ACC(6);
+      // Cholesky of the kb x kb pivot block by warp 0 (lane L holds entries
+      // (L>>2, 2(L&3)) and (L>>2, 2(L&3)+1); padding = identity)
+      if (w == 0) {
+        const int r = lane >> 2, q0 = 2 * (lane & 3);
+        double e0 = (r < kb && q0 < kb) ? colK[(k0 + r) * NB + q0] : (r == q0 ? 1.0 : 0.0);
+        double e1 = (r < kb && q0 + 1 < kb) ? colK[(k0 + r) * NB + q0 + 1] : (r == q0 + 1 ? 1.0 : 0.0);
+        for (int p = 0; p < kb; ++p) {
+          const double mine = (p & 1) ? e1 : e0;
+          double pp = __shfl_sync(FULL, mine, (p << 2) + (p >> 1));
+          const double rp = __shfl_sync(FULL, mine, (r << 2) + (p >> 1));
+          const double tq0 = __shfl_sync(FULL, mine, (q0 << 2) + (p >> 1));
+          const double tq1 = __shfl_sync(FULL, mine, ((q0 + 1) << 2) + (p >> 1));
+          if (!(pp > 0.0)) {   // not SPD (cannot happen for ridge > 0 in exact arithmetic)
+            if (lane == 0) A.ws.flags[0] = 1.0;
+            pp = 1e-300;
+          }
+          const double lpp = sqrt(pp);
+          const double il = rcp64(lpp);
+          const double lrp = (r == p) ? lpp : (r > p ? rp * il : 0.0);
+          const double lq0 = q0 > p ? tq0 * il : 0.0, lq1 = q0 + 1 > p ? tq1 * il : 0.0;
+          e0 = (q0 == p) ? lrp : (q0 > p ? fma(-lrp, lq0, e0) : e0);
+          e1 = (q0 + 1 == p) ? lrp : (q0 + 1 > p ? fma(-lrp, lq1, e1) : e1);
+          if (lane == 0) S.Lr[p] = il;
+        }
+        S.Lb[r * NB + q0] = (q0 <= r) ? e0 : 0.0;
+        S.Lb[r * NB + q0 + 1] = (q0 + 1 <= r) ? e1 : 0.0;
+      }
+      __syncthreads();
+      ACC(7);
+      // W = L^-1 A_K,j and Z = L^-T W = P^-1 A_K,j for every column j (A_K,j = colK[j]);
+      // the last kb tasks form column j of P^-1 from the unit vector e_j
+      for (int task = tid; task < B + kb; task += NT) {
+        const bool unit = task >= B;
+        const int j = unit ? task - B : task;
+        double x[NB];
+  #pragma unroll
+        for (int r = 0; r < NB; ++r) x[r] = unit ? (r == j ? 1.0 : 0.0) : (r < kb ? colK[j * NB + r] : 0.0);
+  #pragma unroll
+        for (int qq = 0; qq < NB; ++qq) {
+          double v = x[qq];
+  #pragma unroll
+          for (int r = 0; r < qq; ++r) v = fma(-S.Lb[qq * NB + r], x[r], v);
+          x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
+        }
+        if (!unit) {
+  #pragma unroll
+          for (int qq = 0; qq < NB; ++qq) S.Wb[qq][j] = x[qq];
+        }
+  #pragma unroll
+        for (int qq = NB - 1; qq >= 0; --qq) {
+          double v = x[qq];
+  #pragma unroll
+          for (int r = qq + 1; r < NB; ++r) v = fma(-S.Lb[r * NB + qq], x[r], v);
+          x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
+        }
+        if (unit) {
+  #pragma unroll
+          for (int qq = 0; qq < NB; ++qq) S.Pinv[qq * NB + j] = x[qq];
+        } else {
+  #pragma unroll
+          for (int qq = 0; qq < NB; ++qq) S.Zb[qq][j] = x[qq];
+        }
+      }
+      __syncthreads();
+      ACC(8);
+      double wi[RS][NB];
+  #pragma unroll
+      for (int s = 0; s < RS; ++s)
+  #pragma unroll
+        for (int r = 0; r < NB; ++r) wi[s][r] = rowi[s] < B ? S.Wb[r][rowi[s]] : 0.0;
+  #pragma unroll
+      for (int t = 0; t < CS; ++t) {
+        const int j = lane + 32 * t;
+        if (j >= B) continue;
+        double wj[NB];
+  #pragma unroll
+        for (int r = 0; r < NB; ++r) wj[r] = S.Wb[r][j];
+        const int jk = j - k0;
+        const bool inj = (unsigned)jk < (unsigned)kb;
+  #pragma unroll
+        for (int s = 0; s < RS; ++s) {
+          const int i = rowi[s];
+          if (i >= B) continue;
+          const int ik = i - k0;
+          const bool ini = (unsigned)ik < (unsigned)kb;
+          if (!ini && !inj) {
+            double u = a[s][t];
+  #pragma unroll
+            for (int r = 0; r < NB; ++r) u = fma(-wi[s][r], wj[r], u);
+            a[s][t] = u;
+          } else if (ini && !inj) {
+            a[s][t] = S.Zb[ik][j];
+          } else if (!ini) {
+            a[s][t] = S.Zb[jk][i];
+          } else {
+            a[s][t] = -S.Pinv[ik * NB + jk];
+          }
+        }
+      }
+      ACC(9);
+    }
+    // a = -(G + ridge I)^-1: sigma_i = sqrt(1 / (N M_ii)), all-gathered
+  #pragma unroll
+    for (int s = 0; s < RS; ++s) {
+      const int i = rowi[s];
+      if (i < B && lane == (i & 31)) {
+        const double mii = -sel(a[s], i >> 5);
+        if (!(mii > 0.0)) A.ws.flags[0] = 1.0;
+        const double sg = sqrt(1.0 / ((double)A.n * mii));
+        st_all<CL>(&S.sig[i], sg);
+        A.sigma[i] = sg;
+      }
+    }
+    if (A.want_M) {
+  #pragma unroll
+      for (int s = 0; s < RS; ++s)
+  #pragma unroll
+        for (int t = 0; t < CS; ++t) {
+          const int i = rowi[s], j = lane + 32 * t;
+          if (i < B && j < B) A.ws.M[(size_t)i * B + j] = -a[s][t];
+        }
+    }
   }
   cl_sync();
   if (prof) stamp(1);
@@ -1216,6 +1229,7 @@ cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, 
   a.G = G;
   a.n = n;
   a.B = B;
+  a.raw = 0;
   a.ridge = ridge;
   a.K = ncomp > 0 ? (ncomp < KM ? ncomp : KM) : 0;
   a.tridiag = (ncomp >= 0) ? 1 : 0;
@@ -1239,6 +1253,45 @@ cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, 
     e = cudaGetLastError();
   }
   return e;
+}
+
+// F1 (HySime): top `ncomp` eigenpairs of the symmetric B x B matrix A itself
+// (no whitening): eigenvalues descending into lam[k], eigenvectors (D6 signs)
+// as the columns of V (row-major B x ldv).  ones[B] receives 1.0 (the "sigma"
+// of the raw mode, reused by launch_eigvec_more for later eigenpairs).
+cudaError_t launch_eig_raw(const double* Amat, int B, int ncomp, double* ones, double* lam, double* V, int ldv,
+                           double* house, double* tri, float* W, float* U, int ldwu, cudaStream_t st) {
+  if (B > BM || B < 3 || ncomp < 1) return cudaErrorInvalidValue;
+  const EigWs ws = carve(house, B);
+  cudaError_t e = cudaMemsetAsync(ws.flags, 0, 8 * sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  K2Args a;
+  a.G = Amat;
+  a.n = 1;
+  a.B = B;
+  a.raw = 1;
+  a.ridge = 0.0;
+  a.K = ncomp < KM ? ncomp : KM;
+  a.tridiag = 1;
+  a.want_M = 0;
+  a.sigma = ones;
+  a.tri = tri;
+  a.ws = ws;
+  a.lam_out = lam;
+  a.V = V;
+  a.ldv = ldv;
+  a.W = W;
+  a.U = U;
+  a.ldwu = ldwu;
+  return run_k2(a, st);
+}
+
+// F1: eigenpairs k0 .. k0+K-1 of the raw-mode matrix (T and Q of the last
+// launch_eig_raw): eigenvalues into lam[k], vectors into column k of V (ldv)
+cudaError_t launch_eig_more_raw(const double* tri, const double* house, const double* ones, int B, int k0, int K,
+                                double* lam, double* V, int ldv, float* W, float* U, int ldwu, cudaStream_t st) {
+  const EigWs ws = carve(const_cast<double*>(house), B);
+  return run_more(tri, ws, ones, B, k0, K, lam, V + k0, ldv, W, U, ldwu, st);
 }
 
 cudaError_t launch_eigvec_more(const double* tri, const double* house, const double* sigma, int B, int k0,
