@@ -466,3 +466,78 @@ def hysime(cube: np.ndarray, ridge: float = DEFAULT_RIDGE) -> HysimeResult:
     tol = HYSIME_TOL * float(np.max(np.abs(p)))
     k = int(np.count_nonzero(delta < -tol))
     return HysimeResult(k, e[:, asc[:k]], delta, mu, e, r_n, r_y)
+
+
+# ----------------------------------------------------------------------------
+# F2: FORPDN
+# ----------------------------------------------------------------------------
+FORPDN_GRID = (0.1, 1.0, 10.0, 100.0)   # SPEC.md:432 D16
+
+
+def spectral_difference(b: int) -> np.ndarray:
+    """D ((b-1) x b): first-order spectral difference, (D x)_i = x_{i+1} - x_i."""
+    d = np.zeros((b - 1, b))
+    for i in range(b - 1):
+        d[i, i] = -1.0
+        d[i, i + 1] = 1.0
+    return d
+
+
+@dataclass
+class ForpdnResult:
+    out: np.ndarray         # float32 BSQ
+    lam: float
+    residual_power: dict    # lambda -> ||W - X(lambda)||_F^2 / (N B)
+    noise_power: float      # trace(R_n) / B (HySime's noise estimate, SPEC.md:432)
+
+
+def forpdn(cube: np.ndarray, lam: Optional[float] = None, taps: int = DEFAULT_TAPS, levels: int = 0,
+           ridge: float = DEFAULT_RIDGE) -> ForpdnResult:
+    """FORPDN (SPEC.md:388-396 D16; "full-rank, wavelet-based"):
+    W (N_c x B) = per-band 2-D DWT coefficients (the C4 transform of every band
+    image); X = argmin ||W - X||_F^2 + lam ||X D^T||_F^2 = W (I + lam D^T D)^-1
+    (one B x B solve for every coefficient row); the output is the per-band
+    inverse DWT of X.  Default lam (SPEC.md:432 D16): from {0.1, 1, 10, 100},
+    the one whose residual power ||W - X||^2 / (N B) is closest to HySime's
+    noise power trace(R_n) / B (first on ties) -- reading R14: the residual is
+    taken in the coefficient domain (equal to the image-domain residual by
+    Parseval when 2^L divides R and C)."""
+    cube = np.asarray(cube)
+    b, r, c = cube.shape
+    if b < 2:
+        raise ValueError("bands >= 2 required (SPEC.md:392)")
+    lv = levels or auto_levels(r, c, taps)
+    check_levels(r, c, lv)
+    tmpl = dwt2(np.zeros((r, c)), lv, taps)
+    rows = [np.concatenate([s.ravel() for s in flatten_coeffs(dwt2(cube[i].astype(np.float64), lv, taps))])
+            for i in range(b)]
+    w = np.stack(rows, axis=1)                          # N_c x B
+    d = spectral_difference(b)
+    n = r * c
+
+    def solve(lmb):
+        a = np.eye(b) + lmb * (d.T @ d)
+        return w @ np.linalg.inv(a)                     # X = W A^-1 (A symmetric)
+
+    res_pow, noise_pow = {}, None
+    if lam is None:
+        res = noise_residual(cube, ridge)
+        noise_pow = float(np.trace(res @ res.T) / n / b)
+        best = None
+        for lmb in FORPDN_GRID:
+            x = solve(lmb)
+            rp = float(np.sum((w - x) ** 2) / (n * b))
+            res_pow[lmb] = rp
+            if best is None or abs(rp - noise_pow) < abs(res_pow[best] - noise_pow):
+                best = lmb
+        lam = best
+    if not lam > 0:
+        raise ValueError("lambda > 0 required (SPEC.md:392)")
+    x = solve(lam)
+    sizes = [s.size for s in flatten_coeffs(tmpl)]
+    offs = np.cumsum([0] + sizes)
+    out = np.empty((b, r, c))
+    for i in range(b):
+        subs = [x[offs[j]:offs[j + 1], i].reshape(flatten_coeffs(tmpl)[j].shape) for j in range(len(sizes))]
+        out[i] = idwt2(unflatten_coeffs(subs, tmpl), taps)
+    return ForpdnResult(out.astype(np.float32), float(lam), res_pow, noise_pow)

@@ -461,3 +461,60 @@ def test_f1_eigen_identities():
     p = np.einsum("ij,ik,kj->j", h.E, h.r_y, h.E)
     s2 = np.einsum("ij,ik,kj->j", h.E, h.noise_cov, h.E)
     assert np.max(np.abs((p - s2) - h.mu)) < 1e-12 * np.max(np.abs(h.mu))
+
+
+# ---------------------------------------------------------------- F2: FORPDN
+def test_f2_closed_form_is_the_minimiser():
+    """X = W (I + lam D^T D)^-1 satisfies the normal equations of
+    min ||W - X||^2 + lam ||X D^T||^2: (X - W) + lam X D^T D = 0; and the
+    objective grows along random perturbations."""
+    rng = np.random.default_rng(31)
+    b = 9
+    w = rng.standard_normal((50, b))
+    d = O.spectral_difference(b)
+    assert np.allclose(d @ np.arange(b, dtype=float), np.ones(b - 1))
+    lam = 3.0
+    x = w @ np.linalg.inv(np.eye(b) + lam * d.T @ d)
+    assert np.max(np.abs((x - w) + lam * x @ d.T @ d)) < 1e-12
+    f = lambda z: np.sum((w - z) ** 2) + lam * np.sum((z @ d.T) ** 2)   # noqa: E731
+    for _ in range(5):
+        assert f(x + 1e-3 * rng.standard_normal(x.shape)) > f(x)
+
+
+def test_f2_spec_examples():
+    """lam -> 0+ gives the input back (1e-3); linearity in the input
+    (1e-4 relative, fixed lam); spectrally smooth cube + 20 dB noise, lam = 10 ->
+    PSNR gain >= 5 dB."""
+    rng = np.random.default_rng(32)
+    b, r, c = 60, 32, 32
+    t = np.arange(b)
+    # spectrally smooth: Gaussian bumps 18 bands wide
+    spectra = np.stack([np.exp(-0.5 * ((t - m) / 18.0) ** 2) + 0.2 for m in (10, 30, 50)])
+    ab = rng.random((3, r * c))
+    clean = (spectra.T @ ab).reshape(b, r, c)
+    out0 = O.forpdn(clean.astype(np.float32), lam=1e-8, levels=2).out
+    assert np.max(np.abs(out0 - clean)) < 1e-3 * np.max(np.abs(clean))
+    x = rng.standard_normal((b, r, c)).astype(np.float32)
+    o1 = O.forpdn(x, lam=2.0, levels=2).out.astype(np.float64)
+    o2 = O.forpdn((3.0 * x).astype(np.float32), lam=2.0, levels=2).out.astype(np.float64)
+    assert np.linalg.norm(o2 - 3.0 * o1) <= 1e-4 * np.linalg.norm(o2)
+    sig = np.sqrt(np.mean(clean ** 2) / 10 ** 2)
+    noisy = (clean + sig * rng.standard_normal(clean.shape)).astype(np.float32)
+    den = O.forpdn(noisy, lam=10.0, levels=2).out
+    gain = 10 * np.log10(np.mean((noisy - clean) ** 2) / np.mean((den - clean) ** 2))
+    assert gain >= 5.0, gain
+
+
+def test_f2_default_lambda_from_grid():
+    """D16: the default lambda is the grid value whose residual power is closest to
+    HySime's noise power; the residual power grows with lambda."""
+    rng = np.random.default_rng(33)
+    b, r, c = 16, 32, 32
+    t = np.linspace(0, 1, b)
+    clean = (np.outer(np.cos(3 * t) + 2, rng.random(r * c))).reshape(b, r, c)
+    noisy = (clean + 0.05 * rng.standard_normal(clean.shape)).astype(np.float32)
+    res = O.forpdn(noisy, levels=2)
+    assert res.lam in O.FORPDN_GRID
+    rp = [res.residual_power[l] for l in O.FORPDN_GRID]
+    assert all(rp[i] < rp[i + 1] for i in range(len(rp) - 1))
+    assert res.lam == min(O.FORPDN_GRID, key=lambda l: abs(res.residual_power[l] - res.noise_power))
