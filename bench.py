@@ -383,6 +383,32 @@ def main():
             ts.append(time.perf_counter() - t0)
         hys = {"ms": round(1e3 * statistics.median(ts), 4), "k": hres["k"], "bands": cfg.bands,
                "timing": "host wall clock of the synchronous call (returns k), median of 3"}
+    fpd = None
+    if args.iso_steps > 0 and not batched and not sharded and rank == 0:
+        # F2: FORPDN with the D16 default lambda -- Gram +
+        # sweep (noise power), per-band DWT, lambda selection on B x B matrices,
+        # Thomas solve along the bands, per-band IDWT
+        fout = torch.empty_like(cube)
+        _, flam = hy.forpdn(cube, fout, return_lambda=True)
+        torch.cuda.synchronize()
+        st_ = torch.cuda.current_stream()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(st_)
+        for _ in range(3):
+            hy.forpdn(cube, fout)
+        f1.record(st_)
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / 3
+        hbm_, _, _ = peaks()
+        lvl = hy.stages.auto_levels(cfg.rows, cfg.cols)
+        ncf = coeff_count(cfg.rows, cfg.cols, lvl)
+        fb = (2 * cfg.bands * dwt_image_bytes(cfg.rows, cfg.cols, lvl)   # per-band DWT + IDWT levels
+              + 2 * 4 * cfg.bands * cfg.rows * cfg.cols                   # Gram: amax + quantised read
+              + 8 * cfg.bands * ncf)                                       # solve: read W, write X
+        fpd = {"ms": round(fms, 4), "lambda": flam, "bytes": fb, "GBps": round(fb / (fms * 1e-3) / 1e9, 1),
+               "frac_hbm": round(fb / (fms * 1e-3) / 1e9 / hbm_, 4),
+               "timing": "CUDA events over 3 calls (lambda by D16 each call)"}
+        del fout
     iso = None
     if args.iso_steps > 0 and not batched and not sharded and rank == 0:
         hbm_, _, _ = peaks()
@@ -513,6 +539,8 @@ def main():
         line["wavelet_isolated"] = iso
     if hys is not None:
         line["hysime"] = hys
+    if fpd is not None:
+        line["forpdn"] = fpd
     if world == 1 and not args.no_cpu_baseline:
         t, cores, thr = cpu_baseline(cubes_h[0], reps=2)
         line["cpu_baseline"] = {"value": cfg.voxels / t, "unit": UNIT, "cores": cores, "threads": thr,

@@ -176,6 +176,20 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
 hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, int bands, int* k_out,
                         double* basis, double* delta, double* mu, double* noise_cov, hyde_stream_t stream);
 
+/* --- F2: FORPDN ("full-rank,
+ * wavelet-based"): W = per-band 2-D DWT of every band (the A4 transform: taps
+ * 0 = 16, levels 0 = auto), X = W (I + lambda D^T D)^-1 with D the first-order
+ * spectral difference (A = I + lambda D^T D is tridiagonal: one Thomas solve
+ * along the bands per coefficient), out = per-band inverse DWT of X.  lambda <= 0
+ * -> HYDE_EPARAM except 0 = the D16 default: the grid value {0.1, 1, 10, 100}
+ * whose residual power ||W - X||^2 / (N B) (coefficient domain) is closest to
+ * HySime's noise power trace(R_n) / B (R14).  cube / out: DEVICE BSQ
+ * (out == cube allowed).  lambda_out (HOST, may be NULL) receives the lambda
+ * used; when it is non-NULL and lambda == 0 the call synchronizes.  bands in
+ * [2, 256] ([3, 256] and pixels > bands for the default lambda). */
+hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
+                        double lambda, int taps, int levels, double* lambda_out, hyde_stream_t stream);
+
 /* Bytes of device workspace hyde_hyres_ex / _batched will hold for this shape. */
 size_t hyde_hyres_workspace_size(int rows, int cols, int bands, int batch,
                                  const hyde_hyres_params* params);

@@ -255,6 +255,21 @@ def estimate_noise(cube, *, return_gram=False, return_residual=False):
     return out[0] if len(out) == 1 else out
 
 
+def forpdn(cube, out=None, *, lam=0.0, taps=16, levels=0, return_lambda=False):
+    """FORPDN (F2; include/hyde.h hyde_forpdn).  lam = 0: the D16 default from
+    {0.1, 1, 10, 100}.  Returns out [, lambda used]."""
+    torch = _torch()
+    _cube(cube)
+    b, r, c = cube.shape
+    if out is None:
+        out = torch.empty_like(cube)
+    lo = ctypes.c_double(0.0)
+    h = handle(cube.device.index)
+    check(lib().hyde_forpdn(h, cube.data_ptr(), r, c, b, out.data_ptr(), float(lam), int(taps), int(levels),
+                            ctypes.byref(lo), _stream(cube)), h)
+    return (out, float(lo.value)) if return_lambda else out
+
+
 def hysime(cube):
     """HySime signal-subspace identification (F1; include/hyde.h hyde_hysime):
     returns dict(k, basis (bands, k) fp64, delta (bands,), mu (bands,), noise_cov (bands, bands))."""

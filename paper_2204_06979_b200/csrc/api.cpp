@@ -925,6 +925,88 @@ hyde_status hyde_estimate_noise(hyde_handle h, const float* cube, int rows, int 
 }
 
 // ---------------------------------------------------------------- stages
+hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out, double lambda,
+                        int taps, int levels, double* lambda_out, hyde_stream_t stream) {
+  if (!h) return HYDE_EPARAM;
+  if (!cube || !out) return fail(h, HYDE_EPARAM, "NULL cube/out");
+  if (bands < 2 || rows < 1 || cols < 1) return fail(h, HYDE_EPARAM, "bands >= 2 required (SPEC.md:392)");
+  if (bands > 256) return fail(h, HYDE_EPARAM, "bands <= 256");
+  if (lambda < 0.0) return fail(h, HYDE_EPARAM, "lambda > 0 required (SPEC.md:392); 0 = D16 default");
+  const bool autolam = lambda == 0.0;
+  if (autolam && (bands < 3 || (long long)rows * cols <= bands))
+    return fail(h, HYDE_EPARAM, "the default lambda needs HySime's noise estimate: bands >= 3, pixels > bands");
+  const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
+  if (cube != out && overlap(cube, bytes, out, bytes)) return fail(h, HYDE_EPARAM, "cube and out partially overlap");
+  hyde_hyres_params pin;
+  hyde_hyres_params_default(&pin);
+  pin.wavelet_taps = taps;
+  pin.levels = levels;
+  hyde_hyres_params p;
+  int lv = 0;
+  hyde_status s = resolve_params(h, rows, cols, &pin, &p, &lv);
+  if (s != HYDE_OK) return s;
+  FilterBank fb;
+  if (hyde_build_filters(p.wavelet_taps, &fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "filter derivation failed");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = bands;
+  Layout L;
+  make_layout(rows, cols, B, B, lv, p.wavelet_taps, &L);
+  const size_t BB = (size_t)B * B;
+  const long long nc = L.plan.n_coeffs;
+  size_t off = L.total;
+  auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
+  const size_t oZ = take(4 * BB * 8), oRp = take(4 * 8), oNp = take(8), oLam = take(8), oGw = take(BB * 8);
+  const int np2 = gram_tc_npairs(nc);
+  const int ns2 = gram_nsplit(nc, B);
+  const size_t oPart = take((size_t)(np2 > ns2 ? np2 : ns2) * BB * 8), oAmax = take((size_t)B * 4);
+  s = ensure_ws(h, off, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  RankState* rs = (RankState*)(ws + L.rs);
+  h->last_rs = rs;
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  float* C = (float*)(ws + L.C);
+  double* lam_dev = (double*)(ws + oLam);
+  const long long n = L.n;
+  if (autolam) {
+    // D16: residual power of each grid lambda vs HySime's noise power (F1)
+    double* G = (double*)(ws + L.G);
+    double* house = (double*)(ws + L.house);
+    CK(run_gram(L, ws, cube, G, &rs->nonfinite, st));
+    CK(launch_noise_eig(G, n, B, 1e-6, -1, 0, (double*)(ws + L.sigma), nullptr, nullptr, house,
+                        (double*)(ws + L.tri), nullptr, nullptr, B, st));
+    CK(dwt_forward(L, ws, cube, n, B, fb, st));
+    const double* Gw = G;   // = W^T W when the DWT is orthonormal on the image (N_c == N)
+    if (nc != n) {          // padded levels: the band Gram of the coefficients themselves
+      double* Gc = (double*)(ws + oGw);
+      if (gram_tc_supported(B))
+        CK(launch_gram_tc(C, nc, B, (unsigned*)(ws + oAmax), (double*)(ws + oPart), np2, Gc, &rs->nonfinite, st));
+      else
+        CK(launch_gram(C, nc, B, (double*)(ws + oPart), ns2, Gc, &rs->nonfinite, st));
+      Gw = Gc;
+    }
+    CK(launch_forpdn_lambda(house + 3 * BB, Gw, B, n, 1e-6, (double*)(ws + oNp), (double*)(ws + oRp), lam_dev,
+                            (double*)(ws + oZ), st));
+  } else {
+    CK(dwt_forward(L, ws, cube, n, B, fb, st));
+  }
+  // X = W (I + lam D^T D)^-1: one Thomas solve along the bands per coefficient, in place
+  CK(launch_forpdn_solve(C, nc, nc, B, lambda, autolam ? lam_dev : nullptr, st));
+  CK(dwt_inverse(L, ws, C, out, n, B, fb, nullptr, st));
+  if (lambda_out) {
+    if (autolam) {
+      double lv_host = 0.0;
+      CK(cudaMemcpyAsync(&lv_host, lam_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      *lambda_out = lv_host;
+    } else {
+      *lambda_out = lambda;
+    }
+  }
+  return HYDE_OK;
+}
+
 hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, int bands, int* k_out, double* basis,
                         double* delta, double* mu, double* noise_cov, hyde_stream_t stream) {
   hyde_status s = validate_shape(h, rows, cols, bands);

@@ -70,6 +70,11 @@ size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,
                              double* tri, float* W, float* U, int ldwu, cudaStream_t st);
+// F2: FORPDN (k_forpdn.cu)
+cudaError_t launch_forpdn_lambda(const double* M, const double* Gw, int B, long long n, double ridge, double* npow,
+                                 double* rp, double* lam_out, double* Zs, cudaStream_t st);
+cudaError_t launch_forpdn_solve(float* C, long long ldc, long long nc, int B, double lam, const double* lam_dev,
+                                cudaStream_t st);
 // F1: HySime (k_hysime.cu)
 cudaError_t launch_hysime_prep(const double* G, const double* M, int B, long long n, double ridge, double* Ry,
                                double* Rn, double* Rx, cudaStream_t st);
