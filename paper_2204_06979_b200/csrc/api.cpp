@@ -1052,10 +1052,7 @@ hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, in
   // every eigenpair of R_x: the first chunk in the cluster kernel, the rest from its T and Q
   const int k1 = B < HYDE_MAX_CHUNK ? B : HYDE_MAX_CHUNK;
   CK(launch_eig_raw(Rx, B, k1, ones, lam, V, B, house, tri, W, U, B, st));
-  for (int k0 = k1; k0 < B; k0 += HYDE_MAX_CHUNK) {
-    const int kc = (B - k0) < HYDE_MAX_CHUNK ? (B - k0) : HYDE_MAX_CHUNK;
-    CK(launch_eig_more_raw(tri, house, ones, B, k0, kc, lam, V, B, W, U, B, st));
-  }
+  if (k1 < B) CK(launch_eig_more_raw(tri, house, ones, B, k1, B - k1, lam, V, B, W, U, B, st));   // one CTA per pair
   CK(launch_hysime_delta(V, B, Ry, Rn, B, (double*)(ws + oP), (double*)(ws + oS2), dl, st));
   CK(launch_hysime_select(dl, (double*)(ws + oP), B, 1e-9, V, B, basis ? (double*)(ws + oB) : nullptr,
                           (int*)(ws + oK), st));
