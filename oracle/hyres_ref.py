@@ -541,3 +541,84 @@ def forpdn(cube: np.ndarray, lam: Optional[float] = None, taps: int = DEFAULT_TA
         subs = [x[offs[j]:offs[j + 1], i].reshape(flatten_coeffs(tmpl)[j].shape) for j in range(len(sizes))]
         out[i] = idwt2(unflatten_coeffs(subs, tmpl), taps)
     return ForpdnResult(out.astype(np.float32), float(lam), res_pow, noise_pow)
+
+
+# ----------------------------------------------------------------------------
+# F4: WSRRR
+# ----------------------------------------------------------------------------
+@dataclass
+class WsrrrResult:
+    out: np.ndarray             # float32 BSQ denoised cube
+    components: np.ndarray      # float32 (rank, R, C): inverse DWT of the columns of C
+    V: np.ndarray               # B x rank, column-orthonormal
+    objective: List[float]      # per sweep
+    lam: float
+    rank: int
+
+
+def band_dwt_matrix(cube: np.ndarray, levels: int, taps: int) -> np.ndarray:
+    """W (N_c x B): the C4 DWT of every band image, one column per band."""
+    cols = [np.concatenate([s.ravel() for s in flatten_coeffs(dwt2(cube[i].astype(np.float64), levels, taps))])
+            for i in range(cube.shape[0])]
+    return np.stack(cols, axis=1)
+
+
+def band_idwt_matrix(x: np.ndarray, rows: int, cols: int, levels: int, taps: int) -> np.ndarray:
+    """Inverse of band_dwt_matrix for the columns of x (N_c x m) -> (m, R, C)."""
+    tmpl = dwt2(np.zeros((rows, cols)), levels, taps)
+    shapes = [s.shape for s in flatten_coeffs(tmpl)]
+    offs = np.cumsum([0] + [int(np.prod(sh)) for sh in shapes])
+    out = np.empty((x.shape[1], rows, cols))
+    for i in range(x.shape[1]):
+        subs = [x[offs[j]:offs[j + 1], i].reshape(shapes[j]) for j in range(len(shapes))]
+        out[i] = idwt2(unflatten_coeffs(subs, tmpl), taps)
+    return out
+
+
+def wsrrr(cube: np.ndarray, rank: Optional[int] = None, lam: Optional[float] = None, max_iters: int = 20,
+          tol: float = 1e-4, taps: int = DEFAULT_TAPS, levels: int = 0, ridge: float = DEFAULT_RIDGE) -> WsrrrResult:
+    """WSRRR (SPEC.md:397-405 D17; §2.1 "Wavelet-Based Sparse Reduced-Rank
+    Regression"): min_{C,V} ||W - C V^T||_F^2 + lam ||C||_1 s.t. V^T V = I, with W
+    (N_c x B) the per-band DWT coefficients.  Alternating: C = soft(W V, lam/2)
+    (the exact minimiser over C for orthonormal V, since ||W - C V^T||^2 =
+    ||W V - C||^2 + const); V = P Q^T from the SVD P S Q^T = W^T C (orthogonal
+    Procrustes).  Readings (R15): V_0 = the top-rank eigenvectors of
+    W^T W (D6 signs); one sweep = C-step then V-step, the objective evaluated
+    after the sweep; stop when |f_prev - f| <= tol f_prev or after max_iters
+    sweeps; default rank = HySime's k (at least 1); default lam (D17) =
+    sigma^ sqrt(2 ln N_c), sigma^ = sqrt(mean_b sigma_b^2) from estimate_noise.
+    Output: inverse DWT of C V^T per band; components: inverse DWT of the
+    columns of C."""
+    cube = np.asarray(cube)
+    b, r, c = cube.shape
+    lv = levels or auto_levels(r, c, taps)
+    check_levels(r, c, lv)
+    if rank is None:
+        rank = max(1, hysime(cube, ridge).k)
+    if rank < 1 or rank > b:
+        raise ValueError("1 <= rank <= bands required (SPEC.md:401)")
+    w = band_dwt_matrix(cube, lv, taps)
+    nc = w.shape[0]
+    if lam is None:
+        sigma, _ = estimate_noise(cube, ridge)
+        lam = float(np.sqrt(np.mean(sigma ** 2)) * np.sqrt(2.0 * np.log(nc)))
+    if lam < 0:
+        raise ValueError("lambda >= 0 required")
+    g = w.T @ w
+    mu, e = np.linalg.eigh(g)
+    order = np.argsort(-mu, kind="stable")
+    v = sign_fix(e[:, order])[:, :rank]
+    obj = []
+    cmat = None
+    for _ in range(max_iters):
+        cmat = soft_threshold(w @ v, lam / 2.0)
+        m = w.T @ cmat
+        p, _, qt = np.linalg.svd(m, full_matrices=False)
+        v = p @ qt
+        f = float(np.sum((w - cmat @ v.T) ** 2) + lam * np.sum(np.abs(cmat)))
+        obj.append(f)
+        if len(obj) > 1 and abs(obj[-2] - obj[-1]) <= tol * obj[-2]:
+            break
+    out = band_idwt_matrix(cmat @ v.T, r, c, lv, taps)
+    comps = band_idwt_matrix(cmat, r, c, lv, taps)
+    return WsrrrResult(out.astype(np.float32), comps.astype(np.float32), v, obj, float(lam), int(rank))

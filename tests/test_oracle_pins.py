@@ -518,3 +518,51 @@ def test_f2_default_lambda_from_grid():
     rp = [res.residual_power[l] for l in O.FORPDN_GRID]
     assert all(rp[i] < rp[i + 1] for i in range(len(rp) - 1))
     assert res.lam == min(O.FORPDN_GRID, key=lambda l: abs(res.residual_power[l] - res.noise_power))
+
+
+# ---------------------------------------------------------------- F4: WSRRR
+def test_f4_spec_lossless_full_rank():
+    """lam = 0, rank = bands -> denoised ~= input within 1e-3."""
+    rng = np.random.default_rng(51)
+    x = rng.standard_normal((8, 32, 32)).astype(np.float32)
+    res = O.wsrrr(x, rank=8, lam=0.0, levels=2)
+    assert np.max(np.abs(res.out - x)) < 1e-3 * np.max(np.abs(x))
+    assert np.max(np.abs(res.V.T @ res.V - np.eye(8))) < 1e-10
+
+
+def test_f4_spec_rank4_gain_and_monotone():
+    """SPEC.md:403-404: rank-4 synthetic cube at 20 dB, rank = 4 -> PSNR gain >= 8 dB;
+    the objective never increases (1e-6 relative slack); components count == rank."""
+    rng = np.random.default_rng(52)
+    b, r, c = 30, 64, 64
+    t = np.arange(b)
+    spectra = np.stack([np.exp(-0.5 * ((t - m) / 6.0) ** 2) for m in (4, 11, 18, 25)])
+    ab = np.stack([np.kron(rng.random((8, 8)), np.ones((8, 8))).ravel() for _ in range(4)])   # piecewise-constant
+    clean = (spectra.T @ ab).reshape(b, r, c)
+    sig = np.sqrt(np.mean(clean ** 2) / 100.0)
+    noisy = (clean + sig * rng.standard_normal(clean.shape)).astype(np.float32)
+    res = O.wsrrr(noisy, rank=4, levels=3, taps=2)   # piecewise-constant abundances: Haar-sparse
+    gain = 10 * np.log10(np.mean((noisy - clean) ** 2) / np.mean((res.out - clean) ** 2))
+    assert gain >= 8.0, gain
+    f = res.objective
+    assert all(f[i + 1] <= f[i] * (1 + 1e-6) for i in range(len(f) - 1))
+    assert res.components.shape == (4, r, c)
+    assert np.max(np.abs(res.V.T @ res.V - np.eye(4))) < 1e-10
+
+
+def test_f4_steps_are_the_block_minimisers():
+    """C-step: soft(W V, lam/2) beats perturbations of C for the fixed V; V-step: the
+    Procrustes V maximises tr(V^T W^T C) against random orthonormal V."""
+    rng = np.random.default_rng(53)
+    w = rng.standard_normal((200, 6))
+    v, _ = np.linalg.qr(rng.standard_normal((6, 2)))
+    lam = 0.7
+    cm = O.soft_threshold(w @ v, lam / 2.0)
+    f = lambda cc, vv: np.sum((w - cc @ vv.T) ** 2) + lam * np.sum(np.abs(cc))   # noqa: E731
+    for _ in range(5):
+        assert f(cm + 1e-3 * rng.standard_normal(cm.shape), v) > f(cm, v)
+    p, _, qt = np.linalg.svd(w.T @ cm, full_matrices=False)
+    vb = p @ qt
+    for _ in range(20):
+        q, _ = np.linalg.qr(rng.standard_normal((6, 2)))
+        assert np.trace(q.T @ w.T @ cm) <= np.trace(vb.T @ w.T @ cm) + 1e-12
