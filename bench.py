@@ -408,7 +408,24 @@ def main():
         fpd = {"ms": round(fms, 4), "lambda": flam, "bytes": fb, "GBps": round(fb / (fms * 1e-3) / 1e9, 1),
                "frac_hbm": round(fb / (fms * 1e-3) / 1e9 / hbm_, 4),
                "timing": "CUDA events over 3 calls (lambda by D16 each call)"}
-        del fout
+        # F4: WSRRR with the D17 defaults (rank = HySime's k)
+        wout = torch.empty_like(cube)
+        hy.wsrrr(cube, wout)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        wres = hy.wsrrr(cube, wout)
+        torch.cuda.synchronize()
+        wms = (time.perf_counter() - t0) * 1e3
+        nsw = len(wres["objective"])
+        wb = (2 * cfg.bands * dwt_image_bytes(cfg.rows, cfg.cols, lvl)       # per-band DWT + IDWT levels
+              + nsw * 2 * 4 * cfg.bands * ncf)                                 # each sweep reads W twice
+        fpd_w = {"ms": round(wms, 3), "rank": wres["rank"], "lambda": wres["lam"], "sweeps": nsw,
+                 "bytes": wb, "GBps": round(wb / (wms * 1e-3) / 1e9, 1),
+                 "frac_hbm": round(wb / (wms * 1e-3) / 1e9 / hbm_, 4),
+                 "timing": "host wall clock of the synchronous call (includes HySime for the rank)"}
+        del fout, wout
+    else:
+        fpd_w = None
     iso = None
     if args.iso_steps > 0 and not batched and not sharded and rank == 0:
         hbm_, _, _ = peaks()
@@ -541,6 +558,8 @@ def main():
         line["hysime"] = hys
     if fpd is not None:
         line["forpdn"] = fpd
+    if fpd_w is not None:
+        line["wsrrr"] = fpd_w
     if world == 1 and not args.no_cpu_baseline:
         t, cores, thr = cpu_baseline(cubes_h[0], reps=2)
         line["cpu_baseline"] = {"value": cfg.voxels / t, "unit": UNIT, "cores": cores, "threads": thr,

@@ -190,6 +190,25 @@ hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, in
 hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
                         double lambda, int taps, int levels, double* lambda_out, hyde_stream_t stream);
 
+/* --- F4: WSRRR (SPEC.md:397-405, :433 D17; §2.1
+ * "Wavelet-Based Sparse Reduced-Rank Regression"): min_{C,V} ||W - C V^T||_F^2 +
+ * lambda ||C||_1 s.t. V^T V = I, W = per-band DWT coefficients (taps 0 = 16,
+ * levels 0 = auto).  V_0 = top-rank eigenvectors of W^T W; per sweep C =
+ * soft(W V, lambda/2), V = polar factor of W^T C (orthogonal Procrustes); stop
+ * when the objective changes by <= tol (relative; < 0 -> 1e-4) or after
+ * max_iters sweeps (<= 0 -> 20) (R15).  rank 0 = HySime's k (at
+ * least 1), else 1..min(bands, 32); lambda < 0 = the D17 default
+ * sigma^ sqrt(2 ln N_c), sigma^ = RMS of the A1 noise estimate; lambda >= 0 is
+ * used as given.  out: DEVICE BSQ denoised cube (inverse DWT of C V^T per
+ * band); components: DEVICE (rank x rows x cols) inverse DWT of the columns of
+ * C, or NULL.  HOST outputs (may be NULL): rank_out, lambda_out, sweeps_out,
+ * objective_out[max_iters] (objective after each sweep).  Synchronous (one
+ * host read of the objective per sweep). */
+hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int bands, int rank,
+                       double lambda, int taps, int levels, int max_iters, double tol, float* out,
+                       float* components, int* rank_out, double* lambda_out, int* sweeps_out,
+                       double* objective_out, hyde_stream_t stream);
+
 /* Bytes of device workspace hyde_hyres_ex / _batched will hold for this shape. */
 size_t hyde_hyres_workspace_size(int rows, int cols, int bands, int batch,
                                  const hyde_hyres_params* params);

@@ -255,6 +255,26 @@ def estimate_noise(cube, *, return_gram=False, return_residual=False):
     return out[0] if len(out) == 1 else out
 
 
+def wsrrr(cube, out=None, *, rank=0, lam=-1.0, taps=16, levels=0, max_iters=20, tol=1e-4, components=False):
+    """WSRRR (F4; include/hyde.h hyde_wsrrr).  rank 0 = HySime's k, lam < 0 = D17
+    default.  Returns dict(out, components (rank, R, C) or None, rank, lam, objective)."""
+    torch = _torch()
+    _cube(cube)
+    b, r, c = cube.shape
+    if out is None:
+        out = torch.empty_like(cube)
+    comps = torch.empty((max(rank, 0) or b, r, c), dtype=torch.float32, device=cube.device) if components else None
+    rk, sw = ctypes.c_int(0), ctypes.c_int(0)
+    lo = ctypes.c_double(0.0)
+    objs = (ctypes.c_double * max(max_iters, 1))()
+    h = handle(cube.device.index)
+    check(lib().hyde_wsrrr(h, cube.data_ptr(), r, c, b, int(rank), float(lam), int(taps), int(levels), int(max_iters),
+                           float(tol), out.data_ptr(), comps.data_ptr() if comps is not None else None,
+                           ctypes.byref(rk), ctypes.byref(lo), ctypes.byref(sw), objs, _stream(cube)), h)
+    return {"out": out, "components": comps[:rk.value] if comps is not None else None, "rank": int(rk.value),
+            "lam": float(lo.value), "objective": [objs[i] for i in range(sw.value)]}
+
+
 def forpdn(cube, out=None, *, lam=0.0, taps=16, levels=0, return_lambda=False):
     """FORPDN (F2; include/hyde.h hyde_forpdn).  lam = 0: the D16 default from
     {0.1, 1, 10, 100}.  Returns out [, lambda used]."""

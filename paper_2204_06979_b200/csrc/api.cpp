@@ -8,6 +8,7 @@
 //       rank decision (device) -> one D2H read of the 16-byte rank state ->
 //       K6a IDWT of the chunk's kept components
 //   -> K6b reconstruct (single write of the BSQ output).
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -925,6 +926,121 @@ hyde_status hyde_estimate_noise(hyde_handle h, const float* cube, int rows, int 
 }
 
 // ---------------------------------------------------------------- stages
+hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int bands, int rank, double lambda,
+                       int taps, int levels, int max_iters, double tol, float* out, float* components,
+                       int* rank_out, double* lambda_out, int* sweeps_out, double* objective_out,
+                       hyde_stream_t stream) {
+  hyde_status s = validate_shape(h, rows, cols, bands);
+  if (s != HYDE_OK) return s;
+  if (!cube || !out) return fail(h, HYDE_EPARAM, "NULL cube/out");
+  if (rank < 0 || rank > bands || rank > HYDE_MAX_CHUNK) return fail(h, HYDE_EPARAM, "rank must be in [0, min(bands, 32)] (SPEC.md:401)");
+  if (max_iters < 1) max_iters = 20;
+  if (!(tol >= 0.0)) tol = 1e-4;
+  const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
+  if (cube != out && overlap(cube, bytes, out, bytes)) return fail(h, HYDE_EPARAM, "cube and out partially overlap");
+  if (rank == 0) {   // D17: default rank = HySime's k (at least 1)
+    int k = 0;
+    s = hyde_hysime(h, cube, rows, cols, bands, &k, nullptr, nullptr, nullptr, nullptr, stream);
+    if (s != HYDE_OK) return s;
+    rank = k < 1 ? 1 : (k > HYDE_MAX_CHUNK ? HYDE_MAX_CHUNK : k);
+  }
+  hyde_hyres_params pin;
+  hyde_hyres_params_default(&pin);
+  pin.wavelet_taps = taps;
+  pin.levels = levels;
+  hyde_hyres_params p;
+  int lv = 0;
+  s = resolve_params(h, rows, cols, &pin, &p, &lv);
+  if (s != HYDE_OK) return s;
+  FilterBank fb;
+  if (hyde_build_filters(p.wavelet_taps, &fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "filter derivation failed");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = bands, r = rank;
+  Layout L;
+  make_layout(rows, cols, B, B, lv, p.wavelet_taps, &L);
+  const size_t BB = (size_t)B * B;
+  const long long nc = L.plan.n_coeffs, n = L.n;
+  size_t off = L.total;
+  auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
+  const size_t oGw = take(BB * 8), oV = take(BB * 8), oM = take(BB * 8), oLam = take((size_t)B * 8),
+               oOnes = take((size_t)B * 8), oScal = take(16 * 8), oPart = take(1024 * 8),
+               oWtc = take((size_t)wtc_chunks(nc, r) * B * r * 8), oObj = take((size_t)max_iters * 8);
+  const int np2 = gram_tc_npairs(nc);
+  const int ns2 = gram_nsplit(nc, B);
+  const size_t oGp = take((size_t)(np2 > ns2 ? np2 : ns2) * BB * 8), oAmax = take((size_t)B * 4);
+  s = ensure_ws(h, off, st);
+  if (s != HYDE_OK) return s;
+  char* ws = h->ws;
+  RankState* rs = (RankState*)(ws + L.rs);
+  h->last_rs = rs;
+  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  float* Cw = (float*)(ws + L.C);          // W: B x N_c (band-major)
+  float* Cc = (float*)(ws + L.surv);       // C: r x N_c
+  double* V = (double*)(ws + oV);
+  double* M = (double*)(ws + oM);
+  double* sc = (double*)(ws + oScal);      // [0] lam [1] ||W||^2 [2] ||C||^2 [3] ||C||_1
+  double* obj = (double*)(ws + oObj);
+  float* V32 = (float*)(ws + L.W);         // B x B fp32, ld = B
+  double* G = (double*)(ws + L.G);
+  double* house = (double*)(ws + L.house);
+  double* tri = (double*)(ws + L.tri);
+  CK(dwt_forward(L, ws, cube, n, B, fb, st));
+  // V_0: top-r eigenvectors of W^T W (K1 Gram of the coefficients, K2 raw mode)
+  double* Gw = G;
+  if (nc == n) {
+    CK(run_gram(L, ws, cube, G, &rs->nonfinite, st));
+  } else {
+    Gw = (double*)(ws + oGw);
+    if (gram_tc_supported(B))
+      CK(launch_gram_tc(Cw, nc, B, (unsigned*)(ws + oAmax), (double*)(ws + oGp), np2, Gw, &rs->nonfinite, st));
+    else
+      CK(launch_gram(Cw, nc, B, (double*)(ws + oGp), ns2, Gw, &rs->nonfinite, st));
+  }
+  if (lambda < 0.0) {   // D17: sigma^ sqrt(2 ln N_c), sigma^ from the regression noise estimate
+    double* Gy = G;
+    if (nc != n) CK(run_gram(L, ws, cube, Gy, &rs->nonfinite, st));
+    CK(launch_noise_eig(Gy, n, B, 1e-6, -1, 0, (double*)(ws + L.sigma), nullptr, nullptr, house, tri, nullptr,
+                        nullptr, B, st));
+    CK(launch_wsrrr_lambda((double*)(ws + L.sigma), B, nc, sc, st));
+  } else {
+    CK(cudaMemcpyAsync(sc, &lambda, sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  CK(launch_eig_raw(Gw, B, r, (double*)(ws + oOnes), (double*)(ws + oLam), V, r, house, tri, (float*)(ws + L.U),
+                    (float*)(ws + L.U), B, st));
+  CK(launch_v32(V, B, r, V32, B, st));
+  CK(launch_sumsq(Cw, (long long)B * nc, (double*)(ws + oPart), sc + 1, st));
+  int sweeps = 0;
+  std::vector<double> fh;
+  for (int it = 0; it < max_iters; ++it) {
+    CK(launch_project(Cw, nc, B, V32, B, r, Cc, nc, st));                             // W V
+    CK(launch_soft_stats(Cc, (long long)r * nc, sc, (double*)(ws + oPart), sc + 2, sc + 3, st));   // C-step
+    CK(launch_wtc(Cw, Cc, nc, B, r, (double*)(ws + oWtc), M, st));                      // W^T C
+    CK(launch_procrustes(M, B, r, V, V32, B, sc + 1, sc + 2, sc + 3, sc, obj + it, st));   // V-step + objective
+    double f = 0.0;
+    CK(cudaMemcpyAsync(&f, obj + it, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fh.push_back(f);
+    ++sweeps;
+    if (it > 0 && std::fabs(fh[it - 1] - f) <= tol * fh[it - 1]) break;
+  }
+  // X = C V^T (band-major B x N_c over W), per-band inverse DWT; components = IDWT of C's rows
+  CK(launch_reconstruct(Cc, nc, nc, B, V32, B, r, Cw, st));
+  CK(dwt_inverse(L, ws, Cw, out, n, B, fb, nullptr, st));
+  if (components) CK(dwt_inverse(L, ws, Cc, components, n, r, fb, nullptr, st));
+  if (rank_out) *rank_out = r;
+  if (sweeps_out) *sweeps_out = sweeps;
+  if (objective_out)
+    for (int i = 0; i < sweeps; ++i) objective_out[i] = fh[i];
+  if (lambda_out) {
+    double lh = 0.0;
+    CK(cudaMemcpyAsync(&lh, sc, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *lambda_out = lh;
+  }
+  return HYDE_OK;
+}
+
 hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out, double lambda,
                         int taps, int levels, double* lambda_out, hyde_stream_t stream) {
   if (!h) return HYDE_EPARAM;

@@ -70,6 +70,17 @@ size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,
                              double* tri, float* W, float* U, int ldwu, cudaStream_t st);
+// F4: WSRRR (k_wsrrr.cu)
+cudaError_t launch_wsrrr_lambda(const double* sigma, int B, long long nc, double* lam, cudaStream_t st);
+cudaError_t launch_sumsq(const float* x, long long n, double* partial, double* out, cudaStream_t st);
+cudaError_t launch_soft_stats(float* c, long long n, const double* lam, double* partial, double* c2, double* c1,
+                              cudaStream_t st);
+int wtc_chunks(long long nc, int r);
+cudaError_t launch_wtc(const float* W, const float* C, long long nc, int B, int r, double* partial, double* M,
+                       cudaStream_t st);
+cudaError_t launch_procrustes(const double* M, int B, int r, double* V, float* V32, int ldv32, const double* w2,
+                              const double* c2, const double* c1, const double* lam, double* f, cudaStream_t st);
+cudaError_t launch_v32(const double* V, int B, int r, float* V32, int ld, cudaStream_t st);
 // F2: FORPDN (k_forpdn.cu)
 cudaError_t launch_forpdn_lambda(const double* M, const double* Gw, int B, long long n, double ridge, double* npow,
                                  double* rp, double* lam_out, double* Zs, cudaStream_t st);
