@@ -622,3 +622,73 @@ def wsrrr(cube: np.ndarray, rank: Optional[int] = None, lam: Optional[float] = N
     out = band_idwt_matrix(cmat @ v.T, r, c, lv, taps)
     comps = band_idwt_matrix(cmat, r, c, lv, taps)
     return WsrrrResult(out.astype(np.float32), comps.astype(np.float32), v, obj, float(lam), int(rank))
+
+
+# ----------------------------------------------------------------------------
+# F3: HyMiNoR
+# ----------------------------------------------------------------------------
+def shrink(v: np.ndarray, t: float) -> np.ndarray:
+    """sign(v) max(|v| - t, 0)."""
+    return np.sign(v) * np.maximum(np.abs(v) - t, 0.0)
+
+
+@dataclass
+class L1SpecResult:
+    out: np.ndarray             # float32 BSQ
+    iters: np.ndarray           # (N,) iterations run per pixel
+    residuals: List[float]      # Bregman residual ||x - m - a||^2 + ||D x - d||^2 (all pixels) per iteration
+
+
+def l1_spectral(m_cube: np.ndarray, lam: float = 10.0, mu: float = 5.0, max_iters: int = 50,
+                tol: float = 1e-3) -> L1SpecResult:
+    """Second stage of HyMiNoR (SPEC.md:415-423 D19; §2.1 "the remaining
+    sparse noise is removed by solving an l1-l1 optimization problem with a
+    modified split-Bregman technique"): per pixel spectrum m (length B),
+    min_x ||m - x||_1 + lam ||D x||_1, D the first-order spectral difference, by
+    split Bregman with a = x - m, d = D x:
+      x = (I + D^T D)^-1 (a + m - b_a + D^T (d - b_d))
+      a = shrink(x - m + b_a, 1/mu),  b_a += x - m - a
+      d = shrink(D x + b_d, lam/mu),   b_d += D x - d
+    from x = m, a = d = b_a = b_d = 0 (reading R16); a pixel stops when
+    ||x_new - x_old|| <= tol ||x_old|| or after max_iters."""
+    b, r, c = m_cube.shape
+    m = np.asarray(m_cube, dtype=np.float64).reshape(b, -1)
+    n = m.shape[1]
+    dmat = spectral_difference(b)
+    ainv = np.linalg.inv(np.eye(b) + dmat.T @ dmat)
+    x = m.copy()
+    a = np.zeros_like(m)
+    ba = np.zeros_like(m)
+    d = np.zeros((b - 1, n))
+    bd = np.zeros((b - 1, n))
+    active = np.ones(n, dtype=bool)
+    iters = np.zeros(n, dtype=np.int64)
+    resid = []
+    for _ in range(max_iters):
+        if not active.any():
+            break
+        idx = np.nonzero(active)[0]
+        xo = x[:, idx]
+        rhs = a[:, idx] + m[:, idx] - ba[:, idx] + dmat.T @ (d[:, idx] - bd[:, idx])
+        xn = ainv @ rhs
+        t = xn - m[:, idx] + ba[:, idx]
+        an = shrink(t, 1.0 / mu)
+        ba[:, idx] = t - an
+        a[:, idx] = an
+        u = dmat @ xn + bd[:, idx]
+        dn = shrink(u, lam / mu)
+        bd[:, idx] = u - dn
+        d[:, idx] = dn
+        x[:, idx] = xn
+        iters[idx] += 1
+        resid.append(float(np.sum((x - m - a) ** 2) + np.sum((dmat @ x - d) ** 2)))
+        done = np.sqrt(np.sum((xn - xo) ** 2, axis=0)) <= tol * np.sqrt(np.sum(xo ** 2, axis=0))
+        active[idx[done]] = False
+    return L1SpecResult(x.reshape(b, r, c).astype(np.float32), iters, resid)
+
+
+def hyminor(cube: np.ndarray, lam: float = 10.0, mu: float = 5.0, max_iters: int = 50, tol: float = 1e-3):
+    """HyMiNoR (SPEC.md:415-423 D19): M = hyres(cube), then l1_spectral(M)."""
+    if not (lam > 0 and mu > 0):
+        raise ValueError("lambda, mu > 0 required (SPEC.md:420)")
+    return l1_spectral(hyres(cube).out, lam, mu, max_iters, tol)

@@ -566,3 +566,57 @@ def test_f4_steps_are_the_block_minimisers():
     for _ in range(20):
         q, _ = np.linalg.qr(rng.standard_normal((6, 2)))
         assert np.trace(q.T @ w.T @ cm) <= np.trace(vb.T @ w.T @ cm) + 1e-12
+
+
+# ---------------------------------------------------------------- F3: HyMiNoR
+def test_f3_split_bregman_reaches_the_l1_minimum():
+    """On tiny spectra the split-Bregman iterate approaches the true minimiser of
+    ||m - x||_1 + lam ||D x||_1 (a linear program, solved here by scipy's
+    linprog as the independent reference); the objective at the iterate is within
+    1 % of the LP optimum."""
+    from scipy.optimize import linprog
+    rng = np.random.default_rng(61)
+    b = 8
+    dmat = O.spectral_difference(b)
+    for trial in range(4):
+        m = rng.standard_normal(b) + np.where(rng.random(b) < 0.2, 5.0, 0.0)
+        lam = 0.7
+        res = O.l1_spectral(m.reshape(b, 1, 1), lam=lam, mu=5.0, max_iters=3000, tol=0.0)
+        x = res.out.reshape(b).astype(np.float64)
+        f = np.sum(np.abs(m - x)) + lam * np.sum(np.abs(dmat @ x))
+        # LP: variables [x (b), s (b) >= |m - x|, t (b-1) >= |D x|]
+        nv = b + b + (b - 1)
+        cvec = np.concatenate([np.zeros(b), np.ones(b), lam * np.ones(b - 1)])
+        A, ub = [], []
+        for i in range(b):
+            row = np.zeros(nv); row[i] = -1; row[b + i] = -1; A.append(row); ub.append(-m[i])   # s >= m - x
+            row = np.zeros(nv); row[i] = 1; row[b + i] = -1; A.append(row); ub.append(m[i])     # s >= x - m
+        for i in range(b - 1):
+            row = np.zeros(nv); row[:b] = dmat[i]; row[2 * b + i] = -1; A.append(row); ub.append(0.0)
+            row = np.zeros(nv); row[:b] = -dmat[i]; row[2 * b + i] = -1; A.append(row); ub.append(0.0)
+        lp = linprog(cvec, A_ub=np.array(A), b_ub=np.array(ub), bounds=[(None, None)] * b + [(0, None)] * (2 * b - 1))
+        assert lp.success
+        assert f <= lp.fun * 1.01 + 1e-9, (f, lp.fun)
+
+
+def test_f3_gaussian_only_stays_with_hyres_and_residual_decreases():
+    """pure Gaussian noise -> HyMiNoR within 1 dB of HyRes; the Bregman
+    residual does not increase over the iterations (1e-6 slack).
+    (SPEC.md:422's derived "+2 dB over HyRes with 5 % salt-and-pepper" does NOT
+    hold for D19's formulation -- the l1 fidelity is to the HyRes output, in which
+    the low-rank projection has already spread the impulses over the bands; on
+    this generator the stage changes PSNR by < 0.2 dB.  Recorded in DESIGN.md R16.)"""
+    rng = np.random.default_rng(62)
+    b, r, c = 31, 64, 64
+    t = np.arange(b)
+    spectra = np.stack([np.exp(-0.5 * ((t - mm) / 5.0) ** 2) + 0.1 for mm in np.linspace(2, 28, 6)])
+    ab = rng.dirichlet(np.ones(6), size=r * c).T
+    clean = (spectra.T @ ab).reshape(b, r, c)
+    sig = np.sqrt(np.mean(clean ** 2) / 100.0)
+    gauss = clean + sig * rng.standard_normal(clean.shape)
+    ps = lambda est: 10 * np.log10(np.max(clean) ** 2 / np.mean((est - clean) ** 2))   # noqa: E731
+    hr = O.hyres(gauss.astype(np.float32)).out
+    res = O.l1_spectral(hr, max_iters=50, tol=0.0)
+    assert abs(ps(res.out) - ps(hr)) <= 1.0
+    rr = res.residuals
+    assert all(rr[i + 1] <= rr[i] * (1 + 1e-6) + 1e-12 for i in range(len(rr) - 1))
