@@ -616,7 +616,7 @@ def test_f3_gaussian_only_stays_with_hyres_and_residual_decreases():
     gauss = clean + sig * rng.standard_normal(clean.shape)
     ps = lambda est: 10 * np.log10(np.max(clean) ** 2 / np.mean((est - clean) ** 2))   # noqa: E731
     hr = O.hyres(gauss.astype(np.float32)).out
-    res = O.l1_spectral(hr, max_iters=50, tol=0.0)
+    res = O.l1_spectral(hr)                       # D19 defaults (lam 10, mu 5, 50 iterations, tol 1e-3)
     assert abs(ps(res.out) - ps(hr)) <= 1.0
-    rr = res.residuals
+    rr = O.l1_spectral(hr, max_iters=50, tol=0.0).residuals
     assert all(rr[i + 1] <= rr[i] * (1 + 1e-6) + 1e-12 for i in range(len(rr) - 1))
