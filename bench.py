@@ -423,9 +423,29 @@ def main():
                  "bytes": wb, "GBps": round(wb / (wms * 1e-3) / 1e9, 1),
                  "frac_hbm": round(wb / (wms * 1e-3) / 1e9 / hbm_, 4),
                  "timing": "host wall clock of the synchronous call (includes HySime for the rank)"}
-        del fout, wout
+        # F3: HyMiNoR's l1-l1 spectral stage on the HyRes output
+        # (D19 defaults), one warp per pixel
+        hout = torch.empty_like(cube)
+        hy.hyres(cube, hout)
+        lout = torch.empty_like(cube)
+        hy.l1_spectral(hout, lout)
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(st_)
+        for _ in range(3):
+            _, its = hy.l1_spectral(hout, lout, return_iters=True)
+        h1.record(st_)
+        torch.cuda.synchronize()
+        lms = h0.elapsed_time(h1) / 3
+        lb = 8 * cfg.bands * cfg.rows * cfg.cols                           # read M, write X
+        fpd_h = {"l1_stage_ms": round(lms, 4), "hyres_plus_l1_ms": round(ms_max + lms, 4),
+                 "mean_iters": round(float(its.float().mean()), 3), "bytes": lb,
+                 "GBps": round(lb / (lms * 1e-3) / 1e9, 1), "frac_hbm": round(lb / (lms * 1e-3) / 1e9 / hbm_, 4),
+                 "timing": "CUDA events over 3 calls of the l1 stage; + the bench's HyRes step time"}
+        del fout, wout, hout, lout
     else:
         fpd_w = None
+        fpd_h = None
     iso = None
     if args.iso_steps > 0 and not batched and not sharded and rank == 0:
         hbm_, _, _ = peaks()
@@ -560,6 +580,8 @@ def main():
         line["forpdn"] = fpd
     if fpd_w is not None:
         line["wsrrr"] = fpd_w
+    if fpd_h is not None:
+        line["hyminor"] = fpd_h
     if world == 1 and not args.no_cpu_baseline:
         t, cores, thr = cpu_baseline(cubes_h[0], reps=2)
         line["cpu_baseline"] = {"value": cfg.voxels / t, "unit": UNIT, "cores": cores, "threads": thr,

@@ -190,6 +190,26 @@ hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, in
 hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
                         double lambda, int taps, int levels, double* lambda_out, hyde_stream_t stream);
 
+/* --- F3: HyMiNoR (SPEC.md:415-423 D19; §2.1
+ * "After the Gaussian noise is removed by HyRes, the remaining sparse noise is
+ * removed by solving an l1-l1 optimization problem with a modified
+ * split-Bregman technique").  hyde_l1_spectral: per pixel spectrum m of cube,
+ * min_x ||m - x||_1 + lambda ||D x||_1 (D the first-order spectral difference)
+ * by split Bregman with penalty mu, from x = m (R16); a pixel stops
+ * when ||x_new - x_old|| <= tol ||x_old|| or after max_iters; iters (DEVICE
+ * int[rows*cols], may be NULL) receives the iterations per pixel.  One warp per
+ * pixel, state in registers; bands in [2, 256]; out == cube allowed.
+ * hyde_hyminor: hyde_hyres_ex (defaults; info may be NULL) into out, then
+ * hyde_l1_spectral in place; lambda 0 -> 10, mu 0 -> 5, max_iters <= 0 -> 50,
+ * tol < 0 -> 1e-3 (D19).  Errors: lambda or mu negative -> HYDE_EPARAM; those of
+ * hyde_hyres_ex. */
+hyde_status hyde_l1_spectral(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
+                             double lambda, double mu, int max_iters, double tol, int* iters,
+                             hyde_stream_t stream);
+hyde_status hyde_hyminor(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out,
+                         double lambda, double mu, int max_iters, double tol, hyde_hyres_info* info,
+                         hyde_stream_t stream);
+
 /* --- F4: WSRRR (SPEC.md:397-405, :433 D17; §2.1
  * "Wavelet-Based Sparse Reduced-Rank Regression"): min_{C,V} ||W - C V^T||_F^2 +
  * lambda ||C||_1 s.t. V^T V = I, W = per-band DWT coefficients (taps 0 = 16,

@@ -255,6 +255,34 @@ def estimate_noise(cube, *, return_gram=False, return_residual=False):
     return out[0] if len(out) == 1 else out
 
 
+def l1_spectral(cube, out=None, *, lam=10.0, mu=5.0, max_iters=50, tol=1e-3, return_iters=False):
+    """HyMiNoR's second stage (F3; include/hyde.h hyde_l1_spectral)."""
+    torch = _torch()
+    _cube(cube)
+    b, r, c = cube.shape
+    if out is None:
+        out = torch.empty_like(cube)
+    its = torch.empty(r * c, dtype=torch.int32, device=cube.device) if return_iters else None
+    h = handle(cube.device.index)
+    check(lib().hyde_l1_spectral(h, cube.data_ptr(), r, c, b, out.data_ptr(), float(lam), float(mu), int(max_iters),
+                                 float(tol), its.data_ptr() if its is not None else None, _stream(cube)), h)
+    return (out, its) if return_iters else out
+
+
+def hyminor(cube, out=None, *, lam=10.0, mu=5.0, max_iters=50, tol=1e-3, return_info=False):
+    """HyMiNoR (F3; include/hyde.h hyde_hyminor): HyRes, then the l1-l1 spectral stage."""
+    torch = _torch()
+    _cube(cube)
+    b, r, c = cube.shape
+    if out is None:
+        out = torch.empty_like(cube)
+    info = Info()
+    h = handle(cube.device.index)
+    check(lib().hyde_hyminor(h, cube.data_ptr(), r, c, b, out.data_ptr(), float(lam), float(mu), int(max_iters),
+                             float(tol), ctypes.byref(info), _stream(cube)), h)
+    return (out, info.as_dict()) if return_info else out
+
+
 def wsrrr(cube, out=None, *, rank=0, lam=-1.0, taps=16, levels=0, max_iters=20, tol=1e-4, components=False):
     """WSRRR (F4; include/hyde.h hyde_wsrrr).  rank 0 = HySime's k, lam < 0 = D17
     default.  Returns dict(out, components (rank, R, C) or None, rank, lam, objective)."""

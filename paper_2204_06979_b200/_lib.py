@@ -70,6 +70,10 @@ _SIGS = {
     "hyde_hyres_workspace_size": (c_size_t, [c_int, c_int, c_int, c_int, POINTER(Params)]),
     "hyde_hyres_batched": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_sync_status": (c_int, [c_void_p, c_void_p]),
+    "hyde_l1_spectral": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, c_double, c_double, c_int, c_double, _P,
+                                 c_void_p]),
+    "hyde_hyminor": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, c_double, c_double, c_int, c_double, POINTER(Info),
+                             c_void_p]),
     "hyde_wsrrr": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_double, c_int, c_int, c_int, c_double, _P, _P,
                            POINTER(c_int), POINTER(c_double), POINTER(c_int), POINTER(c_double), c_void_p]),
     "hyde_forpdn": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, c_double, c_int, c_int, POINTER(c_double),

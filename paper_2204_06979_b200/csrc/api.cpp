@@ -926,6 +926,33 @@ hyde_status hyde_estimate_noise(hyde_handle h, const float* cube, int rows, int 
 }
 
 // ---------------------------------------------------------------- stages
+hyde_status hyde_l1_spectral(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out, double lambda,
+                             double mu, int max_iters, double tol, int* iters, hyde_stream_t stream) {
+  if (!h) return HYDE_EPARAM;
+  if (!cube || !out) return fail(h, HYDE_EPARAM, "NULL cube/out");
+  if (bands < 2 || bands > 256 || rows < 1 || cols < 1) return fail(h, HYDE_EPARAM, "bands in [2, 256]");
+  if (!(lambda > 0.0) || !(mu > 0.0)) return fail(h, HYDE_EPARAM, "lambda, mu > 0 required (SPEC.md:420)");
+  if (max_iters < 1 || !(tol >= 0.0)) return fail(h, HYDE_EPARAM, "max_iters >= 1, tol >= 0");
+  const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
+  if (cube != out && overlap(cube, bytes, out, bytes)) return fail(h, HYDE_EPARAM, "cube and out partially overlap");
+  DeviceGuard g(h->device);
+  CK(launch_l1spec(cube, out, (long long)rows * cols, bands, (float)lambda, (float)mu, max_iters, (float)tol, iters,
+                   (cudaStream_t)stream));
+  return HYDE_OK;
+}
+
+hyde_status hyde_hyminor(hyde_handle h, const float* cube, int rows, int cols, int bands, float* out, double lambda,
+                         double mu, int max_iters, double tol, hyde_hyres_info* info, hyde_stream_t stream) {
+  if (lambda == 0.0) lambda = 10.0;   // D19 defaults
+  if (mu == 0.0) mu = 5.0;
+  if (max_iters <= 0) max_iters = 50;
+  if (tol < 0.0) tol = 1e-3;
+  if (!(lambda > 0.0) || !(mu > 0.0)) return fail(h, HYDE_EPARAM, "lambda, mu > 0 required (SPEC.md:420)");
+  hyde_status s = hyde_hyres_ex(h, cube, rows, cols, bands, out, nullptr, info, stream);
+  if (s != HYDE_OK) return s;
+  return hyde_l1_spectral(h, out, rows, cols, bands, out, lambda, mu, max_iters, tol, nullptr, stream);
+}
+
 hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int bands, int rank, double lambda,
                        int taps, int levels, int max_iters, double tol, float* out, float* components,
                        int* rank_out, double* lambda_out, int* sweeps_out, double* objective_out,

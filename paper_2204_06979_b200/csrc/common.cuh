@@ -70,6 +70,9 @@ size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,
                              double* tri, float* W, float* U, int ldwu, cudaStream_t st);
+// F3: HyMiNoR second stage (k_hyminor.cu)
+cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float lam, float mu, int max_iters, float tol,
+                          int* iters, cudaStream_t st);
 // F4: WSRRR (k_wsrrr.cu)
 cudaError_t launch_wsrrr_lambda(const double* sigma, int B, long long nc, double* lam, cudaStream_t st);
 cudaError_t launch_sumsq(const float* x, long long n, double* partial, double* out, cudaStream_t st);
