@@ -60,112 +60,130 @@ __global__ void __launch_bounds__(NT) l1spec_kernel(const float* __restrict__ M,
     }
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const long long p = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
-  if (p >= n) return;   // warp-uniform
-  float m[S], x[S], a[S], ba[S], d[S], bd[S], al[S], cp[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int i = lane * S + s;
-    m[s] = i < B ? M[(size_t)i * n + p] : 0.f;
-    x[s] = m[s];
-    a[s] = ba[s] = d[s] = bd[s] = 0.f;
-    al[s] = s_alpha[i];
-    cp[s] = s_cp[i];
+  // the CTA stages a tile of TP consecutive pixels x all bands through shared
+  // memory (coalesced 128-byte band rows in and out); warp w solves pixels
+  // w, w + 8, ... of the tile from it
+  extern __shared__ float tile[];   // [32 S][TP + 1]
+  constexpr int TP = 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long p0 = (long long)blockIdx.x * TP;
+  const int np = (int)min((long long)TP, n - p0);
+  for (int x = threadIdx.x; x < B * TP; x += NT) {
+    const int i = x / TP, q = x % TP;
+    tile[i * (TP + 1) + q] = q < np ? M[(size_t)i * n + p0 + q] : 0.f;
   }
+  __syncthreads();
   const float ta = 1.f / mu, td = lam / mu;
-  int it = 0;
-  for (; it < max_iters; ++it) {
-    // rhs_i = a_i + m_i - ba_i + v_{i-1} - v_i, v = d - bd (v_{B-1} = 0, v_{-1} = 0)
-    float v[S];
+  for (int q = wid; q < np; q += NT / 32) {
+    float m[S], x[S], a[S], ba[S], d[S], bd[S], al[S], cp[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int i = lane * S + s;
-      v[s] = i < B - 1 ? d[s] - bd[s] : 0.f;
+      m[s] = i < B ? tile[i * (TP + 1) + q] : 0.f;
+      x[s] = m[s];
+      a[s] = ba[s] = d[s] = bd[s] = 0.f;
+      al[s] = s_alpha[i];
+      cp[s] = s_cp[i];
     }
-    float vprev = __shfl_up_sync(FULL, v[S - 1], 1);
-    if (lane == 0) vprev = 0.f;
-    float r[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      r[s] = a[s] + m[s] - ba[s] + (s == 0 ? vprev : v[s - 1]) - v[s];
-    }
-    // forward: y_i = al_i y_{i-1} + al_i r_i
-    float P = 1.f, Q = 0.f;
-#pragma unroll
-    for (int s = 0; s < S; ++s) { Q = al[s] * (Q + r[s]); P *= al[s]; }
-    scan_up(P, Q, lane);
-    float yin = __shfl_up_sync(FULL, Q, 1);   // y at the end of the previous lane (y_{-1} = 0)
-    if (lane == 0) yin = 0.f;
-    float y[S];
-    {
-      float yy = yin;
-#pragma unroll
-      for (int s = 0; s < S; ++s) { yy = al[s] * (yy + r[s]); y[s] = yy; }
-    }
-    // backward: x_i = -cp_i x_{i+1} + y_i
-    float P2 = 1.f, Q2 = 0.f;
-#pragma unroll
-    for (int s = S - 1; s >= 0; --s) { Q2 = fmaf(-cp[s], Q2, y[s]); P2 *= -cp[s]; }
-    scan_down(P2, Q2, lane);
-    float xin = __shfl_down_sync(FULL, Q2, 1);   // x at the start of the next lane (x_B = 0)
-    if (lane == 31) xin = 0.f;
-    float dx2 = 0.f, xo2 = 0.f;
-    {
-      float xx = xin;
-#pragma unroll
-      for (int s = S - 1; s >= 0; --s) {
-        xx = fmaf(-cp[s], xx, y[s]);
+    int it = 0;
+    for (; it < max_iters; ++it) {
+      // rhs_i = a_i + m_i - ba_i + v_{i-1} - v_i, v = d - bd (v_{B-1} = 0, v_{-1} = 0)
+      float v[S];
+  #pragma unroll
+      for (int s = 0; s < S; ++s) {
         const int i = lane * S + s;
-        const float xn = i < B ? xx : 0.f;
-        dx2 = fmaf(xn - x[s], xn - x[s], dx2);
-        xo2 = fmaf(x[s], x[s], xo2);
-        x[s] = xn;
+        v[s] = i < B - 1 ? d[s] - bd[s] : 0.f;
       }
+      float vprev = __shfl_up_sync(FULL, v[S - 1], 1);
+      if (lane == 0) vprev = 0.f;
+      float r[S];
+  #pragma unroll
+      for (int s = 0; s < S; ++s) {
+        r[s] = a[s] + m[s] - ba[s] + (s == 0 ? vprev : v[s - 1]) - v[s];
+      }
+      // forward: y_i = al_i y_{i-1} + al_i r_i
+      float P = 1.f, Q = 0.f;
+  #pragma unroll
+      for (int s = 0; s < S; ++s) { Q = al[s] * (Q + r[s]); P *= al[s]; }
+      scan_up(P, Q, lane);
+      float yin = __shfl_up_sync(FULL, Q, 1);   // y at the end of the previous lane (y_{-1} = 0)
+      if (lane == 0) yin = 0.f;
+      float y[S];
+      {
+        float yy = yin;
+  #pragma unroll
+        for (int s = 0; s < S; ++s) { yy = al[s] * (yy + r[s]); y[s] = yy; }
+      }
+      // backward: x_i = -cp_i x_{i+1} + y_i
+      float P2 = 1.f, Q2 = 0.f;
+  #pragma unroll
+      for (int s = S - 1; s >= 0; --s) { Q2 = fmaf(-cp[s], Q2, y[s]); P2 *= -cp[s]; }
+      scan_down(P2, Q2, lane);
+      float xin = __shfl_down_sync(FULL, Q2, 1);   // x at the start of the next lane (x_B = 0)
+      if (lane == 31) xin = 0.f;
+      float dx2 = 0.f, xo2 = 0.f;
+      {
+        float xx = xin;
+  #pragma unroll
+        for (int s = S - 1; s >= 0; --s) {
+          xx = fmaf(-cp[s], xx, y[s]);
+          const int i = lane * S + s;
+          const float xn = i < B ? xx : 0.f;
+          dx2 = fmaf(xn - x[s], xn - x[s], dx2);
+          xo2 = fmaf(x[s], x[s], xo2);
+          x[s] = xn;
+        }
+      }
+      // a, b_a
+  #pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const float t = x[s] - m[s] + ba[s];
+        a[s] = shrinkf(t, ta);
+        ba[s] = t - a[s];
+      }
+      // D x: x_{i+1} - x_i (i < B-1), x_{i+1} of the last slot from the next lane
+      float xnext = __shfl_down_sync(FULL, x[0], 1);
+  #pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = lane * S + s;
+        const float x1 = s + 1 < S ? x[s + 1] : xnext;
+        if (i < B - 1) {
+          const float u = (x1 - x[s]) + bd[s];
+          d[s] = shrinkf(u, td);
+          bd[s] = u - d[s];
+        }
+      }
+  #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dx2 += __shfl_xor_sync(FULL, dx2, o);
+        xo2 += __shfl_xor_sync(FULL, xo2, o);
+      }
+      if (sqrtf(dx2) <= tol * sqrtf(xo2)) { ++it; break; }
     }
-    // a, b_a
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const float t = x[s] - m[s] + ba[s];
-      a[s] = shrinkf(t, ta);
-      ba[s] = t - a[s];
-    }
-    // D x: x_{i+1} - x_i (i < B-1), x_{i+1} of the last slot from the next lane
-    float xnext = __shfl_down_sync(FULL, x[0], 1);
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int i = lane * S + s;
-      const float x1 = s + 1 < S ? x[s + 1] : xnext;
-      if (i < B - 1) {
-        const float u = (x1 - x[s]) + bd[s];
-        d[s] = shrinkf(u, td);
-        bd[s] = u - d[s];
-      }
+      if (i < B) tile[i * (TP + 1) + q] = x[s];
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      dx2 += __shfl_xor_sync(FULL, dx2, o);
-      xo2 += __shfl_xor_sync(FULL, xo2, o);
-    }
-    if (sqrtf(dx2) <= tol * sqrtf(xo2)) { ++it; break; }
+    if (iters_out && lane == 0) iters_out[p0 + q] = it;
   }
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int i = lane * S + s;
-    if (i < B) X[(size_t)i * n + p] = x[s];
+  __syncthreads();
+  for (int x = threadIdx.x; x < B * TP; x += NT) {
+    const int i = x / TP, q = x % TP;
+    if (q < np) X[(size_t)i * n + p0 + q] = tile[i * (TP + 1) + q];
   }
-  if (iters_out && lane == 0) iters_out[p] = it;
 }
 
 }  // namespace
 
 cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float lam, float mu, int max_iters, float tol,
                           int* iters, cudaStream_t st) {
-  const unsigned blocks = (unsigned)((n + NT / 32 - 1) / (NT / 32));
+  const unsigned blocks = (unsigned)((n + 31) / 32);
   const int S = (B + 31) / 32;
-  if (S <= 2) l1spec_kernel<2><<<blocks, NT, 0, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
-  else if (S <= 4) l1spec_kernel<4><<<blocks, NT, 0, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
-  else if (S <= 8) l1spec_kernel<8><<<blocks, NT, 0, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
+  const size_t sm = (size_t)32 * S * 33 * sizeof(float);
+  if (S <= 2) l1spec_kernel<2><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
+  else if (S <= 4) l1spec_kernel<4><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
+  else if (S <= 8) l1spec_kernel<8><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
