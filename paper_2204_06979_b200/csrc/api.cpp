@@ -10,6 +10,7 @@
 //   -> K6b reconstruct (single write of the BSQ output).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -731,7 +732,14 @@ hyde_status hyde_hyres(hyde_handle h, const float* cube, int rows, int cols, int
   return hyde_hyres_ex(h, cube, rows, cols, bands, out, nullptr, nullptr, stream);
 }
 
-constexpr int kLanes = 8;   // concurrent cubes in hyde_hyres_batched
+constexpr int kLanesDefault = 8;   // concurrent cubes in hyde_hyres_batched
+static int lanes_wanted() {
+  if (const char* ev = getenv("HYDE_LANES")) {   // experiments
+    const int v = atoi(ev);
+    if (v >= 1 && v <= 32) return v;
+  }
+  return kLanesDefault;
+}
 
 hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int rows, int cols, int bands,
                                float* outs, const hyde_hyres_params* params, hyde_hyres_info* info,
@@ -756,6 +764,7 @@ hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int
   // hyde_hyres_ex gives for that cube alone.
   DeviceGuard g(h->device);
   cudaStream_t st = (cudaStream_t)stream;
+  const int kLanes = lanes_wanted();
   const int L = batch < kLanes ? batch : kLanes;
   while ((int)h->lanes.size() < L) {
     hyde_handle l = nullptr;
