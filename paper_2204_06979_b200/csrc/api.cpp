@@ -1175,7 +1175,8 @@ hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, in
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
   const size_t oRy = take(BB * 8), oRn = take(BB * 8), oRx = take(BB * 8), oV = take(BB * 8), oB = take(BB * 8);
   const size_t oLam = take((size_t)B * 8), oP = take((size_t)B * 8), oS2 = take((size_t)B * 8),
-               oD = take((size_t)B * 8), oOnes = take((size_t)B * 8), oK = take(sizeof(int)), oW = take(BB * 4),
+               oD = take((size_t)B * 8), oOnes = take((size_t)B * 8), oK = take(sizeof(int)), oScal = take(8),
+               oLamN = take((size_t)B * 8), oW = take(BB * 4),
                oU = take(BB * 4);
   s = ensure_ws(h, off, st);
   if (s != HYDE_OK) return s;
@@ -1201,11 +1202,29 @@ hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, in
                       nullptr, B, st));
   const double* M = house + 3 * BB;   // EigWs::M of the K2 workspace
   CK(launch_hysime_prep(G, M, B, L.n, 1e-6, Ry, Rn, Rx, st));
-  // every eigenpair of R_x: the first chunk in the cluster kernel, the rest from its T and Q
+  // the spectrum of R_n first (its smallest eigenvalue bounds which eigenvectors
+  // of R_x can be selected), then the eigenpairs of R_x that can
   const int k1 = B < HYDE_MAX_CHUNK ? B : HYDE_MAX_CHUNK;
+  double* lam_n = (double*)(ws + oLamN);
+  if (k1 < B) {
+    CK(launch_eig_raw(Rn, B, 1, ones, lam_n, V, B, house, tri, W, U, B, st));
+    CK(launch_eig_values(tri, house, B, lam_n, st));
+  }
   CK(launch_eig_raw(Rx, B, k1, ones, lam, V, B, house, tri, W, U, B, st));
-  if (k1 < B) CK(launch_eig_more_raw(tri, house, ones, B, k1, B - k1, lam, V, B, W, U, B, st));   // one CTA per pair
-  CK(launch_hysime_delta(V, B, Ry, Rn, B, (double*)(ws + oP), (double*)(ws + oS2), dl, st));
+  // only eigenvectors that can be selected: mu_i above a lower bound of R_n's
+  // spectrum (the rest have delta_i >= 0 whatever the vector -- k_hysime.cu)
+  int m = k1;
+  if (k1 < B) {
+    CK(launch_eig_values(tri, house, B, lam, st));
+    CK(launch_hysime_bound(lam_n, lam, B, (double*)(ws + oScal), (int*)(ws + oK), st));
+    CK(cudaMemcpyAsync(&h->rs_host->sure_done, ws + oK, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    m = (int)h->rs_host->sure_done;
+    if (m < k1) m = k1;
+    if (m > k1) CK(launch_eig_more_raw(tri, house, ones, B, k1, m - k1, lam, V, B, W, U, B, st));
+  }
+  CK(launch_hysime_delta(V, B, Ry, Rn, B, (double*)(ws + oP), (double*)(ws + oS2), dl, st, m));
+  if (m < B) CK(launch_hysime_fill(lam, (double*)(ws + oScal), m, B, (double*)(ws + oP), dl, st));
   CK(launch_hysime_select(dl, (double*)(ws + oP), B, 1e-9, V, B, basis ? (double*)(ws + oB) : nullptr,
                           (int*)(ws + oK), st));
   if (basis) CK(cudaMemcpyAsync(basis, ws + oB, BB * 8, cudaMemcpyDeviceToDevice, st));

@@ -93,7 +93,11 @@ cudaError_t launch_forpdn_solve(float* C, long long ldc, long long nc, int B, do
 cudaError_t launch_hysime_prep(const double* G, const double* M, int B, long long n, double ridge, double* Ry,
                                double* Rn, double* Rx, cudaStream_t st);
 cudaError_t launch_hysime_delta(const double* V, int ldv, const double* Ry, const double* Rn, int B, double* p,
-                                double* s2, double* delta, cudaStream_t st);
+                                double* s2, double* delta, cudaStream_t st, int ncols = 0);
+cudaError_t launch_hysime_bound(const double* lam_n, const double* mu, int B, double* lb, int* m_out, cudaStream_t st);
+cudaError_t launch_hysime_fill(const double* mu, const double* lb, int m, int B, double* p, double* delta,
+                               cudaStream_t st);
+cudaError_t launch_eig_values(const double* tri, const double* house, int B, double* lam, cudaStream_t st);
 cudaError_t launch_hysime_select(const double* delta, const double* p, int B, double tol_rel, const double* V,
                                  int ldv, double* basis, int* k_out, cudaStream_t st);
 cudaError_t launch_eig_more_raw(const double* tri, const double* house, const double* ones, int B, int k0, int K,

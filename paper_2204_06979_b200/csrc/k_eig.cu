@@ -1286,6 +1286,16 @@ cudaError_t launch_eig_raw(const double* Amat, int B, int ncomp, double* ones, d
   return run_k2(a, st);
 }
 
+// every eigenvalue of the last tridiagonalisation (bisection only), descending index
+cudaError_t launch_eig_values(const double* tri, const double* house, int B, double* lam, cudaStream_t st) {
+  const EigWs ws = carve(const_cast<double*>(house), B);
+  const size_t smem = sizeof(MoreSmem);
+  cudaError_t e = cudaFuncSetAttribute(more_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  more_pairs_kernel<<<B, NT, smem, st>>>(tri, ws, B, 0, 1, lam);
+  return cudaGetLastError();
+}
+
 // F1: eigenpairs k0 .. k0+K-1 of the raw-mode matrix (T and Q of the last
 // launch_eig_raw): eigenvalues into lam[k], vectors into column k of V (ldv)
 cudaError_t launch_eig_more_raw(const double* tri, const double* house, const double* ones, int B, int k0, int K,

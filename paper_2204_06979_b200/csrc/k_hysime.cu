@@ -119,7 +119,45 @@ __global__ void __launch_bounds__(NT) hysime_select_kernel(const double* __restr
     }
 }
 
+// l = the smallest eigenvalue of R_n (lam_n[B-1], from the raw-mode bisection)
+// and m = #{mu_i > l (1 - 1e-6)}: an eigenvector of R_x with mu_i <= l has
+// delta_i = s_i^2 - mu_i >= l - mu_i >= 0 (p_i = mu_i + s_i^2, s_i^2 >= l), so it
+// can never be selected and needs no eigenvector
+__global__ void hysime_bound_kernel(const double* __restrict__ lam_n, const double* __restrict__ mu, int B,
+                                    double* lb, int* m_out) {
+  if (threadIdx.x != 0) return;
+  const double l = lam_n[B - 1];
+  int m = B;
+  if (l > 0.0) {
+    const double cut = l * (1.0 - 1e-6);
+    m = 0;
+    for (int i = 0; i < B; ++i) m += mu[i] > cut ? 1 : 0;
+  }
+  *lb = l;
+  *m_out = m;
+}
+
+// delta_i = l - mu_i (a lower bound, >= 0) for the eigenpairs without a vector
+__global__ void hysime_fill_kernel(const double* mu, const double* lb, int m, int B, double* p, double* delta) {
+  const int i = m + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  delta[i] = *lb - mu[i];
+  p[i] = 0.0;
+}
+
 }  // namespace
+
+cudaError_t launch_hysime_bound(const double* lam_n, const double* mu, int B, double* lb, int* m_out, cudaStream_t st) {
+  hysime_bound_kernel<<<1, 32, 0, st>>>(lam_n, mu, B, lb, m_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hysime_fill(const double* mu, const double* lb, int m, int B, double* p, double* delta,
+                               cudaStream_t st) {
+  if (m >= B) return cudaSuccess;
+  hysime_fill_kernel<<<(B - m + 255) / 256, 256, 0, st>>>(mu, lb, m, B, p, delta);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_hysime_prep(const double* G, const double* M, int B, long long n, double ridge, double* Ry,
                                double* Rn, double* Rx, cudaStream_t st) {
@@ -129,8 +167,8 @@ cudaError_t launch_hysime_prep(const double* G, const double* M, int B, long lon
 }
 
 cudaError_t launch_hysime_delta(const double* V, int ldv, const double* Ry, const double* Rn, int B, double* p,
-                                double* s2, double* delta, cudaStream_t st) {
-  hysime_delta_kernel<<<B, NT, 0, st>>>(V, ldv, Ry, Rn, B, p, s2, delta);
+                                double* s2, double* delta, cudaStream_t st, int ncols) {
+  hysime_delta_kernel<<<ncols > 0 ? ncols : B, NT, 0, st>>>(V, ldv, Ry, Rn, B, p, s2, delta);
   return cudaGetLastError();
 }
 

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(NT) wtc_kernel(const float* __restrict__ W, co
   const long long j0 = (long long)blockIdx.x * JC;
   const int len = (int)min((long long)JC, nc - j0);
   for (int x = threadIdx.x; x < r * JC; x += NT) {
-    const int k = x / JC, j = x % JC;
+    const int k = x / JC, j = x - k * JC;
     cs[k][j] = j < len ? C[(size_t)k * nc + j0 + j] : 0.f;
   }
   __syncthreads();
@@ -230,12 +230,12 @@ cudaError_t launch_wtc(const float* W, const float* C, long long nc, int B, int 
   const int nch = wtc_chunks(nc, r);
   cudaError_t e;
   if (r <= 8) {
-    const int sm = 8 * jc<8>() * 4;
+    const int sm = r * jc<8>() * 4;   // only the r live rows of the C chunk
     e = cudaFuncSetAttribute(wtc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
     wtc_kernel<8><<<nch, NT, sm, st>>>(W, C, nc, B, r, partial);
   } else if (r <= 32) {
-    const int sm = 32 * jc<32>() * 4;
+    const int sm = r * jc<32>() * 4;
     e = cudaFuncSetAttribute(wtc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
     wtc_kernel<32><<<nch, NT, sm, st>>>(W, C, nc, B, r, partial);
