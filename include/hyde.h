@@ -172,7 +172,10 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
  * R13).  Optional DEVICE outputs (NULL = skip): basis (bands x bands row-major;
  * columns 0..k-1 = the selected eigenvectors in ascending-delta order, D6 signs),
  * delta and mu ([bands], in descending-mu order), noise_cov (R_n, bands x
- * bands).  Synchronous (returns after k is known).  Errors: as hyde_hyres. */
+ * bands).  Eigenvectors are computed only where mu_i exceeds the smallest
+ * eigenvalue l of R_n: elsewhere delta_i = s_i^2 - mu_i >= l - mu_i >= 0 for any
+ * vector (never selected) and delta holds that lower bound l - mu_i.
+ * Synchronous (returns after k is known).  Errors: as hyde_hyres. */
 hyde_status hyde_hysime(hyde_handle h, const float* cube, int rows, int cols, int bands, int* k_out,
                         double* basis, double* delta, double* mu, double* noise_cov, hyde_stream_t stream);
 
