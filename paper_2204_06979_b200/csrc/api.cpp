@@ -1108,7 +1108,8 @@ hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, in
   const long long nc = L.plan.n_coeffs;
   size_t off = L.total;
   auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-  const size_t oZ = take(4 * BB * 8), oRp = take(4 * 8), oNp = take(8), oLam = take(8), oGw = take(BB * 8);
+  const size_t oZ = take(4 * BB * 8), oRp = take(4 * 8), oNp = take(8), oLam = take(8), oGw = take(BB * 8),
+               oCoef = take(520 * 4);
   const int np2 = gram_tc_npairs(nc);
   const int ns2 = gram_nsplit(nc, B);
   const size_t oPart = take((size_t)(np2 > ns2 ? np2 : ns2) * BB * 8), oAmax = take((size_t)B * 4);
@@ -1144,7 +1145,7 @@ hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, in
     CK(dwt_forward(L, ws, cube, n, B, fb, st));
   }
   // X = W (I + lam D^T D)^-1: one Thomas solve along the bands per coefficient, in place
-  CK(launch_forpdn_solve(C, nc, nc, B, lambda, autolam ? lam_dev : nullptr, st));
+  CK(launch_forpdn_solve(C, nc, nc, B, lambda, autolam ? lam_dev : nullptr, (float*)(ws + oCoef), st));
   CK(dwt_inverse(L, ws, C, out, n, B, fb, nullptr, st));
   if (lambda_out) {
     if (autolam) {

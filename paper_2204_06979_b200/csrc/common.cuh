@@ -88,7 +88,7 @@ cudaError_t launch_v32(const double* V, int B, int r, float* V32, int ld, cudaSt
 cudaError_t launch_forpdn_lambda(const double* M, const double* Gw, int B, long long n, double ridge, double* npow,
                                  double* rp, double* lam_out, double* Zs, cudaStream_t st);
 cudaError_t launch_forpdn_solve(float* C, long long ldc, long long nc, int B, double lam, const double* lam_dev,
-                                cudaStream_t st);
+                                float* coef, cudaStream_t st);
 // F1: HySime (k_hysime.cu)
 cudaError_t launch_hysime_prep(const double* G, const double* M, int B, long long n, double ridge, double* Ry,
                                double* Rn, double* Rx, cudaStream_t st);

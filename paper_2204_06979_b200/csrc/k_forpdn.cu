@@ -110,61 +110,103 @@ __global__ void lambda_pick_kernel(const double* rp, const double* npow, double*
   *lam_out = kGrid[best];
 }
 
-// X = W A^-1 in place, one coefficient index per thread: Thomas forward sweep
-// (d' written over W), backward sweep (x written over d').  C is band-major
-// (B rows of ldc coefficients): consecutive threads read consecutive
-// coefficients of a band.  lam from device memory (the picked value) or the
-// argument when lam_dev is NULL.
-__global__ void __launch_bounds__(NT) thomas_solve_kernel(float* __restrict__ C, long long ldc, long long nc, int B,
-                                                          double lam_arg, const double* __restrict__ lam_dev) {
-  __shared__ float s_inv_m[256], s_cp[256];
-  __shared__ float s_lam;
-  if (threadIdx.x == 0) {
-    const double lam = lam_dev ? *lam_dev : lam_arg;
-    double cprev = 0.0;
-    for (int i = 0; i < B; ++i) {
+// X = W A^-1 in place.  A CTA takes 32 consecutive coefficients (the lanes)
+// and all B bands: warp w owns the band segment [w SEG, (w+1) SEG) in
+// registers (coalesced 128-byte band rows, every load of the tile in flight
+// at once).  Thomas as two affine recurrences -- forward y_i = alpha_i
+// (y_{i-1} + w_i), backward x_i = y_i - c'_i x_{i+1} -- composed per warp
+// segment, chained across the 8 warps through shared memory, then applied:
+// one read and one write of W.
+constexpr int SEGMAX = 32;   // bands per warp (B <= 256)
+// Thomas factors of A(lam) once per call: coef[0..256) = alpha_i, coef[256..512) = c'_i, coef[512] = lam
+__global__ void thomas_factor_kernel(int B, double lam_arg, const double* __restrict__ lam_dev, float* coef) {
+  if (threadIdx.x != 0) return;
+  const double lam = lam_dev ? *lam_dev : lam_arg;
+  double cprev = 0.0;
+  for (int i = 0; i < 256; ++i) {
+    if (i < B) {
       const double bi = (i == 0 || i == B - 1) ? 1.0 + lam : 1.0 + 2.0 * lam;
       const double m = bi + (i > 0 ? lam * cprev : 0.0);
-      s_inv_m[i] = (float)(1.0 / m);
+      coef[i] = (float)(1.0 / m);
       cprev = (i < B - 1 ? -lam : 0.0) / m;
-      s_cp[i] = (float)cprev;
+      coef[256 + i] = (float)cprev;
+    } else {
+      coef[i] = 0.f;
+      coef[256 + i] = 0.f;
     }
-    s_lam = (float)lam;
+  }
+  coef[512] = (float)lam;
+}
+
+__global__ void __launch_bounds__(NT) thomas_solve_kernel(float* __restrict__ C, long long ldc, long long nc, int B,
+                                                          const float* __restrict__ coef) {
+  __shared__ float s_alpha[256], s_cp[256];
+  __shared__ float s_P[8][32], s_Q[8][32];
+  {
+    s_alpha[threadIdx.x] = coef[threadIdx.x];
+    s_cp[threadIdx.x] = coef[256 + threadIdx.x];
   }
   __syncthreads();
-  const long long j = blockIdx.x * (long long)NT + threadIdx.x;
-  if (j >= nc) return;
-  const float lam = s_lam;
-  float* col = C + j;
-  // forward: d'_i = (w_i + lam d'_{i-1}) / m_i, loads issued 8 bands ahead
-  constexpr int PF = 8;
-  float buf[PF];
+  const float lamf = coef[512];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int seg = (B + 7) / 8;
+  const int b0 = w * seg;
+  const long long j = blockIdx.x * 32LL + l;
+  const bool ok = j < nc;
+  float v[SEGMAX];
 #pragma unroll
-  for (int u = 0; u < PF; ++u) buf[u] = u < B ? __ldcg(col + (long long)u * ldc) : 0.f;
-  float d = 0.f;
-  for (int i0 = 0; i0 < B; i0 += PF) {
-    float nxt[PF];
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int i = i0 + PF + u;
-      nxt[u] = i < B ? __ldcg(col + (long long)i * ldc) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int i = i0 + u;
-      if (i < B) {
-        d = fmaf(lam, d, buf[u]) * s_inv_m[i];
-        col[(long long)i * ldc] = d;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) buf[u] = nxt[u];
+  for (int s = 0; s < SEGMAX; ++s) {
+    const int i = b0 + s;
+    v[s] = (s < seg && i < B && ok) ? C[(size_t)i * ldc + j] : 0.f;
   }
-  // backward: x_i = d'_i - c'_i x_{i+1}
-  float x = d;
-  for (int i = B - 2; i >= 0; --i) {
-    x = fmaf(-s_cp[i], x, __ldcg(col + (long long)i * ldc));
-    col[(long long)i * ldc] = x;
+  // forward: y_i = a_i y_{i-1} + a_i lam... (sub-diagonal -lam): y_i = a_i (w_i + lam y_{i-1})
+  float P = 1.f, Q = 0.f;
+#pragma unroll
+  for (int s = 0; s < SEGMAX; ++s) {
+    const int i = b0 + s;
+    if (s < seg && i < B) {
+      const float a = s_alpha[i];
+      Q = a * fmaf(lamf, Q, v[s]);
+      P = a * lamf * P;
+    }
+  }
+  s_P[w][l] = P;
+  s_Q[w][l] = Q;
+  __syncthreads();
+  float y = 0.f;   // y at the end of the previous segment
+  for (int u = 0; u < w; ++u) y = fmaf(s_P[u][l], y, s_Q[u][l]);
+#pragma unroll
+  for (int s = 0; s < SEGMAX; ++s) {
+    const int i = b0 + s;
+    if (s < seg && i < B) {
+      y = s_alpha[i] * fmaf(lamf, y, v[s]);
+      v[s] = y;
+    }
+  }
+  __syncthreads();
+  // backward: x_i = y_i - c'_i x_{i+1}
+  P = 1.f;
+  Q = 0.f;
+#pragma unroll
+  for (int s = SEGMAX - 1; s >= 0; --s) {
+    const int i = b0 + s;
+    if (s < seg && i < B) {
+      Q = fmaf(-s_cp[i], Q, v[s]);
+      P = -s_cp[i] * P;
+    }
+  }
+  s_P[w][l] = P;
+  s_Q[w][l] = Q;
+  __syncthreads();
+  float x = 0.f;   // x at the start of the next segment
+  for (int u = 7; u > w; --u) x = fmaf(s_P[u][l], x, s_Q[u][l]);
+#pragma unroll
+  for (int s = SEGMAX - 1; s >= 0; --s) {
+    const int i = b0 + s;
+    if (s < seg && i < B) {
+      x = fmaf(-s_cp[i], x, v[s]);
+      if (ok) C[(size_t)i * ldc + j] = x;
+    }
   }
 }
 
@@ -180,9 +222,12 @@ cudaError_t launch_forpdn_lambda(const double* M, const double* Gw, int B, long 
   return cudaGetLastError();
 }
 
+// coef: device scratch of 513 floats
 cudaError_t launch_forpdn_solve(float* C, long long ldc, long long nc, int B, double lam, const double* lam_dev,
-                                cudaStream_t st) {
-  const unsigned blocks = (unsigned)((nc + NT - 1) / NT);
-  thomas_solve_kernel<<<blocks, NT, 0, st>>>(C, ldc, nc, B, lam, lam_dev);
+                                float* coef, cudaStream_t st) {
+  if (B > 8 * SEGMAX) return cudaErrorInvalidValue;
+  thomas_factor_kernel<<<1, 32, 0, st>>>(B, lam, lam_dev, coef);
+  const unsigned blocks = (unsigned)((nc + 31) / 32);
+  thomas_solve_kernel<<<blocks, NT, 0, st>>>(C, ldc, nc, B, coef);
   return cudaGetLastError();
 }
