@@ -64,3 +64,16 @@ def test_wsrrr_lossless_full_rank(hy):
     x = rng.standard_normal((8, 32, 32)).astype(np.float32)
     got = hy.wsrrr(torch.from_numpy(x).cuda(), rank=8, lam=0.0, levels=2)["out"].cpu().numpy()
     assert np.max(np.abs(got - x)) < 1e-3 * np.max(np.abs(x))
+
+
+def test_wsrrr_odd_shape_padded_levels(hy):
+    """Odd extents (padded DWT levels: the coefficient Gram is taken over N_c != N),
+    rank 3, fixed lambda, a few sweeps."""
+    rng = np.random.default_rng(57)
+    b, r, c = 19, 33, 45
+    x = (rng.standard_normal((3, r * c)).T @ rng.random((3, b))).T.reshape(b, r, c)
+    x = (x + 0.1 * rng.standard_normal(x.shape)).astype(np.float32)
+    ref = O.wsrrr(x, rank=3, lam=0.2, levels=2, max_iters=6, tol=0.0)
+    got = hy.wsrrr(torch.from_numpy(x).cuda(), rank=3, lam=0.2, levels=2, max_iters=6, tol=0.0)
+    assert len(got["objective"]) == len(ref.objective) == 6
+    assert metrics.rel_l2(ref.out, got["out"].cpu().numpy()) <= 1e-4
