@@ -18,10 +18,10 @@
 
 namespace {
 
-constexpr int FR = 32;   // forward: subband rows per tile
+constexpr int FR = 24;   // forward: subband rows per tile (row pass: (2 FR + T - 2) x FC/FJ = 248 items, one round of 256 threads)
 constexpr int FC = 32;   // forward: subband cols per tile
 constexpr int FJ = 8;    // forward row pass: outputs per thread (register window 2FJ+T-2)
-constexpr int FI = 4;    // forward column pass: output rows per thread
+constexpr int FI = 3;    // forward column pass: output rows per thread (FC x FR/FI = 256 items)
 constexpr int IR = 32;   // inverse: output rows per tile
 constexpr int IC = 64;   // inverse: output cols per tile
 
