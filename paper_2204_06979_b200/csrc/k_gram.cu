@@ -93,8 +93,11 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restri
   const long long tot = (long long)B * B;
   const long long idx = blockIdx.x * 32LL + lane;
   double s = 0.0;
-  if (idx < tot) {
-    const int i = (int)(idx / B), j = (int)(idx % B);
+  // sym > 0: only i <= j is computed (both G[i][j] and G[j][i] are written)
+  const int i0 = idx < tot ? (int)(idx / B) : 0, j0 = idx < tot ? (int)(idx % B) : 0;
+  const bool active = idx < tot && (sym == 0 || i0 <= j0);
+  if (active) {
+    const int i = i0, j = j0;
     const long long src = (long long)min(i, j) * B + max(i, j);
     // sym > 0: partials of the diagonal blocks ([0, sym) and [sym, B)) are not
     // symmetric -- G = (sum P + sum P^T) / 2 there (tensor-core Gram, K1)
@@ -115,11 +118,12 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restri
   }
   part[w][lane] = s;
   __syncthreads();
-  if (w == 0 && idx < tot) {
+  if (w == 0 && active) {
     double t = part[0][lane];
 #pragma unroll
     for (int q = 1; q < 8; ++q) t += part[q][lane];
     G[idx] = t;
+    if (sym > 0 && i0 != j0) G[(long long)j0 * B + i0] = t;
   }
 }
 
