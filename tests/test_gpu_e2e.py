@@ -179,3 +179,13 @@ def test_zero_cube_and_errors(hy):
         hy.hyres(torch.ones((8, 16, 16), device="cuda"), levels=7)
     with pytest.raises(hy.HydeError):
         hy.hyres(torch.ones((8, 16, 16)))                   # CPU tensor: no CPU path
+
+
+def test_hyres_max_bands_simt_gram_path(hy):
+    """B = 256 (the largest supported; above the tensor-core Gram's 224-band tiling, so
+    K1 falls back to the fp64 SIMT Gram) end to end against the oracle."""
+    s = synth.low_rank_cube(40, 36, 256, rank=3, seed=5, snr_db=20.0)
+    ref = O.hyres(s.noisy)
+    out, info = hy.hyres(torch.from_numpy(s.noisy).cuda(), return_info=True)
+    assert info["rank"] == ref.rank
+    assert metrics.rel_l2(ref.out, out.cpu().numpy()) <= 1e-4
