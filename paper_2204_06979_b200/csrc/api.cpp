@@ -34,7 +34,10 @@ struct Layout {
   size_t s1_img, s2_img;  // per-image strides (floats) of the LL scratch
 };
 
-void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Layout* L) {
+// gram_min_px > 0: at least that many pixels per K1 SM pair (throughput mode of
+// the batched lanes: fewer, longer CTAs leave SMs to the other lanes and keep
+// the per-pair partial Grams few); 0 = as many pairs as the GPU has (latency)
+void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Layout* L, int gram_min_px = 0) {
   L->B = B;
   L->chunk = chunk;
   L->taps = taps;
@@ -43,7 +46,7 @@ void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Lay
   L->ldE = (L->n + 63) / 64 * 64;
   L->nsplit = gram_nsplit(L->n, B);
   L->use_tc = gram_tc_supported(B) ? 1 : 0;
-  L->npairs = gram_tc_npairs(L->n);
+  L->npairs = gram_tc_npairs(L->n, gram_min_px);
   L->ldwu = B;
   hyde_make_plan(rows, cols, levels, &L->plan);
   L->nsub = 3 * levels + 1;
@@ -112,6 +115,7 @@ struct hyde_ctx {
   cudaEvent_t ev_batch = nullptr;
   RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
   cudaEvent_t ev_rank = nullptr; // recorded after the per-chunk D2H copy of the rank state
+  int gram_min_px = 0;           // K1 pixels per SM pair, at least (0: latency mode; lanes: throughput)
   // stage profiling
   int prof = 0;
   struct Rec { int stage; int launches; cudaEvent_t a, b; };
@@ -416,7 +420,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   cudaStream_t st = (cudaStream_t)stream;
   Layout L;
   const int B = bands;
-  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L);
+  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L, h->gram_min_px);
   s = ensure_ws(h, L.total, st);
   if (s != HYDE_OK) return s;
   char* ws = h->ws;
@@ -733,6 +737,7 @@ hyde_status hyde_hyres(hyde_handle h, const float* cube, int rows, int cols, int
 }
 
 constexpr int kLanesDefault = 8;   // concurrent cubes in hyde_hyres_batched
+constexpr int kLaneGramMinPx = 8192;   // K1 pixels per SM pair in the lanes (64 K1 stages)
 static int lanes_wanted() {
   if (const char* ev = getenv("HYDE_LANES")) {   // experiments
     const int v = atoi(ev);
@@ -770,6 +775,7 @@ hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int
     hyde_handle l = nullptr;
     s = hyde_create(&l, h->device);
     if (s != HYDE_OK) return s;
+    l->gram_min_px = kLaneGramMinPx;   // throughput mode: concurrent cubes share the SMs
     h->lanes.push_back(l);
     cudaStream_t ls = nullptr;
     CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));

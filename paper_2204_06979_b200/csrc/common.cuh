@@ -60,7 +60,9 @@ cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int
 int gram_nsplit(long long n, int B);
 cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st, int sym = 0);
 bool gram_tc_supported(int B);
-int gram_tc_npairs(long long n);
+int gram_tc_npairs(long long n, int min_px = 0);
+cudaError_t launch_gram_reduce_i64(const long long* partial, int np, int B, const unsigned* amax_bits, double* G,
+                                   cudaStream_t st);
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
                            double* G, int* nonfinite, cudaStream_t st);
 cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st);

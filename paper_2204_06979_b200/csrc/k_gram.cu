@@ -150,6 +150,64 @@ cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int
   return launch_gram_reduce(partial, nsplit, B, G, st);
 }
 
+// K1 (tensor-core Gram): the per-pair partials are exact int64 (Q Q^T over the
+// pair's pixels; in the diagonal blocks [0, 128) and [128, B) the cross term
+// holds 2X, X = S0 S1^T, and (P + P^T)/2 is the exact integer).  Sum in
+// integers, scale once: G_ij = (sum) s_i s_j, s = 1 / fp32(16256 / max|y|),
+// independent of the pixel split; only i <= j is computed, both halves written.
+__global__ void __launch_bounds__(256) gram_reduce_i64_kernel(const long long* __restrict__ partial, int np, int B,
+                                                              const unsigned* __restrict__ amax_bits,
+                                                              double* __restrict__ G) {
+  __shared__ long long part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long tot = (long long)B * B;
+  const long long idx = blockIdx.x * 32LL + lane;
+  const int i = idx < tot ? (int)(idx / B) : 0, j = idx < tot ? (int)(idx % B) : 0;
+  const bool active = idx < tot && i <= j;
+  long long s = 0;
+  if (active) {
+    const bool both = (i < 128) == (j < 128);
+    const long long src = (long long)i * B + j, srt = (long long)j * B + i;
+    for (int k0 = w; k0 < np; k0 += 8 * 16) {
+      long long v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = k0 + 8 * u;
+        v[u] = 0;
+        if (k < np) {
+          v[u] = __ldcs(partial + (long long)k * tot + src);
+          if (both) v[u] += __ldcs(partial + (long long)k * tot + srt);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+  }
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && active) {
+    long long t = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += part[q][lane];
+    if ((i < 128) == (j < 128)) t /= 2;   // exact: P_ij + P_ji is even there
+    auto scale = [&](int b) {
+      const float m = __uint_as_float(amax_bits[b]);
+      const float is = m > 0.f ? fminf((float)(16256.0 / (double)m), 1e30f) : 1.f;
+      return 1.0 / (double)is;
+    };
+    const double g = (double)t * scale(i) * scale(j);
+    G[(long long)i * B + j] = g;
+    G[(long long)j * B + i] = g;
+  }
+}
+
+cudaError_t launch_gram_reduce_i64(const long long* partial, int np, int B, const unsigned* amax_bits, double* G,
+                                   cudaStream_t st) {
+  const long long tot = (long long)B * B;
+  gram_reduce_i64_kernel<<<(unsigned)((tot + 31) / 32), 256, 0, st>>>(partial, np, B, amax_bits, G);
+  return cudaGetLastError();
+}
+
 // G[i][j] = sum over slices of partial[slice][min(i,j)][max(i,j)], fixed order
 cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st, int sym) {
   long long tot = (long long)B * B;

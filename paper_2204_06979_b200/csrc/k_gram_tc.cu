@@ -273,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const int q4 = warp & 3;                    // TMEM lane quadrant of this warp
       const int L = q4 * 32 + lane;               // TMEM lane = this thread's row slot
       const int m = L & 63, half = L >> 6;
-      double* Pp = P.partial + (long long)pair * B * B;
+      long long* Pq = reinterpret_cast<long long*>(P.partial) + (long long)pair * B * B;
       if (nst > 0) {
         tc::mbar_wait_cluster(&bar_done, 0);
         tc::tc_fence_after();
@@ -285,7 +285,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // row band i and its scale; column bands j
         const int rg_i = t == 2 ? 1 : 0;
         const int bi = band_of(rg_i, m, rank, B, nb);
-        const double si = bi >= 0 ? s_of[rg_i][m] : 0.0;
         for (int c0 = 0; c0 < Nt / 2; c0 += 16) {
           uint32_t a0[16], a1[16], a2[16];
           const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + coff + c0;
@@ -302,24 +301,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int nn = c0 + j + (Nt / 2) * half;    // column within the tile
-            int bj;
-            double sj;
-            if (t == 0) {
-              bj = nn < (B < 128 ? B : 128) ? nn : -1;
-              sj = 0.0;
-            } else {
-              bj = 128 + nn < B ? 128 + nn : -1;
-              sj = 0.0;
-            }
+            const int bj = t == 0 ? (nn < (B < 128 ? B : 128) ? nn : -1) : (128 + nn < B ? 128 + nn : -1);
             if (bj < 0) continue;
-            const float m_j = __uint_as_float(P.amax_bits[bj]);
-            const float isj = m_j > 0.f ? fminf((float)(16256.0 / (double)m_j), 1e30f) : 1.f;
-            sj = 1.0 / (double)isj;
             // T_ab holds S0 S1^T + S1 S0^T; the diagonal tiles hold X = S0 S1^T only:
-            // 256 X here, (P + P^T) / 2 in the reduction gives 128 (X + X^T)
+            // 256 X here, (P + P^T) / 2 in the reduction gives 128 (X + X^T).
+            // The partial is the EXACT integer (Q Q^T over this pair's pixels):
+            // the reduction sums integers and scales once, so G does not depend
+            // on how the pixels were split over pairs.
             const long long qq = 16384LL * (long long)(int)a0[j] + (t == 1 ? 128LL : 256LL) * (long long)(int)a1[j] +
                                  (long long)(int)a2[j];
-            Pp[(long long)bi * B + bj] = (double)qq * si * sj;
+            Pq[(long long)bi * B + bj] = qq;
           }
         }
       }
@@ -378,8 +369,11 @@ __global__ void amax_kernel(const float* __restrict__ Y, long long n, unsigned* 
 
 bool gram_tc_supported(int B) { return B >= 1 && B <= 224; }
 
-int gram_tc_npairs(long long n) {
-  long long np = (n + 4LL * KC - 1) / (4LL * KC);
+// SM pairs for n pixels: min_px = 0 -> as many as the GPU has (at most 74,
+// >= 512 pixels each: latency); min_px > 0 -> at least min_px pixels each
+// (throughput mode of the batched lanes)
+int gram_tc_npairs(long long n, int min_px) {
+  long long np = min_px > 0 ? n / min_px : (n + 4LL * KC - 1) / (4LL * KC);
   if (np > 74) np = 74;
   if (np < 1) np = 1;
   long long per = (n + np - 1) / np;
@@ -426,7 +420,7 @@ cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsi
   gram_tc_kernel<<<2 * npairs, NTHREADS, smem, st>>>(P);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_gram_reduce(partial, npairs, B, G, st, 128);
+  return launch_gram_reduce_i64(reinterpret_cast<const long long*>(partial), npairs, B, amax_bits, G, st);
 }
 
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
