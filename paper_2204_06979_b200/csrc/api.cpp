@@ -776,6 +776,7 @@ hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int
     s = hyde_create(&l, h->device);
     if (s != HYDE_OK) return s;
     l->gram_min_px = kLaneGramMinPx;   // throughput mode: concurrent cubes share the SMs
+    if (const char* ev = getenv("HYDE_LANE_GRAM_PX")) l->gram_min_px = atoi(ev);   // experiments
     h->lanes.push_back(l);
     cudaStream_t ls = nullptr;
     CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
