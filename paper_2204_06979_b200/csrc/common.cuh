@@ -38,6 +38,27 @@ int hyde_build_filters(int taps, FilterBank* fb, double* h64);
 void hyde_make_plan(int rows, int cols, int levels, DwtPlan* p);
 
 // device workspace pieces used by several kernels
+// Programmatic dependent launch: the kernel may be scheduled while its stream
+// predecessor drains and waits at pdl_wait() (griddepcontrol.wait, a no-op
+// without the attribute) before touching any global data -- hides the launch
+// latency of the short dependent kernels of the chunk loop.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 struct RankState {
   int found;        // 1 once a failing component has been seen
   int rank;         // r* once found (else running count of passing components)

@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
                                                       int h_in, int w_in, float* __restrict__ ll,
                                                       long long ll_stride, float* __restrict__ sub,
                                                       long long sub_stride, FilterBank fb) {
+  pdl_wait();
   constexpr int NR = 2 * FR + T - 2;
   constexpr int NC = 2 * FC + T - 2;
   constexpr int WR = 2 * FJ + T - 2;   // row-pass window
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
                                                       const float* __restrict__ sub, long long sub_stride,
                                                       int h_out, int w_out, float* __restrict__ out,
                                                       long long out_stride, FilterBank fb, SoftSpec sp) {
+  pdl_wait();
   constexpr int HT = T / 2;
   constexpr int CR = IR / 2 + HT - 1;
   constexpr int CC = IC / 2 + HT - 1;
@@ -303,9 +305,9 @@ cudaError_t launch_dwt_level(const float* in, long long in_stride, int h_in, int
   const int hs = (h_in + 1) / 2, ws = (w_in + 1) / 2;
   dim3 grid((ws + FC - 1) / FC, (hs + FR - 1) / FR, count);
   switch (fb.taps) {
-    case 2: dwt_fwd_kernel<2><<<grid, 256, 0, st>>>(in, in_stride, h_in, w_in, ll, ll_stride, sub, sub_stride, fb); break;
-    case 8: dwt_fwd_kernel<8><<<grid, 256, 0, st>>>(in, in_stride, h_in, w_in, ll, ll_stride, sub, sub_stride, fb); break;
-    case 16: dwt_fwd_kernel<16><<<grid, 256, 0, st>>>(in, in_stride, h_in, w_in, ll, ll_stride, sub, sub_stride, fb); break;
+    case 2: return launch_pdl(dwt_fwd_kernel<2>, grid, dim3(256), 0, st, in, in_stride, h_in, w_in, ll, ll_stride, sub, sub_stride, fb);
+    case 8: return launch_pdl(dwt_fwd_kernel<8>, grid, dim3(256), 0, st, in, in_stride, h_in, w_in, ll, ll_stride, sub, sub_stride, fb);
+    case 16: return launch_pdl(dwt_fwd_kernel<16>, grid, dim3(256), 0, st, in, in_stride, h_in, w_in, ll, ll_stride, sub, sub_stride, fb);
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -320,9 +322,9 @@ cudaError_t launch_idwt_level(const float* ll, long long ll_stride, const float*
   dim3 grid((Wd + IC - 1) / IC, (H + IR - 1) / IR, count);
   const SoftSpec sp{tstar, nsub, s_lh, s_ll, rs, k0, count};
   switch (fb.taps) {
-    case 2: dwt_inv_kernel<2><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;
-    case 8: dwt_inv_kernel<8><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;
-    case 16: dwt_inv_kernel<16><<<grid, 256, 0, st>>>(ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp); break;
+    case 2: return launch_pdl(dwt_inv_kernel<2>, grid, dim3(256), 0, st, ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp);
+    case 8: return launch_pdl(dwt_inv_kernel<8>, grid, dim3(256), 0, st, ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp);
+    case 16: return launch_pdl(dwt_inv_kernel<16>, grid, dim3(256), 0, st, ll, ll_stride, sub, sub_stride, h_out, w_out, out, out_stride, fb, sp);
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -16,6 +16,7 @@ template <int NC, int PIX, bool VEC, int UB>
 __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ Y, long long n, int B,
                                                       const float* __restrict__ W, int ldw, int ncomp,
                                                       float* __restrict__ E, long long ldE) {
+  pdl_wait();
   extern __shared__ float Ws[];  // B x NC
   for (int i = threadIdx.x; i < B * NC; i += blockDim.x) {
     int b = i / NC, k = i % NC;
@@ -100,10 +101,10 @@ cudaError_t launch_nc(const float* Y, long long n, int B, const float* W, int ld
   const bool vec = (n % 4 == 0) && (ldE % 4 == 0) && ((uintptr_t)Y % 16 == 0) && ((uintptr_t)E % 16 == 0);
   if (vec) {
     cudaFuncSetAttribute(project_kernel<NC, PIX, true, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    project_kernel<NC, PIX, true, UB><<<blocks, 256, smem, st>>>(Y, n, B, W, ldw, ncomp, E, ldE);
+    return launch_pdl(project_kernel<NC, PIX, true, UB>, dim3(blocks), dim3(256), smem, st, Y, n, B, W, ldw, ncomp, E, ldE);
   } else {
     cudaFuncSetAttribute(project_kernel<NC, PIX, false, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    project_kernel<NC, PIX, false, UB><<<blocks, 256, smem, st>>>(Y, n, B, W, ldw, ncomp, E, ldE);
+    return launch_pdl(project_kernel<NC, PIX, false, UB>, dim3(blocks), dim3(256), smem, st, Y, n, B, W, ldw, ncomp, E, ldE);
   }
   return cudaGetLastError();
 }

@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(256) recon_kernel(const float* __restrict__ E,
                                                     int B, const float* __restrict__ U, int ldu, int k0,
                                                     int kcount, int accumulate, float* __restrict__ out,
                                                     const RankState* __restrict__ rs) {
+  pdl_wait();
   if (rs) {   // rank decided on the device: nothing until it is found, then r* - k0 components
     if (!rs->found) return;
     kcount = min(kcount, rs->rank - k0);
@@ -88,9 +89,9 @@ cudaError_t launch_reconstruct(const float* E, long long ldE, long long n, int B
     const int kc = rank - k0 < RK ? rank - k0 : RK;
     const int acc = k0 > 0;
     if (vec)
-      recon_kernel<PIX, true><<<blocks, 256, smem, st>>>(E, ldE, n, B, U, ldu, k0, kc, acc, out, rs);
+      launch_pdl(recon_kernel<PIX, true>, dim3(blocks), dim3(256), smem, st, E, ldE, n, B, U, ldu, k0, kc, acc, out, rs);
     else
-      recon_kernel<PIX, false><<<blocks, 256, smem, st>>>(E, ldE, n, B, U, ldu, k0, kc, acc, out, rs);
+      launch_pdl(recon_kernel<PIX, false>, dim3(blocks), dim3(256), smem, st, E, ldE, n, B, U, ldu, k0, kc, acc, out, rs);
   }
   return cudaGetLastError();
 }

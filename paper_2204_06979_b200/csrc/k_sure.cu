@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
                                                      int count, int keep_ll, int* kstar, float* tstar, double* e_sub,
                                                      RankState* rs, int k0, double n_coeffs, int bands,
                                                      double* e_post, RankState* rs_mirror) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smraw[];
   // union: histogram (HB counts | HB fixed-point sums) | window keys + sort buffer
   unsigned* hcnt = reinterpret_cast<unsigned*>(smraw);
@@ -962,13 +963,15 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = SMEM_DYN;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = G;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, sure_kernel, (const float*)coeffs, cstride, tab, count, keep_ll, kstar, tstar, e_sub,
                             rs, k0, n_coeffs, bands, e_post, rs_mirror);
 }
