@@ -526,6 +526,7 @@ __device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, 
 
 template <int CL>
 __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
+  pdl_wait();
   constexpr int RS = 32 / CL;          // row slots per warp (CL * NW * RS = 256 rows)
   constexpr int LPR = 16 / RS;         // lanes holding one reduced row value
   constexpr int LR = NW * RS;          // rows per CTA
@@ -1134,7 +1135,7 @@ __global__ void residual_kernel(const float* __restrict__ Y, long long n, int B,
 int g_cluster = 0;   // cluster size chosen at the first launch (16, else 8)
 
 template <int CL>
-cudaLaunchConfig_t k2_config(cudaLaunchAttribute* attr, cudaStream_t st) {
+cudaLaunchConfig_t k2_config(cudaLaunchAttribute* attr /* [2] */, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL, 1, 1);
   cfg.blockDim = dim3(NT, 1, 1);
@@ -1144,8 +1145,10 @@ cudaLaunchConfig_t k2_config(cudaLaunchAttribute* attr, cudaStream_t st) {
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cfg;
 }
 
@@ -1164,7 +1167,7 @@ bool cluster_fits() {
     cudaGetLastError();
     return false;
   }
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t cfg = k2_config<CL>(attr, 0);
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, k2_cluster_kernel<CL>, &cfg) != cudaSuccess) {
@@ -1178,7 +1181,7 @@ template <int CL>
 cudaError_t launch_k2(const K2Args& a, cudaStream_t st) {
   cudaError_t e = prepare_k2<CL>();
   if (e != cudaSuccess) return e;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t cfg = k2_config<CL>(attr, st);
   return cudaLaunchKernelEx(&cfg, k2_cluster_kernel<CL>, a);
 }

@@ -158,6 +158,7 @@ cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int
 __global__ void __launch_bounds__(256) gram_reduce_i64_kernel(const long long* __restrict__ partial, int np, int B,
                                                               const unsigned* __restrict__ amax_bits,
                                                               double* __restrict__ G) {
+  pdl_wait();
   __shared__ long long part[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long tot = (long long)B * B;
@@ -204,7 +205,8 @@ __global__ void __launch_bounds__(256) gram_reduce_i64_kernel(const long long* _
 cudaError_t launch_gram_reduce_i64(const long long* partial, int np, int B, const unsigned* amax_bits, double* G,
                                    cudaStream_t st) {
   const long long tot = (long long)B * B;
-  gram_reduce_i64_kernel<<<(unsigned)((tot + 31) / 32), 256, 0, st>>>(partial, np, B, amax_bits, G);
+  return launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, partial, np, B,
+                    amax_bits, G);
   return cudaGetLastError();
 }
 

@@ -69,6 +69,7 @@ __device__ __forceinline__ int band_of(int region, int r, int rank, int B, int n
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     gram_tc_kernel(GramTc P) {
+  pdl_wait();
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NI];
   __shared__ __align__(8) uint64_t bar_empty[NI];
@@ -417,7 +418,8 @@ cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsi
   const size_t smem = (size_t)NI * 2 * P.rows_tot * KC;
   e = cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  gram_tc_kernel<<<2 * npairs, NTHREADS, smem, st>>>(P);
+  e = launch_pdl(gram_tc_kernel, dim3(2 * npairs), dim3(NTHREADS), smem, st, P);   // __cluster_dims__(2)
+  if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_gram_reduce_i64(reinterpret_cast<const long long*>(partial), npairs, B, amax_bits, G, st);
