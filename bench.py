@@ -346,7 +346,6 @@ def main():
     for _ in range(args.warmup - 1):
         run()
     torch.cuda.synchronize()
-    hy.profile_enable(local, True)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -371,6 +370,13 @@ def main():
     # slowest step, average the rest -- reported beside the contract's mean
     olympic = (sum(sorted(per_step)[1:-1]) / (args.steps - 2)) if args.steps >= 3 else None
     launches = hy.launch_count(local) - launches0
+    # stage table: the same number of steps again, with the library's per-stage
+    # events on (outside the timed region: the events split the programmatic
+    # dependent launches between stages)
+    hy.profile_enable(local, True)
+    for _ in range(args.steps):
+        run()
+    torch.cuda.synchronize()
     stages = hy.profile_read(local)
     hy.profile_enable(local, False)
     ms = e0.elapsed_time(e1) / args.steps
