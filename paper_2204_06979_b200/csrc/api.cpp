@@ -242,10 +242,10 @@ static hyde_status resolve_params(hyde_handle h, int rows, int cols, const hyde_
 
 // K1: exact int8 tensor-core Gram (B <= 224) or the fp64 SIMT fallback
 static cudaError_t run_gram(const Layout& L, char* ws, const float* cube, double* G, int* nonfinite,
-                            cudaStream_t st) {
+                            cudaStream_t st, int* state4 = nullptr) {
   if (L.use_tc)
     return launch_gram_tc(cube, L.n, L.B, (unsigned*)(ws + L.amax), (double*)(ws + L.partial), L.npairs, G,
-                          nonfinite, st);
+                          nonfinite, st, state4);
   return launch_gram(cube, L.n, L.B, (double*)(ws + L.partial), L.nsplit, G, nonfinite, st);
 }
 
@@ -429,7 +429,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   if (s != HYDE_OK) return s;
   RankState* rs = (RankState*)(ws + L.rs);
   h->last_rs = rs;
-  CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+  if (!L.use_tc) CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
   double* G = (double*)(ws + L.G);
   double* sigma = (double*)(ws + L.sigma);
   double* house = (double*)(ws + L.house);
@@ -438,8 +438,9 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   float* U = (float*)(ws + L.U);
   float* C = (float*)(ws + L.C);
   {
-    Stage sg(h, HYDE_STAGE_GRAM, L.use_tc ? 3 : 2, st);
-    CK(run_gram(L, ws, cube, G, &rs->nonfinite, st));
+    Stage sg(h, HYDE_STAGE_GRAM, L.use_tc ? 4 : 2, st);
+    // tensor-core path: the state words are zeroed by the Gram's first (zero) kernel
+    CK(run_gram(L, ws, cube, G, &rs->nonfinite, st, L.use_tc ? (int*)rs : nullptr));
     sg.end();
   }
   // Geometric chunk schedule: 4, 8, 16, ... components (capped at p.chunk).

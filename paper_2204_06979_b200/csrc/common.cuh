@@ -85,8 +85,8 @@ int gram_tc_npairs(long long n, int min_px = 0);
 cudaError_t launch_gram_reduce_i64(const long long* partial, int np, int B, const unsigned* amax_bits, double* G,
                                    cudaStream_t st);
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
-                           double* G, int* nonfinite, cudaStream_t st);
-cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st);
+                           double* G, int* nonfinite, cudaStream_t st, int* state4 = nullptr);
+cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st, int* state4 = nullptr);
 cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsigned* amax_bits, double* partial,
                                   int npairs, double* G, int* nonfinite, cudaStream_t st);
 size_t eig_workspace_doubles(int B);

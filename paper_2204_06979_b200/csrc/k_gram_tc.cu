@@ -326,6 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 }
 
 __global__ void amax_kernel(const float* __restrict__ Y, long long n, unsigned* amax_bits, int* nonfinite) {
+  pdl_wait();
   const int b = blockIdx.y;
   const float* row = Y + (long long)b * n;
   unsigned m = 0;
@@ -388,15 +389,23 @@ int gram_tc_npairs(long long n, int min_px) {
 }
 
 // per-band max |y| bit patterns (the quantisation scales of K1) + non-finite flag
-cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(amax_bits, 0, (size_t)B * sizeof(unsigned), st);
+// zero the per-band max words (and the caller's RankState, when given) as a
+// kernel, so the whole step stays a chain of dependent launches (no memset node)
+__global__ void zero_kernel(unsigned* a, int na, int* st4) {
+  pdl_wait();
+  for (int i = threadIdx.x; i < na; i += blockDim.x) a[i] = 0u;
+  if (st4 && threadIdx.x < (int)(sizeof(RankState) / sizeof(int))) st4[threadIdx.x] = 0;
+}
+
+cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st,
+                             int* state4) {
+  cudaError_t e = launch_pdl(zero_kernel, dim3(1), dim3(256), 0, st, amax_bits, B, state4);
   if (e != cudaSuccess) return e;
   long long per_block = 256LL * 4 * 8;
   unsigned gx = (unsigned)((n + per_block - 1) / per_block);
   if (gx > 16) gx = 16;   // 16 x B blocks: 64K-element band segments at B = 224, N = 2^20
   if (gx < 1) gx = 1;
-  amax_kernel<<<dim3(gx, B), 256, 0, st>>>(Y, n, amax_bits, nonfinite);
-  return cudaGetLastError();
+  return launch_pdl(amax_kernel, dim3(gx, B), dim3(256), 0, st, Y, n, amax_bits, nonfinite);
 }
 
 // exact integer Gram of Y with the given per-band scales (amax_bits)
@@ -426,8 +435,8 @@ cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsi
 }
 
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
-                           double* G, int* nonfinite, cudaStream_t st) {
-  cudaError_t e = launch_gram_amax(Y, n, B, amax_bits, nonfinite, st);
+                           double* G, int* nonfinite, cudaStream_t st, int* state4) {
+  cudaError_t e = launch_gram_amax(Y, n, B, amax_bits, nonfinite, st, state4);
   if (e != cudaSuccess) return e;
   return launch_gram_tc_scaled(Y, n, B, amax_bits, partial, npairs, G, nonfinite, st);
 }
