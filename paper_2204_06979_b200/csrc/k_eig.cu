@@ -111,6 +111,11 @@ __device__ __forceinline__ void st_cl_i(unsigned a, int v) {
 }
 // remote store that completes 8 bytes of the destination CTA's mbarrier
 // transaction count (no release fence on the sender)
+__device__ __forceinline__ void st_async2(unsigned a, double v0, double v1, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(a),
+               "d"(v0), "d"(v1), "r"(mbar)
+               : "memory");
+}
 __device__ __forceinline__ void st_async(unsigned a, double v, unsigned mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(a), "d"(v),
                "r"(mbar)
@@ -436,8 +441,8 @@ struct K2Args {
 struct K2Smem {
   unsigned long long mbar[2];   // tridiagonalisation exchange, one per column parity
   unsigned long long smb[2];    // sweep exchange, one per block parity
-  double pbuf[2][BM];      // p = beta A v, all-gathered (double-buffered by column parity)
-  double xbuf[2][BM];      // column k+2 entries, all-gathered one column ahead
+  double2 px[2][BM];       // {p = beta A v, column k+2 entry} per row, all-gathered
+                           // (double-buffered by column parity; one 16-byte message per row and peer)
   double colK[2][BM * NB]; // sweep: pivot-block columns of every row (double-buffered by block)
   double Wb[NB][BM];       // sweep: L^-1 A_K,:
   double Zb[NB][BM];       // sweep: P^-1 A_K,:
@@ -530,6 +535,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
   constexpr int RS = 32 / CL;          // row slots per warp (CL * NW * RS = 256 rows)
   constexpr int LPR = 16 / RS;         // lanes holding one reduced row value
   constexpr int LR = NW * RS;          // rows per CTA
+  static_assert(CL % (2 * LPR) == 0, "one {p, x} message per lane and peer group");
   extern __shared__ __align__(16) unsigned char smraw[];
   K2Smem& S = *reinterpret_cast<K2Smem*>(smraw);
   const int c = (int)cl_rank();
@@ -793,13 +799,22 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
         if (s == sp) xv = tmp;
       }
     }
-    if (ip < B) {
-      const bool isp = lane < 16;
-      const double val = isp ? ((ip > k) ? beta * red : 0.0) : xv;
-      const unsigned la = saddr(isp ? &S.pbuf[par][ip] : &S.xbuf[par][ip]);
-      const unsigned mb = saddr(&S.mbar[par]);
+    {
+      // lanes l and l ^ 16 hold the same row slot sp (p in the low half, the
+      // column k+2 entry in both); each sends {p, x} to half of the row's peers
+      const double pl = (ip > k) ? beta * red : 0.0;
+      const double ph = __shfl_xor_sync(FULL, pl, 16);
+      if (ip < B) {
+        const double pv = lane < 16 ? pl : ph;
+        const int hi = lane >> 4;
+        const unsigned la = saddr(&S.px[par][ip]);
+        const unsigned mb = saddr(&S.mbar[par]);
 #pragma unroll
-      for (int u = 0; u < CL / LPR; ++u) st_async(mapa(la, dA + u * LPR), val, mapa(mb, dA + u * LPR));
+        for (int u = 0; u < CL / (2 * LPR); ++u) {
+          const unsigned dst = dA + LPR * (2 * u + hi);
+          st_async2(mapa(la, dst), pv, xv, mapa(mb, dst));
+        }
+      }
     }
     ACC(10);
     // Q <- Q H_k while the exchange is in flight
@@ -816,7 +831,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
     if (tid == 0 && k + 2 <= B - 3) mbar_expect(saddr(&S.mbar[par]), xbytes);
     ACC(12);
     // (b) w = p - (beta/2)(p.v) v; A <- A - v w^T - w v^T on the live block
-    const double* pb = S.pbuf[par];
+    const double2* pb = S.px[par];
     double wreg[CS], wrow[RS];
     double Kc;
     {
@@ -826,7 +841,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
         if (t < TM) {
           wreg[t] = 0.0;
         } else {
-          wreg[t] = lane + 32 * t < B ? pb[lane + 32 * t] : 0.0;
+          wreg[t] = lane + 32 * t < B ? pb[lane + 32 * t].x : 0.0;
           pv = fma(wreg[t], vreg[t], pv);
         }
       }
@@ -834,7 +849,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
 #pragma unroll
       for (int t = TM; t < CS; ++t) wreg[t] = fma(-Kc, vreg[t], wreg[t]);
 #pragma unroll
-      for (int s = 0; s < RS; ++s) wrow[s] = rowi[s] < B ? fma(-Kc, vrow[s], pb[rowi[s]]) : 0.0;
+      for (int s = 0; s < RS; ++s) wrow[s] = rowi[s] < B ? fma(-Kc, vrow[s], pb[rowi[s]].x) : 0.0;
     }
 #pragma unroll
     for (int s = 0; s < RS; ++s)
@@ -845,13 +860,13 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
     // replica of column k+1 (-> through update k) and the arrived column k+2 (-> through update k)
     const double* vw = S.vw[w];
     const double v1 = vw[k + 1], v2 = vw[k + 2];
-    const double w1 = fma(-Kc, v1, pb[k + 1]), w2 = fma(-Kc, v2, pb[k + 2]);
+    const double w1 = fma(-Kc, v1, pb[k + 1].x), w2 = fma(-Kc, v2, pb[k + 2].x);
     double xn[CS];
 #pragma unroll
     for (int t = TM; t < CS; ++t) {
       const int j = lane + 32 * t;
       rrep[t] = fma(-wreg[t], v1, fma(-vreg[t], w1, rrep[t]));
-      xn[t] = j < B ? fma(-wreg[t], v2, fma(-vreg[t], w2, S.xbuf[par][j])) : 0.0;
+      xn[t] = j < B ? fma(-wreg[t], v2, fma(-vreg[t], w2, pb[j].y)) : 0.0;
     }
     ACC(13);
     // (c) reflector k+1
