@@ -14,6 +14,7 @@
 struct FilterBank {
   float h[HYDE_MAX_TAPS];
   float g[HYDE_MAX_TAPS];
+  float2 hg[HYDE_MAX_TAPS];   // {h_m, g_m}: the operand pair of one packed fp32x2 FMA
   int taps;
 };
 

@@ -103,6 +103,8 @@ int hyde_build_filters(int taps, FilterBank* fb, double* h64) {
       fb->h[k] = k < taps ? (float)h[k] : 0.f;
       ld gk = k < taps ? ((k & 1) ? -h[taps - 1 - k] : h[taps - 1 - k]) : 0;
       fb->g[k] = (float)gk;
+      fb->hg[k].x = fb->h[k];
+      fb->hg[k].y = fb->g[k];
     }
   }
   if (h64)
