@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(256) dwt_fwd_kernel(const float* __restrict__ 
   }
   __syncthreads();
   for (int it = threadIdx.x; it < NR * (FC / FJ); it += 256) {
-    const int r = it / (FC / FJ), q = it - r * (FC / FJ);
+    // lanes run down the rows (odd row stride NC + 1: conflict-free window loads)
+    const int q = it / NR, r = it - q * NR;
     float v[WR];
 #pragma unroll
     for (int t = 0; t < WR; ++t) v[t] = xin[r][2 * FJ * q + t];
@@ -204,7 +205,11 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
   constexpr int W0 = II / 2 + HT - 1;   // axis-0 window
   constexpr int W1 = IJ / 2 + HT - 1;   // axis-1 window
   __shared__ float t_ll[CR][CC + 1], t_hl[CR][CC + 1], t_lh[CR][CC + 1], t_hh[CR][CC + 1];
-  __shared__ float lo1[IR][CC + 1], hi1[IR][CC + 1];
+  // row stride = 1 mod 4: the axis-1 pass (lanes = 4 rows x 8 column groups
+  // 4 apart) reads 32 distinct banks
+  constexpr int LS = CC + ((1 - CC) % 4 + 4) % 4;
+  __shared__ float lo1[IR][LS], hi1[IR][LS];
+  __shared__ float otile[IR][IC + 1];   // output tile: written back with coalesced (float4) rows
   if (sp.rs) {
     const int kept = sp.rs->found ? sp.rs->rank - sp.k0 : sp.cnt;
     if ((int)blockIdx.z >= kept) return;
@@ -299,8 +304,6 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
       wl[t] = lo1[rr][vb + t];
       wh[t] = hi1[rr][vb + t];
     }
-    const int r = r0 + rr;
-    if (r >= h_out) continue;
 #pragma unroll
     for (int k = 0; k < IJ; ++k) {
       const int par = k & 1, u = k >> 1;
@@ -312,8 +315,25 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
         sacc = fmaf(fb.h[m], wl[tj], sacc);
         sacc = fmaf(fb.g[m], wh[tj], sacc);
       }
-      const int cc = c0 + IJ * q8 + k;
-      if (cc < w_out) o[(long long)r * w_out + cc] = sacc;
+      otile[rr][IJ * q8 + k] = sacc;
+    }
+  }
+  __syncthreads();
+  // write-back: lanes along the row (a register-tiled thread's own outputs
+  // are 8 apart -- 32 sectors per store instruction)
+  if ((w_out & 3) == 0 && (reinterpret_cast<unsigned long long>(o) & 15) == 0) {
+    for (int e = threadIdx.x; e < IR * (IC / 4); e += 256) {
+      const int rr = e / (IC / 4), c4 = e - rr * (IC / 4);
+      const int r = r0 + rr, cc = c0 + 4 * c4;
+      if (r < h_out && cc < w_out)
+        *reinterpret_cast<float4*>(o + (long long)r * w_out + cc) =
+            make_float4(otile[rr][4 * c4], otile[rr][4 * c4 + 1], otile[rr][4 * c4 + 2], otile[rr][4 * c4 + 3]);
+    }
+  } else {
+    for (int e = threadIdx.x; e < IR * IC; e += 256) {
+      const int rr = e / IC, c = e - rr * IC;
+      const int r = r0 + rr, cc = c0 + c;
+      if (r < h_out && cc < w_out) o[(long long)r * w_out + cc] = otile[rr][c];
     }
   }
 }
