@@ -18,7 +18,7 @@ LIB = os.path.join(PKG, "libhyde.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3"] + (["-DHYDE_SURE_PROF"] if os.environ.get("HYDE_SURE_PROF") else []) + \
     (["-DHYDE_EIG_PROF"] if os.environ.get("HYDE_EIG_PROF") else []) + ["-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include")] + os.environ.get("HYDE_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:
