@@ -274,6 +274,31 @@ def k2_flops(B):
     return (2.0 + 4.0 / 3.0 + 4.0 / 3.0) * B ** 3
 
 
+def cube_stream(hy, torch, cube, cfg, k, steps):
+    """Throughput of a stream of k cubes (copies of the bench cube, each fully
+    processed) through hyde_hyres_batched: its lanes overlap one cube's
+    latency-bound eigensolver (one 16-SM cluster) with the other cubes'
+    HBM-bound stages.  Reported beside the single-cube number, not instead of it."""
+    cubes = cube.unsqueeze(0).expand(k, *cube.shape).contiguous()
+    outs = torch.empty_like(cubes)
+    for _ in range(2):
+        hy.hyres_batched(cubes, outs)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        hy.hyres_batched(cubes, outs)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del cubes, outs
+    torch.cuda.empty_cache()
+    return {"cubes_per_call": k, "calls": steps, "ms_per_call": round(ms, 4),
+            "ms_per_cube": round(ms / k, 4), "value": k * cfg.voxels / (ms * 1e-3), "unit": "voxels/s",
+            "path": "hyde_hyres_batched on k copies of the seed-0 cube (device-resident), CUDA events"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -282,6 +307,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="large", choices=["tiny", "small", "medium", "wide", "large", "batched"])
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--stream-cubes", type=int, default=4,
+                    help="extra measurement: throughput of a stream of this many copies of the cube "
+                         "through hyde_hyres_batched (lanes overlap the cubes' stages); 0 = off")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--iso-steps", type=int, default=5,
                     help="steps of the stage-isolated DWT/SURE/IDWT leg on all B eigen-images (0: skip)")
@@ -464,6 +492,9 @@ def main():
     if args.iso_steps > 0 and not batched and not sharded and rank == 0:
         hbm_, _, _ = peaks()
         iso = wavelet_isolated(hy, torch, cube, cfg, info["levels"], args.iso_steps, hbm_)
+    strm = None
+    if args.stream_cubes > 1 and not batched and not sharded and rank == 0:
+        strm = cube_stream(hy, torch, cube, cfg, args.stream_cubes, max(2, args.iso_steps // 2))
 
     # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside ----
     # hyde_hyres_host_stream: every step copies its cubes in and its results out;
@@ -589,6 +620,8 @@ def main():
     }
     if iso is not None:
         line["wavelet_isolated"] = iso
+    if strm is not None:
+        line["cube_stream"] = strm
     if hys is not None:
         line["hysime"] = hys
     if fpd is not None:
