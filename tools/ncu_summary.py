@@ -20,11 +20,30 @@ KEYS = {
 }
 
 
-def raw(rep):
+def raw_all(rep):
+    """One dict per profiled launch in the report."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+    hdr, units = rows[0], rows[1]
+    return [{h: (v, u) for h, u, v in zip(hdr, units, vals)} for vals in rows[2:] if len(vals) == len(hdr)]
+
+
+def raw(rep):
+    return raw_all(rep)[0]
+
+
+def stalls_raw(d, top=3):
+    pre = "smsp__pcsamp_warps_issue_stalled_"
+    agg = {}
+    for k, (v, _) in d.items():
+        if k.startswith(pre) and not k.endswith("_not_issued"):
+            try:
+                agg[k[len(pre):]] = float(v.replace(",", ""))
+            except ValueError:
+                pass
+    tot = sum(agg.values()) or 1.0
+    best = sorted(agg.items(), key=lambda kv: -kv[1])[:top]
+    return ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in best)
 
 
 def num(d, key):
@@ -69,15 +88,20 @@ def main(reps):
     print("| kernel | µs | DRAM rd MB | DRAM wr MB | DRAM GB/s | DRAM % | SM % | tensor % | L2 % | warps % | regs | top stalls |")
     print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for rep in reps:
-        d = raw(rep)
+      launches = raw_all(rep)
+      for d in launches:
         name = rep.split("/")[-1].replace(".ncu-rep", "")
+        if len(launches) > 1:
+            kn = d.get("Kernel Name", ("?", ""))[0]
+            name = kn.replace("void ", "").replace("<unnamed>::", "").split("(")[0]
         us = to_us(*num(d, "gpu__time_duration.sum"))
         rd = to_mb(*num(d, "dram__bytes_read.sum"))
         wr = to_mb(*num(d, "dram__bytes_write.sum"))
         gbs = (rd + wr) * 1e-3 / (us * 1e-6) if us > 0 else float("nan")
         f = lambda k: num(d, KEYS[k][0])[0]   # noqa: E731
         print(f"| {name} | {us:.1f} | {rd:.1f} | {wr:.1f} | {gbs:.0f} | {f('dram_pct'):.1f} | {f('sm_pct'):.1f} | "
-              f"{f('tensor_pct'):.1f} | {f('l2_pct'):.1f} | {f('warps_pct'):.1f} | {f('regs'):.0f} | {stalls(rep)} |")
+              f"{f('tensor_pct'):.1f} | {f('l2_pct'):.1f} | {f('warps_pct'):.1f} | {f('regs'):.0f} | "
+              f"{stalls(rep) if len(launches) == 1 else stalls_raw(d)} |")
 
 
 if __name__ == "__main__":
