@@ -286,14 +286,23 @@ __device__ void tri_scaled(const double* d, const double* e2, int B, double sc, 
 // Inverse iteration for eigenvalue lam of T, called by one full warp: lane 0
 // runs the serial partial-pivot LU of T - lam I (two super-diagonals) and the
 // two triangular solves per iteration with running values in registers and
-// select-based pivoting; the start vector and the normalisations are
+// select-based pivoting (the first iteration's forward solve is fused into
+// the factorisation loop); the start vector and the normalisations are
 // lane-parallel.  Two iterations from a fixed pseudo-random start vector.
 __device__ void inv_iter(const double* d, const double* e, int n, double lam, double tnorm, double* x,
                          double* dd, double* u1, double* u2, double* ml, unsigned char* piv, unsigned seed) {
   const int lane = threadIdx.x & 31;
   const double tiny = tnorm > 0.0 ? 2.220446049250313e-16 * tnorm : 1.0;
+  for (int i = lane; i < n; i += 32) {
+    unsigned h = (unsigned)(i * 2654435761u) ^ (seed * 40503u + 0x9E3779B9u);
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    x[i] = 0.5 + (double)(h & 0xFFFF) / 65536.0;
+  }
+  __syncwarp();
+  double cur0 = 0.0;   // lane 0: the first iteration's forward solve runs inside the LU loop
   if (lane == 0) {
     double a = d[0] - lam, b = (n > 1) ? e[0] : 0.0;
+    double cur = x[0];
 #pragma unroll 4
     for (int i = 0; i < n - 1; ++i) {
       const double c = e[i];
@@ -316,26 +325,28 @@ __device__ void inv_iter(const double* d, const double* e, int n, double lam, do
       const double an = fma(-m, sw ? a1 : b, sw ? b : a1);
       b = sw ? -m * b1 : b1;
       a = an;
+      // forward step of iteration 0 (L^-1 with the row interchange of this column)
+      const double nx = x[i + 1];
+      x[i] = sw ? nx : cur;
+      cur = sw ? fma(-m, nx, cur) : fma(-m, cur, nx);
     }
     if (fabs(a) < tiny) a = (a < 0 ? -tiny : tiny);
     dd[n - 1] = rcp64(a);
+    cur0 = cur;
   }
-  for (int i = lane; i < n; i += 32) {
-    unsigned h = (unsigned)(i * 2654435761u) ^ (seed * 40503u + 0x9E3779B9u);
-    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
-    x[i] = 0.5 + (double)(h & 0xFFFF) / 65536.0;
-  }
-  __syncwarp();
   for (int it = 0; it < 2; ++it) {
     if (lane == 0) {
-      double cur = x[0];
+      double cur = cur0;
+      if (it > 0) {
+        cur = x[0];
 #pragma unroll 4
-      for (int i = 0; i < n - 1; ++i) {   // forward: L^-1 with the row interchanges
-        const double nx = x[i + 1];
-        const double m = ml[i];
-        const bool sw = piv[i];
-        x[i] = sw ? nx : cur;
-        cur = sw ? fma(-m, nx, cur) : fma(-m, cur, nx);
+        for (int i = 0; i < n - 1; ++i) {   // forward: L^-1 with the row interchanges
+          const double nx = x[i + 1];
+          const double m = ml[i];
+          const bool sw = piv[i];
+          x[i] = sw ? nx : cur;
+          cur = sw ? fma(-m, nx, cur) : fma(-m, cur, nx);
+        }
       }
       double c1 = cur * dd[n - 1];     // backward: U^-1, two super-diagonals
       x[n - 1] = c1;
@@ -581,30 +592,34 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
         const int i = rowi[s], j = lane + 32 * t;
         a[s][t] = (i < B && j < B) ? G[(size_t)i * B + j] + (i == j ? A.ridge : 0.0) : 0.0;
       }
+    // all-gather of block `gb`'s pivot columns of every row: lane L owns the pair
+    // (row slot, column) = (L % 8RS) / 8, L % 8 and 8 of the CL destinations
+    auto send_block = [&](int gb) {
+      const int gk0 = gb * NB, gkb = min(NB, B - gk0), gt0 = gk0 >> 5, gL0 = gk0 & 31;
+      double* gcol = S.colK[gb & 1];
+      const int pr = lane % (8 * RS), sp = pr >> 3, q = pr & 7;
+      double val = 0.0;
+  #pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        const double tmp = __shfl_sync(FULL, sel(a[s], gt0), gL0 + q);
+        if (s == sp) val = tmp;
+      }
+      const int i = rowi[0] + CL * NW * sp;
+      if (i < B && q < gkb) {
+        const unsigned la = saddr(&gcol[i * NB + q]);
+        const unsigned mb = saddr(&S.smb[gb & 1]);
+        const int d0 = lane / (8 * RS);
+  #pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const unsigned dst = d0 + u * (CL / 8);
+          st_async(mapa(la, dst), val, mapa(mb, dst));
+        }
+      }
+    };
+    send_block(0);
     for (int k0 = 0, blk = 0; k0 < B; k0 += NB, ++blk) {
       const int kb = min(NB, B - k0), t0 = k0 >> 5, L0 = k0 & 31;
       double* colK = S.colK[blk & 1];
-      {   // all-gather the pivot-block columns of every row: lane L owns the pair
-          // (row slot, column) = (L % 8RS) / 8, L % 8 and 8 of the CL destinations
-        const int pr = lane % (8 * RS), sp = pr >> 3, q = pr & 7;
-        double val = 0.0;
-  #pragma unroll
-        for (int s = 0; s < RS; ++s) {
-          const double tmp = __shfl_sync(FULL, sel(a[s], t0), L0 + q);
-          if (s == sp) val = tmp;
-        }
-        const int i = rowi[0] + CL * NW * sp;
-        if (i < B && q < kb) {
-          const unsigned la = saddr(&colK[i * NB + q]);
-          const unsigned mb = saddr(&S.smb[blk & 1]);
-          const int d0 = lane / (8 * RS);
-  #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const unsigned dst = d0 + u * (CL / 8);
-            st_async(mapa(la, dst), val, mapa(mb, dst));
-          }
-        }
-      }
       ACC(5);
       mbar_wait(saddr(&S.smb[blk & 1]), (unsigned)(blk >> 1) & 1u);
       if (tid == 0 && k0 + 2 * NB < B) mbar_expect(saddr(&S.smb[blk & 1]), (unsigned)(B * min(NB, B - k0 - 2 * NB) * 8));
@@ -679,10 +694,11 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
       for (int s = 0; s < RS; ++s)
   #pragma unroll
         for (int r = 0; r < NB; ++r) wi[s][r] = rowi[s] < B ? S.Wb[r][rowi[s]] : 0.0;
-  #pragma unroll
-      for (int t = 0; t < CS; ++t) {
+      // trailing update of column slot t (the pivot block's own rows / columns
+      // take Z, Z^T and -P^-1)
+      auto upd = [&](int t) {
         const int j = lane + 32 * t;
-        if (j >= B) continue;
+        if (j >= B) return;
         double wj[NB];
   #pragma unroll
         for (int r = 0; r < NB; ++r) wj[r] = S.Wb[r][j];
@@ -707,7 +723,19 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
             a[s][t] = -S.Pinv[ik * NB + jk];
           }
         }
+      };
+      // look-ahead: the slot holding the next block's pivot columns first, then
+      // that block's all-gather, whose DSMEM round trip overlaps the rest
+      const int nk0 = k0 + NB, nt0 = nk0 >> 5;
+      if (nk0 < B) {
+  #pragma unroll
+        for (int t = 0; t < CS; ++t)
+          if (t == nt0) upd(t);
+        send_block(blk + 1);
       }
+  #pragma unroll
+      for (int t = 0; t < CS; ++t)
+        if (nk0 >= B || t != nt0) upd(t);
       ACC(9);
     }
     // a = -(G + ridge I)^-1: sigma_i = sqrt(1 / (N M_ii)), all-gathered
