@@ -268,29 +268,26 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
   for (int it = threadIdx.x; it < CC * (IR / II); it += 256) {
     const int c = it % CC, p = it / CC;
     const int ub = (II / 2) * p;   // first coefficient row of the window (tile-relative, + HT - 1 offset)
-    float wl[W0], wh[W0], wlh[W0], whh[W0];
+    f2_t wa[W0], wd[W0];   // {LL, LH} and {HL, HH} of one coefficient row
 #pragma unroll
     for (int t = 0; t < W0; ++t) {
-      wl[t] = t_ll[ub + t][c];
-      wh[t] = t_hl[ub + t][c];
-      wlh[t] = t_lh[ub + t][c];
-      whh[t] = t_hh[ub + t][c];
+      wa[t] = pk2(t_ll[ub + t][c], t_lh[ub + t][c]);
+      wd[t] = pk2(t_hl[ub + t][c], t_hh[ub + t][c]);
     }
 #pragma unroll
     for (int k = 0; k < II; ++k) {
       const int par = k & 1, u = k >> 1;   // output row rr = II p + k = 2 (ub + u) + par (r0 even)
-      float s_lo = 0.f, s_hi = 0.f;
+      f2_t s2 = 0ull;                      // {s_lo, s_hi}: same fma order as the scalar form
 #pragma unroll
       for (int q = 0; q < HT; ++q) {
         const int m = 2 * q + par;
         const int ti = u - q + HT - 1;   // window index of coefficient row (ub + u) - q
-        s_lo = fmaf(fb.h[m], wl[ti], s_lo);
-        s_lo = fmaf(fb.g[m], wh[ti], s_lo);
-        s_hi = fmaf(fb.h[m], wlh[ti], s_hi);
-        s_hi = fmaf(fb.g[m], whh[ti], s_hi);
+        s2 = ffma2(pk2(fb.h[m], fb.h[m]), wa[ti], s2);
+        s2 = ffma2(pk2(fb.g[m], fb.g[m]), wd[ti], s2);
       }
-      lo1[II * p + k][c] = s_lo;
-      hi1[II * p + k][c] = s_hi;
+      const float2 o = up2(s2);
+      lo1[II * p + k][c] = o.x;
+      hi1[II * p + k][c] = o.y;
     }
   }
   __syncthreads();
