@@ -242,7 +242,10 @@ __device__ double bisect_one(const double* d, const double* e2, int n, double gl
   constexpr int NP = NT;
   const double range = fmax(ghi - glo, 1e-300);
   const double tol = 4.0 * 2.220446049250313e-16 * fmax(fabs(glo), fabs(ghi)) + 1e-300;
-  int iters = (int)ceil(log2(range / tol) / log2((double)NP + 1.0)) + 1;
+  // (NP + 1)^iters >= range / tol: the final interval is within tol (at
+  // B = 224, 7 sections reach 2.7e-17 ||T||, below the fp64 spacing at ||T||)
+  int iters = (int)ceil(log2(range / tol) / log2((double)NP + 1.0));
+  if (iters < 1) iters = 1;
   if (iters > 64) iters = 64;
   double lo = glo, hi = ghi;
   const int t = threadIdx.x;
