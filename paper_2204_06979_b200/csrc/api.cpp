@@ -438,7 +438,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   float* U = (float*)(ws + L.U);
   float* C = (float*)(ws + L.C);
   {
-    Stage sg(h, HYDE_STAGE_GRAM, L.use_tc ? 4 : 2, st);
+    Stage sg(h, HYDE_STAGE_GRAM, L.use_tc ? 5 : 2, st);
     // tensor-core path: the state words are zeroed by the Gram's first (zero) kernel
     CK(run_gram(L, ws, cube, G, &rs->nonfinite, st, L.use_tc ? (int*)rs : nullptr));
     sg.end();
@@ -582,7 +582,7 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
   };
   // ---- A1: global per-band scales, local exact Gram, all-reduced ----
   {
-    Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? 3 : 2, st);
+    Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? 5 : 2, st);
     if (Ll.use_tc) {
       unsigned* amax = (unsigned*)(wl + Ll.amax);
       CK(launch_gram_amax(local, n_loc, B, amax, &rs->nonfinite, st));
