@@ -39,25 +39,24 @@ __device__ __forceinline__ void scan_down(float& P, float& Q, int lane) {
   }
 }
 
+// Thomas factors of I + D^T D (diag 2, 3, ..., 3, 2; off-diagonal -1): they
+// depend on B only, so the host computes them once per call (fp64, the same
+// IEEE operations a device loop would do) and every CTA copies them to shared
+// memory (a serial fp64 loop in thread 0 of every CTA cost ~256 divisions
+// per 32-pixel tile).
+struct ThomasF {
+  float alpha[256];
+  float cp[256];
+};
+
 template <int S>
 __global__ void __launch_bounds__(NT) l1spec_kernel(const float* __restrict__ M, float* __restrict__ X, long long n,
                                                     int B, float lam, float mu, int max_iters, float tol,
-                                                    int* __restrict__ iters_out) {
+                                                    int* __restrict__ iters_out, const ThomasF tf) {
   __shared__ float s_alpha[32 * S], s_cp[32 * S];
-  if (threadIdx.x == 0) {   // Thomas factors of I + D^T D (diag 2, 3, ..., 3, 2; off-diagonal -1)
-    double cprev = 0.0;
-    for (int i = 0; i < 32 * S; ++i) {
-      if (i < B) {
-        const double bi = (i == 0 || i == B - 1) ? (B == 1 ? 1.0 : 2.0) : 3.0;
-        const double m = bi + cprev;              // b_i - a_i c'_{i-1}, a_i = -1
-        s_alpha[i] = (float)(1.0 / m);
-        cprev = (i < B - 1 ? -1.0 : 0.0) / m;
-        s_cp[i] = (float)cprev;
-      } else {
-        s_alpha[i] = 0.f;
-        s_cp[i] = 0.f;
-      }
-    }
+  for (int i = threadIdx.x; i < 32 * S; i += NT) {
+    s_alpha[i] = tf.alpha[i];
+    s_cp[i] = tf.cp[i];
   }
   __syncthreads();
   // the CTA stages a tile of TP consecutive pixels x all bands through shared
@@ -180,10 +179,26 @@ cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float la
                           int* iters, cudaStream_t st) {
   const unsigned blocks = (unsigned)((n + 31) / 32);
   const int S = (B + 31) / 32;
+  if (S > 8) return cudaErrorInvalidValue;
   const size_t sm = (size_t)32 * S * 33 * sizeof(float);
-  if (S <= 2) l1spec_kernel<2><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
-  else if (S <= 4) l1spec_kernel<4><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
-  else if (S <= 8) l1spec_kernel<8><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters);
-  else return cudaErrorInvalidValue;
+  ThomasF tf;
+  {
+    double cprev = 0.0;
+    for (int i = 0; i < 256; ++i) {
+      if (i < B) {
+        const double bi = (i == 0 || i == B - 1) ? (B == 1 ? 1.0 : 2.0) : 3.0;
+        const double m = bi + cprev;              // b_i - a_i c'_{i-1}, a_i = -1
+        tf.alpha[i] = (float)(1.0 / m);
+        cprev = (i < B - 1 ? -1.0 : 0.0) / m;
+        tf.cp[i] = (float)cprev;
+      } else {
+        tf.alpha[i] = 0.f;
+        tf.cp[i] = 0.f;
+      }
+    }
+  }
+  if (S <= 2) l1spec_kernel<2><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, tf);
+  else if (S <= 4) l1spec_kernel<4><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, tf);
+  else l1spec_kernel<8><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, tf);
   return cudaGetLastError();
 }
