@@ -38,7 +38,17 @@ __global__ void wsrrr_lambda_kernel(const double* sigma, int B, double nc, doubl
 __global__ void __launch_bounds__(NT) sumsq_kernel(const float* __restrict__ x, long long n, double* partial) {
   __shared__ double red[NT / 32];
   double s = 0.0;
-  for (long long i = blockIdx.x * (long long)NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT) {
+  const long long G = (long long)gridDim.x * NT;
+  long long i = blockIdx.x * (long long)NT + threadIdx.x;
+  // four loads in flight per thread; the same element order as a plain loop
+  for (; i + 3 * G < n; i += 4 * G) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(x + i + u * G);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s = fma((double)v[u], (double)v[u], s);
+  }
+  for (; i < n; i += G) {
     const double v = x[i];
     s = fma(v, v, s);
   }
@@ -93,7 +103,21 @@ __global__ void __launch_bounds__(NT) wtc_kernel(const float* __restrict__ W, co
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0.0;
     const float* wr = W + (size_t)b * nc + j0;
-    for (int j = l; j < len; j += 32) {
+    int j = l;
+    // four loads of the band row in flight per lane (same accumulation order)
+    for (; j + 96 < len; j += 128) {
+      float w4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w4[u] = __ldg(wr + j + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double wv = w4[u];
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (k < r) acc[k] = fma(wv, (double)cs[k][j + 32 * u], acc[k]);
+      }
+    }
+    for (; j < len; j += 32) {
       const double wv = wr[j];
 #pragma unroll
       for (int k = 0; k < R; ++k)
@@ -231,9 +255,15 @@ cudaError_t launch_wtc(const float* W, const float* C, long long nc, int B, int 
   cudaError_t e;
   if (r <= 8) {
     const int sm = r * jc<8>() * 4;   // only the r live rows of the C chunk
-    e = cudaFuncSetAttribute(wtc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    // instantiation by the live rank (the accumulators of a wider one are predicated off)
+    auto go = [&](auto kern) -> cudaError_t {
+      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      if (e2 != cudaSuccess) return e2;
+      kern<<<nch, NT, sm, st>>>(W, C, nc, B, r, partial);
+      return cudaGetLastError();
+    };
+    e = r == 1 ? go(wtc_kernel<1>) : r == 2 ? go(wtc_kernel<2>) : r <= 4 ? go(wtc_kernel<4>) : go(wtc_kernel<8>);
     if (e != cudaSuccess) return e;
-    wtc_kernel<8><<<nch, NT, sm, st>>>(W, C, nc, B, r, partial);
   } else if (r <= 32) {
     const int sm = r * jc<32>() * 4;
     e = cudaFuncSetAttribute(wtc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
