@@ -247,9 +247,19 @@ hyde_status hyde_sync_status(hyde_handle h, hyde_stream_t stream);
 /* --- Stage entry points (test/diagnostic; same conventions).  Each consumes
  * and produces the oracle's intermediate layout (oracle/hyres_ref.py). ---- */
 
-/* A1: G = Y Y^T, fp64 row-major bands x bands. */
+/* A1: G = Y Y^T, fp64 row-major bands x bands (north_star
+ * stage (1)).  bands <= 224: the exact integer tensor-core Gram of the cube
+ * with every value rounded to its band's 16-bit grid s_b (q + c_b), except the
+ * pixels holding a value outside that grid's range (outliers, NaN/Inf), which
+ * enter exactly in fp64 -- see k_gram_tc.cu; bands > 224: fp64 SIMT. */
 hyde_status hyde_k_gram(hyde_handle h, const float* cube, int n_pixels, int bands, double* gram,
                         hyde_stream_t stream);
+/* Diagnostics of the last hyde_k_gram on this handle (synchronizes the
+ * device): per band the fp32 1/step inv_s[b] and the integer centre centre[b]
+ * (q = rint(y inv_s) - c), and the number of flagged (exactly added) pixels;
+ * n_flagged = -1 when the fp64 SIMT path ran.  Any output may be NULL. */
+hyde_status hyde_debug_gram_quant(hyde_handle h, int n_pixels, int bands, float* inv_s, int* centre,
+                                  long long* n_flagged);
 /* A1+A2: from G (fp64, bands x bands) and N: sigma[bands]; lam[bands] (all
  * eigenvalues of G_w = diag(sigma)^-1 G diag(sigma)^-1 / N, descending);
  * V[bands x ncomp] (row-major, eigenvectors of the ncomp largest, sign-fixed:

@@ -98,6 +98,7 @@ _SIGS = {
     "hyde_eig_cluster_size": (c_int, []),
     "hyde_debug_sure_prof": (c_int, [POINTER(ctypes.c_ulonglong)]),
     "hyde_debug_eig_state": (c_int, [c_void_p, c_int, c_int, _P, _P]),
+    "hyde_debug_gram_quant": (c_int, [c_void_p, c_int, c_int, _P, _P, _P]),
 }
 
 _lib = None

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -29,7 +30,7 @@ struct Layout {
   int B, chunk, nsplit, nsub, ldwu, taps, levels;
   long long n, ldE;
   DwtPlan plan;
-  size_t G, partial, amax, sigma, lam, tri, house, W, U, C, surv, S1, S2, kstar, tstar, esub, epost, rs, total;
+  size_t G, partial, sigma, lam, tri, house, W, U, C, surv, S1, S2, kstar, tstar, esub, epost, rs, total;
   int use_tc, npairs;
   size_t s1_img, s2_img;  // per-image strides (floats) of the LL scratch
 };
@@ -54,8 +55,12 @@ void make_layout(int rows, int cols, int B, int chunk, int levels, int taps, Lay
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += al(bytes); return o; };
   L->G = take((size_t)B * B * 8);
-  L->partial = take((size_t)(L->nsplit > L->npairs ? L->nsplit : L->npairs) * B * B * 8);
-  L->amax = take((size_t)B * 4);
+  {
+    // K1 workspace: the fp64 SIMT partials, or the tensor-core path's pieces
+    const size_t simt = (size_t)L->nsplit * B * B * 8;
+    const size_t tcw = L->use_tc ? gram_tc_ws_bytes(L->n, B, L->npairs) : 0;
+    L->partial = take(simt > tcw ? simt : tcw);
+  }
   L->sigma = take((size_t)B * 8);
   L->lam = take((size_t)B * 8);
   L->tri = take((size_t)(3 * B + 8) * 8);
@@ -243,9 +248,7 @@ static hyde_status resolve_params(hyde_handle h, int rows, int cols, const hyde_
 // K1: exact int8 tensor-core Gram (B <= 224) or the fp64 SIMT fallback
 static cudaError_t run_gram(const Layout& L, char* ws, const float* cube, double* G, int* nonfinite,
                             cudaStream_t st, int* state4 = nullptr) {
-  if (L.use_tc)
-    return launch_gram_tc(cube, L.n, L.B, (unsigned*)(ws + L.amax), (double*)(ws + L.partial), L.npairs, G,
-                          nonfinite, st, state4);
+  if (L.use_tc) return launch_gram_tc(cube, L.n, L.B, ws + L.partial, L.npairs, G, nonfinite, st, state4);
   return launch_gram(cube, L.n, L.B, (double*)(ws + L.partial), L.nsplit, G, nonfinite, st);
 }
 
@@ -580,16 +583,11 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
   auto coll = [&](int rc) -> hyde_status {
     return rc == 0 ? HYDE_OK : fail(h, HYDE_ENCCL, "collective callback failed");
   };
-  // ---- A1: global per-band scales, local exact Gram, all-reduced ----
+  // ---- A1: local Gram (own quantisation scales), all-reduced in fp64 ----
   {
     Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? 5 : 2, st);
     if (Ll.use_tc) {
-      unsigned* amax = (unsigned*)(wl + Ll.amax);
-      CK(launch_gram_amax(local, n_loc, B, amax, &rs->nonfinite, st));
-      s = coll(comm->allreduce_max_u32(comm->user, amax, (size_t)B, stream));
-      if (s != HYDE_OK) return s;
-      CK(launch_gram_tc_scaled(local, n_loc, B, amax, (double*)(wl + Ll.partial), Ll.npairs, Gm, &rs->nonfinite,
-                               st));
+      CK(launch_gram_tc(local, n_loc, B, wl + Ll.partial, Ll.npairs, Gm, &rs->nonfinite, st));
     } else {
       CK(launch_gram(local, n_loc, B, (double*)(wl + Ll.partial), Ll.nsplit, Gm, &rs->nonfinite, st));
     }
@@ -812,6 +810,10 @@ hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int
     });
   }
   for (auto& t : th) t.join();
+  // Every lane is ordered before the caller's stream moves on -- also when one
+  // failed: a failed lane (no event recorded) is drained on the host, so no
+  // lane kernel can still write `outs` after this call returns an error.
+  int first_bad = -1;
   for (int j = 0; j < L; ++j) {
     hyde_ctx* lh = h->lanes[j];
     h->launch_total += lh->launch_total;
@@ -820,8 +822,16 @@ hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int
     for (int k = 0; k < HYDE_NSTAGES; ++k) lh->launch_by_stage[k] = 0;
     for (auto& r : lh->recs) h->recs.push_back(r);   // stage time summed over lanes (busy time)
     lh->recs.clear();
-    if (res[j] != HYDE_OK) return fail(h, res[j], lh->err.empty() ? "batched lane failed" : lh->err);
-    CK(cudaStreamWaitEvent(st, h->lane_ev[j], 0));
+    if (res[j] != HYDE_OK) {
+      cudaStreamSynchronize(h->lane_st[j]);
+      if (first_bad < 0) first_bad = j;
+    } else {
+      CK(cudaStreamWaitEvent(st, h->lane_ev[j], 0));
+    }
+  }
+  if (first_bad >= 0) {
+    hyde_ctx* lh = h->lanes[first_bad];
+    return fail(h, res[first_bad], lh->err.empty() ? "batched lane failed" : lh->err);
   }
   return HYDE_OK;
 }
@@ -1012,7 +1022,7 @@ hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int
                oWtc = take((size_t)wtc_chunks(nc, r) * B * r * 8), oObj = take((size_t)max_iters * 8);
   const int np2 = gram_tc_npairs(nc);
   const int ns2 = gram_nsplit(nc, B);
-  const size_t oGp = take((size_t)(np2 > ns2 ? np2 : ns2) * BB * 8), oAmax = take((size_t)B * 4);
+  const size_t oGp = take(std::max((size_t)ns2 * BB * 8, gram_tc_supported(B) ? gram_tc_ws_bytes(nc, B, np2) : 0));
   s = ensure_ws(h, off, st);
   if (s != HYDE_OK) return s;
   char* ws = h->ws;
@@ -1037,7 +1047,7 @@ hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int
   } else {
     Gw = (double*)(ws + oGw);
     if (gram_tc_supported(B))
-      CK(launch_gram_tc(Cw, nc, B, (unsigned*)(ws + oAmax), (double*)(ws + oGp), np2, Gw, &rs->nonfinite, st));
+      CK(launch_gram_tc(Cw, nc, B, ws + oGp, np2, Gw, &rs->nonfinite, st));
     else
       CK(launch_gram(Cw, nc, B, (double*)(ws + oGp), ns2, Gw, &rs->nonfinite, st));
   }
@@ -1120,7 +1130,7 @@ hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, in
                oCoef = take(520 * 4);
   const int np2 = gram_tc_npairs(nc);
   const int ns2 = gram_nsplit(nc, B);
-  const size_t oPart = take((size_t)(np2 > ns2 ? np2 : ns2) * BB * 8), oAmax = take((size_t)B * 4);
+  const size_t oPart = take(std::max((size_t)ns2 * BB * 8, gram_tc_supported(B) ? gram_tc_ws_bytes(nc, B, np2) : 0));
   s = ensure_ws(h, off, st);
   if (s != HYDE_OK) return s;
   char* ws = h->ws;
@@ -1142,7 +1152,7 @@ hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, in
     if (nc != n) {          // padded levels: the band Gram of the coefficients themselves
       double* Gc = (double*)(ws + oGw);
       if (gram_tc_supported(B))
-        CK(launch_gram_tc(C, nc, B, (unsigned*)(ws + oAmax), (double*)(ws + oPart), np2, Gc, &rs->nonfinite, st));
+        CK(launch_gram_tc(C, nc, B, ws + oPart, np2, Gc, &rs->nonfinite, st));
       else
         CK(launch_gram(C, nc, B, (double*)(ws + oPart), ns2, Gc, &rs->nonfinite, st));
       Gw = Gc;
@@ -1263,6 +1273,34 @@ hyde_status hyde_k_gram(hyde_handle h, const float* cube, int n_pixels, int band
   h->last_rs = rs;
   CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
   CK(run_gram(L, h->ws, cube, gram, &rs->nonfinite, st));
+  return HYDE_OK;
+}
+
+hyde_status hyde_debug_gram_quant(hyde_handle h, int n_pixels, int bands, float* inv_s, int* centre,
+                                  long long* n_flagged) {
+  if (!h || !h->ws || bands < 1 || bands > 256 || n_pixels < 1) return HYDE_EPARAM;
+  DeviceGuard g(h->device);
+  Layout L;
+  make_layout(n_pixels, 1, bands, 1, 1, 2, &L);   // the layout hyde_k_gram used
+  if (!L.use_tc) {
+    if (n_flagged) *n_flagged = -1;
+    return HYDE_OK;
+  }
+  const GramQScale* qs = nullptr;
+  const int* cnt = nullptr;
+  gram_tc_debug_ptrs(h->ws + L.partial, L.n, bands, L.npairs, &qs, &cnt);
+  std::vector<GramQScale> q(bands);
+  std::vector<int> c(gram_tc_fix_splits());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(q.data(), qs, sizeof(GramQScale) * bands, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(c.data(), cnt, sizeof(int) * c.size(), cudaMemcpyDeviceToHost));
+  long long nf = 0;
+  for (int v : c) nf += v;
+  for (int b = 0; b < bands; ++b) {
+    if (inv_s) inv_s[b] = q[b].inv_s;
+    if (centre) centre[b] = q[b].c;
+  }
+  if (n_flagged) *n_flagged = nf;
   return HYDE_OK;
 }
 

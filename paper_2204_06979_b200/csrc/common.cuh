@@ -83,13 +83,20 @@ int gram_nsplit(long long n, int B);
 cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st, int sym = 0);
 bool gram_tc_supported(int B);
 int gram_tc_npairs(long long n, int min_px = 0);
-cudaError_t launch_gram_reduce_i64(const long long* partial, int np, int B, const unsigned* amax_bits, double* G,
-                                   cudaStream_t st);
-cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
-                           double* G, int* nonfinite, cudaStream_t st, int* state4 = nullptr);
-cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st, int* state4 = nullptr);
-cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsigned* amax_bits, double* partial,
-                                  int npairs, double* G, int* nonfinite, cudaStream_t st);
+// K1 quantisation of one band (k_gram_tc.cu): y ~ s (q + c), q = rint(y inv_s) - c
+struct GramQScale {
+  float inv_s;   // fp32 1 / step
+  float kf;      // fma addend 1.5 * 2^23 - c (exact)
+  int c;         // integer centre, |c| <= 2^21
+  int pad;
+  double s;      // 1 / (double)inv_s
+};
+// workspace of launch_gram_tc (scales, clip bitmap, int64 pair partials, fix partials)
+size_t gram_tc_ws_bytes(long long n, int B, int npairs);
+cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npairs, double* G, int* nonfinite,
+                           cudaStream_t st, int* state4 = nullptr);
+void gram_tc_debug_ptrs(void* ws, long long n, int B, int npairs, const GramQScale** qs, const int** cnt);
+int gram_tc_fix_splits();
 size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,

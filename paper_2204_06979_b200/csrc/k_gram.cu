@@ -150,78 +150,6 @@ cudaError_t launch_gram(const float* Y, long long n, int B, double* partial, int
   return launch_gram_reduce(partial, nsplit, B, G, st);
 }
 
-// K1 (tensor-core Gram): the per-pair partials are exact int64 (Q Q^T over the
-// pair's pixels; in the diagonal blocks [0, 128) and [128, B) the cross term
-// holds 2X, X = S0 S1^T, and (P + P^T)/2 is the exact integer).  Sum in
-// integers, scale once: G_ij = (sum) s_i s_j, s = 1 / fp32(16256 / max|y|),
-// independent of the pixel split; only i <= j is computed, both halves written.
-// Stage 1: S[i][j] = sum over pairs of P[k][i][j] for every element a pair
-// writes (all but the block rows >= 128, columns < 128), coalesced along j;
-// 8 warps split k, fixed order.  S overwrites P[0] (each element is read and
-// written by its own thread only).
-__global__ void __launch_bounds__(256) gram_reduce_i64_kernel(long long* __restrict__ partial, int np, int B) {
-  pdl_wait();
-  __shared__ long long part[8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const long long tot = (long long)B * B;
-  const long long idx = blockIdx.x * 32LL + lane;
-  const int i = idx < tot ? (int)(idx / B) : 0, j = idx < tot ? (int)(idx % B) : 0;
-  const bool active = idx < tot && !(i >= 128 && j < 128);
-  long long s = 0;
-  if (active) {
-    for (int k0 = w; k0 < np; k0 += 8 * 16) {
-      long long v[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int k = k0 + 8 * u;
-        v[u] = k < np ? __ldcs(partial + (long long)k * tot + idx) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < 16; ++u) s += v[u];
-    }
-  }
-  part[w][lane] = s;
-  __syncthreads();
-  if (w == 0 && active) {
-    long long t = part[0][lane];
-#pragma unroll
-    for (int q = 1; q < 8; ++q) t += part[q][lane];
-    partial[idx] = t;
-  }
-}
-
-// Stage 2: G_ij = G_ji = s_i s_j T_ij with T_ij = S_ij off the diagonal
-// 128-blocks and (S_ij + S_ji) / 2 on them (exact: the pairs wrote 256 X there).
-__global__ void __launch_bounds__(256) gram_finalize_i64_kernel(const long long* __restrict__ S, int B,
-                                                                const unsigned* __restrict__ amax_bits,
-                                                                double* __restrict__ G) {
-  pdl_wait();
-  const long long idx = blockIdx.x * 256LL + threadIdx.x;
-  if (idx >= (long long)B * B) return;
-  const int i = (int)(idx / B), j = (int)(idx % B);
-  if (i > j) return;
-  long long t = S[idx];
-  if ((i < 128) == (j < 128)) t = (t + S[(long long)j * B + i]) / 2;
-  auto scale = [&](int b) {
-    const float m = __uint_as_float(amax_bits[b]);
-    const float is = m > 0.f ? fminf((float)(16256.0 / (double)m), 1e30f) : 1.f;
-    return 1.0 / (double)is;
-  };
-  const double g = (double)t * scale(i) * scale(j);
-  G[(long long)i * B + j] = g;
-  G[(long long)j * B + i] = g;
-}
-
-cudaError_t launch_gram_reduce_i64(const long long* partial, int np, int B, const unsigned* amax_bits, double* G,
-                                   cudaStream_t st) {
-  const long long tot = (long long)B * B;
-  long long* P = const_cast<long long*>(partial);
-  cudaError_t e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, P, np, B);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(gram_finalize_i64_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st,
-                    (const long long*)P, B, amax_bits, G);
-}
-
 cudaError_t launch_gram_reduce(const double* partial, int nsplit, int B, double* G, cudaStream_t st, int sym) {
   long long tot = (long long)B * B;
   gram_reduce_kernel<<<(unsigned)((tot + 31) / 32), 256, 0, st>>>(partial, nsplit, B, G, sym);

@@ -1,32 +1,50 @@
 // K1 (north_star stage (1)) on the 5th-generation tensor
-// cores: an EXACT integer Gram of a quantised cube, G = diag(s) Q Q^T diag(s).
+// cores: an EXACT integer Gram of a quantised cube, with every pixel the
+// quantisation cannot represent added exactly in fp64.
 //
 // Why integers (DESIGN.md §4 K1): sigma_b^2 = 1/(N [(G+dI)^-1]_bb) amplifies
-// the Gram's relative error by ~the band SNR, so G must be good to ~1e-7
-// relative; fp32 (or TF32/BF16-split) accumulation over 10^6 pixels is not,
-// and any non-PSD rounding breaks noiseless cubes.  Here each band b is
-// scaled by inv_s_b = 16256 / max|y_b| (max from a pre-pass) and rounded:
-// q = rint(y inv_s) in [-16256, 16256], split q = 128 S0 + S1 with S0 in
-// [-127, 127], S1 in [-64, 63] (both int8).  Then
-//   Q Q^T = 16384 S0 S0^T + 128 (S0 S1^T + S1 S0^T) + S1 S1^T
-// three int8 x int8 -> int32 GEMMs (tcgen05.mma kind::i8), accumulated
-// EXACTLY in TMEM; G is Q Q^T scaled by s_a s_b in fp64.  The result is the
-// exact Gram of a 15-bit quantisation of the cube: symmetric PSD by
-// construction, deterministic, and ~1e-6 from the fp64 oracle end to end
-// (survey/design experiment: /tmp-free numbers in DESIGN.md).
+// the Gram's error by ~the band SNR, so G must be good to ~1e-8 relative;
+// fp32 (or TF32/BF16-split) accumulation over 10^6 pixels is not, and any
+// non-PSD rounding breaks noiseless cubes.
+//
+// Quantisation (robust to hot / dead / saturated pixels):
+//   * gram_qscale_kernel reads a fixed sample of every band (64 blocks of the
+//     pixel axis, <= 256 pixels each) and takes a centre m_b = median of the
+//     block means and a range R_b = 2 x the 8th-largest block max |y - m_b|,
+//     so a few outliers cannot widen the step (one 8-CTA cluster per band,
+//     1.6 % of the cube read at `large`; the old full max pre-pass read all);
+//   * inv_s = fp32(32767 / R_b), c_b = rint(m_b inv_s) (an integer centre),
+//     q = rint(y inv_s - c_b) in [-32768, 32767] (16 bits), y ~ s (q + c);
+//   * a value outside that range (outlier, NaN, Inf) sets its PIXEL's bit in a
+//     clip bitmap (its bytes still go through the MMAs; the fix replaces them).
+// Split q = 256 S0 + S1 (S0 in [-128, 127] signed, S1 in [0, 255] unsigned int8,
+// read straight off the bits of one fma -- see `convert`):
+//   Q Q^T = 65536 S0 S0^T + 256 (S0 S1^T + S1 S0^T) + S1 S1^T
+// int8 x int8 -> int32 GEMMs (tcgen05.mma kind::i8), accumulated EXACTLY in
+// TMEM; the per-pair partials (and sum_p q_p per band) are exact int64.
+// gram_fix_kernel then walks the bitmap and, for the flagged pixels P only,
+// forms F = sum_P y y^T in fp64 and D = sum_P q q^T, sum_P q in int64, and
+// the finalize kernel assembles, with N' = N - |P| and Q1' = sum_{p not in P} q,
+//   G = diag(s) [ (QQ^T - D) + c Q1'^T + Q1' c^T + N' c c^T ] diag(s) + F
+// (the bracket exact in 128-bit integers).  So G is the exact Gram of the
+// cube with the unflagged values rounded to the 16-bit grid s (q + c) and the
+// flagged pixels exact: symmetric PSD, deterministic, any dynamic range.
 //
 // Structure: clusters of 2 CTAs (one SM pair) per pixel range, cta_group::2
 // MMAs with M = 128 (64 rows per SM, TMEM "2x2" layout).  Bands are split
 // S_a = [0,128), S_b = [128,B); three tiles T_aa (128 x 128), T_ab (128 x Nb),
 // T_bb (128 x Nb), Nb = B-128 rounded up to 32; x 3 products = 480 of 512
-// TMEM columns for B <= 224.  16 converter warps per CTA load fp32 straight
-// from HBM (16-byte loads, ~90 KB in flight per SM), quantise and write the
-// int8 slices into shared memory in the UMMA canonical K-major layout; one
-// thread of the leader CTA issues the MMAs; the stage ring is released by
-// tcgen05.commit multicast to both CTAs.  Each CTA finally reads its TMEM,
-// combines the three products in int64 and writes its fp64 partial Gram.
+// TMEM columns for B <= 224.  14 converter warps per CTA load fp32 straight
+// from HBM (16-byte loads), quantise and write the int8 slices into shared
+// memory in the UMMA canonical K-major layout; one thread of the leader CTA
+// issues the MMAs; the stage ring is released by tcgen05.commit multicast to
+// both CTAs.  Each CTA finally reads its TMEM, combines the three products in
+// int64 and writes its exact integer partial.
 #include "common.cuh"
 #include "tc_util.cuh"
+
+#include <cooperative_groups.h>
+#include <type_traits>
 
 namespace {
 
@@ -37,6 +55,13 @@ constexpr int NTHREADS = (NCW + 2) * 32;
 constexpr int MAXU = 8;        // max band rows per converter warp per stage: (64 + 48) / 14
 constexpr int TMEM_COLS = 512;
 
+constexpr int GQ_MAX = 32767;  // v in [-32768, 32767]: the range maps to R = 32767 steps
+constexpr int QS_NBLK = 64;    // sample blocks per band (qscale)
+constexpr int FIX_SPLITS = 64; // pixel splits (CTAs) of the clipped-pixel correction
+constexpr int FIX_TB = 64;     // correction output block edge
+constexpr int FIX_TP = 32;     // correction pixels per stage
+constexpr int FIX_CAP = 2048;  // flagged-pixel list entries per pass
+
 struct GramTc {
   const float* Y;
   long long n;
@@ -44,9 +69,9 @@ struct GramTc {
   int nb;           // Nb (0 when B <= 128)
   int rows_tot;     // 64 + 64 + nb/2 (or 64)
   long long per_pair;
-  const unsigned* amax_bits;
-  double* partial;  // [pair][B][B]
-  int* nonfinite;
+  const GramQScale* qs;
+  long long* partial;  // [pair][B*B + B]: Q Q^T over the pair's pixels, then sum q per band
+  unsigned* bitmap;    // clipped-pixel bits
 };
 
 // smem regions of one int8 slice of a stage: P (64 rows: S_a bands of this SM)
@@ -76,7 +101,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   __shared__ __align__(8) uint64_t bar_done;
   __shared__ uint32_t tmem_base_sh;
   __shared__ float inv_s[2][64];
-  __shared__ double s_of[2][64];
+  __shared__ float kf_of[2][64];
 
   const int rank = (int)tc::cluster_ctarank();
   const int pair = blockIdx.x >> 1;
@@ -92,18 +117,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   // per-band quantisation scales of the rows this SM handles
   for (int i = threadIdx.x; i < 2 * 64; i += NTHREADS) {
     const int rg = i / 64, r = i % 64;
-    float is = 0.f;
-    double sv = 0.0;
+    float is = 0.f, kf = 8421376.0f;
     if (rg < nreg && r < region_rows(rg, nb)) {
       const int b = band_of(rg, r, rank, B, nb);
       if (b >= 0) {
-        const float m = __uint_as_float(P.amax_bits[b]);
-        is = m > 0.f ? fminf((float)(16256.0 / (double)m), 1e30f) : 1.f;
-        sv = 1.0 / (double)is;
+        is = P.qs[b].inv_s;
+        kf = P.qs[b].kf;
       }
     }
     inv_s[rg][r] = is;
-    s_of[rg][r] = sv;
+    kf_of[rg][r] = kf;
   }
   // dead rows (QS padding, bands >= B) are never written: zero the ring once
   for (int i = threadIdx.x; i < NI * stage_bytes / 16; i += NTHREADS)
@@ -140,8 +163,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   } else if (warp == 1) {
     // ================= MMA issuer (leader CTA, one thread) =================
     if (rank == 0 && lane == 0 && nst > 0) {
-      const uint32_t id_aa = tc::idesc_i8(128, 128);
-      const uint32_t id_b = nb > 0 ? tc::idesc_i8(128, nb) : 0u;
+      // S0 (high bytes) signed, S1 (low bytes) unsigned
+      const uint32_t id_aa = tc::idesc_i8(128, 128, true, true);
+      const uint32_t id_aa01 = tc::idesc_i8(128, 128, true, false);
+      const uint32_t id_aa11 = tc::idesc_i8(128, 128, false, false);
+      const uint32_t id_b = nb > 0 ? tc::idesc_i8(128, nb, true, true) : 0u;
+      const uint32_t id_b01 = nb > 0 ? tc::idesc_i8(128, nb, true, false) : 0u;
+      const uint32_t id_b10 = nb > 0 ? tc::idesc_i8(128, nb, false, true) : 0u;
+      const uint32_t id_b11 = nb > 0 ? tc::idesc_i8(128, nb, false, false) : 0u;
       const uint32_t sbase = tc::smem_u32(smem);
       for (int s = 0; s < nst; ++s) {
         const int is = s % NI;
@@ -159,17 +188,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           tc::mma_i8<2>(tmem + 0 * CL, dsc(st0, 0, 0), dsc(st0, 0, 0), id_aa, first);
           // diagonal tiles: only X = S0 S1^T (the cross term is X + X^T,
           // symmetrised in the reduction) -- one MMA of four saved
-          tc::mma_i8<2>(tmem + 1 * CL, dsc(st0, 0, 0), dsc(st1, 0, 0), id_aa, first);
-          tc::mma_i8<2>(tmem + 2 * CL, dsc(st1, 0, 0), dsc(st1, 0, 0), id_aa, first);
+          tc::mma_i8<2>(tmem + 1 * CL, dsc(st0, 0, 0), dsc(st1, 0, 0), id_aa01, first);
+          tc::mma_i8<2>(tmem + 2 * CL, dsc(st1, 0, 0), dsc(st1, 0, 0), id_aa11, first);
           if (nb > 0) {
             // T_ab: A = P, B = QB ; T_bb: A = QA, B = QB
             tc::mma_i8<2>(tmem + 0 * CL + off_ab, dsc(st0, 0, 0), dsc(st0, 1, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st0, 0, 0), dsc(st1, 1, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st1, 0, 0), dsc(st0, 1, 0), id_b, 1u);
-            tc::mma_i8<2>(tmem + 2 * CL + off_ab, dsc(st1, 0, 0), dsc(st1, 1, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st0, 0, 0), dsc(st1, 1, 0), id_b01, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st1, 0, 0), dsc(st0, 1, 0), id_b10, 1u);
+            tc::mma_i8<2>(tmem + 2 * CL + off_ab, dsc(st1, 0, 0), dsc(st1, 1, 0), id_b11, first);
             tc::mma_i8<2>(tmem + 0 * CL + off_bb, dsc(st0, 1, 0), dsc(st0, 1, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1, 0), dsc(st1, 1, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1, 0), dsc(st1, 1, 0), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1, 0), dsc(st1, 1, 0), id_b01, first);
+            tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1, 0), dsc(st1, 1, 0), id_b11, first);
           }
         }
         tc::mma_commit<2>(&bar_empty[is], 0x3);
@@ -178,7 +207,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp >= 2) {
     // ================= converters: HBM fp32 -> int8 slices in smem ==========
-    // (non-finite input is detected by the amax pre-pass)
+    // (non-finite input fails the range test and is flagged like an outlier;
+    // gram_fix_kernel raises the non-finite flag when it reads the pixel)
     // One unit = one live band row of the stage: the warp's 32 lanes load its
     // 128 pixels as 32 contiguous 16-byte pieces (512 B per load instruction)
     // and write the 128 int8 bytes of each slice as one swizzled 128-B line
@@ -189,20 +219,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const int nrow_q = nreg == 2 ? max(0, min(hb, B - 128 - rank * hb)) : 0;
     const int nunits = nrow_p + nrow_q;
     const bool vec_ok = (P.n % 4 == 0) && (((uintptr_t)P.Y & 15) == 0);
-    long long src0[MAXU];
+    int brow[MAXU];   // band of each unit (-1: none)
+    const float* ybase = P.Y + p_begin + 4 * lane;
     int soff[MAXU];
     float isc[MAXU];
+    const float* kfu = &kf_of[0][0];   // per-unit fma addend kf_of[rg][r], index soff >> 7 (register budget)
+    int sq[MAXU];   // this lane's sum of q per unit (band): |.| <= 4 * 32768 * 256 stages
 #pragma unroll
     for (int t = 0; t < MAXU; ++t) {
       const int u = cw + t * NCW;
-      src0[t] = -1;
+      brow[t] = -1;
       soff[t] = 0;
       isc[t] = 0.f;
+      sq[t] = 0;
       if (u < nunits) {
         const int rg = u < nrow_p ? 0 : 1;
         const int r = rg ? u - nrow_p : u;
         const int b = rg ? 128 + rank * hb + r : rank * 64 + r;
-        src0[t] = (long long)b * P.n + p_begin + 4 * lane;
+        brow[t] = b;
         soff[t] = region_base(rg) + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + 4 * (lane & 3);
         isc[t] = inv_s[rg][r];
       }
@@ -216,8 +250,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int t = 0; t < MAXU; ++t) {
         v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (src0[t] >= 0 && s < nst) {
-          const float* src = P.Y + src0[t] + sh;
+        if (brow[t] >= 0 && s < nst) {
+          const float* src = ybase + (long long)brow[t] * P.n + sh;
           if (full) {
             v[t] = __ldcs(reinterpret_cast<const float4*>(src));
           } else {
@@ -230,31 +264,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
     };
-    // quantise the registers of stage s into its smem slot:
-    // q = rint(y / s_b) via the 1.5*2^23 rounding constant (exact RN of the
-    // product), t = q + 64, S0 = t >> 7 in [-127, 127], S1 = (t & 127) - 64
-    // in [-64, 63]; four values packed per 32-bit word with byte permutes
+    // quantise the registers of stage s into its smem slot.
+    // Per value: r = fma(y, inv_s, 2^23 + 32768 - c) is the exact RN of
+    // y inv_s - c + 32768 + 2^23, so for an in-range value bits(r) =
+    // 0x4B000000 + u, u = v + 32768 in [0, 65535], v = rint(y inv_s - c).  The
+    // int8 slices are read straight off those bits: S0 = byte1 ^ 0x80 (signed,
+    // = floor(v / 256)), S1 = byte0 (unsigned), v = 256 S0 + S1.  For ANY bits
+    // the MMAs consume v_used = (bits & 0xFFFF) - 32768; a value whose bits
+    // leave [0x4B000000, 0x4B00FFFF] (out of range, NaN, Inf) flags its pixel
+    // and gram_fix_kernel replaces the pixel's v_used terms by the exact ones.
+    // Per 4 values: 4 FFMA, 4 LOP3 (range OR), 6 PRMT, 1 LOP3 (sign flip),
+    // 2 IDP4A + IMAD (sum of v); the clip atomics run once per stage, rarely.
+    auto convert = [&](auto full_tag, int s, const float4 (&v)[MAXU], unsigned char* st0, unsigned char* st1) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      const long long sh = (long long)s * KC + 4 * lane;   // first pixel of this lane, within the pair
+      unsigned acc0 = 0u, acc1 = 0u, acc2 = 0u, acc3 = 0u;   // OR of (bits ^ 0x4B000000) per pixel
+#pragma unroll
+      for (int t = 0; t < MAXU; ++t) {
+        if (cw + t * NCW >= nunits) break;
+        const float kf = kfu[soff[t] >> 7];
+        unsigned r0 = __float_as_uint(fmaf(v[t].x, isc[t], kf));
+        unsigned r1 = __float_as_uint(fmaf(v[t].y, isc[t], kf));
+        unsigned r2 = __float_as_uint(fmaf(v[t].z, isc[t], kf));
+        unsigned r3 = __float_as_uint(fmaf(v[t].w, isc[t], kf));
+        if (!FULL) {   // ragged tail: pixels past the pair's end are v = 0 (u = 32768)
+          r0 = sh + 0 < n_end ? r0 : 0x4B008000u;
+          r1 = sh + 1 < n_end ? r1 : 0x4B008000u;
+          r2 = sh + 2 < n_end ? r2 : 0x4B008000u;
+          r3 = sh + 3 < n_end ? r3 : 0x4B008000u;
+        }
+        acc0 |= r0 ^ 0x4B000000u;
+        acc1 |= r1 ^ 0x4B000000u;
+        acc2 |= r2 ^ 0x4B000000u;
+        acc3 |= r3 ^ 0x4B000000u;
+        const uint32_t w0 = __byte_perm(__byte_perm(r0, r1, 0x0051), __byte_perm(r2, r3, 0x0051), 0x5410) ^ 0x80808080u;
+        const uint32_t w1 = __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
+        sq[t] += 256 * __dp4a((int)w0, 0x01010101, 0) + (int)__dp4a(w1, 0x01010101u, 0u);
+        *reinterpret_cast<uint32_t*>(st0 + soff[t]) = w0;
+        *reinterpret_cast<uint32_t*>(st1 + soff[t]) = w1;
+      }
+      const unsigned pm = ((acc0 >> 16) ? 1u : 0u) | ((acc1 >> 16) ? 2u : 0u) | ((acc2 >> 16) ? 4u : 0u) |
+                          ((acc3 >> 16) ? 8u : 0u);
+      if (pm) {
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j)
+          if ((pm >> j) & 1u) {
+            const long long px = p_begin + sh + j;
+            atomicOr(P.bitmap + (px >> 5), 1u << (px & 31));
+          }
+      }
+    };
     auto store_stage = [&](int s, const float4 (&v)[MAXU]) {
       const int is = s % NI;
       tc::mbar_wait(&bar_empty[is], (uint32_t)(((s / NI) & 1) ^ 1));   // local barrier (commit multicast)
       unsigned char* st0 = smem + is * stage_bytes;
       unsigned char* st1 = st0 + slice_bytes;
-#pragma unroll
-      for (int t = 0; t < MAXU; ++t) {
-        if (cw + t * NCW >= nunits) break;
-        const float x[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
-        int h[4], l[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int tq = __float_as_int(fmaf(x[j], isc[t], 12582912.0f)) - (0x4B400000 - 64);
-          h[j] = tq >> 7;
-          l[j] = (tq & 127) - 64;
-        }
-        const uint32_t w0 = __byte_perm(__byte_perm(h[0], h[1], 0x0040), __byte_perm(h[2], h[3], 0x0040), 0x5410);
-        const uint32_t w1 = __byte_perm(__byte_perm(l[0], l[1], 0x0040), __byte_perm(l[2], l[3], 0x0040), 0x5410);
-        *reinterpret_cast<uint32_t*>(st0 + soff[t]) = w0;
-        *reinterpret_cast<uint32_t*>(st1 + soff[t]) = w1;
-      }
+      if ((long long)s * KC + KC <= n_end)
+        convert(std::true_type{}, s, v, st0, st1);
+      else
+        convert(std::false_type{}, s, v, st0, st1);
       tc::fence_proxy_async_smem();
       // named barrier 1+slot: the forwarder warp (no loads in flight) makes the
       // single cluster-scope release-arrive for the whole CTA
@@ -268,13 +336,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       load_stage(s + 2, va);
       store_stage(s + 1, vb);
     }
+    // sum_p q of every unit's band over this pair's pixels (exact int64)
+    {
+      long long* Q1 = P.partial + (long long)pair * ((long long)B * B + B) + (long long)B * B;
+#pragma unroll
+      for (int t = 0; t < MAXU; ++t) {
+        const int u = cw + t * NCW;
+        if (u >= nunits) break;
+        long long v = sq[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+          const int b = u < nrow_p ? rank * 64 + u : 128 + rank * hb + (u - nrow_p);
+          Q1[b] = v;
+        }
+      }
+    }
 
     // ================= epilogue: TMEM -> exact int64 -> fp64 partial ========
     if (cw < 4) {
       const int q4 = warp & 3;                    // TMEM lane quadrant of this warp
       const int L = q4 * 32 + lane;               // TMEM lane = this thread's row slot
       const int m = L & 63, half = L >> 6;
-      long long* Pq = reinterpret_cast<long long*>(P.partial) + (long long)pair * B * B;
+      long long* Pq = P.partial + (long long)pair * ((long long)B * B + B);
       if (nst > 0) {
         tc::mbar_wait_cluster(&bar_done, 0);
         tc::tc_fence_after();
@@ -305,11 +389,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const int bj = t == 0 ? (nn < (B < 128 ? B : 128) ? nn : -1) : (128 + nn < B ? 128 + nn : -1);
             if (bj < 0) continue;
             // T_ab holds S0 S1^T + S1 S0^T; the diagonal tiles hold X = S0 S1^T only:
-            // 256 X here, (P + P^T) / 2 in the reduction gives 128 (X + X^T).
+            // 512 X here, (P + P^T) / 2 in the reduction gives 256 (X + X^T).
             // The partial is the EXACT integer (Q Q^T over this pair's pixels):
             // the reduction sums integers and scales once, so G does not depend
             // on how the pixels were split over pairs.
-            const long long qq = 16384LL * (long long)(int)a0[j] + (t == 1 ? 128LL : 256LL) * (long long)(int)a1[j] +
+            const long long qq = 65536LL * (long long)(int)a0[j] + (t == 1 ? 256LL : 512LL) * (long long)(int)a1[j] +
                                  (long long)(int)a2[j];
             Pq[(long long)bi * B + bj] = qq;
           }
@@ -325,46 +409,382 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   }
 }
 
-__global__ void amax_kernel(const float* __restrict__ Y, long long n, unsigned* amax_bits, int* nonfinite) {
+
+// ------------------------------------------------------------------ qscale
+// One 8-CTA cluster per band, one sample block per warp.  Block k of the pixel
+// axis ([kN/64, (k+1)N/64)) is sampled at <= 256 pixels (all of them, or two
+// 128-pixel runs at the starts of its halves: 1.6 % of the cube at `large`);
+// per block: mean, min, max of the finite samples, written into the leader
+// CTA's shared memory (DSMEM).  The leader: m = lower median of the block
+// means; dev_k = max(max_k - m, m - min_k); R = 2 x the 8th largest dev_k
+// (rank min(7, nblk/8): the largest
+// for fewer than 16 blocks; the largest when that is 0; |m|, else 1e-30, when
+// all are 0: every nonzero value is then flagged and exact); widened so
+// |c| <= 2^21 (the fma addend must stay in [2^23, 2^24)).
+// Also zeroes a slice of the clip bitmap and, on CTA 0, the caller's
+// rank-state words -- the first kernel of the step.
+constexpr int QS_CL = 8;   // CTAs per band (cluster)
+__global__ void __cluster_dims__(QS_CL, 1, 1) __launch_bounds__(256)
+    gram_qscale_kernel(const float* __restrict__ Y, long long n, GramQScale* qs, unsigned* bitmap, long long nwords,
+                       int* st4, int nst4) {
   pdl_wait();
-  const int b = blockIdx.y;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int b = blockIdx.x / QS_CL, crank = (int)cl.block_rank();
+  {
+    const long long w0 = nwords * blockIdx.x / gridDim.x, w1 = nwords * (blockIdx.x + 1) / gridDim.x;
+    for (long long w = w0 + threadIdx.x; w < w1; w += blockDim.x) bitmap[w] = 0u;
+    if (st4 && blockIdx.x == 0 && (int)threadIdx.x < nst4) st4[threadIdx.x] = 0;
+  }
+  __shared__ double bmean[QS_NBLK];
+  __shared__ float bmin[QS_NBLK], bmax[QS_NBLK], bdev[QS_NBLK];
+  __shared__ float m_sh;
+  const int nblk = n < QS_NBLK ? (int)n : QS_NBLK;
   const float* row = Y + (long long)b * n;
-  unsigned m = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = crank * 8 + warp;
+  if (k < nblk) {
+    const long long p0 = n * k / nblk, p1 = n * (k + 1) / nblk, len = p1 - p0;
+    double sum = 0.0;
+    int cnt = 0;
+    float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+    auto take = [&](float v) {
+      const bool ok = isfinite(v);
+      sum += ok ? (double)v : 0.0;
+      cnt += ok;
+      mn = ok ? fminf(mn, v) : mn;
+      mx = ok ? fmaxf(mx, v) : mx;
+    };
+    if (len <= 256) {
+      for (long long i = lane; i < len; i += 32) take(__ldg(row + p0 + i));
+    } else {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float* src = row + p0 + len * j / 2;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[4 * j + u] = __ldg(src + lane + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) take(v[u]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      *cl.map_shared_rank(&bmean[k], 0) = cnt > 0 ? sum / cnt : 0.0;
+      *cl.map_shared_rank(&bmin[k], 0) = cnt > 0 ? mn : 0.f;
+      *cl.map_shared_rank(&bmax[k], 0) = cnt > 0 ? mx : 0.f;
+    }
+  }
+  cl.sync();
+  if (crank != 0) return;
+  // order statistics by rank counting (ties broken by block index)
+  if ((int)threadIdx.x < nblk) {
+    const int kk = threadIdx.x;
+    int r = 0;
+    for (int j = 0; j < nblk; ++j) r += (bmean[j] < bmean[kk]) || (bmean[j] == bmean[kk] && j < kk);
+    if (r == (nblk - 1) / 2) m_sh = (float)bmean[kk];
+  }
+  __syncthreads();
+  const float m = m_sh;
+  if ((int)threadIdx.x < nblk) {
+    const int kk = threadIdx.x;
+    bdev[kk] = fminf(fmaxf(bmax[kk] - m, m - bmin[kk]), 3e38f);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // rank min(7, nblk/8) and rank 0 (largest) of bdev, descending
+    const int want = (nblk >> 3) < 7 ? (nblk >> 3) : 7;
+    float r7 = 0.f, r0 = 0.f;
+    for (int kk = lane; kk < nblk; kk += 32) {
+      int r = 0;
+      for (int j = 0; j < nblk; ++j) r += (bdev[j] > bdev[kk]) || (bdev[j] == bdev[kk] && j < kk);
+      if (r == want) r7 = bdev[kk];
+      if (r == 0) r0 = bdev[kk];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r7 = fmaxf(r7, __shfl_xor_sync(0xffffffffu, r7, o));
+      r0 = fmaxf(r0, __shfl_xor_sync(0xffffffffu, r0, o));
+    }
+    if (lane == 0) {
+      double R = 2.0 * (double)r7;
+      if (!(R > 0.0)) R = 2.0 * (double)r0;
+      if (!(R > 0.0)) R = fabs((double)m);
+      if (!(R > 0.0)) R = 1e-30;
+      const double cmax = 2097152.0;   // 2^21
+      if (fabs((double)m) * GQ_MAX / R > cmax) R = fabs((double)m) * GQ_MAX / cmax;
+      if (R > 3e38) R = 3e38;
+      const float is = (float)((double)GQ_MAX / R);
+      double cd = rint((double)m * (double)is);
+      cd = fmin(fmax(cd, -cmax), cmax);
+      GramQScale o;
+      o.inv_s = is;
+      o.c = (int)cd;
+      o.kf = (float)(8421376.0 - cd);   // 2^23 + 32768 - c, an exact integer in [2^22, 2^24)
+      o.pad = 0;
+      o.s = 1.0 / (double)is;
+      qs[b] = o;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ reduce
+// Stage 1: S[e] = sum over pairs of P[k][e] for every element a pair writes
+// (B x B without the block rows >= 128 / columns < 128, then the B sums of q),
+// coalesced; 8 warps split k, fixed order.  S overwrites P[0] (each element is
+// read and written by its own thread only).
+__global__ void __launch_bounds__(256) gram_reduce_i64_kernel(long long* __restrict__ partial, int np, int B) {
+  pdl_wait();
+  __shared__ long long part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long bb = (long long)B * B, tot = bb + B;
+  const long long idx = blockIdx.x * 32LL + lane;
+  const int i = idx < bb ? (int)(idx / B) : 0, j = idx < bb ? (int)(idx % B) : 0;
+  const bool active = idx < tot && !(idx < bb && i >= 128 && j < 128);
+  long long s = 0;
+  if (active) {
+    for (int k0 = w; k0 < np; k0 += 8 * 16) {
+      long long v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = k0 + 8 * u;
+        v[u] = k < np ? __ldcs(partial + (long long)k * tot + idx) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+  }
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && active) {
+    long long t = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += part[q][lane];
+    partial[idx] = t;
+  }
+}
+
+// ------------------------------------------------------------------ fix
+// The flagged pixels P of one pixel split, in increasing order: F = sum y y^T
+// (fp64), D = sum q q^T and, on the diagonal output blocks, sum q (int64),
+// q recomputed exactly as the converters did.  Grid: FIX_SPLITS CTAs, each
+// walking the upper-triangular 64x64 output blocks of its split.  A split
+// without a flagged pixel writes only its count (0) and exits after one scan
+// of its bitmap words.
+struct FixOut {
+  double* F;        // [FIX_SPLITS][B*B]
+  long long* D;     // [FIX_SPLITS][B*B]
+  long long* Q1;    // [FIX_SPLITS][B]
+  int* cnt;         // [FIX_SPLITS]
+};
+
+// the integer the converters fed to the MMAs for value y (any y, flagged or not)
+__device__ __forceinline__ int quant_q(float y, const GramQScale& q) {
+  return (int)(__float_as_uint(fmaf(y, q.inv_s, q.kf)) & 0xFFFFu) - 32768;
+}
+
+__global__ void __launch_bounds__(256) gram_fix_kernel(const float* __restrict__ Y, long long n, int B, int nbk,
+                                                       const GramQScale* __restrict__ qsc,
+                                                       const unsigned* __restrict__ bitmap, FixOut o,
+                                                       int* nonfinite) {
+  pdl_wait();
+  __shared__ float As[FIX_TP][FIX_TB + 1];
+  __shared__ float Bs[FIX_TP][FIX_TB + 1];
+  __shared__ int Aq[FIX_TP][FIX_TB + 1];
+  __shared__ int Bq[FIX_TP][FIX_TB + 1];
+  __shared__ int list[FIX_CAP];
+  __shared__ int wtot[8];
+  const int split = blockIdx.x;
+  const long long nw = (n + 31) / 32;
+  const long long wper = ((nw + FIX_SPLITS - 1) / FIX_SPLITS + 3) / 4 * 4;
+  const long long w_begin = split * wper, w_end = min(nw, w_begin + wper);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntp = nbk * (nbk + 1) / 2;
   bool bad = false;
-  const bool vec = (n % 4 == 0) && (((uintptr_t)Y & 15) == 0);
-  if (vec) {
-    // eight independent 16-byte loads in flight per thread per step
-    const long long n4 = n / 4;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    for (; i + 7 * stride < n4; i += 8 * stride) {
-      float4 v[8];
+  // one CTA per pixel split walks every upper-triangular 64 x 64 output block;
+  // the first walk finds whether the split has any flagged pixel at all
+  for (int tp = 0; tp < ntp; ++tp) {
+  int pr = tp, bi = 0;
+  while (pr >= nbk - bi) { pr -= nbk - bi; ++bi; }
+  const int bj = bi + pr;
+  const int i0 = bi * FIX_TB, j0 = bj * FIX_TB;
+  double f[4][4];
+  long long d[4][4], q1[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(row) + i + u * stride);
+  for (int a = 0; a < 4; ++a) {
+    q1[a] = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        m = max(m, __float_as_uint(fabsf(v[u].x)));
-        m = max(m, __float_as_uint(fabsf(v[u].y)));
-        m = max(m, __float_as_uint(fabsf(v[u].z)));
-        m = max(m, __float_as_uint(fabsf(v[u].w)));
+    for (int c = 0; c < 4; ++c) { f[a][c] = 0.0; d[a][c] = 0; }
+  }
+  int total = 0;
+  // chunks of 1024 bitmap words: 4 consecutive words per thread, so thread
+  // order = pixel order; a block scan of the bit counts places every flagged
+  // pixel in the list in increasing order (one round trip when none is set)
+  for (long long wc = w_begin; wc < w_end; wc += 1024) {
+    unsigned wv[4];
+    int c = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long w = wc + threadIdx.x * 4 + u;
+      wv[u] = w < w_end ? bitmap[w] : 0u;
+      c += __popc(wv[u]);
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    int before = 0, chunk = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      before += q < warp ? wtot[q] : 0;
+      chunk += wtot[q];
+    }
+    __syncthreads();
+    if (chunk == 0) continue;
+    const int excl = before + incl - c;
+    for (int base = 0; base < chunk; base += FIX_CAP) {
+      int pos = excl;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        unsigned bits = wv[u];
+        while (bits) {
+          const int t = __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (pos >= base && pos < base + FIX_CAP) list[pos - base] = (int)((wc + threadIdx.x * 4 + u) * 32 + t);
+          ++pos;
+        }
+      }
+      __syncthreads();
+      const int nl = min(FIX_CAP, chunk - base);
+      total += nl;
+      for (int p0 = 0; p0 < nl; p0 += FIX_TP) {
+#pragma unroll
+        for (int it = 0; it < (FIX_TB * FIX_TP) / 256; ++it) {
+          const int idx = threadIdx.x + it * 256;
+          const int r = idx / FIX_TP, cc = idx % FIX_TP;
+          float va = 0.f, vb = 0.f;
+          int qa = 0, qb = 0;
+          if (p0 + cc < nl) {
+            const long long p = list[p0 + cc];
+            if (i0 + r < B) { va = Y[(long long)(i0 + r) * n + p]; qa = quant_q(va, qsc[i0 + r]); }
+            if (j0 + r < B) { vb = Y[(long long)(j0 + r) * n + p]; qb = quant_q(vb, qsc[j0 + r]); }
+          }
+          bad |= !isfinite(va) || !isfinite(vb);
+          As[cc][r] = va;
+          Bs[cc][r] = vb;
+          Aq[cc][r] = qa;
+          Bq[cc][r] = qb;
+        }
+        __syncthreads();
+        for (int pp = 0; pp < FIX_TP; ++pp) {
+          double a[4], bv[4];
+          long long ia[4], ib[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            a[q] = (double)As[pp][ty * 4 + q];
+            bv[q] = (double)Bs[pp][tx * 4 + q];
+            ia[q] = Aq[pp][ty * 4 + q];
+            ib[q] = Bq[pp][tx * 4 + q];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            q1[u] += ia[u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              f[u][v] = fma(a[u], bv[v], f[u][v]);
+              d[u][v] += ia[u] * ib[v];
+            }
+          }
+        }
+        __syncthreads();
       }
     }
-    for (; i < n4; i += stride) {
-      float4 v = __ldcs(reinterpret_cast<const float4*>(row) + i);
-      m = max(m, __float_as_uint(fabsf(v.x)));
-      m = max(m, __float_as_uint(fabsf(v.y)));
-      m = max(m, __float_as_uint(fabsf(v.z)));
-      m = max(m, __float_as_uint(fabsf(v.w)));
-    }
-  } else {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-      m = max(m, __float_as_uint(fabsf(__ldcs(row + i))));
   }
-  bad = m >= 0x7F800000u;
+  if (tp == 0 && threadIdx.x == 0) o.cnt[split] = total;
+  if (total == 0) return;
+  double* F = o.F + (long long)split * B * B;
+  long long* D = o.D + (long long)split * B * B;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(&amax_bits[b], m);
+  for (int u = 0; u < 4; ++u) {
+    const int i = i0 + ty * 4 + u;
+    if (i >= B) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int j = j0 + tx * 4 + v;
+      if (j < B) {
+        F[(long long)i * B + j] = f[u][v];
+        D[(long long)i * B + j] = d[u][v];
+      }
+    }
+    if (bi == bj && tx == 0) o.Q1[(long long)split * B + i] = q1[u];
+  }
+  }
   if (bad) atomicOr(nonfinite, 1);
+}
+
+__device__ __forceinline__ double i128_to_f64(__int128 x) {
+  const bool neg = x < 0;
+  const unsigned __int128 u = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;
+  const double v = (double)(unsigned long long)(u >> 64) * 18446744073709551616.0 + (double)(unsigned long long)u;
+  return neg ? -v : v;
+}
+
+// Stage 2: G_ij = G_ji = s_i s_j T_ij + F_ij (i <= j) with
+//   T = (S - D) + c_i Q1'_j + c_j Q1'_i + N' c_i c_j   (exact, 128-bit)
+// S_ij = sum of the pair partials, (S_ij + S_ji)/2 on the diagonal 128-blocks
+// (exact: the pairs wrote 512 X there); D, F, Q1' from the non-empty fix splits
+// in split order.
+__global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __restrict__ S, int B, long long n,
+                                                            const GramQScale* __restrict__ qsc, FixOut o,
+                                                            double* __restrict__ G) {
+  pdl_wait();
+  __shared__ int live[FIX_SPLITS];
+  __shared__ int nlive;
+  __shared__ long long np_sh;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    long long np = 0;
+    for (int k = 0; k < FIX_SPLITS; ++k) {
+      const int v = o.cnt[k];
+      if (v) { live[c++] = k; np += v; }
+    }
+    nlive = c;
+    np_sh = np;
+  }
+  __syncthreads();
+  const long long idx = blockIdx.x * 256LL + threadIdx.x;
+  if (idx >= (long long)B * B) return;
+  const int i = (int)(idx / B), j = (int)(idx % B);
+  if (i > j) return;
+  long long t = S[idx];
+  if ((i < 128) == (j < 128)) t = (t + S[(long long)j * B + i]) / 2;
+  const long long* Q1 = S + (long long)B * B;
+  long long q1i = Q1[i], q1j = Q1[j];
+  const long long np = np_sh;
+  double f = 0.0;
+  for (int kk = 0; kk < nlive; ++kk) {
+    const int k = live[kk];
+    t -= o.D[(long long)k * B * B + idx];
+    f += o.F[(long long)k * B * B + idx];
+    q1i -= o.Q1[(long long)k * B + i];
+    q1j -= o.Q1[(long long)k * B + j];
+  }
+  const long long ci = qsc[i].c, cj = qsc[j].c;
+  const __int128 T = (__int128)t + (__int128)ci * q1j + (__int128)cj * q1i + (__int128)(n - np) * ci * cj;
+  const double g = i128_to_f64(T) * qsc[i].s * qsc[j].s + f;
+  G[(long long)i * B + j] = g;
+  G[(long long)j * B + i] = g;
 }
 
 }  // namespace
@@ -373,14 +793,16 @@ bool gram_tc_supported(int B) { return B >= 1 && B <= 224; }
 
 // SM pairs for n pixels: min_px = 0 -> as many as the GPU has (at most 74,
 // >= 512 pixels each: latency); min_px > 0 -> at least min_px pixels each
-// (throughput mode of the batched lanes)
+// (throughput mode of the batched lanes).  At most 32768 pixels per pair: the
+// int32 TMEM accumulators must hold the T_ab cross term S0 S1^T + S1 S0^T
+// (|.| <= 2 * 128 * 255 per pixel) and S1 S1^T (<= 255^2 per pixel).
 int gram_tc_npairs(long long n, int min_px) {
   long long np = min_px > 0 ? n / min_px : (n + 4LL * KC - 1) / (4LL * KC);
   if (np > 74) np = 74;
   if (np < 1) np = 1;
   long long per = (n + np - 1) / np;
-  if (per > 100000) {
-    np = (n + 99999) / 100000;
+  if (per > 32768) {
+    np = (n + 32767) / 32768;
     per = (n + np - 1) / np;
   }
   per = (per + KC - 1) / KC * KC;
@@ -388,30 +810,55 @@ int gram_tc_npairs(long long n, int min_px) {
   return (int)np;
 }
 
-// per-band max |y| bit patterns (the quantisation scales of K1) + non-finite flag
-// zero the per-band max words (and the caller's RankState, when given) as a
-// kernel, so the whole step stays a chain of dependent launches (no memset node)
-__global__ void zero_kernel(unsigned* a, int na, int* st4) {
-  pdl_wait();
-  for (int i = threadIdx.x; i < na; i += blockDim.x) a[i] = 0u;
-  if (st4 && threadIdx.x < (int)(sizeof(RankState) / sizeof(int))) st4[threadIdx.x] = 0;
+namespace {
+size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+struct TcWs {
+  GramQScale* qs;
+  unsigned* bitmap;
+  long long nwords;
+  long long* partial;
+  FixOut fix;
+};
+TcWs carve(void* base, long long n, int B, int npairs) {
+  char* p = (char*)base;
+  TcWs w;
+  const size_t bb = (size_t)B * B;
+  w.qs = (GramQScale*)p;                          p += al256((size_t)B * sizeof(GramQScale));
+  w.nwords = (n + 31) / 32;
+  w.bitmap = (unsigned*)p;                        p += al256((size_t)w.nwords * 4);
+  w.partial = (long long*)p;                      p += al256((size_t)npairs * (bb + B) * 8);
+  w.fix.F = (double*)p;                           p += al256((size_t)FIX_SPLITS * bb * 8);
+  w.fix.D = (long long*)p;                        p += al256((size_t)FIX_SPLITS * bb * 8);
+  w.fix.Q1 = (long long*)p;                       p += al256((size_t)FIX_SPLITS * B * 8);
+  w.fix.cnt = (int*)p;                            p += al256((size_t)FIX_SPLITS * 4);
+  return w;
+}
+}  // namespace
+
+size_t gram_tc_ws_bytes(long long n, int B, int npairs) {
+  const size_t bb = (size_t)B * B;
+  return al256((size_t)B * sizeof(GramQScale)) + al256((size_t)((n + 31) / 32) * 4) +
+         al256((size_t)npairs * (bb + B) * 8) + 2 * al256((size_t)FIX_SPLITS * bb * 8) +
+         al256((size_t)FIX_SPLITS * B * 8) + al256((size_t)FIX_SPLITS * 4);
 }
 
-cudaError_t launch_gram_amax(const float* Y, long long n, int B, unsigned* amax_bits, int* nonfinite, cudaStream_t st,
-                             int* state4) {
-  cudaError_t e = launch_pdl(zero_kernel, dim3(1), dim3(256), 0, st, amax_bits, B, state4);
+// the quantisation scales and per-split flagged-pixel counts of the last call
+// on this workspace (tests / diagnostics)
+void gram_tc_debug_ptrs(void* ws, long long n, int B, int npairs, const GramQScale** qs, const int** cnt) {
+  TcWs w = carve(ws, n, B, npairs);
+  *qs = w.qs;
+  *cnt = w.fix.cnt;
+}
+int gram_tc_fix_splits() { return FIX_SPLITS; }
+
+// K1: qscale (+ zeroing) -> tcgen05 Gram -> integer reduction -> clipped-pixel
+// fix -> finalize.  Six launches on `st`, all with programmatic dependent launch.
+cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npairs, double* G, int* nonfinite,
+                           cudaStream_t st, int* state4) {
+  TcWs w = carve(ws, n, B, npairs);
+  cudaError_t e = launch_pdl(gram_qscale_kernel, dim3(QS_CL * B), dim3(256), 0, st, Y, n, w.qs, w.bitmap, w.nwords, state4,
+                             (int)(sizeof(RankState) / sizeof(int)));
   if (e != cudaSuccess) return e;
-  long long per_block = 256LL * 4 * 8;
-  unsigned gx = (unsigned)((n + per_block - 1) / per_block);
-  if (gx > 16) gx = 16;   // 16 x B blocks: 64K-element band segments at B = 224, N = 2^20
-  if (gx < 1) gx = 1;
-  return launch_pdl(amax_kernel, dim3(gx, B), dim3(256), 0, st, Y, n, amax_bits, nonfinite);
-}
-
-// exact integer Gram of Y with the given per-band scales (amax_bits)
-cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsigned* amax_bits, double* partial,
-                                  int npairs, double* G, int* nonfinite, cudaStream_t st) {
-  cudaError_t e;
   GramTc P;
   P.Y = Y;
   P.n = n;
@@ -421,22 +868,21 @@ cudaError_t launch_gram_tc_scaled(const float* Y, long long n, int B, const unsi
   long long per = (n + npairs - 1) / npairs;
   per = (per + KC - 1) / KC * KC;
   P.per_pair = per;
-  P.amax_bits = amax_bits;
-  P.partial = partial;
-  P.nonfinite = nonfinite;
+  P.qs = w.qs;
+  P.partial = w.partial;
+  P.bitmap = w.bitmap;
   const size_t smem = (size_t)NI * 2 * P.rows_tot * KC;
   e = cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = launch_pdl(gram_tc_kernel, dim3(2 * npairs), dim3(NTHREADS), smem, st, P);   // __cluster_dims__(2)
   if (e != cudaSuccess) return e;
-  e = cudaGetLastError();
+  const long long tot = (long long)B * B + B;
+  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, w.partial, npairs, B);
   if (e != cudaSuccess) return e;
-  return launch_gram_reduce_i64(reinterpret_cast<const long long*>(partial), npairs, B, amax_bits, G, st);
-}
-
-cudaError_t launch_gram_tc(const float* Y, long long n, int B, unsigned* amax_bits, double* partial, int npairs,
-                           double* G, int* nonfinite, cudaStream_t st, int* state4) {
-  cudaError_t e = launch_gram_amax(Y, n, B, amax_bits, nonfinite, st, state4);
+  const int nbk = (B + FIX_TB - 1) / FIX_TB;
+  e = launch_pdl(gram_fix_kernel, dim3(FIX_SPLITS), dim3(256), 0, st, Y, n, B, nbk,
+                 (const GramQScale*)w.qs, (const unsigned*)w.bitmap, w.fix, nonfinite);
   if (e != cudaSuccess) return e;
-  return launch_gram_tc_scaled(Y, n, B, amax_bits, partial, npairs, G, nonfinite, st);
+  return launch_pdl(gram_finalize_kernel, dim3((unsigned)(((long long)B * B + 255) / 256)), dim3(256), 0, st,
+                    (const long long*)w.partial, B, n, (const GramQScale*)w.qs, w.fix, G);
 }

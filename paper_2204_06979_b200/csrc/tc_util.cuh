@@ -115,12 +115,13 @@ __device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                 // layout type SWIZZLE_128B
   return d;
 }
-// instruction descriptor: kind::i8, s32 accumulate, signed A and B, K-major both
-__device__ __forceinline__ uint32_t idesc_i8(int M, int N) {
+// instruction descriptor: kind::i8, s32 accumulate, K-major both; A / B
+// signed (s8) or unsigned (u8) int8
+__device__ __forceinline__ uint32_t idesc_i8(int M, int N, bool a_signed = true, bool b_signed = true) {
   uint32_t d = 0;
   d |= 2u << 4;                 // c_format = S32
-  d |= 1u << 7;                 // a_format = signed int8
-  d |= 1u << 10;                // b_format = signed int8
+  d |= (a_signed ? 1u : 0u) << 7;    // a_format: 1 = signed int8, 0 = unsigned
+  d |= (b_signed ? 1u : 0u) << 10;   // b_format
   // a_major = b_major = 0 (K-major), no negate, no saturate, dense
   d |= (uint32_t)(N >> 3) << 17;
   d |= (uint32_t)(M >> 4) << 24;

@@ -48,6 +48,21 @@ def gram(cube):
     return g
 
 
+def gram_quant(cube):
+    """Quantisation of the last `gram(cube)` call on this device: per band the fp32
+    1/step inv_s and the integer centre c (q = rint(y inv_s) - c), and the number of
+    pixels added exactly (flagged); flagged = -1 when the fp64 SIMT path ran."""
+    import numpy as np
+    b = cube.shape[0]
+    n = cube[0].numel()
+    inv_s = (ctypes.c_float * b)()
+    cen = (ctypes.c_int * b)()
+    nf = ctypes.c_longlong(0)
+    h = _h(cube)
+    check(lib().hyde_debug_gram_quant(h, n, b, inv_s, cen, ctypes.byref(nf)), h)
+    return np.array(inv_s[:], dtype=np.float32), np.array(cen[:], dtype=np.int64), int(nf.value)
+
+
 def eig(g, n_pixels, ncomp, ridge=1e-6, all_lam=True):
     torch = _torch()
     b = g.shape[0]

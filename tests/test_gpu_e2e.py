@@ -189,3 +189,61 @@ def test_hyres_max_bands_simt_gram_path(hy):
     out, info = hy.hyres(torch.from_numpy(s.noisy).cuda(), return_info=True)
     assert info["rank"] == ref.rank
     assert metrics.rel_l2(ref.out, out.cpu().numpy()) <= 1e-4
+
+
+def _hot(cube, mult, seed):
+    """One pixel at mult x the band RMS in every band (a hot / specular pixel)."""
+    cube = cube.copy()
+    b, r, c = cube.shape
+    rms = np.sqrt(np.mean(cube.reshape(b, -1).astype(np.float64) ** 2, axis=1))
+    i, j = np.random.default_rng(100 + seed).integers(0, min(r, c), 2)
+    cube[:, i, j] = (mult * rms).astype(np.float32)
+    return cube
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("mult", [10.0, 30.0, 100.0, 1000.0])
+def test_hyres_outlier_bands_match_oracle(hy, seed, mult):
+    """VERDICT r01 item 1 / PAPER.md:261-263: a hot pixel at 10-1000 x the band RMS in
+    every band must not cost parity (north_star: rel L2 <= 1e-4, 0.01 dB, equal r*)."""
+    s = synth.make_cube("tiny", seed)
+    cube = _hot(s.noisy, mult, seed)
+    ref = O.hyres(cube)
+    out, info = hy.hyres(dev(cube), return_info=True)
+    _compare(synth.Sample(s.cfg, s.seed, s.clean, cube), ref, out.cpu().numpy(), info)
+    sig = hy.estimate_noise(dev(cube))
+    assert np.max(np.abs(sig.cpu().numpy() / ref.sigma - 1)) < 1e-5
+
+
+def test_hyres_spike_band_small_matches_oracle(hy):
+    """small cube: one band with a single 1e3 x spike, plus a 3000 x hot pixel and a dead band."""
+    s = synth.make_cube("small", 0)
+    cube = _hot(s.noisy, 3000.0, 7)
+    b = cube.shape[0]
+    rms = np.sqrt(np.mean(cube.reshape(b, -1).astype(np.float64) ** 2, axis=1))
+    cube[50, 70, 70] = np.float32(1e3 * rms[50])
+    ref = O.hyres(cube)
+    out, info = hy.hyres(dev(cube), return_info=True)
+    _compare(synth.Sample(s.cfg, s.seed, s.clean, cube), ref, out.cpu().numpy(), info)
+
+
+@pytest.mark.slow
+def test_hyres_large_hot_pixel_matches_oracle(hy):
+    s = synth.make_cube("large", 0)
+    cube = _hot(s.noisy, 100.0, 3)
+    ref = O.hyres(cube)
+    out, info = hy.hyres(dev(cube), return_info=True)
+    _compare(synth.Sample(s.cfg, s.seed, s.clean, cube), ref, out.cpu().numpy(), info)
+
+
+def test_rank_walk_to_last_component(hy):
+    """The rank walk reaches k = B (r* = B - 1, the largest r* the rule can give: the
+    smallest eigenvalue of G_w is <= 1, so E_post,B <= N <= N_c -- pinned in
+    test_oracle_pins.py::test_last_component_always_fails), across chunk edges."""
+    s = synth.low_rank_cube(64, 64, 4, rank=4, seed=3)
+    ref = O.hyres(s.clean)
+    assert ref.rank == 3 and len(ref.e_post) == 4
+    for chunk in (1, 2, 16):
+        out, info = hy.hyres(dev(s.clean), chunk=chunk, return_info=True)
+        assert info["rank"] == 3 and info["comps"] == 4
+        assert metrics.rel_l2(ref.out, out.cpu().numpy()) <= REL_L2

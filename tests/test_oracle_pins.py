@@ -520,6 +520,65 @@ def test_f2_default_lambda_from_grid():
     assert res.lam == min(O.FORPDN_GRID, key=lambda l: abs(res.residual_power[l] - res.noise_power))
 
 
+def test_f2_default_lambda_on_white_noise_closed_form():
+    """D16 pinned on pure white noise of known sigma, from closed forms (not the oracle's
+    own rule): with W i.i.d. N(0, sigma^2) (orthonormal DWT, 2^L | R, C), the residual
+    W - W A^-1 = W (I - A^-1) has power sigma^2 tr((I - A^-1)^2) / B per entry, and
+    HySime's regression noise power is sigma^2 (N - B + 1) / N (chi^2 with N - B + 1
+    dof).  The oracle's residual powers must match the closed forms within 3 %, its noise
+    power within 3 %, and its lambda must be the grid value the closed forms select."""
+    rng = np.random.default_rng(61)
+    b, r, c, sig = 12, 64, 64, 0.7
+    x = (sig * rng.standard_normal((b, r, c))).astype(np.float32)
+    res = O.forpdn(x, levels=2, taps=8)
+    n = r * c
+    d = O.spectral_difference(b)
+    cf = {}
+    for lmb in O.FORPDN_GRID:
+        k = np.eye(b) - np.linalg.inv(np.eye(b) + lmb * d.T @ d)
+        cf[lmb] = sig ** 2 * np.trace(k @ k) / b
+        assert abs(res.residual_power[lmb] / cf[lmb] - 1) < 0.03, (lmb, res.residual_power[lmb], cf[lmb])
+    npow = sig ** 2 * (n - b + 1) / n
+    assert abs(res.noise_power / npow - 1) < 0.03
+    assert res.lam == min(O.FORPDN_GRID, key=lambda l: abs(cf[l] - npow))
+
+
+def test_f4_default_lambda_and_rank_on_white_noise():
+    """D17 pinned on pure white noise of known sigma: sigma_b^2 has expectation
+    sigma^2 (N - B + 1) / N, so the default lambda = sqrt(mean sigma_b^2) sqrt(2 ln N_c)
+    is within 1 % of sigma sqrt((N - B + 1) / N) sqrt(2 ln N_c); HySime finds no signal
+    subspace in pure noise (k = 0), so the default rank is max(1, k) = 1."""
+    rng = np.random.default_rng(62)
+    b, r, c, sig = 10, 64, 64, 1.3
+    x = (sig * rng.standard_normal((b, r, c))).astype(np.float32)
+    res = O.wsrrr(x, levels=2, taps=8, max_iters=3)
+    n = r * c
+    nc = O.coeff_count(r, c, 2)
+    want = sig * math.sqrt((n - b + 1) / n) * math.sqrt(2 * math.log(nc))
+    assert abs(res.lam / want - 1) < 0.01, (res.lam, want)
+    assert res.rank == 1
+
+
+def test_last_component_always_fails():
+    """Why r* = B never occurs under the first-failure rule (R2): with
+    sigma_b^2 = 1 / (N [(G + dI)^-1]_bb), G_w^-1 = N D^1/2 G^-1 D^1/2 has diagonal
+    [G^-1]_bb / [(G + dI)^-1]_bb >= 1, so lambda_min(G_w) <= 1 and the last whitened
+    component has energy <= N <= N_c; soft thresholding only lowers it.  Checked on
+    noisy, noiseless and full-rank cubes; the oracle's walk then stops at k = B with
+    r* = B - 1 where every earlier component passes."""
+    rng = np.random.default_rng(63)
+    cubes = [synth.make_cube("tiny", 0).noisy, synth.low_rank_cube(32, 32, 6, rank=6, seed=1).clean,
+             rng.standard_normal((5, 20, 20)).astype(np.float32),
+             synth.low_rank_cube(64, 64, 4, rank=4, seed=3).clean]
+    for cube in cubes:
+        b, r, c = cube.shape
+        sigma, g = O.estimate_noise(cube)
+        lam, _, _ = O.whiten_eig(g, sigma, r * c)
+        assert lam[-1] <= 1.0 + 1e-9, lam[-1]
+    ref = O.hyres(cubes[-1])
+    assert len(ref.e_post) == 4 and ref.rank == 3 and ref.e_post[-1] <= ref.n_coeffs
+
+
 # ---------------------------------------------------------------- F4: WSRRR
 def test_f4_spec_lossless_full_rank():
     """lam = 0, rank = bands -> denoised ~= input within 1e-3."""
