@@ -6,9 +6,13 @@ python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--c
 A step is one full HyRes pass (north_star stages (1)-(6)) over one synthetic
 cube resident in HBM.  Default workload: `large` (1024 x 1024 x 224 fp32, the
 north_star target; the cube is 940 MB, larger than the 126 MB L2, so no L2
-flush is needed between steps).  For N > 1 (torchrun, one rank per GPU) every
-rank denoises its own cube (seed = rank): independent problems, weak scaling,
-no data-path collective.
+flush is needed between steps).  For N > 1 (torchrun, one rank per GPU) the
+default is the pixel-sharded single cube (hyde_hyres_sharded: rank g holds pixel
+rows [gR/N, (g+1)R/N), NCCL inside libhyde: Gram all-reduce, slab <-> component
+all-to-all for the wavelet stage; strong scaling); independent
+replica cubes (seed = rank, weak scaling) are reported beside it under
+"replicas" (--replicas makes them the headline).  --config batched shards the
+64 independent cubes round-robin (no data-path collective).
 
 Reports one JSON line (rank 0): value = whole-job voxels/s; e2e = the same
 metric through the C-ABI with HOST buffers (H2D + D2H inside the timed
@@ -39,12 +43,35 @@ METRIC = "HyRes voxels/sec and ms/cube"
 UNIT = "voxels/s"
 
 
+NOMINAL_HBM_GBS = 8000.0   # BASELINE.json north_star "~8 TB/s" (B200_PROFILING.md: 7.7 HGX / 8 DGX)
+PEAKS_FILE = os.path.join(ROOT, "profiles", "r02_peaks.json")      # tools/probe_peaks.cu on a B200 of this pool
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_traffic.json")  # ncu --set full dram bytes per launch
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
         return float(d.get("hbm_gbs", 6650.0)), float(d.get("bf16_tflops", 1590.0)), "measured"
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def probe_peaks():
+    """fp64 / int8-tensor peaks measured by tools/probe_peaks.cu (committed JSON), or {}."""
+    try:
+        return json.load(open(PEAKS_FILE))
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu capture, or None."""
+    try:
+        d = json.load(open(TRAFFIC_FILE))
+        v = d["kernels"].get(kernel)
+        return None if v is None else {"bytes": v, "source": d.get("source")}
+    except Exception:  # noqa: BLE001
+        return None
 
 
 # ------------------------------------------------------------------ clocks (NVML)
@@ -212,7 +239,9 @@ def wavelet_isolated(hy, torch, cube, cfg, levels, steps, hbm):
     # the method's minimum: DWT one read of N + one write of N_c
     # per image (a fused multi-level transform), SURE one read of N_c
     mb = b * (4 * n + 4 * nc + 4 * nc)
-    res["dwt+sure_min_bytes"] = {"bytes": mb, "frac_hbm": round(mb / (ds_t * 1e-3) / 1e9 / hbm, 4)}
+    res["dwt+sure_min_bytes"] = {"bytes": mb, "frac_hbm": round(mb / (ds_t * 1e-3) / 1e9 / hbm, 4),
+                                 "frac_nominal_8tbs": round(mb / (ds_t * 1e-3) / 1e9 / NOMINAL_HBM_GBS, 4)}
+    res["dwt+sure"]["frac_nominal_8tbs"] = round(ds_b / (ds_t * 1e-3) / 1e9 / NOMINAL_HBM_GBS, 4)
     del E, out
     torch.cuda.empty_cache()
     return res
@@ -314,7 +343,10 @@ def main():
     ap.add_argument("--iso-steps", type=int, default=5,
                     help="steps of the stage-isolated DWT/SURE/IDWT leg on all B eigen-images (0: skip)")
     ap.add_argument("--shard", action="store_true",
-                    help="one cube split into pixel-row slabs across the ranks (hyde_hyres_sharded; strong scaling)")
+                    help="one cube split into pixel-row slabs across the ranks (hyde_hyres_sharded; strong "
+                         "scaling) -- the default for N > 1; at N = 1 it runs the path on a world-1 NCCL comm")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent cubes per rank (seed = rank, weak scaling) as the headline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = synth.CONFIGS[args.config]
@@ -334,20 +366,17 @@ def main():
     # workload, its round-robin shard of the fixed batch of independent cubes
     # (strong scaling).  No data-path collective either way.
     batched = cfg.batch > 1
-    sharded = args.shard and not batched
+    sharded = (args.shard or (world > 1 and not args.replicas)) and not batched
     seeds = hd.shard(cfg.batch, rank, world) if batched else ([0] if sharded else [rank])
     cubes_h = [np.ascontiguousarray(synth.make_cube(cfg, seed=sd).noisy) for sd in seeds]
     ncube = len(cubes_h)
     if sharded:
-        # this rank's pixel-row slab of cube 0; Gram all-reduce + eigen-image
-        # all-gather through NCCL (torch.distributed) on the library's stream
+        # this rank's pixel-row slab of cube 0; the Gram all-reduce and the
+        # slab <-> component all-to-all run through NCCL inside libhyde
         r0, r1 = hy.slab_rows(cfg.rows, rank, world)
-        cubes_h = [np.ascontiguousarray(cubes_h[0][:, r0:r1, :])]
-        if world > 1:
-            comm = hy.torch_dist_comm()
-        else:
-            comm = hy.make_comm(0, 1, lambda t, st: None, lambda t, st: None,
-                                lambda snd, rcv, st: rcv.copy_(snd))
+        full_h = cubes_h[0]
+        cubes_h = [np.ascontiguousarray(full_h[:, r0:r1, :])]
+        comm = hy.NcclComm() if world > 1 else hy.nccl_comm_single()
         cube = torch.from_numpy(cubes_h[0]).cuda()
         out = torch.empty_like(cube)
         run = lambda: hy.hyres_sharded(cube, cfg.rows, comm, out, return_info=True)   # noqa: E731
@@ -411,6 +440,27 @@ def main():
     ms_max = hd.max_over_ranks(ms, device="cuda")
     cubes_total = 1.0 if sharded else hd.sum_over_ranks(ncube, device="cuda")
     value = hd.whole_job_rate(cubes_total * cfg.voxels, ms_max * 1e-3)
+
+    reps = None
+    if sharded and world > 1:
+        # independent replica cubes (seed = rank): weak scaling, no collective
+        rcube = torch.from_numpy(np.ascontiguousarray(synth.make_cube(cfg, seed=rank).noisy)).cuda()
+        rout = torch.empty_like(rcube)
+        for _ in range(args.warmup):
+            hy.hyres(rcube, rout)
+        torch.cuda.synchronize()
+        dist.barrier()
+        r0e, r1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0e.record(st)
+        for _ in range(args.steps):
+            hy.hyres(rcube, rout)
+        r1e.record(st)
+        torch.cuda.synchronize()
+        rms = hd.max_over_ranks(r0e.elapsed_time(r1e) / args.steps, device="cuda")
+        reps = {"value": hd.whole_job_rate(world * cfg.voxels, rms * 1e-3), "unit": UNIT, "ms_per_step": rms,
+                "scaling": "weak", "path": "hyde_hyres_ex, one whole cube per rank (seed = rank), no collective"}
+        del rcube, rout
+        torch.cuda.empty_cache()
 
     hys = None
     if args.iso_steps > 0 and not batched and not sharded and rank == 0:
@@ -567,24 +617,45 @@ def main():
     tds = (stages["dwt"][0] + stages["sure"][0]) / args.steps
     per["dwt+sure"] = {"ms": round(tds, 5), "bytes": dws,
                        "GBps": round(dws / (tds * 1e-3) / 1e9, 1) if tds > 0 else None,
-                       "frac_hbm": round(dws / (tds * 1e-3) / 1e9 / hbm, 4) if tds > 0 else None}
+                       "frac_hbm": round(dws / (tds * 1e-3) / 1e9 / hbm, 4) if tds > 0 else None,
+                       "frac_nominal_8tbs": round(dws / (tds * 1e-3) / 1e9 / NOMINAL_HBM_GBS, 4) if tds > 0 else None}
+    # SURVEY §8(d) minimum for the in-step DWT+SURE: one read of N and one write of
+    # N_c per transformed component (a fused multi-level DWT), one SURE read of N_c
+    ncf = coeff_count(cfg.rows, cfg.cols, info["levels"])
+    dmin = ncube * comps * 4 * (cfg.rows * cfg.cols + 2 * ncf)
+    if tds > 0:
+        per["dwt+sure"]["min_bytes"] = dmin
+        per["dwt+sure"]["frac_hbm_min_bytes"] = round(dmin / (tds * 1e-3) / 1e9 / hbm, 4)
     dom = max((k for k in stages), key=lambda k: stages[k][0])
     t = stages[dom][0] / args.steps
+    kern = {"eig": "k2_cluster_kernel", "gram": "gram_tc_kernel", "project": "project_kernel", "recon": "recon_kernel",
+            "sure": "sure_kernel", "dwt": "dwt_fwd_kernel", "idwt": "dwt_inv_kernel"}.get(dom, dom)
+    tr = ncu_traffic(kern)
     if dom in sb:
         ach = sb[dom] / (t * 1e-3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
-                "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
-                "peak_source": src, "share_of_step": round(t / ms_max, 4)}
+        roof = {"kernel": kern, "stage": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": tr["bytes"] if tr else None,
+                "algorithmic_bytes": sb[dom], "peak_source": src, "share_of_step": round(t / ms_max, 4),
+                "frac_nominal_8tbs": round(ach / NOMINAL_HBM_GBS, 4)}
     else:   # K2: one 16-CTA cluster, fp64, a B-step dependency chain
         ncta = hy.eig_cluster_size() or 16
         flops = ncube * k2_flops(cfg.bands)
-        peak = ncta * 64 * 2 * 1.965e9 / 1e12          # DFMA/clk/SM x 2 flops x max SM clock
+        pk = probe_peaks()
+        if pk.get("fp64_tflops_per_sm"):
+            peak = ncta * float(pk["fp64_tflops_per_sm"])
+            psrc = (f"measured: {ncta} SMs (one cluster) x {pk['fp64_tflops_per_sm']} fp64 TFLOP/s per SM "
+                    f"(tools/probe_peaks.cu, profiles/r02_peaks.json; whole GPU {pk.get('fp64_tflops')} TFLOP/s)")
+        else:
+            peak = ncta * 64 * 2 * 1.965e9 / 1e12      # DFMA/clk/SM x 2 flops x max SM clock
+            psrc = f"derived: {ncta} SMs (one cluster) x 64 DFMA/clk x 2 x 1965 MHz"
         ach = flops / (t * 1e-3) / 1e12
-        roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4),
-                "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": None,
-                "peak_source": f"derived: {ncta} SMs (one cluster) x 64 DFMA/clk x 2 x 1965 MHz; "
-                               "latency-bound (B sequential Householder steps)",
+        roof = {"kernel": kern, "stage": dom, "bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4),
+                "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": tr["bytes"] if tr else None,
+                "algorithmic_flops": flops,
+                "peak_source": psrc + "; latency-bound (B sequential Householder steps)",
                 "share_of_step": round(t / ms_max, 4)}
+    if tr:
+        roof["traffic_source"] = tr["source"]
 
     if rank != 0:
         if world > 1:
@@ -620,6 +691,8 @@ def main():
     }
     if iso is not None:
         line["wavelet_isolated"] = iso
+    if reps is not None:
+        line["replicas"] = reps
     if strm is not None:
         line["cube_stream"] = strm
     if hys is not None:

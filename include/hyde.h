@@ -129,38 +129,72 @@ hyde_status hyde_hyres_host_stream(hyde_handle h, const float* const* cubes_host
                                    hyde_hyres_info* info, hyde_stream_t stream);
 /* --- E1: pixel-sharded single cube (BASELINE.json
  * north_star: "the pixel-sharded Gram matrix is all-reduced (B x B); eigen-
- * images ... are distributed for the wavelet stage").  Rank g of G holds pixel
- * rows [g*rows/G, (g+1)*rows/G) of every band (a BSQ slab, floor division).
- * The library calls back for the three collectives; each callback receives
- * DEVICE pointers whose contents were produced by work enqueued on `stream`,
- * must run the collective after that work and make its result visible to work
- * enqueued on `stream` afterwards (NCCL on `stream` does both), and returns 0
- * on success.
- *   allreduce_max_u32: element-wise max over ranks (per-band max |y| bit
- *                      patterns: one global quantisation scale per band);
- *   allreduce_sum_f64: element-wise sum (the B x B partial Grams);
- *   allgather:         recv[g * bytes + i] = send_i of rank g (the ranks'
- *                      eigen-image slabs, padded to ceil(rows/G) rows). */
+ * images or row tiles are distributed for the wavelet stage").  Rank g of G
+ * holds pixel rows [g*rows/G, (g+1)*rows/G) of every band (a BSQ slab, floor
+ * division: hyde_shard_rows).  Per call:
+ *   A1  the slab's Gram (K1), ncclAllReduce(sum, fp64, B x B), then a
+ *       finiteness check of the summed G (every rank sees the same G, so a
+ *       non-finite value on any slab stops every rank at the same point);
+ *   A2  replicated (identical input, code and GPU type: identical V);
+ *   per chunk of candidate components (first max(4, G), doubling):
+ *   A3  projection of the local slab; all-to-all (grouped ncclSend/ncclRecv)
+ *       slab -> component: rank g owns component k iff k % G == g
+ *       (hyde_shard_owner) and receives every rank's rows of it into a whole
+ *       eigen-image (the periodised DWT couples the first and last rows);
+ *   A4/A5 DWT + SURE of the owned images only; the per-subband statistics are
+ *       all-reduced so every rank makes the same first-failure rank decision;
+ *   A6  IDWT of the owned kept images, all-to-all component -> slab rows,
+ *       reconstruction of the local rows.
+ * Self transfers are device copies.  The result equals hyde_hyres_ex on the
+ * whole cube up to the summation order of the Gram partials (each rank's G is
+ * the exact Gram of its own 16-bit quantisation, K1).  The exchange buffers
+ * live in the handle.  Errors: HYDE_EPARAM (shape, split, NULL), HYDE_ENCCL
+ * (no libnccl.so.2, a failed NCCL call or callback), and those of
+ * hyde_hyres_ex; non-finite input returns HYDE_EDATA on every rank.
+ *
+ * NCCL is resolved at run time (the libnccl.so.2 already loaded by the caller,
+ * e.g. PyTorch's, is reused).  comm: a communicator from hyde_nccl_comm_init
+ * (or any ncclComm_t of the same NCCL); all collectives are enqueued on
+ * `stream`. */
+#ifndef NCCL_H_
+typedef struct ncclComm* ncclComm_t;
+#endif
+int hyde_nccl_version(void);   /* NCCL_VERSION_CODE of the run-time library, 0 if none */
+/* id_out: 128 bytes (ncclUniqueId) to broadcast to every rank (HOST). */
+hyde_status hyde_nccl_unique_id(void* id_out);
+hyde_status hyde_nccl_comm_init(ncclComm_t* comm, int world, int rank, const void* id, int device);
+hyde_status hyde_nccl_comm_destroy(ncclComm_t comm);
+hyde_status hyde_hyres_sharded(hyde_handle h, ncclComm_t comm, const float* local, int local_rows, int row0,
+                               int rows, int cols, int bands, float* local_out, const hyde_hyres_params* params,
+                               hyde_hyres_info* info, hyde_stream_t stream);
+/* Slab of `rank` (host, no GPU): rows [*row0, *row0 + *nrows); rank == world
+ * gives *row0 = rows.  Returns 0, or -1 for bad arguments. */
+int hyde_shard_rows(int rows, int world, int rank, int* row0, int* nrows);
+/* Owner rank of candidate component `component` (0-based) in the wavelet stage. */
+int hyde_shard_owner(int component, int world);
+
+/* The same path with caller-supplied collectives (tests: ranks emulated as
+ * host threads on one GPU).  Callbacks get DEVICE pointers produced by work
+ * enqueued on `stream`; they must run after that work, make their results
+ * visible to later work on `stream`, and return 0 on success.
+ *   allreduce_sum_f64: element-wise sum over ranks, in place;
+ *   sendrecv: one group of point-to-point transfers to / from OTHER ranks;
+ *             between two ranks the i-th send matches the i-th receive. */
+typedef struct {
+  int peer;
+  void* buf;
+  size_t bytes;
+} hyde_p2p;
 typedef struct {
   int rank, world;
   void* user;
-  int (*allreduce_max_u32)(void* user, unsigned* buf, size_t count, hyde_stream_t stream);
   int (*allreduce_sum_f64)(void* user, double* buf, size_t count, hyde_stream_t stream);
-  int (*allgather)(void* user, const void* send, void* recv, size_t bytes_per_rank, hyde_stream_t stream);
+  int (*sendrecv)(void* user, int nsend, const hyde_p2p* sends, int nrecv, const hyde_p2p* recvs,
+                  hyde_stream_t stream);
 } hyde_comm;
-
-/* Denoise the rank's slab local[bands][local_rows][cols] of a rows x cols x
- * bands cube into local_out (same layout).  Requires row0 == rank*rows/world
- * and local_rows == (rank+1)*rows/world - row0.  The Gram, the noise estimate
- * and the eigendecomposition are global (identical on every rank); the DWT /
- * SURE / rank stages run on the gathered eigen-images (replicated); the
- * reconstruction writes only the local rows.  The result equals
- * hyde_hyres_ex on the whole cube up to the summation order of the Gram
- * partials.  Errors: HYDE_EPARAM (shape, split or NULL callbacks), HYDE_ENCCL
- * (a callback failed), and those of hyde_hyres_ex. */
-hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows, int row0, int rows, int cols,
-                               int bands, float* local_out, const hyde_hyres_params* params,
-                               hyde_hyres_info* info, const hyde_comm* comm, hyde_stream_t stream);
+hyde_status hyde_hyres_sharded_cb(hyde_handle h, const hyde_comm* comm, const float* local, int local_rows,
+                                  int row0, int rows, int cols, int bands, float* local_out,
+                                  const hyde_hyres_params* params, hyde_hyres_info* info, hyde_stream_t stream);
 
 /* --- F1: HySime signal-subspace identification
  * ("HySime ... implemented in HyDe") on the

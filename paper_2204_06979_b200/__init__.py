@@ -13,8 +13,8 @@ from typing import Dict, Optional, Tuple
 from . import _lib
 from ._lib import HydeError, Info, Params, check, lib, make_params
 
-__all__ = ["hyres", "hyres_batched", "hyres_host", "hyres_host_stream", "hyres_sharded", "torch_dist_comm",
-           "make_comm", "estimate_noise", "workspace_size",
+__all__ = ["hyres", "hyres_batched", "hyres_host", "hyres_host_stream", "hyres_sharded", "NcclComm",
+           "nccl_comm_single", "make_comm", "slab_rows", "component_owner", "estimate_noise", "workspace_size",
            "HydeError", "stages", "version"]
 
 _handles: Dict[int, int] = {}
@@ -156,21 +156,24 @@ def dev_view(ptr, count, typestr):
 
 
 def slab_rows(rows, rank, world):
-    """Pixel rows [r0, r1) of rank `rank` in the sharded path (include/hyde.h hyde_hyres_sharded)."""
-    return rank * rows // world, (rank + 1) * rows // world
+    """Pixel rows [r0, r1) of rank `rank` in the sharded path (hyde_shard_rows)."""
+    r0, nr = ctypes.c_int(0), ctypes.c_int(0)
+    if lib().hyde_shard_rows(int(rows), int(world), int(rank), ctypes.byref(r0), ctypes.byref(nr)) != 0:
+        raise HydeError(2, "bad rank / world")
+    return r0.value, r0.value + nr.value
 
 
-def make_comm(rank, world, allreduce_max_u32, allreduce_sum_f64, allgather):
-    """Wrap three Python collectives (each taking torch views of the device
-    buffers and the raw stream handle) into a hyde_comm; keep the returned
-    object alive for the duration of the call."""
-    def amax(user, buf, count, stream):
-        try:
-            allreduce_max_u32(dev_view(buf, count, "<i4"), stream)   # bit patterns of |y| >= 0: int32 max == uint32 max
-            return 0
-        except Exception:  # noqa: BLE001
-            return 1
+def component_owner(k, world):
+    """Rank that owns candidate component k (0-based) in the sharded wavelet stage (hyde_shard_owner)."""
+    return int(lib().hyde_shard_owner(int(k), int(world)))
 
+
+def make_comm(rank, world, allreduce_sum_f64, sendrecv):
+    """Wrap two Python collectives into a hyde_comm (hyde_hyres_sharded_cb):
+    allreduce_sum_f64(t, stream) sums a float64 device view in place over the
+    ranks; sendrecv(sends, recvs, stream) gets lists of (peer, uint8 device view)
+    -- between two ranks the i-th send matches the i-th receive.  Keep the
+    returned object alive for the duration of the call."""
     def asum(user, buf, count, stream):
         try:
             allreduce_sum_f64(dev_view(buf, count, "<f8"), stream)
@@ -178,48 +181,81 @@ def make_comm(rank, world, allreduce_max_u32, allreduce_sum_f64, allgather):
         except Exception:  # noqa: BLE001
             return 1
 
-    def agather(user, send, recv, nbytes, stream):
+    def sr(user, ns, sends, nr, recvs, stream):
         try:
-            allgather(dev_view(send, nbytes, "|u1"), dev_view(recv, nbytes * world, "|u1"), stream)
+            s = [(sends[i].peer, dev_view(sends[i].buf, sends[i].bytes, "|u1")) for i in range(ns)]
+            r = [(recvs[i].peer, dev_view(recvs[i].buf, recvs[i].bytes, "|u1")) for i in range(nr)]
+            sendrecv(s, r, stream)
             return 0
         except Exception:  # noqa: BLE001
             return 1
 
-    fns = (_lib.ALLREDUCE_FN(amax), _lib.ALLREDUCE_FN(asum), _lib.ALLGATHER_FN(agather))
+    fns = (_lib.ALLREDUCE_FN(asum), _lib.SENDRECV_FN(sr))
     c = _lib.Comm(rank, world, None, *fns)
     c._keep = fns
     return c
 
 
-def torch_dist_comm(group=None):
-    """hyde_comm backed by torch.distributed (NCCL over NVLink on B200 boxes);
-    the collectives run ordered on the library's stream."""
-    import torch.distributed as dist
+class NcclComm:
+    """A libhyde NCCL communicator over the ranks of a torch.distributed group:
+    rank 0 draws the ncclUniqueId (hyde_nccl_unique_id), the group broadcasts
+    it, every rank calls hyde_nccl_comm_init on its current CUDA device.  The
+    collectives of hyde_hyres_sharded then run inside libhyde on the call's
+    stream (NCCL over NVLink / NVSwitch on a B200 box)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        torch = _torch()
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        uid = (ctypes.c_ubyte * 128)()
+        if self.rank == 0:
+            check(lib().hyde_nccl_unique_id(uid))
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda(self.device)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        raw = bytes(t.cpu().tolist())
+        self._uid = (ctypes.c_ubyte * 128).from_buffer_copy(raw)
+        c = ctypes.c_void_p()
+        check(lib().hyde_nccl_comm_init(ctypes.byref(c), self.world, self.rank, self._uid, self.device))
+        self.comm = c.value
+
+    def close(self):
+        if self.comm:
+            lib().hyde_nccl_comm_destroy(self.comm)
+            self.comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def nccl_comm_single(device=None) -> "NcclComm":
+    """World-size-1 NCCL communicator (no process group needed): exercises every
+    collective call site of the sharded path on one GPU."""
     torch = _torch()
-
-    def on(stream):
-        return torch.cuda.stream(torch.cuda.ExternalStream(stream))
-
-    def amax(t, stream):
-        with on(stream):
-            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-
-    def asum(t, stream):
-        with on(stream):
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-
-    def agather(send, recv, stream):
-        with on(stream):
-            dist.all_gather_into_tensor(recv, send, group=group)
-
-    return make_comm(dist.get_rank(group), dist.get_world_size(group), amax, asum, agather)
+    obj = NcclComm.__new__(NcclComm)
+    obj.rank, obj.world = 0, 1
+    obj.device = torch.cuda.current_device() if device is None else int(device)
+    uid = (ctypes.c_ubyte * 128)()
+    check(lib().hyde_nccl_unique_id(uid))
+    obj._uid = uid
+    c = ctypes.c_void_p()
+    check(lib().hyde_nccl_comm_init(ctypes.byref(c), 1, 0, uid, obj.device))
+    obj.comm = c.value
+    return obj
 
 
 def hyres_sharded(local, rows, comm, out=None, *, handle_id=None, taps=16, levels=0, chunk=16, ridge=1e-6,
                   keep_ll=False, return_info=False):
     """Pixel-sharded HyRes of one cube (include/hyde.h hyde_hyres_sharded):
     `local` is this rank's BSQ slab (bands, r1 - r0, cols) with
-    (r0, r1) = slab_rows(rows, rank, world); returns the denoised slab."""
+    (r0, r1) = slab_rows(rows, rank, world); `comm` is an NcclComm (NCCL inside
+    libhyde) or a make_comm(...) callback table; returns the denoised slab."""
     torch = _torch()
     _cube(local, "local")
     b, lr, c = local.shape
@@ -229,8 +265,12 @@ def hyres_sharded(local, rows, comm, out=None, *, handle_id=None, taps=16, level
     p = make_params(taps, levels, chunk, ridge, keep_ll)
     info = Info()
     h = handle_id if handle_id is not None else handle(local.device.index)
-    check(lib().hyde_hyres_sharded(h, local.data_ptr(), lr, r0, rows, c, b, out.data_ptr(), ctypes.byref(p),
-                                   ctypes.byref(info), ctypes.byref(comm), _stream(local)), h)
+    if isinstance(comm, NcclComm):
+        check(lib().hyde_hyres_sharded(h, comm.comm, local.data_ptr(), lr, r0, rows, c, b, out.data_ptr(),
+                                       ctypes.byref(p), ctypes.byref(info), _stream(local)), h)
+    else:
+        check(lib().hyde_hyres_sharded_cb(h, ctypes.byref(comm), local.data_ptr(), lr, r0, rows, c, b,
+                                          out.data_ptr(), ctypes.byref(p), ctypes.byref(info), _stream(local)), h)
     return (out, info.as_dict()) if return_info else out
 
 

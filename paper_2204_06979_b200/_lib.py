@@ -44,13 +44,20 @@ _P = c_void_p  # device or host pointer
 
 # hyde_comm callbacks (include/hyde.h): device pointers, the caller's stream
 ALLREDUCE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_void_p, c_size_t, c_void_p)
-ALLGATHER_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p)
+
+
+class P2p(ctypes.Structure):
+    _fields_ = [("peer", c_int), ("buf", c_void_p), ("bytes", c_size_t)]
+
+
+SENDRECV_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_int, POINTER(P2p), c_int, POINTER(P2p), c_void_p)
 
 
 class Comm(ctypes.Structure):
     _fields_ = [("rank", c_int), ("world", c_int), ("user", c_void_p),
-                ("allreduce_max_u32", ALLREDUCE_FN), ("allreduce_sum_f64", ALLREDUCE_FN),
-                ("allgather", ALLGATHER_FN)]
+                ("allreduce_sum_f64", ALLREDUCE_FN), ("sendrecv", SENDRECV_FN)]
+
+
 _SIGS = {
     "hyde_create": (c_int, [POINTER(c_void_p), c_int]),
     "hyde_destroy": (c_int, [c_void_p]),
@@ -65,8 +72,16 @@ _SIGS = {
     "hyde_hyres_host": (c_int, [c_void_p, _P, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_hyres_host_stream": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p), c_int, c_int, c_int, c_int,
                                        POINTER(Params), POINTER(Info), c_void_p]),
-    "hyde_hyres_sharded": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, POINTER(Params),
-                                   POINTER(Info), POINTER(Comm), c_void_p]),
+    "hyde_hyres_sharded": (c_int, [c_void_p, c_void_p, _P, c_int, c_int, c_int, c_int, c_int, _P, POINTER(Params),
+                                   POINTER(Info), c_void_p]),
+    "hyde_hyres_sharded_cb": (c_int, [c_void_p, POINTER(Comm), _P, c_int, c_int, c_int, c_int, c_int, _P,
+                                      POINTER(Params), POINTER(Info), c_void_p]),
+    "hyde_nccl_version": (c_int, []),
+    "hyde_nccl_unique_id": (c_int, [c_void_p]),
+    "hyde_nccl_comm_init": (c_int, [POINTER(c_void_p), c_int, c_int, c_void_p, c_int]),
+    "hyde_nccl_comm_destroy": (c_int, [c_void_p]),
+    "hyde_shard_rows": (c_int, [c_int, c_int, c_int, POINTER(c_int), POINTER(c_int)]),
+    "hyde_shard_owner": (c_int, [c_int, c_int]),
     "hyde_hyres_workspace_size": (c_size_t, [c_int, c_int, c_int, c_int, POINTER(Params)]),
     "hyde_hyres_batched": (c_int, [c_void_p, _P, c_int, c_int, c_int, c_int, _P, POINTER(Params), POINTER(Info), c_void_p]),
     "hyde_sync_status": (c_int, [c_void_p, c_void_p]),

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "nccl_shim.h"
 
 namespace {
 thread_local std::string g_err;
@@ -119,6 +120,8 @@ struct hyde_ctx {
   std::vector<cudaEvent_t> lane_ev;
   cudaEvent_t ev_batch = nullptr;
   RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
+  char* shard_buf = nullptr;     // E1 exchange buffers (grow only)
+  size_t shard_cap = 0;
   cudaEvent_t ev_rank = nullptr; // recorded after the per-chunk D2H copy of the rank state
   int gram_min_px = 0;           // K1 pixels per SM pair, at least (0: latency mode; lanes: throughput)
   // stage profiling
@@ -356,6 +359,7 @@ hyde_status hyde_destroy(hyde_handle h) {
     cudaDeviceSynchronize();
     if (h->ws) cudaFree(h->ws);
     if (h->ebuf) cudaFree(h->ebuf);
+    if (h->shard_buf) cudaFree(h->shard_buf);
     if (h->dev_in) cudaFree(h->dev_in);
     if (h->dev_out) cudaFree(h->dev_out);
     for (auto b : h->pipe_buf)
@@ -537,17 +541,108 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   return HYDE_OK;
 }
 
-hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows, int row0, int rows, int cols,
-                               int bands, float* local_out, const hyde_hyres_params* params,
-                               hyde_hyres_info* info, const hyde_comm* comm, hyde_stream_t stream) {
+}  // extern "C"
+
+// ------------------------------------------------------------------ E1
+// Pixel-sharded single cube (BASELINE.json north_star: "the
+// pixel-sharded Gram matrix is all-reduced (B x B); eigen-images or row tiles
+// are distributed for the wavelet stage").  The collectives go through
+// CommOps: NCCL (hyde_hyres_sharded) or caller callbacks
+// (hyde_hyres_sharded_cb, used to emulate ranks on one GPU in the tests).
+namespace {
+struct P2p {
+  int peer;
+  void* buf;
+  size_t bytes;
+};
+struct CommOps {
+  int rank = 0, world = 1;
+  virtual ~CommOps() {}
+  virtual hyde_status allreduce_sum_f64(hyde_handle h, double* buf, size_t n, cudaStream_t st) = 0;
+  // remote pairs only; between two ranks the i-th send matches the i-th recv
+  virtual hyde_status sendrecv(hyde_handle h, const std::vector<P2p>& sends, const std::vector<P2p>& recvs,
+                               cudaStream_t st) = 0;
+};
+
+struct NcclOps : CommOps {
+  const NcclApi* api = nullptr;
+  ncclComm_t comm = nullptr;
+  hyde_status chk(hyde_handle h, ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return HYDE_OK;
+    return fail(h, HYDE_ENCCL, std::string(what) + ": " + api->GetErrorString(r));
+  }
+  hyde_status allreduce_sum_f64(hyde_handle h, double* buf, size_t n, cudaStream_t st) override {
+    return chk(h, api->AllReduce(buf, buf, n, ncclFloat64, ncclSum, comm, st), "ncclAllReduce");
+  }
+  hyde_status sendrecv(hyde_handle h, const std::vector<P2p>& sends, const std::vector<P2p>& recvs,
+                       cudaStream_t st) override {
+    if (sends.empty() && recvs.empty()) return HYDE_OK;
+    hyde_status s = chk(h, api->GroupStart(), "ncclGroupStart");
+    if (s != HYDE_OK) return s;
+    for (const P2p& x : sends)
+      if ((s = chk(h, api->Send(x.buf, x.bytes, ncclUint8, x.peer, comm, st), "ncclSend")) != HYDE_OK) break;
+    if (s == HYDE_OK)
+      for (const P2p& x : recvs)
+        if ((s = chk(h, api->Recv(x.buf, x.bytes, ncclUint8, x.peer, comm, st), "ncclRecv")) != HYDE_OK) break;
+    const hyde_status e = chk(h, api->GroupEnd(), "ncclGroupEnd");
+    return s != HYDE_OK ? s : e;
+  }
+};
+
+struct CbOps : CommOps {
+  const hyde_comm* cb = nullptr;
+  hyde_status allreduce_sum_f64(hyde_handle h, double* buf, size_t n, cudaStream_t st) override {
+    return cb->allreduce_sum_f64(cb->user, buf, n, (hyde_stream_t)st) == 0
+               ? HYDE_OK
+               : fail(h, HYDE_ENCCL, "allreduce callback failed");
+  }
+  hyde_status sendrecv(hyde_handle h, const std::vector<P2p>& sends, const std::vector<P2p>& recvs,
+                       cudaStream_t st) override {
+    std::vector<hyde_p2p> a(sends.size()), b(recvs.size());
+    for (size_t i = 0; i < sends.size(); ++i) a[i] = {sends[i].peer, sends[i].buf, sends[i].bytes};
+    for (size_t i = 0; i < recvs.size(); ++i) b[i] = {recvs[i].peer, recvs[i].buf, recvs[i].bytes};
+    return cb->sendrecv(cb->user, (int)a.size(), a.data(), (int)b.size(), b.data(), (hyde_stream_t)st) == 0
+               ? HYDE_OK
+               : fail(h, HYDE_ENCCL, "sendrecv callback failed");
+  }
+};
+
+// one all-to-all step: self pairs become device copies (matched in order),
+// the rest goes to the communicator as one group
+hyde_status exchange(hyde_handle h, CommOps& cm, const std::vector<P2p>& sends, const std::vector<P2p>& recvs,
+                     cudaStream_t st) {
+  std::vector<P2p> rs, rr, ss, sr;
+  for (const P2p& x : sends) (x.peer == cm.rank ? ss : rs).push_back(x);
+  for (const P2p& x : recvs) (x.peer == cm.rank ? sr : rr).push_back(x);
+  if (ss.size() != sr.size()) return fail(h, HYDE_EPARAM, "internal: unmatched self transfers");
+  for (size_t i = 0; i < ss.size(); ++i) {
+    if (ss[i].bytes != sr[i].bytes) return fail(h, HYDE_EPARAM, "internal: self transfer size");
+    CK(cudaMemcpyAsync(sr[i].buf, ss[i].buf, ss[i].bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return cm.sendrecv(h, rs, rr, st);
+}
+
+hyde_status ensure_shard_buf(hyde_handle h, size_t bytes, cudaStream_t st) {
+  if (bytes <= h->shard_cap) return HYDE_OK;
+  if (h->shard_buf) CK(cudaFreeAsync(h->shard_buf, st));
+  h->shard_buf = nullptr;
+  h->shard_cap = 0;
+  CK(cudaMallocAsync((void**)&h->shard_buf, bytes, st));
+  h->shard_cap = bytes;
+  return HYDE_OK;
+}
+
+hyde_status sharded_impl(hyde_handle h, CommOps& cm, const float* local, int local_rows, int row0, int rows, int cols,
+                         int bands, float* local_out, const hyde_hyres_params* params, hyde_hyres_info* info,
+                         cudaStream_t st) {
   hyde_status s = validate_shape(h, rows, cols, bands);
   if (s != HYDE_OK) return s;
-  if (!local || !local_out || !comm || !comm->allreduce_max_u32 || !comm->allreduce_sum_f64 || !comm->allgather)
-    return fail(h, HYDE_EPARAM, "NULL slab / output / collective callbacks");
-  const int G = comm->world, gr = comm->rank;
+  if (!local || !local_out) return fail(h, HYDE_EPARAM, "NULL slab / output");
+  const int G = cm.world, gr = cm.rank;
   if (G < 1 || gr < 0 || gr >= G || rows < G) return fail(h, HYDE_EPARAM, "bad rank / world");
-  auto rbeg = [&](int g) { return (int)((long long)g * rows / G); };
-  if (row0 != rbeg(gr) || local_rows != rbeg(gr + 1) - row0)
+  int r0c = 0, nrc = 0;
+  hyde_shard_rows(rows, G, gr, &r0c, &nrc);
+  if (row0 != r0c || local_rows != nrc)
     return fail(h, HYDE_EPARAM, "slab must be rows [rank*rows/world, (rank+1)*rows/world)");
   hyde_hyres_params p;
   int levels = 0;
@@ -556,20 +651,40 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
   FilterBank fb;
   if (hyde_build_filters(p.wavelet_taps, &fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "filter derivation failed");
   DeviceGuard dg(h->device);
-  cudaStream_t st = (cudaStream_t)stream;
   const int B = bands;
-  Layout L;                        // full-image geometry (DWT plan, eigen-images)
-  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L);
+  auto rbeg = [&](int g) {
+    int a = 0, c = 0;
+    hyde_shard_rows(rows, G, g, &a, &c);
+    return a;
+  };
+  // chunk schedule: first max(4, G) components (every rank owns one), doubling
+  const int first_len = std::min(p.chunk, std::max(kFirstChunk, G));
+  auto chunk_len = [&](int c) {
+    long long want = (long long)first_len << (c < 20 ? c : 20);
+    if (want > p.chunk) want = p.chunk;
+    return (int)want;
+  };
+  const int mycap = (p.chunk + G - 1) / G;   // components one rank owns in a chunk, at most
+  Layout L;                                  // full-image geometry: this rank's DWT / SURE / IDWT
+  make_layout(rows, cols, B, mycap, levels, p.wavelet_taps, &L);
   const long long n_loc = (long long)local_rows * cols;
-  Layout Ll;                       // slab geometry (Gram partials, projection)
-  make_layout(local_rows, cols, B, p.chunk, levels < 1 ? 1 : 1, 2, &Ll);
+  Layout Ll;                                 // slab geometry: the local Gram
+  make_layout(local_rows, cols, B, 1, 1, 2, &Ll);
   s = ensure_ws(h, L.total + Ll.total, st);
   if (s != HYDE_OK) return s;
   char* ws = h->ws;
-  char* wl = h->ws + L.total;      // slab-sized pieces (Gram partials, amax)
+  char* wl = h->ws + L.total;
   const long long n = L.n;
-  s = ensure_ebuf(h, (size_t)p.chunk * L.ldE * 4, 0, st);
+  // persistent exchange buffers (handle-owned, grow only): the projected slab
+  // of every chunk component, this rank's whole eigen-images, the chunk's
+  // per-subband SURE statistics (+ one overflow slot)
+  const size_t b_slab = al((size_t)p.chunk * n_loc * 4), b_full = al((size_t)mycap * L.ldE * 4),
+               b_esub = al(((size_t)p.chunk * L.nsub + 1) * 8);
+  s = ensure_shard_buf(h, b_slab + b_full + b_esub, st);
   if (s != HYDE_OK) return s;
+  float* slab_e = (float*)h->shard_buf;
+  float* full_e = (float*)(h->shard_buf + b_slab);
+  double* esub_all = (double*)(h->shard_buf + b_slab + b_full);
   RankState* rs = (RankState*)(ws + L.rs);
   h->last_rs = rs;
   CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
@@ -580,89 +695,72 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
   float* W = (float*)(ws + L.W);
   float* U = (float*)(ws + L.U);
   float* C = (float*)(ws + L.C);
-  auto coll = [&](int rc) -> hyde_status {
-    return rc == 0 ? HYDE_OK : fail(h, HYDE_ENCCL, "collective callback failed");
-  };
-  // ---- A1: local Gram (own quantisation scales), all-reduced in fp64 ----
+  // ---- A1: local Gram of the slab, all-reduced; a global finiteness check ----
   {
-    Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? 5 : 2, st);
-    if (Ll.use_tc) {
+    Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? 6 : 3, st);
+    if (Ll.use_tc)
       CK(launch_gram_tc(local, n_loc, B, wl + Ll.partial, Ll.npairs, Gm, &rs->nonfinite, st));
-    } else {
+    else
       CK(launch_gram(local, n_loc, B, (double*)(wl + Ll.partial), Ll.nsplit, Gm, &rs->nonfinite, st));
-    }
-    s = coll(comm->allreduce_sum_f64(comm->user, Gm, (size_t)B * B, stream));
+    s = cm.allreduce_sum_f64(h, Gm, (size_t)B * B, st);
     if (s != HYDE_OK) return s;
+    CK(launch_check_finite(Gm, (long long)B * B, &rs->nonfinite, st));
     sg.end();
   }
-  auto chunk_len = [&](int c) {
-    long long want = (long long)kFirstChunk << (c < 20 ? c : 20);
-    if (want > p.chunk) want = p.chunk;
-    return (int)want;
-  };
+  // ---- A2 (replicated: identical G, code and GPU type give identical V) ----
   const int first = chunk_len(0) < B ? chunk_len(0) : B;
   {
     Stage sg(h, HYDE_STAGE_EIG, 1, st);
     CK(launch_noise_eig(Gm, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
     sg.end();
   }
-  // all-gather buffers: every rank's slab of every chunk component, padded to ceil(rows/G) rows
-  const long long lr_max = (rows + G - 1) / G;
-  const size_t slab_f = (size_t)lr_max * cols;
-  float* sendb = nullptr;
-  float* recvb = nullptr;
-  CK(cudaMallocAsync((void**)&sendb, (size_t)p.chunk * slab_f * 4, st));
-  CK(cudaMallocAsync((void**)&recvb, (size_t)G * p.chunk * slab_f * 4, st));
-  struct Free {
-    float *a, *b;
-    cudaStream_t st;
-    ~Free() {
-      cudaFreeAsync(a, st);
-      cudaFreeAsync(b, st);
-    }
-  } fr{sendb, recvb, st};
-  int rank = 0, chunks = 0;
-  int k0 = 0, comps = 0;
+  int rank = 0, chunks = 0, k0 = 0, comps = 0;
   for (int c = 0;; ++c) {
     const int cl = chunk_len(c);
     const int cnt = (B - k0) < cl ? (B - k0) : cl;
     if (c > 0) {
-      s = ensure_ebuf(h, (size_t)(k0 + cnt) * L.ldE * 4, (size_t)k0 * L.ldE * 4, st);
-      if (s != HYDE_OK) return s;
       Stage sg(h, HYDE_STAGE_EIG, 1, st);
       CK(launch_eigvec_more(tri, house, sigma, B, k0, cnt, nullptr, nullptr, W, U, L.ldwu, st));
       sg.end();
     }
-    float* E = h->ebuf + (size_t)k0 * L.ldE;
+    std::vector<int> mine;   // chunk positions of the components this rank owns (global k % G == rank)
+    for (int k = 0; k < cnt; ++k)
+      if (hyde_shard_owner(k0 + k, G) == gr) mine.push_back(k);
+    const int my = (int)mine.size();
     {
-      // A3 on the local slab, then slab -> whole eigen-images on every rank
-      Stage sg(h, HYDE_STAGE_PROJECT, 1 + G * cnt, st);
-      CK(launch_project(local, n_loc, B, W + k0, L.ldwu, cnt, sendb, (long long)slab_f, st));
-      s = coll(comm->allgather(comm->user, sendb, recvb, (size_t)cnt * slab_f * 4, stream));
+      // A3 on the local slab, then slab -> whole eigen-images of the owned components
+      Stage sg(h, HYDE_STAGE_PROJECT, 1, st);
+      CK(launch_project(local, n_loc, B, W + k0, L.ldwu, cnt, slab_e, n_loc, st));
+      std::vector<P2p> snd, rcv;
+      for (int k = 0; k < cnt; ++k)
+        snd.push_back({hyde_shard_owner(k0 + k, G), slab_e + (size_t)k * n_loc, (size_t)n_loc * 4});
+      for (int j = 0; j < my; ++j)
+        for (int g = 0; g < G; ++g)
+          rcv.push_back({g, full_e + (size_t)j * L.ldE + (size_t)rbeg(g) * cols,
+                         (size_t)(rbeg(g + 1) - rbeg(g)) * cols * 4});
+      s = exchange(h, cm, snd, rcv, st);
       if (s != HYDE_OK) return s;
-      for (int g = 0; g < G; ++g) {
-        const long long rb = rbeg(g), lr = rbeg(g + 1) - rb;
-        for (int k = 0; k < cnt; ++k)
-          CK(cudaMemcpyAsync(E + (size_t)k * L.ldE + rb * cols, recvb + ((size_t)g * cnt + k) * slab_f,
-                             (size_t)lr * cols * 4, cudaMemcpyDeviceToDevice, st));
-      }
       sg.end();
     }
-    {
+    if (my > 0) {
       Stage sg(h, HYDE_STAGE_DWT, levels, st);
-      CK(dwt_forward(L, ws, E, L.ldE, cnt, fb, st));
+      CK(dwt_forward(L, ws, full_e, L.ldE, my, fb, st));
       sg.end();
-    }
-    {
-      Stage sg(h, HYDE_STAGE_SURE, 1, st);
-      CK(launch_sure(C, L.plan.n_coeffs, L.plan, cnt, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
+      Stage sg2(h, HYDE_STAGE_SURE, 1, st);
+      CK(launch_sure(C, L.plan.n_coeffs, L.plan, my, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
                      (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, (unsigned*)(ws + L.surv), st));
-      sg.end();
+      sg2.end();
     }
     {
-      Stage sg(h, HYDE_STAGE_RANK, 1, st);
-      CK(launch_rank_decide((double*)(ws + L.esub), L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs,
-                            (double*)(ws + L.epost), st));
+      // every rank gets every component's subband statistics (its own rows,
+      // zeros elsewhere, summed) and makes the same first-failure decision
+      Stage sg(h, HYDE_STAGE_RANK, 3, st);
+      CK(launch_scatter_rows((const double*)(ws + L.esub), my, L.nsub, mine.data(), esub_all, cnt,
+                             &rs->sure_overflow, st));
+      s = cm.allreduce_sum_f64(h, esub_all, (size_t)cnt * L.nsub + 1, st);
+      if (s != HYDE_OK) return s;
+      CK(launch_flag_from_sum(esub_all + (size_t)cnt * L.nsub, &rs->sure_overflow, st));
+      CK(launch_rank_decide(esub_all, L.nsub, cnt, k0, (double)L.plan.n_coeffs, B, rs, (double*)(ws + L.epost), st));
       CK(cudaMemcpyAsync(h->rs_host, rs, sizeof(RankState), cudaMemcpyDeviceToHost, st));
       sg.end();
     }
@@ -673,9 +771,27 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
     if (r.nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
     if (r.sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
     const int kept = r.found ? (r.rank - k0) : cnt;
-    if (kept > 0) {
+    int my_kept = 0;
+    while (my_kept < my && mine[my_kept] < kept) ++my_kept;
+    if (my_kept > 0) {
       Stage sg(h, HYDE_STAGE_IDWT, levels, st);
-      CK(dwt_inverse(L, ws, C, E, L.ldE, kept, fb, (const float*)(ws + L.tstar), st));
+      CK(dwt_inverse(L, ws, C, full_e, L.ldE, my_kept, fb, (const float*)(ws + L.tstar), st));
+      sg.end();
+    }
+    s = ensure_ebuf(h, (size_t)(k0 + cnt) * n_loc * 4, (size_t)k0 * n_loc * 4, st);
+    if (s != HYDE_OK) return s;
+    if (kept > 0) {
+      // whole denoised images -> the rows of every rank's slab
+      Stage sg(h, HYDE_STAGE_IDWT, 0, st);
+      std::vector<P2p> snd, rcv;
+      for (int j = 0; j < my_kept; ++j)
+        for (int g = 0; g < G; ++g)
+          snd.push_back({g, full_e + (size_t)j * L.ldE + (size_t)rbeg(g) * cols,
+                         (size_t)(rbeg(g + 1) - rbeg(g)) * cols * 4});
+      for (int k = 0; k < kept; ++k)
+        rcv.push_back({hyde_shard_owner(k0 + k, G), h->ebuf + (size_t)(k0 + k) * n_loc, (size_t)n_loc * 4});
+      s = exchange(h, cm, snd, rcv, st);
+      if (s != HYDE_OK) return s;
       sg.end();
     }
     if (r.found) {
@@ -687,7 +803,7 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
   {
     // A6 on the local rows only
     Stage sg(h, HYDE_STAGE_RECON, (rank + 7) / 8, st);
-    CK(launch_reconstruct(h->ebuf + (size_t)row0 * cols, L.ldE, n_loc, B, U, L.ldwu, rank, local_out, st));
+    CK(launch_reconstruct(h->ebuf, n_loc, n_loc, B, U, L.ldwu, rank, local_out, st));
     sg.end();
   }
   if (info) {
@@ -699,6 +815,97 @@ hyde_status hyde_hyres_sharded(hyde_handle h, const float* local, int local_rows
     info->comps = comps;
   }
   return HYDE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int hyde_shard_rows(int rows, int world, int rank, int* row0, int* nrows) {
+  if (world < 1 || rank < 0 || rank > world || rows < 0) return -1;
+  const long long a = (long long)rank * rows / world;
+  const long long b = rank < world ? (long long)(rank + 1) * rows / world : rows;
+  if (row0) *row0 = (int)a;
+  if (nrows) *nrows = (int)(b - a);
+  return 0;
+}
+
+int hyde_shard_owner(int component, int world) { return world < 1 || component < 0 ? -1 : component % world; }
+
+int hyde_nccl_version(void) {
+  const NcclApi* a = nccl_api();
+  int v = 0;
+  if (!a || a->GetVersion(&v) != ncclSuccess) return 0;
+  return v;
+}
+
+hyde_status hyde_nccl_unique_id(void* id_out) {
+  const NcclApi* a = nccl_api();
+  if (!id_out) return HYDE_EPARAM;
+  if (!a) {
+    g_err = "libnccl.so.2 not found";
+    return HYDE_ENCCL;
+  }
+  ncclUniqueId id;
+  const ncclResult_t r = a->GetUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_err = std::string("ncclGetUniqueId: ") + a->GetErrorString(r);
+    return HYDE_ENCCL;
+  }
+  memcpy(id_out, &id, sizeof(id));
+  return HYDE_OK;
+}
+
+hyde_status hyde_nccl_comm_init(ncclComm_t* comm, int world, int rank, const void* id, int device) {
+  const NcclApi* a = nccl_api();
+  if (!comm || !id || world < 1 || rank < 0 || rank >= world) return HYDE_EPARAM;
+  if (!a) {
+    g_err = "libnccl.so.2 not found";
+    return HYDE_ENCCL;
+  }
+  DeviceGuard g(device);
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  const ncclResult_t r = a->CommInitRank(comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    g_err = std::string("ncclCommInitRank: ") + a->GetErrorString(r);
+    return HYDE_ENCCL;
+  }
+  return HYDE_OK;
+}
+
+hyde_status hyde_nccl_comm_destroy(ncclComm_t comm) {
+  const NcclApi* a = nccl_api();
+  if (!comm) return HYDE_OK;
+  if (!a) return HYDE_ENCCL;
+  return a->CommDestroy(comm) == ncclSuccess ? HYDE_OK : HYDE_ENCCL;
+}
+
+hyde_status hyde_hyres_sharded(hyde_handle h, ncclComm_t comm, const float* local, int local_rows, int row0, int rows,
+                               int cols, int bands, float* local_out, const hyde_hyres_params* params,
+                               hyde_hyres_info* info, hyde_stream_t stream) {
+  if (!h) return HYDE_EPARAM;
+  if (!comm) return fail(h, HYDE_EPARAM, "NULL communicator");
+  NcclOps ops;
+  ops.api = nccl_api();
+  if (!ops.api) return fail(h, HYDE_ENCCL, "libnccl.so.2 not found");
+  ops.comm = comm;
+  if (ops.api->CommCount(comm, &ops.world) != ncclSuccess || ops.api->CommUserRank(comm, &ops.rank) != ncclSuccess)
+    return fail(h, HYDE_ENCCL, "bad communicator");
+  return sharded_impl(h, ops, local, local_rows, row0, rows, cols, bands, local_out, params, info,
+                      (cudaStream_t)stream);
+}
+
+hyde_status hyde_hyres_sharded_cb(hyde_handle h, const hyde_comm* comm, const float* local, int local_rows, int row0,
+                                  int rows, int cols, int bands, float* local_out, const hyde_hyres_params* params,
+                                  hyde_hyres_info* info, hyde_stream_t stream) {
+  if (!h) return HYDE_EPARAM;
+  if (!comm || !comm->allreduce_sum_f64 || !comm->sendrecv) return fail(h, HYDE_EPARAM, "NULL collective callbacks");
+  CbOps ops;
+  ops.cb = comm;
+  ops.rank = comm->rank;
+  ops.world = comm->world;
+  return sharded_impl(h, ops, local, local_rows, row0, rows, cols, bands, local_out, params, info,
+                      (cudaStream_t)stream);
 }
 
 hyde_status hyde_profile_enable(hyde_handle h, int on) {

@@ -160,5 +160,10 @@ cudaError_t launch_sure(float* coeffs, long long cstride, const DwtPlan& plan, i
 int sure_prof_read(unsigned long long* out16);   // K5 phase cycles (HYDE_SURE_PROF builds), 0 otherwise
 cudaError_t launch_rank_decide(const double* e_sub, int nsub, int count, int k0, double n_coeffs,
                                int bands, RankState* rs, double* e_post, cudaStream_t st);
+// E1 helpers (k_util.cu)
+cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStream_t st);
+cudaError_t launch_scatter_rows(const double* src, int nrows, int ncols, const int* to, double* dst, int dst_rows,
+                                const int* flag_in, cudaStream_t st);
+cudaError_t launch_flag_from_sum(const double* x, int* flag, cudaStream_t st);
 cudaError_t launch_reconstruct(const float* E, long long ldE, long long n, int B, const float* U,
                                int ldu, int rank, float* out, cudaStream_t st, const RankState* rs = nullptr);

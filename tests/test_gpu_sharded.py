@@ -26,30 +26,23 @@ def hy():
 
 
 class ThreadComm:
-    """In-process collectives among `world` threads on one GPU."""
+    """In-process collectives among `world` threads on one GPU (host-synchronised
+    copies: no kernel ever waits on another rank's kernel)."""
 
     def __init__(self, world):
         self.world = world
         self.bar = threading.Barrier(world)
         self.slot = [None] * world
 
-    def _exchange(self, rank, t, stream):
+    def _publish(self, rank, item, stream):
         torch.cuda.ExternalStream(stream).synchronize()   # the producing kernels are done
-        self.slot[rank] = t
+        self.slot[rank] = item
         self.bar.wait()
         return list(self.slot)
 
     def for_rank(self, hy, rank):
-        def amax(t, stream):
-            parts = self._exchange(rank, t, stream)
-            res = torch.stack([p.clone() for p in parts]).amax(0)
-            self.bar.wait()                                   # everyone has read every buffer
-            t.copy_(res)
-            torch.cuda.synchronize()
-            self.bar.wait()
-
         def asum(t, stream):
-            parts = self._exchange(rank, t, stream)
+            parts = self._publish(rank, t, stream)
             res = torch.zeros_like(t)
             for p in parts:                                   # fixed rank order
                 res += p
@@ -58,15 +51,19 @@ class ThreadComm:
             torch.cuda.synchronize()
             self.bar.wait()
 
-        def agather(send, recv, stream):
-            parts = self._exchange(rank, send, stream)
-            n = send.numel()
-            for g, p in enumerate(parts):
-                recv[g * n:(g + 1) * n].copy_(p)
+        def sendrecv(sends, recvs, stream):
+            parts = self._publish(rank, sends, stream)
+            for peer in range(self.world):
+                mine = [buf for (p, buf) in recvs if p == peer]
+                theirs = [buf for (p, buf) in parts[peer] if p == rank]
+                assert len(mine) == len(theirs), (rank, peer, len(mine), len(theirs))
+                for dst, src in zip(mine, theirs):            # i-th send matches i-th receive
+                    assert dst.numel() == src.numel()
+                    dst.copy_(src)
             torch.cuda.synchronize()
             self.bar.wait()
 
-        return hy.make_comm(rank, self.world, amax, asum, agather)
+        return hy.make_comm(rank, self.world, asum, sendrecv)
 
 
 def run_sharded(hy, cube, world):
@@ -102,7 +99,7 @@ def run_sharded(hy, cube, world):
     return np.concatenate(outs, axis=1), infos
 
 
-@pytest.mark.parametrize("name,world", [("tiny", 2), ("small", 3), ("wide", 2)])
+@pytest.mark.parametrize("name,world", [("tiny", 2), ("small", 3), ("wide", 2), ("small", 5), ("tiny", 8)])
 def test_sharded_equals_whole_cube(hy, name, world):
     s = synth.make_cube(name, 0)
     whole, winfo = hy.hyres(torch.from_numpy(s.noisy).cuda(), return_info=True)
@@ -123,3 +120,42 @@ def test_sharded_rejects_wrong_slab(hy):
     bad = torch.from_numpy(np.ascontiguousarray(s.noisy[:, :10, :])).cuda()   # rank 0 of 2 owns 32 rows
     with pytest.raises(hy.HydeError):
         hy.hyres_sharded(bad, 64, comm)
+
+
+def test_sharded_nccl_world1_equals_whole_cube(hy):
+    """World-size-1 NCCL communicator: every collective call site of hyde_hyres_sharded
+    (Gram all-reduce, slab <-> component exchange as self copies, SURE statistics
+    all-reduce) runs through libhyde's NCCL on one GPU."""
+    assert hy._lib.lib().hyde_nccl_version() >= 22000
+    for name in ("tiny", "small"):
+        s = synth.make_cube(name, 0)
+        x = torch.from_numpy(s.noisy).cuda()
+        whole, winfo = hy.hyres(x, return_info=True)
+        comm = hy.nccl_comm_single()
+        try:
+            got, info = hy.hyres_sharded(x, s.noisy.shape[1], comm, return_info=True)
+            torch.cuda.synchronize()
+        finally:
+            comm.close()
+        assert info["rank"] == winfo["rank"]
+        assert metrics.rel_l2(whole.cpu().numpy(), got.cpu().numpy()) < 1e-6
+
+
+def test_sharded_nonfinite_on_one_rank_stops_every_rank(hy):
+    """a NaN in ONE rank's slab must return HYDE_EDATA on every rank
+    (no rank left waiting in a collective)."""
+    s = synth.make_cube("tiny", 0)
+    cube = s.noisy.copy()
+    cube[3, 50, 7] = np.nan                      # rows 32..63: rank 1 of 2
+    with pytest.raises(hy.HydeError) as ei:
+        run_sharded(hy, cube, 2)
+    assert ei.value.status == 3
+
+
+def test_shard_plan_covers_rows_and_components(hy):
+    for rows, world in [(64, 2), (349, 8), (7, 7), (1024, 3)]:
+        spans = [hy.slab_rows(rows, g, world) for g in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == rows
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+        own = [hy.component_owner(k, world) for k in range(40)]
+        assert own == [k % world for k in range(40)]
