@@ -495,7 +495,7 @@ def main():
         lvl = hy.stages.auto_levels(cfg.rows, cfg.cols)
         ncf = coeff_count(cfg.rows, cfg.cols, lvl)
         fb = (2 * cfg.bands * dwt_image_bytes(cfg.rows, cfg.cols, lvl)   # per-band DWT + IDWT levels
-              + 2 * 4 * cfg.bands * cfg.rows * cfg.cols                   # Gram: amax + quantised read
+              + 4 * cfg.bands * cfg.rows * cfg.cols                       # Gram: one read (K1)
               + 8 * cfg.bands * ncf)                                       # solve: read W, write X
         fpd = {"ms": round(fms, 4), "lambda": flam, "bytes": fb, "GBps": round(fb / (fms * 1e-3) / 1e9, 1),
                "frac_hbm": round(fb / (fms * 1e-3) / 1e9 / hbm_, 4),

@@ -124,6 +124,7 @@ struct hyde_ctx {
   size_t shard_cap = 0;
   cudaEvent_t ev_rank = nullptr; // recorded after the per-chunk D2H copy of the rank state
   int gram_min_px = 0;           // K1 pixels per SM pair, at least (0: latency mode; lanes: throughput)
+  int eig_cl = 0;                // K2 cluster size preference (0: largest; 8: throughput lanes)
   // stage profiling
   int prof = 0;
   struct Rec { int stage; int launches; cudaEvent_t a, b; };
@@ -461,7 +462,8 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   const int first = chunk_len(0) < B ? chunk_len(0) : B;
   {
     Stage sg(h, HYDE_STAGE_EIG, 1, st);
-    CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
+    CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st,
+                        h->eig_cl));
     sg.end();
   }
   int rank = 0, chunks = 0;
@@ -942,7 +944,7 @@ hyde_status hyde_hyres(hyde_handle h, const float* cube, int rows, int cols, int
   return hyde_hyres_ex(h, cube, rows, cols, bands, out, nullptr, nullptr, stream);
 }
 
-constexpr int kLanesDefault = 8;   // concurrent cubes in hyde_hyres_batched
+constexpr int kLanesDefault = 16;  // concurrent cubes in hyde_hyres_batched (8-CTA K2 clusters: 5.9 vs 7.3 ms for 64 x 256x256x191 with 8 lanes of 16-CTA K2)
 constexpr int kLaneGramMinPx = 8192;   // K1 pixels per SM pair in the lanes (64 K1 stages)
 static int lanes_wanted() {
   if (const char* ev = getenv("HYDE_LANES")) {   // experiments
@@ -983,6 +985,8 @@ hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int
     if (s != HYDE_OK) return s;
     l->gram_min_px = kLaneGramMinPx;   // throughput mode: concurrent cubes share the SMs
     if (const char* ev = getenv("HYDE_LANE_GRAM_PX")) l->gram_min_px = atoi(ev);   // experiments
+    l->eig_cl = 8;                     // more concurrent eigensolvers (fewer SMs each)
+    if (const char* ev = getenv("HYDE_LANE_EIG_CL")) l->eig_cl = atoi(ev);        // experiments (16 = latency)
     h->lanes.push_back(l);
     cudaStream_t ls = nullptr;
     CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));

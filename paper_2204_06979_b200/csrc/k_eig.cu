@@ -1250,9 +1250,12 @@ extern "C" int hyde_eig_cluster_size(void) {
 
 size_t eig_workspace_doubles(int B) { return 4 * (size_t)B * B + (size_t)B + 8 + 64; }
 
-static cudaError_t run_k2(const K2Args& a, cudaStream_t st) {
+// cl_pref: 0 = the largest cluster the GPU co-schedules (latency: one cube);
+// 8 = an 8-CTA cluster (throughput: the batched lanes run several cubes'
+// eigensolvers at once, and half the SMs per solver lets twice as many overlap)
+static cudaError_t run_k2(const K2Args& a, cudaStream_t st, int cl_pref = 0) {
   hyde_eig_cluster_size();
-  return g_cluster == 16 ? launch_k2<16>(a, st) : launch_k2<8>(a, st);
+  return (g_cluster == 16 && cl_pref != 8) ? launch_k2<16>(a, st) : launch_k2<8>(a, st);
 }
 
 static cudaError_t run_more(const double* tri, const EigWs& ws, const double* sigma, int B, int k0, int K,
@@ -1269,7 +1272,7 @@ static cudaError_t run_more(const double* tri, const EigWs& ws, const double* si
 // sigma (+ optionally the eigenpairs of the first ncomp components; ncomp < 0 = sigma only)
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house, double* tri, float* W, float* U,
-                             int ldwu, cudaStream_t st) {
+                             int ldwu, cudaStream_t st, int cl_pref) {
   if (B > BM || B < 3) return cudaErrorInvalidValue;
   const EigWs ws = carve(house, B);
   cudaError_t e = cudaMemsetAsync(ws.flags, 0, 8 * sizeof(double), st);
@@ -1292,7 +1295,7 @@ cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, 
   a.W = W;
   a.U = U;
   a.ldwu = ldwu;
-  e = run_k2(a, st);
+  e = run_k2(a, st, cl_pref);
   if (e != cudaSuccess) return e;
   if (all_lam && lam) {
     const size_t smem = sizeof(MoreSmem);
