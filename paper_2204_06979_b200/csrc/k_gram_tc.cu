@@ -44,15 +44,25 @@
 #include "tc_util.cuh"
 
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <type_traits>
 
 namespace {
 
 constexpr int KC = 128;        // pixels (bytes per int8 row) per stage
-constexpr int NI = 4;          // int8 stages
-constexpr int NCW = 14;        // converter warps
-constexpr int NTHREADS = (NCW + 2) * 32;
-constexpr int MAXU = 8;        // max band rows per converter warp per stage: (64 + 48) / 14
+constexpr int NTHREADS = 16 * 32;
+// Two feeds of the converters: registers (each converter warp loads its band
+// rows from HBM, one stage in flight: the fallback for unaligned pixel counts)
+// or TMA (one producer thread streams fp32 tiles of the stage -- two 2-D boxes,
+// the P and QS band ranges -- into a 2-stage smem ring, ~115 KB in flight per
+// SM, and the converters read shared memory).
+template <bool TMA> struct Feed;
+template <> struct Feed<false> { static constexpr int NI = 4, NCW = 14, MAXU = 8, W0 = 2; };
+template <> struct Feed<true>  { static constexpr int NI = 3, NCW = 13, MAXU = 9, W0 = 3; };
+constexpr int NF = 2;                   // fp32 stages (TMA feed)
+constexpr int FROWS = 64 + 48;          // fp32 rows per stage: P (64) + QS (<= 48)
+constexpr int FSTAGE = FROWS * KC * 4;  // 57344 B
 constexpr int TMEM_COLS = 512;
 
 constexpr int GQ_MAX = 32767;  // v in [-32768, 32767]: the range maps to R = 32767 steps
@@ -92,13 +102,25 @@ __device__ __forceinline__ int band_of(int region, int r, int rank, int B, int n
   return b < B ? b : -1;
 }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+template <bool TMA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-    gram_tc_kernel(GramTc P) {
+    gram_tc_kernel(GramTc P, const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ) {
+  enum : int { NI = Feed<TMA>::NI, NCW = Feed<TMA>::NCW, MAXU = Feed<TMA>::MAXU, W0 = Feed<TMA>::W0 };
   pdl_wait();
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NI];
   __shared__ __align__(8) uint64_t bar_empty[NI];
   __shared__ __align__(8) uint64_t bar_done;
+  __shared__ __align__(8) uint64_t f_full[NF];
+  __shared__ __align__(8) uint64_t f_empty[NF];
   __shared__ uint32_t tmem_base_sh;
   __shared__ float inv_s[2][64];
   __shared__ float kf_of[2][64];
@@ -138,6 +160,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       tc::mbar_init(&bar_empty[i], 1);
     }
     tc::mbar_init(&bar_done, 1);
+    for (int i = 0; i < NF; ++i) {
+      tc::mbar_init(&f_full[i], 1);       // the producer's expect_tx arrival
+      tc::mbar_init(&f_empty[i], NCW);    // one arrival per converter warp
+    }
     tc::fence_mbar_init();
   }
   if (warp == 0) {
@@ -205,7 +231,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       }
       tc::mma_commit<2>(&bar_done, 0x3);
     }
-  } else if (warp >= 2) {
+  } else if (TMA && warp == 2) {
+    // ================= TMA producer: fp32 stage tiles -> smem ring ==========
+    if (lane == 0) {
+      unsigned char* fring = smem + NI * stage_bytes;
+      const int hb = nb / 2;
+      const uint32_t bytes = (uint32_t)(64 + (nreg == 2 ? hb : 0)) * KC * 4;
+      for (int s = 0; s < nst; ++s) {
+        const int fs = s % NF;
+        if (s >= NF) tc::mbar_wait(&f_empty[fs], (uint32_t)(((s / NF) - 1) & 1));
+        tc::mbar_expect_tx(&f_full[fs], bytes);
+        unsigned char* dst = fring + fs * FSTAGE;
+        const int x = (int)(p_begin + (long long)s * KC);
+        tma_load_2d(dst, &tmP, x, rank * 64, &f_full[fs]);
+        if (nreg == 2) tma_load_2d(dst + 64 * KC * 4, &tmQ, x, 128 + rank * hb, &f_full[fs]);
+      }
+    }
+  } else if (warp >= W0) {
     // ================= converters: HBM fp32 -> int8 slices in smem ==========
     // (non-finite input fails the range test and is flagged like an outlier;
     // gram_fix_kernel raises the non-finite flag when it reads the pixel)
@@ -213,13 +255,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     // 128 pixels as 32 contiguous 16-byte pieces (512 B per load instruction)
     // and write the 128 int8 bytes of each slice as one swizzled 128-B line
     // (conflict-free).  The per-unit offsets and scale are stage-invariant.
-    const int cw = warp - 2;
+    const int cw = warp - W0;
     const int hb = nb / 2;
     const int nrow_p = max(0, min(64, (B < 128 ? B : 128) - rank * 64));
     const int nrow_q = nreg == 2 ? max(0, min(hb, B - 128 - rank * hb)) : 0;
     const int nunits = nrow_p + nrow_q;
     const bool vec_ok = (P.n % 4 == 0) && (((uintptr_t)P.Y & 15) == 0);
-    int brow[MAXU];   // band of each unit (-1: none)
+    int brow[MAXU];   // band of each unit (-1: none); TMA feed: its row in the fp32 stage
     const float* ybase = P.Y + p_begin + 4 * lane;
     int soff[MAXU];
     float isc[MAXU];
@@ -236,7 +278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const int rg = u < nrow_p ? 0 : 1;
         const int r = rg ? u - nrow_p : u;
         const int b = rg ? 128 + rank * hb + r : rank * 64 + r;
-        brow[t] = b;
+        brow[t] = TMA ? (rg ? 64 + r : r) : b;
         soff[t] = region_base(rg) + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + 4 * (lane & 3);
         isc[t] = inv_s[rg][r];
       }
@@ -245,6 +287,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     float4 va[MAXU], vb[MAXU];
     // issue every load of stage s for this warp (memory-level parallelism)
     auto load_stage = [&](int s, float4 (&v)[MAXU]) {
+      if (TMA) {   // from the fp32 ring; the slot is released as soon as it is read
+        if (s >= nst) return;
+        const int fs = s % NF;
+        tc::mbar_wait(&f_full[fs], (uint32_t)((s / NF) & 1));
+        const float* fr = reinterpret_cast<const float*>(smem + NI * stage_bytes + fs * FSTAGE) + 4 * lane;
+#pragma unroll
+        for (int t = 0; t < MAXU; ++t)
+          v[t] = brow[t] >= 0 ? *reinterpret_cast<const float4*>(fr + brow[t] * KC) : make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&f_empty[fs]);
+        return;
+      }
       const long long sh = (long long)s * KC;
       const bool full = vec_ok && sh + KC <= n_end;
 #pragma unroll
@@ -328,13 +382,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       // single cluster-scope release-arrive for the whole CTA
       asm volatile("bar.arrive %0, %1;" ::"r"(1 + is), "r"((NCW + 1) * 32) : "memory");
     };
-    load_stage(0, va);
-    for (int s = 0; s < nst; s += 2) {
-      load_stage(s + 1, vb);          // next stage's loads fly while this one converts
-      store_stage(s, va);
-      if (s + 1 >= nst) break;
-      load_stage(s + 2, va);
-      store_stage(s + 1, vb);
+    if (TMA) {
+      // smem-fed: read a stage, release its fp32 slot, convert
+      for (int s = 0; s < nst; ++s) {
+        load_stage(s, va);
+        store_stage(s, va);
+      }
+    } else {
+      load_stage(0, va);
+      for (int s = 0; s < nst; s += 2) {
+        load_stage(s + 1, vb);          // next stage's loads fly while this one converts
+        store_stage(s, va);
+        if (s + 1 >= nst) break;
+        load_stage(s + 2, va);
+        store_stage(s + 1, vb);
+      }
     }
     // sum_p q of every unit's band over this pair's pixels (exact int64)
     {
@@ -851,6 +913,36 @@ void gram_tc_debug_ptrs(void* ws, long long n, int B, int npairs, const GramQSca
 }
 int gram_tc_fix_splits() { return FIX_SPLITS; }
 
+// 2-D tensor maps of the cube viewed as B rows of n fp32 pixels: boxes of
+// 128 pixels x 64 bands (P region) and x hb bands (QS region); bands past B
+// and pixels past n are zero-filled by the TMA unit.
+static bool make_maps(const float* Y, long long n, int B, int hb, CUtensorMap* tmP, CUtensorMap* tmQ) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  }
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)B};
+  const cuuint64_t strides[1] = {(cuuint64_t)n * 4};
+  const cuuint32_t estr[2] = {1, 1};
+  auto one = [&](CUtensorMap* tm, int rows) {
+    const cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)rows};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)Y, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!one(tmP, 64)) return false;
+  return one(tmQ, hb >= 8 ? hb : 64);
+}
+
 // K1: qscale (+ zeroing) -> tcgen05 Gram -> integer reduction -> clipped-pixel
 // fix -> finalize.  Six launches on `st`, all with programmatic dependent launch.
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npairs, double* G, int* nonfinite,
@@ -871,10 +963,21 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
   P.qs = w.qs;
   P.partial = w.partial;
   P.bitmap = w.bitmap;
-  const size_t smem = (size_t)NI * 2 * P.rows_tot * KC;
-  e = cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = launch_pdl(gram_tc_kernel, dim3(2 * npairs), dim3(NTHREADS), smem, st, P);   // __cluster_dims__(2)
+  CUtensorMap tmP, tmQ;
+  const bool tma = (n % 4 == 0) && (((uintptr_t)Y & 15) == 0) && !getenv("HYDE_GRAM_NO_TMA") &&
+                   make_maps(Y, n, B, P.nb / 2, &tmP, &tmQ);
+  if (tma) {
+    const size_t smem = (size_t)Feed<true>::NI * 2 * P.rows_tot * KC + (size_t)NF * FSTAGE;
+    e = cudaFuncSetAttribute(gram_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(gram_tc_kernel<true>, dim3(2 * npairs), dim3(NTHREADS), smem, st, P, tmP, tmQ);
+  } else {
+    memset(&tmP, 0, sizeof(tmP));
+    const size_t smem = (size_t)Feed<false>::NI * 2 * P.rows_tot * KC;
+    e = cudaFuncSetAttribute(gram_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(gram_tc_kernel<false>, dim3(2 * npairs), dim3(NTHREADS), smem, st, P, tmP, tmP);
+  }
   if (e != cudaSuccess) return e;
   const long long tot = (long long)B * B + B;
   e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, w.partial, npairs, B);
