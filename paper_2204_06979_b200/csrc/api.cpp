@@ -122,6 +122,13 @@ struct hyde_ctx {
   RankState* last_rs = nullptr;  // device rank/flag state of the last enqueued call
   char* shard_buf = nullptr;     // E1 exchange buffers (grow only)
   size_t shard_cap = 0;
+  // phased batched path: per-cube workspaces, pinned mapped rank states, K2 args
+  char* bws = nullptr;
+  size_t bws_cap = 0;
+  RankState* b_rs_host = nullptr;
+  RankState* b_rs_dev = nullptr;
+  void* b_args_host = nullptr;
+  int b_cap = 0;
   cudaEvent_t ev_rank = nullptr; // recorded after the per-chunk D2H copy of the rank state
   int gram_min_px = 0;           // K1 pixels per SM pair, at least (0: latency mode; lanes: throughput)
   int eig_cl = 0;                // K2 cluster size preference (0: largest; 8: throughput lanes)
@@ -361,6 +368,9 @@ hyde_status hyde_destroy(hyde_handle h) {
     if (h->ws) cudaFree(h->ws);
     if (h->ebuf) cudaFree(h->ebuf);
     if (h->shard_buf) cudaFree(h->shard_buf);
+    if (h->bws) cudaFree(h->bws);
+    if (h->b_rs_host) cudaFreeHost(h->b_rs_host);
+    if (h->b_args_host) cudaFreeHost(h->b_args_host);
     if (h->dev_in) cudaFree(h->dev_in);
     if (h->dev_out) cudaFree(h->dev_out);
     for (auto b : h->pipe_buf)
@@ -954,6 +964,163 @@ static int lanes_wanted() {
   return kLanesDefault;
 }
 
+// Phased batched HyRes (the default of hyde_hyres_batched): the cubes go
+// through the stages TOGETHER -- every Gram (on the lane streams), then ONE
+// launch of the K2 eigensolver for all cubes (cluster b = cube b: the hardware
+// packs the latency-bound solvers back to back on the GPU), then the first
+// chunk of every cube (projection, DWT, SURE with the in-kernel rank decision,
+// gated IDWT and reconstruction) -- with a single host synchronisation for the
+// whole batch.  A cube whose rank rule needs a second chunk (r* >= the first
+// chunk) is redone on its own through hyde_hyres_ex.  Every output equals the
+// single-cube result (the Gram is exact in integers whatever the pixel split,
+// and K2 does not depend on its cluster size).
+static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, int rows, int cols, int bands,
+                                  float* outs, const hyde_hyres_params* params, hyde_hyres_info* info,
+                                  cudaStream_t st) {
+  hyde_hyres_params p;
+  int levels = 0;
+  hyde_status s = resolve_params(h, rows, cols, params, &p, &levels);
+  if (s != HYDE_OK) return s;
+  FilterBank fb;
+  if (hyde_build_filters(p.wavelet_taps, &fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "filter derivation failed");
+  const int B = bands;
+  Layout L;
+  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L, kLaneGramMinPx);
+  const long long n = L.n;
+  const size_t per = (size_t)rows * cols * bands;
+  const int first = std::min(std::min(kFirstChunk, p.chunk), B);
+  const size_t per_ws = al(L.total), per_e = al((size_t)first * L.ldE * 4);
+  const size_t args_b = al((size_t)batch * eig_args_bytes());
+  const size_t need = (size_t)batch * (per_ws + per_e) + args_b;
+  if (need > h->bws_cap) {
+    if (h->bws) CK(cudaFreeAsync(h->bws, st));
+    h->bws = nullptr;
+    h->bws_cap = 0;
+    CK(cudaMallocAsync((void**)&h->bws, need, st));
+    h->bws_cap = need;
+  }
+  if (batch > h->b_cap) {
+    CK(cudaStreamSynchronize(st));
+    if (h->b_rs_host) CK(cudaFreeHost(h->b_rs_host));
+    if (h->b_args_host) CK(cudaFreeHost(h->b_args_host));
+    h->b_rs_host = nullptr;
+    h->b_args_host = nullptr;
+    h->b_cap = 0;
+    CK(cudaHostAlloc((void**)&h->b_rs_host, sizeof(RankState) * batch, cudaHostAllocMapped | cudaHostAllocPortable));
+    CK(cudaHostGetDevicePointer((void**)&h->b_rs_dev, h->b_rs_host, 0));
+    CK(cudaHostAlloc(&h->b_args_host, (size_t)batch * eig_args_bytes(), cudaHostAllocPortable));
+    h->b_cap = batch;
+  }
+  const int NS = std::min(batch, lanes_wanted());
+  while ((int)h->lane_st.size() < NS) {
+    cudaStream_t ls = nullptr;
+    CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
+    h->lane_st.push_back(ls);
+    cudaEvent_t le = nullptr;
+    CK(cudaEventCreateWithFlags(&le, cudaEventDisableTiming));
+    h->lane_ev.push_back(le);
+  }
+  if (!h->ev_batch) CK(cudaEventCreateWithFlags(&h->ev_batch, cudaEventDisableTiming));
+  auto ws_of = [&](int i) { return h->bws + (size_t)i * (per_ws + per_e); };
+  auto e_of = [&](int i) { return (float*)(ws_of(i) + per_ws); };
+  auto join_lanes = [&]() -> hyde_status {   // st waits for every lane stream
+    for (int j = 0; j < NS; ++j) {
+      CK(cudaEventRecord(h->lane_ev[j], h->lane_st[j]));
+      CK(cudaStreamWaitEvent(st, h->lane_ev[j], 0));
+    }
+    return HYDE_OK;
+  };
+  auto fork_lanes = [&]() -> hyde_status {   // every lane stream waits for st
+    CK(cudaEventRecord(h->ev_batch, st));
+    for (int j = 0; j < NS; ++j) CK(cudaStreamWaitEvent(h->lane_st[j], h->ev_batch, 0));
+    return HYDE_OK;
+  };
+  memset(h->b_rs_host, 0, sizeof(RankState) * batch);
+  s = fork_lanes();
+  if (s != HYDE_OK) return s;
+  // ---- A1 for every cube ----
+  {
+    Stage sg(h, HYDE_STAGE_GRAM, batch * (L.use_tc ? 5 : 2), st);
+    for (int i = 0; i < batch; ++i) {
+      cudaStream_t ls = h->lane_st[i % NS];
+      char* ws = ws_of(i);
+      RankState* rs = (RankState*)(ws + L.rs);
+      if (!L.use_tc) CK(cudaMemsetAsync(rs, 0, sizeof(RankState), ls));
+      CK(run_gram(L, ws, cubes + per * i, (double*)(ws + L.G), &rs->nonfinite, ls, L.use_tc ? (int*)rs : nullptr));
+      CK(cudaMemsetAsync(eig_flags_ptr((double*)(ws + L.house), B), 0, 8 * sizeof(double), ls));
+    }
+    s = join_lanes();
+    if (s != HYDE_OK) return s;
+    sg.end();
+  }
+  // ---- A1 tail + A2: every cube's eigensolver in one launch ----
+  {
+    Stage sg(h, HYDE_STAGE_EIG, 1, st);
+    std::vector<const double*> G(batch);
+    std::vector<double*> sig(batch), house(batch), tri(batch);
+    std::vector<float*> W(batch), U(batch);
+    for (int i = 0; i < batch; ++i) {
+      char* ws = ws_of(i);
+      G[i] = (const double*)(ws + L.G);
+      sig[i] = (double*)(ws + L.sigma);
+      house[i] = (double*)(ws + L.house);
+      tri[i] = (double*)(ws + L.tri);
+      W[i] = (float*)(ws + L.W);
+      U[i] = (float*)(ws + L.U);
+    }
+    CK(launch_noise_eig_batched(batch, G.data(), n, B, p.ridge, first, sig.data(), house.data(), tri.data(),
+                                W.data(), U.data(), L.ldwu, h->b_args_host,
+                                h->bws + (size_t)batch * (per_ws + per_e), st, h->eig_cl ? h->eig_cl : 8));
+    sg.end();
+  }
+  s = fork_lanes();
+  if (s != HYDE_OK) return s;
+  // ---- A3..A6, first chunk of every cube (decision and gating on the device) ----
+  {
+    Stage sg(h, HYDE_STAGE_SURE, batch * (3 + 2 * levels), st);
+    for (int i = 0; i < batch; ++i) {
+      cudaStream_t ls = h->lane_st[i % NS];
+      char* ws = ws_of(i);
+      RankState* rs = (RankState*)(ws + L.rs);
+      float* E = e_of(i);
+      float* C = (float*)(ws + L.C);
+      CK(launch_project(cubes + per * i, n, B, (float*)(ws + L.W), L.ldwu, first, E, L.ldE, ls));
+      CK(dwt_forward(L, ws, E, L.ldE, first, fb, ls));
+      CK(launch_sure(C, L.plan.n_coeffs, L.plan, first, p.flags & HYDE_KEEP_LL, (int*)(ws + L.kstar),
+                     (float*)(ws + L.tstar), (double*)(ws + L.esub), rs, (unsigned*)(ws + L.surv), ls, 0,
+                     (double)L.plan.n_coeffs, B, (double*)(ws + L.epost), h->b_rs_dev + i));
+      CK(dwt_inverse(L, ws, C, E, L.ldE, first, fb, (const float*)(ws + L.tstar), ls, rs, 0));
+      CK(launch_reconstruct(E, L.ldE, n, B, (float*)(ws + L.U), L.ldwu, first, outs + per * i, ls, rs));
+    }
+    s = join_lanes();
+    if (s != HYDE_OK) return s;
+    sg.end();
+  }
+  CK(cudaStreamSynchronize(st));
+  hyde_hyres_info* inf = info;
+  for (int i = 0; i < batch; ++i) {
+    const RankState r = h->b_rs_host[i];
+    if (r.nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
+    if (r.sure_overflow) return fail(h, HYDE_EMETHOD, "SURE survivor set exceeded its capacity");
+    if (!r.found) {
+      // r* >= the first chunk: this cube alone through the chunked rank walk
+      s = hyde_hyres_ex(h, cubes + per * i, rows, cols, bands, outs + per * i, params, inf ? inf + i : nullptr,
+                        (hyde_stream_t)st);
+      if (s != HYDE_OK) return s;
+      continue;
+    }
+    if (inf) {
+      memset(inf + i, 0, sizeof(*inf));
+      inf[i].rank = r.rank;
+      inf[i].levels = levels;
+      inf[i].chunks_run = 1;
+      inf[i].n_coeffs = (int)L.plan.n_coeffs;
+      inf[i].comps = first;
+    }
+  }
+  return HYDE_OK;
+}
+
 hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int rows, int cols, int bands,
                                float* outs, const hyde_hyres_params* params, hyde_hyres_info* info,
                                hyde_stream_t stream) {
@@ -970,6 +1137,10 @@ hyde_status hyde_hyres_batched(hyde_handle h, const float* cubes, int batch, int
   }
   hyde_status s = validate_shape(h, rows, cols, bands);
   if (s != HYDE_OK) return s;
+  if (!getenv("HYDE_BATCH_LANES")) {   // HYDE_BATCH_LANES=1: the older per-lane path (experiments)
+    DeviceGuard g(h->device);
+    return batched_phased(h, cubes, batch, rows, cols, bands, outs, params, info, (cudaStream_t)stream);
+  }
   // Independent cubes run on kLanes lanes -- each its own workspace, stream and
   // host thread (hyres_ex synchronises its stream once per rank-loop chunk) --
   // so that, e.g., one cube's K2 cluster (16 SMs) overlaps another cube's

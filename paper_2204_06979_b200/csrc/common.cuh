@@ -101,6 +101,12 @@ size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,
                              double* tri, float* W, float* U, int ldwu, cudaStream_t st, int cl_pref = 0);
+size_t eig_args_bytes();
+double* eig_flags_ptr(double* house, int B);
+cudaError_t launch_noise_eig_batched(int nb, const double* const* G, long long n, int B, double ridge, int ncomp,
+                                     double* const* sigma, double* const* house, double* const* tri,
+                                     float* const* W, float* const* U, int ldwu, void* hargs, void* dargs,
+                                     cudaStream_t st, int cl_pref = 0);
 // F3: HyMiNoR second stage (k_hyminor.cu)
 cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float lam, float mu, int max_iters, float tol,
                           int* iters, cudaStream_t st);

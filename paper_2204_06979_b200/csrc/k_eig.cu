@@ -42,6 +42,7 @@
 // sweep is both more work and a longer dependency chain than Householder.
 #include <math.h>
 #include <cstdlib>
+#include <cstring>
 
 #include <type_traits>
 
@@ -543,9 +544,12 @@ __device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, 
   }
 }
 
-template <int CL>
-__global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A) {
+// BATCHED: cluster b of the grid takes args[b] (independent cubes' eigensolvers
+// in one launch -- the throughput mode of hyde_hyres_batched); else A0.
+template <int CL, bool BATCHED>
+__global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Args* __restrict__ args) {
   pdl_wait();
+  const K2Args A = BATCHED ? args[blockIdx.x / CL] : A0;
   constexpr int RS = 32 / CL;          // row slots per warp (CL * NW * RS = 256 rows)
   constexpr int LPR = 16 / RS;         // lanes holding one reduced row value
   constexpr int LR = NW * RS;          // rows per CTA
@@ -1181,9 +1185,9 @@ __global__ void residual_kernel(const float* __restrict__ Y, long long n, int B,
 int g_cluster = 0;   // cluster size chosen at the first launch (16, else 8)
 
 template <int CL>
-cudaLaunchConfig_t k2_config(cudaLaunchAttribute* attr /* [2] */, cudaStream_t st) {
+cudaLaunchConfig_t k2_config(cudaLaunchAttribute* attr /* [2] */, cudaStream_t st, int nclusters = 1) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CL, 1, 1);
+  cfg.gridDim = dim3(CL * nclusters, 1, 1);
   cfg.blockDim = dim3(NT, 1, 1);
   cfg.dynamicSmemBytes = sizeof(K2Smem);
   cfg.stream = st;
@@ -1198,12 +1202,12 @@ cudaLaunchConfig_t k2_config(cudaLaunchAttribute* attr /* [2] */, cudaStream_t s
   return cfg;
 }
 
-template <int CL>
+template <int CL, bool BATCHED = false>
 cudaError_t prepare_k2() {
-  cudaError_t e = cudaFuncSetAttribute(k2_cluster_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k2_cluster_kernel<CL, BATCHED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(K2Smem));
   if (e == cudaSuccess && CL > 8)
-    e = cudaFuncSetAttribute(k2_cluster_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k2_cluster_kernel<CL, BATCHED>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
@@ -1216,7 +1220,7 @@ bool cluster_fits() {
   cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t cfg = k2_config<CL>(attr, 0);
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k2_cluster_kernel<CL>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, k2_cluster_kernel<CL, false>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -1229,7 +1233,18 @@ cudaError_t launch_k2(const K2Args& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t cfg = k2_config<CL>(attr, st);
-  return cudaLaunchKernelEx(&cfg, k2_cluster_kernel<CL>, a);
+  return cudaLaunchKernelEx(&cfg, k2_cluster_kernel<CL, false>, a, (const K2Args*)nullptr);
+}
+
+template <int CL>
+cudaError_t launch_k2_batched(const K2Args* dargs, int nb, cudaStream_t st) {
+  cudaError_t e = prepare_k2<CL, true>();
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[2];
+  cudaLaunchConfig_t cfg = k2_config<CL>(attr, st, nb);
+  K2Args dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  return cudaLaunchKernelEx(&cfg, k2_cluster_kernel<CL, true>, dummy, dargs);
 }
 
 }  // namespace
@@ -1305,6 +1320,49 @@ cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, 
     e = cudaGetLastError();
   }
   return e;
+}
+
+// Throughput mode of hyde_hyres_batched: sigma and the first ncomp eigenpairs of
+// nb independent Grams in ONE launch (cluster b takes cube b), so the hardware
+// packs the cubes' latency-bound eigensolvers onto the GPU back to back instead
+// of each waiting for its own lane.  Per cube: the same arguments as
+// launch_noise_eig (all_lam = 0); the flags words of every house[b] must be
+// zeroed before (eig_flags_ptr).  hargs: pinned host scratch, dargs: device
+// scratch, nb * eig_args_bytes() each.
+size_t eig_args_bytes() { return sizeof(K2Args); }
+double* eig_flags_ptr(double* house, int B) { return carve(house, B).flags; }
+cudaError_t launch_noise_eig_batched(int nb, const double* const* G, long long n, int B, double ridge, int ncomp,
+                                     double* const* sigma, double* const* house, double* const* tri,
+                                     float* const* W, float* const* U, int ldwu, void* hargs, void* dargs,
+                                     cudaStream_t st, int cl_pref) {
+  if (B > BM || B < 3 || nb < 1) return cudaErrorInvalidValue;
+  K2Args* ha = reinterpret_cast<K2Args*>(hargs);
+  for (int b = 0; b < nb; ++b) {
+    K2Args& a = ha[b];
+    memset(&a, 0, sizeof(a));
+    a.G = G[b];
+    a.n = n;
+    a.B = B;
+    a.raw = 0;
+    a.ridge = ridge;
+    a.K = ncomp > 0 ? (ncomp < KM ? ncomp : KM) : 0;
+    a.tridiag = ncomp >= 0 ? 1 : 0;
+    a.want_M = 0;
+    a.sigma = sigma[b];
+    a.tri = tri[b];
+    a.ws = carve(house[b], B);
+    a.lam_out = nullptr;
+    a.V = nullptr;
+    a.ldv = ncomp > 0 ? ncomp : 1;
+    a.W = W[b];
+    a.U = U[b];
+    a.ldwu = ldwu;
+  }
+  cudaError_t e = cudaMemcpyAsync(dargs, hargs, (size_t)nb * sizeof(K2Args), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  hyde_eig_cluster_size();
+  return (g_cluster == 16 && cl_pref != 8) ? launch_k2_batched<16>((const K2Args*)dargs, nb, st)
+                                           : launch_k2_batched<8>((const K2Args*)dargs, nb, st);
 }
 
 // F1 (HySime): top `ncomp` eigenpairs of the symmetric B x B matrix A itself
