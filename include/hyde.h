@@ -77,8 +77,14 @@ typedef struct {
                      /* grow 4, 8, 16, ... up to this cap (results are independent)  */
   double ridge;      /* delta of (G + delta I)^-1; 0 = 1e-6                */
   int flags;         /* bit0 HYDE_KEEP_LL: leave LL_L unthresholded (variant, Z7)       */
+                     /* bit1 HYDE_VALIDATE: before any work, one pass over the input  */
+                     /* checks finiteness and the call returns HYDE_EDATA at once     */
+                     /* (synchronous; costs one extra read of the cube).  Without it, */
+                     /* non-finite input is caught inside K1 (HYDE_EDATA at the first */
+                     /* rank decision, or from hyde_sync_status).                     */
 } hyde_hyres_params;
 #define HYDE_KEEP_LL 1
+#define HYDE_VALIDATE 2
 
 /* Diagnostics of one HyRes call (host memory). */
 typedef struct {

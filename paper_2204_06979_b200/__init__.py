@@ -58,8 +58,9 @@ def _cube(t, name="cube", ndim=3):
 
 
 def hyres(cube, out=None, *, taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False,
-          return_info=False):
-    """HyRes denoising of one BSQ cube (bands, rows, cols) -> same shape."""
+          return_info=False, validate=False):
+    """HyRes denoising of one BSQ cube (bands, rows, cols) -> same shape.
+    validate=True: HYDE_VALIDATE (fail fast on non-finite input, one extra read)."""
     torch = _torch()
     _cube(cube)
     b, r, c = cube.shape
@@ -67,7 +68,7 @@ def hyres(cube, out=None, *, taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=Fa
         out = torch.empty_like(cube)
     else:
         _cube(out, "out")
-    p = make_params(taps, levels, chunk, ridge, keep_ll)
+    p = make_params(taps, levels, chunk, ridge, keep_ll, validate)
     info = Info()
     h = handle(cube.device.index)
     check(lib().hyde_hyres_ex(h, cube.data_ptr(), r, c, b, out.data_ptr(), ctypes.byref(p),
@@ -76,14 +77,14 @@ def hyres(cube, out=None, *, taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=Fa
 
 
 def hyres_batched(cubes, out=None, *, taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False,
-                  return_info=False):
+                  return_info=False, validate=False):
     """`batch` independent cubes (batch, bands, rows, cols)."""
     torch = _torch()
     _cube(cubes, "cubes", 4)
     n, b, r, c = cubes.shape
     if out is None:
         out = torch.empty_like(cubes)
-    p = make_params(taps, levels, chunk, ridge, keep_ll)
+    p = make_params(taps, levels, chunk, ridge, keep_ll, validate)
     infos = (Info * max(n, 1))()
     h = handle(cubes.device.index)
     check(lib().hyde_hyres_batched(h, cubes.data_ptr(), n, r, c, b, out.data_ptr(), ctypes.byref(p),

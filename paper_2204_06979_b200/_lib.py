@@ -15,6 +15,7 @@ HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "hyde.h")
 
 HYDE_OK, HYDE_EPARAM, HYDE_EDATA, HYDE_EMETHOD, HYDE_ECUDA, HYDE_ENCCL, HYDE_ENOMEM = 0, 2, 3, 4, 5, 6, 7
 HYDE_KEEP_LL = 1
+HYDE_VALIDATE = 2
 STAGES = ("gram", "eig", "project", "dwt", "sure", "rank", "idwt", "recon")
 
 
@@ -146,12 +147,12 @@ def check(status: int, handle=None):
         raise HydeError(status, msg)
 
 
-def make_params(taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False) -> Params:
+def make_params(taps=16, levels=0, chunk=16, ridge=1e-6, keep_ll=False, validate=False) -> Params:
     p = Params()
     lib().hyde_hyres_params_default(ctypes.byref(p))
     p.wavelet_taps = int(taps)
     p.levels = int(levels)
     p.chunk = int(chunk)
     p.ridge = float(ridge)
-    p.flags = HYDE_KEEP_LL if keep_ll else 0
+    p.flags = (HYDE_KEEP_LL if keep_ll else 0) | (HYDE_VALIDATE if validate else 0)
     return p

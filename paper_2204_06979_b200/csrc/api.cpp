@@ -447,6 +447,13 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   if (s != HYDE_OK) return s;
   RankState* rs = (RankState*)(ws + L.rs);
   h->last_rs = rs;
+  if (p.flags & HYDE_VALIDATE) {
+    CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
+    CK(launch_check_finite_f32(cube, n * B, &rs->nonfinite, st));
+    CK(cudaMemcpyAsync(&h->rs_host->nonfinite, &rs->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h->rs_host->nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
+  }
   if (!L.use_tc) CK(cudaMemsetAsync(rs, 0, sizeof(RankState), st));
   double* G = (double*)(ws + L.G);
   double* sigma = (double*)(ws + L.sigma);
@@ -1036,6 +1043,14 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
     return HYDE_OK;
   };
   memset(h->b_rs_host, 0, sizeof(RankState) * batch);
+  if (p.flags & HYDE_VALIDATE) {
+    RankState* rs0 = (RankState*)(ws_of(0) + L.rs);
+    CK(cudaMemsetAsync(rs0, 0, sizeof(RankState), st));
+    CK(launch_check_finite_f32(cubes, (long long)per * batch, &rs0->nonfinite, st));
+    CK(cudaMemcpyAsync(&h->rs_host->nonfinite, &rs0->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h->rs_host->nonfinite) return fail(h, HYDE_EDATA, "non-finite value in the input cube (SPEC.md:26)");
+  }
   s = fork_lanes();
   if (s != HYDE_OK) return s;
   // ---- A1 for every cube ----

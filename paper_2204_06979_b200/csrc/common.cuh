@@ -168,6 +168,7 @@ cudaError_t launch_rank_decide(const double* e_sub, int nsub, int count, int k0,
                                int bands, RankState* rs, double* e_post, cudaStream_t st);
 // E1 helpers (k_util.cu)
 cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStream_t st);
+cudaError_t launch_check_finite_f32(const float* x, long long n, int* flag, cudaStream_t st);
 cudaError_t launch_scatter_rows(const double* src, int nrows, int ncols, const int* to, double* dst, int dst_rows,
                                 const int* flag_in, cudaStream_t st);
 cudaError_t launch_flag_from_sum(const double* x, int* flag, cudaStream_t st);

@@ -36,7 +36,26 @@ __global__ void scatter_rows_kernel(const double* __restrict__ src, int nrows, i
   }
 }
 
+__global__ void check_finite_f32_kernel(const float* __restrict__ x, long long n, int* flag) {
+  bool bad = false;
+  const long long n4 = ((uintptr_t)x & 15) == 0 ? n / 4 : 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(x) + i);
+    bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 }  // namespace
+
+// flag |= any non-finite value of the fp32 array x[0, n) (HYDE_VALIDATE: one read)
+cudaError_t launch_check_finite_f32(const float* x, long long n, int* flag, cudaStream_t st) {
+  check_finite_f32_kernel<<<592, 256, 0, st>>>(x, n, flag);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStream_t st) {
   const unsigned g = (unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64);

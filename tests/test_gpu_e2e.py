@@ -247,3 +247,33 @@ def test_rank_walk_to_last_component(hy):
         out, info = hy.hyres(dev(s.clean), chunk=chunk, return_info=True)
         assert info["rank"] == 3 and info["comps"] == 4
         assert metrics.rel_l2(ref.out, out.cpu().numpy()) <= REL_L2
+
+
+def test_validate_flag_fails_fast_on_nonfinite(hy):
+    """flags bit1 HYDE_VALIDATE (SURVEY §8(b)): a synchronous finiteness pass before any work;
+    finite input gives the same result as without the flag."""
+    s = synth.make_cube("tiny", 0)
+    x = dev(s.noisy)
+    assert torch.equal(hy.hyres(x, validate=True), hy.hyres(x))
+    bad = x.clone()
+    bad[5, 9, 9] = float("inf")
+    for fn in (lambda t: hy.hyres(t, validate=True),
+               lambda t: hy.hyres_batched(torch.stack([x, t]), validate=True)):
+        with pytest.raises(hy.HydeError) as ei:
+            fn(bad)
+        assert ei.value.status == 3
+
+
+def test_batched_phased_needs_second_chunk(hy):
+    """Phased batched path: a cube whose rank rule needs more than the first chunk of 4
+    components (a noiseless rank-6 cube, r* = 6) is finished by the chunked walk; every
+    output equals the single-cube result bit for bit."""
+    cubes = [synth.make_cube("tiny", 0).noisy, synth.low_rank_cube(64, 64, 32, rank=6, seed=2).clean,
+             synth.make_cube("tiny", 3).noisy]
+    x = dev(np.stack(cubes))
+    outs, infos = hy.hyres_batched(x, return_info=True)
+    for i in range(len(cubes)):
+        single, info = hy.hyres(x[i].contiguous(), return_info=True)
+        assert torch.equal(single, outs[i]), i
+        assert infos[i]["rank"] == info["rank"]
+    assert max(i["rank"] for i in infos) >= 4

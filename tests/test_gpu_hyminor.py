@@ -41,13 +41,30 @@ def test_l1_spectral_matches_oracle(hy, b, lam, mu, iters, tol):
     assert np.linalg.norm(d) <= 1e-4 * np.linalg.norm(r)
 
 
-def test_hyminor_end_to_end(hy):
-    s = synth.make_cube("tiny", 0)
+@pytest.mark.parametrize("name", ["tiny", "medium"])
+def test_hyminor_end_to_end(hy, name):
+    """End to end at the north_star bar: relative L2 <= 1e-4 over the pixels whose
+    l1-stage iteration counts agree (>= 98 % of them: a pixel whose stopping test sits
+    at the tolerance may stop one iteration earlier or later -- D19's ||dx|| <= 1e-3
+    ||x|| is a discontinuous rule), |dMPSNR| <= 0.01 dB overall, equal HyRes rank."""
+    s = synth.make_cube(name, 0)
     ref = O.hyminor(s.noisy)
-    got, info = hy.hyminor(torch.from_numpy(s.noisy).cuda(), return_info=True)
-    got = got.cpu().numpy()
-    assert metrics.rel_l2(ref.out, got) <= 1e-3
-    assert abs(metrics.mpsnr(s.clean, got) - metrics.mpsnr(s.clean, ref.out)) <= 0.05
+    x = torch.from_numpy(s.noisy).cuda()
+    m, info = hy.hyres(x, return_info=True)
+    got_t, its = hy.l1_spectral(m, return_iters=True)
+    got = got_t.cpu().numpy()
+    its = its.cpu().numpy()
+    assert info["rank"] == O.hyres(s.noisy).rank
+    agree = its.ravel() == ref.iters.ravel()
+    assert agree.mean() >= 0.98
+    b = s.noisy.shape[0]
+    d = (got - ref.out).reshape(b, -1)[:, agree]
+    r = ref.out.reshape(b, -1)[:, agree]
+    assert np.linalg.norm(d) <= 1e-4 * np.linalg.norm(r)
+    assert abs(metrics.mpsnr(s.clean, got) - metrics.mpsnr(s.clean, ref.out)) <= 0.01
+    # the one-call entry point is the same two stages
+    one = hy.hyminor(x).cpu().numpy()
+    assert np.array_equal(one, got)
 
 
 def test_hyminor_errors_and_in_place(hy):
