@@ -240,8 +240,12 @@ hyde_status hyde_forpdn(hyde_handle h, const float* cube, int rows, int cols, in
  * min_x ||m - x||_1 + lambda ||D x||_1 (D the first-order spectral difference)
  * by split Bregman with penalty mu, from x = m (R16); a pixel stops
  * when ||x_new - x_old|| <= tol ||x_old|| or after max_iters; iters (DEVICE
- * int[rows*cols], may be NULL) receives the iterations per pixel.  One warp per
- * pixel, state in registers; bands in [2, 256]; out == cube allowed.
+ * int[rows*cols], may be NULL) receives the iterations per pixel.  The first
+ * iteration runs one thread per pixel (a sequential Thomas sweep along the
+ * bands, HBM-bound); pixels that continue run one warp per pixel, state in
+ * registers; bands in [2, 256]; out == cube allowed (a pixel continued past
+ * the first iteration then uses m = (I + D^T D) x_1, equal to its input up to
+ * fp32 rounding).  Uses the handle's workspace (n/32 words).
  * hyde_hyminor: hyde_hyres_ex (defaults; info may be NULL) into out, then
  * hyde_l1_spectral in place; lambda 0 -> 10, mu 0 -> 5, max_iters <= 0 -> 50,
  * tol < 0 -> 1e-3 (D19).  Errors: lambda or mu negative -> HYDE_EPARAM; those of

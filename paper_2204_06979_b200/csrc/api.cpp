@@ -125,6 +125,8 @@ struct hyde_ctx {
   // phased batched path: per-cube workspaces, pinned mapped rank states, K2 args
   char* bws = nullptr;
   size_t bws_cap = 0;
+  float* cubebuf = nullptr;      // F3: the l1 stage's input when it would alias its output
+  size_t cubebuf_cap = 0;
   RankState* b_rs_host = nullptr;
   RankState* b_rs_dev = nullptr;
   void* b_args_host = nullptr;
@@ -369,6 +371,7 @@ hyde_status hyde_destroy(hyde_handle h) {
     if (h->ebuf) cudaFree(h->ebuf);
     if (h->shard_buf) cudaFree(h->shard_buf);
     if (h->bws) cudaFree(h->bws);
+    if (h->cubebuf) cudaFree(h->cubebuf);
     if (h->b_rs_host) cudaFreeHost(h->b_rs_host);
     if (h->b_args_host) cudaFreeHost(h->b_args_host);
     if (h->dev_in) cudaFree(h->dev_in);
@@ -1360,8 +1363,23 @@ hyde_status hyde_l1_spectral(hyde_handle h, const float* cube, int rows, int col
   const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
   if (cube != out && overlap(cube, bytes, out, bytes)) return fail(h, HYDE_EPARAM, "cube and out partially overlap");
   DeviceGuard g(h->device);
-  CK(launch_l1spec(cube, out, (long long)rows * cols, bands, (float)lambda, (float)mu, max_iters, (float)tol, iters,
-                   (cudaStream_t)stream));
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long n = (long long)rows * cols;
+  hyde_status s = ensure_ws(h, l1spec_ws_bytes(n), st);   // per-tile continue masks
+  if (s != HYDE_OK) return s;
+  const float* M = cube;
+  if (cube == out) {   // in place: the stage streams its output over its input, so keep m aside
+    if (bytes > h->cubebuf_cap) {
+      if (h->cubebuf) CK(cudaFreeAsync(h->cubebuf, st));
+      h->cubebuf = nullptr;
+      h->cubebuf_cap = 0;
+      CK(cudaMallocAsync((void**)&h->cubebuf, bytes, st));
+      h->cubebuf_cap = bytes;
+    }
+    if (h->cubebuf != cube) CK(cudaMemcpyAsync(h->cubebuf, cube, bytes, cudaMemcpyDeviceToDevice, st));
+    M = h->cubebuf;
+  }
+  CK(launch_l1spec(M, out, n, bands, (float)lambda, (float)mu, max_iters, (float)tol, iters, h->ws, st));
   return HYDE_OK;
 }
 
@@ -1372,9 +1390,21 @@ hyde_status hyde_hyminor(hyde_handle h, const float* cube, int rows, int cols, i
   if (max_iters <= 0) max_iters = 50;
   if (tol < 0.0) tol = 1e-3;
   if (!(lambda > 0.0) || !(mu > 0.0)) return fail(h, HYDE_EPARAM, "lambda, mu > 0 required (SPEC.md:420)");
-  hyde_status s = hyde_hyres_ex(h, cube, rows, cols, bands, out, nullptr, info, stream);
+  // HyRes into the handle's cube buffer, then the l1 stage from it into out
+  // (no in-place pass: the l1 stage reads its input once more than it writes)
+  const size_t bytes = (size_t)rows * cols * bands * sizeof(float);
+  if (validate_shape(h, rows, cols, bands) == HYDE_OK && bytes > h->cubebuf_cap) {
+    DeviceGuard g(h->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (h->cubebuf) CK(cudaFreeAsync(h->cubebuf, st));
+    h->cubebuf = nullptr;
+    h->cubebuf_cap = 0;
+    CK(cudaMallocAsync((void**)&h->cubebuf, bytes, st));
+    h->cubebuf_cap = bytes;
+  }
+  hyde_status s = hyde_hyres_ex(h, cube, rows, cols, bands, h->cubebuf, nullptr, info, stream);
   if (s != HYDE_OK) return s;
-  return hyde_l1_spectral(h, out, rows, cols, bands, out, lambda, mu, max_iters, tol, nullptr, stream);
+  return hyde_l1_spectral(h, h->cubebuf, rows, cols, bands, out, lambda, mu, max_iters, tol, nullptr, stream);
 }
 
 hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int bands, int rank, double lambda,

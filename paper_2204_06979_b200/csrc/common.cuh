@@ -108,8 +108,9 @@ cudaError_t launch_noise_eig_batched(int nb, const double* const* G, long long n
                                      float* const* W, float* const* U, int ldwu, void* hargs, void* dargs,
                                      cudaStream_t st, int cl_pref = 0);
 // F3: HyMiNoR second stage (k_hyminor.cu)
+size_t l1spec_ws_bytes(long long n);
 cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float lam, float mu, int max_iters, float tol,
-                          int* iters, cudaStream_t st);
+                          int* iters, void* todo_ws, cudaStream_t st);
 // F4: WSRRR (k_wsrrr.cu)
 cudaError_t launch_wsrrr_lambda(const double* sigma, int B, long long nc, double* lam, cudaStream_t st);
 cudaError_t launch_sumsq(const float* x, long long n, double* partial, double* out, cudaStream_t st);

@@ -6,6 +6,17 @@
 //   x = (I + D^T D)^-1 (a + m - b_a + D^T (d - b_d))
 //   a = shrink(x - m + b_a, 1/mu), b_a += x - m - a
 //   d = shrink(D x + b_d, lam/mu), b_d += D x - d
+// Two kernels.  (1) l1spec_first_kernel: ONE THREAD PER PIXEL for the first
+// iteration, which starts from x = m, a = d = b = 0 so its right-hand side is m
+// itself: a sequential Thomas sweep along the bands (forward y_i = alpha_i
+// (y_{i-1} + m_i) stored in X as scratch, backward x_i = y_i - c'_i x_{i+1}
+// written over it), the stopping test ||x - m|| <= tol ||m|| on the way back.
+// Band rows are read and written by consecutive threads (coalesced, no
+// staging), so the stage streams M once and X once (the backward re-reads are
+// L2 hits): the D19 defaults stop every pixel of the BJ cubes here.  Every
+// pixel that has not stopped is marked in a per-32-pixel tile mask.
+// (2) l1spec_kernel continues the marked tiles' unstopped pixels from
+// x_1 (a_1, b_a, d_1, b_d follow from x_1 and m):
 // ONE WARP PER PIXEL, the whole state in registers: lane l owns the S = B/32
 // consecutive bands [l S, l S + S).  The tridiagonal x-update (I + D^T D is
 // tridiagonal, strictly diagonally dominant) is the Thomas algorithm written
@@ -14,6 +25,10 @@
 // composition of affine maps plus a 5-step warp scan (no shared memory, no
 // serial 224-step chain).  A pixel stops when ||x_new - x_old|| <= tol ||x_old||.
 #include "common.cuh"
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 namespace {
 
@@ -49,11 +64,86 @@ struct ThomasF {
   float cp[256];
 };
 
+// (1) first iteration, one thread per pixel.  From x_0 = m and zero state the
+// right-hand side is m itself: a sequential Thomas sweep along the bands,
+// forward y_i = alpha_i (y_{i-1} + m_i) stored in X as scratch, backward
+// x_i = y_i - c'_i x_{i+1} written over it; ||m|| on the way forward and
+// ||x_1 - m|| on the way back from x - m = -(D^T D) x, so M is read once (and
+// M == X works).  Consecutive threads touch consecutive pixels of a band row
+// (coalesced, no staging).  (A 41-tap band filter of rows of A^-1 -- one pass,
+// no scratch -- measured slower: 1.8 vs 0.8 ms at `large`, long-scoreboard and
+// instruction-fetch bound.)
+__global__ void __launch_bounds__(128) l1spec_first_kernel(const float* __restrict__ M, float* __restrict__ X,
+                                                          long long n, int B, float tol, int max_iters,
+                                                          int* __restrict__ iters_out,
+                                                          unsigned* __restrict__ tile_todo, const ThomasF tf) {
+  __shared__ float s_alpha[256], s_cp[256];
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    s_alpha[i] = tf.alpha[i];
+    s_cp[i] = tf.cp[i];
+  }
+  __syncthreads();
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool live = p < n;
+  float y = 0.f, xo2 = 0.f;
+  if (live) {
+#pragma unroll 8
+    for (int i = 0; i < B; ++i) {
+      const float m = M[(size_t)i * n + p];
+      xo2 = fmaf(m, m, xo2);
+      y = s_alpha[i] * (y + m);
+      X[(size_t)i * n + p] = y;
+    }
+  }
+  float dx2 = 0.f;
+  if (live) {
+    float x1 = 0.f, x2 = 0.f;   // x_{i+1}, x_{i+2}
+#pragma unroll 8
+    for (int i = B - 1; i >= 0; --i) {
+      const float x = fmaf(-s_cp[i], x1, X[(size_t)i * n + p]);
+      __stcs(X + (size_t)i * n + p, x);
+      if (i + 1 <= B - 1) {   // (D^T D x)_{i+1} now that x_i is known
+        const float t = (i + 1 == B - 1) ? x1 - x : (2.f * x1 - x - x2);
+        dx2 = fmaf(t, t, dx2);
+      }
+      x2 = x1;
+      x1 = x;
+    }
+    if (B >= 2) {
+      const float t = x1 - x2;   // row 0: x_0 - x_1
+      dx2 = fmaf(t, t, dx2);
+    }
+  }
+  const bool stop = live && (max_iters <= 1 || sqrtf(dx2) <= tol * sqrtf(xo2));
+  if (live && iters_out) iters_out[p] = 1;
+  const unsigned more = __ballot_sync(0xffffffffu, live && !stop);
+  if ((threadIdx.x & 31) == 0 && live) tile_todo[p >> 5] = more;
+}
+
+// (2) later iterations of the marked pixels, one warp per pixel, from x_1
 template <int S>
 __global__ void __launch_bounds__(NT) l1spec_kernel(const float* __restrict__ M, float* __restrict__ X, long long n,
                                                     int B, float lam, float mu, int max_iters, float tol,
-                                                    int* __restrict__ iters_out, const ThomasF tf) {
+                                                    int* __restrict__ iters_out, const unsigned* __restrict__ tile_todo,
+                                                    const ThomasF tf) {
   __shared__ float s_alpha[32 * S], s_cp[32 * S];
+  __shared__ unsigned long long s_tile;
+  const long long ntile = (n + 31) / 32;
+  for (long long tile_i = blockIdx.x;; tile_i += gridDim.x) {
+  // next tile of this CTA with a pixel to continue (most CTAs find none)
+  __syncthreads();
+  if (threadIdx.x == 0) s_tile = ~0ull;
+  __syncthreads();
+  // the first tile >= tile_i (stride gridDim) with work: NT candidates at a time
+  for (long long t0 = tile_i; t0 < ntile; t0 += (long long)NT * gridDim.x) {
+    const long long t = t0 + (long long)threadIdx.x * gridDim.x;
+    const bool has = t < ntile && tile_todo[t] != 0u;
+    if (has) atomicMin(&s_tile, (unsigned long long)t);   // ~0 (none) is the largest u64
+    if (__syncthreads_or(has)) break;
+  }
+  if (s_tile == ~0ull) return;
+  tile_i = (long long)s_tile;
+  const unsigned todo = tile_todo[tile_i];
   for (int i = threadIdx.x; i < 32 * S; i += NT) {
     s_alpha[i] = tf.alpha[i];
     s_cp[i] = tf.cp[i];
@@ -62,29 +152,61 @@ __global__ void __launch_bounds__(NT) l1spec_kernel(const float* __restrict__ M,
   // the CTA stages a tile of TP consecutive pixels x all bands through shared
   // memory (coalesced 128-byte band rows in and out); warp w solves pixels
   // w, w + 8, ... of the tile from it
-  extern __shared__ float tile[];   // [32 S][TP + 1]
+  extern __shared__ float tile[];   // m: [32 S][TP + 1], then x_1: [32 S][TP + 1]
   constexpr int TP = 32;
+  float* tx = tile + 32 * S * (TP + 1);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long p0 = (long long)blockIdx.x * TP;
+  const long long p0 = tile_i * TP;
   const int np = (int)min((long long)TP, n - p0);
   for (int x = threadIdx.x; x < B * TP; x += NT) {
     const int i = x / TP, q = x % TP;
-    tile[i * (TP + 1) + q] = q < np ? M[(size_t)i * n + p0 + q] : 0.f;
+    if (M != X) tile[i * (TP + 1) + q] = q < np ? M[(size_t)i * n + p0 + q] : 0.f;
+    tx[i * (TP + 1) + q] = q < np ? X[(size_t)i * n + p0 + q] : 0.f;
   }
   __syncthreads();
+  if (M == X) {
+    // in place: m was overwritten by x_1; m = (I + D^T D) x_1 (to fp32 rounding)
+    for (int x = threadIdx.x; x < B * TP; x += NT) {
+      const int i = x / TP, q = x % TP;
+      const float xc = tx[i * (TP + 1) + q];
+      const float xl = i > 0 ? tx[(i - 1) * (TP + 1) + q] : xc;
+      const float xr = i < B - 1 ? tx[(i + 1) * (TP + 1) + q] : xc;
+      tile[i * (TP + 1) + q] = xc + (xc - xl) + (xc - xr);
+    }
+    __syncthreads();
+  }
   const float ta = 1.f / mu, td = lam / mu;
   for (int q = wid; q < np; q += NT / 32) {
+    if (!((todo >> q) & 1u)) continue;   // stopped after the first iteration
     float m[S], x[S], a[S], ba[S], d[S], bd[S], al[S], cp[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int i = lane * S + s;
       m[s] = i < B ? tile[i * (TP + 1) + q] : 0.f;
-      x[s] = m[s];
-      a[s] = ba[s] = d[s] = bd[s] = 0.f;
+      x[s] = i < B ? tx[i * (TP + 1) + q] : 0.f;
       al[s] = s_alpha[i];
       cp[s] = s_cp[i];
     }
-    int it = 0;
+    // the first iteration's a, b_a, d, b_d from x_1 and m (x_0 = m, zero state)
+    {
+      float xnext = __shfl_down_sync(FULL, x[0], 1);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = lane * S + s;
+        const float t = x[s] - m[s];
+        a[s] = shrinkf(t, ta);
+        ba[s] = t - a[s];
+        const float x1 = s + 1 < S ? x[s + 1] : xnext;
+        if (i < B - 1) {
+          const float u = x1 - x[s];
+          d[s] = shrinkf(u, td);
+          bd[s] = u - d[s];
+        } else {
+          d[s] = bd[s] = 0.f;
+        }
+      }
+    }
+    int it = 1;
     for (; it < max_iters; ++it) {
       // rhs_i = a_i + m_i - ba_i + v_{i-1} - v_i, v = d - bd (v_{B-1} = 0, v_{-1} = 0)
       float v[S];
@@ -162,25 +284,34 @@ __global__ void __launch_bounds__(NT) l1spec_kernel(const float* __restrict__ M,
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int i = lane * S + s;
-      if (i < B) tile[i * (TP + 1) + q] = x[s];
+      if (i < B) tx[i * (TP + 1) + q] = x[s];
     }
     if (iters_out && lane == 0) iters_out[p0 + q] = it;
   }
   __syncthreads();
   for (int x = threadIdx.x; x < B * TP; x += NT) {
     const int i = x / TP, q = x % TP;
-    if (q < np) X[(size_t)i * n + p0 + q] = tile[i * (TP + 1) + q];
+    if (q < np && ((todo >> q) & 1u)) X[(size_t)i * n + p0 + q] = tx[i * (TP + 1) + q];
+  }
   }
 }
 
 }  // namespace
 
+size_t l1spec_ws_bytes(long long n) { return (size_t)((n + 31) / 32) * sizeof(unsigned); }
+
+// todo_ws: l1spec_ws_bytes(n) bytes of device scratch (the per-tile masks).
+// M and X may alias only when equal (in place): the first iteration never
+// re-reads M; a pixel continued past it then works from m = (I + D^T D) x_1
+// (equal to m up to fp32 rounding) instead of the overwritten input.
 cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float lam, float mu, int max_iters, float tol,
-                          int* iters, cudaStream_t st) {
+                          int* iters, void* todo_ws, cudaStream_t st) {
   const unsigned blocks = (unsigned)((n + 31) / 32);
   const int S = (B + 31) / 32;
   if (S > 8) return cudaErrorInvalidValue;
-  const size_t sm = (size_t)32 * S * 33 * sizeof(float);
+  const int St = S <= 2 ? 2 : (S <= 4 ? 4 : 8);   // the instantiated register width
+  const unsigned g2 = blocks < 1184u ? blocks : 1184u;   // continuation: grid-stride over 32-pixel tiles
+  const size_t sm = (size_t)2 * 32 * St * 33 * sizeof(float);
   ThomasF tf;
   {
     double cprev = 0.0;
@@ -197,8 +328,24 @@ cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float la
       }
     }
   }
-  if (S <= 2) l1spec_kernel<2><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, tf);
-  else if (S <= 4) l1spec_kernel<4><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, tf);
-  else l1spec_kernel<8><<<blocks, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, tf);
+  unsigned* todo = (unsigned*)todo_ws;
+  l1spec_first_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(M, X, n, B, tol, max_iters, iters, todo, tf);
+  cudaError_t e = cudaGetLastError();
+  if (getenv("HYDE_DEBUG_SYNC")) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { fprintf(stderr, "l1spec_first_kernel: %s\n", cudaGetErrorString(e)); return e; }
+  }
+  if (e != cudaSuccess || max_iters <= 1) return e;
+  if (S <= 2) {
+    e = cudaFuncSetAttribute(l1spec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    l1spec_kernel<2><<<g2, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, todo, tf);
+  } else if (S <= 4) {
+    e = cudaFuncSetAttribute(l1spec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    l1spec_kernel<4><<<g2, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, todo, tf);
+  } else {
+    e = cudaFuncSetAttribute(l1spec_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    l1spec_kernel<8><<<g2, NT, sm, st>>>(M, X, n, B, lam, mu, max_iters, tol, iters, todo, tf);
+  }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
