@@ -130,6 +130,7 @@ struct hyde_ctx {
   RankState* b_rs_host = nullptr;
   RankState* b_rs_dev = nullptr;
   void* b_args_host = nullptr;
+  void* b_jobs_host = nullptr;
   int b_cap = 0;
   cudaEvent_t ev_rank = nullptr; // recorded after the per-chunk D2H copy of the rank state
   int gram_min_px = 0;           // K1 pixels per SM pair, at least (0: latency mode; lanes: throughput)
@@ -374,6 +375,7 @@ hyde_status hyde_destroy(hyde_handle h) {
     if (h->cubebuf) cudaFree(h->cubebuf);
     if (h->b_rs_host) cudaFreeHost(h->b_rs_host);
     if (h->b_args_host) cudaFreeHost(h->b_args_host);
+    if (h->b_jobs_host) cudaFreeHost(h->b_jobs_host);
     if (h->dev_in) cudaFree(h->dev_in);
     if (h->dev_out) cudaFree(h->dev_out);
     for (auto b : h->pipe_buf)
@@ -1001,7 +1003,8 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
   const int first = std::min(std::min(kFirstChunk, p.chunk), B);
   const size_t per_ws = al(L.total), per_e = al((size_t)first * L.ldE * 4);
   const size_t args_b = al((size_t)batch * eig_args_bytes());
-  const size_t need = (size_t)batch * (per_ws + per_e) + args_b;
+  const size_t jobs_b = al((size_t)batch * gram_job_bytes());
+  const size_t need = (size_t)batch * (per_ws + per_e) + args_b + jobs_b;
   if (need > h->bws_cap) {
     if (h->bws) CK(cudaFreeAsync(h->bws, st));
     h->bws = nullptr;
@@ -1013,12 +1016,15 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
     CK(cudaStreamSynchronize(st));
     if (h->b_rs_host) CK(cudaFreeHost(h->b_rs_host));
     if (h->b_args_host) CK(cudaFreeHost(h->b_args_host));
+    if (h->b_jobs_host) CK(cudaFreeHost(h->b_jobs_host));
     h->b_rs_host = nullptr;
     h->b_args_host = nullptr;
+    h->b_jobs_host = nullptr;
     h->b_cap = 0;
     CK(cudaHostAlloc((void**)&h->b_rs_host, sizeof(RankState) * batch, cudaHostAllocMapped | cudaHostAllocPortable));
     CK(cudaHostGetDevicePointer((void**)&h->b_rs_dev, h->b_rs_host, 0));
     CK(cudaHostAlloc(&h->b_args_host, (size_t)batch * eig_args_bytes(), cudaHostAllocPortable));
+    CK(cudaHostAlloc(&h->b_jobs_host, (size_t)batch * gram_job_bytes(), cudaHostAllocPortable));
     h->b_cap = batch;
   }
   const int NS = std::min(batch, lanes_wanted());
@@ -1056,9 +1062,28 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
   }
   s = fork_lanes();
   if (s != HYDE_OK) return s;
-  // ---- A1 for every cube ----
-  {
-    Stage sg(h, HYDE_STAGE_GRAM, batch * (L.use_tc ? 5 : 2), st);
+  // ---- A1 for every cube: five launches for the whole batch ----
+  if (L.use_tc) {
+    Stage sg(h, HYDE_STAGE_GRAM, 5, st);
+    std::vector<const float*> Y(batch);
+    std::vector<void*> W(batch);
+    std::vector<double*> G(batch), Z(batch);
+    std::vector<int*> NF(batch), S4(batch);
+    for (int i = 0; i < batch; ++i) {
+      char* ws = ws_of(i);
+      RankState* rs = (RankState*)(ws + L.rs);
+      Y[i] = cubes + per * i;
+      W[i] = ws + L.partial;
+      G[i] = (double*)(ws + L.G);
+      NF[i] = &rs->nonfinite;
+      S4[i] = (int*)rs;
+      Z[i] = eig_flags_ptr((double*)(ws + L.house), B);
+    }
+    CK(launch_gram_tc_batched(batch, Y.data(), W.data(), G.data(), NF.data(), S4.data(), Z.data(), n, B, L.npairs,
+                              h->b_jobs_host, h->bws + (size_t)batch * (per_ws + per_e) + args_b, st));
+    sg.end();
+  } else {
+    Stage sg(h, HYDE_STAGE_GRAM, batch * 2, st);
     for (int i = 0; i < batch; ++i) {
       cudaStream_t ls = h->lane_st[i % NS];
       char* ws = ws_of(i);

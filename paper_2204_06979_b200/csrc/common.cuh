@@ -95,6 +95,10 @@ struct GramQScale {
 size_t gram_tc_ws_bytes(long long n, int B, int npairs);
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npairs, double* G, int* nonfinite,
                            cudaStream_t st, int* state4 = nullptr);
+size_t gram_job_bytes();
+cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* ws, double* const* G,
+                                   int* const* nonfinite, int* const* state4, double* const* zero8, long long n,
+                                   int B, int npairs, void* hjobs, void* djobs, cudaStream_t st);
 void gram_tc_debug_ptrs(void* ws, long long n, int B, int npairs, const GramQScale** qs, const int** cnt);
 int gram_tc_fix_splits();
 size_t eig_workspace_doubles(int B);

@@ -72,6 +72,27 @@ constexpr int FIX_TB = 64;     // correction output block edge
 constexpr int FIX_TP = 32;     // correction pixels per stage
 constexpr int FIX_CAP = 2048;  // flagged-pixel list entries per pass
 
+struct FixOut {
+  double* F;        // [FIX_SPLITS][B*B]
+  long long* D;     // [FIX_SPLITS][B*B]
+  long long* Q1;    // [FIX_SPLITS][B]
+  int* cnt;         // [FIX_SPLITS]
+};
+
+// One cube of a batched Gram (hyde_hyres_batched's phased mode): the kernels
+// take jobs[blockIdx.y] instead of their pointer arguments (same n and B).
+struct GramJob {
+  const float* Y;
+  GramQScale* qs;
+  unsigned* bitmap;
+  long long* partial;
+  FixOut fix;
+  double* G;
+  int* nonfinite;
+  int* state4;     // rank-state words to zero (or NULL)
+  double* zero8;   // 8 more words to zero (the eigensolver's flags), or NULL
+};
+
 struct GramTc {
   const float* Y;
   long long n;
@@ -112,9 +133,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, in
 
 template <bool TMA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-    gram_tc_kernel(GramTc P, const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ) {
+    gram_tc_kernel(GramTc P, const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
+                   const GramJob* __restrict__ jobs) {
   enum : int { NI = Feed<TMA>::NI, NCW = Feed<TMA>::NCW, MAXU = Feed<TMA>::MAXU, W0 = Feed<TMA>::W0 };
   pdl_wait();
+  if (!TMA && jobs) {
+    const GramJob& j = jobs[blockIdx.y];
+    P.Y = j.Y;
+    P.qs = j.qs;
+    P.partial = j.partial;
+    P.bitmap = j.bitmap;
+  }
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NI];
   __shared__ __align__(8) uint64_t bar_empty[NI];
@@ -488,8 +517,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 constexpr int QS_CL = 8;   // CTAs per band (cluster)
 __global__ void __cluster_dims__(QS_CL, 1, 1) __launch_bounds__(256)
     gram_qscale_kernel(const float* __restrict__ Y, long long n, GramQScale* qs, unsigned* bitmap, long long nwords,
-                       int* st4, int nst4) {
+                       int* st4, int nst4, const GramJob* __restrict__ jobs) {
   pdl_wait();
+  if (jobs) {
+    const GramJob& j = jobs[blockIdx.y];
+    Y = j.Y;
+    qs = j.qs;
+    bitmap = j.bitmap;
+    st4 = j.state4;
+    if (j.zero8 && blockIdx.x == 0 && threadIdx.x < 8) j.zero8[threadIdx.x] = 0.0;
+  }
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int b = blockIdx.x / QS_CL, crank = (int)cl.block_rank();
@@ -601,8 +638,10 @@ __global__ void __cluster_dims__(QS_CL, 1, 1) __launch_bounds__(256)
 // (B x B without the block rows >= 128 / columns < 128, then the B sums of q),
 // coalesced; 8 warps split k, fixed order.  S overwrites P[0] (each element is
 // read and written by its own thread only).
-__global__ void __launch_bounds__(256) gram_reduce_i64_kernel(long long* __restrict__ partial, int np, int B) {
+__global__ void __launch_bounds__(256) gram_reduce_i64_kernel(long long* __restrict__ partial, int np, int B,
+                                                              const GramJob* __restrict__ jobs) {
   pdl_wait();
+  if (jobs) partial = jobs[blockIdx.y].partial;
   __shared__ long long part[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long bb = (long long)B * B, tot = bb + B;
@@ -639,12 +678,6 @@ __global__ void __launch_bounds__(256) gram_reduce_i64_kernel(long long* __restr
 // walking the upper-triangular 64x64 output blocks of its split.  A split
 // without a flagged pixel writes only its count (0) and exits after one scan
 // of its bitmap words.
-struct FixOut {
-  double* F;        // [FIX_SPLITS][B*B]
-  long long* D;     // [FIX_SPLITS][B*B]
-  long long* Q1;    // [FIX_SPLITS][B]
-  int* cnt;         // [FIX_SPLITS]
-};
 
 // the integer the converters fed to the MMAs for value y (any y, flagged or not)
 __device__ __forceinline__ int quant_q(float y, const GramQScale& q) {
@@ -654,8 +687,16 @@ __device__ __forceinline__ int quant_q(float y, const GramQScale& q) {
 __global__ void __launch_bounds__(256) gram_fix_kernel(const float* __restrict__ Y, long long n, int B, int nbk,
                                                        const GramQScale* __restrict__ qsc,
                                                        const unsigned* __restrict__ bitmap, FixOut o,
-                                                       int* nonfinite) {
+                                                       int* nonfinite, const GramJob* __restrict__ jobs) {
   pdl_wait();
+  if (jobs) {
+    const GramJob& j = jobs[blockIdx.y];
+    Y = j.Y;
+    qsc = j.qs;
+    bitmap = j.bitmap;
+    o = j.fix;
+    nonfinite = j.nonfinite;
+  }
   __shared__ float As[FIX_TP][FIX_TB + 1];
   __shared__ float Bs[FIX_TP][FIX_TB + 1];
   __shared__ int Aq[FIX_TP][FIX_TB + 1];
@@ -809,8 +850,15 @@ __device__ __forceinline__ double i128_to_f64(__int128 x) {
 // in split order.
 __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __restrict__ S, int B, long long n,
                                                             const GramQScale* __restrict__ qsc, FixOut o,
-                                                            double* __restrict__ G) {
+                                                            double* __restrict__ G, const GramJob* __restrict__ jobs) {
   pdl_wait();
+  if (jobs) {
+    const GramJob& j = jobs[blockIdx.y];
+    S = j.partial;
+    qsc = j.qs;
+    o = j.fix;
+    G = j.G;
+  }
   __shared__ int live[FIX_SPLITS];
   __shared__ int nlive;
   __shared__ long long np_sh;
@@ -949,7 +997,7 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
                            cudaStream_t st, int* state4) {
   TcWs w = carve(ws, n, B, npairs);
   cudaError_t e = launch_pdl(gram_qscale_kernel, dim3(QS_CL * B), dim3(256), 0, st, Y, n, w.qs, w.bitmap, w.nwords, state4,
-                             (int)(sizeof(RankState) / sizeof(int)));
+                             (int)(sizeof(RankState) / sizeof(int)), (const GramJob*)nullptr);
   if (e != cudaSuccess) return e;
   GramTc P;
   P.Y = Y;
@@ -970,22 +1018,83 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
     const size_t smem = (size_t)Feed<true>::NI * 2 * P.rows_tot * KC + (size_t)NF * FSTAGE;
     e = cudaFuncSetAttribute(gram_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(gram_tc_kernel<true>, dim3(2 * npairs), dim3(NTHREADS), smem, st, P, tmP, tmQ);
+    e = launch_pdl(gram_tc_kernel<true>, dim3(2 * npairs), dim3(NTHREADS), smem, st, P, tmP, tmQ,
+                   (const GramJob*)nullptr);
   } else {
     memset(&tmP, 0, sizeof(tmP));
     const size_t smem = (size_t)Feed<false>::NI * 2 * P.rows_tot * KC;
     e = cudaFuncSetAttribute(gram_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(gram_tc_kernel<false>, dim3(2 * npairs), dim3(NTHREADS), smem, st, P, tmP, tmP);
+    e = launch_pdl(gram_tc_kernel<false>, dim3(2 * npairs), dim3(NTHREADS), smem, st, P, tmP, tmP,
+                   (const GramJob*)nullptr);
   }
   if (e != cudaSuccess) return e;
   const long long tot = (long long)B * B + B;
-  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, w.partial, npairs, B);
+  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, w.partial, npairs, B,
+                 (const GramJob*)nullptr);
   if (e != cudaSuccess) return e;
   const int nbk = (B + FIX_TB - 1) / FIX_TB;
   e = launch_pdl(gram_fix_kernel, dim3(FIX_SPLITS), dim3(256), 0, st, Y, n, B, nbk,
-                 (const GramQScale*)w.qs, (const unsigned*)w.bitmap, w.fix, nonfinite);
+                 (const GramQScale*)w.qs, (const unsigned*)w.bitmap, w.fix, nonfinite, (const GramJob*)nullptr);
   if (e != cudaSuccess) return e;
   return launch_pdl(gram_finalize_kernel, dim3((unsigned)(((long long)B * B + 255) / 256)), dim3(256), 0, st,
-                    (const long long*)w.partial, B, n, (const GramQScale*)w.qs, w.fix, G);
+                    (const long long*)w.partial, B, n, (const GramQScale*)w.qs, w.fix, G, (const GramJob*)nullptr);
+}
+
+// The same five kernels for nb cubes of one shape in one launch each
+// (blockIdx.y = cube; register feed): the phased batched path.  hjobs: pinned
+// host scratch, djobs: device scratch, nb * sizeof(GramJob) each.
+size_t gram_job_bytes() { return sizeof(GramJob); }
+cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* ws, double* const* G,
+                                   int* const* nonfinite, int* const* state4, double* const* zero8, long long n,
+                                   int B, int npairs, void* hjobs, void* djobs, cudaStream_t st) {
+  GramJob* hj = reinterpret_cast<GramJob*>(hjobs);
+  for (int b = 0; b < nb; ++b) {
+    TcWs w = carve(ws[b], n, B, npairs);
+    hj[b].Y = Y[b];
+    hj[b].qs = w.qs;
+    hj[b].bitmap = w.bitmap;
+    hj[b].partial = w.partial;
+    hj[b].fix = w.fix;
+    hj[b].G = G[b];
+    hj[b].nonfinite = nonfinite[b];
+    hj[b].state4 = state4 ? state4[b] : nullptr;
+    hj[b].zero8 = zero8 ? zero8[b] : nullptr;
+  }
+  const GramJob* dj = reinterpret_cast<const GramJob*>(djobs);
+  cudaError_t e = cudaMemcpyAsync(djobs, hjobs, (size_t)nb * sizeof(GramJob), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  const long long nwords = (n + 31) / 32;
+  e = launch_pdl(gram_qscale_kernel, dim3(QS_CL * B, nb), dim3(256), 0, st, (const float*)nullptr, n,
+                 (GramQScale*)nullptr, (unsigned*)nullptr, nwords, (int*)nullptr,
+                 (int)(sizeof(RankState) / sizeof(int)), dj);
+  if (e != cudaSuccess) return e;
+  GramTc P;
+  memset(&P, 0, sizeof(P));
+  P.n = n;
+  P.B = B;
+  P.nb = B > 128 ? ((B - 128 + 31) / 32) * 32 : 0;
+  P.rows_tot = B > 128 ? 128 : 64;
+  long long per = (n + npairs - 1) / npairs;
+  per = (per + KC - 1) / KC * KC;
+  P.per_pair = per;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  const size_t smem = (size_t)Feed<false>::NI * 2 * P.rows_tot * KC;
+  e = cudaFuncSetAttribute(gram_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(gram_tc_kernel<false>, dim3(2 * npairs, nb), dim3(NTHREADS), smem, st, P, tm, tm, dj);
+  if (e != cudaSuccess) return e;
+  const long long tot = (long long)B * B + B;
+  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32), nb), dim3(256), 0, st,
+                 (long long*)nullptr, npairs, B, dj);
+  if (e != cudaSuccess) return e;
+  const int nbk = (B + FIX_TB - 1) / FIX_TB;
+  FixOut fo;
+  memset(&fo, 0, sizeof(fo));
+  e = launch_pdl(gram_fix_kernel, dim3(FIX_SPLITS, nb), dim3(256), 0, st, (const float*)nullptr, n, B, nbk,
+                 (const GramQScale*)nullptr, (const unsigned*)nullptr, fo, (int*)nullptr, dj);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(gram_finalize_kernel, dim3((unsigned)(((long long)B * B + 255) / 256), nb), dim3(256), 0, st,
+                    (const long long*)nullptr, B, n, (const GramQScale*)nullptr, fo, (double*)nullptr, dj);
 }
