@@ -158,6 +158,19 @@ __device__ __forceinline__ double rcp64(double a) {
   return fma(r, e, r);
 }
 
+// 1/sqrt(a) (a > 0 finite): MUFU seed + two Newton steps -- one short
+// dependent sequence instead of an IEEE sqrt followed by a reciprocal
+__device__ __forceinline__ double rsqrt64(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double t = a * y;
+  double e = fma(-t, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  t = a * y;
+  e = fma(-t, y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -461,8 +474,6 @@ struct K2Smem {
   double colK[2][BM * NB]; // sweep: pivot-block columns of every row (double-buffered by block)
   double Wb[NB][BM];       // sweep: L^-1 A_K,:
   double Zb[NB][BM];       // sweep: P^-1 A_K,:
-  double Lb[NB * NB];      // sweep: Cholesky factor of the pivot block
-  double Lr[NB];           //        1 / L_qq
   double Pinv[NB * NB];
   double sig[BM];
   double vw[NW][BM];       // per-warp copy of the current reflector vector
@@ -514,7 +525,7 @@ __device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, 
   beta = 0.0;
   if (tail > 0.0 && kk < B - 2) {
     const double sumsq = fma(x0, x0, tail);
-    alpha = -copysign(sqrt(sumsq), x0);
+    alpha = -copysign(sumsq * rsqrt64(sumsq), x0);
     v0 = x0 - alpha;
     beta = 2.0 * rcp64(fma(v0, v0, tail));
   }
@@ -570,8 +581,9 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
     mbar_init(saddr(&S.smb[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const int nblk = (A.B + NB - 1) / NB;
-    mbar_expect(saddr(&S.smb[0]), (unsigned)(A.B * min(NB, A.B) * 8));
-    if (nblk > 1) mbar_expect(saddr(&S.smb[1]), (unsigned)(A.B * min(NB, A.B - NB) * 8));
+    // bytes of block b's all-gather: B rows x its column count rounded up to pairs
+    mbar_expect(saddr(&S.smb[0]), (unsigned)(A.B * ((min(NB, A.B) + 1) & ~1) * 8));
+    if (nblk > 1) mbar_expect(saddr(&S.smb[1]), (unsigned)(A.B * ((min(NB, A.B - NB) + 1) & ~1) * 8));
   }
   cl_sync();   // barrier initialisation visible cluster-wide before any remote st.async
   const bool prof = (c == 0);
@@ -599,66 +611,79 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
         const int i = rowi[s], j = lane + 32 * t;
         a[s][t] = (i < B && j < B) ? G[(size_t)i * B + j] + (i == j ? A.ridge : 0.0) : 0.0;
       }
-    // all-gather of block `gb`'s pivot columns of every row: lane L owns the pair
-    // (row slot, column) = (L % 8RS) / 8, L % 8 and 8 of the CL destinations
+    // all-gather of block `gb`'s pivot columns of every row in 16-byte messages
+    // (the receiver's cost is per message): lane L owns the pair (row slot,
+    // column pair) = (L % 4RS) / 4, L % 4 and 4 of the CL destinations
     auto send_block = [&](int gb) {
       const int gk0 = gb * NB, gkb = min(NB, B - gk0), gt0 = gk0 >> 5, gL0 = gk0 & 31;
       double* gcol = S.colK[gb & 1];
-      const int pr = lane % (8 * RS), sp = pr >> 3, q = pr & 7;
-      double val = 0.0;
+      const int pr = lane % (4 * RS), sp = pr >> 2, qp = pr & 3;
+      double v0 = 0.0, v1 = 0.0;
   #pragma unroll
       for (int s = 0; s < RS; ++s) {
-        const double tmp = __shfl_sync(FULL, sel(a[s], gt0), gL0 + q);
-        if (s == sp) val = tmp;
+        const double src = sel(a[s], gt0);
+        const double t0v = __shfl_sync(FULL, src, gL0 + 2 * qp);
+        const double t1v = __shfl_sync(FULL, src, (gL0 + 2 * qp + 1) & 31);
+        if (s == sp) { v0 = t0v; v1 = t1v; }
       }
       const int i = rowi[0] + CL * NW * sp;
-      if (i < B && q < gkb) {
-        const unsigned la = saddr(&gcol[i * NB + q]);
+      if (i < B && 2 * qp < gkb) {
+        const unsigned la = saddr(&gcol[i * NB + 2 * qp]);
         const unsigned mb = saddr(&S.smb[gb & 1]);
-        const int d0 = lane / (8 * RS);
+        const int d0 = lane / (4 * RS);
   #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const unsigned dst = d0 + u * (CL / 8);
-          st_async(mapa(la, dst), val, mapa(mb, dst));
+        for (int u = 0; u < 4; ++u) {
+          const unsigned dst = d0 + u * (8 / RS);
+          st_async2(mapa(la, dst), v0, v1, mapa(mb, dst));
         }
       }
     };
+    // W / Z columns past B stay zero (the update runs branch-free over every slot)
+    for (int x = tid; x < NB * BM; x += NT) {
+      (&S.Wb[0][0])[x] = 0.0;
+      (&S.Zb[0][0])[x] = 0.0;
+    }
     send_block(0);
     for (int k0 = 0, blk = 0; k0 < B; k0 += NB, ++blk) {
       const int kb = min(NB, B - k0), t0 = k0 >> 5, L0 = k0 & 31;
       double* colK = S.colK[blk & 1];
       ACC(5);
       mbar_wait(saddr(&S.smb[blk & 1]), (unsigned)(blk >> 1) & 1u);
-      if (tid == 0 && k0 + 2 * NB < B) mbar_expect(saddr(&S.smb[blk & 1]), (unsigned)(B * min(NB, B - k0 - 2 * NB) * 8));
+      if (tid == 0 && k0 + 2 * NB < B) mbar_expect(saddr(&S.smb[blk & 1]), (unsigned)(B * ((min(NB, B - k0 - 2 * NB) + 1) & ~1) * 8));
       ACC(6);
-      // Cholesky of the kb x kb pivot block by warp 0 (lane L holds entries
-      // (L>>2, 2(L&3)) and (L>>2, 2(L&3)+1); padding = identity)
-      if (w == 0) {
-        const int r = lane >> 2, q0 = 2 * (lane & 3);
-        double e0 = (r < kb && q0 < kb) ? colK[(k0 + r) * NB + q0] : (r == q0 ? 1.0 : 0.0);
-        double e1 = (r < kb && q0 + 1 < kb) ? colK[(k0 + r) * NB + q0 + 1] : (r == q0 + 1 ? 1.0 : 0.0);
-        for (int p = 0; p < kb; ++p) {
-          const double mine = (p & 1) ? e1 : e0;
-          double pp = __shfl_sync(FULL, mine, (p << 2) + (p >> 1));
-          const double rp = __shfl_sync(FULL, mine, (r << 2) + (p >> 1));
-          const double tq0 = __shfl_sync(FULL, mine, (q0 << 2) + (p >> 1));
-          const double tq1 = __shfl_sync(FULL, mine, ((q0 + 1) << 2) + (p >> 1));
-          if (!(pp > 0.0)) {   // not SPD (cannot happen for ridge > 0 in exact arithmetic)
-            if (lane == 0) A.ws.flags[0] = 1.0;
-            pp = 1e-300;
-          }
-          const double lpp = sqrt(pp);
-          const double il = rcp64(lpp);
-          const double lrp = (r == p) ? lpp : (r > p ? rp * il : 0.0);
-          const double lq0 = q0 > p ? tq0 * il : 0.0, lq1 = q0 + 1 > p ? tq1 * il : 0.0;
-          e0 = (q0 == p) ? lrp : (q0 > p ? fma(-lrp, lq0, e0) : e0);
-          e1 = (q0 + 1 == p) ? lrp : (q0 + 1 > p ? fma(-lrp, lq1, e1) : e1);
-          if (lane == 0) S.Lr[p] = il;
-        }
-        S.Lb[r * NB + q0] = (q0 <= r) ? e0 : 0.0;
-        S.Lb[r * NB + q0 + 1] = (q0 + 1 <= r) ? e1 : 0.0;
+      // Cholesky of the kb x kb pivot block, redundantly in every thread's
+      // registers (broadcast reads of the block; padding = identity): no
+      // shuffles on the pivot chain and no barrier before the solves.
+      // Lm = L row-major lower triangle; Li = 1 / L_qq (0 on the padding)
+      double Lm[NB * (NB + 1) / 2], Li[NB];
+  #pragma unroll
+      for (int r = 0; r < NB; ++r) {
+  #pragma unroll
+        for (int q = 0; q <= r; ++q)
+          Lm[r * (r + 1) / 2 + q] = r < kb ? colK[(k0 + r) * NB + q] : (r == q ? 1.0 : 0.0);
       }
-      __syncthreads();
+  #pragma unroll
+      for (int p = 0; p < NB; ++p) {
+        if (p >= kb) {
+          Li[p] = 0.0;
+          continue;
+        }
+        double pp = Lm[p * (p + 1) / 2 + p];
+        if (!(pp > 0.0)) {   // not SPD (cannot happen for ridge > 0 in exact arithmetic)
+          if (tid == 0) A.ws.flags[0] = 1.0;
+          pp = 1e-300;
+        }
+        const double il = rsqrt64(pp);
+        Li[p] = il;
+        Lm[p * (p + 1) / 2 + p] = pp * il;
+  #pragma unroll
+        for (int r = p + 1; r < NB; ++r) Lm[r * (r + 1) / 2 + p] *= il;
+  #pragma unroll
+        for (int r = p + 1; r < NB; ++r)
+  #pragma unroll
+          for (int q = p + 1; q <= r; ++q)
+            Lm[r * (r + 1) / 2 + q] = fma(-Lm[r * (r + 1) / 2 + p], Lm[q * (q + 1) / 2 + p], Lm[r * (r + 1) / 2 + q]);
+      }
       ACC(7);
       // W = L^-1 A_K,j and Z = L^-T W = P^-1 A_K,j for every column j (A_K,j = colK[j]);
       // the last kb tasks form column j of P^-1 from the unit vector e_j
@@ -666,14 +691,24 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
         const bool unit = task >= B;
         const int j = unit ? task - B : task;
         double x[NB];
+        if (unit) {
   #pragma unroll
-        for (int r = 0; r < NB; ++r) x[r] = unit ? (r == j ? 1.0 : 0.0) : (r < kb ? colK[j * NB + r] : 0.0);
+          for (int r = 0; r < NB; ++r) x[r] = r == j ? 1.0 : 0.0;
+        } else {
+          const double2* cj = reinterpret_cast<const double2*>(colK + j * NB);
+  #pragma unroll
+          for (int r = 0; r < NB / 2; ++r) {
+            const double2 t2 = cj[r];
+            x[2 * r] = 2 * r < kb ? t2.x : 0.0;
+            x[2 * r + 1] = 2 * r + 1 < kb ? t2.y : 0.0;
+          }
+        }
   #pragma unroll
         for (int qq = 0; qq < NB; ++qq) {
           double v = x[qq];
   #pragma unroll
-          for (int r = 0; r < qq; ++r) v = fma(-S.Lb[qq * NB + r], x[r], v);
-          x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
+          for (int r = 0; r < qq; ++r) v = fma(-Lm[qq * (qq + 1) / 2 + r], x[r], v);
+          x[qq] = v * Li[qq];
         }
         if (!unit) {
   #pragma unroll
@@ -683,8 +718,8 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
         for (int qq = NB - 1; qq >= 0; --qq) {
           double v = x[qq];
   #pragma unroll
-          for (int r = qq + 1; r < NB; ++r) v = fma(-S.Lb[r * NB + qq], x[r], v);
-          x[qq] = qq < kb ? v * S.Lr[qq] : 0.0;
+          for (int r = qq + 1; r < NB; ++r) v = fma(-Lm[r * (r + 1) / 2 + qq], x[r], v);
+          x[qq] = v * Li[qq];
         }
         if (unit) {
   #pragma unroll
@@ -701,34 +736,34 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
       for (int s = 0; s < RS; ++s)
   #pragma unroll
         for (int r = 0; r < NB; ++r) wi[s][r] = rowi[s] < B ? S.Wb[r][rowi[s]] : 0.0;
+      ACC(15);
+      // trailing update of column slot t (the pivot block's own rows / columns
+      // take Z, Z^T and -P^-1)
       // trailing update of column slot t (the pivot block's own rows / columns
       // take Z, Z^T and -P^-1)
       auto upd = [&](int t) {
         const int j = lane + 32 * t;
-        if (j >= B) return;
         double wj[NB];
   #pragma unroll
-        for (int r = 0; r < NB; ++r) wj[r] = S.Wb[r][j];
+        for (int r = 0; r < NB; ++r) wj[r] = S.Wb[r][j];   // zero past B
+        // branch-free FMA update of the whole slot (padding rows have wi = 0)...
+  #pragma unroll
+        for (int s = 0; s < RS; ++s) {
+          double u = a[s][t];
+  #pragma unroll
+          for (int r = 0; r < NB; ++r) u = fma(-wi[s][r], wj[r], u);
+          a[s][t] = u;
+        }
+        // ...then the pivot block's rows / columns (one warp per CTA holds a
+        // pivot row; the pivot columns are 8 lanes of one slot)
         const int jk = j - k0;
         const bool inj = (unsigned)jk < (unsigned)kb;
   #pragma unroll
         for (int s = 0; s < RS; ++s) {
-          const int i = rowi[s];
-          if (i >= B) continue;
-          const int ik = i - k0;
+          const int i = rowi[s], ik = i - k0;
           const bool ini = (unsigned)ik < (unsigned)kb;
-          if (!ini && !inj) {
-            double u = a[s][t];
-  #pragma unroll
-            for (int r = 0; r < NB; ++r) u = fma(-wi[s][r], wj[r], u);
-            a[s][t] = u;
-          } else if (ini && !inj) {
-            a[s][t] = S.Zb[ik][j];
-          } else if (!ini) {
-            a[s][t] = S.Zb[jk][i];
-          } else {
-            a[s][t] = -S.Pinv[ik * NB + jk];
-          }
+          if (ini || (inj && i < B))
+            a[s][t] = ini ? (inj ? -S.Pinv[ik * NB + jk] : S.Zb[ik][j]) : S.Zb[jk][i];
         }
       };
       // look-ahead: the slot holding the next block's pivot columns first, then
@@ -740,6 +775,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
           if (t == nt0) upd(t);
         send_block(blk + 1);
       }
+      ACC(18);
   #pragma unroll
       for (int t = 0; t < CS; ++t)
         if (nk0 >= B || t != nt0) upd(t);

@@ -23,6 +23,6 @@ hy._lib.lib().hyde_debug_eig_clocks(clk)
 print(name, "B=%d K=%d: K2 %.1f us per call (CUDA events)" % (b, k, e0.elapsed_time(e1) / 10 * 1e3))
 for nm, a, bb in [("sweep (sigma)", 0, 1), ("whiten+tridiag", 1, 2), ("eigenpairs", 2, 3), ("vectors", 3, 4)]:
     print("  %-24s %9d cycles (%.1f us)" % (nm, clk[bb] - clk[a], (clk[bb] - clk[a]) / 1.965e3))
-for nm, i in [("sweep gather", 5), ("sweep cl_sync", 6), ("sweep Pinv", 7), ("sweep Z", 8), ("sweep update", 9),
+for nm, i in [("sweep gather", 5), ("sweep cl_sync", 6), ("sweep Pinv", 7), ("sweep Z", 8), ("sweep wi loads", 15), ("sweep upd+send next", 18), ("sweep update rest", 9),
               ("tri symv+send", 10), ("tri Q update", 11), ("tri wait", 12), ("tri update", 13), ("tri reflector", 14), ("bisection", 16), ("inverse iteration", 17)]:
     print("  %-24s %9d cycles" % (nm, clk[i]))
