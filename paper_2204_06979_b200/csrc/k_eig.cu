@@ -251,9 +251,12 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
 }
 
 // Eigenvalue with ascending index `asc` of the pre-scaled T (interval [glo,
-// ghi] in scaled units) by NT-section; all threads end with the same (lo, hi).
+// ghi] in scaled units) by NP-section; all threads end with the same (lo, hi).
+// NP = 128 of the NT threads: a pass is then bound by the Sturm recurrence's
+// dependent FMA chain, not the SM's fp64 throughput (256 sections: 7 passes
+// of 256 x B x ~3.5 fp64 operations; 128 sections: 8 latency-bound passes).
 __device__ double bisect_one(const double* d, const double* e2, int n, double glo, double ghi, int asc, int* qsh) {
-  constexpr int NP = NT;
+  constexpr int NP = 128;
   const double range = fmax(ghi - glo, 1e-300);
   const double tol = 4.0 * 2.220446049250313e-16 * fmax(fabs(glo), fabs(ghi)) + 1e-300;
   // (NP + 1)^iters >= range / tol: the final interval is within tol (at
@@ -265,7 +268,8 @@ __device__ double bisect_one(const double* d, const double* e2, int n, double gl
   const int t = threadIdx.x;
   for (int it = 0; it < iters; ++it) {
     const double h = (hi - lo) / (double)(NP + 1);
-    int q = sturm_count(d, e2, n, lo + h * (double)(t + 1)) > asc ? t : NP;
+    int q = NP;
+    if (t < NP) q = sturm_count(d, e2, n, lo + h * (double)(t + 1)) > asc ? t : NP;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) q = min(q, __shfl_xor_sync(FULL, q, o));
     if ((t & 31) == 0) qsh[t >> 5] = q;

@@ -161,9 +161,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const int nreg = B > 128 ? 2 : 1;
   const int slice_bytes = P.rows_tot * KC;
   const int stage_bytes = 2 * slice_bytes;
+  // Pixel tiles of KC.  TMA feed: tiles are dealt to the pairs cyclically
+  // (tile s * npairs + pair), so the pass ends on the LAST pixels of the cube
+  // -- a contiguous ~L2-sized tail that K3 (which walks the cube backwards)
+  // then reads from L2.  Register feed: one contiguous range per pair.  (The
+  // per-pair partials are exact integers: G does not depend on the split.)
   const long long p_begin = (long long)pair * P.per_pair;
   const long long p_end = min(P.n, p_begin + P.per_pair);
-  const int nst = p_end > p_begin ? (int)((p_end - p_begin + KC - 1) / KC) : 0;
+  const int npairs = (int)(gridDim.x >> 1);
+  const long long ntiles = (P.n + KC - 1) / KC;
+  const int nst = TMA ? (pair < ntiles ? (int)((ntiles - 1 - pair) / npairs + 1) : 0)
+                      : (p_end > p_begin ? (int)((p_end - p_begin + KC - 1) / KC) : 0);
+  // absolute first pixel of stage s and the pixel limit of this pair
+  auto tile_px = [&](int s) -> long long {
+    return TMA ? ((long long)s * npairs + pair) * KC : p_begin + (long long)s * KC;
+  };
+  const long long px_lim = TMA ? P.n : p_end;
 
   // per-band quantisation scales of the rows this SM handles
   for (int i = threadIdx.x; i < 2 * 64; i += NTHREADS) {
@@ -271,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (s >= NF) tc::mbar_wait(&f_empty[fs], (uint32_t)(((s / NF) - 1) & 1));
         tc::mbar_expect_tx(&f_full[fs], bytes);
         unsigned char* dst = fring + fs * FSTAGE;
-        const int x = (int)(p_begin + (long long)s * KC);
+        const int x = (int)tile_px(s);
         tma_load_2d(dst, &tmP, x, rank * 64, &f_full[fs]);
         if (nreg == 2) tma_load_2d(dst + 64 * KC * 4, &tmQ, x, 128 + rank * hb, &f_full[fs]);
       }
@@ -360,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     // 2 IDP4A + IMAD (sum of v); the clip atomics run once per stage, rarely.
     auto convert = [&](auto full_tag, int s, const float4 (&v)[MAXU], unsigned char* st0, unsigned char* st1) {
       constexpr bool FULL = decltype(full_tag)::value;
-      const long long sh = (long long)s * KC + 4 * lane;   // first pixel of this lane, within the pair
+      const long long sh = tile_px(s) + 4 * lane;   // absolute first pixel of this lane
       unsigned acc0 = 0u, acc1 = 0u, acc2 = 0u, acc3 = 0u;   // OR of (bits ^ 0x4B000000) per pixel
 #pragma unroll
       for (int t = 0; t < MAXU; ++t) {
@@ -371,10 +384,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         unsigned r2 = __float_as_uint(fmaf(v[t].z, isc[t], kf));
         unsigned r3 = __float_as_uint(fmaf(v[t].w, isc[t], kf));
         if (!FULL) {   // ragged tail: pixels past the pair's end are v = 0 (u = 32768)
-          r0 = sh + 0 < n_end ? r0 : 0x4B008000u;
-          r1 = sh + 1 < n_end ? r1 : 0x4B008000u;
-          r2 = sh + 2 < n_end ? r2 : 0x4B008000u;
-          r3 = sh + 3 < n_end ? r3 : 0x4B008000u;
+          r0 = sh + 0 < px_lim ? r0 : 0x4B008000u;
+          r1 = sh + 1 < px_lim ? r1 : 0x4B008000u;
+          r2 = sh + 2 < px_lim ? r2 : 0x4B008000u;
+          r3 = sh + 3 < px_lim ? r3 : 0x4B008000u;
         }
         acc0 |= r0 ^ 0x4B000000u;
         acc1 |= r1 ^ 0x4B000000u;
@@ -392,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
         for (int j = 0; j < 4; ++j)
           if ((pm >> j) & 1u) {
-            const long long px = p_begin + sh + j;
+            const long long px = sh + j;
             atomicOr(P.bitmap + (px >> 5), 1u << (px & 31));
           }
       }
@@ -402,7 +415,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       tc::mbar_wait(&bar_empty[is], (uint32_t)(((s / NI) & 1) ^ 1));   // local barrier (commit multicast)
       unsigned char* st0 = smem + is * stage_bytes;
       unsigned char* st1 = st0 + slice_bytes;
-      if ((long long)s * KC + KC <= n_end)
+      if (tile_px(s) + KC <= px_lim)
         convert(std::true_type{}, s, v, st0, st1);
       else
         convert(std::false_type{}, s, v, st0, st1);

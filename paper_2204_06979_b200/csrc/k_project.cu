@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
     Ws[i] = (k < ncomp) ? W[(size_t)b * ldw + k] : 0.f;
   }
   __syncthreads();
-  const long long p0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * PIX;
+  // blocks walk the cube from its END: K1's pass finishes on the last pixels,
+  // which are still in L2 when this kernel starts
+  const long long p0 = ((long long)(gridDim.x - 1 - blockIdx.x) * blockDim.x + threadIdx.x) * PIX;
   if (p0 >= n) return;
   float acc[NC][PIX];
 #pragma unroll
