@@ -402,6 +402,93 @@ __device__ void inv_iter(const double* d, const double* e, int n, double lam, do
   }
 }
 
+// Eigenvector of T for the (bisection-accurate) eigenvalue lam by a twisted
+// factorisation, called by one full warp.  Lanes 0 and 1 run the two
+// independent recurrences in lockstep (one instruction stream, per-lane
+// indices):
+//   top-down    T - lam I = L+ D+ L+^T:  D+_0 = d_0 - lam,
+//               l_i = e_i / D+_i,  D+_{i+1} = (d_{i+1} - lam) - l_i e_i;
+//   bottom-up   T - lam I = U- D- U-^T:  D-_{n-1} = d_{n-1} - lam,
+//               u_i = e_{i-1} / D-_i,  D-_{i-1} = (d_{i-1} - lam) - u_i e_{i-1};
+// gamma_r = D+_r + D-_r - (d_r - lam); at the twist index r = argmin |gamma_r|
+// (lowest index on ties) z_r = 1, z_i = -l_i z_{i+1} above it and
+// z_i = -u_i z_{i-1} below it (two more lockstep chains), then z / ||z||.
+// This is the vector one inverse-iteration step from the best unit start
+// vector e_r would give ((T - lam I) z = gamma_r e_r), without the pivoted
+// LU's long per-step chain.  Pivots below tnorm * eps are moved to +-tiny.
+__device__ void twisted_vec(const double* d, const double* e, int n, double lam, double tnorm, double* x,
+                            double* dp, double* dm, double* lp, double* um) {
+  const int lane = threadIdx.x & 31;
+  const double tiny = tnorm > 0.0 ? 2.220446049250313e-16 * tnorm : 1e-300;
+  if (lane < 2) {
+    const bool fw = lane == 0;
+    double* D = fw ? dp : dm;
+    double* M = fw ? lp : um;
+    int cur = fw ? 0 : n - 1;
+    double Dc = d[cur] - lam;
+    if (fabs(Dc) < tiny) Dc = Dc < 0.0 ? -tiny : tiny;
+    D[cur] = Dc;
+#pragma unroll 4
+    for (int i = 0; i < n - 1; ++i) {
+      const int nx = fw ? i + 1 : n - 2 - i;   // next diagonal index
+      const int ei = fw ? i : n - 2 - i;       // the coupling e between cur and nx
+      const double ev = e[ei];
+      const double m = ev * rcp64(Dc);
+      M[ei] = m;                               // l_i (top-down) or u_{i+1} (bottom-up)
+      double Dn = fma(-m, ev, d[nx] - lam);
+      if (fabs(Dn) < tiny) Dn = Dn < 0.0 ? -tiny : tiny;
+      D[nx] = Dn;
+      Dc = Dn;
+    }
+  }
+  __syncwarp();
+  // twist index: smallest |gamma_r|, lowest r on ties
+  double best = INFINITY;
+  int br = 0x7fffffff;
+  for (int r = lane; r < n; r += 32) {
+    const double g = fabs(dp[r] + dm[r] - (d[r] - lam));
+    if (g < best) { best = g; br = r; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(FULL, best, o);
+    const int orr = __shfl_xor_sync(FULL, br, o);
+    if (ob < best || (ob == best && orr < br)) { best = ob; br = orr; }
+  }
+  const int r = br;
+  if (lane < 2) {
+    const bool up = lane == 0;
+    const int len = up ? r : n - 1 - r;
+    double z = 1.0;
+    if (up) x[r] = 1.0;
+#pragma unroll 4
+    for (int i = 0; i < len; ++i) {
+      const int idx = up ? r - 1 - i : r + 1 + i;
+      const double m = up ? lp[idx] : um[idx - 1];
+      z = -m * z;
+      x[idx] = z;
+    }
+  }
+  __syncwarp();
+  double mx = 0.0;
+  for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(x[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  mx = 1.0 / mx;
+  double ss = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double v = x[i] * mx;
+    ss = fma(v, v, ss);
+  }
+  ss = 1.0 / sqrt(warp_sum(ss));
+  const double f = mx * ss;
+  for (int i = lane; i < n; i += 32) x[i] *= f;
+  __syncwarp();
+}
+
+__constant__ int c_eig_vec_mode;   // 0: twisted factorisation; 1: pivoted-LU inverse iteration (experiments)
+__device__ __forceinline__ bool use_twisted() { return c_eig_vec_mode == 0; }
+
 // Gershgorin interval of T and e2 = e^2 (NT threads; d, e, e2 in shared memory)
 __device__ void tri_bounds(const double* d, const double* e, double* e2, int B, double* red, double& glo,
                            double& ghi) {
@@ -997,7 +1084,10 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
     tc = clock64();
     const double lam = bisect_one(S.ds, S.e2s, B, glo * tsc, ghi * tsc, B - 1 - kd, S.qsh) / tsc;
     ACC(16);
-    if (w == 0) inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
+    if (w == 0) {
+      if (use_twisted()) twisted_vec(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml);
+      else inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
+    }
     __syncthreads();
     ACC(17);
     for (int j = tid; j < B; j += NT) st_all<CL>(&S.zb[kd][j], S.y[j]);
@@ -1131,7 +1221,10 @@ __global__ void __launch_bounds__(NT) more_pairs_kernel(const double* __restrict
     return;
   }
   const double tnorm = fmax(fabs(glo), fabs(ghi));
-  if (tid < 32) inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
+  if (tid < 32) {
+    if (use_twisted()) twisted_vec(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml);
+    else inv_iter(S.d, S.e, B, lam, tnorm, S.y, S.dd, S.u1, S.u2, S.ml, S.piv, (unsigned)kd);
+  }
   if (tid == 0) {
     ws.lam_top[kd] = lam;
     if (lam_out) lam_out[kd] = lam;
@@ -1267,8 +1360,22 @@ bool cluster_fits() {
   return n >= 1;
 }
 
+// HYDE_EIG_INVITER=1 (experiments): eigenvectors by the pivoted-LU inverse
+// iteration instead of the twisted factorisation
+static void eig_vec_mode_once() {
+  static const int once = [] {
+    if (getenv("HYDE_EIG_INVITER")) {
+      const int one = 1;
+      cudaMemcpyToSymbol(c_eig_vec_mode, &one, sizeof(int));
+    }
+    return 0;
+  }();
+  (void)once;
+}
+
 template <int CL>
 cudaError_t launch_k2(const K2Args& a, cudaStream_t st) {
+  eig_vec_mode_once();
   cudaError_t e = prepare_k2<CL>();
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[2];
@@ -1278,6 +1385,7 @@ cudaError_t launch_k2(const K2Args& a, cudaStream_t st) {
 
 template <int CL>
 cudaError_t launch_k2_batched(const K2Args* dargs, int nb, cudaStream_t st) {
+  eig_vec_mode_once();
   cudaError_t e = prepare_k2<CL, true>();
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[2];
@@ -1450,6 +1558,7 @@ cudaError_t launch_eig_values(const double* tri, const double* house, int B, dou
 // launch_eig_raw): eigenvalues into lam[k], vectors into column k of V (ldv)
 cudaError_t launch_eig_more_raw(const double* tri, const double* house, const double* ones, int B, int k0, int K,
                                 double* lam, double* V, int ldv, float* W, float* U, int ldwu, cudaStream_t st) {
+  eig_vec_mode_once();
   const EigWs ws = carve(const_cast<double*>(house), B);
   return run_more(tri, ws, ones, B, k0, K, lam, V + k0, ldv, W, U, ldwu, st);
 }
@@ -1457,6 +1566,7 @@ cudaError_t launch_eig_more_raw(const double* tri, const double* house, const do
 cudaError_t launch_eigvec_more(const double* tri, const double* house, const double* sigma, int B, int k0,
                                int ncomp, double* lam_top_unused, double* V, float* W, float* U, int ldwu,
                                cudaStream_t st) {
+  eig_vec_mode_once();
   (void)lam_top_unused;
   const EigWs ws = carve(const_cast<double*>(house), B);
   return run_more(tri, ws, sigma, B, k0, ncomp, nullptr, V, ncomp, W, U, ldwu, st);
