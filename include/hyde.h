@@ -378,7 +378,13 @@ long long hyde_launch_count(hyde_handle h);
  * [5..17] hold per-segment accumulators (sweep gather / exchange / pivot
  * Cholesky / solves / update; column symv+send / Q update / wait / update /
  * reflector; bisection; inverse iteration).  Copies 32 values; synchronizes. */
-hyde_status hyde_debug_eig_clocks(long long* out32);
+hyde_status hyde_debug_eig_clocks(long long* out40);
+/* Test hook for K2's first chunk: enable = 0 runs the Householder path (phase
+ * 2 + 3) instead of the Lanczos phase 2L; max_steps > 0 caps the Lanczos steps
+ * (a cap below convergence exercises the in-kernel fallback).  Process-wide;
+ * the default is enable = 1 (HYDE_EIG_LANCZOS=0 in the environment: 0),
+ * max_steps = 0 (no cap).  Always HYDE_OK. */
+hyde_status hyde_debug_eig_lanczos(int enable, int max_steps);
 
 /* K5 phase profile of the SURE launches since the last call (builds with
  * HYDE_SURE_PROF=1 only; returns 0 and zeros otherwise, 1 when filled):

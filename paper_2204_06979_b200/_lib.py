@@ -111,6 +111,7 @@ _SIGS = {
     "hyde_profile_read": (c_int, [c_void_p, POINTER(c_double), POINTER(ctypes.c_longlong)]),
     "hyde_launch_count": (ctypes.c_longlong, [c_void_p]),
     "hyde_debug_eig_clocks": (c_int, [POINTER(ctypes.c_longlong)]),
+    "hyde_debug_eig_lanczos": (c_int, [c_int, c_int]),
     "hyde_eig_cluster_size": (c_int, []),
     "hyde_debug_sure_prof": (c_int, [POINTER(ctypes.c_ulonglong)]),
     "hyde_debug_eig_state": (c_int, [c_void_p, c_int, c_int, _P, _P]),

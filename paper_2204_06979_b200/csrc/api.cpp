@@ -485,9 +485,10 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   {
     Stage sg(h, HYDE_STAGE_EIG, 1, st);
     CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st,
-                        h->eig_cl));
+                        h->eig_cl, EIG_LANCZOS));
     sg.end();
   }
+  const bool lanczos = first < B && eig_lanczos_enabled();
   int rank = 0, chunks = 0;
   int k0 = 0, comps = 0;
   for (int c = 0;; ++c) {
@@ -497,6 +498,11 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
       s = ensure_ebuf(h, (size_t)(k0 + cnt) * L.ldE * 4, (size_t)k0 * L.ldE * 4, st);
       if (s != HYDE_OK) return s;
       Stage sg(h, HYDE_STAGE_EIG, 1, st);
+      // the first chunk may have come from Lanczos (no T, Q): form them now,
+      // keeping the first chunk's W / U
+      if (c == 1 && lanczos)
+        CK(launch_noise_eig(G, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st,
+                            h->eig_cl, EIG_RETRI));
       CK(launch_eigvec_more(tri, house, sigma, B, k0, cnt, nullptr, nullptr, W, U, L.ldwu, st));
       sg.end();
     }

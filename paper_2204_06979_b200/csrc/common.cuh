@@ -104,7 +104,12 @@ int gram_tc_fix_splits();
 size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,
-                             double* tri, float* W, float* U, int ldwu, cudaStream_t st, int cl_pref = 0);
+                             double* tri, float* W, float* U, int ldwu, cudaStream_t st, int cl_pref = 0,
+                             int mode = 0);
+// launch_noise_eig modes: the first chunk by Lanczos when it converges (T and Q
+// then absent); the tridiagonal rerun (sigma given, W/U of the first ncomp kept)
+enum { EIG_HOUSEHOLDER = 0, EIG_LANCZOS = 1, EIG_RETRI = 2 };
+bool eig_lanczos_enabled();
 size_t eig_args_bytes();
 double* eig_flags_ptr(double* house, int B);
 cudaError_t launch_noise_eig_batched(int nb, const double* const* G, long long n, int B, double ridge, int ncomp,

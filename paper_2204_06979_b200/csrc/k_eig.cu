@@ -62,7 +62,7 @@ constexpr int CLMAX = 16;
 // clock64() stamps (diagnostics, hyde_debug_eig_clocks; CTA 0 of the cluster):
 // [0] start [1] sweep done [2] tridiagonalisation done [3] eigenpairs done
 // [4] vectors written; [5..] per-segment accumulators
-__device__ long long g_eig_clk[32];
+__device__ long long g_eig_clk[40];
 __device__ __forceinline__ void stamp(int i) {
   if (threadIdx.x == 0) g_eig_clk[i] = clock64();
 }
@@ -455,7 +455,7 @@ __device__ void twisted_vec(const double* d, const double* e, int n, double lam,
     const int orr = __shfl_xor_sync(FULL, br, o);
     if (ob < best || (ob == best && orr < br)) { best = ob; br = orr; }
   }
-  const int r = br;
+  const int r = br < n ? br : 0;   // every gamma NaN (non-finite input): any index, no out-of-range store
   if (lane < 2) {
     const bool up = lane == 0;
     const int len = up ? r : n - 1 - r;
@@ -474,16 +474,111 @@ __device__ void twisted_vec(const double* d, const double* e, int n, double lam,
   for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(x[i]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
-  mx = 1.0 / mx;
+  mx = rcp64(mx);   // mx >= 1 (z_r = 1)
   double ss = 0.0;
   for (int i = lane; i < n; i += 32) {
     const double v = x[i] * mx;
     ss = fma(v, v, ss);
   }
-  ss = 1.0 / sqrt(warp_sum(ss));
+  ss = rsqrt64(warp_sum(ss));
   const double f = mx * ss;
   for (int i = lane; i < n; i += 32) x[i] *= f;
   __syncwarp();
+}
+
+// twisted_vec with the pivot recurrences in product (Sturm) form: lanes 0 / 1
+// run p_{i+1} = (d_{i+1} - lam) p_i - e_i^2 p_{i-1} (top-down) and the mirror
+// q recurrence (bottom-up) -- ONE dependent FMA per step -- while the pivots
+// D_{i+1} = p_{i+1} / p_i and multipliers l_i = e_i p_{i-1} / p_i (the same
+// quantities twisted_vec forms by a reciprocal on its chain) are side
+// products off the chain.  Consecutive p share a power-of-two rescale every 8
+// steps (ratios unchanged).  The twist and the two outward solves are as in
+// twisted_vec.  Used by phase 2L (its residual checks run this per Ritz pair).
+__device__ void twisted_prod(const double* __restrict__ d, const double* __restrict__ e, int n, double lam,
+                             double* __restrict__ x, double* __restrict__ dp, double* __restrict__ dm,
+                             double* __restrict__ lp, double* __restrict__ um) {
+  const int lane = threadIdx.x & 31;
+  if (lane < 2) {
+    const bool fw = lane == 0;
+    double* D = fw ? dp : dm;
+    double* M = fw ? lp : um;
+    const int cur = fw ? 0 : n - 1;
+    double pa = 1.0, pb = d[cur] - lam;
+    if (pb == 0.0) pb = 1e-300;
+    D[cur] = pb;
+    for (int i = 0; i < n - 1; ++i) {
+      const int nx = fw ? i + 1 : n - 2 - i;
+      const int ei = fw ? i : n - 2 - i;
+      const double ev = e[ei];
+      double pn = fma(d[nx] - lam, pb, -(ev * ev) * pa);
+      if (pn == 0.0) pn = 1e-300;
+      const double r = rcp64(pb);
+      M[ei] = ev * pa * r;
+      D[nx] = pn * r;
+      pa = pb;
+      pb = pn;
+      if ((i & 7) == 7) {
+        const double mx = fmax(fabs(pa), fabs(pb));
+        const double sc = mx > 0x1p+400 ? 0x1p-400 : (mx < 0x1p-400 ? 0x1p+400 : 1.0);
+        pa *= sc;
+        pb *= sc;
+      }
+    }
+  }
+  __syncwarp();
+  double best = INFINITY;
+  int br = 0x7fffffff;
+  for (int r = lane; r < n; r += 32) {
+    const double g = fabs(dp[r] + dm[r] - (d[r] - lam));
+    if (g < best) { best = g; br = r; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(FULL, best, o);
+    const int orr = __shfl_xor_sync(FULL, br, o);
+    if (ob < best || (ob == best && orr < br)) { best = ob; br = orr; }
+  }
+  const int r = br < n ? br : 0;
+  if (lane < 2) {
+    const bool up = lane == 0;
+    const int len = up ? r : n - 1 - r;
+    double z = 1.0;
+    if (up) x[r] = 1.0;
+    for (int i = 0; i < len; ++i) {
+      const int idx = up ? r - 1 - i : r + 1 + i;
+      z = -(up ? lp[idx] : um[idx - 1]) * z;
+      x[idx] = z;
+    }
+  }
+  __syncwarp();
+  double mx = 0.0;
+  for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(x[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  mx = rcp64(mx);
+  double ss = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double v = x[i] * mx;
+    ss = fma(v, v, ss);
+  }
+  const double f = mx * rsqrt64(warp_sum(ss));
+  for (int i = lane; i < n; i += 32) x[i] *= f;
+  __syncwarp();
+}
+
+// Rayleigh-quotient correction z^T (T - lam I) z / z^T z for a vector z of
+// the tridiagonal T (one warp; every lane returns the same value)
+__device__ double rayleigh_corr(const double* d, const double* e, int n, double lam, const double* z) {
+  const int lane = threadIdx.x & 31;
+  double num = 0.0, den = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    double r = (d[i] - lam) * z[i];
+    if (i > 0) r = fma(e[i - 1], z[i - 1], r);
+    if (i < n - 1) r = fma(e[i], z[i + 1], r);
+    num = fma(z[i], r, num);
+    den = fma(z[i], z[i], den);
+  }
+  return warp_sum(num) / warp_sum(den);
 }
 
 __constant__ int c_eig_vec_mode;   // 0: twisted factorisation; 1: pivoted-LU inverse iteration (experiments)
@@ -555,18 +650,25 @@ struct K2Args {
   float* W;
   float* U;
   int ldwu;
+  int lanczos;     // 1: the first K pairs by Lanczos (phase 2L); T and Q are then NOT written
+  int skip_sweep;  // 1: sigma is read from A.sigma (no phase 1) -- the tridiagonal rerun after phase 2L
+  int kw0;         // phase 3 writes W / U / V only for pairs k >= kw0 (the rerun keeps the first chunk's)
+  int lzmax;       // > 0: at most this many Lanczos steps (tests force the fallback)
 };
 
 struct K2Smem {
   unsigned long long mbar[2];   // tridiagonalisation exchange, one per column parity
   unsigned long long smb[2];    // sweep exchange, one per block parity
+  unsigned long long lmb[2];    // Lanczos exchange, one per step parity
   double2 px[2][BM];       // {p = beta A v, column k+2 entry} per row, all-gathered
                            // (double-buffered by column parity; one 16-byte message per row and peer)
+                           // phase 2L: y = A v_m all-gathered (double-buffered by step parity)
+  double Pinv[NB * NB];
+  double sig[BM];
+  // colK .. cw are contiguous: phase 2L keeps its Lanczos basis there (LVD doubles)
   double colK[2][BM * NB]; // sweep: pivot-block columns of every row (double-buffered by block)
   double Wb[NB][BM];       // sweep: L^-1 A_K,:
   double Zb[NB][BM];       // sweep: P^-1 A_K,:
-  double Pinv[NB * NB];
-  double sig[BM];
   double vw[NW][BM];       // per-warp copy of the current reflector vector
   double cw[NW][BM];       // per-warp copy of the column being reduced
   double d[BM], e[BM], e2[BM];
@@ -577,11 +679,96 @@ struct K2Smem {
   double am[CLMAX][KM];    // sign reduction: max |V_ik| per CTA
   double av[CLMAX][KM];    //                 the entry itself
   int ai[CLMAX][KM];       //                 its lowest row index
-  double dd[BM], u1[BM], u2[BM], ml[BM], y[BM];
+  __align__(16) double dd[BM];
+  __align__(16) double u1[BM];
+  __align__(16) double u2[BM];
+  double ml[BM], y[BM];
   unsigned char piv[BM];
   double red[4 * NW];
   int qsh[NW];
+  int lok[NW];             // phase 2L: Ritz pair w converged
 };
+// phase 2L basis: colK .. cw (see K2Smem)
+constexpr int LVD = 2 * BM * NB + 2 * NB * BM + 2 * NW * BM;
+constexpr int LZK = 6;     // phase 2L serves first chunks of at most LZK pairs (zb rows: K vectors + 4K scratch)
+static_assert(8 + 4 * LZK <= KM, "phase 2L scratch rows");
+
+// Two Sturm counts at once (independent chains interleaved: the dependent
+// FMA latency of one hides the other's); same arithmetic as sturm_count.
+__device__ __forceinline__ void sturm_count2(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                                             double x0, double x1, int& c0, int& c1) {
+  double a0 = 1.0, b0 = d[0] - x0, a1 = 1.0, b1 = d[0] - x1;
+  c0 = (int)((unsigned)__double2hiint(b0) >> 31);
+  c1 = (int)((unsigned)__double2hiint(b1) >> 31);
+  int i = 1;
+  for (; i + 7 < n; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double dv = d[i + u], ev = e2[i + u - 1];
+      const double t0 = fma(dv - x0, b0, -ev * a0);
+      const double t1 = fma(dv - x1, b1, -ev * a1);
+      c0 += (int)((unsigned)(__double2hiint(t0) ^ __double2hiint(b0)) >> 31);
+      c1 += (int)((unsigned)(__double2hiint(t1) ^ __double2hiint(b1)) >> 31);
+      a0 = b0; b0 = t0;
+      a1 = b1; b1 = t1;
+    }
+    const double m0 = fmax(fabs(a0), fabs(b0)), m1 = fmax(fabs(a1), fabs(b1));
+    const double s0 = m0 > 0x1p+500 ? 0x1p-500 : (m0 < 0x1p-500 ? 0x1p+500 : 1.0);
+    const double s1 = m1 > 0x1p+500 ? 0x1p-500 : (m1 < 0x1p-500 ? 0x1p+500 : 1.0);
+    a0 *= s0; b0 *= s0;
+    a1 *= s1; b1 *= s1;
+  }
+  for (; i < n; ++i) {
+    const double dv = d[i], ev = e2[i - 1];
+    const double t0 = fma(dv - x0, b0, -ev * a0);
+    const double t1 = fma(dv - x1, b1, -ev * a1);
+    c0 += (int)((unsigned)(__double2hiint(t0) ^ __double2hiint(b0)) >> 31);
+    c1 += (int)((unsigned)(__double2hiint(t1) ^ __double2hiint(b1)) >> 31);
+    a0 = b0; b0 = t0;
+    a1 = b1; b1 = t1;
+  }
+}
+
+// NP = 64-section bisection by one warp (two points per lane; all lanes end
+// with the same bracket): the eigenvalue with ascending index asc of the
+// pre-scaled T inside [lo, hi], narrowed until hi - lo <= tolabs.  The K
+// Ritz values of phase 2L run on K warps at once.
+__device__ void bisect_warp(const double* d, const double* e2, int n, double& lo, double& hi, int asc,
+                            double tolabs) {
+  const int l = threadIdx.x & 31;
+  const double range = fmax(hi - lo, 1e-300);
+  int iters = (int)ceil(log2(range / fmax(tolabs, 1e-300)) / 6.022367813028454);   // log2(65)
+  iters = iters < 1 ? 1 : (iters > 64 ? 64 : iters);
+  for (int it = 0; it < iters; ++it) {
+    const double h = (hi - lo) * (1.0 / 65.0);
+    int c0, c1;
+    sturm_count2(d, e2, n, lo + h * (double)(2 * l + 1), lo + h * (double)(2 * l + 2), c0, c1);
+    const unsigned m0 = __ballot_sync(FULL, c0 > asc), m1 = __ballot_sync(FULL, c1 > asc);
+    // point p = 2 l + 1 + s sits at lo + h p; the target lies in (x_{q-1}, x_q]
+    // for the first point q with count > asc (the count is monotone)
+    const int q0 = m0 ? 2 * (__ffs(m0) - 1) + 1 : 65;
+    const int q1 = m1 ? 2 * (__ffs(m1) - 1) + 2 : 65;
+    const int q = min(q0, q1);
+    const double nlo = q > 1 ? lo + h * (double)(q - 1) : lo;
+    const double nhi = q < 65 ? lo + h * (double)q : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+}
+
+// deterministic block sum (fixed order; identical bits in every CTA of the
+// cluster for identical inputs), broadcast to every thread
+__device__ __forceinline__ double blk_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double t = red[0];
+#pragma unroll
+  for (int q = 1; q < NW; ++q) t += red[q];
+  __syncthreads();
+  return t;
+}
 
 // Householder reflector from column kk (lane-distributed in col[], rows j >
 // kk used): H = I - beta v v^T with H x = alpha e_1 on rows kk+1.. (LAPACK
@@ -646,6 +833,315 @@ __device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, 
   }
 }
 
+// ================= phase 2L: the first chunk's eigenpairs by Lanczos =================
+// The rank rule (A5) visits the leading components first, and the first chunk
+// (K <= LZK pairs) decides the rank on every BASELINE workload.  Those pairs
+// are extremal and separated from the Marchenko-Pastur bulk of the whitened
+// noise, so a Lanczos process on G_w converges to them in tens of steps
+// (22-25 at `large`, against the B = 224 dependent columns of the Householder
+// reduction).  Step m:
+//   y = G_w v_m                    (the owners' rows, all-gathered: ONE
+//                                   8-byte message per row and peer)
+//   y -= V h, h = V^T y  (twice)   (full re-orthogonalisation, classical
+//                                   Gram-Schmidt applied twice, against
+//                                   v_0 .. v_m; alpha_m = h_m + h'_m)
+//   beta_m = ||y||, v_{m+1} = y / beta_m
+// Everything after the all-gather runs REDUNDANTLY in every CTA on identical
+// data in a fixed order, so every CTA holds the same basis and takes the same
+// branches with no further exchange.  Every 4 steps the K largest Ritz values
+// of T_m (warp k: 32-section bisection on its Sturm counts) and their T_m
+// eigenvectors z_k (twisted factorisation) give the residuals
+// ||G_w x_k - theta_k x_k|| = beta_m |z_k[m-1]|; when all K are below
+// LZ_TOL theta_k the pairs are x_k = V z_k (normalised, D6 sign fix).  A
+// breakdown (beta ~ 0 before convergence) or LVD / B steps without
+// convergence returns false: the caller runs the Householder path (phase 2)
+// as before.  T_B at m = B is the whole space: converged by construction.
+constexpr double LZ_TOL = 1e-14;
+
+template <int CL, int RS>
+__device__ bool lanczos_top(const K2Args& A, K2Smem& S, const int (&rowi)[RS], double (&a)[RS][CS], int c) {
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int B = A.B, K = A.K;
+  const double* __restrict__ G = A.G;
+  double* LV = &S.colK[0][0];
+  const int ldv = (B + 1) & ~1;                  // 16-byte rows; the odd-B pad entry stays 0
+  const int mmax = min(A.lzmax > 0 ? A.lzmax : B, min(B, LVD / ldv - 1));
+  const double invn = 1.0 / (double)A.n;
+#pragma unroll
+  for (int s = 0; s < RS; ++s)
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int i = rowi[s], j = lane + 32 * t;
+      a[s][t] = (i < B && j < B) ? G[(size_t)i * B + j] / (S.sig[i] * S.sig[j]) * invn : 0.0;
+    }
+  double* ly0 = reinterpret_cast<double*>(&S.px[0][0]);   // ly[par] = ly0 + par * 2 BM
+  double* hb = S.dd;    // h  = V^T y
+  double* h2 = S.u1;    // h' = V^T (y - V h)
+  double* yb = S.u2;    // y after the first pass
+  const int i = tid;
+  const bool own = i < B;
+  if (i == B && (B & 1)) {   // pad entries of the 16-byte paired loads
+    ly0[B] = 0.0;
+    ly0[2 * BM + B] = 0.0;
+    yb[B] = 0.0;
+  }
+  // start vector: 1 + u_i, u_i in [0, 1) from an integer hash of i (generic:
+  // no leading eigenvector of a real covariance is orthogonal to it)
+  double yi = 0.0;
+  if (own) {
+    unsigned hsh = (unsigned)i * 2654435761u;
+    hsh ^= hsh >> 15;
+    hsh *= 2246822519u;
+    hsh ^= hsh >> 13;
+    yi = 1.0 + (double)(hsh >> 8) * 0x1p-24;
+  }
+  {
+    const double nr = blk_sum(yi * yi, S.red);
+    if (own) LV[i] = yi / sqrt(nr);
+    if (i == B && (B & 1)) LV[i] = 0.0;
+  }
+  if (tid == 0) {
+    mbar_expect(saddr(&S.lmb[0]), 8u * (unsigned)B);
+    mbar_expect(saddr(&S.lmb[1]), 8u * (unsigned)B);
+  }
+  __syncthreads();
+  const int sv = lane / CL, peer = lane % CL;   // 32 / RS = CL lanes per row slot
+  const int irow = rowi[0] + CL * NW * sv;
+  // cycle split (CTA 0, thread 0 -> g_eig_clk[20..24]): matvec + send, wait, CGS2, Ritz checks
+  long long lc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, lt = clock64();
+  auto lclk = [&](int q) {
+    const long long t_ = clock64();
+    lc[q] += t_ - lt;
+    lt = t_;
+  };
+  double anorm = 0.0;
+  double plo = -INFINITY, pres = INFINITY;   // warp k: last check's bracket lower end and residual
+  int next_chk = max(K, 18);                  // Ritz checks at 18, 23, 28, ...
+  bool conv = false;
+  int mm = 0;
+  for (int m = 0; m < mmax; ++m) {
+    const int par = m & 1;
+    double* ly = ly0 + par * 2 * BM;
+    {
+      const double* vm = LV + (size_t)m * ldv;
+      double vreg[CS], x[RS];
+#pragma unroll
+      for (int t = 0; t < CS; ++t) vreg[t] = lane + 32 * t < B ? vm[lane + 32 * t] : 0.0;
+#pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < CS; ++t) acc = fma(a[s][t], vreg[t], acc);
+        x[s] = acc;
+      }
+      const double yv = reduceT<RS>(x, lane) - (irow < B ? vm[irow] : 0.0);   // (G_w - I) v_m
+      if (irow < B) st_async(mapa(saddr(&ly[irow]), peer), yv, mapa(saddr(&S.lmb[par]), peer));
+    }
+    lclk(0);
+    mbar_wait(saddr(&S.lmb[par]), (unsigned)(m >> 1) & 1u);
+    if (tid == 0) mbar_expect(saddr(&S.lmb[par]), 8u * (unsigned)B);
+    lclk(1);
+    // Gram-Schmidt against v_0 .. v_m.  The operator is G_w - I (the
+    // whitened noise level): Krylov spaces do not see the shift, but the new
+    // direction beta_m v_{m+1} is then no longer a percent-level remainder of
+    // y next to the bulk's alpha ~ 1, so ONE classical pass keeps the basis
+    // orthogonal; a second pass runs only when the pass removed more than 99 %
+    // of ||y|| (DGKS criterion, eta = 0.1; rare).  Dots: warp w takes
+    // j = w, w + 8, ... in groups of 8 (y in registers, one transposed warp
+    // reduction per group); slot m + 1 of the first pass is y . y = ||y||^2.
+    // Update: thread i owns element i.
+    yi = own ? ly[i] : 0.0;
+    double alpha = 0.0, ynorm2 = 0.0, beta2 = 0.0;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      const double* src = pass == 0 ? ly : yb;
+      double* hv = pass == 0 ? hb : h2;
+      const int jtop = pass == 0 ? m + 1 : m;   // pass 0: also ||y||^2 in slot m + 1
+      double ys[CS];
+#pragma unroll
+      for (int u = 0; u < CS; ++u) ys[u] = lane + 32 * u < B ? src[lane + 32 * u] : 0.0;
+      for (int jb = w; jb <= jtop; jb += NW * 8) {
+        double acc[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = jb + NW * jj;
+          double s0 = 0.0;
+          if (j <= jtop) {
+            const double* vj = j <= m ? LV + (size_t)j * ldv : src;
+#pragma unroll
+            for (int u = 0; u < CS; ++u)
+              if (lane + 32 * u < B) s0 = fma(vj[lane + 32 * u], ys[u], s0);
+          }
+          acc[jj] = s0;
+        }
+        const double r = reduceT<8>(acc, lane);   // lane L: the sum of acc[L / 4]
+        const int j = jb + NW * (lane >> 2);
+        if ((lane & 3) == 0 && j <= jtop) hv[j] = r;
+      }
+      lclk(4);
+      __syncthreads();
+      lclk(5);
+      if (own) {
+        double ac[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int j0 = 0; j0 <= m; j0 += 8) {
+          double lv8[8], h8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            lv8[u] = LV[(size_t)min(j0 + u, m) * ldv + i];
+            h8[u] = j0 + u <= m ? hv[j0 + u] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) ac[u & 3] = fma(h8[u], lv8[u], ac[u & 3]);
+        }
+        yi -= (ac[0] + ac[1]) + (ac[2] + ac[3]);
+        yb[i] = yi;
+      }
+      lclk(6);
+      alpha += hv[m];
+      if (pass == 0) ynorm2 = hb[m + 1];
+      beta2 = blk_sum(yi * yi, S.red);   // (its barriers also publish yb)
+      lclk(7);
+      if (beta2 >= 0.01 * ynorm2) break;
+    }
+    const double beta = sqrt(beta2);
+    anorm = fmax(anorm, fabs(alpha) + beta);
+    if (tid == 0) {
+      S.d[m] = alpha;
+      S.e[m] = beta;
+    }
+    mm = m + 1;
+    if (mm < B && !(beta > 64.0 * 2.220446049250313e-16 * anorm)) break;   // breakdown: fall back
+    if (own) LV[(size_t)mm * ldv + i] = yi / beta;
+    if (i == B && (B & 1)) LV[(size_t)mm * ldv + i] = 0.0;
+    __syncthreads();
+    lclk(2);
+    if (mm >= K && (mm == B || mm == mmax || mm == next_chk)) {
+      // Ritz pairs of T_mm (d[0..mm), e[0..mm-1)); residual factor e[mm-1]
+      double glo, ghi;
+      tri_bounds(S.d, S.e, S.e2, mm, S.red, glo, ghi);
+      const double tnorm = fmax(fabs(glo), fabs(ghi));
+      const double tsc = tri_scale(tnorm);
+      tri_scaled(S.d, S.e2, mm, tsc, S.ds, S.e2s);
+      lclk(3);
+      if (w < K) {
+        // residual estimate from a 1e-10 ||T|| Ritz value (the z_k it gives is
+        // accurate to ~1e-10 / gap); the converged pairs are refined below.
+        // Warm start: T_{m'} has T_m as its leading block, so by interlacing
+        // the k-th largest Ritz value only grows -- the last check's lower
+        // end stays a lower bound; an upper end a few residuals above it is
+        // accepted when the Sturm count confirms it.
+        const int asc = mm - 1 - w;
+        double lo = glo * tsc, hi = ghi * tsc;
+        if (plo > -INFINITY) {
+          const double l2 = plo * tsc, h2 = (plo + fmax(4.0 * pres, 1e-9 * tnorm)) * tsc;
+          if (l2 > lo) lo = l2;
+          if (h2 < hi && h2 > lo && sturm_count(S.ds, S.e2s, mm, h2) > asc) hi = h2;
+        }
+        bisect_warp(S.ds, S.e2s, mm, lo, hi, asc, 1e-10 * fmax(fabs(glo), fabs(ghi)) * tsc);
+        const double th = 0.5 * (lo + hi) / tsc;
+        plo = lo / tsc;
+        double* z = S.zb[w];
+        twisted_prod(S.d, S.e, mm, th, z, S.zb[8 + 4 * w], S.zb[9 + 4 * w], S.zb[10 + 4 * w],
+                     S.zb[11 + 4 * w]);
+        const double res = (mm == B ? 0.0 : S.e[mm - 1]) * fabs(z[mm - 1]);
+        const bool okw = res <= LZ_TOL * fabs(th + 1.0);   // T is of G_w - I
+        pres = res;
+        if (okw) {
+          // full precision by one Rayleigh-quotient step from the 1e-10 value
+          // (cubic: the correction leaves ~1e-30 ||T||), then z again
+          const double thf = th + rayleigh_corr(S.d, S.e, mm, th, z);
+          twisted_prod(S.d, S.e, mm, thf, z, S.zb[8 + 4 * w], S.zb[9 + 4 * w], S.zb[10 + 4 * w],
+                      S.zb[11 + 4 * w]);
+          if (lane == 0) S.lamk[w] = thf + 1.0;
+        }
+        if (lane == 0) S.lok[w] = okw ? 1 : 0;
+      }
+      __syncthreads();
+      bool ok = true;
+      for (int k = 0; k < K; ++k) ok = ok && S.lok[k];
+      next_chk = mm + 5;
+      lclk(3);
+      if (ok) {
+        conv = true;
+        break;
+      }
+    }
+  }
+  if (c == 0 && tid == 0) {
+    for (int q = 0; q < 4; ++q) g_eig_clk[20 + q] = lc[q];
+    for (int q = 4; q < 8; ++q) g_eig_clk[25 + q] = lc[q];
+    g_eig_clk[24] = mm;
+    g_eig_clk[25] = conv ? 1 : 0;
+    g_eig_clk[28] = lc[3];
+  }
+  if (!conv) {
+    cl_sync();   // no CTA starts phase 2's exchange into px while a peer still reads ly
+    return false;
+  }
+  // x_k = V z_k, normalised, D6 sign (largest |.| entry positive, lowest index on ties)
+  double xk[LZK];
+#pragma unroll
+  for (int k = 0; k < LZK; ++k) {
+    double acc = 0.0;
+    if (k < K && own)
+      for (int j = 0; j < mm; ++j) acc = fma(S.zb[k][j], LV[(size_t)j * ldv + i], acc);
+    xk[k] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < LZK; ++k) {
+    if (k >= K) break;
+    const double nr = blk_sum(xk[k] * xk[k], S.red);
+    xk[k] /= sqrt(nr);
+    double best = own ? fabs(xk[k]) : -1.0, bv = xk[k];
+    int bi = own ? i : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(FULL, best, o);
+      const int oi = __shfl_xor_sync(FULL, bi, o);
+      const double ov = __shfl_xor_sync(FULL, bv, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; bv = ov; }
+    }
+    if (lane == 0) {
+      S.am[0][w] = best;
+      S.av[0][w] = bv;
+      S.ai[0][w] = bi;
+    }
+    __syncthreads();
+    double gb = -1.0, gv = 0.0;
+    int gi = 0x7fffffff;
+    for (int q = 0; q < NW; ++q) {
+      const double ob = S.am[0][q];
+      const int oi = S.ai[0][q];
+      if (ob > gb || (ob == gb && oi < gi)) { gb = ob; gi = oi; gv = S.av[0][q]; }
+    }
+    __syncthreads();
+    if (gv < 0.0) xk[k] = -xk[k];
+  }
+  if (c == 0) {
+    if (own) {
+      const double si = S.sig[i];
+#pragma unroll
+      for (int k = 0; k < LZK; ++k) {
+        if (k >= K) break;
+        const double vi = xk[k];
+        A.ws.vtop[(size_t)i * B + k] = vi;
+        if (A.V) A.V[(size_t)i * A.ldv + k] = vi;
+        A.W[(size_t)i * A.ldwu + k] = (float)(vi / si);
+        A.U[(size_t)i * A.ldwu + k] = (float)(vi * si);
+      }
+    }
+    if (tid < K) {
+      A.ws.lam_top[tid] = S.lamk[tid];
+      if (A.lam_out) A.lam_out[tid] = S.lamk[tid];
+    }
+    if (tid == 0) {
+      A.ws.flags[1] = 1.0;            // phase 2L result: T and Q were not formed
+      A.ws.flags[2] = (double)mm;     // Lanczos steps
+    }
+  }
+  return true;
+}
+
 // BATCHED: cluster b of the grid takes args[b] (independent cubes' eigensolvers
 // in one launch -- the throughput mode of hyde_hyres_batched); else A0.
 template <int CL, bool BATCHED>
@@ -670,6 +1166,8 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
     mbar_init(saddr(&S.mbar[1]), 1);
     mbar_init(saddr(&S.smb[0]), 1);
     mbar_init(saddr(&S.smb[1]), 1);
+    mbar_init(saddr(&S.lmb[0]), 1);
+    mbar_init(saddr(&S.lmb[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const int nblk = (A.B + NB - 1) / NB;
     // bytes of block b's all-gather: B rows x its column count rounded up to pairs
@@ -693,6 +1191,10 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
         A.sigma[i] = 1.0;
       }
     }
+  } else if (A.skip_sweep) {
+    // tridiagonal rerun after phase 2L: sigma is already known
+    for (int i = tid; i < B; i += NT) S.sig[i] = A.sigma[i];
+    __syncthreads();
   } else {
     // ================= phase 1: blocked sweep of G + ridge I =================
   #pragma unroll
@@ -897,6 +1399,11 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
   cl_sync();
   if (prof) stamp(1);
   if (!A.tridiag) return;
+  if (A.lanczos && A.K > 0 && A.K <= LZK && lanczos_top<CL, RS>(A, S, rowi, a, c)) {
+    if (prof) { stamp(2); stamp(3); stamp(4); }
+    CLK_FLUSH
+    return;
+  }
 
   // ================= phase 2: whitening + tridiagonalisation =================
   const double invn = 1.0 / (double)A.n;
@@ -1183,6 +1690,7 @@ __global__ void __launch_bounds__(NT, 1) k2_cluster_kernel(K2Args A0, const K2Ar
     const double vi = (bv < 0.0 ? -1.0 : 1.0) * S.vrow[kk][lr];
     const double si = S.sig[i];
     A.ws.vtop[(size_t)i * B + kk] = vi;
+    if (kk < A.kw0) continue;   // rerun: the first chunk keeps the vectors it was processed with
     if (A.V) A.V[(size_t)i * A.ldv + kk] = vi;
     A.W[(size_t)i * A.ldwu + kk] = (float)(vi / si);
     A.U[(size_t)i * A.ldwu + kk] = (float)(vi * si);
@@ -1399,7 +1907,7 @@ cudaError_t launch_k2_batched(const K2Args* dargs, int nb, cudaStream_t st) {
 
 extern "C" hyde_status hyde_debug_eig_clocks(long long* out) {
   if (!out) return HYDE_EPARAM;
-  return cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(long long) * 32) == cudaSuccess ? HYDE_OK : HYDE_ECUDA;
+  return cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(long long) * 40) == cudaSuccess ? HYDE_OK : HYDE_ECUDA;
 }
 
 extern "C" int hyde_eig_cluster_size(void) {
@@ -1409,6 +1917,22 @@ extern "C" int hyde_eig_cluster_size(void) {
       if (atoi(ev) == 8) g_cluster = 8;
   }
   return g_cluster;
+}
+
+// HYDE_EIG_LANCZOS=0 (experiments): the first chunk by the Householder path;
+// hyde_debug_eig_lanczos overrides it (tests: both paths, forced fallback)
+static int g_lz_enable = -1, g_lz_max = 0;
+bool eig_lanczos_enabled() {
+  if (g_lz_enable < 0) {
+    const char* ev = getenv("HYDE_EIG_LANCZOS");
+    g_lz_enable = (ev && atoi(ev) == 0) ? 0 : 1;
+  }
+  return g_lz_enable == 1;
+}
+extern "C" hyde_status hyde_debug_eig_lanczos(int enable, int max_steps) {
+  g_lz_enable = enable ? 1 : 0;
+  g_lz_max = max_steps > 0 ? max_steps : 0;
+  return HYDE_OK;
 }
 
 size_t eig_workspace_doubles(int B) { return 4 * (size_t)B * B + (size_t)B + 8 + 64; }
@@ -1435,12 +1959,13 @@ static cudaError_t run_more(const double* tri, const EigWs& ws, const double* si
 // sigma (+ optionally the eigenpairs of the first ncomp components; ncomp < 0 = sigma only)
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house, double* tri, float* W, float* U,
-                             int ldwu, cudaStream_t st, int cl_pref) {
+                             int ldwu, cudaStream_t st, int cl_pref, int mode) {
   if (B > BM || B < 3) return cudaErrorInvalidValue;
   const EigWs ws = carve(house, B);
   cudaError_t e = cudaMemsetAsync(ws.flags, 0, 8 * sizeof(double), st);
   if (e != cudaSuccess) return e;
   K2Args a;
+  memset(&a, 0, sizeof(a));
   a.G = G;
   a.n = n;
   a.B = B;
@@ -1458,6 +1983,10 @@ cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, 
   a.W = W;
   a.U = U;
   a.ldwu = ldwu;
+  a.lanczos = (mode == EIG_LANCZOS && !all_lam && eig_lanczos_enabled()) ? 1 : 0;
+  a.skip_sweep = mode == EIG_RETRI ? 1 : 0;
+  a.kw0 = mode == EIG_RETRI ? a.K : 0;
+  a.lzmax = g_lz_max;
   e = run_k2(a, st, cl_pref);
   if (e != cudaSuccess) return e;
   if (all_lam && lam) {
@@ -1505,6 +2034,10 @@ cudaError_t launch_noise_eig_batched(int nb, const double* const* G, long long n
     a.W = W[b];
     a.U = U[b];
     a.ldwu = ldwu;
+    // the batched throughput mode keeps the Householder path: at 256 x 256 x 191
+    // the whitened bulk is ~3x wider than at `large` and Lanczos needs ~55
+    // steps (measured 2.52 vs 2.21 ms for the 64 cubes' eigensolvers)
+    a.lanczos = 0;
   }
   cudaError_t e = cudaMemcpyAsync(dargs, hargs, (size_t)nb * sizeof(K2Args), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
@@ -1524,6 +2057,7 @@ cudaError_t launch_eig_raw(const double* Amat, int B, int ncomp, double* ones, d
   cudaError_t e = cudaMemsetAsync(ws.flags, 0, 8 * sizeof(double), st);
   if (e != cudaSuccess) return e;
   K2Args a;
+  memset(&a, 0, sizeof(a));
   a.G = Amat;
   a.n = 1;
   a.B = B;

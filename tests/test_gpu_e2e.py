@@ -277,3 +277,31 @@ def test_batched_phased_needs_second_chunk(hy):
         assert torch.equal(single, outs[i]), i
         assert infos[i]["rank"] == info["rank"]
     assert max(i["rank"] for i in infos) >= 4
+
+
+def _lanczos(hy, enable, max_steps=0):
+    assert hy._lib.lib().hyde_debug_eig_lanczos(enable, max_steps) == 0
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "medium", "wide"])
+def test_first_chunk_lanczos_householder_and_fallback(hy, name):
+    """K2's first chunk three ways: Lanczos (phase 2L, the default), the Householder
+    path (phase 2 + 3), and Lanczos capped at 5 steps -- below convergence, so the
+    kernel falls back to Householder in place.  Same rank, outputs within 1e-6 of
+    each other, each within the oracle tolerance (wide: r* > the first chunk, so the
+    tridiagonal rerun after Lanczos serves the second chunk)."""
+    s = synth.make_cube(name, 0)
+    ref = O.hyres(s.noisy)
+    x = dev(s.noisy)
+    outs = []
+    try:
+        for en, cap in ((1, 0), (0, 0), (1, 5)):
+            _lanczos(hy, en, cap)
+            out, info = hy.hyres(x, return_info=True)
+            o = out.cpu().numpy()
+            _compare(s, ref, o, info)
+            outs.append(o)
+    finally:
+        _lanczos(hy, 1, 0)
+    assert metrics.rel_l2(outs[1], outs[0]) <= 1e-6
+    assert metrics.rel_l2(outs[1], outs[2]) <= 1e-6

@@ -18,7 +18,7 @@ e0.record()
 for rep in range(10):
     sig, lam, V = hy.stages.eig(g, r * c, k, all_lam=False)
 e1.record(); torch.cuda.synchronize()
-clk = (ctypes.c_longlong * 32)()
+clk = (ctypes.c_longlong * 40)()
 hy._lib.lib().hyde_debug_eig_clocks(clk)
 print(name, "B=%d K=%d: K2 %.1f us per call (CUDA events)" % (b, k, e0.elapsed_time(e1) / 10 * 1e3))
 for nm, a, bb in [("sweep (sigma)", 0, 1), ("whiten+tridiag", 1, 2), ("eigenpairs", 2, 3), ("vectors", 3, 4)]:
