@@ -1003,7 +1003,11 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
   if (hyde_build_filters(p.wavelet_taps, &fb, nullptr) != 0) return fail(h, HYDE_EPARAM, "filter derivation failed");
   const int B = bands;
   Layout L;
-  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L, kLaneGramMinPx);
+  static const int lane_px = [] {
+    const char* ev = getenv("HYDE_LANE_GRAM_PX");   // experiments
+    return ev ? atoi(ev) : kLaneGramMinPx;
+  }();
+  make_layout(rows, cols, B, p.chunk, levels, p.wavelet_taps, &L, lane_px);
   const long long n = L.n;
   const size_t per = (size_t)rows * cols * bands;
   const int first = std::min(std::min(kFirstChunk, p.chunk), B);

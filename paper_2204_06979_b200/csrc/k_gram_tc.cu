@@ -11,7 +11,7 @@
 //   * gram_qscale_kernel reads a fixed sample of every band (64 blocks of the
 //     pixel axis, <= 256 pixels each) and takes a centre m_b = median of the
 //     block means and a range R_b = 2 x the 8th-largest block max |y - m_b|,
-//     so a few outliers cannot widen the step (one 8-CTA cluster per band,
+//     so a few outliers cannot widen the step (one CTA per band,
 //     1.6 % of the cube read at `large`; the old full max pre-pass read all);
 //   * inv_s = fp32(32767 / R_b), c_b = rint(m_b inv_s) (an integer centre),
 //     q = rint(y inv_s - c_b) in [-32768, 32767] (16 bits), y ~ s (q + c);
@@ -515,11 +515,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
 
 // ------------------------------------------------------------------ qscale
-// One 8-CTA cluster per band, one sample block per warp.  Block k of the pixel
+// One CTA per band; warp w samples blocks w, w + 8, ... (all eight of its
+// blocks' loads in flight before the reductions).  Block k of the pixel
 // axis ([kN/64, (k+1)N/64)) is sampled at <= 256 pixels (all of them, or two
 // 128-pixel runs at the starts of its halves: 1.6 % of the cube at `large`);
-// per block: mean, min, max of the finite samples, written into the leader
-// CTA's shared memory (DSMEM).  The leader: m = lower median of the block
+// per block: mean, min, max of the finite samples.  (An 8-CTA cluster per
+// band with one block per warp cost 450 us for the 64 x 191 bands of the
+// batched mode -- 98k CTAs of latency -- against 16 us for one cube.)  Then:
+// m = lower median of the block
 // means; dev_k = max(max_k - m, m - min_k); R = 2 x the 8th largest dev_k
 // (rank min(7, nblk/8): the largest
 // for fewer than 16 blocks; the largest when that is 0; |m|, else 1e-30, when
@@ -527,8 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 // |c| <= 2^21 (the fma addend must stay in [2^23, 2^24)).
 // Also zeroes a slice of the clip bitmap and, on CTA 0, the caller's
 // rank-state words -- the first kernel of the step.
-constexpr int QS_CL = 8;   // CTAs per band (cluster)
-__global__ void __cluster_dims__(QS_CL, 1, 1) __launch_bounds__(256)
+__global__ void __launch_bounds__(256)
     gram_qscale_kernel(const float* __restrict__ Y, long long n, GramQScale* qs, unsigned* bitmap, long long nwords,
                        int* st4, int nst4, const GramJob* __restrict__ jobs) {
   pdl_wait();
@@ -540,9 +542,7 @@ __global__ void __cluster_dims__(QS_CL, 1, 1) __launch_bounds__(256)
     st4 = j.state4;
     if (j.zero8 && blockIdx.x == 0 && threadIdx.x < 8) j.zero8[threadIdx.x] = 0.0;
   }
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  const int b = blockIdx.x / QS_CL, crank = (int)cl.block_rank();
+  const int b = blockIdx.x;
   {
     const long long w0 = nwords * blockIdx.x / gridDim.x, w1 = nwords * (blockIdx.x + 1) / gridDim.x;
     for (long long w = w0 + threadIdx.x; w < w1; w += blockDim.x) bitmap[w] = 0u;
@@ -554,31 +554,41 @@ __global__ void __cluster_dims__(QS_CL, 1, 1) __launch_bounds__(256)
   const int nblk = n < QS_NBLK ? (int)n : QS_NBLK;
   const float* row = Y + (long long)b * n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k = crank * 8 + warp;
-  if (k < nblk) {
+  constexpr int KPW = QS_NBLK / 8;   // blocks per warp
+  float v[KPW][8];
+  bool full[KPW];
+#pragma unroll
+  for (int q = 0; q < KPW; ++q) {
+    const int k = warp + 8 * q;
+    const long long p0 = n * k / nblk, p1 = n * (k + 1) / nblk, len = p1 - p0;
+    full[q] = k < nblk && len > 256;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float* src = row + p0 + len * j / 2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[q][4 * j + u] = full[q] ? __ldg(src + lane + 32 * u) : 0.f;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < KPW; ++q) {
+    const int k = warp + 8 * q;
+    if (k >= nblk) continue;
     const long long p0 = n * k / nblk, p1 = n * (k + 1) / nblk, len = p1 - p0;
     double sum = 0.0;
     int cnt = 0;
     float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
-    auto take = [&](float v) {
-      const bool ok = isfinite(v);
-      sum += ok ? (double)v : 0.0;
+    auto take = [&](float x) {
+      const bool ok = isfinite(x);
+      sum += ok ? (double)x : 0.0;
       cnt += ok;
-      mn = ok ? fminf(mn, v) : mn;
-      mx = ok ? fmaxf(mx, v) : mx;
+      mn = ok ? fminf(mn, x) : mn;
+      mx = ok ? fmaxf(mx, x) : mx;
     };
-    if (len <= 256) {
+    if (!full[q]) {
       for (long long i = lane; i < len; i += 32) take(__ldg(row + p0 + i));
     } else {
-      float v[8];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float* src = row + p0 + len * j / 2;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[4 * j + u] = __ldg(src + lane + 32 * u);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) take(v[u]);
+      for (int u = 0; u < 8; ++u) take(v[q][u]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -588,13 +598,13 @@ __global__ void __cluster_dims__(QS_CL, 1, 1) __launch_bounds__(256)
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
     if (lane == 0) {
-      *cl.map_shared_rank(&bmean[k], 0) = cnt > 0 ? sum / cnt : 0.0;
-      *cl.map_shared_rank(&bmin[k], 0) = cnt > 0 ? mn : 0.f;
-      *cl.map_shared_rank(&bmax[k], 0) = cnt > 0 ? mx : 0.f;
+      bmean[k] = cnt > 0 ? sum / cnt : 0.0;
+      bmin[k] = cnt > 0 ? mn : 0.f;
+      bmax[k] = cnt > 0 ? mx : 0.f;
     }
   }
-  cl.sync();
-  if (crank != 0) return;
+  __syncthreads();
+
   // order statistics by rank counting (ties broken by block index)
   if ((int)threadIdx.x < nblk) {
     const int kk = threadIdx.x;
@@ -658,6 +668,23 @@ __global__ void __launch_bounds__(256) gram_reduce_i64_kernel(long long* __restr
   __shared__ long long part[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long bb = (long long)B * B, tot = bb + B;
+  if (np <= 16) {
+    // few pairs (the batched mode's 8 per cube): one element per thread, all
+    // np loads in flight -- 256 elements per CTA instead of 32 (the 32-wide
+    // split below left 73k latency-bound CTAs for 64 cubes)
+    const long long idx = blockIdx.x * 256LL + threadIdx.x;
+    const int i = idx < bb ? (int)(idx / B) : 0, j = idx < bb ? (int)(idx % B) : 0;
+    if (idx < tot && !(idx < bb && i >= 128 && j < 128)) {
+      long long v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = k < np ? __ldcs(partial + (long long)k * tot + idx) : 0;
+      long long s = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s += v[k];
+      partial[idx] = s;
+    }
+    return;
+  }
   const long long idx = blockIdx.x * 32LL + lane;
   const int i = idx < bb ? (int)(idx / B) : 0, j = idx < bb ? (int)(idx % B) : 0;
   const bool active = idx < tot && !(idx < bb && i >= 128 && j < 128);
@@ -1009,7 +1036,7 @@ static bool make_maps(const float* Y, long long n, int B, int hb, CUtensorMap* t
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npairs, double* G, int* nonfinite,
                            cudaStream_t st, int* state4) {
   TcWs w = carve(ws, n, B, npairs);
-  cudaError_t e = launch_pdl(gram_qscale_kernel, dim3(QS_CL * B), dim3(256), 0, st, Y, n, w.qs, w.bitmap, w.nwords, state4,
+  cudaError_t e = launch_pdl(gram_qscale_kernel, dim3(B), dim3(256), 0, st, Y, n, w.qs, w.bitmap, w.nwords, state4,
                              (int)(sizeof(RankState) / sizeof(int)), (const GramJob*)nullptr);
   if (e != cudaSuccess) return e;
   GramTc P;
@@ -1043,7 +1070,7 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
   }
   if (e != cudaSuccess) return e;
   const long long tot = (long long)B * B + B;
-  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, w.partial, npairs, B,
+  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)(npairs <= 16 ? (tot + 255) / 256 : (tot + 31) / 32)), dim3(256), 0, st, w.partial, npairs, B,
                  (const GramJob*)nullptr);
   if (e != cudaSuccess) return e;
   const int nbk = (B + FIX_TB - 1) / FIX_TB;
@@ -1078,7 +1105,7 @@ cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* w
   cudaError_t e = cudaMemcpyAsync(djobs, hjobs, (size_t)nb * sizeof(GramJob), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   const long long nwords = (n + 31) / 32;
-  e = launch_pdl(gram_qscale_kernel, dim3(QS_CL * B, nb), dim3(256), 0, st, (const float*)nullptr, n,
+  e = launch_pdl(gram_qscale_kernel, dim3(B, nb), dim3(256), 0, st, (const float*)nullptr, n,
                  (GramQScale*)nullptr, (unsigned*)nullptr, nwords, (int*)nullptr,
                  (int)(sizeof(RankState) / sizeof(int)), dj);
   if (e != cudaSuccess) return e;
@@ -1099,7 +1126,7 @@ cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* w
   e = launch_pdl(gram_tc_kernel<false>, dim3(2 * npairs, nb), dim3(NTHREADS), smem, st, P, tm, tm, dj);
   if (e != cudaSuccess) return e;
   const long long tot = (long long)B * B + B;
-  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)((tot + 31) / 32), nb), dim3(256), 0, st,
+  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)(npairs <= 16 ? (tot + 255) / 256 : (tot + 31) / 32), nb), dim3(256), 0, st,
                  (long long*)nullptr, npairs, B, dj);
   if (e != cudaSuccess) return e;
   const int nbk = (B + FIX_TB - 1) / FIX_TB;
