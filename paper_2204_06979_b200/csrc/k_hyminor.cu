@@ -85,29 +85,70 @@ __global__ void __launch_bounds__(128) l1spec_first_kernel(const float* __restri
   __syncthreads();
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool live = p < n;
+  // Both sweeps run in blocks of L1B bands with the NEXT block's loads issued
+  // (in program order) before this block's stores: the compiler may not hoist
+  // a load of M / X above a store to X (M == X is allowed), so a plain loop
+  // waited one DRAM / L2 round trip per band (0.97 ms at `large`).  Same
+  // arithmetic, same order as the band-by-band loop.
+  constexpr int L1B = 32;
   float y = 0.f, xo2 = 0.f;
   if (live) {
-#pragma unroll 8
-    for (int i = 0; i < B; ++i) {
-      const float m = M[(size_t)i * n + p];
-      xo2 = fmaf(m, m, xo2);
-      y = s_alpha[i] * (y + m);
-      X[(size_t)i * n + p] = y;
+    float mc[L1B], mn[L1B];
+#pragma unroll
+    for (int u = 0; u < L1B; ++u) mc[u] = u < B ? M[(size_t)u * n + p] : 0.f;
+    for (int i0 = 0; i0 < B; i0 += L1B) {
+#pragma unroll
+      for (int u = 0; u < L1B; ++u) {
+        const int i = i0 + L1B + u;
+        mn[u] = i < B ? M[(size_t)i * n + p] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < L1B; ++u) {
+        const int i = i0 + u;
+        if (i < B) {
+          const float m = mc[u];
+          xo2 = fmaf(m, m, xo2);
+          y = s_alpha[i] * (y + m);
+          X[(size_t)i * n + p] = y;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < L1B; ++u) mc[u] = mn[u];
     }
   }
   float dx2 = 0.f;
   if (live) {
     float x1 = 0.f, x2 = 0.f;   // x_{i+1}, x_{i+2}
-#pragma unroll 8
-    for (int i = B - 1; i >= 0; --i) {
-      const float x = fmaf(-s_cp[i], x1, X[(size_t)i * n + p]);
-      __stcs(X + (size_t)i * n + p, x);
-      if (i + 1 <= B - 1) {   // (D^T D x)_{i+1} now that x_i is known
-        const float t = (i + 1 == B - 1) ? x1 - x : (2.f * x1 - x - x2);
-        dx2 = fmaf(t, t, dx2);
+    // blocks from the top: [i1 - L1B + 1, i1]
+    float yc[L1B], yn[L1B];
+    const int itop = B - 1;
+#pragma unroll
+    for (int u = 0; u < L1B; ++u) {
+      const int i = itop - u;
+      yc[u] = i >= 0 ? X[(size_t)i * n + p] : 0.f;
+    }
+    for (int i1 = itop; i1 >= 0; i1 -= L1B) {
+#pragma unroll
+      for (int u = 0; u < L1B; ++u) {
+        const int i = i1 - L1B - u;
+        yn[u] = i >= 0 ? X[(size_t)i * n + p] : 0.f;
       }
-      x2 = x1;
-      x1 = x;
+#pragma unroll
+      for (int u = 0; u < L1B; ++u) {
+        const int i = i1 - u;
+        if (i >= 0) {
+          const float x = fmaf(-s_cp[i], x1, yc[u]);
+          __stcs(X + (size_t)i * n + p, x);
+          if (i + 1 <= B - 1) {   // (D^T D x)_{i+1} now that x_i is known
+            const float t = (i + 1 == B - 1) ? x1 - x : (2.f * x1 - x - x2);
+            dx2 = fmaf(t, t, dx2);
+          }
+          x2 = x1;
+          x1 = x;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < L1B; ++u) yc[u] = yn[u];
     }
     if (B >= 2) {
       const float t = x1 - x2;   // row 0: x_0 - x_1
@@ -329,7 +370,27 @@ cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float la
     }
   }
   unsigned* todo = (unsigned*)todo_ws;
-  l1spec_first_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(M, X, n, B, tol, max_iters, iters, todo, tf);
+  // At most 8 resident CTAs per SM (an unused dynamic shared-memory
+  // reservation): measured at `large`, 3 / 4 / 6 / 8 / 16 per SM gave 0.86 /
+  // 0.67 / 0.57 / 0.57 / 0.57 ms and no cap 0.66 ms (more pixels in flight
+  // than the L2 holds scratch for).  (A register-resident variant -- 32 pixels
+  // per CTA, band segments per warp chained by affine scans, like FORPDN's
+  // solve -- measured 0.97 ms: too few pixels in flight per SM.)
+  // HYDE_L1_CTAS_PER_SM overrides (experiments).
+  static const int cap = [] {
+    const char* ev = getenv("HYDE_L1_CTAS_PER_SM");
+    return ev ? atoi(ev) : 8;
+  }();
+  size_t pad = 0;
+  if (cap > 0) {
+    pad = (size_t)(227 * 1024) / (size_t)cap > 2048 ? (size_t)(227 * 1024) / (size_t)cap - 2048 : 0;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaFuncSetAttribute(l1spec_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_done = true;
+    }
+  }
+  l1spec_first_kernel<<<(unsigned)((n + 127) / 128), 128, pad, st>>>(M, X, n, B, tol, max_iters, iters, todo, tf);
   cudaError_t e = cudaGetLastError();
   if (getenv("HYDE_DEBUG_SYNC")) {
     e = cudaStreamSynchronize(st);
