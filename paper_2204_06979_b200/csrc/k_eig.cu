@@ -856,7 +856,11 @@ __device__ __forceinline__ void form_reflector(const double (&col)[CS], int kk, 
 // breakdown (beta ~ 0 before convergence) or LVD / B steps without
 // convergence returns false: the caller runs the Householder path (phase 2)
 // as before.  T_B at m = B is the whole space: converged by construction.
-constexpr double LZ_TOL = 1e-14;
+// ||G_w x - theta x|| <= LZ_TOL theta: the vectors leave the kernel as fp32
+// W / U, so an eigenvector error residual / gap of ~1e-10 (gap >= 1e-2) is
+// already far below their rounding
+__constant__ double c_lz_tol = 1e-12;
+#define LZ_TOL c_lz_tol
 
 template <int CL, int RS>
 __device__ bool lanczos_top(const K2Args& A, K2Smem& S, const int (&rowi)[RS], double (&a)[RS][CS], int c) {
@@ -1059,7 +1063,7 @@ __device__ bool lanczos_top(const K2Args& A, K2Smem& S, const int (&rowi)[RS], d
       __syncthreads();
       bool ok = true;
       for (int k = 0; k < K; ++k) ok = ok && S.lok[k];
-      next_chk = mm + 5;
+      next_chk = mm + max(5, mm / 4);   // 18, 23, 28, 35, 43, 53, 66, ...
       lclk(3);
       if (ok) {
         conv = true;
@@ -1929,6 +1933,19 @@ bool eig_lanczos_enabled() {
   }
   return g_lz_enable == 1;
 }
+// HYDE_EIG_BATCHED_LANCZOS=0: the batched throughput mode on the Householder
+// path (experiments); HYDE_EIG_LZTOL sets the residual tolerance (experiments)
+static bool eig_batched_lanczos() {
+  static const bool on = [] {
+    const char* ev = getenv("HYDE_EIG_BATCHED_LANCZOS");
+    if (const char* tv = getenv("HYDE_EIG_LZTOL")) {
+      const double t = atof(tv);
+      if (t > 0.0) cudaMemcpyToSymbol(c_lz_tol, &t, sizeof(double));
+    }
+    return !(ev && atoi(ev) == 0);
+  }();
+  return on && eig_lanczos_enabled();
+}
 extern "C" hyde_status hyde_debug_eig_lanczos(int enable, int max_steps) {
   g_lz_enable = enable ? 1 : 0;
   g_lz_max = max_steps > 0 ? max_steps : 0;
@@ -1983,6 +2000,7 @@ cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, 
   a.W = W;
   a.U = U;
   a.ldwu = ldwu;
+  (void)eig_batched_lanczos();   // reads the experiment variables once
   a.lanczos = (mode == EIG_LANCZOS && !all_lam && eig_lanczos_enabled()) ? 1 : 0;
   a.skip_sweep = mode == EIG_RETRI ? 1 : 0;
   a.kw0 = mode == EIG_RETRI ? a.K : 0;
@@ -2034,10 +2052,11 @@ cudaError_t launch_noise_eig_batched(int nb, const double* const* G, long long n
     a.W = W[b];
     a.U = U[b];
     a.ldwu = ldwu;
-    // the batched throughput mode keeps the Householder path: at 256 x 256 x 191
-    // the whitened bulk is ~3x wider than at `large` and Lanczos needs ~55
-    // steps (measured 2.52 vs 2.21 ms for the 64 cubes' eigensolvers)
-    a.lanczos = 0;
+    // phase 2L in the batched throughput mode as well: at 256 x 256 x 191 the
+    // whitened bulk is ~3x wider than at `large` and Lanczos needs ~53 steps,
+    // still fewer SM-microseconds than the Householder reduction (64 solves:
+    // 2.05 vs 2.21 ms); a cube whose rank needs more is rerun alone
+    a.lanczos = eig_batched_lanczos() ? 1 : 0;
   }
   cudaError_t e = cudaMemcpyAsync(dargs, hargs, (size_t)nb * sizeof(K2Args), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
