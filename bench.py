@@ -207,9 +207,18 @@ def wavelet_isolated(hy, torch, cube, cfg, levels, steps, hbm):
     hy.stages.wavelet_shrink(E, levels, out=out, stats=False)
     torch.cuda.synchronize()
     dev = cube.device.index
-    hy.profile_enable(dev, True)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # DWT + SURE alone (the analysis-only call): its own wall time
+    hy.stages.wavelet_shrink(E, levels, stats=False, analyze_only=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(steps):
+        hy.stages.wavelet_shrink(E, levels, stats=False, analyze_only=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ds_wall = e0.elapsed_time(e1) / steps
+    hy.profile_enable(dev, True)
     e0.record(st)
     for _ in range(steps):
         hy.stages.wavelet_shrink(E, levels, out=out, stats=False)
@@ -221,7 +230,9 @@ def wavelet_isolated(hy, torch, cube, cfg, levels, steps, hbm):
     nc = coeff_count(cfg.rows, cfg.cols, levels)
     lvl = b * dwt_image_bytes(cfg.rows, cfg.cols, levels)
     byt = {"dwt": lvl, "sure": b * 4 * nc, "idwt": lvl}
-    res = {"images": b, "rows": cfg.rows, "cols": cfg.cols, "levels": levels, "ms": round(ms, 4)}
+    res = {"images": b, "rows": cfg.rows, "cols": cfg.cols, "levels": levels, "ms": round(ms, 4),
+           "timing": "CUDA events around the calls (wall); per-stage ms from the library's stage events; "
+                     "dwt+sure = wall time of the analysis-only call (out = NULL)"}
     tot_b, tot_t = 0, 0.0
     for k in ("dwt", "sure", "idwt"):
         t = stg[k][0] / steps
@@ -230,12 +241,13 @@ def wavelet_isolated(hy, torch, cube, cfg, levels, steps, hbm):
         tot_b += byt[k]
         tot_t += t
     ds_b = byt["dwt"] + byt["sure"]
-    ds_t = res["dwt"]["ms"] + res["sure"]["ms"]
+    ds_t = ds_wall
     res["dwt+sure"] = {"ms": round(ds_t, 4), "bytes": ds_b, "GBps": round(ds_b / (ds_t * 1e-3) / 1e9, 1),
                        "frac_hbm": round(ds_b / (ds_t * 1e-3) / 1e9 / hbm, 4)}
-    res["dwt+sure+idwt"] = {"ms": round(tot_t, 4), "bytes": tot_b,
-                            "GBps": round(tot_b / (tot_t * 1e-3) / 1e9, 1),
-                            "frac_hbm": round(tot_b / (tot_t * 1e-3) / 1e9 / hbm, 4)}
+    res["dwt+sure+idwt"] = {"ms": round(ms, 4), "bytes": tot_b,
+                            "GBps": round(tot_b / (ms * 1e-3) / 1e9, 1),
+                            "frac_hbm": round(tot_b / (ms * 1e-3) / 1e9 / hbm, 4),
+                            "busy_ms_sum": round(tot_t, 4)}
     # the method's minimum: DWT one read of N + one write of N_c
     # per image (a fused multi-level transform), SURE one read of N_c
     mb = b * (4 * n + 4 * nc + 4 * nc)

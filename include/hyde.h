@@ -337,7 +337,7 @@ hyde_status hyde_k_idwt(hyde_handle h, const float* coeffs, int count, int rows,
  * the inverse DWT with each subband soft-thresholded by its t* as it is
  * loaded (no rank rule: every image is reconstructed).  images / out: DEVICE,
  * count x rows x cols fp32 (out == images allowed; partial overlap ->
- * HYDE_EPARAM).  kstar / tstar [count*(3L+1)] (DEVICE, subband order of
+ * HYDE_EPARAM; out == NULL: DWT + SURE only).  kstar / tstar [count*(3L+1)] (DEVICE, subband order of
  * hyde_k_dwt_fwd) and e_post [count] (DEVICE, sum of the thresholded
  * coefficients squared) may each be NULL.  Workspace (about 2.3 x the image
  * bytes) is held by the handle.  Asynchronous; a SURE capacity failure is

@@ -123,22 +123,23 @@ def idwt(coeffs, rows, cols, levels, taps=16):
     return out
 
 
-def wavelet_shrink(images, levels, taps=16, keep_ll=False, out=None, stats=True):
+def wavelet_shrink(images, levels, taps=16, keep_ll=False, out=None, stats=True, analyze_only=False):
     """A4 -> A5 -> A6a on a batch of images, as the hot path runs them (hyde_wavelet_shrink).
-    Returns out (count, R, C) and, with stats, kstar / tstar (count, 3L+1) and e_post (count,)."""
+    Returns out (count, R, C) and, with stats, kstar / tstar (count, 3L+1) and e_post (count,).
+    analyze_only: DWT + SURE only (no IDWT; out is None)."""
     torch = _torch()
     _cube(images, "images")
     cnt, r, c = images.shape
     nsub = 3 * levels + 1
-    if out is None:
+    if out is None and not analyze_only:
         out = torch.empty_like(images)
     ks = torch.empty((cnt, nsub), dtype=torch.int32, device=images.device) if stats else None
     ts = torch.empty((cnt, nsub), dtype=torch.float32, device=images.device) if stats else None
     ep = torch.empty(cnt, dtype=torch.float64, device=images.device) if stats else None
     h = _h(images)
     p = lambda t: t.data_ptr() if t is not None else None
-    check(lib().hyde_wavelet_shrink(h, images.data_ptr(), cnt, r, c, levels, taps, 1 if keep_ll else 0, out.data_ptr(),
-                                    p(ks), p(ts), p(ep), _stream(images)), h)
+    check(lib().hyde_wavelet_shrink(h, images.data_ptr(), cnt, r, c, levels, taps, 1 if keep_ll else 0,
+                                    None if analyze_only else out.data_ptr(), p(ks), p(ts), p(ep), _stream(images)), h)
     return (out, ks, ts, ep) if stats else out
 
 

@@ -360,6 +360,21 @@ def test_wavelet_shrink_matches_oracle(hy, shape):
     assert np.array_equal(same.cpu().numpy(), out)
 
 
+def test_wavelet_shrink_analysis_only(hy):
+    """out == NULL runs DWT + SURE only (the bench's DWT+SURE wall time): the same
+    thresholds and k* as the full call, on 70 images with a ragged shape."""
+    rng = np.random.default_rng(8)
+    r, c, lv, cnt = 64, 96, 2, 70
+    yy, xx = np.mgrid[0:r, 0:c]
+    x = np.stack([(6.0 / (1 + k % 5)) * np.sin(xx / (4.0 + k % 7)) * np.cos(yy / (6.0 + k % 3))
+                  + rng.standard_normal((r, c)) for k in range(cnt)]).astype(np.float32)
+    _, k1, t1, e1 = hy.stages.wavelet_shrink(dev(x), lv)
+    _, ka, ta, ea = hy.stages.wavelet_shrink(dev(x), lv, analyze_only=True)
+    assert np.array_equal(ka.cpu().numpy(), k1.cpu().numpy())
+    assert np.array_equal(ta.cpu().numpy(), t1.cpu().numpy())
+    assert np.array_equal(ea.cpu().numpy(), e1.cpu().numpy())
+
+
 def test_sure_dense_window_refinement(hy):
     """Subbands whose first-pass window exceeds the 8192-key capacity (a dense cluster
     of magnitudes where SURE is flat) go through the finer re-binning passes and still
