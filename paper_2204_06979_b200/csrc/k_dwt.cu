@@ -28,8 +28,9 @@ constexpr int IC = 64;   // inverse: output cols per tile
 // Packed fp32x2 FMA (FFMA2): two lanes of arithmetic per issue slot.  The
 // forward filter passes are issue-bound, and FFMA2 halves their FMA
 // instructions; each half of the pair is the same fp32 fma as before (so the
-// coefficients are bit-identical).  The inverse keeps scalar FFMA: its packed
-// variant (coefficient rows loaded as pairs) measured 18 % slower.
+// coefficients are bit-identical).  The inverse packs the two output parities
+// of a window position along axis 1 (same window entries, taps 2q / 2q + 1)
+// and the {LL, LH} / {HL, HH} subband pairs along axis 0.
 typedef unsigned long long f2_t;
 __device__ __forceinline__ f2_t pk2(float a, float b) {
   f2_t r;
@@ -301,18 +302,21 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
       wl[t] = lo1[rr][vb + t];
       wh[t] = hi1[rr][vb + t];
     }
+    // outputs 2u (taps 2q) and 2u + 1 (taps 2q + 1) read the SAME window
+    // entries: one packed FMA per (q, subband) computes both, each half the
+    // scalar fma sequence of its output (bit-identical)
 #pragma unroll
-    for (int k = 0; k < IJ; ++k) {
-      const int par = k & 1, u = k >> 1;
-      float sacc = 0.f;
+    for (int u = 0; u < IJ / 2; ++u) {
+      f2_t s2 = 0ull;   // {s_2u, s_2u+1}
 #pragma unroll
       for (int q = 0; q < HT; ++q) {
-        const int m = 2 * q + par;
         const int tj = u - q + HT - 1;
-        sacc = fmaf(fb.h[m], wl[tj], sacc);
-        sacc = fmaf(fb.g[m], wh[tj], sacc);
+        s2 = ffma2(pk2(fb.h[2 * q], fb.h[2 * q + 1]), pk2(wl[tj], wl[tj]), s2);
+        s2 = ffma2(pk2(fb.g[2 * q], fb.g[2 * q + 1]), pk2(wh[tj], wh[tj]), s2);
       }
-      otile[rr][IJ * q8 + k] = sacc;
+      const float2 o2 = up2(s2);
+      otile[rr][IJ * q8 + 2 * u] = o2.x;
+      otile[rr][IJ * q8 + 2 * u + 1] = o2.y;
     }
   }
   __syncthreads();
