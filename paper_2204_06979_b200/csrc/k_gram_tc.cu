@@ -518,7 +518,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 // One CTA per band; warp w samples blocks w, w + 8, ... (all eight of its
 // blocks' loads in flight before the reductions).  Block k of the pixel
 // axis ([kN/64, (k+1)N/64)) is sampled at <= 256 pixels (all of them, or two
-// 128-pixel runs at the starts of its halves: 1.6 % of the cube at `large`);
+// runs at the starts of its halves: 128 pixels each -- 1.6 % of the cube at
+// `large` -- 64 or 32 for blocks under 8192 / 4096 pixels);
 // per block: mean, min, max of the finite samples.  (An 8-CTA cluster per
 // band with one block per warp cost 450 us for the 64 x 191 bands of the
 // batched mode -- 98k CTAs of latency -- against 16 us for one cube.)  Then:
@@ -555,25 +556,36 @@ __global__ void __launch_bounds__(256)
   const float* row = Y + (long long)b * n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int KPW = QS_NBLK / 8;   // blocks per warp
+  // block k starts at n k / nblk: a shift for nblk = 64 (a 64-bit division is a
+  // ~100-instruction routine; three per block made this kernel 0.42 ms for the
+  // 64 x 191 bands of the batched mode)
+  static_assert(QS_NBLK == 64, "blk_lo shifts by log2(QS_NBLK)");
+  auto blk_lo = [&](int k) -> long long { return nblk == QS_NBLK ? (n * k) >> 6 : (long long)k; };
+  // samples per half-block run: 128 (blocks of >= 8192 pixels: 1.6 % of the
+  // cube at `large`), 64 / 32 for shorter blocks (the batched mode's
+  // 1024-pixel blocks: 6 % of the band instead of 25 %, which made this
+  // kernel 0.42 ms for 64 cubes)
+  const long long blen = n / QS_NBLK;
+  const int uu = blen >= 8192 ? 4 : (blen >= 4096 ? 2 : 1);
   float v[KPW][8];
   bool full[KPW];
 #pragma unroll
   for (int q = 0; q < KPW; ++q) {
     const int k = warp + 8 * q;
-    const long long p0 = n * k / nblk, p1 = n * (k + 1) / nblk, len = p1 - p0;
+    const long long p0 = blk_lo(k), p1 = blk_lo(k + 1), len = p1 - p0;
     full[q] = k < nblk && len > 256;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const float* src = row + p0 + len * j / 2;
+      const float* src = row + p0 + ((len * j) >> 1);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[q][4 * j + u] = full[q] ? __ldg(src + lane + 32 * u) : 0.f;
+      for (int u = 0; u < 4; ++u) v[q][4 * j + u] = (full[q] && u < uu) ? __ldg(src + lane + 32 * u) : 0.f;
     }
   }
 #pragma unroll
   for (int q = 0; q < KPW; ++q) {
     const int k = warp + 8 * q;
     if (k >= nblk) continue;
-    const long long p0 = n * k / nblk, p1 = n * (k + 1) / nblk, len = p1 - p0;
+    const long long p0 = blk_lo(k), p1 = blk_lo(k + 1), len = p1 - p0;
     double sum = 0.0;
     int cnt = 0;
     float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
@@ -588,7 +600,8 @@ __global__ void __launch_bounds__(256)
       for (long long i = lane; i < len; i += 32) take(__ldg(row + p0 + i));
     } else {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) take(v[q][u]);
+      for (int u = 0; u < 8; ++u)
+        if ((u & 3) < uu) take(v[q][u]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -28,13 +28,20 @@ def dev(a):
 def _quantized_gram(y, inv_s, c):
     """The Gram K1 defines (k_gram_tc.cu, DESIGN.md §4 K1), from the scales it chose:
     q = rint(y inv_s - c) (fp32 inv_s, the exact product, ties to even); a pixel with any
-    q outside [-32768, 32767] is flagged and enters exactly (fp64 y y^T); every other pixel enters as
+    value whose fma r = fp32(y inv_s + 2^23 + 32768 - c) leaves [2^23, 2^23 + 65535]
+    is flagged and enters exactly (fp64 y y^T); every other pixel enters as
     s (q + c), s = 1 / inv_s, with the integer Gram exact:
     G = diag(s) [sum_unflagged (q + c)(q + c)^T] diag(s) + sum_flagged y y^T."""
     y = np.asarray(y, dtype=np.float32)
     isl = inv_s.astype(np.longdouble)
+    # the kernel's rounding exactly: r = fp32(y inv_s + kf), kf = 2^23 + 32768 - c
+    # (one fma), in range iff 2^23 <= r <= 2^23 + 65535; just below 2^23 the fp32
+    # spacing is 1/2, so y inv_s - c in (-32768.5, -32768.25) is flagged although
+    # rint() would give -32768
+    kf = (8421376 - c.astype(np.int64)).astype(np.longdouble)
+    r = (y.astype(np.longdouble) * isl[:, None] + kf[:, None]).astype(np.float32).astype(np.float64)
+    flag = ((r < 8388608.0) | (r > 8388608.0 + 65535.0)).any(axis=0)
     q = np.rint(y.astype(np.longdouble) * isl[:, None] - c[:, None].astype(np.longdouble))
-    flag = ((q < -32768) | (q > 32767)).any(axis=0)
     qc = (q[:, ~flag].astype(np.int64) + c[:, None])
     assert float(np.max(np.abs(qc))) ** 2 * qc.shape[1] < 2.0 ** 62
     t = qc @ qc.T
