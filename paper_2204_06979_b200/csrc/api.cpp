@@ -742,15 +742,20 @@ hyde_status sharded_impl(hyde_handle h, CommOps& cm, const float* local, int loc
   const int first = chunk_len(0) < B ? chunk_len(0) : B;
   {
     Stage sg(h, HYDE_STAGE_EIG, 1, st);
-    CK(launch_noise_eig(Gm, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st));
+    CK(launch_noise_eig(Gm, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st,
+                        h->eig_cl, EIG_LANCZOS));
     sg.end();
   }
+  const bool lanczos = first < B && eig_lanczos_enabled();
   int rank = 0, chunks = 0, k0 = 0, comps = 0;
   for (int c = 0;; ++c) {
     const int cl = chunk_len(c);
     const int cnt = (B - k0) < cl ? (B - k0) : cl;
     if (c > 0) {
       Stage sg(h, HYDE_STAGE_EIG, 1, st);
+      if (c == 1 && lanczos)   // T and Q for the later chunks (the first chunk's W / U kept)
+        CK(launch_noise_eig(Gm, n, B, p.ridge, first, 0, sigma, nullptr, nullptr, house, tri, W, U, L.ldwu, st,
+                            h->eig_cl, EIG_RETRI));
       CK(launch_eigvec_more(tri, house, sigma, B, k0, cnt, nullptr, nullptr, W, U, L.ldwu, st));
       sg.end();
     }
