@@ -239,13 +239,18 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
     // as they land
     constexpr int NL = (CR * CC + 255) / 256;
     float v0[NL], v1[NL], v2[NL], v3[NL];
+    // interior tiles (no periodic wrap): one base offset, the element's
+    // (row, col) from the constant divide only
+    const bool interior = ilo >= 0 && jlo >= 0 && ilo + CR <= hs && jlo + CC <= ws;
+    const long long obase = (long long)ilo * ws + jlo;
 #pragma unroll
     for (int u = 0; u < NL; ++u) {
       const int idx = threadIdx.x + 256 * u;
       v0[u] = v1[u] = v2[u] = v3[u] = 0.f;
       if (idx < CR * CC) {
         const int r = idx / CC, c = idx - r * CC;
-        const long long o = (long long)wrap(ilo + r, hs) * ws + wrap(jlo + c, ws);
+        const long long o = interior ? obase + (long long)r * ws + c
+                                     : (long long)wrap(ilo + r, hs) * ws + wrap(jlo + c, ws);
         v0[u] = a_ll[o];
         v1[u] = a_lh[o];
         v2[u] = a_hl[o];
