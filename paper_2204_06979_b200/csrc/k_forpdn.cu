@@ -33,24 +33,29 @@ __device__ void thomas_factor(int B, double lam, double* inv_m, double* cp) {
   }
 }
 
-// noise power (HySime): mean_b (M_bb - delta (M^2)_bb) / (M_bb^2 N)
-__global__ void __launch_bounds__(NT) noise_power_kernel(const double* __restrict__ M, int B, double n, double ridge,
-                                                         double* out) {
-  __shared__ double red[NT / 32];
+// noise power (HySime): mean_b (M_bb - delta (M^2)_bb) / (M_bb^2 N).  One CTA
+// of 1024 threads, warp w takes rows b = w, w + 32, ...: lanes split k (all
+// loads of a row in flight), a warp sum, then the per-warp partials in a fixed
+// order.  (One thread per row walked 224 dependent-latency loads: 100 us.)
+constexpr int NPT = 1024;
+__global__ void __launch_bounds__(NPT) noise_power_kernel(const double* __restrict__ M, int B, double n, double ridge,
+                                                          double* out) {
+  __shared__ double red[NPT / 32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   double acc = 0.0;
-  for (int b = threadIdx.x; b < B; b += NT) {
+  for (int b = w; b < B; b += NPT / 32) {
     double m2 = 0.0;
-    for (int k = 0; k < B; ++k) m2 = fma(M[(size_t)b * B + k], M[(size_t)k * B + b], m2);
-    const double mbb = M[(size_t)b * B + b];
-    acc += (mbb - ridge * m2) / (mbb * mbb * n);
-  }
+    for (int k = l; k < B; k += 32) m2 = fma(M[(size_t)b * B + k], M[(size_t)k * B + b], m2);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    for (int o = 16; o > 0; o >>= 1) m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+    const double mbb = M[(size_t)b * B + b];
+    acc += (mbb - ridge * m2) / (mbb * mbb * n);   // same value in every lane
+  }
+  if (l == 0) red[w] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < NT / 32; ++w) t += red[w];
+    for (int q = 0; q < NPT / 32; ++q) t += red[q];
     *out = t / B;
   }
 }
@@ -70,16 +75,47 @@ __global__ void __launch_bounds__(NT) lambda_residual_kernel(const double* __res
   double acc = 0.0;
   const int j = threadIdx.x;
   if (j < B) {
-    auto solve = [&]() {   // column j of Z in place: Z[:, j] <- A^-1 Z[:, j]
+    // column j of Z in place: Z[:, j] <- A^-1 Z[:, j].  Both sweeps in blocks
+    // of LB rows with the next block's loads issued before this block's
+    // stores (a load cannot be hoisted over a store to Z by the compiler: one
+    // L2 round trip per row otherwise -- 200 us for the 4 grid values)
+    constexpr int LB = 16;
+    auto solve = [&]() {
       double d = 0.0;
-      for (int i = 0; i < B; ++i) {
-        d = (Z[(size_t)i * B + j] + (i > 0 ? lam * d : 0.0)) * inv_m[i];
-        Z[(size_t)i * B + j] = d;
+      double zc[LB], zn[LB];
+#pragma unroll
+      for (int u = 0; u < LB; ++u) zc[u] = u < B ? Z[(size_t)u * B + j] : 0.0;
+      for (int i0 = 0; i0 < B; i0 += LB) {
+#pragma unroll
+        for (int u = 0; u < LB; ++u) zn[u] = i0 + LB + u < B ? Z[(size_t)(i0 + LB + u) * B + j] : 0.0;
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int i = i0 + u;
+          if (i < B) {
+            d = (zc[u] + (i > 0 ? lam * d : 0.0)) * inv_m[i];
+            Z[(size_t)i * B + j] = d;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < LB; ++u) zc[u] = zn[u];
       }
       double x = d;
-      for (int i = B - 2; i >= 0; --i) {
-        x = Z[(size_t)i * B + j] - cp[i] * x;
-        Z[(size_t)i * B + j] = x;
+      // backward over rows B-2 .. 0, blocks from the top
+#pragma unroll
+      for (int u = 0; u < LB; ++u) zc[u] = B - 2 - u >= 0 ? Z[(size_t)(B - 2 - u) * B + j] : 0.0;
+      for (int i1 = B - 2; i1 >= 0; i1 -= LB) {
+#pragma unroll
+        for (int u = 0; u < LB; ++u) zn[u] = i1 - LB - u >= 0 ? Z[(size_t)(i1 - LB - u) * B + j] : 0.0;
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int i = i1 - u;
+          if (i >= 0) {
+            x = zc[u] - cp[i] * x;
+            Z[(size_t)i * B + j] = x;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < LB; ++u) zc[u] = zn[u];
       }
     };
     for (int i = 0; i < B; ++i) Z[(size_t)i * B + j] = Gw[(size_t)i * B + j];
@@ -138,7 +174,7 @@ __global__ void thomas_factor_kernel(int B, double lam_arg, const double* __rest
   coef[512] = (float)lam;
 }
 
-__global__ void __launch_bounds__(NT) thomas_solve_kernel(float* __restrict__ C, long long ldc, long long nc, int B,
+__global__ void __launch_bounds__(NT, 3) thomas_solve_kernel(float* __restrict__ C, long long ldc, long long nc, int B,
                                                           const float* __restrict__ coef) {
   __shared__ float s_alpha[256], s_cp[256];
   __shared__ float s_P[8][32], s_Q[8][32];
@@ -216,7 +252,7 @@ __global__ void __launch_bounds__(NT) thomas_solve_kernel(float* __restrict__ C,
 cudaError_t launch_forpdn_lambda(const double* M, const double* Gw, int B, long long n, double ridge, double* npow,
                                  double* rp, double* lam_out, double* Zs, cudaStream_t st) {
   if (B > 256) return cudaErrorInvalidValue;
-  noise_power_kernel<<<1, NT, 0, st>>>(M, B, (double)n, ridge, npow);
+  noise_power_kernel<<<1, NPT, 0, st>>>(M, B, (double)n, ridge, npow);
   lambda_residual_kernel<<<NGRID, NT, 0, st>>>(Gw, B, (double)n, Zs, rp);
   lambda_pick_kernel<<<1, 32, 0, st>>>(rp, npow, lam_out);
   return cudaGetLastError();
