@@ -1528,8 +1528,9 @@ hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int
   } else {
     CK(cudaMemcpyAsync(sc, &lambda, sizeof(double), cudaMemcpyHostToDevice, st));
   }
+  // V0: only the top r eigenpairs of W^T W (phase 2L when it converges)
   CK(launch_eig_raw(Gw, B, r, (double*)(ws + oOnes), (double*)(ws + oLam), V, r, house, tri, (float*)(ws + L.U),
-                    (float*)(ws + L.U), B, st));
+                    (float*)(ws + L.U), B, st, EIG_LANCZOS));
   CK(launch_v32(V, B, r, V32, B, st));
   CK(launch_sumsq(Cw, (long long)B * nc, (double*)(ws + oPart), sc + 1, st));
   int sweeps = 0;

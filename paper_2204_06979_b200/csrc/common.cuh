@@ -150,7 +150,8 @@ cudaError_t launch_hysime_select(const double* delta, const double* p, int B, do
 cudaError_t launch_eig_more_raw(const double* tri, const double* house, const double* ones, int B, int k0, int K,
                                 double* lam, double* V, int ldv, float* W, float* U, int ldwu, cudaStream_t st);
 cudaError_t launch_eig_raw(const double* Amat, int B, int ncomp, double* ones, double* lam, double* V, int ldv,
-                           double* house, double* tri, float* W, float* U, int ldwu, cudaStream_t st);
+                           double* house, double* tri, float* W, float* U, int ldwu, cudaStream_t st,
+                           int mode = 0);   // EIG_LANCZOS: the top ncomp pairs only (no T / Q afterwards)
 cudaError_t launch_eigvec_more(const double* tri, const double* house, const double* sigma, int B,
                                int k0, int ncomp, double* lam_top, double* V, float* W, float* U,
                                int ldwu, cudaStream_t st);

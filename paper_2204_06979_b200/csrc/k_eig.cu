@@ -2070,7 +2070,7 @@ cudaError_t launch_noise_eig_batched(int nb, const double* const* G, long long n
 // as the columns of V (row-major B x ldv).  ones[B] receives 1.0 (the "sigma"
 // of the raw mode, reused by launch_eigvec_more for later eigenpairs).
 cudaError_t launch_eig_raw(const double* Amat, int B, int ncomp, double* ones, double* lam, double* V, int ldv,
-                           double* house, double* tri, float* W, float* U, int ldwu, cudaStream_t st) {
+                           double* house, double* tri, float* W, float* U, int ldwu, cudaStream_t st, int mode) {
   if (B > BM || B < 3 || ncomp < 1) return cudaErrorInvalidValue;
   const EigWs ws = carve(house, B);
   cudaError_t e = cudaMemsetAsync(ws.flags, 0, 8 * sizeof(double), st);
@@ -2094,6 +2094,8 @@ cudaError_t launch_eig_raw(const double* Amat, int B, int ncomp, double* ones, d
   a.W = W;
   a.U = U;
   a.ldwu = ldwu;
+  a.lanczos = (mode == EIG_LANCZOS && eig_lanczos_enabled()) ? 1 : 0;
+  a.lzmax = g_lz_max;
   return run_k2(a, st);
 }
 
