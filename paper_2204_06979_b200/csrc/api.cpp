@@ -267,13 +267,12 @@ static cudaError_t run_gram(const Layout& L, char* ws, const float* cube, double
 }
 
 // forward DWT of `count` images at E (stride ldE) into C (stride N_c)
-// g0: first image of a group (its coefficient set and LL scratch slots)
 static cudaError_t dwt_forward(const Layout& L, char* ws, const float* E, long long ldE, int count,
-                               const FilterBank& fb, cudaStream_t st, long long g0 = 0) {
+                               const FilterBank& fb, cudaStream_t st) {
   const long long nc = L.plan.n_coeffs;
-  float* C = (float*)(ws + L.C) + g0 * nc;
+  float* C = (float*)(ws + L.C);
   long long sstr[2] = {(long long)L.s1_img, (long long)L.s2_img};
-  float* S[2] = {(float*)(ws + L.S1) + g0 * sstr[0], (float*)(ws + L.S2) + g0 * sstr[1]};
+  float* S[2] = {(float*)(ws + L.S1), (float*)(ws + L.S2)};
   for (int l = 0; l < L.levels; ++l) {
     const float* in = l == 0 ? E : S[(l - 1) & 1];
     long long in_str = l == 0 ? ldE : sstr[(l - 1) & 1];
@@ -290,9 +289,9 @@ static cudaError_t dwt_forward(const Layout& L, char* ws, const float* E, long l
 // soft-thresholded with its t* as it is loaded (K5 -> K6a fusion)
 static cudaError_t dwt_inverse(const Layout& L, char* ws, const float* Cin, float* Eout, long long ldE,
                                int count, const FilterBank& fb, const float* tstar, cudaStream_t st,
-                               const RankState* rs = nullptr, int k0 = 0, long long g0 = 0) {
+                               const RankState* rs = nullptr, int k0 = 0) {
   long long sstr[2] = {(long long)L.s1_img, (long long)L.s2_img};
-  float* S[2] = {(float*)(ws + L.S1) + g0 * sstr[0], (float*)(ws + L.S2) + g0 * sstr[1]};
+  float* S[2] = {(float*)(ws + L.S1), (float*)(ws + L.S2)};
   const long long nc = L.plan.n_coeffs;
   for (int l = L.levels - 1; l >= 0; --l) {
     const float* llin = (l == L.levels - 1) ? Cin + L.plan.ll_off : S[l & 1];
