@@ -307,7 +307,9 @@ hyde_status hyde_debug_gram_quant(hyde_handle h, int n_pixels, int bands, float*
 /* A1+A2: from G (fp64, bands x bands) and N: sigma[bands]; lam[bands] (all
  * eigenvalues of G_w = diag(sigma)^-1 G diag(sigma)^-1 / N, descending);
  * V[bands x ncomp] (row-major, eigenvectors of the ncomp largest, sign-fixed:
- * largest-|.| entry positive, SPEC.md:181 D6). */
+ * largest-|.| entry positive, SPEC.md:181 D6).  lam may be NULL; then for
+ * ncomp <= 6 the pairs come from the hot path's Lanczos phase (Householder
+ * when it does not converge), otherwise from the Householder reduction. */
 hyde_status hyde_k_eig(hyde_handle h, const double* gram, int n_pixels, int bands, double ridge,
                        int ncomp, double* sigma, double* lam, double* V, hyde_stream_t stream);
 /* A3: E[k][p] = sum_b W[b][k] Y[b][p], W = float32 row-major bands x ncomp. */

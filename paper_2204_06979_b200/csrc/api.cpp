@@ -1784,9 +1784,12 @@ hyde_status hyde_k_eig(hyde_handle h, const double* gram, int n_pixels, int band
   hyde_status s = ensure_ws(h, L.total, st);
   if (s != HYDE_OK) return s;
   char* ws = h->ws;
+  // without eigenvalues requested, a first chunk of <= EIG_LANCZOS_MAX_K pairs
+  // takes the hot path's phase 2L (the stage test of the Lanczos pairs)
+  const int mode = (!lam && ncomp > 0 && ncomp <= EIG_LANCZOS_MAX_K) ? EIG_LANCZOS : EIG_HOUSEHOLDER;
   CK(launch_noise_eig(gram, n_pixels, bands, ridge, ncomp, lam ? 1 : 0, sigma, lam, V,
                       (double*)(ws + L.house), (double*)(ws + L.tri), (float*)(ws + L.W),
-                      (float*)(ws + L.U), L.ldwu, st));
+                      (float*)(ws + L.U), L.ldwu, st, 0, mode));
   return HYDE_OK;
 }
 

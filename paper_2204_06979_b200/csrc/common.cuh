@@ -109,6 +109,7 @@ cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, 
 // launch_noise_eig modes: the first chunk by Lanczos when it converges (T and Q
 // then absent); the tridiagonal rerun (sigma given, W/U of the first ncomp kept)
 enum { EIG_HOUSEHOLDER = 0, EIG_LANCZOS = 1, EIG_RETRI = 2 };
+constexpr int EIG_LANCZOS_MAX_K = 6;   // phase 2L serves at most this many pairs (k_eig.cu LZK)
 bool eig_lanczos_enabled();
 size_t eig_args_bytes();
 double* eig_flags_ptr(double* house, int B);

@@ -690,7 +690,7 @@ struct K2Smem {
 };
 // phase 2L basis: colK .. cw (see K2Smem)
 constexpr int LVD = 2 * BM * NB + 2 * NB * BM + 2 * NW * BM;
-constexpr int LZK = 6;     // phase 2L serves first chunks of at most LZK pairs (zb rows: K vectors + 4K scratch)
+constexpr int LZK = EIG_LANCZOS_MAX_K;   // phase 2L serves first chunks of at most LZK pairs (zb rows: K vectors + 4K scratch)
 static_assert(8 + 4 * LZK <= KM, "phase 2L scratch rows");
 
 // Two Sturm counts at once (independent chains interleaved: the dependent

@@ -189,6 +189,35 @@ def test_eigenpairs_are_eigenpairs(hy, b, r, c, kmax):
         assert V[i, j] > 0
 
 
+@pytest.mark.parametrize("name", ["tiny", "small", "medium", "wide"])
+def test_lanczos_first_chunk_matches_oracle(hy, name):
+    """The hot path's first chunk (K2 phase 2L: Lanczos on G_w - I, hyde_k_eig without
+    eigenvalues, K = 4): every pair is an eigenpair of G_w, its Rayleigh quotient is the
+    oracle's eigenvalue, the vectors match the oracle's (D6 signs) where the eigenvalue is
+    separated from its neighbours, and they are orthonormal."""
+    s = synth.make_cube(name, 0)
+    b, r, c = s.noisy.shape
+    n = r * c
+    g = O.gram(s.noisy)
+    sig_ref, _ = O.estimate_noise(s.noisy)
+    lam_ref, v_ref, gw = O.whiten_eig(g, sig_ref, n)
+    k = 4
+    sig, lam, V = hy.stages.eig(dev(g), n, k, all_lam=False)
+    assert lam is None
+    sig, V = sig.cpu().numpy(), V.cpu().numpy()
+    assert np.max(np.abs(sig / sig_ref - 1)) < 1e-9
+    gw = g / np.outer(sig, sig) / n
+    rq = np.einsum("ij,ij->j", V, gw @ V)
+    assert np.max(np.abs(rq - lam_ref[:k])) < 1e-11 * lam_ref[0]
+    assert np.max(np.abs(gw @ V - V * rq[None, :])) < 1e-9 * lam_ref[0]
+    assert np.max(np.abs(V.T @ V - np.eye(k))) < 1e-10
+    for j in range(k):
+        gap = min([abs(lam_ref[j] - lam_ref[i]) for i in range(b) if i != j])
+        if gap > 1e-6 * lam_ref[0]:
+            err = np.max(np.abs(V[:, j] - v_ref[:, j]))
+            assert err < 1e-12 * lam_ref[0] / gap + 1e-10, (j, err, gap)
+
+
 def test_estimate_noise_api(hy):
     s = synth.make_cube("small", 0)
     sig, g, res = hy.estimate_noise(dev(s.noisy), return_gram=True, return_residual=True)
