@@ -488,13 +488,18 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
       if (tid == 0) s_kmax = 0u;
       __syncthreads();
       if (p1) {
+        // bins 0..HB-1 cover [KB0, KE0]; below -> HB, above -> HB + 1 (the
+        // first bin width past KE0 included: it was counted as "below"); the
+        // largest key is a register max, one shared atomic per thread
+        unsigned kmx = 0u;
         stream_keys(x, ns, [&](unsigned k, int) {
-          int b = (int)(k >> HS0) - (int)(KB0 >> HS0);
-          b = b < 0 ? HB : b;
-          if (b >= HB + 1) { b = HB + 1; atomicMax(&s_kmax, k); }
+          const int br = (int)(k >> HS0) - (int)(KB0 >> HS0);
+          const int b = br < 0 ? HB : (br >= HB ? HB + 1 : br);
+          kmx = max(kmx, k);
           atomicAdd(hcnt + b, 1u);
           atomicAdd(hsum + b, fxsq(k));
         });
+        if (kmx > KE0) atomicMax(&s_kmax, kmx);
       } else {
         stream_keys(x, ns, [&](unsigned k, int) {
           if (k >= bl && k <= bh) {

@@ -352,6 +352,37 @@ def test_sure_edge_cases(hy):
                 assert ks[i, j] == sr.k and ts[i, j] == np.float32(sr.t), (i, j, ks[i, j], sr.k)
 
 
+def test_sure_catch_all_bin_edges(hy):
+    """Keys at the edges of the first histogram pass's binned range [2^-40, 2^24): values
+    in [2^24, 2^24 (1 + 1/64)) -- the first bin width past the range -- belong to the
+    high catch-all bin, values just under 2^-40 to the low one; both in big subbands (the
+    histogram path, n > 8192) and mixed with unit noise.  k* / t* bit-exact vs the
+    oracle's exact SURE, E_post to 1e-12."""
+    r, c, lv = 256, 256, 1
+    nc = O.coeff_count(r, c, lv)
+    rng = np.random.default_rng(9)
+    rows = []
+    for big in (2.0 ** 24, 2.0 ** 24 * 1.01, 2.0 ** 24 * (1 + 1 / 64), 3.0e7):
+        a = rng.standard_normal(nc)
+        idx = rng.choice(nc, 40, replace=False)
+        a[idx[:20]] = big * (1 + 1e-3 * rng.random(20)) * np.sign(rng.standard_normal(20))
+        a[idx[20:]] = 2.0 ** -41 * (1 + rng.random(20))
+        rows.append(a)
+    co = np.stack(rows).astype(np.float32)
+    g = dev(co)
+    ks, ts, ep = hy.stages.sure(g, r, c, lv)
+    ks, ts, ep = ks.cpu().numpy(), ts.cpu().numpy(), ep.cpu().numpy()
+    for i in range(co.shape[0]):
+        res, offs = _oracle_sure_on(co[i], r, c, lv)
+        e_ref = 0.0
+        for j, sr in enumerate(res):
+            scale = offs[j + 1] - offs[j] + float(np.sum(co[i, offs[j]:offs[j + 1]].astype(np.float64) ** 2))
+            if sr.margin > 1e-9 * scale:
+                assert ks[i, j] == sr.k and ts[i, j] == np.float32(sr.t), (i, j, ks[i, j], sr.k)
+            e_ref += float(np.sum(O.soft_threshold(co[i, offs[j]:offs[j + 1]].astype(np.float64), float(ts[i, j])) ** 2))
+        assert abs(ep[i] - e_ref) <= 1e-12 * e_ref, (i, ep[i], e_ref)
+
+
 def test_reconstruct_matches_fp64(hy):
     rng = np.random.default_rng(5)
     for b, n, r in [(224, 4096, 1), (32, 1001, 3), (200, 21025, 9), (17, 64, 17)]:
