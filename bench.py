@@ -277,6 +277,19 @@ def cpu_baseline(cube, reps=2):
 
 
 # ------------------------------------------------------------------ reference arm
+def config_dict(cfg, world, batched, sharded, ncube, nbytes):
+    """The workload keys of a bench line -- identical for both arms at N = 1
+    (the reference arm's sample is the same seed-0 cube); run results go under
+    "result"."""
+    return {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols, "bands": cfg.bands,
+            "cubes_per_rank": ncube,
+            "seeds": (f"batch of {cfg.batch} (seeds 0..{cfg.batch - 1}) round-robin over ranks"
+                      if batched else ("one cube (seed 0), pixel-row slabs per rank (hyde_hyres_sharded)"
+                                       if sharded else f"rank r uses seed r (0..{world - 1})")),
+            "l2": (f"inputs larger than L2 ({nbytes / 1e6:.0f} MB per rank > 126 MB L2); no flush"
+                   if nbytes > 126e6 else "cube fits in L2: steps run back to back (L2-warm)")}
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return 0
@@ -297,8 +310,7 @@ def run_reference(args, cfg, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols, "bands": cfg.bands,
-                   "seed": 0},
+        "config": config_dict(cfg, 1, cfg.batch > 1, False, 1, cube.nbytes),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"full {cfg.name} cube per step (oracle.hyres, numpy fp64, as it stands)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -680,14 +692,8 @@ def main():
         "ms_per_step_olympic": olympic, "ms_per_step_min": min(per_step), "ms_per_step_max": max(per_step),
         "higher_is_better": True, "scaling": "strong" if (batched or sharded) else "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols,
-                   "bands": cfg.bands, "cubes_per_rank": ncube,
-                   "seeds": (f"batch of {cfg.batch} (seeds 0..{cfg.batch - 1}) round-robin over ranks"
-                             if batched else ("one cube (seed 0), pixel-row slabs per rank (hyde_hyres_sharded)"
-                                              if sharded else f"rank r uses seed r (0..{world - 1})")),
-                   "l2": (f"inputs larger than L2 ({nbytes / 1e6:.0f} MB per rank > 126 MB L2); no flush"
-                          if nbytes > 126e6 else "cube fits in L2: steps run back to back (L2-warm)"),
-                   "rank": rank_k, "levels": info["levels"], "chunks": chunks, "components": comps},
+        "config": config_dict(cfg, world, batched, sharded, ncube, nbytes),
+        "result": {"rank": rank_k, "levels": info["levels"], "chunks": chunks, "components": comps},
         "roofline": roof,
         "stages": per,
         "e2e": {"value": (1 if sharded else world * ncube) * cfg.voxels / e2e_s, "unit": UNIT,

@@ -32,11 +32,13 @@
 //
 // Structure: clusters of 2 CTAs (one SM pair) per pixel range, cta_group::2
 // MMAs with M = 128 (64 rows per SM, TMEM "2x2" layout).  Bands are split
-// S_a = [0,128), S_b = [128,B); three tiles T_aa (128 x 128), T_ab (128 x Nb),
-// T_bb (128 x Nb), Nb = B-128 rounded up to 32; x 3 products = 480 of 512
-// TMEM columns for B <= 224.  14 converter warps per CTA load fp32 straight
-// from HBM (16-byte loads), quantise and write the int8 slices into shared
-// memory in the UMMA canonical K-major layout; one thread of the leader CTA
+// S_a = [0,128), S_b = [128,B), Nb = B-128 rounded up to 32; two tiles:
+// T_a* = [T_aa | T_ab] (128 x (128 + Nb): A = S_a, B = S_a then S_b in ONE
+// MMA per product) and T_bb (128 x Nb); x 3 products = 480 of 512 TMEM
+// columns for B <= 224.  A TMA producer streams fp32 tiles into a 2-stage
+// ring; 13 converter warps per CTA quantise them and write the int8 slices
+// into shared memory in the UMMA canonical K-major layout; one thread of the
+// leader CTA
 // issues the MMAs; the stage ring is released by tcgen05.commit multicast to
 // both CTAs.  Each CTA finally reads its TMEM, combines the three products in
 // int64 and writes its exact integer partial.
@@ -103,6 +105,7 @@ struct GramTc {
   const GramQScale* qs;
   long long* partial;  // [pair][B*B + B]: Q Q^T over the pair's pixels, then sum q per band
   unsigned* bitmap;    // clipped-pixel bits
+  int exp;             // experiments only (HYDE_GRAM_EXP; wrong results, timing): 1 no MMAs, 2 no T_bb MMAs, 4 no conversion
 };
 
 // smem regions of one int8 slice of a stage: P (64 rows: S_a bands of this SM)
@@ -219,25 +222,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
   // TMEM column map per product level: T_aa 64 cols, T_ab nb/2, T_bb nb/2
   const int CL = 64 + nb;
-  const int off_ab = 64, off_bb = 64 + nb / 2;
+  const int off_bb = 64 + nb / 2;
 
   if (warp == 0) {
     // ================= forwarder: converters' stage s -> leader's bar_full ===
     for (int s = 0; s < nst; ++s) {
       const int is = s % NI;
       asm volatile("bar.sync %0, %1;" ::"r"(1 + is), "r"((NCW + 1) * 32) : "memory");
-      if (lane == 0) tc::mbar_arrive_cluster(&bar_full[is], 0);
+      if (lane == 0) {
+        // CTA-scope release (the converters' writes were fenced to the async
+        // proxy and joined by the named barrier; a cluster-scope release
+        // compiles to MEMBAR.ALL.GPU on this thread: 3-4 us per gram call)
+        tc::mbar_arrive_cluster_cta(&bar_full[is], 0);
+      }
     }
   } else if (warp == 1) {
     // ================= MMA issuer (leader CTA, one thread) =================
     if (rank == 0 && lane == 0 && nst > 0) {
-      // S0 (high bytes) signed, S1 (low bytes) unsigned
-      const uint32_t id_aa = tc::idesc_i8(128, 128, true, true);
-      const uint32_t id_aa01 = tc::idesc_i8(128, 128, true, false);
-      const uint32_t id_aa11 = tc::idesc_i8(128, 128, false, false);
+      // S0 (high bytes) signed, S1 (low bytes) unsigned.  B <= 128: T_aa
+      // (N = 128).  B > 128: T_a* = [T_aa | T_ab] with A = P and B = [P ; QS]
+      // -- this CTA's 64 P rows then its nb/2 QS rows, contiguous in the slice
+      // -- in ONE MMA per product (N = 128 + nb), plus T_bb (A = QS, B = the
+      // live QS rows, N = nb): 7 MMAs per k-slice instead of 10 with a
+      // separate T_ab (large: gram stage 254 -> 227 us on the same box).
+      const int Na = 128 + nb;
+      const uint32_t id_a00 = tc::idesc_i8(128, Na, true, true);
+      const uint32_t id_a01 = tc::idesc_i8(128, Na, true, false);
+      const uint32_t id_a10 = nb > 0 ? tc::idesc_i8(128, Na, false, true) : 0u;
+      const uint32_t id_a11 = tc::idesc_i8(128, Na, false, false);
       const uint32_t id_b = nb > 0 ? tc::idesc_i8(128, nb, true, true) : 0u;
       const uint32_t id_b01 = nb > 0 ? tc::idesc_i8(128, nb, true, false) : 0u;
-      const uint32_t id_b10 = nb > 0 ? tc::idesc_i8(128, nb, false, true) : 0u;
       const uint32_t id_b11 = nb > 0 ? tc::idesc_i8(128, nb, false, false) : 0u;
       const uint32_t sbase = tc::smem_u32(smem);
       for (int s = 0; s < nst; ++s) {
@@ -246,27 +260,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         tc::tc_fence_after();
         const uint32_t st0 = sbase + is * stage_bytes;   // S0 slice
         const uint32_t st1 = st0 + slice_bytes;           // S1 slice
+        if (P.exp & 1) {   // experiment: no MMAs
+          tc::mma_commit<2>(&bar_empty[is], 0x3);
+          continue;
+        }
         for (int ks = 0; ks < KC / 32; ++ks) {
-          auto dsc = [&](uint32_t slice, int rg, int row0) -> uint64_t {
-            (void)row0;
+          auto dsc = [&](uint32_t slice, int rg) -> uint64_t {
             return tc::sdesc_kmajor_sw128(slice + region_base(rg) + ks * 32);
           };
           const uint32_t first = (s == 0 && ks == 0) ? 0u : 1u;
-          // T_aa: A = P, B = P
-          tc::mma_i8<2>(tmem + 0 * CL, dsc(st0, 0, 0), dsc(st0, 0, 0), id_aa, first);
-          // diagonal tiles: only X = S0 S1^T (the cross term is X + X^T,
-          // symmetrised in the reduction) -- one MMA of four saved
-          tc::mma_i8<2>(tmem + 1 * CL, dsc(st0, 0, 0), dsc(st1, 0, 0), id_aa01, first);
-          tc::mma_i8<2>(tmem + 2 * CL, dsc(st1, 0, 0), dsc(st1, 0, 0), id_aa11, first);
+          tc::mma_i8<2>(tmem + 0 * CL, dsc(st0, 0), dsc(st0, 0), id_a00, first);
+          tc::mma_i8<2>(tmem + 1 * CL, dsc(st0, 0), dsc(st1, 0), id_a01, first);
           if (nb > 0) {
-            // T_ab: A = P, B = QB ; T_bb: A = QA, B = QB
-            tc::mma_i8<2>(tmem + 0 * CL + off_ab, dsc(st0, 0, 0), dsc(st0, 1, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st0, 0, 0), dsc(st1, 1, 0), id_b01, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_ab, dsc(st1, 0, 0), dsc(st0, 1, 0), id_b10, 1u);
-            tc::mma_i8<2>(tmem + 2 * CL + off_ab, dsc(st1, 0, 0), dsc(st1, 1, 0), id_b11, first);
-            tc::mma_i8<2>(tmem + 0 * CL + off_bb, dsc(st0, 1, 0), dsc(st0, 1, 0), id_b, first);
-            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1, 0), dsc(st1, 1, 0), id_b01, first);
-            tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1, 0), dsc(st1, 1, 0), id_b11, first);
+            // the cross accumulator of T_a* holds S0 S1^T + S1 S0^T (the T_ab
+            // block needs both; on the diagonal block it is the symmetric sum)
+            tc::mma_i8<2>(tmem + 1 * CL, dsc(st1, 0), dsc(st0, 0), id_a10, 1u);
+          }
+          // (B <= 128: the diagonal tile holds X = S0 S1^T only; the cross
+          // term X + X^T is symmetrised in the reduction -- one MMA saved)
+          tc::mma_i8<2>(tmem + 2 * CL, dsc(st1, 0), dsc(st1, 0), id_a11, first);
+          if (nb > 0 && !(P.exp & 2)) {
+            // T_bb: A = QS, B = the live QS rows; cross term X = S0 S1^T only
+            tc::mma_i8<2>(tmem + 0 * CL + off_bb, dsc(st0, 1), dsc(st0, 1), id_b, first);
+            tc::mma_i8<2>(tmem + 1 * CL + off_bb, dsc(st0, 1), dsc(st1, 1), id_b01, first);
+            tc::mma_i8<2>(tmem + 2 * CL + off_bb, dsc(st1, 1), dsc(st1, 1), id_b11, first);
           }
         }
         tc::mma_commit<2>(&bar_empty[is], 0x3);
@@ -415,7 +432,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       tc::mbar_wait(&bar_empty[is], (uint32_t)(((s / NI) & 1) ^ 1));   // local barrier (commit multicast)
       unsigned char* st0 = smem + is * stage_bytes;
       unsigned char* st1 = st0 + slice_bytes;
-      if (tile_px(s) + KC <= px_lim)
+      if (P.exp & 4) {
+      } else if (tile_px(s) + KC <= px_lim)
         convert(std::true_type{}, s, v, st0, st1);
       else
         convert(std::false_type{}, s, v, st0, st1);
@@ -468,9 +486,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         tc::tc_fence_after();
       }
       const int ntile = nb > 0 ? 3 : 1;
+      const bool merged = nb > 0;   // tile 0 is T_a* = [T_aa | T_ab]
+      const int hb = nb / 2;
       for (int t = 0; t < ntile; ++t) {
-        const int Nt = t == 0 ? 128 : nb;
-        const int coff = t == 0 ? 0 : (t == 1 ? off_ab : off_bb);
+        if (t == 1) continue;          // (T_ab is part of tile 0)
+        const int Nt = t == 0 ? 128 + nb : nb;
+        const int coff = t == 0 ? 0 : off_bb;
         // row band i and its scale; column bands j
         const int rg_i = t == 2 ? 1 : 0;
         const int bi = band_of(rg_i, m, rank, B, nb);
@@ -490,14 +511,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int nn = c0 + j + (Nt / 2) * half;    // column within the tile
-            const int bj = t == 0 ? (nn < (B < 128 ? B : 128) ? nn : -1) : (128 + nn < B ? 128 + nn : -1);
+            int bj;
+            if (merged && t == 0) {   // column half h = CTA h's B rows: its 64 P bands, then its hb QS bands
+              const int rho = c0 + j;
+              bj = rho < 64 ? 64 * half + rho : 128 + hb * half + (rho - 64);
+              bj = bj < B ? bj : -1;
+            } else {
+              bj = t == 0 ? (nn < (B < 128 ? B : 128) ? nn : -1) : (128 + nn < B ? 128 + nn : -1);
+            }
             if (bj < 0) continue;
-            // T_ab holds S0 S1^T + S1 S0^T; the diagonal tiles hold X = S0 S1^T only:
-            // 512 X here, (P + P^T) / 2 in the reduction gives 256 (X + X^T).
+            // T_a* (B > 128) holds S0 S1^T + S1 S0^T: weight 256; T_bb and the
+            // B <= 128 T_aa hold X = S0 S1^T only: 512 X here, (P + P^T) / 2 in
+            // the reduction gives 256 (X + X^T).
             // The partial is the EXACT integer (Q Q^T over this pair's pixels):
             // the reduction sums integers and scales once, so G does not depend
             // on how the pixels were split over pairs.
-            const long long qq = 65536LL * (long long)(int)a0[j] + (t == 1 ? 256LL : 512LL) * (long long)(int)a1[j] +
+            const long long qq = 65536LL * (long long)(int)a0[j] + (merged && t == 0 ? 256LL : 512LL) * (long long)(int)a1[j] +
                                  (long long)(int)a2[j];
             Pq[(long long)bi * B + bj] = qq;
           }
@@ -1064,6 +1093,10 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
   P.qs = w.qs;
   P.partial = w.partial;
   P.bitmap = w.bitmap;
+  {
+    static const int gexp = [] { const char* ev = getenv("HYDE_GRAM_EXP"); return ev ? atoi(ev) : 0; }();
+    P.exp = gexp;
+  }
   CUtensorMap tmP, tmQ;
   const bool tma = (n % 4 == 0) && (((uintptr_t)Y & 15) == 0) && !getenv("HYDE_GRAM_NO_TMA") &&
                    make_maps(Y, n, B, P.nb / 2, &tmP, &tmQ);

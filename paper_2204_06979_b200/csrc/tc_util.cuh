@@ -43,6 +43,12 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
   uint32_t a = mapa(smem_u32(bar), rank);
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
+// same, CTA-scope release (no GPU-scope membar): for arrivals that only
+// publish this CTA's async-proxy-fenced shared-memory writes
+__device__ __forceinline__ void mbar_arrive_cluster_cta(uint64_t* bar, uint32_t rank) {
+  uint32_t a = mapa(smem_u32(bar), rank);
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
