@@ -663,15 +663,17 @@ def main():
                 "frac_nominal_8tbs": round(ach / NOMINAL_HBM_GBS, 4)}
     else:   # K2: one 16-CTA cluster, fp64, a B-step dependency chain
         ncta = hy.eig_cluster_size() or 16
+        if batched:   # ONE launch of 8-CTA clusters for the whole batch: up to 18 clusters (144 SMs) at once
+            ncta = 8 * min(ncube, 148 // 8)
         flops = ncube * k2_flops(cfg.bands)
         pk = probe_peaks()
         if pk.get("fp64_tflops_per_sm"):
             peak = ncta * float(pk["fp64_tflops_per_sm"])
-            psrc = (f"measured: {ncta} SMs (one cluster) x {pk['fp64_tflops_per_sm']} fp64 TFLOP/s per SM "
+            psrc = (f"measured: {ncta} SMs ({'the concurrent clusters' if batched else 'one cluster'}) x {pk['fp64_tflops_per_sm']} fp64 TFLOP/s per SM "
                     f"(tools/probe_peaks.cu, profiles/r02_peaks.json; whole GPU {pk.get('fp64_tflops')} TFLOP/s)")
         else:
             peak = ncta * 64 * 2 * 1.965e9 / 1e12      # DFMA/clk/SM x 2 flops x max SM clock
-            psrc = f"derived: {ncta} SMs (one cluster) x 64 DFMA/clk x 2 x 1965 MHz"
+            psrc = f"derived: {ncta} SMs x 64 DFMA/clk x 2 x 1965 MHz"
         ach = flops / (t * 1e-3) / 1e12
         roof = {"kernel": kern, "stage": dom, "bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4),
                 "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": tr["bytes"] if tr else None,
