@@ -161,6 +161,77 @@ __global__ void __launch_bounds__(128) l1spec_first_kernel(const float* __restri
   if ((threadIdx.x & 31) == 0 && live) tile_todo[p >> 5] = more;
 }
 
+// (1b) the same first iteration with the forward-sweep scratch y in SHARED
+// memory ([B][CP] per CTA of CP pixels) instead of X: the stage then moves the
+// method's minimum bytes (read M once, write X once) -- the X-scratch kernel's
+// y spills past the L2 (ncu at `large`: 2.55 GB of DRAM traffic for 1.88 GB).
+// Fewer pixels fit per SM (~7 CTAs of 32), so the forward sweep keeps a
+// deeper window of M loads in flight (L1S bands, double-buffered in
+// registers).  Same arithmetic in the same order as (1): bit-identical.
+template <int CP, int L1S>
+__global__ void __launch_bounds__(CP) l1spec_first_smem_kernel(const float* __restrict__ M, float* __restrict__ X,
+                                                               long long n, int B, float tol, int max_iters,
+                                                               int* __restrict__ iters_out,
+                                                               unsigned* __restrict__ tile_todo, const ThomasF tf) {
+  extern __shared__ float l1sh[];
+  float* s_alpha = l1sh;
+  float* s_cp = l1sh + 256;
+  float* ys = l1sh + 512;   // y[i][t] at ys[i * CP + t]
+  for (int i = threadIdx.x; i < B; i += CP) {
+    s_alpha[i] = tf.alpha[i];
+    s_cp[i] = tf.cp[i];
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const long long p = blockIdx.x * (long long)CP + t;
+  const bool live = p < n;
+  float xo2 = 0.f, dx2 = 0.f;
+  if (live) {
+    float y = 0.f;
+    float mc[L1S], mn[L1S];
+#pragma unroll
+    for (int u = 0; u < L1S; ++u) mc[u] = u < B ? __ldcs(M + (size_t)u * n + p) : 0.f;
+    for (int i0 = 0; i0 < B; i0 += L1S) {
+#pragma unroll
+      for (int u = 0; u < L1S; ++u) {
+        const int i = i0 + L1S + u;
+        mn[u] = i < B ? __ldcs(M + (size_t)i * n + p) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < L1S; ++u) {
+        const int i = i0 + u;
+        if (i < B) {
+          const float m = mc[u];
+          xo2 = fmaf(m, m, xo2);
+          y = s_alpha[i] * (y + m);
+          ys[i * CP + t] = y;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < L1S; ++u) mc[u] = mn[u];
+    }
+    float x1 = 0.f, x2 = 0.f;   // x_{i+1}, x_{i+2}
+    for (int i = B - 1; i >= 0; --i) {
+      const float x = fmaf(-s_cp[i], x1, ys[i * CP + t]);
+      __stcs(X + (size_t)i * n + p, x);
+      if (i + 1 <= B - 1) {   // (D^T D x)_{i+1} now that x_i is known
+        const float tt = (i + 1 == B - 1) ? x1 - x : (2.f * x1 - x - x2);
+        dx2 = fmaf(tt, tt, dx2);
+      }
+      x2 = x1;
+      x1 = x;
+    }
+    if (B >= 2) {
+      const float tt = x1 - x2;   // row 0: x_0 - x_1
+      dx2 = fmaf(tt, tt, dx2);
+    }
+  }
+  const bool stop = live && (max_iters <= 1 || sqrtf(dx2) <= tol * sqrtf(xo2));
+  if (live && iters_out) iters_out[p] = 1;
+  const unsigned more = __ballot_sync(0xffffffffu, live && !stop);
+  if ((t & 31) == 0 && live) tile_todo[p >> 5] = more;
+}
+
 // (2) later iterations of the marked pixels, one warp per pixel, from x_1
 template <int S>
 __global__ void __launch_bounds__(NT) l1spec_kernel(const float* __restrict__ M, float* __restrict__ X, long long n,
@@ -390,7 +461,24 @@ cudaError_t launch_l1spec(const float* M, float* X, long long n, int B, float la
       attr_done = true;
     }
   }
-  l1spec_first_kernel<<<(unsigned)((n + 127) / 128), 128, pad, st>>>(M, X, n, B, tol, max_iters, iters, todo, tf);
+  static const int smem_mode = [] {
+    const char* ev = getenv("HYDE_L1_SMEM");   // experiments: 0 = X scratch, 32 / 64 = y in shared memory
+    return ev ? atoi(ev) : 0;
+  }();
+  if (smem_mode == 32 || smem_mode == 64) {
+    const size_t shb = (size_t)(512 + B * smem_mode) * sizeof(float);
+    if (smem_mode == 32) {
+      cudaFuncSetAttribute(l1spec_first_smem_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb);
+      l1spec_first_smem_kernel<32, 64><<<(unsigned)((n + 31) / 32), 32, shb, st>>>(M, X, n, B, tol, max_iters, iters,
+                                                                                  todo, tf);
+    } else {
+      cudaFuncSetAttribute(l1spec_first_smem_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb);
+      l1spec_first_smem_kernel<64, 64><<<(unsigned)((n + 63) / 64), 64, shb, st>>>(M, X, n, B, tol, max_iters, iters,
+                                                                                  todo, tf);
+    }
+  } else {
+    l1spec_first_kernel<<<(unsigned)((n + 127) / 128), 128, pad, st>>>(M, X, n, B, tol, max_iters, iters, todo, tf);
+  }
   cudaError_t e = cudaGetLastError();
   if (getenv("HYDE_DEBUG_SYNC")) {
     e = cudaStreamSynchronize(st);
