@@ -468,7 +468,7 @@ hyde_status hyde_hyres_ex(hyde_handle h, const float* cube, int rows, int cols, 
   float* U = (float*)(ws + L.U);
   float* C = (float*)(ws + L.C);
   {
-    Stage sg(h, HYDE_STAGE_GRAM, L.use_tc ? 5 : 2, st);
+    Stage sg(h, HYDE_STAGE_GRAM, L.use_tc ? gram_tc_launches() : 2, st);
     // tensor-core path: the state words are zeroed by the Gram's first (zero) kernel
     CK(run_gram(L, ws, cube, G, &rs->nonfinite, st, L.use_tc ? (int*)rs : nullptr));
     sg.end();
@@ -727,7 +727,7 @@ hyde_status sharded_impl(hyde_handle h, CommOps& cm, const float* local, int loc
   float* C = (float*)(ws + L.C);
   // ---- A1: local Gram of the slab, all-reduced; a global finiteness check ----
   {
-    Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? 6 : 3, st);
+    Stage sg(h, HYDE_STAGE_GRAM, Ll.use_tc ? gram_tc_launches() + 1 : 3, st);
     if (Ll.use_tc)
       CK(launch_gram_tc(local, n_loc, B, wl + Ll.partial, Ll.npairs, Gm, &rs->nonfinite, st));
     else

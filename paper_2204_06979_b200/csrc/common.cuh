@@ -93,6 +93,7 @@ struct GramQScale {
 };
 // workspace of launch_gram_tc (scales, clip bitmap, int64 pair partials, fix partials)
 size_t gram_tc_ws_bytes(long long n, int B, int npairs);
+int gram_tc_launches();   // kernels launch_gram_tc enqueues (4; 5 with HYDE_GRAM_REDUCE)
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npairs, double* G, int* nonfinite,
                            cudaStream_t st, int* state4 = nullptr);
 size_t gram_job_bytes();

@@ -105,6 +105,7 @@ struct GramTc {
   const GramQScale* qs;
   long long* partial;  // [pair][B*B + B]: Q Q^T over the pair's pixels, then sum q per band
   unsigned* bitmap;    // clipped-pixel bits
+  int atomic_sum;      // 1: pairs add their exact partials into partial[0] (zeroed by qscale) -- no reduce kernel
   int exp;             // experiments only (HYDE_GRAM_EXP; wrong results, timing): 1 no MMAs, 2 no T_bb MMAs, 4 no conversion
 };
 
@@ -460,7 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     // sum_p q of every unit's band over this pair's pixels (exact int64)
     {
-      long long* Q1 = P.partial + (long long)pair * ((long long)B * B + B) + (long long)B * B;
+      long long* Q1 = P.partial + (P.atomic_sum ? 0LL : (long long)pair * ((long long)B * B + B)) + (long long)B * B;
 #pragma unroll
       for (int t = 0; t < MAXU; ++t) {
         const int u = cw + t * NCW;
@@ -470,7 +471,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) {
           const int b = u < nrow_p ? rank * 64 + u : 128 + rank * hb + (u - nrow_p);
-          Q1[b] = v;
+          if (!P.atomic_sum) Q1[b] = v;
+          else if (v != 0) atomicAdd(reinterpret_cast<unsigned long long*>(Q1 + b), (unsigned long long)v);
         }
       }
     }
@@ -480,7 +482,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const int q4 = warp & 3;                    // TMEM lane quadrant of this warp
       const int L = q4 * 32 + lane;               // TMEM lane = this thread's row slot
       const int m = L & 63, half = L >> 6;
-      long long* Pq = P.partial + (long long)pair * ((long long)B * B + B);
+      // atomic_sum: every pair adds its exact integer partial into partial[0]
+      // (integer adds: the sum does not depend on their order)
+      long long* Pq = P.partial + (P.atomic_sum ? 0LL : (long long)pair * ((long long)B * B + B));
       if (nst > 0) {
         tc::mbar_wait_cluster(&bar_done, 0);
         tc::tc_fence_after();
@@ -528,7 +532,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             // on how the pixels were split over pairs.
             const long long qq = 65536LL * (long long)(int)a0[j] + (merged && t == 0 ? 256LL : 512LL) * (long long)(int)a1[j] +
                                  (long long)(int)a2[j];
-            Pq[(long long)bi * B + bj] = qq;
+            if (!P.atomic_sum) Pq[(long long)bi * B + bj] = qq;
+            else if (qq != 0) atomicAdd(reinterpret_cast<unsigned long long*>(Pq + (long long)bi * B + bj), (unsigned long long)qq);
           }
         }
       }
@@ -562,7 +567,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 // rank-state words -- the first kernel of the step.
 __global__ void __launch_bounds__(256)
     gram_qscale_kernel(const float* __restrict__ Y, long long n, GramQScale* qs, unsigned* bitmap, long long nwords,
-                       int* st4, int nst4, const GramJob* __restrict__ jobs) {
+                       int* st4, int nst4, const GramJob* __restrict__ jobs, long long* zs = nullptr,
+                       long long nzs = 0) {
   pdl_wait();
   if (jobs) {
     const GramJob& j = jobs[blockIdx.y];
@@ -577,6 +583,10 @@ __global__ void __launch_bounds__(256)
     const long long w0 = nwords * blockIdx.x / gridDim.x, w1 = nwords * (blockIdx.x + 1) / gridDim.x;
     for (long long w = w0 + threadIdx.x; w < w1; w += blockDim.x) bitmap[w] = 0u;
     if (st4 && blockIdx.x == 0 && (int)threadIdx.x < nst4) st4[threadIdx.x] = 0;
+    if (zs) {   // the atomic Gram sum's accumulator
+      const long long z0 = nzs * blockIdx.x / gridDim.x, z1 = nzs * (blockIdx.x + 1) / gridDim.x;
+      for (long long z = z0 + threadIdx.x; z < z1; z += blockDim.x) zs[z] = 0;
+    }
   }
   __shared__ double bmean[QS_NBLK];
   __shared__ float bmin[QS_NBLK], bmax[QS_NBLK], bdev[QS_NBLK];
@@ -1073,13 +1083,24 @@ static bool make_maps(const float* Y, long long n, int B, int hb, CUtensorMap* t
   return one(tmQ, hb >= 8 ? hb : 64);
 }
 
-// K1: qscale (+ zeroing) -> tcgen05 Gram -> integer reduction -> clipped-pixel
-// fix -> finalize.  Six launches on `st`, all with programmatic dependent launch.
+// K1: qscale (+ zeroing) -> tcgen05 Gram (the pairs' exact partials summed by
+// int64 atomics into one accumulator; HYDE_GRAM_REDUCE: per-pair partials and
+// an integer reduction kernel) -> clipped-pixel fix -> finalize.  Four launches
+// on `st`, all with programmatic dependent launch.
+static bool gram_atomic_sum() {
+  static const bool a = !getenv("HYDE_GRAM_REDUCE");   // experiments: the separate reduce kernel
+  return a;
+}
+int gram_tc_launches() { return gram_atomic_sum() ? 4 : 5; }
+
 cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npairs, double* G, int* nonfinite,
                            cudaStream_t st, int* state4) {
   TcWs w = carve(ws, n, B, npairs);
+  const bool atomic_sum = gram_atomic_sum();
+  const long long tot = (long long)B * B + B;
   cudaError_t e = launch_pdl(gram_qscale_kernel, dim3(B), dim3(256), 0, st, Y, n, w.qs, w.bitmap, w.nwords, state4,
-                             (int)(sizeof(RankState) / sizeof(int)), (const GramJob*)nullptr);
+                             (int)(sizeof(RankState) / sizeof(int)), (const GramJob*)nullptr,
+                             atomic_sum ? w.partial : (long long*)nullptr, atomic_sum ? tot : 0LL);
   if (e != cudaSuccess) return e;
   GramTc P;
   P.Y = Y;
@@ -1093,6 +1114,7 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
   P.qs = w.qs;
   P.partial = w.partial;
   P.bitmap = w.bitmap;
+  P.atomic_sum = atomic_sum ? 1 : 0;
   {
     static const int gexp = [] { const char* ev = getenv("HYDE_GRAM_EXP"); return ev ? atoi(ev) : 0; }();
     P.exp = gexp;
@@ -1115,10 +1137,11 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
                    (const GramJob*)nullptr);
   }
   if (e != cudaSuccess) return e;
-  const long long tot = (long long)B * B + B;
-  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)(npairs <= 16 ? (tot + 255) / 256 : (tot + 31) / 32)), dim3(256), 0, st, w.partial, npairs, B,
-                 (const GramJob*)nullptr);
-  if (e != cudaSuccess) return e;
+  if (!atomic_sum) {
+    e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)(npairs <= 16 ? (tot + 255) / 256 : (tot + 31) / 32)),
+                   dim3(256), 0, st, w.partial, npairs, B, (const GramJob*)nullptr);
+    if (e != cudaSuccess) return e;
+  }
   const int nbk = (B + FIX_TB - 1) / FIX_TB;
   e = launch_pdl(gram_fix_kernel, dim3(FIX_SPLITS), dim3(256), 0, st, Y, n, B, nbk,
                  (const GramQScale*)w.qs, (const unsigned*)w.bitmap, w.fix, nonfinite, (const GramJob*)nullptr);
@@ -1153,7 +1176,7 @@ cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* w
   const long long nwords = (n + 31) / 32;
   e = launch_pdl(gram_qscale_kernel, dim3(B, nb), dim3(256), 0, st, (const float*)nullptr, n,
                  (GramQScale*)nullptr, (unsigned*)nullptr, nwords, (int*)nullptr,
-                 (int)(sizeof(RankState) / sizeof(int)), dj);
+                 (int)(sizeof(RankState) / sizeof(int)), dj, (long long*)nullptr, 0LL);
   if (e != cudaSuccess) return e;
   GramTc P;
   memset(&P, 0, sizeof(P));
