@@ -210,7 +210,14 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
   // 4 apart) reads 32 distinct banks
   constexpr int LS = CC + ((1 - CC) % 4 + 4) % 4;
   __shared__ float lo1[IR][LS], hi1[IR][LS];
-  __shared__ float otile[IR][IC + 1];   // output tile: written back with coalesced (float4) rows
+  // output tile, written back with coalesced float4 rows.  Swizzled so that
+  // both its writers (float2 pairs: 4 rows x 8 column groups per warp) and its
+  // readers (float4, a row's 16 slots per half-warp) are conflict-free: slot
+  // c4 of row r lives at r * IC / 4 + oslot(c4) and, in odd rows, its two
+  // float2 halves are swapped.
+  __shared__ __align__(16) float otile[IR * IC];
+  auto oslot = [](int c4) { return c4 ^ ((c4 >> 3) & 1); };
+  auto oidx = [&](int rr, int c) { return rr * IC + 4 * oslot(c >> 2) + ((c & 3) ^ ((rr & 1) << 1)); };
   if (sp.rs) {
     const int kept = sp.rs->found ? sp.rs->rank - sp.k0 : sp.cnt;
     if ((int)blockIdx.z >= kept) return;
@@ -320,8 +327,7 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
         s2 = ffma2(pk2(fb.g[2 * q], fb.g[2 * q + 1]), pk2(wh[tj], wh[tj]), s2);
       }
       const float2 o2 = up2(s2);
-      otile[rr][IJ * q8 + 2 * u] = o2.x;
-      otile[rr][IJ * q8 + 2 * u + 1] = o2.y;
+      *reinterpret_cast<float2*>(&otile[oidx(rr, IJ * q8 + 2 * u)]) = o2;
     }
   }
   __syncthreads();
@@ -331,15 +337,17 @@ __global__ void __launch_bounds__(256) dwt_inv_kernel(const float* __restrict__ 
     for (int e = threadIdx.x; e < IR * (IC / 4); e += 256) {
       const int rr = e / (IC / 4), c4 = e - rr * (IC / 4);
       const int r = r0 + rr, cc = c0 + 4 * c4;
-      if (r < h_out && cc < w_out)
-        *reinterpret_cast<float4*>(o + (long long)r * w_out + cc) =
-            make_float4(otile[rr][4 * c4], otile[rr][4 * c4 + 1], otile[rr][4 * c4 + 2], otile[rr][4 * c4 + 3]);
+      if (r < h_out && cc < w_out) {
+        float4 v = *reinterpret_cast<const float4*>(&otile[rr * IC + 4 * oslot(c4)]);
+        if (rr & 1) v = make_float4(v.z, v.w, v.x, v.y);
+        *reinterpret_cast<float4*>(o + (long long)r * w_out + cc) = v;
+      }
     }
   } else {
     for (int e = threadIdx.x; e < IR * IC; e += 256) {
       const int rr = e / IC, c = e - rr * IC;
       const int r = r0 + rr, cc = c0 + c;
-      if (r < h_out && cc < w_out) o[(long long)r * w_out + cc] = otile[rr][c];
+      if (r < h_out && cc < w_out) o[(long long)r * w_out + cc] = otile[oidx(rr, c)];
     }
   }
 }

@@ -954,15 +954,21 @@ __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __r
   __shared__ int live[FIX_SPLITS];
   __shared__ int nlive;
   __shared__ long long np_sh;
-  if (threadIdx.x == 0) {
-    int c = 0;
-    long long np = 0;
-    for (int k = 0; k < FIX_SPLITS; ++k) {
-      const int v = o.cnt[k];
-      if (v) { live[c++] = k; np += v; }
+  static_assert(FIX_SPLITS == 64, "two splits per lane");
+  if (threadIdx.x < 32) {   // the non-empty splits in split order: one warp, both loads in flight
+    const int l = threadIdx.x;
+    const int v0 = o.cnt[l], v1 = o.cnt[32 + l];
+    const unsigned b0 = __ballot_sync(0xffffffffu, v0 != 0), b1 = __ballot_sync(0xffffffffu, v1 != 0);
+    const unsigned below = (1u << l) - 1u;
+    if (v0) live[__popc(b0 & below)] = l;
+    if (v1) live[__popc(b0) + __popc(b1 & below)] = 32 + l;
+    long long np = (long long)v0 + (long long)v1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) np += __shfl_xor_sync(0xffffffffu, np, off);
+    if (l == 0) {
+      nlive = __popc(b0) + __popc(b1);
+      np_sh = np;
     }
-    nlive = c;
-    np_sh = np;
   }
   __syncthreads();
   const long long idx = blockIdx.x * 256LL + threadIdx.x;
