@@ -1111,32 +1111,40 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
     if (s != HYDE_OK) return s;
     sg.end();
   }
-  // ---- A1 tail + A2: every cube's eigensolver in one launch ----
-  {
-    Stage sg(h, HYDE_STAGE_EIG, 1, st);
-    std::vector<const double*> G(batch);
-    std::vector<double*> sig(batch), house(batch), tri(batch);
-    std::vector<float*> W(batch), U(batch);
-    for (int i = 0; i < batch; ++i) {
+  // ---- A1 tail + A2: the eigensolvers, one launch per group of cubes ----
+  // The solves are latency-bound 8-SM clusters (up to 18 at once): the last,
+  // partial wave of one launch for the whole batch leaves SMs idle.  With two
+  // groups the second group's solves overlap the first group's chunk phase on
+  // the lane streams.  HYDE_BATCH_SPLIT = cubes in the first group (0: one launch).
+  static const int split_env = [] {
+    const char* ev = getenv("HYDE_BATCH_SPLIT");
+    return ev ? atoi(ev) : -1;
+  }();
+  const int sA = split_env >= 0 ? (split_env == 0 || split_env >= batch ? batch : split_env)
+                                : batch;
+  auto eig_group = [&](int i0, int i1) -> hyde_status {
+    const int nbg = i1 - i0;
+    std::vector<const double*> G(nbg);
+    std::vector<double*> sig(nbg), house(nbg), tri(nbg);
+    std::vector<float*> W(nbg), U(nbg);
+    for (int i = i0; i < i1; ++i) {
       char* ws = ws_of(i);
-      G[i] = (const double*)(ws + L.G);
-      sig[i] = (double*)(ws + L.sigma);
-      house[i] = (double*)(ws + L.house);
-      tri[i] = (double*)(ws + L.tri);
-      W[i] = (float*)(ws + L.W);
-      U[i] = (float*)(ws + L.U);
+      G[i - i0] = (const double*)(ws + L.G);
+      sig[i - i0] = (double*)(ws + L.sigma);
+      house[i - i0] = (double*)(ws + L.house);
+      tri[i - i0] = (double*)(ws + L.tri);
+      W[i - i0] = (float*)(ws + L.W);
+      U[i - i0] = (float*)(ws + L.U);
     }
-    CK(launch_noise_eig_batched(batch, G.data(), n, B, p.ridge, first, sig.data(), house.data(), tri.data(),
-                                W.data(), U.data(), L.ldwu, h->b_args_host,
-                                h->bws + (size_t)batch * (per_ws + per_e), st, h->eig_cl ? h->eig_cl : 8));
-    sg.end();
-  }
-  s = fork_lanes();
-  if (s != HYDE_OK) return s;
+    char* hargs = (char*)h->b_args_host + (size_t)i0 * eig_args_bytes();
+    char* dargs = h->bws + (size_t)batch * (per_ws + per_e) + (size_t)i0 * eig_args_bytes();
+    CK(launch_noise_eig_batched(nbg, G.data(), n, B, p.ridge, first, sig.data(), house.data(), tri.data(),
+                                W.data(), U.data(), L.ldwu, hargs, dargs, st, h->eig_cl ? h->eig_cl : 8));
+    return HYDE_OK;
+  };
   // ---- A3..A6, first chunk of every cube (decision and gating on the device) ----
-  {
-    Stage sg(h, HYDE_STAGE_SURE, batch * (3 + 2 * levels), st);
-    for (int i = 0; i < batch; ++i) {
+  auto chunk_group = [&](int i0, int i1) -> hyde_status {
+    for (int i = i0; i < i1; ++i) {
       cudaStream_t ls = h->lane_st[i % NS];
       char* ws = ws_of(i);
       RankState* rs = (RankState*)(ws + L.rs);
@@ -1149,6 +1157,30 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
                      (double)L.plan.n_coeffs, B, (double*)(ws + L.epost), h->b_rs_dev + i));
       CK(dwt_inverse(L, ws, C, E, L.ldE, first, fb, (const float*)(ws + L.tstar), ls, rs, 0));
       CK(launch_reconstruct(E, L.ldE, n, B, (float*)(ws + L.U), L.ldwu, first, outs + per * i, ls, rs));
+    }
+    return HYDE_OK;
+  };
+  {
+    Stage sg(h, HYDE_STAGE_EIG, sA < batch ? 2 : 1, st);
+    s = eig_group(0, sA);
+    if (s != HYDE_OK) return s;
+    s = fork_lanes();                       // the first group's chunks may start
+    if (s != HYDE_OK) return s;
+    if (sA < batch) {
+      s = eig_group(sA, batch);
+      if (s != HYDE_OK) return s;
+    }
+    sg.end();
+  }
+  {
+    Stage sg(h, HYDE_STAGE_SURE, batch * (3 + 2 * levels), st);
+    s = chunk_group(0, sA);
+    if (s != HYDE_OK) return s;
+    if (sA < batch) {
+      s = fork_lanes();                     // after the second group's solves
+      if (s != HYDE_OK) return s;
+      s = chunk_group(sA, batch);
+      if (s != HYDE_OK) return s;
     }
     s = join_lanes();
     if (s != HYDE_OK) return s;
@@ -1485,7 +1517,7 @@ hyde_status hyde_wsrrr(hyde_handle h, const float* cube, int rows, int cols, int
   size_t off = L.total;
   auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
   const size_t oGw = take(BB * 8), oV = take(BB * 8), oM = take(BB * 8), oLam = take((size_t)B * 8),
-               oOnes = take((size_t)B * 8), oScal = take(16 * 8), oPart = take(1024 * 8),
+               oOnes = take((size_t)B * 8), oScal = take(16 * 8), oPart = take(2048 * 8),
                oWtc = take((size_t)wtc_chunks(nc, r) * B * r * 8), oObj = take((size_t)max_iters * 8);
   const int np2 = gram_tc_npairs(nc);
   const int ns2 = gram_nsplit(nc, B);

@@ -34,22 +34,41 @@ __global__ void wsrrr_lambda_kernel(const double* sigma, int B, double nc, doubl
   *lam = sqrt(s / B) * sqrt(2.0 * log(nc));
 }
 
-// per-CTA fp64 partial sums of x^2 (fixed order), then one CTA adds them
+// per-CTA fp64 partial sums of x^2 (fixed order), then one CTA adds them.
+// 16-byte loads, four in flight per thread, over SUMSQ_CTAS CTAs (8 per SM: a
+// 940 MB stream needs ~40 KB in flight per SM; 296 CTAs of four scalar loads
+// per thread ran at 4.3 TB/s)
+constexpr int SUMSQ_CTAS = 1184;
 __global__ void __launch_bounds__(NT) sumsq_kernel(const float* __restrict__ x, long long n, double* partial) {
   __shared__ double red[NT / 32];
   double s = 0.0;
   const long long G = (long long)gridDim.x * NT;
-  long long i = blockIdx.x * (long long)NT + threadIdx.x;
-  // four loads in flight per thread; the same element order as a plain loop
-  for (; i + 3 * G < n; i += 4 * G) {
-    float v[4];
+  const long long tid = blockIdx.x * (long long)NT + threadIdx.x;
+  const bool vec = ((reinterpret_cast<unsigned long long>(x) & 15) == 0);
+  const long long n4 = vec ? n / 4 : 0;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  long long i = tid;
+  for (; i + 3 * G < n4; i += 4 * G) {
+    float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldg(x + i + u * G);
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(x4 + i + u * G);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s = fma((double)v[u], (double)v[u], s);
+    for (int u = 0; u < 4; ++u) {
+      s = fma((double)v[u].x, (double)v[u].x, s);
+      s = fma((double)v[u].y, (double)v[u].y, s);
+      s = fma((double)v[u].z, (double)v[u].z, s);
+      s = fma((double)v[u].w, (double)v[u].w, s);
+    }
   }
-  for (; i < n; i += G) {
-    const double v = x[i];
+  for (; i < n4; i += G) {
+    const float4 v = __ldcs(x4 + i);
+    s = fma((double)v.x, (double)v.x, s);
+    s = fma((double)v.y, (double)v.y, s);
+    s = fma((double)v.z, (double)v.z, s);
+    s = fma((double)v.w, (double)v.w, s);
+  }
+  for (long long k = 4 * n4 + tid; k < n; k += G) {
+    const double v = x[k];
     s = fma(v, v, s);
   }
   s = block_sum(s, red);
@@ -227,10 +246,10 @@ cudaError_t launch_wsrrr_lambda(const double* sigma, int B, long long nc, double
   return cudaGetLastError();
 }
 
-// *out = sum x^2 (fp64, fixed order); partial: >= 296 doubles
+// *out = sum x^2 (fp64, fixed order); partial: >= SUMSQ_CTAS doubles
 cudaError_t launch_sumsq(const float* x, long long n, double* partial, double* out, cudaStream_t st) {
-  sumsq_kernel<<<296, NT, 0, st>>>(x, n, partial);
-  reduce_kernel<<<1, NT, 0, st>>>(partial, 296, out);
+  sumsq_kernel<<<SUMSQ_CTAS, NT, 0, st>>>(x, n, partial);
+  reduce_kernel<<<1, NT, 0, st>>>(partial, SUMSQ_CTAS, out);
   return cudaGetLastError();
 }
 
