@@ -1115,13 +1115,19 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
   // The solves are latency-bound 8-SM clusters (up to 18 at once): the last,
   // partial wave of one launch for the whole batch leaves SMs idle.  With two
   // groups the second group's solves overlap the first group's chunk phase on
-  // the lane streams.  HYDE_BATCH_SPLIT = cubes in the first group (0: one launch).
+  // the lane streams.  HYDE_BATCH_SPLIT = cubes in the first group (0: one launch;
+  // experiments).
   static const int split_env = [] {
     const char* ev = getenv("HYDE_BATCH_SPLIT");
     return ev ? atoi(ev) : -1;
   }();
+  // default: two full waves of 8-SM clusters in the first launch (36 on a
+  // 148-SM B200: 64 cubes 4.99 -> 4.92 ms; 18 or 27 measured no better)
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+  const int two_waves = 2 * (nsm / 8);
   const int sA = split_env >= 0 ? (split_env == 0 || split_env >= batch ? batch : split_env)
-                                : batch;
+                                : (batch > two_waves ? two_waves : batch);
   auto eig_group = [&](int i0, int i1) -> hyde_status {
     const int nbg = i1 - i0;
     std::vector<const double*> G(nbg);
