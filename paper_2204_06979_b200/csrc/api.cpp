@@ -1079,7 +1079,7 @@ static hyde_status batched_phased(hyde_handle h, const float* cubes, int batch, 
   if (s != HYDE_OK) return s;
   // ---- A1 for every cube: five launches for the whole batch ----
   if (L.use_tc) {
-    Stage sg(h, HYDE_STAGE_GRAM, 5, st);
+    Stage sg(h, HYDE_STAGE_GRAM, gram_tc_launches(), st);
     std::vector<const float*> Y(batch);
     std::vector<void*> W(batch);
     std::vector<double*> G(batch), Z(batch);
@@ -1796,7 +1796,7 @@ hyde_status hyde_debug_gram_quant(hyde_handle h, int n_pixels, int bands, float*
   const int* cnt = nullptr;
   gram_tc_debug_ptrs(h->ws + L.partial, L.n, bands, L.npairs, &qs, &cnt);
   std::vector<GramQScale> q(bands);
-  std::vector<int> c(gram_tc_fix_splits());
+  std::vector<int> c(gram_tc_fix_splits(L.n));
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(q.data(), qs, sizeof(GramQScale) * bands, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(c.data(), cnt, sizeof(int) * c.size(), cudaMemcpyDeviceToHost));

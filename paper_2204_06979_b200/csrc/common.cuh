@@ -101,7 +101,7 @@ cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* w
                                    int* const* nonfinite, int* const* state4, double* const* zero8, long long n,
                                    int B, int npairs, void* hjobs, void* djobs, cudaStream_t st);
 void gram_tc_debug_ptrs(void* ws, long long n, int B, int npairs, const GramQScale** qs, const int** cnt);
-int gram_tc_fix_splits();
+int gram_tc_fix_splits(long long n);
 size_t eig_workspace_doubles(int B);
 cudaError_t launch_noise_eig(const double* G, long long n, int B, double ridge, int ncomp, int all_lam,
                              double* sigma, double* lam, double* V, double* house,

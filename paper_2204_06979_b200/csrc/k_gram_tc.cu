@@ -565,6 +565,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 // |c| <= 2^21 (the fma addend must stay in [2^23, 2^24)).
 // Also zeroes a slice of the clip bitmap and, on CTA 0, the caller's
 // rank-state words -- the first kernel of the step.
+// UU = 32-pixel loads per half-block run (qscale_uu(n)): a template so the
+// sample registers are sized to the run (107 registers for UU = 4 held the
+// batched mode's UU = 1 launch of 12k CTAs to 2 CTAs per SM).
+template <int UU>
 __global__ void __launch_bounds__(256)
     gram_qscale_kernel(const float* __restrict__ Y, long long n, GramQScale* qs, unsigned* bitmap, long long nwords,
                        int* st4, int nst4, const GramJob* __restrict__ jobs, long long* zs = nullptr,
@@ -577,6 +581,7 @@ __global__ void __launch_bounds__(256)
     bitmap = j.bitmap;
     st4 = j.state4;
     if (j.zero8 && blockIdx.x == 0 && threadIdx.x < 8) j.zero8[threadIdx.x] = 0.0;
+    if (nzs > 0) zs = j.partial;   // the cube's atomic-sum accumulator
   }
   const int b = blockIdx.x;
   {
@@ -604,9 +609,7 @@ __global__ void __launch_bounds__(256)
   // cube at `large`), 64 / 32 for shorter blocks (the batched mode's
   // 1024-pixel blocks: 6 % of the band instead of 25 %, which made this
   // kernel 0.42 ms for 64 cubes)
-  const long long blen = n / QS_NBLK;
-  const int uu = blen >= 8192 ? 4 : (blen >= 4096 ? 2 : 1);
-  float v[KPW][8];
+  float v[KPW][2 * UU];
   bool full[KPW];
 #pragma unroll
   for (int q = 0; q < KPW; ++q) {
@@ -617,7 +620,7 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < 2; ++j) {
       const float* src = row + p0 + ((len * j) >> 1);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[q][4 * j + u] = (full[q] && u < uu) ? __ldg(src + lane + 32 * u) : 0.f;
+      for (int u = 0; u < UU; ++u) v[q][UU * j + u] = full[q] ? __ldg(src + lane + 32 * u) : 0.f;
     }
   }
 #pragma unroll
@@ -639,8 +642,7 @@ __global__ void __launch_bounds__(256)
       for (long long i = lane; i < len; i += 32) take(__ldg(row + p0 + i));
     } else {
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if ((u & 3) < uu) take(v[q][u]);
+      for (int u = 0; u < 2 * UU; ++u) take(v[q][u]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(256) gram_reduce_i64_kernel(long long* __restr
 // ------------------------------------------------------------------ fix
 // The flagged pixels P of one pixel split, in increasing order: F = sum y y^T
 // (fp64), D = sum q q^T and, on the diagonal output blocks, sum q (int64),
-// q recomputed exactly as the converters did.  Grid: FIX_SPLITS CTAs, each
+// q recomputed exactly as the converters did.  Grid: fix_splits(n) CTAs, each
 // walking the upper-triangular 64x64 output blocks of its split.  A split
 // without a flagged pixel writes only its count (0) and exits after one scan
 // of its bitmap words.
@@ -797,7 +799,7 @@ __global__ void __launch_bounds__(256) gram_fix_kernel(const float* __restrict__
   __shared__ int wtot[8];
   const int split = blockIdx.x;
   const long long nw = (n + 31) / 32;
-  const long long wper = ((nw + FIX_SPLITS - 1) / FIX_SPLITS + 3) / 4 * 4;
+  const long long wper = ((nw + gridDim.x - 1) / gridDim.x + 3) / 4 * 4;   // gridDim.x = fix_splits(n)
   const long long w_begin = split * wper, w_end = min(nw, w_begin + wper);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -942,7 +944,8 @@ __device__ __forceinline__ double i128_to_f64(__int128 x) {
 // in split order.
 __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __restrict__ S, int B, long long n,
                                                             const GramQScale* __restrict__ qsc, FixOut o,
-                                                            double* __restrict__ G, const GramJob* __restrict__ jobs) {
+                                                            double* __restrict__ G, const GramJob* __restrict__ jobs,
+                                                            int nsplit) {
   pdl_wait();
   if (jobs) {
     const GramJob& j = jobs[blockIdx.y];
@@ -957,7 +960,7 @@ __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __r
   static_assert(FIX_SPLITS == 64, "two splits per lane");
   if (threadIdx.x < 32) {   // the non-empty splits in split order: one warp, both loads in flight
     const int l = threadIdx.x;
-    const int v0 = o.cnt[l], v1 = o.cnt[32 + l];
+    const int v0 = l < nsplit ? o.cnt[l] : 0, v1 = 32 + l < nsplit ? o.cnt[32 + l] : 0;
     const unsigned b0 = __ballot_sync(0xffffffffu, v0 != 0), b1 = __ballot_sync(0xffffffffu, v1 != 0);
     const unsigned below = (1u << l) - 1u;
     if (v0) live[__popc(b0 & below)] = l;
@@ -1057,7 +1060,15 @@ void gram_tc_debug_ptrs(void* ws, long long n, int B, int npairs, const GramQSca
   *qs = w.qs;
   *cnt = w.fix.cnt;
 }
-int gram_tc_fix_splits() { return FIX_SPLITS; }
+// CTAs of the clipped-pixel correction: one per 256 bitmap words (8192
+// pixels), at most FIX_SPLITS (a 65536-pixel cube of the batched mode: 8, not
+// 64 -- the kernel's 222 registers keep one CTA per SM, so 64 x 64 mostly
+// empty CTAs took 107 us)
+static int fix_splits(long long n) {
+  const long long nw = (n + 31) / 32, k = nw / 256;
+  return (int)(k < 1 ? 1 : (k > FIX_SPLITS ? FIX_SPLITS : k));
+}
+int gram_tc_fix_splits(long long n) { return fix_splits(n); }
 
 // 2-D tensor maps of the cube viewed as B rows of n fp32 pixels: boxes of
 // 128 pixels x 64 bands (P region) and x hb bands (QS region); bands past B
@@ -1093,6 +1104,19 @@ static bool make_maps(const float* Y, long long n, int B, int hb, CUtensorMap* t
 // int64 atomics into one accumulator; HYDE_GRAM_REDUCE: per-pair partials and
 // an integer reduction kernel) -> clipped-pixel fix -> finalize.  Four launches
 // on `st`, all with programmatic dependent launch.
+static int qscale_uu(long long n) {
+  const long long blen = n / QS_NBLK;
+  return blen >= 8192 ? 4 : (blen >= 4096 ? 2 : 1);
+}
+template <typename... Args>
+static cudaError_t launch_qscale(long long n, dim3 grid, cudaStream_t st, Args... args) {
+  switch (qscale_uu(n)) {
+    case 4: return launch_pdl(gram_qscale_kernel<4>, grid, dim3(256), 0, st, args...);
+    case 2: return launch_pdl(gram_qscale_kernel<2>, grid, dim3(256), 0, st, args...);
+    default: return launch_pdl(gram_qscale_kernel<1>, grid, dim3(256), 0, st, args...);
+  }
+}
+
 static bool gram_atomic_sum() {
   static const bool a = !getenv("HYDE_GRAM_REDUCE");   // experiments: the separate reduce kernel
   return a;
@@ -1104,7 +1128,7 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
   TcWs w = carve(ws, n, B, npairs);
   const bool atomic_sum = gram_atomic_sum();
   const long long tot = (long long)B * B + B;
-  cudaError_t e = launch_pdl(gram_qscale_kernel, dim3(B), dim3(256), 0, st, Y, n, w.qs, w.bitmap, w.nwords, state4,
+  cudaError_t e = launch_qscale(n, dim3(B), st, Y, n, w.qs, w.bitmap, w.nwords, state4,
                              (int)(sizeof(RankState) / sizeof(int)), (const GramJob*)nullptr,
                              atomic_sum ? w.partial : (long long*)nullptr, atomic_sum ? tot : 0LL);
   if (e != cudaSuccess) return e;
@@ -1149,11 +1173,12 @@ cudaError_t launch_gram_tc(const float* Y, long long n, int B, void* ws, int npa
     if (e != cudaSuccess) return e;
   }
   const int nbk = (B + FIX_TB - 1) / FIX_TB;
-  e = launch_pdl(gram_fix_kernel, dim3(FIX_SPLITS), dim3(256), 0, st, Y, n, B, nbk,
+  e = launch_pdl(gram_fix_kernel, dim3(fix_splits(n)), dim3(256), 0, st, Y, n, B, nbk,
                  (const GramQScale*)w.qs, (const unsigned*)w.bitmap, w.fix, nonfinite, (const GramJob*)nullptr);
   if (e != cudaSuccess) return e;
   return launch_pdl(gram_finalize_kernel, dim3((unsigned)(((long long)B * B + 255) / 256)), dim3(256), 0, st,
-                    (const long long*)w.partial, B, n, (const GramQScale*)w.qs, w.fix, G, (const GramJob*)nullptr);
+                    (const long long*)w.partial, B, n, (const GramQScale*)w.qs, w.fix, G, (const GramJob*)nullptr,
+                    fix_splits(n));
 }
 
 // The same five kernels for nb cubes of one shape in one launch each
@@ -1180,9 +1205,10 @@ cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* w
   cudaError_t e = cudaMemcpyAsync(djobs, hjobs, (size_t)nb * sizeof(GramJob), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   const long long nwords = (n + 31) / 32;
-  e = launch_pdl(gram_qscale_kernel, dim3(B, nb), dim3(256), 0, st, (const float*)nullptr, n,
+  e = launch_qscale(n, dim3(B, nb), st, (const float*)nullptr, n,
                  (GramQScale*)nullptr, (unsigned*)nullptr, nwords, (int*)nullptr,
-                 (int)(sizeof(RankState) / sizeof(int)), dj, (long long*)nullptr, 0LL);
+                 (int)(sizeof(RankState) / sizeof(int)), dj, (long long*)nullptr,
+                 gram_atomic_sum() ? (long long)B * B + B : 0LL);
   if (e != cudaSuccess) return e;
   GramTc P;
   memset(&P, 0, sizeof(P));
@@ -1193,6 +1219,7 @@ cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* w
   long long per = (n + npairs - 1) / npairs;
   per = (per + KC - 1) / KC * KC;
   P.per_pair = per;
+  P.atomic_sum = gram_atomic_sum() ? 1 : 0;
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   const size_t smem = (size_t)Feed<false>::NI * 2 * P.rows_tot * KC;
@@ -1200,16 +1227,19 @@ cudaError_t launch_gram_tc_batched(int nb, const float* const* Y, void* const* w
   if (e != cudaSuccess) return e;
   e = launch_pdl(gram_tc_kernel<false>, dim3(2 * npairs, nb), dim3(NTHREADS), smem, st, P, tm, tm, dj);
   if (e != cudaSuccess) return e;
-  const long long tot = (long long)B * B + B;
-  e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)(npairs <= 16 ? (tot + 255) / 256 : (tot + 31) / 32), nb), dim3(256), 0, st,
-                 (long long*)nullptr, npairs, B, dj);
-  if (e != cudaSuccess) return e;
+  if (!gram_atomic_sum()) {
+    const long long tot = (long long)B * B + B;
+    e = launch_pdl(gram_reduce_i64_kernel, dim3((unsigned)(npairs <= 16 ? (tot + 255) / 256 : (tot + 31) / 32), nb),
+                   dim3(256), 0, st, (long long*)nullptr, npairs, B, dj);
+    if (e != cudaSuccess) return e;
+  }
   const int nbk = (B + FIX_TB - 1) / FIX_TB;
   FixOut fo;
   memset(&fo, 0, sizeof(fo));
-  e = launch_pdl(gram_fix_kernel, dim3(FIX_SPLITS, nb), dim3(256), 0, st, (const float*)nullptr, n, B, nbk,
+  e = launch_pdl(gram_fix_kernel, dim3(fix_splits(n), nb), dim3(256), 0, st, (const float*)nullptr, n, B, nbk,
                  (const GramQScale*)nullptr, (const unsigned*)nullptr, fo, (int*)nullptr, dj);
   if (e != cudaSuccess) return e;
   return launch_pdl(gram_finalize_kernel, dim3((unsigned)(((long long)B * B + 255) / 256), nb), dim3(256), 0, st,
-                    (const long long*)nullptr, B, n, (const GramQScale*)nullptr, fo, (double*)nullptr, dj);
+                    (const long long*)nullptr, B, n, (const GramQScale*)nullptr, fo, (double*)nullptr, dj,
+                    fix_splits(n));
 }
