@@ -799,7 +799,11 @@ __global__ void __launch_bounds__(NT, 3) sure_kernel(const float* __restrict__ c
     while (P2 < mc) P2 <<= 1;
     for (int i = mc + tid; i < P2; i += NT) skeys[sw(i)] = 0xFFFFFFFFu;
     __syncthreads();
-    sk = P2 <= NT * 16 ? block_sort<16>(skeys, sbuf, P2) : block_sort<32>(skeys, sbuf, P2);
+    // all NT threads in the merge for windows of up to NT * 16 keys: fewer
+    // items per thread = fewer dependent steps per merge level
+    sk = P2 <= NT * 4 ? block_sort<4>(skeys, sbuf, P2)
+         : P2 <= NT * 8 ? block_sort<8>(skeys, sbuf, P2)
+         : P2 <= NT * 16 ? block_sort<16>(skeys, sbuf, P2) : block_sort<32>(skeys, sbuf, P2);
     const int seg = (mc + NT - 1) / NT;
     const int e0 = min(mc, tid * seg), e1 = min(mc, e0 + seg);
     double tsum = 0.0;
